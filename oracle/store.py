@@ -1,0 +1,216 @@
+"""Oracle store: packed item blobs, build, assemble (TEST INFRASTRUCTURE).
+
+Packed item blob (one item = one K or V chunk, this rank's KV heads; the
+format is DESIGN.md §"Packed item blob", written independently on both sides):
+
+  codes section at offset 0, slabs in (layer, local head) order, each slab
+        the T*D elements in [t][d] order:
+        PASS16 2 B/elem (source bits, little endian) | 8-bit schemes 1 B/elem |
+        INT4 ½ B/elem (element 2i low nibble, 2i+1 high nibble)
+  meta section at align256(codes bytes), one record per slab, each record
+        padded to a multiple of 16 B:
+        INT8  fp32 s per group of G elements (G | T*D, groups never cross a slab)
+        INT4  (fp32 s, fp32 mn) per group, interleaved
+        GSE8  int8 shared-exponent array [2^e], unused = -128
+        FP8 / PASS16: no meta
+  blob size = align256(meta offset + L*Hl*record stride)  (FP8/PASS16: align256(codes))
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import codecs, numerics
+
+PASS16, INT8, FP8E4M3, FP8E5M2, GSE8, INT4 = 0, 1, 2, 3, 4, 5
+SCHEME_NAMES = {PASS16: "PASS16", INT8: "INT8", FP8E4M3: "FP8E4M3", FP8E5M2: "FP8E5M2",
+                GSE8: "GSE8", INT4: "INT4"}
+
+
+def _a(x: int, n: int) -> int:
+    return (x + n - 1) // n * n
+
+
+@dataclass(frozen=True)
+class Layout:
+    L: int
+    H: int
+    T: int
+    D: int
+    dtype: str = "bf16"      # source == output dtype
+    group: int = 0           # 0 -> D
+    gse_e: int = 4
+    gse_m: int = 3
+    rank: int = 0
+    world: int = 1
+
+    @property
+    def G(self) -> int:
+        return self.group or self.D
+
+    @property
+    def Hl(self) -> int:
+        return self.H // self.world
+
+    @property
+    def heads(self) -> tuple[int, int]:
+        return self.rank * self.Hl, (self.rank + 1) * self.Hl
+
+    @property
+    def slab(self) -> int:
+        return self.T * self.D
+
+    def code_bytes(self, scheme: int) -> int:
+        per = {PASS16: 2 * self.slab, INT4: self.slab // 2}.get(scheme, self.slab)
+        return per
+
+    def meta_record(self, scheme: int) -> int:
+        ng = self.slab // self.G
+        raw = {INT8: 4 * ng, INT4: 8 * ng, GSE8: 1 << self.gse_e}.get(scheme, 0)
+        return _a(raw, 16)
+
+    def meta_offset(self, scheme: int) -> int:
+        return _a(self.L * self.Hl * self.code_bytes(scheme), 256)
+
+    def item_bytes(self, scheme: int) -> int:
+        return _a(self.meta_offset(scheme) + self.L * self.Hl * self.meta_record(scheme), 256)
+
+
+def encode_slab(bits: np.ndarray, scheme: int, lay: Layout):
+    """One (item, layer, head) slab of T*D source bit patterns -> (codes bytes, meta bytes).
+
+    Ingest (R1): exact fp32 value of each element; NaN/Inf rejected."""
+    bits = np.asarray(bits, dtype=np.uint16).reshape(-1)
+    x = numerics.to_f32(bits, lay.dtype)
+    if not np.all(np.isfinite(x)):
+        raise ValueError("NaN/Inf in source")
+    rec = lay.meta_record(scheme)
+    meta = np.zeros(rec, dtype=np.uint8)
+    if scheme == PASS16:
+        return bits.astype("<u2").view(np.uint8), meta
+    if scheme == INT8:
+        q, s = codecs.int8_encode(x.reshape(-1, lay.G))
+        m = s.astype("<f4").view(np.uint8)
+        meta[: m.size] = m
+        return q.reshape(-1).view(np.uint8), meta
+    if scheme == INT4:
+        q, s, mn = codecs.int4_encode(x.reshape(-1, lay.G))
+        m = np.stack([s, mn], axis=1).astype("<f4").reshape(-1).view(np.uint8)
+        meta[: m.size] = m
+        return codecs.int4_pack(q), meta
+    if scheme == FP8E4M3:
+        return codecs.fp8_encode(x, "e4m3"), meta
+    if scheme == FP8E5M2:
+        return codecs.fp8_encode(x, "e5m2"), meta
+    if scheme == GSE8:
+        table = codecs.gse_slab_table(x, lay.gse_e, lay.gse_m)
+        m = codecs.gse_meta(table, lay.gse_e).view(np.uint8)
+        meta[: m.size] = m
+        return codecs.gse_encode(x, table, lay.gse_e, lay.gse_m), meta
+    raise ValueError(scheme)
+
+
+def decode_slab(codes: np.ndarray, meta: np.ndarray, scheme: int, lay: Layout) -> np.ndarray:
+    """Packed slab -> output bit patterns (source dtype), RNE (R25)."""
+    codes = np.asarray(codes, dtype=np.uint8)
+    ng = lay.slab // lay.G
+    if scheme == PASS16:
+        return codes.view("<u2").astype(np.uint16).copy()
+    if scheme == INT8:
+        s = meta[: 4 * ng].view("<f4").astype(np.float32)
+        v = codecs.int8_decode(codes.view(np.int8).reshape(ng, lay.G), s)
+    elif scheme == INT4:
+        sm = meta[: 8 * ng].view("<f4").astype(np.float32).reshape(ng, 2)
+        q = codecs.int4_unpack(codes).reshape(ng, lay.G)
+        v = codecs.int4_decode(q, sm[:, 0], sm[:, 1])
+    elif scheme == FP8E4M3:
+        v = codecs.fp8_decode(codes, "e4m3")
+    elif scheme == FP8E5M2:
+        v = codecs.fp8_decode(codes, "e5m2")
+    elif scheme == GSE8:
+        tab8 = meta[: 1 << lay.gse_e].view(np.int8)
+        table = [int(t) for t in tab8 if t != -128]
+        v = codecs.gse_decode(codes, table, lay.gse_e, lay.gse_m)
+    else:
+        raise ValueError(scheme)
+    return numerics.round_out(np.asarray(v).reshape(-1), lay.dtype)
+
+
+def encode_item(bits: np.ndarray, scheme: int, lay: Layout) -> np.ndarray:
+    """bits: uint16 [L][Hl][T][D] (this rank's heads) -> packed blob (uint8)."""
+    bits = np.asarray(bits, dtype=np.uint16).reshape(lay.L, lay.Hl, lay.slab)
+    blob = np.zeros(lay.item_bytes(scheme), dtype=np.uint8)
+    cb, mo, mr = lay.code_bytes(scheme), lay.meta_offset(scheme), lay.meta_record(scheme)
+    for l in range(lay.L):
+        for h in range(lay.Hl):
+            i = l * lay.Hl + h
+            c, m = encode_slab(bits[l, h], scheme, lay)
+            blob[i * cb:(i + 1) * cb] = c
+            if mr:
+                blob[mo + i * mr: mo + (i + 1) * mr] = m
+    return blob
+
+
+def decode_item_slab(blob: np.ndarray, scheme: int, lay: Layout, l: int, h: int) -> np.ndarray:
+    cb, mo, mr = lay.code_bytes(scheme), lay.meta_offset(scheme), lay.meta_record(scheme)
+    i = l * lay.Hl + h
+    return decode_slab(blob[i * cb:(i + 1) * cb], blob[mo + i * mr: mo + (i + 1) * mr], scheme, lay)
+
+
+def decode_item(blob: np.ndarray, scheme: int, lay: Layout) -> np.ndarray:
+    out = np.empty((lay.L, lay.Hl, lay.T, lay.D), dtype=np.uint16)
+    for l in range(lay.L):
+        for h in range(lay.Hl):
+            out[l, h] = decode_item_slab(blob, scheme, lay, l, h).reshape(lay.T, lay.D)
+    return out
+
+
+def assemble(decoded_items: dict, request, lay: Layout):
+    """a8 / R19: per-request KV cache, docs in request order.
+
+    K[l][h][j*T + t][d] = dec(item 2*doc_j)[l][h][t][d], V likewise with item
+    2*doc_j + 1.  decoded_items maps item id -> uint16 [L][Hl][T][D]."""
+    k = len(request)
+    K = np.empty((lay.L, lay.Hl, k * lay.T, lay.D), dtype=np.uint16)
+    V = np.empty_like(K)
+    for j, doc in enumerate(request):
+        K[:, :, j * lay.T:(j + 1) * lay.T, :] = decoded_items[2 * int(doc)]
+        V[:, :, j * lay.T:(j + 1) * lay.T, :] = decoded_items[2 * int(doc) + 1]
+    return K, V
+
+
+class OracleStore:
+    """build_store(chunks, hotness) -> quantised store + placement (P:182-206,
+    P:233-237), assemble_kv(ids) -> KV cache; everything in host memory."""
+
+    def __init__(self, lay: Layout, ladder, taus):
+        self.lay, self.ladder, self.taus = lay, list(ladder), list(taus)
+        self.blobs: dict[int, np.ndarray] = {}
+        self.schemes: list[int] = []
+        self._dec: dict[int, np.ndarray] = {}
+
+    def build(self, n_docs: int, hotness, source) -> None:
+        """source(doc, kind) -> uint16 [L][Hl][T][D] (this rank's heads)."""
+        from .hotness import assign_schemes
+        self.n_docs = n_docs
+        self.schemes = assign_schemes(hotness, self.ladder, self.taus)
+        for item in range(2 * n_docs):
+            self.blobs[item] = encode_item(source(item // 2, item % 2), self.schemes[item], self.lay)
+
+    def decoded(self, item: int) -> np.ndarray:
+        if item not in self._dec:
+            self._dec[item] = decode_item(self.blobs[item], self.schemes[item], self.lay)
+        return self._dec[item]
+
+    def assemble(self, request):
+        if len(set(int(d) for d in request)) != len(request):
+            raise ValueError("duplicate doc id in request")
+        for d in request:
+            if not (0 <= int(d) < self.n_docs):
+                raise KeyError(int(d))
+        items = {}
+        for d in request:
+            items[2 * int(d)] = self.decoded(2 * int(d))
+            items[2 * int(d) + 1] = self.decoded(2 * int(d) + 1)
+        return assemble(items, request, self.lay)

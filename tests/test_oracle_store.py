@@ -1,0 +1,117 @@
+"""Pins of the oracle store: blob sizes (Table II compression ratio), layout
+probe for the assembled KV (closed-form index), PASS16 byte identity, and
+sharded == unsharded."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import store
+from oracle.store import FP8E4M3, FP8E5M2, GSE8, INT4, INT8, PASS16, Layout
+
+ALL = (PASS16, INT8, FP8E4M3, FP8E5M2, GSE8, INT4)
+
+
+def test_blob_sizes_closed_form():
+    lay = Layout(L=32, H=8, T=512, D=128)          # Llama-3-8B KV shape
+    n = 32 * 8 * 512 * 128
+    assert lay.item_bytes(INT8) == n + 32 * 8 * 512 * 4
+    assert lay.item_bytes(FP8E4M3) == n
+    assert lay.item_bytes(GSE8) == n + 32 * 8 * 16
+    assert lay.item_bytes(INT4) == n // 2 + 32 * 8 * 512 * 8
+    assert lay.item_bytes(PASS16) == 2 * n
+
+
+def test_paper_ratio_mode():
+    """Table II: 8-bit schemes compress BF16 by 1.9988-1.9996.
+    With one scale per (layer, head) slab (G = T*D) every 8-bit scheme is in
+    [1.99, 2.0]; the default G = D costs 3% of metadata."""
+    lay = Layout(L=32, H=32, T=512, D=128, group=512 * 128)   # LLaMA-2-7B
+    bf16 = 2 * 32 * 32 * 512 * 128
+    for s in (INT8, FP8E4M3, FP8E5M2, GSE8):
+        assert 1.99 <= bf16 / lay.item_bytes(s) <= 2.0
+    assert abs(bf16 / Layout(32, 32, 512, 128).item_bytes(INT8) - 1.939) < 1e-3
+
+
+def _items(lay, n_docs):
+    return {(d, k): synth.gen_item(lay.L, lay.H, lay.T, lay.D, d, k, heads=lay.heads, dtype=lay.dtype)
+            for d in range(n_docs) for k in (0, 1)}
+
+
+def test_layout_probe_pass16_byte_identical():
+    """Every output element must be the source element of (doc_j, kind, l, h, t, d)
+    with index (l, h, j*T + t, d) — PASS16 is byte identical (north_star)."""
+    lay = Layout(L=2, H=2, T=64, D=64, dtype="fp16")
+    src = _items(lay, 6)
+    st = store.OracleStore(lay, [PASS16], [])
+    st.build(6, np.zeros(12, np.int64), lambda d, k: src[(d, k)])
+    req = [4, 0, 5, 2]
+    K, V = st.assemble(req)
+    for j, doc in enumerate(req):
+        for l in range(lay.L):
+            for h in range(lay.Hl):
+                for t in (0, 17, 63):
+                    assert np.array_equal(K[l, h, j * lay.T + t], src[(doc, 0)][l, h, t])
+                    assert np.array_equal(V[l, h, j * lay.T + t], src[(doc, 1)][l, h, t])
+    with pytest.raises(ValueError):
+        st.assemble([1, 1, 2, 3])
+    with pytest.raises(KeyError):
+        st.assemble([1, 99, 2, 3])
+
+
+@pytest.mark.parametrize("scheme", ALL)
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+def test_sharded_equals_unsharded(scheme, dtype):
+    """Groups and GSE tables never cross a head (R8, R21): the blob of a head
+    shard decodes to exactly the unsharded item's heads."""
+    full = Layout(L=2, H=4, T=32, D=64, dtype=dtype, group=64)
+    x = synth.gen_item(2, 4, 32, 64, 3, 0, dtype=dtype)
+    ref = store.decode_item(store.encode_item(x, scheme, full), scheme, full)
+    for world in (2, 4):
+        for r in range(world):
+            lay = Layout(L=2, H=4, T=32, D=64, dtype=dtype, group=64, rank=r, world=world)
+            h0, h1 = lay.heads
+            xs = synth.gen_item(2, 4, 32, 64, 3, 0, heads=(h0, h1), dtype=dtype)
+            assert np.array_equal(xs, x[:, h0:h1])
+            got = store.decode_item(store.encode_item(xs, scheme, lay), scheme, lay)
+            assert np.array_equal(got, ref[:, h0:h1])
+
+
+def test_pass16_roundtrip_and_nan_rejected():
+    lay = Layout(L=1, H=1, T=16, D=16)
+    x = synth.gen_item(1, 1, 16, 16, 0, 1)
+    assert np.array_equal(store.decode_item(store.encode_item(x, PASS16, lay), PASS16, lay), x)
+    bad = x.copy()
+    bad[0, 0, 3, 3] = 0x7FC0          # bf16 NaN
+    with pytest.raises(ValueError):
+        store.encode_item(bad, INT8, lay)
+
+
+def test_decode_error_bounds_per_scheme():
+    """Round-trip error per scheme on a synthetic slab stays within each codec's
+    bound: INT8 s/2, INT4 s/2 (+ output rounding, half a bf16 ulp); FP8 half an
+    ulp of the format (3 / 2 fraction bits; subnormal floor 2^-10 / 2^-17);
+    GSE-8 below 2^-(m-1-d) relative (<= 2^-1 at 1+4+3) or flushed below the
+    array's reach."""
+    from oracle import codecs, numerics
+    lay = Layout(L=1, H=1, T=64, D=128)
+    x = synth.gen_item(1, 1, 64, 128, 7, 0)
+    xf = numerics.bf16_to_f32(x.reshape(-1)).astype(np.float64)
+    ax = np.abs(xf)
+    out = 2.0 ** -8 * (ax + 1.0)  # half an ulp of bf16 on the decoded value
+    for s in (INT8, FP8E4M3, FP8E5M2, GSE8, INT4):
+        y = numerics.bf16_to_f32(store.decode_item(store.encode_item(x, s, lay), s, lay).reshape(-1))
+        err = np.abs(xf - y)
+        g = ax.reshape(-1, 128).max(1).repeat(128)
+        if s == INT8:
+            bound = g / 127 / 2 * 1.001 + out
+        elif s == INT4:
+            rng = (xf.reshape(-1, 128).max(1) - xf.reshape(-1, 128).min(1)).repeat(128)
+            bound = rng / 15 / 2 * 1.001 + out
+        elif s == FP8E4M3:
+            bound = np.maximum(2.0 ** -4 * ax, 2.0 ** -10)
+        elif s == FP8E5M2:
+            bound = np.maximum(2.0 ** -3 * ax, 2.0 ** -17)
+        else:
+            t = codecs.gse_slab_table(xf.astype(np.float32), 4, 3)
+            bound = np.where(ax >= 2.0 ** (t[0] - 2), 0.5 * ax, ax)
+        assert np.all(err <= bound), s
