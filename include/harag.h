@@ -1,0 +1,220 @@
+/*
+ * harag.h — C ABI of the B200-native HA-RAG hot path (arXiv 2510.20878).
+ *
+ * "build_store(chunks, hotness) -> quantised store + placement" and
+ * "assemble_kv(request chunk ids) -> KV cache", plus hotness update and
+ * re-placement (BASELINE.json north_star).  Paper citations are
+ * /root/reference/PAPER.md line numbers (P:<line>); readings R<n> are the
+ * numbered rows of DESIGN.md §2.
+ *
+ * Conventions
+ *  - Plain C: fixed-width integers, plain pointers, sizes in bytes.  CUDA
+ *    streams are passed as `void*` holding a cudaStream_t (NULL = legacy
+ *    default stream).  Device pointers are CUDA device addresses on the
+ *    store's device.
+ *  - Every function returns hr_status; on failure hr_last_error() returns a
+ *    thread-local message.  Validation errors (HR_EINVAL, HR_ENOTFOUND) are
+ *    returned BEFORE any device work is enqueued: no partial writes.
+ *  - No C++ exception crosses the ABI.
+ *  - A store is single-writer: calls on one store must be serialised by the
+ *    caller.  Different stores (one per rank/GPU) are independent.
+ *  - Ownership: the store owns every buffer it allocates (HBM arena, pinned
+ *    tier, host backing, staging ring, descriptor buffers, the per-doc source
+ *    buffers handed to hr_src_fn).  The caller owns inputs and outputs.
+ *
+ * Item numbering: item = 2*doc + kind, kind 0 = K, 1 = V — the paper's 2n
+ * chunks [C_1^k, C_1^v, ..., C_n^k, C_n^v] (Alg. 1 input).
+ */
+#ifndef HARAG_H
+#define HARAG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HR_ABI_VERSION 1
+
+typedef enum {
+  HR_OK = 0,
+  HR_EINVAL = 1,     /* bad argument: shape, tau out of range, duplicate id in a request, NaN/Inf source */
+  HR_ENOMEM = 2,     /* device or host allocation failed */
+  HR_ECUDA = 3,      /* a CUDA runtime call failed (message has the CUDA error string) */
+  HR_ENOTFOUND = 4,  /* unknown doc / item id */
+  HR_ECORRUPT = 5,   /* malformed packed data (e.g. GSE-8 index past the array) */
+  HR_ESTATE = 6      /* call not valid in the store's current state (e.g. assemble before build) */
+} hr_status;
+
+typedef enum { HR_BF16 = 0, HR_FP16 = 1 } hr_dtype;   /* source dtype == output dtype */
+
+/* Compression schemes S_i of Alg. 1 plus the north_star 16-bit
+ * passthrough and INT4.  P:397: INT8 -> E4M3 -> E5M2 -> GSE-8 hottest to coldest. */
+typedef enum {
+  HR_S_PASS16 = 0,   /* source bits unchanged (byte-identical tier) */
+  HR_S_INT8 = 1,     /* P:144; symmetric per-group absmax, codes [-127,127] (R1-R3) */
+  HR_S_FP8E4M3 = 2,  /* P:144; RNE, saturating at 448 (R5) */
+  HR_S_FP8E5M2 = 3,  /* P:144; RNE, saturating at 57344 (R5) */
+  HR_S_GSE8 = 4,     /* P:155-172; 1+e+m grouped shared exponent, per-slab array (R6-R9) */
+  HR_S_INT4 = 5      /* north_star; per-group min-max, two codes per byte (R4) */
+} hr_scheme;
+
+typedef enum {
+  HR_T_HBM = 0,      /* GPU memory (queueGPU) */
+  HR_T_PIN = 1,      /* pinned host memory (queuePIN) */
+  HR_T_PAGE = 2      /* pageable host memory (queuePAGE / backing store) */
+} hr_tier;
+
+typedef struct {
+  /* model KV shape: L layers, H KV heads, D head_dim, T tokens per chunk (512) */
+  uint32_t L, H, D, T;
+  uint32_t dtype;          /* hr_dtype */
+  uint32_t group;          /* INT8/INT4 group G in elements (0 -> D); power of two, 32 <= G, G | T*D (R1) */
+  uint32_t gse_ebits;      /* GSE-8 layout 1+e+m, e+m = 7, e,m >= 2 (default 4,3) */
+  uint32_t gse_mbits;
+  uint32_t n_ladder;       /* 1..6 schemes, hottest first (Alg. 1 S_1..S_m) */
+  uint32_t ladder[6];      /* hr_scheme */
+  double   tau[6];         /* tau[0..n_ladder-2]: fractions of the 2n items per group; the last group takes the remainder (R11) */
+  uint64_t hbm_budget;     /* bytes of HBM arena per rank (GPU_LIST capacity, R15) */
+  uint64_t pin_budget;     /* bytes of pinned host tier per rank (PIN_LIST capacity) */
+  int32_t  backing_pinned; /* 1: host backing is pinned (every non-HBM item is served as PIN); 0: pageable */
+  int32_t  keep_backing;   /* 1: every item keeps a host backing copy (needed by hr_replace); 0: HBM items live only in HBM */
+  int32_t  demand_mode;    /* 0: eager placement (lists resident); 1: reserved (paper-literal Alg. 2 fill, see hr_alg2_*) */
+  uint32_t decay_shift;    /* epoch: h <- (h >> decay_shift) + delta (R20) */
+  uint32_t bench_alias_R;  /* 0 = off; >0: docs d and d' with d % R == d' % R and equal scheme share one host backing blob (bench only) */
+  int32_t  device;         /* CUDA device ordinal */
+  int32_t  rank, world;    /* this store owns KV heads [rank*H/world, (rank+1)*H/world) */
+  uint32_t staging_slots;  /* host-tier staging ring slots in HBM (0 -> 3) */
+} hr_store_config;
+
+typedef struct {
+  uint64_t requests;          /* requests assembled */
+  uint64_t hits[3];           /* item accesses served per hr_tier */
+  uint64_t bytes_out;         /* assembled KV bytes written */
+  uint64_t bytes_hbm_alg;     /* algorithmic HBM bytes of the assemble kernels (codes+meta read, out written) */
+  uint64_t bytes_h2d;         /* host -> device bytes moved by the streamer */
+  uint64_t kernel_launches;   /* assemble kernel launches */
+  uint64_t migrations_in;     /* items promoted into HBM by hr_replace */
+  uint64_t migrations_out;    /* items evicted from HBM by hr_replace */
+  uint64_t failed_promotions; /* promotions that found no contiguous arena space */
+  double   kernel_ms;         /* sum of assemble-kernel durations (CUDA events) when timing is on */
+  uint64_t timed_launches;    /* launches included in kernel_ms */
+  uint64_t hbm_used;          /* bytes of HBM arena in use */
+  uint64_t pin_used;          /* bytes of pinned tier in use */
+} hr_stats;
+
+typedef struct hr_store hr_store;
+typedef struct hr_alg2 hr_alg2;
+
+/* Source of one document's K and V chunks for hr_build_store: write them as
+ * [L][H][T][D] (ALL heads, source dtype) into the library-owned DEVICE
+ * buffers k_dst / v_dst, ordered on `stream`.  Return HR_OK or an error that
+ * aborts the build. */
+typedef int (*hr_src_fn)(void* user, uint32_t doc, void* k_dst, void* v_dst, void* stream);
+
+/* ---------------------------------------------------------------- basics */
+const char* hr_last_error(void);             /* thread-local message of the last failure ("" if none) */
+uint32_t    hr_abi_version(void);            /* HR_ABI_VERSION */
+void        hr_config_default(hr_store_config* cfg);  /* paper defaults: ladder INT8,E4M3,E5M2,GSE8 at tau 10/10/10%, GSE 1+4+3, bf16 */
+
+/* Create an empty store on cfg->device.  Validates the shape (D % 8 == 0,
+ * T*D % 256 == 0, H % world == 0, group rules), ladder and taus (HR_EINVAL).
+ * Allocates nothing large until hr_build_begin. */
+hr_status hr_store_create(const hr_store_config* cfg, hr_store** out);
+void      hr_store_destroy(hr_store* s);     /* frees everything; NULL is a no-op; synchronises the device */
+
+/* ------------------------------------------------------------------ build
+ * Alg. 1: rank items by hotness (desc, ties by id, R12), give
+ * group j scheme ladder[j]; then quantise every item (a3/a4) and place it
+ * (Alg. 2 step 1 by bytes, R15): GPU_LIST -> HBM arena, PIN_LIST -> pinned
+ * tier, the rest -> host backing.
+ *   hotness: host uint64[2*n_docs], the access-frequency vector AF. */
+hr_status hr_build_store(hr_store* s, uint32_t n_docs, const uint64_t* hotness,
+                         hr_src_fn src, void* user, void* stream);
+
+/* The same build in three calls: begin (ranking, schemes, placement,
+ * allocations), put (quantise one doc from caller-owned DEVICE buffers k_src,
+ * v_src, each [L][H][T][D] all heads, source dtype; they are read on
+ * `stream`, so the caller keeps them alive until the stream passes this
+ * point), end (synchronise; every doc must have been put and no NaN/Inf
+ * seen, else HR_EINVAL). */
+hr_status hr_build_begin(hr_store* s, uint32_t n_docs, const uint64_t* hotness);
+hr_status hr_build_put(hr_store* s, uint32_t doc, const void* k_src, const void* v_src, void* stream);
+hr_status hr_build_end(hr_store* s, void* stream);
+
+/* --------------------------------------------------------------- assemble
+ * a6-a8: for each request r (n_req requests of k DISTINCT doc ids, host
+ * uint32 [n_req][k], copied at call time) write this rank's heads of
+ *   K_out[r][l][h][j*T + t][d] = dequant(item 2*doc_{r,j})[l][h][t][d]
+ *   V_out[r][l][h][j*T + t][d] = dequant(item 2*doc_{r,j}+1)[l][h][t][d]
+ * into k_out[r] / v_out[r] (DEVICE pointers, each hr_kv_bytes(s,k) bytes,
+ * 16-B aligned, source dtype, RNE — R25).  HBM-resident items are decoded
+ * in place; host-tier items are streamed through the staging ring first
+ * (pageable -> pinned bounce -> HBM).  Also counts hotness (a1): each
+ * request q (running count over the store's life) with q % world == rank
+ * adds 1 to both items of each of its docs in the device delta vector.
+ * Stream-ordered: outputs are valid when `stream` reaches this point.
+ * Errors: unknown doc -> HR_ENOTFOUND; duplicate doc in one request or k == 0
+ * -> HR_EINVAL (R19); before build -> HR_ESTATE. */
+size_t    hr_kv_bytes(const hr_store* s, uint32_t k);   /* bytes of ONE of K/V for k docs on this rank */
+hr_status hr_assemble_kv(hr_store* s, uint32_t n_req, uint32_t k, const uint32_t* doc_ids,
+                         void* const* k_out, void* const* v_out, void* stream);
+
+/* ------------------------------------------------------- hotness / epochs
+ * a9 (R20).  hr_hotness_delta exposes the store's DEVICE int64[2*n_docs]
+ * per-item access counts since the last hr_replace (for an in-place
+ * torch.distributed.all_reduce(SUM) across ranks).  hr_replace consumes the
+ * (reduced) delta: h <- (h >> decay_shift) + delta, re-rank, recompute the
+ * GPU/PIN lists (schemes stay fixed: compress once), evict items that
+ * left GPU_LIST and promote the newcomers (H2D from the host backing; needs
+ * keep_backing = 1, else HR_ESTATE), zero the delta.  Synchronises `stream`. */
+hr_status hr_hotness_delta(hr_store* s, int64_t** dev_ptr, uint32_t* n);
+hr_status hr_replace(hr_store* s, void* stream);
+
+/* ------------------------------------------------------------- inspection */
+hr_status hr_item_info(const hr_store* s, uint32_t item, uint32_t* scheme, uint32_t* tier, uint64_t* bytes);
+hr_status hr_item_rank(const hr_store* s, uint32_t item, uint32_t* rank);   /* position in the hotness order */
+hr_status hr_export_item(const hr_store* s, uint32_t item, void* host_dst, size_t cap, size_t* len); /* packed blob; synchronous */
+hr_status hr_store_stats(const hr_store* s, hr_stats* out);                 /* synchronises pending timing events */
+hr_status hr_set_timing(hr_store* s, int enable);                           /* 1: time every assemble launch with CUDA events */
+hr_status hr_reset_stats(hr_store* s);
+
+/* ------------------------------------------ host policy (no GPU needed)
+ * The same C++ code the store uses, exposed for host-side tests and tools. */
+/* Alg. 1 line 1: order_out = item ids by (h desc, id asc). */
+hr_status hr_policy_rank(uint32_t n_items, const uint64_t* h, uint32_t* order_out);
+/* Alg. 1: scheme per item. */
+hr_status hr_policy_assign(uint32_t n_items, const uint64_t* h, uint32_t n_ladder, const uint32_t* ladder,
+                           const double* tau, uint32_t* scheme_out);
+/* Alg. 2 step 1 by bytes (R15): tier per item (0 HBM, 1 PIN, 2 PAGE). */
+hr_status hr_policy_lists_bytes(uint32_t n_items, const uint32_t* order, const uint64_t* sizes,
+                                uint64_t hbm_budget, uint64_t pin_budget, uint32_t* tier_out);
+/* Alg. 2 step 1 by fractions (R13, R14): list per item (0 GPU, 1 PIN, 2 PAGE, 3 DISK). */
+hr_status hr_policy_lists_fraction(uint32_t n_items, const uint32_t* order, double tau_gpu, double tau_pin,
+                                   double tau_page, uint32_t* list_out);
+/* a1 on the host: delta[2*doc+kind] += 1 for requests q = req_base + r with q % world == rank. */
+hr_status hr_policy_count(uint32_t n_req, uint32_t k, const uint32_t* ids, uint32_t n_docs, uint64_t req_base,
+                          uint32_t rank, uint32_t world, int64_t* delta_inout);
+/* a9: h <- (h >> decay_shift) + delta (negative results -> HR_EINVAL). */
+hr_status hr_policy_epoch(uint32_t n_items, uint64_t* h_inout, const int64_t* delta, uint32_t decay_shift);
+/* Packed blob size of one item for a config and scheme. */
+hr_status hr_item_bytes(const hr_store_config* cfg, uint32_t scheme, uint64_t* bytes);
+
+/* Alg. 2 step 2 demand-mode state machine.  list_of_item: 0 GPU,
+ * 1 PIN, 2 PAGE, 3 DISK; sizes: bytes per item (NULL = 1 each); caps in the
+ * same unit.  access(): hit_tier 0 GPU / 1 PIN / 2 PAGE / 3 DISK; put_mask bit
+ * t = inserted into tier t; evicted[0..*n_evicted) = (tier << 28 | item)
+ * (cap entries, HR_EINVAL if too small).  Inclusive promotion, LRU (R16). */
+hr_status hr_alg2_create(uint32_t n_items, const uint32_t* list_of_item, const uint64_t* sizes,
+                         uint64_t cap_gpu, uint64_t cap_pin, uint64_t cap_page, hr_alg2** out);
+hr_status hr_alg2_access(hr_alg2* a, uint32_t item, uint32_t* hit_tier, uint32_t* put_mask,
+                         uint32_t* evicted, uint32_t cap, uint32_t* n_evicted);
+hr_status hr_alg2_set_lists(hr_alg2* a, const uint32_t* list_of_item);
+hr_status hr_alg2_resident(const hr_alg2* a, uint32_t tier, uint32_t* items, uint32_t cap, uint32_t* n);
+void      hr_alg2_destroy(hr_alg2* a);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HARAG_H */

@@ -1,0 +1,523 @@
+// The HA-RAG store runtime (C++ / CUDA runtime API): packed chunk store,
+// tier placement (Alg. 1 + Alg. 2 step 1 by bytes), request planning
+// (Alg. 2 step 2 lookups), the host-tier streamer (pageable -> pinned bounce ->
+// HBM staging ring) and epochs (hotness decay + re-placement).
+#include "store.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <unordered_set>
+
+#include "kernels.h"
+#include "policy.h"
+
+namespace harag {
+
+// ------------------------------------------------------------ FreeList
+uint64_t FreeList::alloc(uint64_t size) {
+  size = align_up(size, kAlign);
+  for (auto it = free_.begin(); it != free_.end(); ++it) {  // first fit
+    if (it->second >= size) {
+      const uint64_t off = it->first, rest = it->second - size;
+      free_.erase(it);
+      if (rest) free_[off + size] = rest;
+      used_ += size;
+      return off;
+    }
+  }
+  return kNone;
+}
+
+void FreeList::release(uint64_t off, uint64_t size) {
+  size = align_up(size, kAlign);
+  used_ -= size;
+  auto it = free_.emplace(off, size).first;
+  auto next = std::next(it);
+  if (next != free_.end() && it->first + it->second == next->first) {
+    it->second += next->second;
+    free_.erase(next);
+  }
+  if (it != free_.begin()) {
+    auto prev = std::prev(it);
+    if (prev->first + prev->second == it->first) {
+      prev->second += it->second;
+      free_.erase(it);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- Store
+Store::Store(const hr_store_config& c) : cfg(c), lay(make_layout(c)) {
+  require(cfg.n_ladder >= 1 && cfg.n_ladder <= 6, HR_EINVAL, "n_ladder must be 1..6");
+  for (uint32_t j = 0; j < cfg.n_ladder; ++j) require(cfg.ladder[j] <= HR_S_INT4, HR_EINVAL, "unknown scheme in ladder");
+  double sum = 0;
+  for (uint32_t j = 0; j + 1 < cfg.n_ladder; ++j) {
+    require(cfg.tau[j] >= 0.0 && cfg.tau[j] <= 1.0, HR_EINVAL, "tau out of [0,1]");
+    sum += cfg.tau[j];
+  }
+  require(sum <= 1.0 + 1e-12, HR_EINVAL, "taus sum above 1");
+  require(cfg.demand_mode == 0, HR_EINVAL, "demand_mode store not available: use hr_alg2_* for the Alg. 2 state machine");
+  slots = cfg.staging_slots ? cfg.staging_slots : 3;
+  HR_CUDA(cudaSetDevice(cfg.device));
+  HR_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+}
+
+Store::~Store() {
+  cudaSetDevice(cfg.device);
+  cudaDeviceSynchronize();
+  for (auto& d : dbuf) {
+    if (d.dev) cudaFree(d.dev);
+    if (d.host) cudaFreeHost(d.host);
+    if (d.done) cudaEventDestroy(d.done);
+  }
+  for (auto& r : ring) {
+    if (r.dev) cudaFree(r.dev);
+    if (r.bounce) cudaFreeHost(r.bounce);
+    if (r.copied) cudaEventDestroy(r.copied);
+    if (r.free_ev) cudaEventDestroy(r.free_ev);
+  }
+  for (auto& t : timers) cudaEventDestroy(t.first), cudaEventDestroy(t.second);
+  if (hbm_base) cudaFree(hbm_base);
+  if (pin_base) cudaFreeHost(pin_base);
+  if (backing_base) {
+    if (backing_is_pinned)
+      cudaFreeHost(backing_base);
+    else
+      free(backing_base);
+  }
+  if (delta) cudaFree(delta);
+  if (err_flag) cudaFree(err_flag);
+  if (scratch) cudaFree(scratch);
+  if (src_k) cudaFree(src_k);
+  if (src_v) cudaFree(src_v);
+  if (copy_stream) cudaStreamDestroy(copy_stream);
+}
+
+uint8_t* Store::hbm_ptr(uint32_t item) const { return hbm_base + loc[item].hbm_off; }
+
+void Store::build_begin(uint32_t nd, const uint64_t* hot) {
+  require(state == State::Empty, HR_ESTATE, "store already built");
+  require(nd > 0, HR_EINVAL, "n_docs must be > 0");
+  require(hot != nullptr, HR_EINVAL, "hotness is NULL");
+  HR_CUDA(cudaSetDevice(cfg.device));
+  n_docs = nd;
+  n_items = 2 * nd;
+  h.assign(hot, hot + n_items);
+  // Alg. 1: schemes by hotness rank
+  scheme = assign_schemes(h.data(), n_items, cfg.ladder, cfg.n_ladder, cfg.tau);
+  bytes.resize(n_items);
+  for (uint32_t i = 0; i < n_items; ++i) bytes[i] = lay.item_bytes(scheme[i]);
+  // Alg. 2 step 1 by bytes (R15)
+  order = rank_items(h.data(), n_items);
+  tier = lists_by_bytes(order, bytes.data(), cfg.hbm_budget, cfg.backing_pinned ? 0 : cfg.pin_budget);
+  if (cfg.backing_pinned)
+    for (auto& t : tier)
+      if (t == HR_T_PAGE) t = HR_T_PIN;
+  loc.assign(n_items, Loc{});
+  max_item = 0;
+  for (uint32_t i = 0; i < n_items; ++i) max_item = std::max(max_item, bytes[i]);
+
+  // HBM arena: the whole budget (re-placement may fill it differently later)
+  if (cfg.hbm_budget) {
+    uint64_t need = 0;
+    for (uint32_t i = 0; i < n_items; ++i)
+      if (tier[i] == HR_T_HBM) need += align_up(bytes[i], FreeList::kAlign);
+    hbm_cap = cfg.keep_backing ? align_up(cfg.hbm_budget, FreeList::kAlign) : need;
+    if (hbm_cap) {
+      if (cudaMalloc(&hbm_base, hbm_cap) != cudaSuccess) {
+        cudaGetLastError();
+        fail(HR_ENOMEM, "cudaMalloc of the HBM arena failed");
+      }
+    }
+    hbm.reset(hbm_cap);
+  }
+  // pinned tier (PIN_LIST copies when the backing is pageable)
+  if (!cfg.backing_pinned && cfg.pin_budget) {
+    pin_cap = align_up(cfg.pin_budget, FreeList::kAlign);
+    if (cudaHostAlloc((void**)&pin_base, pin_cap, cudaHostAllocPortable) != cudaSuccess) {
+      cudaGetLastError();
+      fail(HR_ENOMEM, "cudaHostAlloc of the pinned tier failed");
+    }
+    pin.reset(pin_cap);
+  }
+  // host backing: one blob per item that needs one (all if keep_backing), aliased in bench mode
+  uint64_t total = 0;
+  std::map<uint64_t, uint64_t> alias_off;
+  for (uint32_t i = 0; i < n_items; ++i) {
+    if (!cfg.keep_backing && tier[i] == HR_T_HBM) continue;
+    const uint64_t key = backing_key(i);
+    auto it = alias_off.find(key);
+    if (it != alias_off.end()) {
+      loc[i].backing_off = it->second;
+      loc[i].backing_alias = true;
+    } else {
+      loc[i].backing_off = total;
+      alias_off[key] = total;
+      total += align_up(bytes[i], 4096);
+    }
+  }
+  if (total) {
+    backing_is_pinned = cfg.backing_pinned != 0;
+    if (backing_is_pinned) {
+      if (cudaHostAlloc((void**)&backing_base, total, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        fail(HR_ENOMEM, "cudaHostAlloc of the pinned backing failed");
+      }
+    } else {
+      backing_base = (uint8_t*)aligned_alloc(4096, total);
+      require(backing_base != nullptr, HR_ENOMEM, "host backing allocation failed");
+    }
+  }
+  backing_bytes = total;
+  // arena / pinned placement of the lists
+  for (uint32_t pos = 0; pos < n_items; ++pos) {
+    const uint32_t i = order[pos];
+    if (tier[i] == HR_T_HBM) {
+      loc[i].hbm_off = hbm.alloc(bytes[i]);
+      require(loc[i].hbm_off != FreeList::kNone, HR_ENOMEM, "HBM arena exhausted during placement");
+    } else if (tier[i] == HR_T_PIN && !cfg.backing_pinned) {
+      loc[i].pin_off = pin.alloc(bytes[i]);
+      require(loc[i].pin_off != FreeList::kNone, HR_ENOMEM, "pinned tier exhausted during placement");
+    }
+  }
+  HR_CUDA(cudaMalloc(&delta, sizeof(int64_t) * n_items));
+  HR_CUDA(cudaMemset(delta, 0, sizeof(int64_t) * n_items));
+  HR_CUDA(cudaMalloc(&err_flag, sizeof(int)));
+  HR_CUDA(cudaMemset(err_flag, 0, sizeof(int)));
+  HR_CUDA(cudaMalloc(&scratch, 2 * max_item));
+  put_done.assign(n_docs, 0);
+  backing_filled.clear();
+  state = State::Building;
+}
+
+uint64_t Store::backing_key(uint32_t item) const {
+  const uint32_t doc = item / 2, kind = item % 2;
+  const uint32_t adoc = cfg.bench_alias_R ? doc % cfg.bench_alias_R : doc;
+  if (!cfg.bench_alias_R) return item;
+  return ((uint64_t)adoc * 2 + kind) * 8 + scheme[item];
+}
+
+void Store::build_put(uint32_t doc, const void* k_src, const void* v_src, cudaStream_t st) {
+  require(state == State::Building, HR_ESTATE, "hr_build_put outside begin/end");
+  require(doc < n_docs, HR_ENOTFOUND, "doc id out of range");
+  require(k_src && v_src, HR_EINVAL, "source pointer is NULL");
+  for (uint32_t kind = 0; kind < 2; ++kind) {
+    const uint32_t item = 2 * doc + kind;
+    const uint32_t s = scheme[item];
+    uint8_t* dst = tier[item] == HR_T_HBM ? hbm_ptr(item) : scratch + kind * max_item;
+    QuantParams q{};
+    q.src = (const uint16_t*)(kind ? v_src : k_src);
+    q.dst = dst;
+    q.L = lay.L, q.H = lay.H, q.Hl = lay.Hl, q.h0 = lay.h0, q.T = lay.T, q.D = lay.D, q.G = lay.G;
+    q.gse_e = lay.gse_e, q.gse_m = lay.gse_m, q.dtype = lay.dtype, q.scheme = s;
+    q.code_bytes_slab = lay.code_bytes_slab(s);
+    q.meta_offset = lay.meta_offset(s);
+    q.meta_stride = lay.meta_stride(s);
+    q.err = err_flag;
+    // zero the blob's padding so exported blobs are deterministic
+    const uint64_t cend = lay.n_slabs() * q.code_bytes_slab;
+    const uint64_t mend = q.meta_offset + lay.n_slabs() * q.meta_stride;
+    if (q.meta_offset > cend) HR_CUDA(cudaMemsetAsync(dst + cend, 0, q.meta_offset - cend, st));
+    if (bytes[item] > mend) HR_CUDA(cudaMemsetAsync(dst + mend, 0, bytes[item] - mend, st));
+    launch_quantize(q, st);
+    if (loc[item].backing_off != FreeList::kNone && !backing_filled.count(loc[item].backing_off)) {
+      // bench aliasing: a shared blob is written once (its docs have identical sources by contract)
+      HR_CUDA(cudaMemcpyAsync(backing_base + loc[item].backing_off, dst, bytes[item], cudaMemcpyDeviceToHost, st));
+      backing_filled.insert(loc[item].backing_off);
+    }
+    if (loc[item].pin_off != FreeList::kNone)
+      HR_CUDA(cudaMemcpyAsync(pin_base + loc[item].pin_off, dst, bytes[item], cudaMemcpyDeviceToHost, st));
+  }
+  if (!put_done[doc]) ++n_put;
+  put_done[doc] = 1;
+}
+
+void Store::build_end(cudaStream_t st) {
+  require(state == State::Building, HR_ESTATE, "hr_build_end without hr_build_begin");
+  HR_CUDA(cudaStreamSynchronize(st));
+  int err = 0;
+  HR_CUDA(cudaMemcpy(&err, err_flag, sizeof(int), cudaMemcpyDeviceToHost));
+  require(n_put == n_docs, HR_EINVAL, "hr_build_end: not every doc was put");
+  require(err == 0, HR_EINVAL, "NaN/Inf in the source chunks (rejected at ingestion, S:30)");
+  cudaFree(scratch);
+  scratch = nullptr;
+  state = State::Built;
+}
+
+void Store::build_with_source(uint32_t nd, const uint64_t* hot, hr_src_fn src, void* user, cudaStream_t st) {
+  require(src != nullptr, HR_EINVAL, "source callback is NULL");
+  build_begin(nd, hot);
+  const uint64_t full = 2ull * lay.L * lay.H * lay.T * lay.D;
+  HR_CUDA(cudaMalloc(&src_k, full));
+  HR_CUDA(cudaMalloc(&src_v, full));
+  for (uint32_t d = 0; d < nd; ++d) {
+    const int rc = src(user, d, src_k, src_v, (void*)st);
+    require(rc == HR_OK, (hr_status)rc, "source callback failed for doc " + std::to_string(d));
+    build_put(d, src_k, src_v, st);
+  }
+  build_end(st);
+  cudaFree(src_k);
+  cudaFree(src_v);
+  src_k = src_v = nullptr;
+}
+
+// --------------------------------------------------------------- assemble
+Store::DescBuf& Store::desc_buffer(size_t n) {
+  if (dbuf.empty()) dbuf.resize(kDescBufs);
+  DescBuf& d = dbuf[dbuf_next];
+  dbuf_next = (dbuf_next + 1) % kDescBufs;
+  if (d.done) HR_CUDA(cudaEventSynchronize(d.done));  // previous user of this buffer finished
+  else HR_CUDA(cudaEventCreateWithFlags(&d.done, cudaEventDisableTiming));
+  if (d.cap < n) {
+    if (d.dev) HR_CUDA(cudaFree(d.dev));
+    if (d.host) HR_CUDA(cudaFreeHost(d.host));
+    d.cap = std::max<size_t>(n, 256);
+    HR_CUDA(cudaMalloc(&d.dev, d.cap * sizeof(AsmDesc)));
+    HR_CUDA(cudaHostAlloc((void**)&d.host, d.cap * sizeof(AsmDesc), cudaHostAllocPortable));
+  }
+  return d;
+}
+
+void Store::ensure_ring() {
+  if (!ring.empty()) return;
+  ring.resize(slots);
+  for (auto& r : ring) {
+    HR_CUDA(cudaMalloc(&r.dev, max_item));
+    HR_CUDA(cudaEventCreateWithFlags(&r.copied, cudaEventDisableTiming));
+    HR_CUDA(cudaEventCreateWithFlags(&r.free_ev, cudaEventDisableTiming));
+  }
+}
+
+void Store::launch(const AsmDesc* dev_descs, uint32_t n, uint32_t k, cudaStream_t st) {
+  AsmParams p{};
+  p.descs = dev_descs;
+  p.n_desc = n;
+  p.L = lay.L, p.Hl = lay.Hl, p.T = lay.T, p.D = lay.D, p.k = k, p.G = lay.G;
+  p.g_shift = (uint32_t)__builtin_ctz(lay.G);
+  p.gse_m = lay.gse_m;
+  p.dtype = lay.dtype;
+  p.slab = (uint32_t)lay.slab();
+  p.tiles_per_slab = (uint32_t)((lay.slab() + kAsmTileE - 1) / kAsmTileE);
+  p.n_tiles = (uint64_t)n * lay.L * lay.Hl * p.tiles_per_slab;
+  for (uint32_t s = 0; s <= HR_S_INT4; ++s) p.meta_stride[s] = (uint32_t)lay.meta_stride(s);
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (timing) {
+    HR_CUDA(cudaEventCreate(&a));
+    HR_CUDA(cudaEventCreate(&b));
+    HR_CUDA(cudaEventRecord(a, st));
+  }
+  launch_assemble(p, st, grid_override);
+  if (timing) {
+    HR_CUDA(cudaEventRecord(b, st));
+    timers.emplace_back(a, b);
+  }
+  stats.kernel_launches++;
+}
+
+void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* const* k_out, void* const* v_out,
+                     cudaStream_t st) {
+  require(state == State::Built, HR_ESTATE, "hr_assemble_kv before the store is built");
+  require(n_req > 0 && k > 0, HR_EINVAL, "n_req and k must be > 0");
+  require(ids && k_out && v_out, HR_EINVAL, "NULL argument");
+  // validate everything before any device work (no partial writes)
+  std::vector<uint32_t> tmp(k);
+  for (uint32_t r = 0; r < n_req; ++r) {
+    require(k_out[r] && v_out[r], HR_EINVAL, "NULL output pointer");
+    require(((uintptr_t)k_out[r] & 15) == 0 && ((uintptr_t)v_out[r] & 15) == 0, HR_EINVAL,
+            "output pointers must be 16-byte aligned");
+    for (uint32_t j = 0; j < k; ++j) {
+      tmp[j] = ids[(uint64_t)r * k + j];
+      require(tmp[j] < n_docs, HR_ENOTFOUND, "unknown doc id " + std::to_string(tmp[j]));
+    }
+    std::sort(tmp.begin(), tmp.end());
+    require(std::adjacent_find(tmp.begin(), tmp.end()) == tmp.end(), HR_EINVAL,
+            "duplicate doc id in request " + std::to_string(r) + " (R19)");
+  }
+  HR_CUDA(cudaSetDevice(cfg.device));
+  const size_t n_desc = 2ull * n_req * k;
+  DescBuf& db = desc_buffer(n_desc);
+  // Alg. 2 step 2 lookups (eager placement: GPU_LIST items are resident)
+  std::vector<uint32_t> miss_items;
+  std::unordered_map<uint32_t, std::vector<AsmDesc>> miss_descs;
+  size_t nh = 0;
+  for (uint32_t r = 0; r < n_req; ++r) {
+    const bool counted = ((req_counter + r) % (uint64_t)cfg.world) == (uint64_t)cfg.rank;
+    for (uint32_t j = 0; j < k; ++j) {
+      for (uint32_t kind = 0; kind < 2; ++kind) {
+        const uint32_t item = 2 * ids[(uint64_t)r * k + j] + kind;
+        AsmDesc d{};
+        d.out = (uint8_t*)(kind ? v_out[r] : k_out[r]);
+        d.count = counted ? reinterpret_cast<unsigned long long*>(delta + item) : nullptr;
+        d.slot = j;
+        d.scheme = scheme[item];
+        const uint64_t alg = lay.n_slabs() * lay.slab() * 2 + (bytes_read_alg(item));
+        stats.bytes_out += lay.n_slabs() * lay.slab() * 2;
+        stats.bytes_hbm_alg += alg;
+        if (loc[item].hbm_off != FreeList::kNone) {
+          d.codes = hbm_ptr(item);
+          d.meta = d.codes + lay.meta_offset(d.scheme);
+          db.host[nh++] = d;
+          stats.hits[HR_T_HBM]++;
+        } else {
+          auto it = miss_descs.find(item);
+          if (it == miss_descs.end()) {
+            miss_items.push_back(item);
+            it = miss_descs.emplace(item, std::vector<AsmDesc>{}).first;
+          }
+          it->second.push_back(d);
+          stats.hits[tier[item]]++;
+        }
+      }
+    }
+  }
+  // descriptors of the host-tier items point at their staging-ring slot
+  if (!miss_items.empty()) ensure_ring();
+  size_t pos = nh;
+  std::vector<std::pair<size_t, size_t>> miss_range;
+  for (size_t i = 0; i < miss_items.size(); ++i) {
+    const uint32_t item = miss_items[i];
+    uint8_t* slot_ptr = ring[i % slots].dev;
+    const size_t b = pos;
+    for (AsmDesc d : miss_descs[item]) {
+      d.codes = slot_ptr;
+      d.meta = slot_ptr + lay.meta_offset(d.scheme);
+      db.host[pos++] = d;
+    }
+    miss_range.emplace_back(b, pos - b);
+  }
+  HR_CUDA(cudaMemcpyAsync(db.dev, db.host, pos * sizeof(AsmDesc), cudaMemcpyHostToDevice, st));
+  // launch A: every HBM-resident (request, slot, kind)
+  if (nh) launch(db.dev, (uint32_t)nh, k, st);
+  // host-tier items: pinned (or pageable -> pinned bounce) -> staging ring -> launch B
+  for (size_t i = 0; i < miss_items.size(); ++i) {
+    const uint32_t item = miss_items[i];
+    Slot& sl = ring[i % slots];
+    const uint8_t* src = nullptr;
+    if (loc[item].pin_off != FreeList::kNone) {
+      src = pin_base + loc[item].pin_off;
+    } else {
+      require(loc[item].backing_off != FreeList::kNone, HR_ESTATE, "item has no host copy");
+      src = backing_base + loc[item].backing_off;
+      if (!backing_is_pinned) {  // pageable data is first copied to pinned memory
+        if (!sl.bounce) HR_CUDA(cudaHostAlloc((void**)&sl.bounce, max_item, cudaHostAllocPortable));
+        if (sl.used) HR_CUDA(cudaEventSynchronize(sl.copied));  // previous DMA out of this bounce buffer done
+        std::memcpy(sl.bounce, src, bytes[item]);
+        src = sl.bounce;
+      }
+    }
+    HR_CUDA(cudaStreamWaitEvent(copy_stream, sl.free_ev, 0));
+    HR_CUDA(cudaMemcpyAsync(sl.dev, src, bytes[item], cudaMemcpyHostToDevice, copy_stream));
+    HR_CUDA(cudaEventRecord(sl.copied, copy_stream));
+    sl.used = true;
+    stats.bytes_h2d += bytes[item];
+    HR_CUDA(cudaStreamWaitEvent(st, sl.copied, 0));
+    launch(db.dev + miss_range[i].first, (uint32_t)miss_range[i].second, k, st);
+    HR_CUDA(cudaEventRecord(sl.free_ev, st));
+  }
+  HR_CUDA(cudaEventRecord(db.done, st));
+  req_counter += n_req;
+  stats.requests += n_req;
+}
+
+uint64_t Store::bytes_read_alg(uint32_t item) const {
+  const uint32_t s = scheme[item];
+  return lay.n_slabs() * (lay.code_bytes_slab(s) + lay.meta_raw_slab(s));
+}
+
+// ---------------------------------------------------------------- epochs
+void Store::replace(cudaStream_t st) {
+  require(state == State::Built, HR_ESTATE, "hr_replace before the store is built");
+  HR_CUDA(cudaSetDevice(cfg.device));
+  HR_CUDA(cudaStreamSynchronize(st));
+  std::vector<int64_t> dh(n_items);
+  HR_CUDA(cudaMemcpy(dh.data(), delta, sizeof(int64_t) * n_items, cudaMemcpyDeviceToHost));
+  epoch_update(h.data(), dh.data(), n_items, cfg.decay_shift);  // a9 (R20)
+  HR_CUDA(cudaMemsetAsync(delta, 0, sizeof(int64_t) * n_items, st));
+  order = rank_items(h.data(), n_items);
+  std::vector<uint32_t> nt = lists_by_bytes(order, bytes.data(), cfg.hbm_budget, cfg.backing_pinned ? 0 : cfg.pin_budget);
+  if (cfg.backing_pinned)
+    for (auto& t : nt)
+      if (t == HR_T_PAGE) t = HR_T_PIN;
+  bool any_move = false;
+  for (uint32_t i = 0; i < n_items; ++i) any_move |= (nt[i] == HR_T_HBM) != (loc[i].hbm_off != FreeList::kNone);
+  require(!any_move || cfg.keep_backing, HR_ESTATE, "re-placement needs keep_backing = 1");
+  // evict first (host copies are inclusive, R16)
+  for (uint32_t i = 0; i < n_items; ++i) {
+    if (nt[i] != HR_T_HBM && loc[i].hbm_off != FreeList::kNone) {
+      hbm.release(loc[i].hbm_off, bytes[i]);
+      loc[i].hbm_off = FreeList::kNone;
+      stats.migrations_out++;
+    }
+    if (nt[i] != HR_T_PIN && loc[i].pin_off != FreeList::kNone) {
+      pin.release(loc[i].pin_off, bytes[i]);
+      loc[i].pin_off = FreeList::kNone;
+    }
+  }
+  // promote in rank order
+  for (uint32_t pos = 0; pos < n_items; ++pos) {
+    const uint32_t i = order[pos];
+    if (nt[i] == HR_T_HBM && loc[i].hbm_off == FreeList::kNone) {
+      const uint64_t off = hbm.alloc(bytes[i]);
+      if (off == FreeList::kNone) {
+        stats.failed_promotions++;
+        nt[i] = cfg.backing_pinned ? HR_T_PIN : HR_T_PAGE;
+        continue;
+      }
+      loc[i].hbm_off = off;
+      HR_CUDA(cudaMemcpyAsync(hbm_base + off, backing_base + loc[i].backing_off, bytes[i], cudaMemcpyHostToDevice,
+                              copy_stream));
+      stats.migrations_in++;
+    } else if (nt[i] == HR_T_PIN && !cfg.backing_pinned && loc[i].pin_off == FreeList::kNone) {
+      const uint64_t off = pin.alloc(bytes[i]);
+      if (off == FreeList::kNone) {
+        nt[i] = HR_T_PAGE;
+        continue;
+      }
+      loc[i].pin_off = off;
+      std::memcpy(pin_base + off, backing_base + loc[i].backing_off, bytes[i]);
+    }
+  }
+  tier = nt;
+  HR_CUDA(cudaStreamSynchronize(copy_stream));
+  HR_CUDA(cudaStreamSynchronize(st));
+}
+
+void Store::export_item(uint32_t item, void* dst, size_t cap, size_t* len) const {
+  require(state == State::Built, HR_ESTATE, "store not built");
+  require(item < n_items, HR_ENOTFOUND, "item id out of range");
+  if (len) *len = bytes[item];
+  require(cap >= bytes[item], HR_EINVAL, "destination too small");
+  if (loc[item].hbm_off != FreeList::kNone) {
+    HR_CUDA(cudaSetDevice(cfg.device));
+    HR_CUDA(cudaDeviceSynchronize());
+    HR_CUDA(cudaMemcpy(dst, hbm_ptr(item), bytes[item], cudaMemcpyDeviceToHost));
+  } else if (loc[item].pin_off != FreeList::kNone) {
+    std::memcpy(dst, pin_base + loc[item].pin_off, bytes[item]);
+  } else {
+    require(loc[item].backing_off != FreeList::kNone, HR_ESTATE, "item has no copy");
+    std::memcpy(dst, backing_base + loc[item].backing_off, bytes[item]);
+  }
+}
+
+void Store::get_stats(hr_stats* out) {
+  if (!timers.empty()) {
+    for (auto& t : timers) {
+      HR_CUDA(cudaEventSynchronize(t.second));
+      float ms = 0;
+      HR_CUDA(cudaEventElapsedTime(&ms, t.first, t.second));
+      stats.kernel_ms += ms;
+      stats.timed_launches++;
+      cudaEventDestroy(t.first);
+      cudaEventDestroy(t.second);
+    }
+    timers.clear();
+  }
+  stats.hbm_used = hbm.used();
+  stats.pin_used = pin.used();
+  *out = stats;
+}
+
+}  // namespace harag

@@ -1,0 +1,121 @@
+// The HA-RAG store (one per rank / GPU).  See store.cpp and DESIGN.md §1, §4.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <unordered_set>
+#include <utility>
+#include <vector>
+
+#include "common.h"
+#include "kernels.h"
+#include "layout.h"
+
+namespace harag {
+
+// First-fit free list over one contiguous region (HBM arena / pinned tier).
+class FreeList {
+ public:
+  static constexpr uint64_t kAlign = 256;
+  static constexpr uint64_t kNone = ~0ull;
+  void reset(uint64_t cap) {
+    free_.clear();
+    used_ = 0;
+    if (cap) free_[0] = cap;
+  }
+  uint64_t alloc(uint64_t size);  // kNone when no contiguous block fits
+  void release(uint64_t off, uint64_t size);
+  uint64_t used() const { return used_; }
+
+ private:
+  std::map<uint64_t, uint64_t> free_;  // offset -> size
+  uint64_t used_ = 0;
+};
+
+struct Store {
+  enum class State { Empty, Building, Built };
+  struct Loc {
+    uint64_t hbm_off = FreeList::kNone;      // HBM arena copy
+    uint64_t pin_off = FreeList::kNone;      // pinned-tier copy
+    uint64_t backing_off = FreeList::kNone;  // host backing copy
+    bool backing_alias = false;
+  };
+  struct DescBuf {
+    AsmDesc* dev = nullptr;
+    AsmDesc* host = nullptr;  // pinned
+    size_t cap = 0;
+    cudaEvent_t done = nullptr;
+  };
+  struct Slot {  // host-tier staging ring slot
+    uint8_t* dev = nullptr;
+    uint8_t* bounce = nullptr;  // pinned bounce buffer for pageable items
+    cudaEvent_t copied = nullptr, free_ev = nullptr;
+    bool used = false;
+  };
+  static constexpr int kDescBufs = 8;
+
+  explicit Store(const hr_store_config& c);
+  ~Store();
+
+  void build_begin(uint32_t n_docs, const uint64_t* hotness);
+  void build_put(uint32_t doc, const void* k_src, const void* v_src, cudaStream_t st);
+  void build_end(cudaStream_t st);
+  void build_with_source(uint32_t n_docs, const uint64_t* hotness, hr_src_fn src, void* user, cudaStream_t st);
+  void assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* const* k_out, void* const* v_out,
+                cudaStream_t st);
+  void replace(cudaStream_t st);
+  void export_item(uint32_t item, void* dst, size_t cap, size_t* len) const;
+  void get_stats(hr_stats* out);
+
+  uint8_t* hbm_ptr(uint32_t item) const;
+  uint64_t backing_key(uint32_t item) const;
+  uint64_t bytes_read_alg(uint32_t item) const;
+  DescBuf& desc_buffer(size_t n);
+  void ensure_ring();
+  void launch(const AsmDesc* dev_descs, uint32_t n, uint32_t k, cudaStream_t st);
+
+  hr_store_config cfg;
+  Layout lay;
+  State state = State::Empty;
+  uint32_t n_docs = 0, n_items = 0, n_put = 0;
+  uint32_t slots = 3;
+  std::vector<uint64_t> h;       // hotness per item (AF)
+  std::vector<uint32_t> scheme;  // Alg. 1 result
+  std::vector<uint64_t> bytes;   // packed blob bytes per item
+  std::vector<uint32_t> order;   // hotness rank order
+  std::vector<uint32_t> tier;    // current tier per item
+  std::vector<Loc> loc;
+  std::vector<uint8_t> put_done;
+  std::unordered_set<uint64_t> backing_filled;
+  uint64_t max_item = 0;
+
+  uint8_t* hbm_base = nullptr;
+  uint64_t hbm_cap = 0;
+  FreeList hbm;
+  uint8_t* pin_base = nullptr;
+  uint64_t pin_cap = 0;
+  FreeList pin;
+  uint8_t* backing_base = nullptr;
+  uint64_t backing_bytes = 0;
+  bool backing_is_pinned = false;
+
+  int64_t* delta = nullptr;  // device int64[n_items] hotness delta (a1)
+  int* err_flag = nullptr;
+  uint8_t* scratch = nullptr;  // build: quantised blobs headed for the host
+  void* src_k = nullptr;
+  void* src_v = nullptr;
+  cudaStream_t copy_stream = nullptr;
+  std::vector<DescBuf> dbuf;
+  int dbuf_next = 0;
+  std::vector<Slot> ring;
+  uint64_t req_counter = 0;
+
+  bool timing = false;
+  int grid_override = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timers;
+  hr_stats stats{};
+};
+
+}  // namespace harag

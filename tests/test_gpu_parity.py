@@ -1,0 +1,288 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, on the
+same seeded inputs.  Packed blobs, placement and assembled KV are compared bit
+for bit (R3: both sides take every decision in fp32 RNE)."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import hotness, placement
+from oracle import store as ost
+
+pytestmark = pytest.mark.gpu
+
+NAMES = {"PASS16": ost.PASS16, "INT8": ost.INT8, "FP8E4M3": ost.FP8E4M3, "FP8E5M2": ost.FP8E5M2,
+         "GSE8": ost.GSE8, "INT4": ost.INT4}
+PAPER = ("INT8", "FP8E4M3", "FP8E5M2", "GSE8")
+NORTH = ("PASS16", "INT8", "INT4")
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def gpu_source(L, H, T, D, dtype, seed=synth.CORPUS_SEED):
+    def src(doc, kp, vp, stream):
+        synth.gen_item_device(kp, L, H, T, D, doc, 0, dtype=dtype, seed=seed, stream=stream)
+        synth.gen_item_device(vp, L, H, T, D, doc, 1, dtype=dtype, seed=seed, stream=stream)
+    return src
+
+
+def make_pair(torch, *, L, H, T, D, n_docs, ladder, taus, dtype="bf16", group=0, gse=(4, 3),
+              hbm_items=None, pin_items=0, rank=0, world=1, hot_seed=7, backing_pinned=False,
+              keep_backing=True, decay_shift=1):
+    """Build the GPU store and the oracle store on the same inputs."""
+    import paper_2510_20878_b200 as hr
+    prof = synth.gen_requests(n_docs, 4 * n_docs, min(4, n_docs), 1.1, seed=hot_seed)
+    h = hotness.count_requests(prof, n_docs).astype(np.uint64)
+    lay = ost.Layout(L=L, H=H, T=T, D=D, dtype=dtype, group=group, gse_e=gse[0], gse_m=gse[1],
+                     rank=rank, world=world)
+    schemes = hotness.assign_schemes(h.tolist(), [NAMES[s] for s in ladder], taus)
+    sizes = [lay.item_bytes(s) for s in schemes]
+    order = hotness.rank_items(h)
+    if hbm_items is None:
+        hbm_budget = sum(sizes) + 4096
+    else:
+        hbm_budget = sum(sizes[i] for i in order[:hbm_items])
+    pin_budget = sum(sizes[i] for i in order[len(order) if hbm_items is None else hbm_items:][:pin_items])
+    st = hr.Store(L=L, H=H, D=D, T=T, dtype=dtype, group=group, gse=gse, ladder=ladder, taus=taus,
+                  hbm_budget=hbm_budget, pin_budget=pin_budget, rank=rank, world=world,
+                  backing_pinned=backing_pinned, keep_backing=keep_backing, decay_shift=decay_shift)
+    st.build(n_docs, h, gpu_source(L, H, T, D, dtype))
+    ora = ost.OracleStore(lay, [NAMES[s] for s in ladder], taus)
+    ora.build(n_docs, h, lambda d, k: synth.gen_item(L, H, T, D, d, k, heads=lay.heads, dtype=dtype))
+    return st, ora, lay, h, sizes
+
+
+def alloc_out(torch, st, n_req, k):
+    nb = st.kv_bytes(k)
+    ko = [torch.full((nb // 2,), 0x7FFF, dtype=torch.int16, device="cuda") for _ in range(n_req)]
+    vo = [torch.full((nb // 2,), 0x7FFF, dtype=torch.int16, device="cuda") for _ in range(n_req)]
+    return ko, vo
+
+
+def check_requests(torch, st, ora, lay, reqs):
+    k = reqs.shape[1]
+    ko, vo = alloc_out(torch, st, len(reqs), k)
+    st.assemble(reqs, ko, vo)
+    torch.cuda.synchronize()
+    for r, req in enumerate(reqs):
+        K, V = ora.assemble(list(req))
+        gk = ko[r].cpu().numpy().view(np.uint16).reshape(K.shape)
+        gv = vo[r].cpu().numpy().view(np.uint16).reshape(V.shape)
+        assert np.array_equal(gk, K), f"K mismatch request {r}: {np.argwhere(gk != K)[:5]}"
+        assert np.array_equal(gv, V), f"V mismatch request {r}"
+
+
+# ------------------------------------------------------------------ synth
+def test_device_generator_matches_numpy(torch_cuda):
+    torch = torch_cuda
+    for (L, H, T, D, dtype, heads) in [(2, 2, 64, 64, "fp16", None), (3, 8, 512, 128, "bf16", (2, 5))]:
+        h0, h1 = heads or (0, H)
+        for kind in (0, 1):
+            buf = torch.empty(L * (h1 - h0) * T * D, dtype=torch.int16, device="cuda")
+            synth.gen_item_device(buf.data_ptr(), L, H, T, D, 11, kind, heads=heads, dtype=dtype)
+            torch.cuda.synchronize()
+            want = synth.gen_item(L, H, T, D, 11, kind, heads=heads, dtype=dtype)
+            assert np.array_equal(buf.cpu().numpy().view(np.uint16).reshape(want.shape), want)
+
+
+# -------------------------------------------------------- packed blobs (a3/a4)
+@pytest.mark.parametrize("scheme", list(NAMES))
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+def test_packed_blobs_bitexact_tiny(torch_cuda, scheme, dtype):
+    st, ora, lay, h, _ = make_pair(torch_cuda, L=2, H=2, T=64, D=64, n_docs=6, ladder=(scheme,), taus=(),
+                                   dtype=dtype)
+    for item in range(12):
+        s, tier, nbytes = st.item_info(item)
+        assert s == NAMES[scheme] and nbytes == lay.item_bytes(s)
+        assert np.array_equal(st.export_item(item), ora.blobs[item]), (scheme, item)
+
+
+@pytest.mark.parametrize("scheme", list(NAMES))
+@pytest.mark.parametrize("group,gse", [(32, (3, 4)), (4096 * 2, (2, 5))])
+def test_packed_blobs_groups_and_layouts(torch_cuda, scheme, group, gse):
+    st, ora, lay, h, _ = make_pair(torch_cuda, L=1, H=2, T=128, D=64, n_docs=3, ladder=(scheme,), taus=(),
+                                   group=group, gse=gse)
+    for item in range(6):
+        assert np.array_equal(st.export_item(item), ora.blobs[item]), (scheme, item)
+
+
+def test_packed_blobs_full_shape_sampled(torch_cuda):
+    """Llama-3-8B item shape (32 x 8 x 512 x 128): every scheme's blob, sampled
+    slabs recomputed by the oracle one by one."""
+    import paper_2510_20878_b200 as hr
+    torch = torch_cuda
+    L, H, T, D = 32, 8, 512, 128
+    lay = ost.Layout(L=L, H=H, T=T, D=D)
+    rng = np.random.default_rng(0)
+    for scheme in NAMES:
+        st = hr.Store(L=L, H=H, D=D, T=T, ladder=(scheme,), taus=(), hbm_budget=2 * lay.item_bytes(NAMES[scheme]) + 4096)
+        st.build(1, np.array([3, 1], np.uint64), gpu_source(L, H, T, D, "bf16"))
+        for item in (0, 1):
+            blob = st.export_item(item)
+            src = None
+            for (l, hh) in [(0, 0), (31, 7)] + [tuple(x) for x in rng.integers(0, [L, H], (2, 2))]:
+                if src is None:
+                    src = synth.gen_item(L, H, T, D, 0, item)
+                c, m = ost.encode_slab(src[l, hh], NAMES[scheme], lay)
+                i = l * H + hh
+                cb, mo, mr = lay.code_bytes(NAMES[scheme]), lay.meta_offset(NAMES[scheme]), lay.meta_record(NAMES[scheme])
+                assert np.array_equal(blob[i * cb:(i + 1) * cb], c), (scheme, item, l, hh)
+                assert np.array_equal(blob[mo + i * mr: mo + (i + 1) * mr], m), (scheme, item, l, hh)
+        st.close()
+
+
+def test_nan_rejected(torch_cuda):
+    import paper_2510_20878_b200 as hr
+    torch = torch_cuda
+    st = hr.Store(L=1, H=1, D=64, T=64, ladder=("INT8",), taus=(), hbm_budget=1 << 20)
+    k = torch.zeros(64 * 64, dtype=torch.int16, device="cuda")
+    v = torch.zeros(64 * 64, dtype=torch.int16, device="cuda")
+    v[100] = 0x7FC0
+    st.build_begin(1, np.zeros(2, np.uint64))
+    st.build_put(0, k, v)
+    with pytest.raises(hr.HaragError, match="EINVAL"):
+        st.build_end()
+
+
+# ------------------------------------------------------ assemble (a6-a8, a1)
+@pytest.mark.parametrize("ladder,taus,dtype", [(NORTH, (0.25, 0.25), "fp16"), (PAPER, (0.1, 0.1, 0.1), "bf16"),
+                                               (PAPER, (0.25, 0.25, 0.25), "fp16")])
+def test_assemble_tiny_all_hbm(torch_cuda, ladder, taus, dtype):
+    """BASELINE config 0: 16 chunks x 64 tokens, 2 layers, 2 KV heads, head_dim 64, top-k 4."""
+    st, ora, lay, h, _ = make_pair(torch_cuda, L=2, H=2, T=64, D=64, n_docs=16, ladder=ladder, taus=taus,
+                                   dtype=dtype)
+    reqs = synth.gen_requests(16, 64, 4, 1.1, seed=1)
+    check_requests(torch_cuda, st, ora, lay, reqs)
+
+
+def test_assemble_tiny_tiered(torch_cuda):
+    """HBM + pinned + pageable tiers (eager placement by bytes) on the tiny config:
+    placement equals the oracle's and every output is bit-exact."""
+    torch = torch_cuda
+    st, ora, lay, h, sizes = make_pair(torch, L=2, H=2, T=64, D=64, n_docs=16, ladder=NORTH, taus=(0.25, 0.25),
+                                       dtype="fp16", hbm_items=8, pin_items=8)
+    hb = sum(sizes[i] for i in hotness.rank_items(h)[:8])
+    pb = sum(sizes[i] for i in hotness.rank_items(h)[8:16])
+    want = placement.eager_tiers(h, sizes, hb, pb)
+    names = {0: placement.GPU, 1: placement.PIN, 2: placement.PAGE}
+    got = [names[st.item_info(i)[1]] for i in range(32)]
+    assert got == want
+    reqs = synth.gen_requests(16, 64, 4, 1.1, seed=1)
+    check_requests(torch, st, ora, lay, reqs)
+    s = st.stats()
+    assert sum(s["hits"]) == 64 * 4 * 2 and s["hits"][1] > 0 and s["hits"][2] > 0
+
+
+def test_assemble_pinned_backing_and_ragged(torch_cuda):
+    """Pinned backing (config-3 style), ragged slab (T*D = 17408 = 2 tiles + 1024)."""
+    st, ora, lay, h, _ = make_pair(torch_cuda, L=2, H=2, T=136, D=128, n_docs=10, ladder=PAPER,
+                                   taus=(0.2, 0.2, 0.2), hbm_items=6, backing_pinned=True)
+    reqs = synth.gen_requests(10, 12, 3, 1.1, seed=2)
+    check_requests(torch_cuda, st, ora, lay, reqs)
+
+
+def test_assemble_small_slab_and_group32(torch_cuda):
+    st, ora, lay, h, _ = make_pair(torch_cuda, L=3, H=4, T=100, D=64, n_docs=8, ladder=("INT4", "INT8", "GSE8"),
+                                   taus=(0.3, 0.3), group=32, gse=(3, 4))
+    reqs = synth.gen_requests(8, 10, 5, 1.1, seed=3)
+    check_requests(torch_cuda, st, ora, lay, reqs)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_head_sharded_equals_oracle(torch_cuda, world):
+    """KV-head sharding: each rank's store assembles exactly its
+    heads of the unsharded oracle result."""
+    reqs = synth.gen_requests(12, 6, 4, 1.1, seed=4)
+    full = None
+    for rank in range(world):
+        st, ora, lay, h, _ = make_pair(torch_cuda, L=2, H=4, T=64, D=64, n_docs=12, ladder=PAPER,
+                                       taus=(0.2, 0.2, 0.2), rank=rank, world=world)
+        check_requests(torch_cuda, st, ora, lay, reqs)
+        if full is None:
+            _, fora, flay, _, _ = make_pair(torch_cuda, L=2, H=4, T=64, D=64, n_docs=12, ladder=PAPER,
+                                            taus=(0.2, 0.2, 0.2))
+            full = [fora.assemble(list(r)) for r in reqs]
+        for r, req in enumerate(reqs):
+            K, V = ora.assemble(list(req))
+            h0, h1 = lay.heads
+            assert np.array_equal(K, full[r][0][:, h0:h1]) and np.array_equal(V, full[r][1][:, h0:h1])
+        st.close()
+
+
+def test_assemble_full_shape_sampled(torch_cuda):
+    """Llama-3-8B shape, paper ladder, batch of 4 requests x k=10 in the
+    launch configuration bench.py times; sampled (l, h) slabs of every output
+    checked against the oracle's decode of that slab."""
+    import paper_2510_20878_b200 as hr
+    torch = torch_cuda
+    L, H, T, D, n_docs, k = 32, 8, 512, 128, 24, 10
+    lay = ost.Layout(L=L, H=H, T=T, D=D)
+    prof = synth.gen_requests(n_docs, 200, k, 1.1, seed=9)
+    h = hotness.count_requests(prof, n_docs).astype(np.uint64)
+    schemes = hotness.assign_schemes(h.tolist(), [NAMES[s] for s in PAPER], (0.1, 0.1, 0.1))
+    st = hr.Store(L=L, H=H, D=D, T=T, ladder=PAPER, taus=(0.1, 0.1, 0.1),
+                  hbm_budget=sum(lay.item_bytes(s) for s in schemes) + 4096, keep_backing=False)
+    st.build(n_docs, h, gpu_source(L, H, T, D, "bf16"))
+    reqs = synth.gen_requests(n_docs, 4, k, 1.1, seed=1)
+    ko, vo = alloc_out(torch, st, 4, k)
+    st.assemble(reqs, ko, vo)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(5)
+    for r in range(4):
+        gk = ko[r].view(L, H, k * T, D)
+        gv = vo[r].view(L, H, k * T, D)
+        for j in rng.choice(k, 3, replace=False):
+            doc = int(reqs[r, j])
+            for kind, g in ((0, gk), (1, gv)):
+                item = 2 * doc + kind
+                src = synth.gen_item(L, H, T, D, doc, kind)
+                for (l, hh) in [(0, 0), (L - 1, H - 1), tuple(rng.integers(0, [L, H]))]:
+                    c, m = ost.encode_slab(src[l, hh], schemes[item], lay)
+                    want = ost.decode_slab(c, m, schemes[item], lay)
+                    got = g[l, hh, j * T:(j + 1) * T].cpu().numpy().view(np.uint16).reshape(-1)
+                    assert np.array_equal(got, want), (r, j, kind, l, hh)
+
+
+# ------------------------------------------------------------- hotness / epochs
+def test_hotness_delta_counts_and_replace(torch_cuda):
+    torch = torch_cuda
+    st, ora, lay, h, sizes = make_pair(torch, L=2, H=2, T=64, D=64, n_docs=16, ladder=NORTH, taus=(0.25, 0.25),
+                                       dtype="fp16", hbm_items=6, pin_items=6, decay_shift=1)
+    hb = sum(sizes[i] for i in hotness.rank_items(h)[:6])
+    pb = sum(sizes[i] for i in hotness.rank_items(h)[6:12])
+    hcur = h.astype(np.int64)
+    for epoch in range(4):
+        reqs = synth.gen_requests(16, 40, 4, 1.1, seed=100 + epoch, perm_seed=500 + epoch)
+        check_requests(torch, st, ora, lay, reqs)
+        delta = st.hotness_delta()
+        assert np.array_equal(delta.cpu().numpy(), hotness.count_requests(reqs, 16))
+        st.replace()
+        hcur = hotness.epoch_update(hcur, hotness.count_requests(reqs, 16), 1)
+        want = placement.eager_tiers(hcur, sizes, hb, pb)
+        names = {0: placement.GPU, 1: placement.PIN, 2: placement.PAGE}
+        assert [names[st.item_info(i)[1]] for i in range(32)] == want, epoch
+        assert not st.hotness_delta().any()
+    assert st.stats()["migrations_in"] > 0
+
+
+# --------------------------------------------------------------- error paths
+def test_validation_before_any_write(torch_cuda):
+    import paper_2510_20878_b200 as hr
+    torch = torch_cuda
+    st, ora, lay, h, _ = make_pair(torch, L=2, H=2, T=64, D=64, n_docs=8, ladder=NORTH, taus=(0.25, 0.25),
+                                   dtype="fp16")
+    ko, vo = alloc_out(torch, st, 2, 3)
+    with pytest.raises(hr.HaragError, match="EINVAL"):
+        st.assemble(np.array([[1, 2, 3], [4, 4, 5]]), ko, vo)
+    with pytest.raises(hr.HaragError, match="ENOTFOUND"):
+        st.assemble(np.array([[1, 2, 3], [4, 8, 5]]), ko, vo)
+    torch.cuda.synchronize()
+    assert bool((ko[0] == 0x7FFF).all()) and bool((vo[1] == 0x7FFF).all())
+    st2 = hr.Store(L=2, H=2, D=64, T=64, ladder=NORTH, taus=(0.25, 0.25), hbm_budget=1 << 20)
+    with pytest.raises(hr.HaragError, match="ESTATE"):
+        st2.assemble(np.array([[0]]), ko[:1], vo[:1])
