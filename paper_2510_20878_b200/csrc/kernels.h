@@ -18,7 +18,7 @@ struct AsmDesc {
   uint32_t scheme;           // hr_scheme
 };
 
-constexpr int kAsmThreads = 256;
+constexpr int kAsmThreads = 288;       // 1 producer warp + 8 consumer warps
 constexpr int kAsmTileE = 8192;       // elements per tile (16 KB of 16-bit output)
 constexpr int kAsmStages = 4;         // shared-memory ring depth
 constexpr int kAsmCodeStage = 2 * kAsmTileE;           // PASS16 worst case

@@ -432,6 +432,7 @@ void Store::replace(cudaStream_t st) {
   require(state == State::Built, HR_ESTATE, "hr_replace before the store is built");
   HR_CUDA(cudaSetDevice(cfg.device));
   HR_CUDA(cudaStreamSynchronize(st));
+  HR_CUDA(cudaDeviceSynchronize());  // no assemble may read the arena while items move
   std::vector<int64_t> dh(n_items);
   HR_CUDA(cudaMemcpy(dh.data(), delta, sizeof(int64_t) * n_items, cudaMemcpyDeviceToHost));
   epoch_update(h.data(), dh.data(), n_items, cfg.decay_shift);  // a9 (R20)
@@ -460,7 +461,11 @@ void Store::replace(cudaStream_t st) {
   for (uint32_t pos = 0; pos < n_items; ++pos) {
     const uint32_t i = order[pos];
     if (nt[i] == HR_T_HBM && loc[i].hbm_off == FreeList::kNone) {
-      const uint64_t off = hbm.alloc(bytes[i]);
+      uint64_t off = hbm.alloc(bytes[i]);
+      if (off == FreeList::kNone && hbm_cap - hbm.used() >= align_up(bytes[i], FreeList::kAlign)) {
+        compact_hbm();  // the lists fit the budget by construction: defragment and retry
+        off = hbm.alloc(bytes[i]);
+      }
       if (off == FreeList::kNone) {
         stats.failed_promotions++;
         nt[i] = cfg.backing_pinned ? HR_T_PIN : HR_T_PAGE;
@@ -471,7 +476,11 @@ void Store::replace(cudaStream_t st) {
                               copy_stream));
       stats.migrations_in++;
     } else if (nt[i] == HR_T_PIN && !cfg.backing_pinned && loc[i].pin_off == FreeList::kNone) {
-      const uint64_t off = pin.alloc(bytes[i]);
+      uint64_t off = pin.alloc(bytes[i]);
+      if (off == FreeList::kNone && pin_cap - pin.used() >= align_up(bytes[i], FreeList::kAlign)) {
+        compact_pin();
+        off = pin.alloc(bytes[i]);
+      }
       if (off == FreeList::kNone) {
         nt[i] = HR_T_PAGE;
         continue;
@@ -483,6 +492,52 @@ void Store::replace(cudaStream_t st) {
   tier = nt;
   HR_CUDA(cudaStreamSynchronize(copy_stream));
   HR_CUDA(cudaStreamSynchronize(st));
+}
+
+void Store::compact_hbm() {
+  std::vector<std::pair<uint64_t, uint32_t>> res;
+  for (uint32_t i = 0; i < n_items; ++i)
+    if (loc[i].hbm_off != FreeList::kNone) res.emplace_back(loc[i].hbm_off, i);
+  std::sort(res.begin(), res.end());
+  uint8_t* tmp = nullptr;
+  uint64_t cursor = 0;
+  for (auto& r : res) {
+    const uint32_t i = r.second;
+    const uint64_t sz = align_up(bytes[i], FreeList::kAlign);
+    if (r.first != cursor) {
+      if (r.first - cursor >= sz) {
+        HR_CUDA(cudaMemcpyAsync(hbm_base + cursor, hbm_base + r.first, bytes[i], cudaMemcpyDeviceToDevice,
+                                copy_stream));
+      } else {  // overlapping move: through a bounce buffer
+        if (!tmp) HR_CUDA(cudaMalloc(&tmp, max_item));
+        HR_CUDA(cudaMemcpyAsync(tmp, hbm_base + r.first, bytes[i], cudaMemcpyDeviceToDevice, copy_stream));
+        HR_CUDA(cudaMemcpyAsync(hbm_base + cursor, tmp, bytes[i], cudaMemcpyDeviceToDevice, copy_stream));
+      }
+      loc[i].hbm_off = cursor;
+    }
+    cursor += sz;
+  }
+  HR_CUDA(cudaStreamSynchronize(copy_stream));
+  if (tmp) HR_CUDA(cudaFree(tmp));
+  hbm.reset_compacted(cursor, hbm_cap);
+  compactions++;
+}
+
+void Store::compact_pin() {  // host-side twin of compact_hbm (no DMA reads the pinned tier here)
+  std::vector<std::pair<uint64_t, uint32_t>> res;
+  for (uint32_t i = 0; i < n_items; ++i)
+    if (loc[i].pin_off != FreeList::kNone) res.emplace_back(loc[i].pin_off, i);
+  std::sort(res.begin(), res.end());
+  uint64_t cursor = 0;
+  for (auto& r : res) {
+    const uint32_t i = r.second;
+    if (r.first != cursor) {
+      std::memmove(pin_base + cursor, pin_base + r.first, bytes[i]);
+      loc[i].pin_off = cursor;
+    }
+    cursor += align_up(bytes[i], FreeList::kAlign);
+  }
+  pin.reset_compacted(cursor, pin_cap);
 }
 
 void Store::export_item(uint32_t item, void* dst, size_t cap, size_t* len) const {

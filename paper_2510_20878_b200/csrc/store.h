@@ -28,6 +28,12 @@ class FreeList {
   uint64_t alloc(uint64_t size);  // kNone when no contiguous block fits
   void release(uint64_t off, uint64_t size);
   uint64_t used() const { return used_; }
+  // after compaction: [0, end) in use, [end, cap) one free block
+  void reset_compacted(uint64_t end, uint64_t cap) {
+    free_.clear();
+    if (cap > end) free_[end] = cap - end;
+    used_ = end;
+  }
 
  private:
   std::map<uint64_t, uint64_t> free_;  // offset -> size
@@ -75,6 +81,8 @@ struct Store {
   DescBuf& desc_buffer(size_t n);
   void ensure_ring();
   void launch(const AsmDesc* dev_descs, uint32_t n, uint32_t k, cudaStream_t st);
+  void compact_hbm();
+  void compact_pin();
 
   hr_store_config cfg;
   Layout lay;
@@ -94,6 +102,7 @@ struct Store {
   uint8_t* hbm_base = nullptr;
   uint64_t hbm_cap = 0;
   FreeList hbm;
+  uint64_t compactions = 0;
   uint8_t* pin_base = nullptr;
   uint64_t pin_cap = 0;
   FreeList pin;
