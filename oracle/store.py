@@ -11,7 +11,9 @@ format is DESIGN.md §"Packed item blob", written independently on both sides):
         padded to a multiple of 16 B:
         INT8  fp32 s per group of G elements (G | T*D, groups never cross a slab)
         INT4  (fp32 s, fp32 mn) per group, interleaved
-        GSE8  int8 shared-exponent array [2^e], unused = -128
+        GSE8  int8 shared-exponent array [2^e], unused = -128, padded to 16 B,
+              then the fp32 decode table [2^(e+1)]: entry (sign << e | i) =
+              (-1)^sign * 2^(G_i - (m-1)), 0 for unused i (gse_decode_table)
         FP8 / PASS16: no meta
   blob size = align256(meta offset + L*Hl*record stride)  (FP8/PASS16: align256(codes))
 """
@@ -67,7 +69,7 @@ class Layout:
 
     def meta_record(self, scheme: int) -> int:
         ng = self.slab // self.G
-        raw = {INT8: 4 * ng, INT4: 8 * ng, GSE8: 1 << self.gse_e}.get(scheme, 0)
+        raw = {INT8: 4 * ng, INT4: 8 * ng, GSE8: 16 + 4 * (2 << self.gse_e)}.get(scheme, 0)
         return _a(raw, 16)
 
     def meta_offset(self, scheme: int) -> int:
@@ -75,6 +77,21 @@ class Layout:
 
     def item_bytes(self, scheme: int) -> int:
         return _a(self.meta_offset(scheme) + self.L * self.Hl * self.meta_record(scheme), 256)
+
+
+def gse_decode_table(table, e_bits: int, m_bits: int) -> np.ndarray:
+    """fp32 [2^(e+1)] stored after the shared-exponent array in a GSE-8 meta
+    record: entry (sign << e | i) = (-1)^sign * 2^(G_i - (m-1)), 0 for unused i.
+    A non-zero field f then decodes to f * entry[byte >> m] (the
+    closed form of P:163 pinned by test_gse_decode_closed_form).  Derived data
+    carried in the blob; the oracle's own decoder still walks the marker."""
+    n = 1 << e_bits
+    out = np.zeros(2 * n, dtype=np.float32)
+    for i, g in enumerate(table):
+        v = np.float32(np.ldexp(1.0, int(g) - (m_bits - 1)))
+        out[i] = v
+        out[n + i] = -v
+    return out
 
 
 def encode_slab(bits: np.ndarray, scheme: int, lay: Layout):
@@ -107,6 +124,8 @@ def encode_slab(bits: np.ndarray, scheme: int, lay: Layout):
         table = codecs.gse_slab_table(x, lay.gse_e, lay.gse_m)
         m = codecs.gse_meta(table, lay.gse_e).view(np.uint8)
         meta[: m.size] = m
+        dt = gse_decode_table(table, lay.gse_e, lay.gse_m).astype("<f4").view(np.uint8)
+        meta[16:16 + dt.size] = dt
         return codecs.gse_encode(x, table, lay.gse_e, lay.gse_m), meta
     raise ValueError(scheme)
 

@@ -20,6 +20,7 @@ PKG = os.path.join(ROOT, "paper_2510_20878_b200")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC,-O3,-Wall", f"-I{ROOT}/include"]
+COMMON += os.environ.get("HARAG_NVCC_EXTRA", "").split()  # experiments only (e.g. -DHARAG_ST_CS)
 
 LIBHARAG = os.path.join(PKG, "libharag.so")
 LIBSYNTH = os.path.join(ROOT, "synth", "libharag_synth.so")
@@ -41,7 +42,7 @@ def _run(cmd: list[str]) -> None:
 
 
 def _lib(target: str, sources: list[str], headers: list[str], objdir: str, extra: list[str] | None = None) -> bool:
-    if not _newer(target, sources + headers):
+    if not _newer(target, sources + headers) and not os.environ.get("HARAG_FORCE_BUILD"):
         return False
     os.makedirs(objdir, exist_ok=True)
     extra = extra or []

@@ -19,10 +19,9 @@ struct AsmDesc {
 };
 
 constexpr int kAsmThreads = 288;       // 1 producer warp + 8 consumer warps
-constexpr int kAsmTileE = 8192;       // elements per tile (16 KB of 16-bit output)
-constexpr int kAsmStages = 4;         // shared-memory ring depth
-constexpr int kAsmCodeStage = 2 * kAsmTileE;           // PASS16 worst case
-constexpr int kAsmMetaStage = 2048 + 64;               // INT4 at G=32 worst case + 16-B window slack
+constexpr int kAsmStages = 4;          // shared-memory ring depth
+constexpr int kAsmMaxTileE = 16384;    // elements per tile (8192 when a launch holds PASS16 items)
+constexpr int kAsmCodeStage = 16384;   // bytes of packed codes per stage (16 KB for every scheme mix)
 
 struct AsmParams {
   const AsmDesc* descs;
@@ -32,14 +31,18 @@ struct AsmParams {
   uint32_t gse_m;
   uint32_t dtype;            // hr_dtype of the output
   uint32_t slab;             // T*D
-  uint32_t tiles_per_slab;   // ceil(slab / kAsmTileE)
+  uint32_t tile_e;           // elements per tile (power of two)
+  uint32_t tiles_per_slab;   // ceil(slab / tile_e)
+  uint32_t meta_stage;       // bytes of meta window per stage (multiple of 128)
   uint64_t n_tiles;          // n_desc * L * Hl * tiles_per_slab
   uint32_t meta_stride[6];   // per scheme, bytes per slab record
 };
 
 // Launch the fused gather -> unpack -> dequantise -> scatter (+ hotness count).
+// scheme_mask: bit s set when some descriptor has scheme s (chooses tile and meta window).
+// tile_e, tiles_per_slab, n_tiles and meta_stage are filled in here.
 // grid_ctas <= 0: persistent grid of SMs x resident CTAs.
-void launch_assemble(const AsmParams& p, cudaStream_t stream, int grid_ctas = 0);
+void launch_assemble(AsmParams p, uint32_t scheme_mask, cudaStream_t stream, int grid_ctas = 0);
 int assemble_ctas_per_sm();
 
 struct QuantParams {

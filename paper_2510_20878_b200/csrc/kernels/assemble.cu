@@ -13,7 +13,7 @@
 // then one round-to-nearest-even to the output dtype (R25).
 //
 // Structure (warp-specialised, persistent): CTA = 1 producer warp + 8
-// consumer warps; tiles t = blockIdx.x + i*gridDim.x.  A tile = kAsmTileE
+// consumer warps; CTA b owns a contiguous block of tiles.  A tile = p.tile_e
 // consecutive elements of one (request, slot, kind, layer, head) slab.  The
 // producer lane resolves the tile (descriptor, addresses, hotness count),
 // writes a small header to shared memory and has the TMA engine bulk-copy
@@ -28,6 +28,8 @@
 
 #include "../common.h"
 #include "../kernels.h"
+
+#include <algorithm>
 
 namespace harag {
 namespace {
@@ -77,7 +79,11 @@ __device__ __forceinline__ void bulk_wait_read_all() {
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ void st_v4(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+#ifdef HARAG_ST_CS
+  asm volatile("st.global.cs.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+#else
   asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+#endif
 }
 
 // two fp32 -> output dtype, one RNE each (first argument -> low half)
@@ -108,34 +114,49 @@ struct TileHdr {
   uint32_t goff;     // e0 mod G: group of element e is (goff + e) >> g_shift
 };
 
+// Dynamic shared memory: [codes ring | meta ring | headers | full barriers | empty barriers];
+// every meta stage starts 256-B aligned
 struct Smem {
-  uint8_t codes[kAsmStages][kAsmCodeStage];
-  uint8_t meta[kAsmStages][kAsmMetaStage];
-  TileHdr hdr[kAsmStages];
-  float gse_scale[kConsumerWarps][32];  // per consumer warp: (sign, index) -> +-2^(G_i - (m-1))
-  uint64_t full[kAsmStages];
-  uint64_t empty[kAsmStages];
+  uint8_t* base;
+  uint32_t meta_stage;
+  __device__ __forceinline__ uint8_t* codes(int s) const { return base + s * kAsmCodeStage; }
+  __device__ __forceinline__ uint8_t* meta(int s) const {
+    return base + kAsmStages * kAsmCodeStage + s * meta_stage;
+  }
+  __device__ __forceinline__ TileHdr* hdr() const {
+    return reinterpret_cast<TileHdr*>(base + kAsmStages * (kAsmCodeStage + meta_stage));
+  }
+  __device__ __forceinline__ uint64_t* full() const { return reinterpret_cast<uint64_t*>(hdr() + kAsmStages); }
+  __device__ __forceinline__ uint64_t* empty() const { return full() + kAsmStages; }
 };
 
+size_t smem_bytes(uint32_t meta_stage) {
+  return (size_t)kAsmStages * (kAsmCodeStage + meta_stage) + kAsmStages * sizeof(TileHdr) + 2 * kAsmStages * 8;
+}
+
+// Blocked distribution: CTA b owns tiles [b*n/grid, (b+1)*n/grid) — consecutive tiles of one slab /
+// item, so the producer reloads a descriptor only when it crosses an item.
+__device__ __forceinline__ void my_tiles(const AsmParams& p, uint64_t& t0, uint64_t& t1) {
+  t0 = p.n_tiles * blockIdx.x / gridDim.x;
+  t1 = p.n_tiles * (blockIdx.x + 1) / gridDim.x;
+}
+
 // ------------------------------------------------------------------ producer
-__device__ __forceinline__ void produce(const AsmParams& p, Smem& sm) {
-  const uint64_t per_desc = (uint64_t)p.L * p.Hl * p.tiles_per_slab;
-  uint32_t cur = 0xFFFFFFFFu;
-  AsmDesc d{};
-  uint64_t i = 0;
-  for (uint64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++i) {
+__device__ __forceinline__ void produce(const AsmParams& p, const Smem& sm) {
+  uint64_t t0, t1;
+  my_tiles(p, t0, t1);
+  const uint32_t per_desc = p.L * p.Hl * p.tiles_per_slab;
+  const uint32_t n_slabs = p.L * p.Hl;
+  uint32_t di = (uint32_t)(t0 / per_desc);
+  uint32_t r = (uint32_t)(t0 - (uint64_t)di * per_desc);
+  uint32_t slab_i = r / p.tiles_per_slab;
+  uint32_t sub = r - slab_i * p.tiles_per_slab;
+  AsmDesc d = p.descs[di];
+  for (uint64_t i = 0; i < t1 - t0; ++i) {
     const int stage = (int)(i % kAsmStages);
-    if (i >= kAsmStages) mbar_wait(&sm.empty[stage], (uint32_t)(((i / kAsmStages) - 1) & 1));
-    const uint32_t di = (uint32_t)(t / per_desc);
-    const uint32_t r = (uint32_t)(t - (uint64_t)di * per_desc);
-    const uint32_t slab_i = r / p.tiles_per_slab;
-    const uint32_t sub = r - slab_i * p.tiles_per_slab;
-    if (di != cur) {
-      d = p.descs[di];
-      cur = di;
-    }
-    const uint32_t e0 = sub * (uint32_t)kAsmTileE;
-    const uint32_t n_el = min((uint32_t)kAsmTileE, p.slab - e0);
+    if (i >= kAsmStages) mbar_wait(&sm.empty()[stage], (uint32_t)(((i / kAsmStages) - 1) & 1));
+    const uint32_t e0 = sub * p.tile_e;
+    const uint32_t n_el = min(p.tile_e, p.slab - e0);
     const uint32_t cb = code_bytes(d.scheme, n_el);
     const uint8_t* csrc = d.codes + (uint64_t)slab_i * code_bytes(d.scheme, p.slab) + code_bytes(d.scheme, e0);
     uint32_t mb = 0, moff = 0;
@@ -147,20 +168,28 @@ __device__ __forceinline__ void produce(const AsmParams& p, Smem& sm) {
       msrc = d.meta + (uint64_t)slab_i * p.meta_stride[d.scheme] + b0;
       mb = b1 - b0;
       moff = g0 * me - b0;
-    } else if (d.scheme == HR_S_GSE8) {
+    } else if (d.scheme == HR_S_GSE8) {  // whole record: shared-exponent array + fp32 decode table
       msrc = d.meta + (uint64_t)slab_i * p.meta_stride[d.scheme];
-      mb = 16;
+      mb = p.meta_stride[d.scheme];
     }
-    TileHdr& h = sm.hdr[stage];
+    TileHdr& h = sm.hdr()[stage];
     h.out = d.out + 2ull * (((uint64_t)slab_i * p.k + d.slot) * p.slab + e0);
     h.n_el = n_el;
     h.scheme = d.scheme;
     h.meta_off = moff;
     h.goff = e0 & (p.G - 1);
     if (d.count != nullptr && slab_i == 0 && sub == 0) atomicAdd(d.count, 1ull);  // a1
-    mbar_arrive_expect_tx(&sm.full[stage], cb + mb);  // release: the header is visible with the phase flip
-    bulk_g2s(sm.codes[stage], csrc, cb, &sm.full[stage]);
-    if (mb) bulk_g2s(sm.meta[stage], msrc, mb, &sm.full[stage]);
+    uint64_t* full = &sm.full()[stage];
+    mbar_arrive_expect_tx(full, cb + mb);  // release: the header is visible with the phase flip
+    bulk_g2s(sm.codes(stage), csrc, cb, full);
+    if (mb) bulk_g2s(sm.meta(stage), msrc, mb, full);
+    if (++sub == p.tiles_per_slab) {  // advance (sub, slab, descriptor) without divisions
+      sub = 0;
+      if (++slab_i == n_slabs) {
+        slab_i = 0;
+        if (i + 1 < t1 - t0) d = p.descs[++di];
+      }
+    }
   }
 }
 
@@ -225,21 +254,31 @@ __device__ __forceinline__ void decode_fp8(const TileHdr& h, const uint8_t* code
   }
 }
 
-template <int DT>
-__device__ __forceinline__ void decode_gse(const TileHdr& h, const uint8_t* codes, const float* scale, int ctid,
-                                           uint32_t m) {
-  // byte = s | idx (e bits) | f (m bits); value = f * scale[byte >> m] (the table carries the sign);
-  // "+ 0" turns the -0 of a (s=1, f=0) byte into +0: field 0 decodes to +0
-  const uint32_t fmask = ((1u << m) - 1u) * 0x01010101u;
+__device__ __forceinline__ float lds_f32(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
+
+template <int DT, int M>
+__device__ __forceinline__ void decode_gse(const TileHdr& h, const uint8_t* codes, uint32_t record, int ctid) {
+  // byte = s | idx (7-M bits) | f (M bits); value = f * T[byte >> M] with T[(s << e) | idx] =
+  // (-1)^s 2^(G_idx - (M-1)), the fp32 table at record + 16 (record: 256-B-aligned shared address).
+  // fma(f, T, +0) is that exact product, except that the -0 of a (s=1, f=0) byte becomes +0: field 0
+  // decodes to +0.  The table address of byte i is built by one PRMT: low byte = 16 + 4*(byte >> M),
+  // upper bytes from `record`.
+  constexpr uint32_t fmask = ((1u << M) - 1u) * 0x01010101u;
+  constexpr uint32_t omask = ((0xFFu >> M) << 2) * 0x01010101u;
 #pragma unroll 2
   for (uint32_t e = ctid * 8; e < h.n_el; e += kChunkStride) {
     const uint2 c = *reinterpret_cast<const uint2*>(codes + e);
-    const uint32_t fx = c.x & fmask, fy = c.y & fmask;
+    const uint32_t fx = c.x & fmask, fy = c.y & fmask;  // f < 2^M < 128: exact through I2F.S8
+    const uint32_t ox = ((c.x >> (M - 2)) & omask) + 0x10101010u, oy = ((c.y >> (M - 2)) & omask) + 0x10101010u;
     float f[8];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      f[i] = __fadd_rn(__fmul_rn(u8f(fx, i), scale[(c.x >> (8 * i + m)) & (0xFFu >> m)]), 0.f);
-      f[4 + i] = __fadd_rn(__fmul_rn(u8f(fy, i), scale[(c.y >> (8 * i + m)) & (0xFFu >> m)]), 0.f);
+      f[i] = __fmaf_rn(s8f(fx, i), lds_f32(__byte_perm(ox, record, 0x7650u | i)), 0.f);
+      f[4 + i] = __fmaf_rn(s8f(fy, i), lds_f32(__byte_perm(oy, record, 0x7650u | i)), 0.f);
     }
     st_v4(h.out + 2ull * e, pack2<DT>(f[0], f[1]), pack2<DT>(f[2], f[3]), pack2<DT>(f[4], f[5]),
           pack2<DT>(f[6], f[7]));
@@ -247,15 +286,16 @@ __device__ __forceinline__ void decode_gse(const TileHdr& h, const uint8_t* code
 }
 
 template <int DT>
-__device__ __forceinline__ void consume(const AsmParams& p, Smem& sm, int warp, int lane) {
+__device__ __forceinline__ void consume(const AsmParams& p, const Smem& sm, int warp, int lane) {
   const int ctid = warp * 32 + lane;
-  float* gscale = sm.gse_scale[warp];
-  uint64_t i = 0;
-  for (uint64_t t = blockIdx.x; t < p.n_tiles; t += gridDim.x, ++i) {
+  uint64_t t0, t1;
+  my_tiles(p, t0, t1);
+  for (uint64_t i = 0; i < t1 - t0; ++i) {
     const int stage = (int)(i % kAsmStages);
-    mbar_wait(&sm.full[stage], (uint32_t)((i / kAsmStages) & 1));
-    const TileHdr h = sm.hdr[stage];
-    const uint8_t* codes = sm.codes[stage];
+    mbar_wait(&sm.full()[stage], (uint32_t)((i / kAsmStages) & 1));
+    const TileHdr h = sm.hdr()[stage];
+    const uint8_t* codes = sm.codes(stage);
+    const uint8_t* meta = sm.meta(stage);
     switch (h.scheme) {
       case HR_S_PASS16:
         if (warp == 0 && lane == 0) {
@@ -264,10 +304,10 @@ __device__ __forceinline__ void consume(const AsmParams& p, Smem& sm, int warp, 
         }
         break;
       case HR_S_INT8:
-        decode_int8<DT>(h, codes, sm.meta[stage], ctid, p.g_shift);
+        decode_int8<DT>(h, codes, meta, ctid, p.g_shift);
         break;
       case HR_S_INT4:
-        decode_int4<DT>(h, codes, sm.meta[stage], ctid, p.g_shift);
+        decode_int4<DT>(h, codes, meta, ctid, p.g_shift);
         break;
       case HR_S_FP8E4M3:
         decode_fp8<DT, HR_S_FP8E4M3>(h, codes, ctid);
@@ -275,37 +315,33 @@ __device__ __forceinline__ void consume(const AsmParams& p, Smem& sm, int warp, 
       case HR_S_FP8E5M2:
         decode_fp8<DT, HR_S_FP8E5M2>(h, codes, ctid);
         break;
-      case HR_S_GSE8: {
-        // per-warp table, entry j = (sign = j >> e, idx = j & (2^e - 1)) -> (-1)^sign 2^(G_idx - (m-1)), exact
-        const int e_bits = 7 - (int)p.gse_m;
-        if (lane < (2 << e_bits)) {
-          const int k = (int)(int8_t)sm.meta[stage][lane & ((1 << e_bits) - 1)] - ((int)p.gse_m - 1);
-          const float v =
-              k >= -126 ? __int_as_float((k + 127) << 23) : (k >= -149 ? __int_as_float(1 << (k + 149)) : 0.f);
-          gscale[lane] = (lane >> e_bits) ? -v : v;
-        }
-        __syncwarp();
-        decode_gse<DT>(h, codes, gscale, ctid, p.gse_m);
+      case HR_S_GSE8:
+        if (p.gse_m == 3)
+          decode_gse<DT, 3>(h, codes, smem_addr(meta), ctid);
+        else if (p.gse_m == 4)
+          decode_gse<DT, 4>(h, codes, smem_addr(meta), ctid);
+        else
+          decode_gse<DT, 5>(h, codes, smem_addr(meta), ctid);
         break;
-      }
       default:
         break;
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty[stage]);
+    if (lane == 0) mbar_arrive(&sm.empty()[stage]);
   }
   if (warp == 0 && lane == 0) bulk_wait_all();
 }
 
 template <int DT>
 __global__ void __launch_bounds__(kAsmThreads) assemble_kv_kernel(const __grid_constant__ AsmParams p) {
-  extern __shared__ __align__(128) uint8_t smem_raw[];
-  Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const Smem sm{smem_raw, p.meta_stage};
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   if (threadIdx.x == 0) {
+    if (smem_addr(smem_raw) & 255u) __trap();  // GSE-8 table addressing needs 256-B-aligned meta stages
     for (int s = 0; s < kAsmStages; ++s) {
-      mbar_init(&sm.full[s], 1);
-      mbar_init(&sm.empty[s], kConsumerWarps);
+      mbar_init(&sm.full()[s], 1);
+      mbar_init(&sm.empty()[s], kConsumerWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -317,36 +353,59 @@ __global__ void __launch_bounds__(kAsmThreads) assemble_kv_kernel(const __grid_c
   }
 }
 
-int g_ctas_per_sm = 0;
 int g_num_sms = 0;
+constexpr uint32_t kMaxMetaStage = 8192;
+
+int ctas_per_sm(size_t smem) {
+  static int cache_bytes[8] = {0}, cache_val[8] = {0};
+  for (int i = 0; i < 8; ++i)
+    if (cache_bytes[i] == (int)smem) return cache_val[i];
+  int n = 0;
+  HR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, assemble_kv_kernel<HR_BF16>, kAsmThreads, smem));
+  for (int i = 0; i < 8; ++i)
+    if (cache_bytes[i] == 0) {
+      cache_bytes[i] = (int)smem, cache_val[i] = n;
+      break;
+    }
+  return n < 1 ? 1 : n;
+}
 
 }  // namespace
 
 int assemble_ctas_per_sm() {
-  if (!g_ctas_per_sm) {
-    HR_CUDA(cudaFuncSetAttribute(assemble_kv_kernel<HR_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(Smem)));
-    HR_CUDA(cudaFuncSetAttribute(assemble_kv_kernel<HR_FP16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(Smem)));
-    HR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&g_ctas_per_sm, assemble_kv_kernel<HR_BF16>, kAsmThreads,
-                                                          sizeof(Smem)));
+  if (!g_num_sms) {
+    const int mx = (int)smem_bytes(kMaxMetaStage);
+    HR_CUDA(cudaFuncSetAttribute(assemble_kv_kernel<HR_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
+    HR_CUDA(cudaFuncSetAttribute(assemble_kv_kernel<HR_FP16>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx));
     int dev = 0;
     HR_CUDA(cudaGetDevice(&dev));
     HR_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
-    if (g_ctas_per_sm < 1) g_ctas_per_sm = 1;
   }
-  return g_ctas_per_sm;
+  return ctas_per_sm(smem_bytes(256));
 }
 
-void launch_assemble(const AsmParams& p, cudaStream_t st, int grid_ctas) {
+void launch_assemble(AsmParams p, uint32_t scheme_mask, cudaStream_t st, int grid_ctas) {
+  assemble_ctas_per_sm();
+  // tile: 16 KB of codes per stage for every mix (8-bit: 16384 elements; PASS16 forces 8192)
+  p.tile_e = (scheme_mask & (1u << HR_S_PASS16)) ? 8192u : (uint32_t)kAsmMaxTileE;
+  p.tiles_per_slab = (p.slab + p.tile_e - 1) / p.tile_e;
+  p.n_tiles = (uint64_t)p.n_desc * p.L * p.Hl * p.tiles_per_slab;
   if (p.n_tiles == 0) return;
-  const int per_sm = assemble_ctas_per_sm();
-  uint64_t grid = grid_ctas > 0 ? (uint64_t)grid_ctas : (uint64_t)g_num_sms * per_sm;
+  // meta window per stage: the tile's groups (+16-B alignment slack) or the GSE-8 record
+  uint32_t meta = 0;
+  const uint32_t groups = p.tile_e >= p.G ? p.tile_e / p.G : 1;
+  if (scheme_mask & (1u << HR_S_INT8)) meta = std::max(meta, 4 * groups + 32);
+  if (scheme_mask & (1u << HR_S_INT4)) meta = std::max(meta, 8 * groups + 32);
+  if (scheme_mask & (1u << HR_S_GSE8)) meta = std::max(meta, p.meta_stride[HR_S_GSE8]);
+  p.meta_stage = (meta + 255) / 256 * 256;  // 256-B-aligned records (GSE-8 table addressing)
+  require(p.meta_stage <= kMaxMetaStage, HR_EINVAL, "group too small for the assemble tile");
+  const size_t smem = smem_bytes(p.meta_stage);
+  uint64_t grid = grid_ctas > 0 ? (uint64_t)grid_ctas : (uint64_t)g_num_sms * ctas_per_sm(smem);
   if (grid > p.n_tiles) grid = p.n_tiles;
   if (p.dtype == HR_BF16)
-    assemble_kv_kernel<HR_BF16><<<(unsigned)grid, kAsmThreads, sizeof(Smem), st>>>(p);
+    assemble_kv_kernel<HR_BF16><<<(unsigned)grid, kAsmThreads, smem, st>>>(p);
   else
-    assemble_kv_kernel<HR_FP16><<<(unsigned)grid, kAsmThreads, sizeof(Smem), st>>>(p);
+    assemble_kv_kernel<HR_FP16><<<(unsigned)grid, kAsmThreads, smem, st>>>(p);
   HR_CUDA(cudaGetLastError());
 }
 

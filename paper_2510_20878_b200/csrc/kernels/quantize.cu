@@ -220,10 +220,22 @@ __global__ void __launch_bounds__(kQThreads) quantize_slab_kernel(QuantParams p)
     // P:172 / R6: lo = max(Emin, Emax - (2^e - 1) * step); G_i = min(lo + i*step, Emax)
     const int lo = max(Emin, Emax - (nmax - 1) * step);
     const int n = any ? (Emax - lo + step - 1) / step + 1 : 0;
-    for (uint32_t w = tid; w < p.meta_stride; w += kQThreads) {
+    // meta record: int8 array [2^e] (unused -128), zero pad to 16 B, then the fp32 decode table
+    // [2^(e+1)]: entry (sign << e | i) = (-1)^sign 2^(G_i - (m-1)) (0 for unused i)
+    for (uint32_t w = tid; w < 16; w += kQThreads) {
       int v = 0;
       if ((int)w < nmax) v = ((int)w < n) ? min(lo + (int)w * step, Emax) : -128;
       meta[w] = (uint8_t)(int8_t)v;
+    }
+    for (uint32_t w = tid; w < (p.meta_stride - 16) / 4; w += kQThreads) {
+      float v = 0.f;
+      const int i = (int)w & (nmax - 1);
+      if ((int)w < 2 * nmax && i < n) {
+        const int k = min(lo + i * step, Emax) - (step);  // G_i - (m-1)
+        v = k >= -126 ? __int_as_float((k + 127) << 23) : (k >= -149 ? __int_as_float(1 << (k + 149)) : 0.f);
+        if ((int)w >= nmax) v = -v;
+      }
+      reinterpret_cast<float*>(meta + 16)[w] = v;
     }
     const int m = (int)p.gse_m;
     for (uint32_t v = tid; v < n_vec; v += kQThreads) {

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <unordered_set>
@@ -61,6 +62,7 @@ Store::Store(const hr_store_config& c) : cfg(c), lay(make_layout(c)) {
   require(sum <= 1.0 + 1e-12, HR_EINVAL, "taus sum above 1");
   require(cfg.demand_mode == 0, HR_EINVAL, "demand_mode store not available: use hr_alg2_* for the Alg. 2 state machine");
   slots = cfg.staging_slots ? cfg.staging_slots : 3;
+  if (const char* g = std::getenv("HARAG_ASM_GRID")) grid_override = std::atoi(g);  // tuning experiments
   HR_CUDA(cudaSetDevice(cfg.device));
   HR_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
 }
@@ -291,7 +293,7 @@ void Store::ensure_ring() {
   }
 }
 
-void Store::launch(const AsmDesc* dev_descs, uint32_t n, uint32_t k, cudaStream_t st) {
+void Store::launch(const AsmDesc* dev_descs, uint32_t n, uint32_t k, uint32_t scheme_mask, cudaStream_t st) {
   AsmParams p{};
   p.descs = dev_descs;
   p.n_desc = n;
@@ -300,8 +302,6 @@ void Store::launch(const AsmDesc* dev_descs, uint32_t n, uint32_t k, cudaStream_
   p.gse_m = lay.gse_m;
   p.dtype = lay.dtype;
   p.slab = (uint32_t)lay.slab();
-  p.tiles_per_slab = (uint32_t)((lay.slab() + kAsmTileE - 1) / kAsmTileE);
-  p.n_tiles = (uint64_t)n * lay.L * lay.Hl * p.tiles_per_slab;
   for (uint32_t s = 0; s <= HR_S_INT4; ++s) p.meta_stride[s] = (uint32_t)lay.meta_stride(s);
   cudaEvent_t a = nullptr, b = nullptr;
   if (timing) {
@@ -309,7 +309,7 @@ void Store::launch(const AsmDesc* dev_descs, uint32_t n, uint32_t k, cudaStream_
     HR_CUDA(cudaEventCreate(&b));
     HR_CUDA(cudaEventRecord(a, st));
   }
-  launch_assemble(p, st, grid_override);
+  launch_assemble(p, scheme_mask, st, grid_override);
   if (timing) {
     HR_CUDA(cudaEventRecord(b, st));
     timers.emplace_back(a, b);
@@ -343,6 +343,7 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
   std::vector<uint32_t> miss_items;
   std::unordered_map<uint32_t, std::vector<AsmDesc>> miss_descs;
   size_t nh = 0;
+  uint32_t hbm_mask = 0;
   for (uint32_t r = 0; r < n_req; ++r) {
     const bool counted = ((req_counter + r) % (uint64_t)cfg.world) == (uint64_t)cfg.rank;
     for (uint32_t j = 0; j < k; ++j) {
@@ -360,6 +361,7 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
           d.codes = hbm_ptr(item);
           d.meta = d.codes + lay.meta_offset(d.scheme);
           db.host[nh++] = d;
+          hbm_mask |= 1u << d.scheme;
           stats.hits[HR_T_HBM]++;
         } else {
           auto it = miss_descs.find(item);
@@ -390,7 +392,7 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
   }
   HR_CUDA(cudaMemcpyAsync(db.dev, db.host, pos * sizeof(AsmDesc), cudaMemcpyHostToDevice, st));
   // launch A: every HBM-resident (request, slot, kind)
-  if (nh) launch(db.dev, (uint32_t)nh, k, st);
+  if (nh) launch(db.dev, (uint32_t)nh, k, hbm_mask, st);
   // host-tier items: pinned (or pageable -> pinned bounce) -> staging ring -> launch B
   for (size_t i = 0; i < miss_items.size(); ++i) {
     const uint32_t item = miss_items[i];
@@ -414,7 +416,7 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
     sl.used = true;
     stats.bytes_h2d += bytes[item];
     HR_CUDA(cudaStreamWaitEvent(st, sl.copied, 0));
-    launch(db.dev + miss_range[i].first, (uint32_t)miss_range[i].second, k, st);
+    launch(db.dev + miss_range[i].first, (uint32_t)miss_range[i].second, k, 1u << scheme[item], st);
     HR_CUDA(cudaEventRecord(sl.free_ev, st));
   }
   HR_CUDA(cudaEventRecord(db.done, st));

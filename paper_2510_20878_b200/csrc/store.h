@@ -80,7 +80,7 @@ struct Store {
   uint64_t bytes_read_alg(uint32_t item) const;
   DescBuf& desc_buffer(size_t n);
   void ensure_ring();
-  void launch(const AsmDesc* dev_descs, uint32_t n, uint32_t k, cudaStream_t st);
+  void launch(const AsmDesc* dev_descs, uint32_t n, uint32_t k, uint32_t scheme_mask, cudaStream_t st);
   void compact_hbm();
   void compact_pin();
 

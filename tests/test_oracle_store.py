@@ -16,7 +16,7 @@ def test_blob_sizes_closed_form():
     n = 32 * 8 * 512 * 128
     assert lay.item_bytes(INT8) == n + 32 * 8 * 512 * 4
     assert lay.item_bytes(FP8E4M3) == n
-    assert lay.item_bytes(GSE8) == n + 32 * 8 * 16
+    assert lay.item_bytes(GSE8) == n + 32 * 8 * (16 + 4 * 32)
     assert lay.item_bytes(INT4) == n // 2 + 32 * 8 * 512 * 8
     assert lay.item_bytes(PASS16) == 2 * n
 
@@ -115,3 +115,20 @@ def test_decode_error_bounds_per_scheme():
             t = codecs.gse_slab_table(xf.astype(np.float32), 4, 3)
             bound = np.where(ax >= 2.0 ** (t[0] - 2), 0.5 * ax, ax)
         assert np.all(err <= bound), s
+
+
+@pytest.mark.parametrize("e_bits,m_bits", [(4, 3), (3, 4), (2, 5)])
+def test_gse_decode_table_matches_marker_decoder(e_bits, m_bits):
+    """The fp32 decode table carried in GSE-8 meta records reproduces the
+    oracle's marker-walk decoder for every byte: field 0 -> +0, else
+    f * table[byte >> m]."""
+    from oracle import codecs
+    t = codecs.gse_table(-20, 7, e_bits, m_bits)
+    dt = ost_table = store.gse_decode_table(t, e_bits, m_bits)
+    codes = np.arange(256, dtype=np.uint16).astype(np.uint8)
+    f = codes & ((1 << m_bits) - 1)
+    idx = (codes >> m_bits) & ((1 << e_bits) - 1)
+    ok = (idx < len(t)) | (f == 0)
+    want = codecs.gse_decode(codes[ok], t, e_bits, m_bits)
+    got = np.where(f[ok] == 0, 0.0, f[ok].astype(np.float64) * dt[codes[ok] >> m_bits].astype(np.float64))
+    assert np.array_equal(got, want) and not np.signbit(got[f[ok] == 0]).any()
