@@ -19,9 +19,15 @@ struct AsmDesc {
 };
 
 constexpr int kAsmThreads = 288;       // 1 producer warp + 8 consumer warps
-constexpr int kAsmStages = 4;          // shared-memory ring depth
-constexpr int kAsmMaxTileE = 16384;    // elements per tile (8192 when a launch holds PASS16 items)
-constexpr int kAsmCodeStage = 16384;   // bytes of packed codes per stage (16 KB for every scheme mix)
+#ifndef HARAG_STAGES
+#define HARAG_STAGES 4
+#endif
+#ifndef HARAG_CODE_STAGE
+#define HARAG_CODE_STAGE 16384
+#endif
+constexpr int kAsmStages = HARAG_STAGES;         // shared-memory ring depth
+constexpr int kAsmCodeStage = HARAG_CODE_STAGE;  // bytes of packed codes per stage (every scheme mix)
+constexpr int kAsmMaxTileE = kAsmCodeStage;      // elements per tile (half when a launch holds PASS16 items)
 
 struct AsmParams {
   const AsmDesc* descs;

@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(kAsmThreads) assemble_kv_kernel(const __grid_c
 }
 
 int g_num_sms = 0;
-constexpr uint32_t kMaxMetaStage = 8192;
+constexpr uint32_t kMaxMetaStage = 2 * kAsmCodeStage / 32 * 8 / 2 + 256;  // INT4 at G = 32
 
 int ctas_per_sm(size_t smem) {
   static int cache_bytes[8] = {0}, cache_val[8] = {0};
@@ -387,7 +387,7 @@ int assemble_ctas_per_sm() {
 void launch_assemble(AsmParams p, uint32_t scheme_mask, cudaStream_t st, int grid_ctas) {
   assemble_ctas_per_sm();
   // tile: 16 KB of codes per stage for every mix (8-bit: 16384 elements; PASS16 forces 8192)
-  p.tile_e = (scheme_mask & (1u << HR_S_PASS16)) ? 8192u : (uint32_t)kAsmMaxTileE;
+  p.tile_e = (scheme_mask & (1u << HR_S_PASS16)) ? (uint32_t)kAsmMaxTileE / 2 : (uint32_t)kAsmMaxTileE;
   p.tiles_per_slab = (p.slab + p.tile_e - 1) / p.tile_e;
   p.n_tiles = (uint64_t)p.n_desc * p.L * p.Hl * p.tiles_per_slab;
   if (p.n_tiles == 0) return;
