@@ -102,6 +102,9 @@ typedef struct {
   uint64_t timed_launches;    /* launches included in kernel_ms */
   uint64_t hbm_used;          /* bytes of HBM arena in use */
   uint64_t pin_used;          /* bytes of pinned tier in use */
+  double   h2d_ms;            /* sum over assemble calls of the host->device copy window (first copy start ->
+                                 last copy end, CUDA events on the copy stream) when timing is on */
+  uint64_t h2d_items;         /* host-tier items streamed */
 } hr_stats;
 
 typedef struct hr_store hr_store;

@@ -82,6 +82,8 @@ Store::~Store() {
     if (r.free_ev) cudaEventDestroy(r.free_ev);
   }
   for (auto& t : timers) cudaEventDestroy(t.first), cudaEventDestroy(t.second);
+  for (auto& t : h2d_timers) cudaEventDestroy(t.first), cudaEventDestroy(t.second);
+  copy_pool.reset();
   if (hbm_base) cudaFree(hbm_base);
   if (pin_base) cudaFreeHost(pin_base);
   if (backing_base) {
@@ -394,6 +396,11 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
   // launch A: every HBM-resident (request, slot, kind)
   if (nh) launch(db.dev, (uint32_t)nh, k, hbm_mask, st);
   // host-tier items: pinned (or pageable -> pinned bounce) -> staging ring -> launch B
+  cudaEvent_t c0 = nullptr, c1 = nullptr;
+  if (timing && !miss_items.empty()) {
+    HR_CUDA(cudaEventCreate(&c0));
+    HR_CUDA(cudaEventCreate(&c1));
+  }
   for (size_t i = 0; i < miss_items.size(); ++i) {
     const uint32_t item = miss_items[i];
     Slot& sl = ring[i % slots];
@@ -406,13 +413,24 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
       if (!backing_is_pinned) {  // pageable data is first copied to pinned memory
         if (!sl.bounce) HR_CUDA(cudaHostAlloc((void**)&sl.bounce, max_item, cudaHostAllocPortable));
         if (sl.used) HR_CUDA(cudaEventSynchronize(sl.copied));  // previous DMA out of this bounce buffer done
-        std::memcpy(sl.bounce, src, bytes[item]);
+        if (!copy_pool) {
+          unsigned n = std::thread::hardware_concurrency() / 2;
+          if (const char* e = std::getenv("HARAG_COPY_THREADS")) n = (unsigned)std::atoi(e);
+          copy_pool.reset(new CopyPool(std::max(0u, std::min(n, 15u))));
+        }
+        copy_pool->copy(sl.bounce, src, bytes[item]);
         src = sl.bounce;
       }
     }
     HR_CUDA(cudaStreamWaitEvent(copy_stream, sl.free_ev, 0));
+    if (c0 && i == 0) HR_CUDA(cudaEventRecord(c0, copy_stream));
     HR_CUDA(cudaMemcpyAsync(sl.dev, src, bytes[item], cudaMemcpyHostToDevice, copy_stream));
     HR_CUDA(cudaEventRecord(sl.copied, copy_stream));
+    if (c1 && i + 1 == miss_items.size()) {
+      HR_CUDA(cudaEventRecord(c1, copy_stream));
+      h2d_timers.emplace_back(c0, c1);
+    }
+    stats.h2d_items++;
     sl.used = true;
     stats.bytes_h2d += bytes[item];
     HR_CUDA(cudaStreamWaitEvent(st, sl.copied, 0));
@@ -572,6 +590,15 @@ void Store::get_stats(hr_stats* out) {
     }
     timers.clear();
   }
+  for (auto& t : h2d_timers) {
+    HR_CUDA(cudaEventSynchronize(t.second));
+    float ms = 0;
+    HR_CUDA(cudaEventElapsedTime(&ms, t.first, t.second));
+    stats.h2d_ms += ms;
+    cudaEventDestroy(t.first);
+    cudaEventDestroy(t.second);
+  }
+  h2d_timers.clear();
   stats.hbm_used = hbm.used();
   stats.pin_used = pin.used();
   *out = stats;

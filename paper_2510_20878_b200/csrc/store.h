@@ -12,6 +12,9 @@
 #include "common.h"
 #include "kernels.h"
 #include "layout.h"
+#include "pool.h"
+
+#include <memory>
 
 namespace harag {
 
@@ -124,6 +127,8 @@ struct Store {
   bool timing = false;
   int grid_override = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timers;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> h2d_timers;  // copy-stream window per assemble call
+  std::unique_ptr<CopyPool> copy_pool;                           // pageable -> pinned bounce workers
   hr_stats stats{};
 };
 
