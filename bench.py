@@ -207,9 +207,16 @@ class Ctx:
         self.local = env_int("LOCAL_RANK", 0)
         if args.gpus != self.world:
             raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={self.world}: launch N>1 with torchrun")
-        torch.cuda.set_device(self.local)
+        # test hooks: HARAG_SINGLE_DEVICE=1 puts every rank on cuda:0 and HARAG_DIST_BACKEND=gloo
+        # replaces NCCL, so the N > 1 path can be exercised on a one-GPU box
+        self.device = 0 if os.environ.get("HARAG_SINGLE_DEVICE") else self.local
+        torch.cuda.set_device(self.device)
         if self.world > 1:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local))
+            backend = os.environ.get("HARAG_DIST_BACKEND", "nccl")
+            if backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.device))
+            else:
+                dist.init_process_group(backend)
         self.stream = torch.cuda.current_stream()
 
     def barrier(self):
@@ -235,7 +242,7 @@ def build_store(ctx, wl, **over):
     schemes = hr.policy_assign(h, wl["ladder"], wl["taus"])
     geo = dict(L=L, H=H, D=D, T=T, dtype=wl["dtype"], rank=ctx.rank, world=ctx.world)
     total = sum(hr.item_bytes(int(sc), **geo) for sc in schemes)
-    cfg = dict(geo, ladder=wl["ladder"], taus=wl["taus"], device=ctx.local, decay_shift=1,
+    cfg = dict(geo, ladder=wl["ladder"], taus=wl["taus"], device=ctx.device, decay_shift=1,
                keep_backing=False, hbm_budget=total + (1 << 20))
     cfg.update(over)
     st = hr.Store(**cfg)
@@ -268,7 +275,7 @@ def timed_steps(ctx, st, pool, ko, vo, steps, warmup, epoch_every, sample_clocks
     ctx.barrier()
     st.reset_stats()
     st.set_timing(True)
-    sampler = clocks_sampler(ctx.local) if sample_clocks else (None, None)
+    sampler = clocks_sampler(ctx.device) if sample_clocks else (None, None)
     if sample_clocks:
         time.sleep(0.1)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -446,7 +453,8 @@ def run_tiered(ctx, wl, ko, vo, kvb, args):
     B, k = wl["batch"], wl["k"]
     per_rank, agg = link_peak(ctx)
     st, h, schemes, build_s, total = build_store(
-        ctx, wl, hbm_budget=wl["hbm_budget"], backing_pinned=True, keep_backing=True, alias_R=wl["alias_R"])
+        ctx, wl, hbm_budget=wl["hbm_budget"], backing_pinned=True, keep_backing=True, alias_R=wl["alias_R"],
+        decay_shift=wl.get("decay_shift", 0))
     pool = synth.gen_requests(wl["n_docs"], 8 * B, k, wl["s"], seed=1).reshape(8, B, k)
     steps = max(3, min(args.steps, wl.get("steps", 20)))
     ms_max, tot_bytes, stats, _ = timed_steps(ctx, st, pool, ko, vo, steps, 3, args.epoch_every, sample_clocks=False)
@@ -468,6 +476,7 @@ def run_tiered(ctx, wl, ko, vo, kvb, args):
                                    "frac": round(t_star / step_s, 4),
                                    "formula": "max(HBM alg bytes / hbm_gbs, H2D bytes / link peak) / step time"},
            "hbm_budget_bytes": wl["hbm_budget"], "alias_R": wl["alias_R"], "build_seconds": round(build_s, 2),
+           "decay_shift": wl.get("decay_shift", 0),
            "migrations": [stats["migrations_in"], stats["migrations_out"]]}
     st.close()
     return res

@@ -80,7 +80,9 @@ typedef struct {
   uint64_t pin_budget;     /* bytes of pinned host tier per rank (PIN_LIST capacity) */
   int32_t  backing_pinned; /* 1: host backing is pinned (every non-HBM item is served as PIN); 0: pageable */
   int32_t  keep_backing;   /* 1: every item keeps a host backing copy (needed by hr_replace); 0: HBM items live only in HBM */
-  int32_t  demand_mode;    /* 0: eager placement (lists resident); 1: reserved (paper-literal Alg. 2 fill, see hr_alg2_*) */
+  int32_t  demand_mode;    /* 0: eager placement (GPU_LIST / PIN_LIST resident after build and after each hr_replace);
+                              1: paper-literal Alg. 2 step 2: queues start empty, every access takes one
+                              branch, promotes inclusively with LRU (R16); forces keep_backing = 1 */
   uint32_t decay_shift;    /* epoch: h <- (h >> decay_shift) + delta (R20) */
   uint32_t bench_alias_R;  /* 0 = off; >0: docs d and d' with d % R == d' % R and equal scheme share one host backing blob (bench only) */
   int32_t  device;         /* CUDA device ordinal */
@@ -176,6 +178,8 @@ hr_status hr_hotness_delta(hr_store* s, int64_t** dev_ptr, uint32_t* n);
 hr_status hr_replace(hr_store* s, void* stream);
 
 /* ------------------------------------------------------------- inspection */
+/* tier: eager mode -> where the item is served from (HBM arena, pinned tier, backing);
+ * demand mode -> the Alg. 2 queue holding it (queueGPU -> HBM, queuePIN -> PIN, none -> PAGE/backing). */
 hr_status hr_item_info(const hr_store* s, uint32_t item, uint32_t* scheme, uint32_t* tier, uint64_t* bytes);
 hr_status hr_item_rank(const hr_store* s, uint32_t item, uint32_t* rank);   /* position in the hotness order */
 hr_status hr_export_item(const hr_store* s, uint32_t item, void* host_dst, size_t cap, size_t* len); /* packed blob; synchronous */

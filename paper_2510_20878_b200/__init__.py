@@ -53,7 +53,7 @@ def _p(a, ct):
 def make_config(*, L, H, D, T, dtype="bf16", group=0, gse=(4, 3),
                 ladder=("INT8", "FP8E4M3", "FP8E5M2", "GSE8"), taus=(0.1, 0.1, 0.1),
                 hbm_budget=0, pin_budget=0, backing_pinned=False, keep_backing=True, decay_shift=1,
-                alias_R=0, device=0, rank=0, world=1, staging_slots=3) -> _lib.Config:
+                alias_R=0, device=0, rank=0, world=1, staging_slots=3, demand_mode=False) -> _lib.Config:
     c = _lib.default_config()
     c.L, c.H, c.D, c.T = L, H, D, T
     c.dtype = HR_FP16 if dtype == "fp16" else HR_BF16
@@ -68,6 +68,7 @@ def make_config(*, L, H, D, T, dtype="bf16", group=0, gse=(4, 3),
     c.backing_pinned, c.keep_backing = int(backing_pinned), int(keep_backing)
     c.decay_shift, c.bench_alias_R = decay_shift, alias_R
     c.device, c.rank, c.world, c.staging_slots = device, rank, world, staging_slots
+    c.demand_mode = int(bool(demand_mode))
     return c
 
 

@@ -137,7 +137,7 @@ hr_status hr_item_info(const hr_store* s, uint32_t item, uint32_t* scheme, uint3
     harag::require(st.state != harag::Store::State::Empty, HR_ESTATE, "store not built");
     harag::require(item < st.n_items, HR_ENOTFOUND, "item id out of range");
     if (scheme) *scheme = st.scheme[item];
-    if (tier) *tier = st.loc[item].hbm_off != harag::FreeList::kNone ? HR_T_HBM : st.tier[item];
+    if (tier) *tier = st.logical_tier(item);
     if (bytes) *bytes = st.bytes[item];
   });
 }

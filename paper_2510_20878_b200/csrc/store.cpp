@@ -60,7 +60,8 @@ Store::Store(const hr_store_config& c) : cfg(c), lay(make_layout(c)) {
     sum += cfg.tau[j];
   }
   require(sum <= 1.0 + 1e-12, HR_EINVAL, "taus sum above 1");
-  require(cfg.demand_mode == 0, HR_EINVAL, "demand_mode store not available: use hr_alg2_* for the Alg. 2 state machine");
+  require(cfg.demand_mode == 0 || cfg.demand_mode == 1, HR_EINVAL, "demand_mode must be 0 or 1");
+  if (cfg.demand_mode) cfg.keep_backing = 1;  // the backing plays the paper's disk: every item has a copy
   slots = cfg.staging_slots ? cfg.staging_slots : 3;
   if (const char* g = std::getenv("HARAG_ASM_GRID")) grid_override = std::atoi(g);  // tuning experiments
   HR_CUDA(cudaSetDevice(cfg.device));
@@ -97,7 +98,13 @@ Store::~Store() {
   if (scratch) cudaFree(scratch);
   if (src_k) cudaFree(src_k);
   if (src_v) cudaFree(src_v);
+  if (start_ev) cudaEventDestroy(start_ev);
   if (copy_stream) cudaStreamDestroy(copy_stream);
+}
+
+uint32_t Store::logical_tier(uint32_t item) const {
+  if (alg2) return alg2->contains(Alg2::GPU, item) ? HR_T_HBM : alg2->contains(Alg2::PIN, item) ? HR_T_PIN : HR_T_PAGE;
+  return loc[item].hbm_off != FreeList::kNone ? HR_T_HBM : tier[item];
 }
 
 uint8_t* Store::hbm_ptr(uint32_t item) const { return hbm_base + loc[item].hbm_off; }
@@ -117,9 +124,15 @@ void Store::build_begin(uint32_t nd, const uint64_t* hot) {
   // Alg. 2 step 1 by bytes (R15)
   order = rank_items(h.data(), n_items);
   tier = lists_by_bytes(order, bytes.data(), cfg.hbm_budget, cfg.backing_pinned ? 0 : cfg.pin_budget);
-  if (cfg.backing_pinned)
+  if (cfg.demand_mode) {
+    // Alg. 2 step 1 gives the lists; the queues start empty and fill on access (step 2)
+    alg2.reset(new Alg2(n_items, tier.data(), bytes.data(), cfg.hbm_budget, cfg.backing_pinned ? 0 : cfg.pin_budget,
+                        0));
+    tier.assign(n_items, HR_T_PAGE);
+  } else if (cfg.backing_pinned) {
     for (auto& t : tier)
       if (t == HR_T_PAGE) t = HR_T_PIN;
+  }
   loc.assign(n_items, Loc{});
   max_item = 0;
   for (uint32_t i = 0; i < n_items; ++i) max_item = std::max(max_item, bytes[i]);
@@ -176,8 +189,8 @@ void Store::build_begin(uint32_t nd, const uint64_t* hot) {
     }
   }
   backing_bytes = total;
-  // arena / pinned placement of the lists
-  for (uint32_t pos = 0; pos < n_items; ++pos) {
+  // arena / pinned placement of the lists (eager mode)
+  for (uint32_t pos = 0; pos < n_items && !cfg.demand_mode; ++pos) {
     const uint32_t i = order[pos];
     if (tier[i] == HR_T_HBM) {
       loc[i].hbm_off = hbm.alloc(bytes[i]);
@@ -319,12 +332,11 @@ void Store::launch(const AsmDesc* dev_descs, uint32_t n, uint32_t k, uint32_t sc
   stats.kernel_launches++;
 }
 
-void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* const* k_out, void* const* v_out,
-                     cudaStream_t st) {
+void Store::validate_request(uint32_t n_req, uint32_t k, const uint32_t* ids, void* const* k_out,
+                             void* const* v_out) const {
   require(state == State::Built, HR_ESTATE, "hr_assemble_kv before the store is built");
   require(n_req > 0 && k > 0, HR_EINVAL, "n_req and k must be > 0");
   require(ids && k_out && v_out, HR_EINVAL, "NULL argument");
-  // validate everything before any device work (no partial writes)
   std::vector<uint32_t> tmp(k);
   for (uint32_t r = 0; r < n_req; ++r) {
     require(k_out[r] && v_out[r], HR_EINVAL, "NULL output pointer");
@@ -338,12 +350,43 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
     require(std::adjacent_find(tmp.begin(), tmp.end()) == tmp.end(), HR_EINVAL,
             "duplicate doc id in request " + std::to_string(r) + " (R19)");
   }
+}
+
+// Demand mode (paper-literal Alg. 2 step 2): space freed by evictions of the previous call is
+// released now — its readers are ordered before this call's promotion copies by `start_ev`, and
+// the copy stream is drained before pinned space is rewritten by the host.
+void Store::release_deferred() {
+  if (!pending_pin_free.empty()) {
+    HR_CUDA(cudaStreamSynchronize(copy_stream));
+    for (auto& f : pending_pin_free) pin.release(f.first, f.second);
+    pending_pin_free.clear();
+  }
+  for (auto& f : pending_hbm_free) hbm.release(f.first, f.second);
+  pending_hbm_free.clear();
+}
+
+void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* const* k_out, void* const* v_out,
+                     cudaStream_t st) {
+  validate_request(n_req, k, ids, k_out, v_out);  // before any device work: no partial writes
   HR_CUDA(cudaSetDevice(cfg.device));
+  const bool demand = alg2 != nullptr;
+  if (demand) {
+    release_deferred();
+    if (!start_ev) HR_CUDA(cudaEventCreateWithFlags(&start_ev, cudaEventDisableTiming));
+    HR_CUDA(cudaEventRecord(start_ev, st));  // every kernel that may read freed arena space
+    HR_CUDA(cudaStreamWaitEvent(copy_stream, start_ev, 0));
+  }
   const size_t n_desc = 2ull * n_req * k;
   DescBuf& db = desc_buffer(n_desc);
-  // Alg. 2 step 2 lookups (eager placement: GPU_LIST items are resident)
-  std::vector<uint32_t> miss_items;
-  std::unordered_map<uint32_t, std::vector<AsmDesc>> miss_descs;
+  // a6 planning.  Resident items (physically in the HBM arena when the call starts, or promoted in
+  // eager mode) go to launch A; the rest are streamed, each item once per call.
+  struct Stream {
+    uint32_t item;
+    uint64_t arena_off;  // != kNone: promotion target (demand mode), else a staging-ring slot
+    std::vector<AsmDesc> descs;
+  };
+  std::vector<Stream> streamed;
+  std::unordered_map<uint32_t, size_t> stream_idx;
   size_t nh = 0;
   uint32_t hbm_mask = 0;
   for (uint32_t r = 0; r < n_req; ++r) {
@@ -356,54 +399,85 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
         d.count = counted ? reinterpret_cast<unsigned long long*>(delta + item) : nullptr;
         d.slot = j;
         d.scheme = scheme[item];
-        const uint64_t alg = lay.n_slabs() * lay.slab() * 2 + (bytes_read_alg(item));
         stats.bytes_out += lay.n_slabs() * lay.slab() * 2;
-        stats.bytes_hbm_alg += alg;
-        if (loc[item].hbm_off != FreeList::kNone) {
+        stats.bytes_hbm_alg += lay.n_slabs() * lay.slab() * 2 + bytes_read_alg(item);
+        bool promote = false;
+        if (demand) {  // Alg. 2 step 2: one branch per access, inclusive promotion, LRU
+          const Alg2::Outcome o = alg2->access(item);
+          stats.hits[o.hit == Alg2::GPU ? HR_T_HBM : o.hit == Alg2::PIN ? HR_T_PIN : HR_T_PAGE]++;
+          for (const auto& ev : o.evicted) {
+            Loc& l = loc[ev.second];
+            if (ev.first == Alg2::GPU && l.hbm_off != FreeList::kNone) {
+              pending_hbm_free.emplace_back(l.hbm_off, bytes[ev.second]);  // readers may still be in flight
+              l.hbm_off = FreeList::kNone;
+              stats.migrations_out++;
+            } else if (ev.first == Alg2::PIN && l.pin_off != FreeList::kNone) {
+              pending_pin_free.emplace_back(l.pin_off, bytes[ev.second]);
+              l.pin_off = FreeList::kNone;
+            }
+          }
+          if ((o.put_mask & (1u << Alg2::PIN)) && loc[item].pin_off == FreeList::kNone && pin_base) {
+            const uint64_t off = pin.alloc(bytes[item]);  // queuePIN.put: a pinned copy from the backing
+            if (off != FreeList::kNone) {
+              loc[item].pin_off = off;
+              host_copy(pin_base + off, backing_base + loc[item].backing_off, bytes[item]);
+            }
+          }
+          promote = alg2->contains(Alg2::GPU, item) && loc[item].hbm_off == FreeList::kNone;
+        } else {
+          stats.hits[loc[item].hbm_off != FreeList::kNone ? HR_T_HBM : tier[item]]++;
+        }
+        auto it = stream_idx.find(item);
+        if (it == stream_idx.end() && loc[item].hbm_off != FreeList::kNone) {
           d.codes = hbm_ptr(item);
           d.meta = d.codes + lay.meta_offset(d.scheme);
           db.host[nh++] = d;
           hbm_mask |= 1u << d.scheme;
-          stats.hits[HR_T_HBM]++;
-        } else {
-          auto it = miss_descs.find(item);
-          if (it == miss_descs.end()) {
-            miss_items.push_back(item);
-            it = miss_descs.emplace(item, std::vector<AsmDesc>{}).first;
-          }
-          it->second.push_back(d);
-          stats.hits[tier[item]]++;
+          continue;
         }
+        if (it == stream_idx.end()) {
+          Stream s{item, FreeList::kNone, {}};
+          if (promote) {  // "put C_i in queueGPU": the DMA lands in the arena instead of the ring
+            s.arena_off = hbm.alloc(bytes[item]);
+            if (s.arena_off != FreeList::kNone) stats.migrations_in++;
+          }
+          it = stream_idx.emplace(item, streamed.size()).first;
+          streamed.push_back(std::move(s));
+        }
+        streamed[it->second].descs.push_back(d);
       }
     }
   }
-  // descriptors of the host-tier items point at their staging-ring slot
-  if (!miss_items.empty()) ensure_ring();
-  size_t pos = nh;
-  std::vector<std::pair<size_t, size_t>> miss_range;
-  for (size_t i = 0; i < miss_items.size(); ++i) {
-    const uint32_t item = miss_items[i];
-    uint8_t* slot_ptr = ring[i % slots].dev;
+  // descriptors of streamed items point at their arena slot or staging-ring slot
+  if (!streamed.empty()) ensure_ring();
+  size_t pos = nh, ring_i = 0;
+  std::vector<uint8_t*> dest(streamed.size());
+  std::vector<std::pair<size_t, size_t>> range(streamed.size());
+  for (size_t i = 0; i < streamed.size(); ++i) {
+    Stream& s = streamed[i];
+    dest[i] = s.arena_off != FreeList::kNone ? hbm_base + s.arena_off : ring[ring_i++ % slots].dev;
     const size_t b = pos;
-    for (AsmDesc d : miss_descs[item]) {
-      d.codes = slot_ptr;
-      d.meta = slot_ptr + lay.meta_offset(d.scheme);
+    for (AsmDesc d : s.descs) {
+      d.codes = dest[i];
+      d.meta = dest[i] + lay.meta_offset(d.scheme);
       db.host[pos++] = d;
     }
-    miss_range.emplace_back(b, pos - b);
+    range[i] = {b, pos - b};
   }
   HR_CUDA(cudaMemcpyAsync(db.dev, db.host, pos * sizeof(AsmDesc), cudaMemcpyHostToDevice, st));
-  // launch A: every HBM-resident (request, slot, kind)
+  // launch A: every resident (request, slot, kind)
   if (nh) launch(db.dev, (uint32_t)nh, k, hbm_mask, st);
-  // host-tier items: pinned (or pageable -> pinned bounce) -> staging ring -> launch B
+  // a7: host-tier items -> (pinned, or pageable -> pinned bounce) -> HBM (ring slot or arena) -> launch B
   cudaEvent_t c0 = nullptr, c1 = nullptr;
-  if (timing && !miss_items.empty()) {
+  if (timing && !streamed.empty()) {
     HR_CUDA(cudaEventCreate(&c0));
     HR_CUDA(cudaEventCreate(&c1));
   }
-  for (size_t i = 0; i < miss_items.size(); ++i) {
-    const uint32_t item = miss_items[i];
-    Slot& sl = ring[i % slots];
+  ring_i = 0;
+  for (size_t i = 0; i < streamed.size(); ++i) {
+    const uint32_t item = streamed[i].item;
+    const bool to_arena = streamed[i].arena_off != FreeList::kNone;
+    Slot& sl = ring[(to_arena ? ring_i : ring_i++) % slots];
     const uint8_t* src = nullptr;
     if (loc[item].pin_off != FreeList::kNone) {
       src = pin_base + loc[item].pin_off;
@@ -413,20 +487,15 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
       if (!backing_is_pinned) {  // pageable data is first copied to pinned memory
         if (!sl.bounce) HR_CUDA(cudaHostAlloc((void**)&sl.bounce, max_item, cudaHostAllocPortable));
         if (sl.used) HR_CUDA(cudaEventSynchronize(sl.copied));  // previous DMA out of this bounce buffer done
-        if (!copy_pool) {
-          unsigned n = std::thread::hardware_concurrency() / 2;
-          if (const char* e = std::getenv("HARAG_COPY_THREADS")) n = (unsigned)std::atoi(e);
-          copy_pool.reset(new CopyPool(std::max(0u, std::min(n, 15u))));
-        }
-        copy_pool->copy(sl.bounce, src, bytes[item]);
+        host_copy(sl.bounce, src, bytes[item]);
         src = sl.bounce;
       }
     }
-    HR_CUDA(cudaStreamWaitEvent(copy_stream, sl.free_ev, 0));
+    if (!to_arena) HR_CUDA(cudaStreamWaitEvent(copy_stream, sl.free_ev, 0));
     if (c0 && i == 0) HR_CUDA(cudaEventRecord(c0, copy_stream));
-    HR_CUDA(cudaMemcpyAsync(sl.dev, src, bytes[item], cudaMemcpyHostToDevice, copy_stream));
+    HR_CUDA(cudaMemcpyAsync(dest[i], src, bytes[item], cudaMemcpyHostToDevice, copy_stream));
     HR_CUDA(cudaEventRecord(sl.copied, copy_stream));
-    if (c1 && i + 1 == miss_items.size()) {
+    if (c1 && i + 1 == streamed.size()) {
       HR_CUDA(cudaEventRecord(c1, copy_stream));
       h2d_timers.emplace_back(c0, c1);
     }
@@ -434,12 +503,24 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
     sl.used = true;
     stats.bytes_h2d += bytes[item];
     HR_CUDA(cudaStreamWaitEvent(st, sl.copied, 0));
-    launch(db.dev + miss_range[i].first, (uint32_t)miss_range[i].second, k, 1u << scheme[item], st);
-    HR_CUDA(cudaEventRecord(sl.free_ev, st));
+    launch(db.dev + range[i].first, (uint32_t)range[i].second, k, 1u << scheme[item], st);
+    if (to_arena)
+      loc[item].hbm_off = streamed[i].arena_off;  // resident from now on (stream-ordered)
+    else
+      HR_CUDA(cudaEventRecord(sl.free_ev, st));
   }
   HR_CUDA(cudaEventRecord(db.done, st));
   req_counter += n_req;
   stats.requests += n_req;
+}
+
+void Store::host_copy(void* dst, const void* src, size_t n) {
+  if (!copy_pool) {
+    unsigned t = std::thread::hardware_concurrency() / 2;
+    if (const char* e = std::getenv("HARAG_COPY_THREADS")) t = (unsigned)std::atoi(e);
+    copy_pool.reset(new CopyPool(std::min(t, 15u)));
+  }
+  copy_pool->copy(dst, src, n);
 }
 
 uint64_t Store::bytes_read_alg(uint32_t item) const {
@@ -459,6 +540,10 @@ void Store::replace(cudaStream_t st) {
   HR_CUDA(cudaMemsetAsync(delta, 0, sizeof(int64_t) * n_items, st));
   order = rank_items(h.data(), n_items);
   std::vector<uint32_t> nt = lists_by_bytes(order, bytes.data(), cfg.hbm_budget, cfg.backing_pinned ? 0 : cfg.pin_budget);
+  if (alg2) {  // demand mode (R20): only the lists change; stale queue entries leave by LRU
+    alg2->set_lists(nt.data());
+    return;
+  }
   if (cfg.backing_pinned)
     for (auto& t : nt)
       if (t == HR_T_PAGE) t = HR_T_PIN;

@@ -13,6 +13,7 @@
 #include "kernels.h"
 #include "layout.h"
 #include "pool.h"
+#include "policy.h"
 
 #include <memory>
 
@@ -85,6 +86,11 @@ struct Store {
   void ensure_ring();
   void launch(const AsmDesc* dev_descs, uint32_t n, uint32_t k, uint32_t scheme_mask, cudaStream_t st);
   void compact_hbm();
+  void validate_request(uint32_t n_req, uint32_t k, const uint32_t* ids, void* const* k_out,
+                        void* const* v_out) const;
+  void release_deferred();
+  void host_copy(void* dst, const void* src, size_t n);
+  uint32_t logical_tier(uint32_t item) const;
   void compact_pin();
 
   hr_store_config cfg;
@@ -129,6 +135,10 @@ struct Store {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timers;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> h2d_timers;  // copy-stream window per assemble call
   std::unique_ptr<CopyPool> copy_pool;                           // pageable -> pinned bounce workers
+  // demand mode (cfg.demand_mode = 1): the paper-literal Alg. 2 step 2 state machine
+  std::unique_ptr<Alg2> alg2;
+  std::vector<std::pair<uint64_t, uint64_t>> pending_hbm_free, pending_pin_free;  // (offset, bytes)
+  cudaEvent_t start_ev = nullptr;
   hr_stats stats{};
 };
 

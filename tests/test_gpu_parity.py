@@ -286,3 +286,48 @@ def test_validation_before_any_write(torch_cuda):
     st2 = hr.Store(L=2, H=2, D=64, T=64, ladder=NORTH, taus=(0.25, 0.25), hbm_budget=1 << 20)
     with pytest.raises(hr.HaragError, match="ESTATE"):
         st2.assemble(np.array([[0]]), ko[:1], vo[:1])
+
+
+# ------------------------------------------------- demand mode (paper-literal Alg. 2)
+@pytest.mark.parametrize("backing_pinned", [False, True])
+def test_demand_mode_matches_oracle_alg2(torch_cuda, backing_pinned):
+    """demand_mode = 1: queues start empty; every access takes one Alg. 2 branch
+     with inclusive promotion and LRU (R16).  Per-tier hit counts and
+    the queue contents after every call equal the oracle's Alg2 run on the same
+    access order, and every output stays bit-exact."""
+    import paper_2510_20878_b200 as hr
+    torch = torch_cuda
+    L, H, T, D, n_docs = 2, 2, 64, 64, 16
+    lay = ost.Layout(L=L, H=H, T=T, D=D, dtype="fp16")
+    prof = synth.gen_requests(n_docs, 64, 4, 1.1, seed=7)
+    h = hotness.count_requests(prof, n_docs).astype(np.uint64)
+    ladder, taus = NORTH, (0.25, 0.25)
+    schemes = hotness.assign_schemes(h.tolist(), [NAMES[s] for s in ladder], taus)
+    sizes = [lay.item_bytes(s) for s in schemes]
+    order = hotness.rank_items(h)
+    hb = sum(sizes[i] for i in order[:10]) - 1      # capacity slightly below the list: LRU fires
+    pb = 0 if backing_pinned else sum(sizes[i] for i in order[10:16])
+    st = hr.Store(L=L, H=H, D=D, T=T, dtype="fp16", ladder=ladder, taus=taus, hbm_budget=hb, pin_budget=pb,
+                  backing_pinned=backing_pinned, demand_mode=True)
+    st.build(n_docs, h, gpu_source(L, H, T, D, "fp16"))
+    ora = ost.OracleStore(lay, [NAMES[s] for s in ladder], taus)
+    ora.build(n_docs, h, lambda d, k: synth.gen_item(L, H, T, D, d, k, dtype="fp16"))
+    gl, pl, rest = placement.lists_by_bytes(order, sizes, hb, pb)
+    alg = placement.Alg2(gl, pl, rest, (hb, pb, 0), sizes)
+    names = {placement.GPU: 0, placement.PIN: 1, placement.PAGE: 2, placement.DISK: 2}
+    want_hits = [0, 0, 0]
+    for call in range(6):
+        reqs = synth.gen_requests(n_docs, 5, 4, 1.1, seed=40 + call)
+        check_requests(torch, st, ora, lay, reqs)
+        for req in reqs:
+            for doc in req:
+                for kind in (0, 1):
+                    want_hits[names[alg.access(2 * int(doc) + kind)[0]]] += 1
+        assert st.stats()["hits"] == want_hits, call
+        gpu_q = set(alg.resident(placement.GPU))
+        pin_q = set(alg.resident(placement.PIN))
+        got = [st.item_info(i)[1] for i in range(2 * n_docs)]
+        assert {i for i in range(2 * n_docs) if got[i] == 0} == gpu_q, call
+        assert {i for i in range(2 * n_docs) if got[i] == 1} == pin_q - gpu_q, call
+    s = st.stats()
+    assert s["hbm_used"] <= hb and s["migrations_in"] > 0
