@@ -18,7 +18,10 @@ struct AsmDesc {
   uint32_t scheme;           // hr_scheme
 };
 
-constexpr int kAsmThreads = 288;       // 1 producer warp + 8 consumer warps
+#ifndef HARAG_CONSUMER_WARPS
+#define HARAG_CONSUMER_WARPS 8
+#endif
+constexpr int kAsmThreads = 32 * (1 + HARAG_CONSUMER_WARPS);  // 1 producer warp + consumer warps
 #ifndef HARAG_STAGES
 #define HARAG_STAGES 4
 #endif
