@@ -333,7 +333,10 @@ __device__ __forceinline__ void consume(const AsmParams& p, const Smem& sm, int 
 }
 
 template <int DT>
-__global__ void __launch_bounds__(kAsmThreads) assemble_kv_kernel(const __grid_constant__ AsmParams p) {
+#ifndef HARAG_MIN_BLOCKS
+#define HARAG_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(kAsmThreads, HARAG_MIN_BLOCKS) assemble_kv_kernel(const __grid_constant__ AsmParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const Smem sm{smem_raw, p.meta_stage};
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
