@@ -19,7 +19,7 @@ struct AsmDesc {
 };
 
 #ifndef HARAG_CONSUMER_WARPS
-#define HARAG_CONSUMER_WARPS 8
+#define HARAG_CONSUMER_WARPS 28
 #endif
 constexpr int kAsmThreads = 32 * (1 + HARAG_CONSUMER_WARPS);  // 1 producer warp + consumer warps
 #ifndef HARAG_STAGES
