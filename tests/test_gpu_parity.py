@@ -331,3 +331,114 @@ def test_demand_mode_matches_oracle_alg2(torch_cuda, backing_pinned):
         assert {i for i in range(2 * n_docs) if got[i] == 1} == pin_q - gpu_q, call
     s = st.stats()
     assert s["hbm_used"] <= hb and s["migrations_in"] > 0
+
+
+# ------------------------------------------- BASELINE configs 2-4 at full shape
+def _sampled_check(torch, st, reqs, outs, lay, schemes, rng, n_slabs=2, src_heads=None):
+    """Oracle decode of sampled (request, slot, kind, layer, head) slabs, one by one."""
+    L, Hl, T, D = lay.L, lay.Hl, lay.T, lay.D
+    k = reqs.shape[1]
+    for r in range(len(reqs)):
+        for j in rng.choice(k, min(2, k), replace=False):
+            doc = int(reqs[r, j])
+            for kind in (0, 1):
+                item = 2 * doc + kind
+                g = outs[kind][r].view(L, Hl, k * T, D)
+                for _ in range(n_slabs):
+                    l, hh = int(rng.integers(L)), int(rng.integers(Hl))
+                    h_glob = lay.heads[0] + hh
+                    x = synth.gen_item(L, lay.H, T, D, doc, kind, heads=(h_glob, h_glob + 1))[l, 0]
+                    c, m = ost.encode_slab(x, schemes[item], lay)
+                    want = ost.decode_slab(c, m, schemes[item], lay)
+                    got = g[l, hh, j * T:(j + 1) * T].cpu().numpy().view(np.uint16).reshape(-1)
+                    assert np.array_equal(got, want), (r, j, kind, l, hh)
+
+
+def test_config2_llama2_mha_tiered_sampled(torch_cuda):
+    """BASELINE config 2: Llama-2-7B MHA KV shape (32 layers x 32 heads x 128),
+    hot items in HBM, cold in pinned host DRAM, batch of requests; sampled slabs."""
+    import paper_2510_20878_b200 as hr
+    torch = torch_cuda
+    L, H, T, D, n_docs, k, B = 32, 32, 512, 128, 14, 4, 4
+    lay = ost.Layout(L=L, H=H, T=T, D=D)
+    prof = synth.gen_requests(n_docs, 80, k, 1.1, seed=9)
+    h = hotness.count_requests(prof, n_docs).astype(np.uint64)
+    schemes = hotness.assign_schemes(h.tolist(), [NAMES[s] for s in PAPER], (0.1, 0.1, 0.1))
+    order = hotness.rank_items(h)
+    hb = sum(lay.item_bytes(schemes[i]) for i in order[:8])
+    st = hr.Store(L=L, H=H, D=D, T=T, ladder=PAPER, taus=(0.1, 0.1, 0.1), hbm_budget=hb,
+                  backing_pinned=True, keep_backing=True)
+    st.build(n_docs, h, gpu_source(L, H, T, D, "bf16"))
+    tiers = [st.item_info(i)[1] for i in range(2 * n_docs)]
+    assert tiers.count(0) == 8 and tiers.count(1) == 2 * n_docs - 8
+    reqs = synth.gen_requests(n_docs, B, k, 1.1, seed=3)
+    ko, vo = alloc_out(torch, st, B, k)
+    st.assemble(reqs, ko, vo)
+    torch.cuda.synchronize()
+    assert st.stats()["hits"][1] > 0
+    _sampled_check(torch, st, reqs, (ko, vo), lay, schemes, np.random.default_rng(1))
+
+
+@pytest.mark.parametrize("world", [2, 8])
+def test_config3_llama3_70b_sharded_sampled(torch_cuda, world):
+    """BASELINE config 3: Llama-3-70B KV shape (80 layers x 8 KV heads), KV-head
+    sharded across `world` ranks (stores built one rank at a time on this GPU)."""
+    import paper_2510_20878_b200 as hr
+    torch = torch_cuda
+    L, H, T, D, n_docs, k, B = 80, 8, 512, 128, 10, 4, 2
+    prof = synth.gen_requests(n_docs, 60, k, 1.1, seed=11)
+    h = hotness.count_requests(prof, n_docs).astype(np.uint64)
+    schemes = hotness.assign_schemes(h.tolist(), [NAMES[s] for s in NORTH], (0.2, 0.3))
+    reqs = synth.gen_requests(n_docs, B, k, 1.1, seed=5)
+    for rank in (0, world - 1):
+        lay = ost.Layout(L=L, H=H, T=T, D=D, rank=rank, world=world)
+        st = hr.Store(L=L, H=H, D=D, T=T, ladder=NORTH, taus=(0.2, 0.3), rank=rank, world=world,
+                      hbm_budget=sum(lay.item_bytes(s) for s in schemes) + 4096, keep_backing=False)
+        st.build(n_docs, h, gpu_source(L, H, T, D, "bf16"))
+        ko, vo = alloc_out(torch, st, B, k)
+        st.assemble(reqs, ko, vo)
+        torch.cuda.synchronize()
+        _sampled_check(torch, st, reqs, (ko, vo), lay, schemes, np.random.default_rng(rank))
+        # request q is counted by rank q mod world only
+        d = st.hotness_delta().cpu().numpy()
+        assert np.array_equal(d, hotness.count_requests(reqs, n_docs, rank, world))
+        st.close()
+
+
+def test_config4_hotness_drift_replacement(torch_cuda):
+    """BASELINE config 4 (scaled): re-placement under shifting Zipf skew
+    (s = 0.6 -> 0.8 -> 1.0 -> 1.2 -> 0.6, fresh permutation per phase), per-rank
+    view of 8-way head sharding of the Llama-3-8B shape (1 KV head per rank),
+    decay_shift 1, an epoch per phase: placement after every epoch equals the
+    oracle's, and assembled slabs stay bit-exact across migrations."""
+    import paper_2510_20878_b200 as hr
+    torch = torch_cuda
+    L, H, T, D, n_docs, k, world = 32, 8, 512, 128, 40, 8, 8
+    lay = ost.Layout(L=L, H=H, T=T, D=D, rank=0, world=world)
+    prof = synth.gen_requests(n_docs, 100, k, 1.1, seed=12)
+    h = hotness.count_requests(prof, n_docs).astype(np.uint64)
+    schemes = hotness.assign_schemes(h.tolist(), [NAMES[s] for s in PAPER], (0.1, 0.1, 0.1))
+    sizes = [lay.item_bytes(s) for s in schemes]
+    order = hotness.rank_items(h)
+    hb = sum(sizes[i] for i in order[:20])
+    pb = sum(sizes[i] for i in order[20:40])
+    st = hr.Store(L=L, H=H, D=D, T=T, ladder=PAPER, taus=(0.1, 0.1, 0.1), rank=0, world=world,
+                  hbm_budget=hb, pin_budget=pb, keep_backing=True, decay_shift=1)
+    st.build(n_docs, h, gpu_source(L, H, T, D, "bf16"))
+    hcur = h.astype(np.int64)
+    names = {0: placement.GPU, 1: placement.PIN, 2: placement.PAGE}
+    rng = np.random.default_rng(4)
+    for phase, s in enumerate((0.6, 0.8, 1.0, 1.2, 0.6)):
+        reqs = synth.gen_requests(n_docs, 32, k, s, seed=200 + phase, perm_seed=300 + phase)
+        ko, vo = alloc_out(torch, st, len(reqs), k)
+        st.assemble(reqs, ko, vo)
+        torch.cuda.synchronize()
+        _sampled_check(torch, st, reqs[:3], (ko[:3], vo[:3]), lay, schemes, rng, n_slabs=1)
+        # the all-reduce of the 8 ranks' deltas equals the count of every request
+        full = hotness.count_requests(reqs, n_docs)
+        st.hotness_delta().copy_(torch.from_numpy(full).cuda())
+        st.replace()
+        hcur = hotness.epoch_update(hcur, full, 1)
+        want = placement.eager_tiers(hcur, sizes, hb, pb)
+        assert [names[st.item_info(i)[1]] for i in range(2 * n_docs)] == want, phase
+    assert st.stats()["migrations_in"] > 0
