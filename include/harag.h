@@ -173,7 +173,11 @@ hr_status hr_assemble_kv(hr_store* s, uint32_t n_req, uint32_t k, const uint32_t
  * (reduced) delta: h <- (h >> decay_shift) + delta, re-rank, recompute the
  * GPU/PIN lists (schemes stay fixed: compress once), evict items that
  * left GPU_LIST and promote the newcomers (H2D from the host backing; needs
- * keep_backing = 1, else HR_ESTATE), zero the delta.  Synchronises `stream`. */
+ * keep_backing = 1, else HR_ESTATE), zero the delta.  Synchronises `stream`
+ * once to read the delta; promotions are asynchronous (an item is served from
+ * the host until its copy lands) and are ordered after all work already
+ * enqueued on `stream` — callers that assemble on several streams must
+ * synchronise the others first.  Demand mode: only the lists change. */
 hr_status hr_hotness_delta(hr_store* s, int64_t** dev_ptr, uint32_t* n);
 hr_status hr_replace(hr_store* s, void* stream);
 

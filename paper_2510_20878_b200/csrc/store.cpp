@@ -99,12 +99,14 @@ Store::~Store() {
   if (src_k) cudaFree(src_k);
   if (src_v) cudaFree(src_v);
   if (start_ev) cudaEventDestroy(start_ev);
+  if (mig_ev) cudaEventDestroy(mig_ev);
+  for (auto& p : promos) cudaEventDestroy(p.ev);
   if (copy_stream) cudaStreamDestroy(copy_stream);
 }
 
 uint32_t Store::logical_tier(uint32_t item) const {
   if (alg2) return alg2->contains(Alg2::GPU, item) ? HR_T_HBM : alg2->contains(Alg2::PIN, item) ? HR_T_PIN : HR_T_PAGE;
-  return loc[item].hbm_off != FreeList::kNone ? HR_T_HBM : tier[item];
+  return tier[item];  // eager: the placement target (a promotion may still be in flight)
 }
 
 uint8_t* Store::hbm_ptr(uint32_t item) const { return hbm_base + loc[item].hbm_off; }
@@ -369,6 +371,7 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
                      cudaStream_t st) {
   validate_request(n_req, k, ids, k_out, v_out);  // before any device work: no partial writes
   HR_CUDA(cudaSetDevice(cfg.device));
+  if (!promos.empty()) poll_promotions(false);
   const bool demand = alg2 != nullptr;
   if (demand) {
     release_deferred();
@@ -425,7 +428,9 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
           }
           promote = alg2->contains(Alg2::GPU, item) && loc[item].hbm_off == FreeList::kNone;
         } else {
-          stats.hits[loc[item].hbm_off != FreeList::kNone ? HR_T_HBM : tier[item]]++;
+          stats.hits[loc[item].hbm_off != FreeList::kNone                        ? HR_T_HBM
+                     : (loc[item].pin_off != FreeList::kNone || backing_is_pinned) ? HR_T_PIN
+                                                                                   : HR_T_PAGE]++;
         }
         auto it = stream_idx.find(item);
         if (it == stream_idx.end() && loc[item].hbm_off != FreeList::kNone) {
@@ -529,13 +534,33 @@ uint64_t Store::bytes_read_alg(uint32_t item) const {
 }
 
 // ---------------------------------------------------------------- epochs
+void Store::poll_promotions(bool wait_all) {
+  size_t w = 0;
+  for (auto& p : promos) {
+    const cudaError_t q = wait_all ? cudaEventSynchronize(p.ev) : cudaEventQuery(p.ev);
+    if (q == cudaSuccess) {
+      loc[p.item].hbm_off = p.off;  // the copy landed: served from HBM from now on
+      cudaEventDestroy(p.ev);
+    } else if (q == cudaErrorNotReady) {
+      promos[w++] = p;
+    } else {
+      HR_CUDA(q);
+    }
+  }
+  promos.resize(w);
+}
+
+// a9 re-placement.  Eviction frees arena space at once: the promotion copies that may reuse it are
+// ordered (copy stream waits `mig_ev`) after every launch already enqueued on `st`, and no later
+// launch reads an evicted item from HBM.  Promotions are asynchronous: an item becomes resident
+// when its copy event has completed (polled at the next hr_assemble_kv), and until then it is
+// streamed from the host like any host-tier item — requests never wait for a migration.
 void Store::replace(cudaStream_t st) {
   require(state == State::Built, HR_ESTATE, "hr_replace before the store is built");
   HR_CUDA(cudaSetDevice(cfg.device));
-  HR_CUDA(cudaStreamSynchronize(st));
-  HR_CUDA(cudaDeviceSynchronize());  // no assemble may read the arena while items move
   std::vector<int64_t> dh(n_items);
-  HR_CUDA(cudaMemcpy(dh.data(), delta, sizeof(int64_t) * n_items, cudaMemcpyDeviceToHost));
+  HR_CUDA(cudaMemcpyAsync(dh.data(), delta, sizeof(int64_t) * n_items, cudaMemcpyDeviceToHost, st));
+  HR_CUDA(cudaStreamSynchronize(st));
   epoch_update(h.data(), dh.data(), n_items, cfg.decay_shift);  // a9 (R20)
   HR_CUDA(cudaMemsetAsync(delta, 0, sizeof(int64_t) * n_items, st));
   order = rank_items(h.data(), n_items);
@@ -547,9 +572,14 @@ void Store::replace(cudaStream_t st) {
   if (cfg.backing_pinned)
     for (auto& t : nt)
       if (t == HR_T_PAGE) t = HR_T_PIN;
+  poll_promotions(true);  // the previous epoch's copies (normally long done)
   bool any_move = false;
   for (uint32_t i = 0; i < n_items; ++i) any_move |= (nt[i] == HR_T_HBM) != (loc[i].hbm_off != FreeList::kNone);
   require(!any_move || cfg.keep_backing, HR_ESTATE, "re-placement needs keep_backing = 1");
+  if (!mig_ev) HR_CUDA(cudaEventCreateWithFlags(&mig_ev, cudaEventDisableTiming));
+  HR_CUDA(cudaEventRecord(mig_ev, st));
+  HR_CUDA(cudaStreamWaitEvent(copy_stream, mig_ev, 0));
+  bool pin_changed = false;
   // evict first (host copies are inclusive, R16)
   for (uint32_t i = 0; i < n_items; ++i) {
     if (nt[i] != HR_T_HBM && loc[i].hbm_off != FreeList::kNone) {
@@ -560,15 +590,21 @@ void Store::replace(cudaStream_t st) {
     if (nt[i] != HR_T_PIN && loc[i].pin_off != FreeList::kNone) {
       pin.release(loc[i].pin_off, bytes[i]);
       loc[i].pin_off = FreeList::kNone;
+      pin_changed = true;
     }
   }
+  // pinned space freed above may still be the source of an in-flight DMA
+  if (pin_changed) HR_CUDA(cudaStreamSynchronize(copy_stream));
   // promote in rank order
   for (uint32_t pos = 0; pos < n_items; ++pos) {
     const uint32_t i = order[pos];
     if (nt[i] == HR_T_HBM && loc[i].hbm_off == FreeList::kNone) {
       uint64_t off = hbm.alloc(bytes[i]);
       if (off == FreeList::kNone && hbm_cap - hbm.used() >= align_up(bytes[i], FreeList::kAlign)) {
-        compact_hbm();  // the lists fit the budget by construction: defragment and retry
+        // the lists fit the budget by construction: defragment (needs an idle device) and retry
+        HR_CUDA(cudaDeviceSynchronize());
+        poll_promotions(true);
+        compact_hbm();
         off = hbm.alloc(bytes[i]);
       }
       if (off == FreeList::kNone) {
@@ -576,13 +612,18 @@ void Store::replace(cudaStream_t st) {
         nt[i] = cfg.backing_pinned ? HR_T_PIN : HR_T_PAGE;
         continue;
       }
-      loc[i].hbm_off = off;
       HR_CUDA(cudaMemcpyAsync(hbm_base + off, backing_base + loc[i].backing_off, bytes[i], cudaMemcpyHostToDevice,
                               copy_stream));
+      Promo pr{i, off, nullptr};
+      HR_CUDA(cudaEventCreateWithFlags(&pr.ev, cudaEventDisableTiming));
+      HR_CUDA(cudaEventRecord(pr.ev, copy_stream));
+      promos.push_back(pr);
       stats.migrations_in++;
+      stats.bytes_h2d += bytes[i];
     } else if (nt[i] == HR_T_PIN && !cfg.backing_pinned && loc[i].pin_off == FreeList::kNone) {
       uint64_t off = pin.alloc(bytes[i]);
       if (off == FreeList::kNone && pin_cap - pin.used() >= align_up(bytes[i], FreeList::kAlign)) {
+        HR_CUDA(cudaStreamSynchronize(copy_stream));
         compact_pin();
         off = pin.alloc(bytes[i]);
       }
@@ -591,12 +632,10 @@ void Store::replace(cudaStream_t st) {
         continue;
       }
       loc[i].pin_off = off;
-      std::memcpy(pin_base + off, backing_base + loc[i].backing_off, bytes[i]);
+      host_copy(pin_base + off, backing_base + loc[i].backing_off, bytes[i]);
     }
   }
-  tier = nt;
-  HR_CUDA(cudaStreamSynchronize(copy_stream));
-  HR_CUDA(cudaStreamSynchronize(st));
+  tier = nt;  // target placement; HBM promotions become resident as their copies land
 }
 
 void Store::compact_hbm() {

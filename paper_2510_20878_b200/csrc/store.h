@@ -139,6 +139,15 @@ struct Store {
   std::unique_ptr<Alg2> alg2;
   std::vector<std::pair<uint64_t, uint64_t>> pending_hbm_free, pending_pin_free;  // (offset, bytes)
   cudaEvent_t start_ev = nullptr;
+  // eager re-placement: asynchronous promotions (item becomes resident when its copy event completes)
+  struct Promo {
+    uint32_t item;
+    uint64_t off;
+    cudaEvent_t ev;
+  };
+  std::vector<Promo> promos;
+  cudaEvent_t mig_ev = nullptr;
+  void poll_promotions(bool wait_all);
   hr_stats stats{};
 };
 
