@@ -462,11 +462,13 @@ def run_tiered(ctx, wl, ko, vo, kvb, args):
     step_s = ms_max / steps / 1e3
     hbm_alg_per_step = stats["bytes_hbm_alg"] / steps
     h2d_per_step = stats["bytes_h2d"] / steps
+    mig_per_step = stats["bytes_migrated"] / steps
     peak = 6456.8
-    t_star = max(hbm_alg_per_step / (peak * 1e9), h2d_per_step / (per_rank * 1e9))
+    t_star = max(hbm_alg_per_step / (peak * 1e9), (h2d_per_step + mig_per_step) / (per_rank * 1e9))
     res = {"workload": wl["desc"], "value": round(tot_bytes / (ms_max / 1e3) / 1e9, 2), "unit": "GB/s",
            "ms_per_step": round(ms_max / steps, 3), "steps": steps,
            "hits_per_tier": stats["hits"], "h2d_bytes_per_step": int(h2d_per_step),
+           "migration_bytes_per_step": int(mig_per_step),
            "h2d_items_per_step": stats["h2d_items"] / steps,
            "link": {"achieved_GBps": round(h2d_GBps, 2) if h2d_GBps else None,
                     "peak_GBps": round(per_rank, 2), "peak_all_ranks_GBps": round(agg, 2),
@@ -474,7 +476,8 @@ def run_tiered(ctx, wl, ko, vo, kvb, args):
                     "peak_source": "pinned H2D 1 GiB cudaMemcpyAsync best of 10, measured in this run"},
            "overlapped_roofline": {"t_star_ms": round(t_star * 1e3, 3),
                                    "frac": round(t_star / step_s, 4),
-                                   "formula": "max(HBM alg bytes / hbm_gbs, H2D bytes / link peak) / step time"},
+                                   "formula": "max(HBM alg bytes / hbm_gbs, (H2D + migration bytes) / link peak)"
+                                              " / step time"},
            "hbm_budget_bytes": wl["hbm_budget"], "alias_R": wl["alias_R"], "build_seconds": round(build_s, 2),
            "decay_shift": wl.get("decay_shift", 0),
            "migrations": [stats["migrations_in"], stats["migrations_out"]]}

@@ -107,6 +107,7 @@ typedef struct {
   double   h2d_ms;            /* sum over assemble calls of the host->device copy window (first copy start ->
                                  last copy end, CUDA events on the copy stream) when timing is on */
   uint64_t h2d_items;         /* host-tier items streamed */
+  uint64_t bytes_migrated;    /* host -> device bytes of hr_replace promotions (not in bytes_h2d) */
 } hr_stats;
 
 typedef struct hr_store hr_store;

@@ -178,7 +178,8 @@ class Store:
                 "kernel_launches": s.kernel_launches, "migrations_in": s.migrations_in,
                 "migrations_out": s.migrations_out, "failed_promotions": s.failed_promotions,
                 "kernel_ms": s.kernel_ms, "timed_launches": s.timed_launches, "hbm_used": s.hbm_used,
-                "pin_used": s.pin_used, "h2d_ms": s.h2d_ms, "h2d_items": s.h2d_items}
+                "pin_used": s.pin_used, "h2d_ms": s.h2d_ms, "h2d_items": s.h2d_items,
+                "bytes_migrated": s.bytes_migrated}
 
     def close(self) -> None:
         if self._h:

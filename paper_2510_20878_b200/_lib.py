@@ -40,6 +40,7 @@ class Stats(C.Structure):
         ("migrations_in", C.c_uint64), ("migrations_out", C.c_uint64), ("failed_promotions", C.c_uint64),
         ("kernel_ms", C.c_double), ("timed_launches", C.c_uint64), ("hbm_used", C.c_uint64),
         ("pin_used", C.c_uint64), ("h2d_ms", C.c_double), ("h2d_items", C.c_uint64),
+        ("bytes_migrated", C.c_uint64),
     ]
 
 

@@ -619,7 +619,7 @@ void Store::replace(cudaStream_t st) {
       HR_CUDA(cudaEventRecord(pr.ev, copy_stream));
       promos.push_back(pr);
       stats.migrations_in++;
-      stats.bytes_h2d += bytes[i];
+      stats.bytes_migrated += bytes[i];
     } else if (nt[i] == HR_T_PIN && !cfg.backing_pinned && loc[i].pin_off == FreeList::kNone) {
       uint64_t off = pin.alloc(bytes[i]);
       if (off == FreeList::kNone && pin_cap - pin.used() >= align_up(bytes[i], FreeList::kAlign)) {
