@@ -315,6 +315,39 @@ def link_peak(ctx, gib=1, reps=10):
     return per_rank, agg
 
 
+def measured_hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (copy, read+write)"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, "B200_PROFILING.md fallback (6.65 TB/s)"
+
+
+def run_per_scheme(ctx, wl, args):
+    """Table II analogue on B200: decode throughput of each scheme alone (C2 shape,
+    400-doc single-scheme HBM store, batch 16, k = 10)."""
+    import synth
+    peak, _ = measured_hbm_peak()
+    res = {}
+    B, k = 16, wl["k"]
+    for scheme in ("PASS16", "INT8", "FP8E4M3", "FP8E5M2", "GSE8", "INT4"):
+        w = dict(wl, n_docs=400, ladder=(scheme,), taus=())
+        st, _, _, _, _ = build_store(ctx, w)
+        kvb = st.kv_bytes(k)
+        out = ctx.torch.empty(2 * B * kvb // 2, dtype=ctx.torch.int16, device="cuda")
+        ko = [out[(2 * r) * kvb // 2:(2 * r + 1) * kvb // 2] for r in range(B)]
+        vo = [out[(2 * r + 1) * kvb // 2:(2 * r + 2) * kvb // 2] for r in range(B)]
+        pool = synth.gen_requests(400, 4 * B, k, wl["s"], seed=1).reshape(4, B, k)
+        ms, tot, stats, _ = timed_steps(ctx, st, pool, ko, vo, 20, 3, 0, sample_clocks=False)
+        avg = stats["kernel_ms"] / max(1, stats["timed_launches"])
+        ach = stats["bytes_hbm_alg"] / max(1, stats["kernel_launches"]) / (avg / 1e3) / 1e9
+        res[scheme] = {"assembled_GBps": round(tot / (ms / 1e3) / 1e9, 1), "achieved_hbm_GBps": round(ach, 1),
+                       "frac": round(ach / peak, 4)}
+        st.close()
+        del out, ko, vo
+    return res
+
+
 def run_ours(args, wl):
     import paper_2510_20878_b200 as hr
     import synth
@@ -344,14 +377,7 @@ def run_ours(args, wl):
     value = tot_bytes / (ms_max / 1e3) / 1e9
 
     # ---- roofline of the dominant kernel (assemble_kv_kernel), live CUDA events
-    peaks = {}
-    try:
-        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            peaks = json.load(f)
-    except OSError:
-        pass
-    peak = peaks.get("hbm_gbs", 6650.0)
-    peak_src = "MEASURED_PEAKS.json hbm_gbs (copy, read+write)" if "hbm_gbs" in peaks else "B200_PROFILING.md fallback"
+    peak, peak_src = measured_hbm_peak()
     launches = max(1, stats["timed_launches"])
     avg_ms = stats["kernel_ms"] / launches
     alg_per_launch = stats["bytes_hbm_alg"] / max(1, stats["kernel_launches"])
@@ -415,6 +441,10 @@ def run_ours(args, wl):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = oracle_baseline(wl, pool[0][0], budget_s=10.0, layers=2)
 
+    per_scheme = None
+    if not args.no_per_scheme and wl.get("tiered_variant"):
+        per_scheme = run_per_scheme(ctx, wl, args)
+
     # ---- host-tier leg (a7): HBM hot set + pinned cold set, streamed over the host link
     tiered = None
     if not args.no_tiered and wl.get("tiered_variant"):
@@ -437,6 +467,7 @@ def run_ours(args, wl):
         "clocks": clocks,
         "build": build,
         "tiered": tiered,
+        "per_scheme": per_scheme,
         "impl": "ours",
     }
     if rank == 0:
@@ -463,7 +494,7 @@ def run_tiered(ctx, wl, ko, vo, kvb, args):
     hbm_alg_per_step = stats["bytes_hbm_alg"] / steps
     h2d_per_step = stats["bytes_h2d"] / steps
     mig_per_step = stats["bytes_migrated"] / steps
-    peak = 6456.8
+    peak = measured_hbm_peak()[0]
     t_star = max(hbm_alg_per_step / (peak * 1e9), (h2d_per_step + mig_per_step) / (per_rank * 1e9))
     res = {"workload": wl["desc"], "value": round(tot_bytes / (ms_max / 1e3) / 1e9, 2), "unit": "GB/s",
            "ms_per_step": round(ms_max / steps, 3), "steps": steps,
@@ -497,6 +528,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tiered", action="store_true", help="skip the host-tier leg")
+    ap.add_argument("--no-per-scheme", action="store_true", help="skip the per-scheme decode table")
     ap.add_argument("--ncu-traffic", type=float, default=None,
                     help="dram read+write bytes per launch from an ncu --set full capture (profiles/)")
     args = ap.parse_args()
