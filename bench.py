@@ -324,25 +324,49 @@ def measured_hbm_peak():
 
 
 def run_per_scheme(ctx, wl, args):
-    """Table II analogue on B200: decode throughput of each scheme alone (C2 shape,
-    400-doc single-scheme HBM store, batch 16, k = 10)."""
+    """Table II analogue on B200, per scheme alone (C2 shape, 400-doc single-scheme
+    HBM store): quantise throughput (a3+a4, build) and assemble throughput (a8,
+    batch 16, k = 10).  Quantise bytes = 2 B source read + packed blob written."""
+    import paper_2510_20878_b200 as hr
     import synth
+    torch = ctx.torch
     peak, _ = measured_hbm_peak()
     res = {}
-    B, k = 16, wl["k"]
+    B, k, n_docs = 16, wl["k"], 400
+    L, H, D, T = wl["L"], wl["H"], wl["D"], wl["T"]
+    geo = dict(L=L, H=H, D=D, T=T, dtype=wl["dtype"], rank=ctx.rank, world=ctx.world)
+    src = torch.empty(2, L * H * T * D, dtype=torch.int16, device="cuda")
+    synth.gen_item_device(src[0].data_ptr(), L, H, T, D, 0, 0, dtype=wl["dtype"])
+    synth.gen_item_device(src[1].data_ptr(), L, H, T, D, 0, 1, dtype=wl["dtype"])
     for scheme in ("PASS16", "INT8", "FP8E4M3", "FP8E5M2", "GSE8", "INT4"):
-        w = dict(wl, n_docs=400, ladder=(scheme,), taus=())
-        st, _, _, _, _ = build_store(ctx, w)
+        item = hr.item_bytes(scheme, **geo)
+        st = hr.Store(ladder=(scheme,), taus=(), device=ctx.device, keep_backing=False,
+                      hbm_budget=2 * n_docs * item + (1 << 20), **geo)
+        st.build_begin(n_docs, np.zeros(2 * n_docs, np.uint64))
+        for d in range(3):
+            st.build_put(d, src[0], src[1], stream=ctx.stream)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(ctx.stream)
+        for d in range(n_docs):   # every doc quantised from the same resident source (identical items)
+            st.build_put(d, src[0], src[1], stream=ctx.stream)
+        e1.record(ctx.stream)
+        st.build_end(stream=ctx.stream)
+        q_ms = e0.elapsed_time(e1)
+        q_bytes = n_docs * 2 * (L * (H // ctx.world) * T * D * 2 + item)
         kvb = st.kv_bytes(k)
-        out = ctx.torch.empty(2 * B * kvb // 2, dtype=ctx.torch.int16, device="cuda")
+        out = torch.empty(2 * B * kvb // 2, dtype=torch.int16, device="cuda")
         ko = [out[(2 * r) * kvb // 2:(2 * r + 1) * kvb // 2] for r in range(B)]
         vo = [out[(2 * r + 1) * kvb // 2:(2 * r + 2) * kvb // 2] for r in range(B)]
-        pool = synth.gen_requests(400, 4 * B, k, wl["s"], seed=1).reshape(4, B, k)
+        pool = synth.gen_requests(n_docs, 4 * B, k, wl["s"], seed=1).reshape(4, B, k)
         ms, tot, stats, _ = timed_steps(ctx, st, pool, ko, vo, 20, 3, 0, sample_clocks=False)
         avg = stats["kernel_ms"] / max(1, stats["timed_launches"])
         ach = stats["bytes_hbm_alg"] / max(1, stats["kernel_launches"]) / (avg / 1e3) / 1e9
-        res[scheme] = {"assembled_GBps": round(tot / (ms / 1e3) / 1e9, 1), "achieved_hbm_GBps": round(ach, 1),
-                       "frac": round(ach / peak, 4)}
+        qg = q_bytes / (q_ms / 1e3) / 1e9
+        res[scheme] = {"assemble_GBps_out": round(tot / (ms / 1e3) / 1e9, 1), "assemble_hbm_GBps": round(ach, 1),
+                       "assemble_frac": round(ach / peak, 4),
+                       "quantize_hbm_GBps": round(qg, 1), "quantize_frac": round(qg / peak, 4),
+                       "quantize_us_per_item": round(1e3 * q_ms / (2 * n_docs), 2)}
         st.close()
         del out, ko, vo
     return res

@@ -60,6 +60,7 @@ struct QuantParams {
   uint32_t L, H, Hl, h0, T, D, G, gse_e, gse_m, dtype, scheme;
   uint64_t code_bytes_slab, meta_offset, meta_stride;
   int* err;                  // set to 1 on NaN/Inf
+  int* gse_range;            // device scratch int[2 * L * Hl] (GSE-8 per-slab exponent range)
 };
 
 // a3 + a4: one CTA per (layer, local head) slab.

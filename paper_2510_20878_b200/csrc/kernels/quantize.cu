@@ -9,6 +9,15 @@
 //   PASS16 source bits unchanged
 // Every fp decision is one IEEE fp32 operation with round-to-nearest-even
 // (__fdiv_rn, __fsub_rn, __fadd_rn; no reciprocal, no contraction, R3).
+//
+// Work decomposition: a warp owns a 256-element chunk (8 elements = one
+// 16-byte load per lane) of one slab and grid-strides over the item.  For
+// G <= 256 a group is G/8 consecutive lanes and its statistics are a segmented
+// warp-shuffle reduction — one read of the source, one write of codes + meta.
+// G > 256 (e.g. the paper-ratio mode G = T*D): one warp per group, two passes
+// (the second read hits L2).  GSE-8 needs the slab-wide exponent range first:
+// a reduction kernel (warp shuffles + one atomicMin/Max per warp) then the
+// encode kernel, which rebuilds the shared-exponent array per warp.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_fp8.h>
@@ -20,6 +29,7 @@ namespace harag {
 namespace {
 
 constexpr int kQThreads = 256;
+constexpr int kChunk = 256;  // elements per warp iteration
 
 template <int DT>
 __device__ __forceinline__ float to_f32(uint32_t bits16) {
@@ -42,263 +52,354 @@ __device__ __forceinline__ void load8(const uint16_t* p, float (&x)[8], uint4& r
   }
 }
 
-__device__ __forceinline__ uint32_t ord_key(float f) {  // float order == unsigned order
-  uint32_t b = __float_as_uint(f);
-  return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-}
-__device__ __forceinline__ float ord_unkey(uint32_t k) {
-  return __uint_as_float((k & 0x80000000u) ? (k & 0x7FFFFFFFu) : ~k);
-}
-
-template <int SCHEME, int DT>
-__global__ void __launch_bounds__(kQThreads) quantize_slab_kernel(QuantParams p) {
-  extern __shared__ __align__(16) uint32_t qsm[];
-  const uint32_t slab_id = blockIdx.x;  // = l * Hl + h_local
-  const uint32_t l = slab_id / p.Hl, hl = slab_id % p.Hl;
-  const uint64_t slab = (uint64_t)p.T * p.D;
-  const uint16_t* src = p.src + ((uint64_t)l * p.H + p.h0 + hl) * slab;
-  uint8_t* codes = p.dst + slab_id * p.code_bytes_slab;
-  uint8_t* meta = p.dst + p.meta_offset + slab_id * p.meta_stride;
-  const uint32_t n_vec = (uint32_t)(slab / 8);
-  const uint32_t ng = (uint32_t)(slab / p.G);
-  const uint32_t tid = threadIdx.x;
+__device__ __forceinline__ bool any_nonfinite(const float (&x)[8]) {
   bool bad = false;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) bad |= !isfinite(x[i]);
+  return bad;
+}
 
-  if constexpr (SCHEME == HR_S_PASS16) {
-    for (uint32_t v = tid; v < n_vec; v += kQThreads) {
-      float x[8];
-      uint4 raw;
-      load8<DT>(src + 8ull * v, x, raw);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) bad |= !isfinite(x[i]);
-      reinterpret_cast<uint4*>(codes)[v] = raw;
-    }
-  } else if constexpr (SCHEME == HR_S_FP8E4M3 || SCHEME == HR_S_FP8E5M2) {
-    constexpr __nv_fp8_interpretation_t kInterp = SCHEME == HR_S_FP8E4M3 ? __NV_E4M3 : __NV_E5M2;
-    for (uint32_t v = tid; v < n_vec; v += kQThreads) {
-      float x[8];
-      uint4 raw;
-      load8<DT>(src + 8ull * v, x, raw);
-      uint32_t w[2];
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        uint32_t lo = __nv_cvt_float2_to_fp8x2(make_float2(x[4 * i], x[4 * i + 1]), __NV_SATFINITE, kInterp);
-        uint32_t hi = __nv_cvt_float2_to_fp8x2(make_float2(x[4 * i + 2], x[4 * i + 3]), __NV_SATFINITE, kInterp);
-        w[i] = (lo & 0xFFFFu) | (hi << 16);
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) bad |= !isfinite(x[i]);
-      reinterpret_cast<uint2*>(codes)[v] = make_uint2(w[0], w[1]);
-    }
-  } else if constexpr (SCHEME == HR_S_INT8) {
-    uint32_t* amax = qsm;  // |x| bits per group (non-negative floats order as unsigned)
-    float* scale = reinterpret_cast<float*>(qsm + ng);
-    for (uint32_t g = tid; g < ng; g += kQThreads) amax[g] = 0u;
-    __syncthreads();
-    // a3: a = max |x| per group
-    for (uint32_t v = tid; v < n_vec; v += kQThreads) {
-      float x[8];
-      uint4 raw;
-      load8<DT>(src + 8ull * v, x, raw);
+// segmented reductions over `seg` consecutive lanes (seg a power of two <= 32)
+__device__ __forceinline__ float seg_max(float v, int seg) {
+  for (int o = seg >> 1; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+  return v;
+}
+__device__ __forceinline__ float seg_min(float v, int seg) {
+  for (int o = seg >> 1; o; o >>= 1) v = fminf(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+  return v;
+}
+
+struct Geo {  // slab addressing shared by the kernels
+  const uint16_t* src;
+  uint8_t* codes;
+  uint8_t* meta;
+};
+__device__ __forceinline__ Geo slab_geo(const QuantParams& p, uint32_t slab_i) {
+  const uint32_t l = slab_i / p.Hl, hl = slab_i - l * p.Hl;
+  const uint64_t slab = (uint64_t)p.T * p.D;
+  return {p.src + ((uint64_t)l * p.H + p.h0 + hl) * slab, p.dst + slab_i * p.code_bytes_slab,
+          p.dst + p.meta_offset + slab_i * p.meta_stride};
+}
+
+// ---------------------------------------------------------------- INT8 / INT4 (G <= 256)
+template <int SCHEME, int DT>
+__global__ void __launch_bounds__(kQThreads) quant_group_kernel(QuantParams p) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t slab = (uint64_t)p.T * p.D;
+  const uint64_t chunks_per_slab = slab / kChunk;
+  const uint64_t n_chunks = (uint64_t)p.L * p.Hl * chunks_per_slab;
+  const int seg = (int)(p.G / 8);  // lanes per group
+  bool bad = false;
+  for (uint64_t c = (blockIdx.x * (uint64_t)kQThreads + threadIdx.x) / 32; c < n_chunks;
+       c += (uint64_t)gridDim.x * kQThreads / 32) {
+    const uint32_t slab_i = (uint32_t)(c / chunks_per_slab);
+    const uint32_t e0 = (uint32_t)(c - (uint64_t)slab_i * chunks_per_slab) * kChunk;
+    const Geo g = slab_geo(p, slab_i);
+    const uint32_t e = e0 + lane * 8;
+    float x[8];
+    uint4 raw;
+    load8<DT>(g.src + e, x, raw);
+    bad |= any_nonfinite(x);
+    const uint32_t grp = e / p.G;
+    const bool leader = (lane & (seg - 1)) == 0;
+    if constexpr (SCHEME == HR_S_INT8) {
+      // a3: a = max |x| (exact); s = 1 if a == 0 else fl(a / 127)
       float a = 0.f;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        bad |= !isfinite(x[i]);
-        a = fmaxf(a, fabsf(x[i]));
-      }
-      atomicMax(&amax[(8ull * v) / p.G], __float_as_uint(a));
-    }
-    __syncthreads();
-    // s = 1 if a == 0 else fl(a / 127)
-    const uint32_t rec_words = (uint32_t)(p.meta_stride / 4);
-    for (uint32_t g = tid; g < rec_words; g += kQThreads) {
-      float s = 0.f;
-      if (g < ng) {
-        const float a = __uint_as_float(amax[g]);
-        s = (a == 0.f) ? 1.f : __fdiv_rn(a, 127.f);
-        scale[g] = s;
-      }
-      reinterpret_cast<float*>(meta)[g] = s;  // padding words written as 0
-    }
-    __syncthreads();
-    // a4: q = clamp(rne(fl(x / s)), -127, 127)
-    for (uint32_t v = tid; v < n_vec; v += kQThreads) {
-      float x[8];
-      uint4 raw;
-      load8<DT>(src + 8ull * v, x, raw);
-      const float s = scale[(8ull * v) / p.G];
+      for (int i = 0; i < 8; ++i) a = fmaxf(a, fabsf(x[i]));
+      a = seg_max(a, seg);
+      const float s = (a == 0.f) ? 1.f : __fdiv_rn(a, 127.f);
+      if (leader) reinterpret_cast<float*>(g.meta)[grp] = s;
+      // a4: q = clamp(rne(fl(x / s)), -127, 127)
       uint32_t w[2] = {0u, 0u};
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        int q = __float2int_rn(__fdiv_rn(x[i], s));
-        q = max(-127, min(127, q));
+        const int q = max(-127, min(127, __float2int_rn(__fdiv_rn(x[i], s))));
         w[i >> 2] |= ((uint32_t)q & 0xFFu) << (8 * (i & 3));
       }
-      reinterpret_cast<uint2*>(codes)[v] = make_uint2(w[0], w[1]);
-    }
-  } else if constexpr (SCHEME == HR_S_INT4) {
-    uint32_t* kmin = qsm;
-    uint32_t* kmax = qsm + ng;
-    float* scale = reinterpret_cast<float*>(qsm + 2 * ng);
-    float* minv = reinterpret_cast<float*>(qsm + 3 * ng);
-    for (uint32_t g = tid; g < ng; g += kQThreads) kmin[g] = 0xFFFFFFFFu, kmax[g] = 0u;
-    __syncthreads();
-    for (uint32_t v = tid; v < n_vec; v += kQThreads) {
-      float x[8];
-      uint4 raw;
-      load8<DT>(src + 8ull * v, x, raw);
+      *reinterpret_cast<uint2*>(g.codes + e) = make_uint2(w[0], w[1]);
+    } else {
+      // a3: mn = min + 0, mx = max + 0 (a zero extreme is +0); s = (mx == mn) ? 1 : fl(fl(mx - mn) / 15)
       float mn = x[0], mx = x[0];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        bad |= !isfinite(x[i]);
-        mn = fminf(mn, x[i]);
-        mx = fmaxf(mx, x[i]);
-      }
-      const uint32_t g = (uint32_t)((8ull * v) / p.G);
-      atomicMin(&kmin[g], ord_key(mn));
-      atomicMax(&kmax[g], ord_key(mx));
-    }
-    __syncthreads();
-    const uint32_t rec_words = (uint32_t)(p.meta_stride / 4);
-    for (uint32_t w = tid; w < rec_words; w += kQThreads) {
-      float val = 0.f;
-      const uint32_t g = w >> 1;
-      if (g < ng) {
-        // mn = min + 0, mx = max + 0 (a zero extreme is +0); s = (mx == mn) ? 1 : fl(fl(mx - mn) / 15)
-        const float mn = __fadd_rn(ord_unkey(kmin[g]), 0.f);
-        const float mx = __fadd_rn(ord_unkey(kmax[g]), 0.f);
-        const float s = (mx == mn) ? 1.f : __fdiv_rn(__fsub_rn(mx, mn), 15.f);
-        if ((w & 1) == 0) scale[g] = s, minv[g] = mn;
-        val = (w & 1) ? mn : s;
-      }
-      reinterpret_cast<float*>(meta)[w] = val;
-    }
-    __syncthreads();
-    for (uint32_t v = tid; v < n_vec; v += kQThreads) {
-      float x[8];
-      uint4 raw;
-      load8<DT>(src + 8ull * v, x, raw);
-      const uint32_t g = (uint32_t)((8ull * v) / p.G);
-      const float s = scale[g], mn = minv[g];
+      for (int i = 1; i < 8; ++i) mn = fminf(mn, x[i]), mx = fmaxf(mx, x[i]);
+      mn = __fadd_rn(seg_min(mn, seg), 0.f);
+      mx = __fadd_rn(seg_max(mx, seg), 0.f);
+      const float s = (mx == mn) ? 1.f : __fdiv_rn(__fsub_rn(mx, mn), 15.f);
+      if (leader) reinterpret_cast<float2*>(g.meta)[grp] = make_float2(s, mn);
+      // a4: q = clamp(rne(fl(fl(x - mn) / s)), 0, 15); element 2i -> low nibble (R24)
       uint32_t w = 0u;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        int q = __float2int_rn(__fdiv_rn(__fsub_rn(x[i], mn), s));
-        q = max(0, min(15, q));
-        w |= (uint32_t)q << (4 * i);  // element 2i -> low nibble (R24)
+        const int q = max(0, min(15, __float2int_rn(__fdiv_rn(__fsub_rn(x[i], mn), s))));
+        w |= (uint32_t)q << (4 * i);
       }
-      reinterpret_cast<uint32_t*>(codes)[v] = w;
+      *reinterpret_cast<uint32_t*>(g.codes + e / 2) = w;
     }
-  } else if constexpr (SCHEME == HR_S_GSE8) {
-    int* rng = reinterpret_cast<int*>(qsm);  // [0] = min biased exponent, [1] = max, [2] = lo, [3] = n
-    if (tid == 0) rng[0] = 255, rng[1] = 0;
-    __syncthreads();
-    // a3: exponent range over nonzero normal values (R8, R9)
-    int emin = 255, emax = 0;
-    for (uint32_t v = tid; v < n_vec; v += kQThreads) {
+  }
+  if (bad) atomicOr(p.err, 1);
+}
+
+// ---------------------------------------------------------------- INT8 / INT4 (G > 256): warp per group
+template <int SCHEME, int DT>
+__global__ void __launch_bounds__(kQThreads) quant_biggroup_kernel(QuantParams p) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t slab = (uint64_t)p.T * p.D;
+  const uint32_t groups_per_slab = (uint32_t)(slab / p.G);
+  const uint64_t n_groups = (uint64_t)p.L * p.Hl * groups_per_slab;
+  bool bad = false;
+  for (uint64_t gi = (blockIdx.x * (uint64_t)kQThreads + threadIdx.x) / 32; gi < n_groups;
+       gi += (uint64_t)gridDim.x * kQThreads / 32) {
+    const uint32_t slab_i = (uint32_t)(gi / groups_per_slab);
+    const uint32_t grp = (uint32_t)(gi - (uint64_t)slab_i * groups_per_slab);
+    const Geo g = slab_geo(p, slab_i);
+    const uint32_t base = grp * p.G;
+    float a = 0.f, mn = INFINITY, mx = -INFINITY;
+    for (uint32_t e = base + lane * 8; e < base + p.G; e += kChunk) {  // pass 1: statistics
       float x[8];
       uint4 raw;
-      load8<DT>(src + 8ull * v, x, raw);
+      load8<DT>(g.src + e, x, raw);
+      bad |= any_nonfinite(x);
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        bad |= !isfinite(x[i]);
-        const int ef = (__float_as_uint(x[i]) >> 23) & 0xFF;
-        if (ef != 0) emin = min(emin, ef), emax = max(emax, ef);
+      for (int i = 0; i < 8; ++i) a = fmaxf(a, fabsf(x[i])), mn = fminf(mn, x[i]), mx = fmaxf(mx, x[i]);
+    }
+    float s, m0 = 0.f;
+    if constexpr (SCHEME == HR_S_INT8) {
+      a = seg_max(a, 32);
+      s = (a == 0.f) ? 1.f : __fdiv_rn(a, 127.f);
+      if (lane == 0) reinterpret_cast<float*>(g.meta)[grp] = s;
+    } else {
+      mn = __fadd_rn(seg_min(mn, 32), 0.f);
+      mx = __fadd_rn(seg_max(mx, 32), 0.f);
+      s = (mx == mn) ? 1.f : __fdiv_rn(__fsub_rn(mx, mn), 15.f);
+      m0 = mn;
+      if (lane == 0) reinterpret_cast<float2*>(g.meta)[grp] = make_float2(s, mn);
+    }
+    for (uint32_t e = base + lane * 8; e < base + p.G; e += kChunk) {  // pass 2: encode (L2 re-read)
+      float x[8];
+      uint4 raw;
+      load8<DT>(g.src + e, x, raw);
+      if constexpr (SCHEME == HR_S_INT8) {
+        uint32_t w[2] = {0u, 0u};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int q = max(-127, min(127, __float2int_rn(__fdiv_rn(x[i], s))));
+          w[i >> 2] |= ((uint32_t)q & 0xFFu) << (8 * (i & 3));
+        }
+        *reinterpret_cast<uint2*>(g.codes + e) = make_uint2(w[0], w[1]);
+      } else {
+        uint32_t w = 0u;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int q = max(0, min(15, __float2int_rn(__fdiv_rn(__fsub_rn(x[i], m0), s))));
+          w |= (uint32_t)q << (4 * i);
+        }
+        *reinterpret_cast<uint32_t*>(g.codes + e / 2) = w;
       }
+    }
+  }
+  if (bad) atomicOr(p.err, 1);
+}
+
+// ---------------------------------------------------------------- FP8 / PASS16: elementwise
+template <int SCHEME, int DT>
+__global__ void __launch_bounds__(kQThreads) quant_elementwise_kernel(QuantParams p) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t slab = (uint64_t)p.T * p.D;
+  const uint64_t chunks_per_slab = slab / kChunk;
+  const uint64_t n_chunks = (uint64_t)p.L * p.Hl * chunks_per_slab;
+  bool bad = false;
+  for (uint64_t c = (blockIdx.x * (uint64_t)kQThreads + threadIdx.x) / 32; c < n_chunks;
+       c += (uint64_t)gridDim.x * kQThreads / 32) {
+    const uint32_t slab_i = (uint32_t)(c / chunks_per_slab);
+    const uint32_t e = (uint32_t)(c - (uint64_t)slab_i * chunks_per_slab) * kChunk + lane * 8;
+    const Geo g = slab_geo(p, slab_i);
+    float x[8];
+    uint4 raw;
+    load8<DT>(g.src + e, x, raw);
+    bad |= any_nonfinite(x);
+    if constexpr (SCHEME == HR_S_PASS16) {
+      *reinterpret_cast<uint4*>(g.codes + 2ull * e) = raw;
+    } else {
+      constexpr __nv_fp8_interpretation_t kInterp = SCHEME == HR_S_FP8E4M3 ? __NV_E4M3 : __NV_E5M2;
+      uint32_t w[2];
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {  // nearest code, ties to even, saturating (R5)
+        const uint32_t lo = __nv_cvt_float2_to_fp8x2(make_float2(x[4 * i], x[4 * i + 1]), __NV_SATFINITE, kInterp);
+        const uint32_t hi = __nv_cvt_float2_to_fp8x2(make_float2(x[4 * i + 2], x[4 * i + 3]), __NV_SATFINITE, kInterp);
+        w[i] = (lo & 0xFFFFu) | (hi << 16);
+      }
+      *reinterpret_cast<uint2*>(g.codes + e) = make_uint2(w[0], w[1]);
+    }
+  }
+  if (bad) atomicOr(p.err, 1);
+}
+
+// ---------------------------------------------------------------- GSE-8
+// pass A: per-slab min/max biased exponent over nonzero normal values (R8, R9)
+template <int DT>
+__global__ void __launch_bounds__(kQThreads) gse_range_kernel(QuantParams p) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t slab = (uint64_t)p.T * p.D;
+  const uint64_t chunks_per_slab = slab / kChunk;
+  const uint64_t n_chunks = (uint64_t)p.L * p.Hl * chunks_per_slab;
+  bool bad = false;
+  for (uint64_t c = (blockIdx.x * (uint64_t)kQThreads + threadIdx.x) / 32; c < n_chunks;
+       c += (uint64_t)gridDim.x * kQThreads / 32) {
+    const uint32_t slab_i = (uint32_t)(c / chunks_per_slab);
+    const uint32_t e = (uint32_t)(c - (uint64_t)slab_i * chunks_per_slab) * kChunk + lane * 8;
+    const Geo g = slab_geo(p, slab_i);
+    float x[8];
+    uint4 raw;
+    load8<DT>(g.src + e, x, raw);
+    bad |= any_nonfinite(x);
+    int emin = 255, emax = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int ef = (__float_as_uint(x[i]) >> 23) & 0xFF;
+      if (ef != 0) emin = min(emin, ef), emax = max(emax, ef);
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       emin = min(emin, __shfl_xor_sync(0xFFFFFFFFu, emin, o));
       emax = max(emax, __shfl_xor_sync(0xFFFFFFFFu, emax, o));
     }
-    if ((tid & 31) == 0) atomicMin(&rng[0], emin), atomicMax(&rng[1], emax);
-    __syncthreads();
-    const int step = (int)p.gse_m - 1;
-    const int nmax = 1 << p.gse_e;
-    const bool any = rng[1] != 0;
-    const int Emin = rng[0] - 127, Emax = rng[1] - 127;
-    // P:172 / R6: lo = max(Emin, Emax - (2^e - 1) * step); G_i = min(lo + i*step, Emax)
-    const int lo = max(Emin, Emax - (nmax - 1) * step);
-    const int n = any ? (Emax - lo + step - 1) / step + 1 : 0;
-    // meta record: int8 array [2^e] (unused -128), zero pad to 16 B, then the fp32 decode table
-    // [2^(e+1)]: entry (sign << e | i) = (-1)^sign 2^(G_i - (m-1)) (0 for unused i)
-    for (uint32_t w = tid; w < 16; w += kQThreads) {
-      int v = 0;
-      if ((int)w < nmax) v = ((int)w < n) ? min(lo + (int)w * step, Emax) : -128;
-      meta[w] = (uint8_t)(int8_t)v;
-    }
-    for (uint32_t w = tid; w < (p.meta_stride - 16) / 4; w += kQThreads) {
-      float v = 0.f;
-      const int i = (int)w & (nmax - 1);
-      if ((int)w < 2 * nmax && i < n) {
-        const int k = min(lo + i * step, Emax) - (step);  // G_i - (m-1)
-        v = k >= -126 ? __int_as_float((k + 127) << 23) : (k >= -149 ? __int_as_float(1 << (k + 149)) : 0.f);
-        if ((int)w >= nmax) v = -v;
-      }
-      reinterpret_cast<float*>(meta + 16)[w] = v;
-    }
-    const int m = (int)p.gse_m;
-    for (uint32_t v = tid; v < n_vec; v += kQThreads) {
-      float x[8];
-      uint4 raw;
-      load8<DT>(src + 8ull * v, x, raw);
-      uint32_t w[2] = {0u, 0u};
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const uint32_t b = __float_as_uint(x[i]);
-        const int ef = (b >> 23) & 0xFF;
-        uint32_t byte = 0u;
-        if (ef != 0) {
-          const int E = ef - 127;
-          // smallest shared exponent >= E
-          const int idx = (E <= lo) ? 0 : (E - lo + step - 1) / step;
-          const int G = min(lo + idx * step, Emax);
-          const int d = G - E;
-          if (d <= m - 1) {  // else: below the array's reach, flush (R9)
-            const int keep = m - 1 - d;
-            // marker 1 at position d+1 from the MSB, then the top fraction bits (truncated)
-            const uint32_t field = (1u << keep) | ((b & 0x7FFFFFu) >> (23 - keep));
-            byte = ((b >> 31) << 7) | ((uint32_t)idx << m) | field;
-          }
-        }
-        w[i >> 2] |= byte << (8 * (i & 3));
-      }
-      reinterpret_cast<uint2*>(codes)[v] = make_uint2(w[0], w[1]);
+    if (lane == 0 && emax != 0) {  // range stored as (255 - min, max) so a zero fill initialises it
+      atomicMax(&p.gse_range[2 * slab_i], 255 - emin);
+      atomicMax(&p.gse_range[2 * slab_i + 1], emax);
     }
   }
   if (bad) atomicOr(p.err, 1);
 }
 
-template <int SCHEME>
-void launch_q(const QuantParams& p, cudaStream_t st) {
-  const uint32_t ng = (uint32_t)((uint64_t)p.T * p.D / p.G);
-  size_t smem = SCHEME == HR_S_INT8 ? 8ull * ng : SCHEME == HR_S_INT4 ? 16ull * ng : 16;
-  const dim3 grid(p.L * p.Hl);
-  if (smem > 48 * 1024) {
-    HR_CUDA(cudaFuncSetAttribute(quantize_slab_kernel<SCHEME, HR_BF16>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    HR_CUDA(cudaFuncSetAttribute(quantize_slab_kernel<SCHEME, HR_FP16>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+// pass B: shared-exponent array from the range (R6) and the three steps of P:157-161
+template <int DT>
+__global__ void __launch_bounds__(kQThreads) gse_encode_kernel(QuantParams p) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t slab = (uint64_t)p.T * p.D;
+  const uint64_t chunks_per_slab = slab / kChunk;
+  const uint64_t n_chunks = (uint64_t)p.L * p.Hl * chunks_per_slab;
+  const int step = (int)p.gse_m - 1, m = (int)p.gse_m, nmax = 1 << p.gse_e;
+  for (uint64_t c = (blockIdx.x * (uint64_t)kQThreads + threadIdx.x) / 32; c < n_chunks;
+       c += (uint64_t)gridDim.x * kQThreads / 32) {
+    const uint32_t slab_i = (uint32_t)(c / chunks_per_slab);
+    const uint32_t chunk = (uint32_t)(c - (uint64_t)slab_i * chunks_per_slab);
+    const uint32_t e = chunk * kChunk + lane * 8;
+    const Geo g = slab_geo(p, slab_i);
+    const int rmin = 255 - p.gse_range[2 * slab_i], rmax = p.gse_range[2 * slab_i + 1];
+    const bool any = rmax != 0;
+    const int Emin = rmin - 127, Emax = rmax - 127;
+    // lo = max(Emin, Emax - (2^e - 1) * step); G_i = min(lo + i*step, Emax), i < n
+    const int lo = max(Emin, Emax - (nmax - 1) * step);
+    const int n = any ? (Emax - lo + step - 1) / step + 1 : 0;
+    if (chunk == 0) {
+      // meta record: int8 array [2^e] (unused -128), zero pad to 16 B, then the fp32 decode table
+      // [2^(e+1)]: entry (sign << e | i) = (-1)^sign 2^(G_i - (m-1)), 0 for unused i
+      if (lane < 16) {
+        int v = 0;
+        if ((int)lane < nmax) v = ((int)lane < n) ? min(lo + (int)lane * step, Emax) : -128;
+        g.meta[lane] = (uint8_t)(int8_t)v;
+      }
+      for (uint32_t w = lane; w < (p.meta_stride - 16) / 4; w += 32) {
+        float v = 0.f;
+        const int i = (int)w & (nmax - 1);
+        if ((int)w < 2 * nmax && i < n) {
+          const int k = min(lo + i * step, Emax) - step;
+          v = k >= -126 ? __int_as_float((k + 127) << 23) : (k >= -149 ? __int_as_float(1 << (k + 149)) : 0.f);
+          if ((int)w >= nmax) v = -v;
+        }
+        reinterpret_cast<float*>(g.meta + 16)[w] = v;
+      }
+    }
+    float x[8];
+    uint4 raw;
+    load8<DT>(g.src + e, x, raw);
+    uint32_t w[2] = {0u, 0u};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t b = __float_as_uint(x[i]);
+      const int ef = (b >> 23) & 0xFF;
+      uint32_t byte = 0u;
+      if (ef != 0) {
+        const int E = ef - 127;
+        const int idx = (E <= lo) ? 0 : (E - lo + step - 1) / step;  // smallest G_i >= E
+        const int G = min(lo + idx * step, Emax);
+        const int d = G - E;
+        if (d <= m - 1) {  // else below the array's reach: flush (R9)
+          const int keep = m - 1 - d;
+          // marker 1 at position d+1 from the MSB, then the top fraction bits (truncated)
+          const uint32_t field = (1u << keep) | ((b & 0x7FFFFFu) >> (23 - keep));
+          byte = ((b >> 31) << 7) | ((uint32_t)idx << m) | field;
+        }
+      }
+      w[i >> 2] |= byte << (8 * (i & 3));
+    }
+    *reinterpret_cast<uint2*>(g.codes + e) = make_uint2(w[0], w[1]);
   }
-  if (p.dtype == HR_BF16)
-    quantize_slab_kernel<SCHEME, HR_BF16><<<grid, kQThreads, smem, st>>>(p);
-  else
-    quantize_slab_kernel<SCHEME, HR_FP16><<<grid, kQThreads, smem, st>>>(p);
+}
+
+int g_num_sms = 0;
+int grid_for(uint64_t warps) {
+  if (!g_num_sms) {
+    int dev = 0;
+    HR_CUDA(cudaGetDevice(&dev));
+    HR_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const uint64_t want = (warps * 32 + kQThreads - 1) / kQThreads;
+  const uint64_t cap = (uint64_t)g_num_sms * 8;
+  return (int)(want < cap ? (want ? want : 1) : cap);
+}
+
+template <int DT>
+void launch_dt(const QuantParams& p, cudaStream_t st) {
+  const uint64_t slab = (uint64_t)p.T * p.D;
+  const uint64_t chunks = (uint64_t)p.L * p.Hl * (slab / kChunk);
+  const int grid = grid_for(chunks);
+  switch (p.scheme) {
+    case HR_S_PASS16:
+      quant_elementwise_kernel<HR_S_PASS16, DT><<<grid, kQThreads, 0, st>>>(p);
+      break;
+    case HR_S_FP8E4M3:
+      quant_elementwise_kernel<HR_S_FP8E4M3, DT><<<grid, kQThreads, 0, st>>>(p);
+      break;
+    case HR_S_FP8E5M2:
+      quant_elementwise_kernel<HR_S_FP8E5M2, DT><<<grid, kQThreads, 0, st>>>(p);
+      break;
+    case HR_S_INT8:
+    case HR_S_INT4: {
+      const bool small = p.G <= (uint32_t)kChunk;
+      const uint64_t work = small ? chunks : (uint64_t)p.L * p.Hl * (slab / p.G);
+      const int g = grid_for(work);
+      if (p.scheme == HR_S_INT8) {
+        if (small) quant_group_kernel<HR_S_INT8, DT><<<g, kQThreads, 0, st>>>(p);
+        else quant_biggroup_kernel<HR_S_INT8, DT><<<g, kQThreads, 0, st>>>(p);
+      } else {
+        if (small) quant_group_kernel<HR_S_INT4, DT><<<g, kQThreads, 0, st>>>(p);
+        else quant_biggroup_kernel<HR_S_INT4, DT><<<g, kQThreads, 0, st>>>(p);
+      }
+      break;
+    }
+    case HR_S_GSE8: {
+      const uint64_t n_slabs = (uint64_t)p.L * p.Hl;
+      HR_CUDA(cudaMemsetAsync(p.gse_range, 0, sizeof(int) * 2 * n_slabs, st));
+      gse_range_kernel<DT><<<grid, kQThreads, 0, st>>>(p);
+      gse_encode_kernel<DT><<<grid, kQThreads, 0, st>>>(p);
+      break;
+    }
+    default:
+      fail(HR_EINVAL, "unknown scheme");
+  }
   HR_CUDA(cudaGetLastError());
 }
 
 }  // namespace
 
 void launch_quantize(const QuantParams& p, cudaStream_t st) {
-  switch (p.scheme) {
-    case HR_S_PASS16: return launch_q<HR_S_PASS16>(p, st);
-    case HR_S_INT8: return launch_q<HR_S_INT8>(p, st);
-    case HR_S_FP8E4M3: return launch_q<HR_S_FP8E4M3>(p, st);
-    case HR_S_FP8E5M2: return launch_q<HR_S_FP8E5M2>(p, st);
-    case HR_S_GSE8: return launch_q<HR_S_GSE8>(p, st);
-    case HR_S_INT4: return launch_q<HR_S_INT4>(p, st);
-    default: fail(HR_EINVAL, "unknown scheme");
-  }
+  require(((uint64_t)p.T * p.D) % kChunk == 0, HR_EINVAL, "T*D must be a multiple of 256");
+  if (p.dtype == HR_BF16)
+    launch_dt<HR_BF16>(p, st);
+  else
+    launch_dt<HR_FP16>(p, st);
 }
 
 }  // namespace harag

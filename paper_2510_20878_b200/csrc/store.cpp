@@ -96,6 +96,7 @@ Store::~Store() {
   if (delta) cudaFree(delta);
   if (err_flag) cudaFree(err_flag);
   if (scratch) cudaFree(scratch);
+  if (gse_range) cudaFree(gse_range);
   if (src_k) cudaFree(src_k);
   if (src_v) cudaFree(src_v);
   if (start_ev) cudaEventDestroy(start_ev);
@@ -207,6 +208,7 @@ void Store::build_begin(uint32_t nd, const uint64_t* hot) {
   HR_CUDA(cudaMalloc(&err_flag, sizeof(int)));
   HR_CUDA(cudaMemset(err_flag, 0, sizeof(int)));
   HR_CUDA(cudaMalloc(&scratch, 2 * max_item));
+  HR_CUDA(cudaMalloc(&gse_range, sizeof(int) * 2 * lay.n_slabs()));
   put_done.assign(n_docs, 0);
   backing_filled.clear();
   state = State::Building;
@@ -236,11 +238,10 @@ void Store::build_put(uint32_t doc, const void* k_src, const void* v_src, cudaSt
     q.meta_offset = lay.meta_offset(s);
     q.meta_stride = lay.meta_stride(s);
     q.err = err_flag;
-    // zero the blob's padding so exported blobs are deterministic
+    q.gse_range = gse_range;
+    // zero padding and meta (records may end in padding) so exported blobs are deterministic
     const uint64_t cend = lay.n_slabs() * q.code_bytes_slab;
-    const uint64_t mend = q.meta_offset + lay.n_slabs() * q.meta_stride;
-    if (q.meta_offset > cend) HR_CUDA(cudaMemsetAsync(dst + cend, 0, q.meta_offset - cend, st));
-    if (bytes[item] > mend) HR_CUDA(cudaMemsetAsync(dst + mend, 0, bytes[item] - mend, st));
+    if (bytes[item] > cend) HR_CUDA(cudaMemsetAsync(dst + cend, 0, bytes[item] - cend, st));
     launch_quantize(q, st);
     if (loc[item].backing_off != FreeList::kNone && !backing_filled.count(loc[item].backing_off)) {
       // bench aliasing: a shared blob is written once (its docs have identical sources by contract)

@@ -122,6 +122,7 @@ struct Store {
   int64_t* delta = nullptr;  // device int64[n_items] hotness delta (a1)
   int* err_flag = nullptr;
   uint8_t* scratch = nullptr;  // build: quantised blobs headed for the host
+  int* gse_range = nullptr;    // build: GSE-8 per-slab exponent range scratch
   void* src_k = nullptr;
   void* src_v = nullptr;
   cudaStream_t copy_stream = nullptr;
