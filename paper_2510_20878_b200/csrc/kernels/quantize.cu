@@ -59,6 +59,21 @@ __device__ __forceinline__ bool any_nonfinite(const float (&x)[8]) {
   return bad;
 }
 
+// rne(fl(x / s)) — the quantised code of R3 — without an IEEE division per element.
+// y = RN(1/s) (one division per group); t = RN(x*y) is within |x/s| * 2^-23 <= 2^-16 of x/s
+// (|x/s| <= 128).  fl(x/s) lies within 2^-18 of x/s, so unless t is within 2^-15 of a
+// half-integer, x/s, fl(x/s) and t all round to the same integer; near a half-integer the
+// element falls back to the exact __fdiv_rn.  Valid when s and y are normal (`fast`).
+__device__ __forceinline__ int div_rne(float x, float s, float y, bool fast) {
+  if (fast) {
+    const float t = __fmul_rn(x, y);
+    const float r = rintf(t);
+    if (fabsf(fabsf(__fsub_rn(t, r)) - 0.5f) > 3.0517578125e-05f) return (int)r;
+  }
+  return __float2int_rn(__fdiv_rn(x, s));
+}
+__device__ __forceinline__ bool div_fast_ok(float s) { return s >= 1.17549435e-38f && s <= 8.50705917e+37f; }
+
 // segmented reductions over `seg` consecutive lanes (seg a power of two <= 32)
 __device__ __forceinline__ float seg_max(float v, int seg) {
   for (int o = seg >> 1; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
@@ -111,10 +126,12 @@ __global__ void __launch_bounds__(kQThreads) quant_group_kernel(QuantParams p) {
       const float s = (a == 0.f) ? 1.f : __fdiv_rn(a, 127.f);
       if (leader) reinterpret_cast<float*>(g.meta)[grp] = s;
       // a4: q = clamp(rne(fl(x / s)), -127, 127)
+      const bool fast = div_fast_ok(s);
+      const float y = __fdiv_rn(1.f, s);
       uint32_t w[2] = {0u, 0u};
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const int q = max(-127, min(127, __float2int_rn(__fdiv_rn(x[i], s))));
+        const int q = max(-127, min(127, div_rne(x[i], s, y, fast)));
         w[i >> 2] |= ((uint32_t)q & 0xFFu) << (8 * (i & 3));
       }
       *reinterpret_cast<uint2*>(g.codes + e) = make_uint2(w[0], w[1]);
@@ -128,10 +145,12 @@ __global__ void __launch_bounds__(kQThreads) quant_group_kernel(QuantParams p) {
       const float s = (mx == mn) ? 1.f : __fdiv_rn(__fsub_rn(mx, mn), 15.f);
       if (leader) reinterpret_cast<float2*>(g.meta)[grp] = make_float2(s, mn);
       // a4: q = clamp(rne(fl(fl(x - mn) / s)), 0, 15); element 2i -> low nibble (R24)
+      const bool fast = div_fast_ok(s);
+      const float y = __fdiv_rn(1.f, s);
       uint32_t w = 0u;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const int q = max(0, min(15, __float2int_rn(__fdiv_rn(__fsub_rn(x[i], mn), s))));
+        const int q = max(0, min(15, div_rne(__fsub_rn(x[i], mn), s, y, fast)));
         w |= (uint32_t)q << (4 * i);
       }
       *reinterpret_cast<uint32_t*>(g.codes + e / 2) = w;
@@ -273,13 +292,13 @@ __global__ void __launch_bounds__(kQThreads) gse_range_kernel(QuantParams p) {
 }
 
 // pass B: shared-exponent array from the range (R6) and the three steps of P:157-161
-template <int DT>
+template <int DT, int M>
 __global__ void __launch_bounds__(kQThreads) gse_encode_kernel(QuantParams p) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t slab = (uint64_t)p.T * p.D;
   const uint64_t chunks_per_slab = slab / kChunk;
   const uint64_t n_chunks = (uint64_t)p.L * p.Hl * chunks_per_slab;
-  const int step = (int)p.gse_m - 1, m = (int)p.gse_m, nmax = 1 << p.gse_e;
+  constexpr int step = M - 1, m = M, nmax = 1 << (7 - M);  // compile-time step: no integer division
   for (uint64_t c = (blockIdx.x * (uint64_t)kQThreads + threadIdx.x) / 32; c < n_chunks;
        c += (uint64_t)gridDim.x * kQThreads / 32) {
     const uint32_t slab_i = (uint32_t)(c / chunks_per_slab);
@@ -383,7 +402,12 @@ void launch_dt(const QuantParams& p, cudaStream_t st) {
       const uint64_t n_slabs = (uint64_t)p.L * p.Hl;
       HR_CUDA(cudaMemsetAsync(p.gse_range, 0, sizeof(int) * 2 * n_slabs, st));
       gse_range_kernel<DT><<<grid, kQThreads, 0, st>>>(p);
-      gse_encode_kernel<DT><<<grid, kQThreads, 0, st>>>(p);
+      if (p.gse_m == 3)
+        gse_encode_kernel<DT, 3><<<grid, kQThreads, 0, st>>>(p);
+      else if (p.gse_m == 4)
+        gse_encode_kernel<DT, 4><<<grid, kQThreads, 0, st>>>(p);
+      else
+        gse_encode_kernel<DT, 5><<<grid, kQThreads, 0, st>>>(p);
       break;
     }
     default:

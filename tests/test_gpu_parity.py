@@ -442,3 +442,38 @@ def test_config4_hotness_drift_replacement(torch_cuda):
         want = placement.eager_tiers(hcur, sizes, hb, pb)
         assert [names[st.item_info(i)[1]] for i in range(2 * n_docs)] == want, phase
     assert st.stats()["migrations_in"] > 0
+
+
+@pytest.mark.parametrize("scheme", ["INT8", "INT4"])
+def test_quantize_exact_ties(torch_cuda, scheme):
+    """Groups whose quotients x/s land exactly on half-integers (ties to even)
+    and within a few ulps of them: the GPU's division-free fast path must fall
+    back to the IEEE quotient there (R3) — packed blobs equal the oracle's."""
+    import paper_2510_20878_b200 as hr
+    from oracle import numerics
+    torch = torch_cuda
+    L, H, T, D = 1, 1, 64, 128
+    rng = np.random.default_rng(3)
+    vals = np.empty((T, D), np.float32)
+    for t in range(T):
+        j = int(rng.integers(-20, 10))
+        top = 127 if scheme == "INT8" else 15
+        k = rng.integers(0, top, D).astype(np.float32)
+        row = (k + np.float32(0.5)) * np.float32(2.0 ** j)
+        if t % 2:   # nudge by a few ulps around the tie
+            row = np.nextafter(row, np.float32(np.inf) * rng.choice([-1, 1], D)).astype(np.float32)
+        row[0] = np.float32(top * 2.0 ** j)          # the group's max |x| (INT8) / max (INT4)
+        if scheme == "INT4":
+            row[1] = np.float32(0.0)                  # min = 0 -> s = 2^j exactly
+        if scheme == "INT8" and t % 3 == 0:
+            row = -row
+        vals[t] = row
+    bits = numerics.f32_to_bf16(vals).reshape(L, H, T, D)
+    lay = ost.Layout(L=L, H=H, T=T, D=D)
+    want = ost.encode_item(bits, NAMES[scheme], lay)
+    st = hr.Store(L=L, H=H, D=D, T=T, ladder=(scheme,), taus=(), hbm_budget=1 << 20)
+    src = torch.from_numpy(bits.view(np.int16).reshape(-1).copy()).cuda()
+    st.build_begin(1, np.zeros(2, np.uint64))
+    st.build_put(0, src, src)
+    st.build_end()
+    assert np.array_equal(st.export_item(0), want)
