@@ -51,14 +51,20 @@ def int4_encode(x: np.ndarray):
     """x: float32 [n_groups][G] -> (q uint8 [n_groups][G] in 0..15, s, mn float32).
 
     mn = min(x) + 0 and mx = max(x) + 0 (the +0 makes a zero extreme +0);
-    s = 1 if mx == mn else fl32(fl32(mx - mn) / 15);
-    q = clamp(rne(fl32(fl32(x - mn) / s)), 0, 15).
+    s = 1 if mx == mn else fl32(sub(mx, mn) / 15);
+    q = clamp(rne(fl32(sub(x, mn) / s)), 0, 15),
+    where sub(a, b) = min(fl32(a - b), FLT_MAX): a difference of two finite
+    values that overflows saturates instead of becoming inf (R4).
     """
     x = np.asarray(x, dtype=F32)
+    big = F32(np.finfo(np.float32).max)
     mn = (np.min(x, axis=1) + F32(0.0)).astype(F32)
     mx = (np.max(x, axis=1) + F32(0.0)).astype(F32)
-    s = np.where(mx == mn, F32(1.0), (mx - mn) / F32(15.0)).astype(F32)
-    q = np.rint((x - mn[:, None]) / s[:, None])
+    with np.errstate(over="ignore"):
+        d = np.minimum((mx - mn).astype(F32), big)
+        s = np.where(mx == mn, F32(1.0), d / F32(15.0)).astype(F32)
+        u = np.minimum((x - mn[:, None]).astype(F32), big)
+    q = np.rint(u / s[:, None])
     return np.clip(q, 0, 15).astype(np.uint8), s, mn
 
 

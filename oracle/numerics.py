@@ -31,7 +31,10 @@ def f32_to_bf16(x: np.ndarray) -> np.ndarray:
     hi = (lo.astype(np.uint32) + 1).astype(np.uint16)  # next magnitude, same sign
     xv = x.astype(np.float64)
     dlo = np.abs(xv - bf16_to_f32(lo).astype(np.float64))
-    hv = bf16_to_f32(hi).astype(np.float64)  # may be +-inf at the top: never nearer
+    hv = bf16_to_f32(hi).astype(np.float64)
+    # IEEE overflow: past the largest finite bf16 the next candidate is inf, which
+    # RNE picks from max + ulp/2 on — i.e. treat inf as the value 2^128 here
+    hv = np.where(np.isinf(hv), np.copysign(2.0 ** 128, hv), hv)
     dhi = np.abs(xv - hv)
     take_hi = (dhi < dlo) | ((dhi == dlo) & ((lo & 1) == 1))
     return np.where(take_hi, hi, lo).astype(np.uint16)

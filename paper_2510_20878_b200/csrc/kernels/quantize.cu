@@ -74,6 +74,9 @@ __device__ __forceinline__ int div_rne(float x, float s, float y, bool fast) {
 }
 __device__ __forceinline__ bool div_fast_ok(float s) { return s >= 1.17549435e-38f && s <= 8.50705917e+37f; }
 
+// sub(a, b) of R4: fl(a - b) saturated at FLT_MAX (finite inputs whose difference overflows)
+__device__ __forceinline__ float sub_sat(float a, float b) { return fminf(__fsub_rn(a, b), 3.40282347e+38f); }
+
 // segmented reductions over `seg` consecutive lanes (seg a power of two <= 32)
 __device__ __forceinline__ float seg_max(float v, int seg) {
   for (int o = seg >> 1; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
@@ -142,7 +145,7 @@ __global__ void __launch_bounds__(kQThreads) quant_group_kernel(QuantParams p) {
       for (int i = 1; i < 8; ++i) mn = fminf(mn, x[i]), mx = fmaxf(mx, x[i]);
       mn = __fadd_rn(seg_min(mn, seg), 0.f);
       mx = __fadd_rn(seg_max(mx, seg), 0.f);
-      const float s = (mx == mn) ? 1.f : __fdiv_rn(__fsub_rn(mx, mn), 15.f);
+      const float s = (mx == mn) ? 1.f : __fdiv_rn(sub_sat(mx, mn), 15.f);
       if (leader) reinterpret_cast<float2*>(g.meta)[grp] = make_float2(s, mn);
       // a4: q = clamp(rne(fl(fl(x - mn) / s)), 0, 15); element 2i -> low nibble (R24)
       const bool fast = div_fast_ok(s);
@@ -150,7 +153,7 @@ __global__ void __launch_bounds__(kQThreads) quant_group_kernel(QuantParams p) {
       uint32_t w = 0u;
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const int q = max(0, min(15, div_rne(__fsub_rn(x[i], mn), s, y, fast)));
+        const int q = max(0, min(15, div_rne(sub_sat(x[i], mn), s, y, fast)));
         w |= (uint32_t)q << (4 * i);
       }
       *reinterpret_cast<uint32_t*>(g.codes + e / 2) = w;
@@ -190,7 +193,7 @@ __global__ void __launch_bounds__(kQThreads) quant_biggroup_kernel(QuantParams p
     } else {
       mn = __fadd_rn(seg_min(mn, 32), 0.f);
       mx = __fadd_rn(seg_max(mx, 32), 0.f);
-      s = (mx == mn) ? 1.f : __fdiv_rn(__fsub_rn(mx, mn), 15.f);
+      s = (mx == mn) ? 1.f : __fdiv_rn(sub_sat(mx, mn), 15.f);
       m0 = mn;
       if (lane == 0) reinterpret_cast<float2*>(g.meta)[grp] = make_float2(s, mn);
     }
@@ -210,7 +213,7 @@ __global__ void __launch_bounds__(kQThreads) quant_biggroup_kernel(QuantParams p
         uint32_t w = 0u;
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const int q = max(0, min(15, __float2int_rn(__fdiv_rn(__fsub_rn(x[i], m0), s))));
+          const int q = max(0, min(15, __float2int_rn(__fdiv_rn(sub_sat(x[i], m0), s))));
           w |= (uint32_t)q << (4 * i);
         }
         *reinterpret_cast<uint32_t*>(g.codes + e / 2) = w;

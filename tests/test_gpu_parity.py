@@ -477,3 +477,62 @@ def test_quantize_exact_ties(torch_cuda, scheme):
     st.build_put(0, src, src)
     st.build_end()
     assert np.array_equal(st.export_item(0), want)
+
+
+def _edge_source(dtype, rng, L=2, H=2, T=64, D=128):
+    """Slabs of special values: signed zeros, subnormals, the smallest normal,
+    the largest finite value, FP8 saturation neighbours, all-tiny slabs,
+    all-zero groups, and exponent ranges wider than any GSE-8 array."""
+    n = T * D
+    if dtype == "bf16":
+        special = [0x0000, 0x8000, 0x0001, 0x807F, 0x0080, 0x8080, 0x7F7F, 0xFF7F, 0x43E0, 0x43E1, 0xC3E1,
+                   0x4780, 0x477F, 0x3F80, 0x3F81, 0x0100, 0x2000, 0x6000]
+        rand = lambda k: rng.integers(0, 0x7F80, k).astype(np.uint16) | (rng.integers(0, 2, k) << 15).astype(np.uint16)
+        tiny = lambda k: rng.integers(0, 0x0080, k).astype(np.uint16) | (rng.integers(0, 2, k) << 15).astype(np.uint16)
+        huge = lambda k: rng.integers(0x7B00, 0x7F80, k).astype(np.uint16)
+    else:
+        special = [0x0000, 0x8000, 0x0001, 0x83FF, 0x0400, 0x7BFF, 0xFBFF, 0x5F00, 0x5F08, 0x3C00, 0x3C01, 0x7800]
+        rand = lambda k: rng.integers(0, 0x7C00, k).astype(np.uint16) | (rng.integers(0, 2, k) << 15).astype(np.uint16)
+        tiny = lambda k: rng.integers(0, 0x0400, k).astype(np.uint16)
+        huge = lambda k: rng.integers(0x7000, 0x7C00, k).astype(np.uint16)
+    slabs = []
+    a = rand(n)
+    a[: len(special)] = special
+    a[1024:1152] = 0                                   # an all-zero group (INT8/INT4)
+    a[2048:2176] = tiny(128)                           # a subnormal-only group
+    slabs.append(a)
+    slabs.append(np.where(rng.random(n) < 0.5, 0, tiny(n)).astype(np.uint16))     # only zeros/subnormals
+    h = huge(n)
+    h[::7] = rand(len(h[::7]))
+    slabs.append(h)                                    # huge values + a wide exponent range
+    slabs.append(np.zeros(n, np.uint16))               # all zero
+    return np.stack(slabs).reshape(L, H, T, D)
+
+
+@pytest.mark.parametrize("scheme", list(NAMES))
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+def test_edge_values_bitexact(torch_cuda, scheme, dtype):
+    """Degenerate inputs for every scheme: blobs and decoded outputs equal the oracle's."""
+    import paper_2510_20878_b200 as hr
+    torch = torch_cuda
+    rng = np.random.default_rng(17)
+    L, H, T, D = 2, 2, 64, 128
+    k_bits = _edge_source(dtype, rng)
+    v_bits = _edge_source(dtype, rng)[::-1].copy()
+    lay = ost.Layout(L=L, H=H, T=T, D=D, dtype=dtype)
+    st = hr.Store(L=L, H=H, D=D, T=T, dtype=dtype, ladder=(scheme,), taus=(), hbm_budget=1 << 22)
+    ks = torch.from_numpy(k_bits.view(np.int16).reshape(-1).copy()).cuda()
+    vs = torch.from_numpy(v_bits.view(np.int16).reshape(-1).copy()).cuda()
+    st.build_begin(1, np.zeros(2, np.uint64))
+    st.build_put(0, ks, vs)
+    st.build_end()
+    for item, bits in ((0, k_bits), (1, v_bits)):
+        want_blob = ost.encode_item(bits, NAMES[scheme], lay)
+        assert np.array_equal(st.export_item(item), want_blob), (scheme, dtype, item)
+    ko, vo = alloc_out(torch, st, 1, 1)
+    st.assemble(np.array([[0]]), ko, vo)
+    torch.cuda.synchronize()
+    for out, item in ((ko[0], 0), (vo[0], 1)):
+        want = ost.decode_item(st.export_item(item), NAMES[scheme], lay)
+        got = out.cpu().numpy().view(np.uint16).reshape(want.shape)
+        assert np.array_equal(got, want), (scheme, dtype, item, np.argwhere(got != want)[:4])

@@ -40,6 +40,11 @@ def test_bf16_roundtrip_all_patterns():
     assert np.array_equal(numerics.f32_to_bf16(x), b)
 
 
+def test_bf16_rne_overflow_matches_ieee():
+    big = np.float32([3.3895314e38, 3.3961e38, 3.4028235e38, -3.4028235e38])
+    assert np.array_equal(numerics.f32_to_bf16(big), big.astype(ml_dtypes.bfloat16).view(np.uint16))
+
+
 def test_bf16_rne_vs_library_and_bruteforce():
     rng = np.random.default_rng(1)
     x = (rng.standard_normal(200000) * rng.choice([1e-3, 1, 30, 1e5], 200000)).astype(np.float32)
@@ -107,6 +112,17 @@ def test_int4_constant_group_and_signed_zero():
     assert s[0] == 1.0 and not q.any() and np.all(codecs.int4_decode(q, s, mn) == -3.5)
     q, s, mn = codecs.int4_encode(np.float32([[-0.0, 0.0, 1.0, 2.0]]))
     assert np.signbit(mn[0]) == False  # noqa: E712  (+0 canonical, R4)
+
+
+def test_int4_range_overflow_saturates():
+    """R4: a group spanning (-3e38, 3e38) has an fp32 range that overflows; the
+    difference saturates at FLT_MAX (the extremes take codes 0 and 15) and decoding
+    stays finite."""
+    big = np.float32(3.0e38)
+    q, s, mn = codecs.int4_encode(np.float32([[-big, big, 0.0, -big]]))
+    assert s[0] == np.float32(np.finfo(np.float32).max) / np.float32(15)
+    assert q.tolist() == [[0, 15, 13, 0]]   # 3e38 / (FLT_MAX / 15) = 13.2
+    assert np.all(np.isfinite(codecs.int4_decode(q, s, mn)))
 
 
 def test_int4_bound_and_bruteforce():
