@@ -58,6 +58,7 @@ struct QuantParams {
   const uint16_t* src;       // [L][H][T][D] all heads, source dtype
   uint8_t* dst;              // item blob base
   uint32_t L, H, Hl, h0, T, D, G, gse_e, gse_m, dtype, scheme;
+  uint32_t g_shift;          // log2(G)
   uint64_t code_bytes_slab, meta_offset, meta_stride;
   int* err;                  // set to 1 on NaN/Inf
   int* gse_range;            // device scratch int[2 * L * Hl] (GSE-8 per-slab exponent range)

@@ -59,20 +59,30 @@ __device__ __forceinline__ bool any_nonfinite(const float (&x)[8]) {
   return bad;
 }
 
-// rne(fl(x / s)) — the quantised code of R3 — without an IEEE division per element.
-// y = RN(1/s) (one division per group); t = RN(x*y) is within |x/s| * 2^-23 <= 2^-16 of x/s
-// (|x/s| <= 128).  fl(x/s) lies within 2^-18 of x/s, so unless t is within 2^-15 of a
-// half-integer, x/s, fl(x/s) and t all round to the same integer; near a half-integer the
-// element falls back to the exact __fdiv_rn.  Valid when s and y are normal (`fast`).
-__device__ __forceinline__ int div_rne(float x, float s, float y, bool fast) {
-  if (fast) {
-    const float t = __fmul_rn(x, y);
-    const float r = rintf(t);
-    if (fabsf(fabsf(__fsub_rn(t, r)) - 0.5f) > 3.0517578125e-05f) return (int)r;
+// rne(fl(x / s)) for 8 elements of one group — the quantised codes of R3 — without an IEEE
+// division per element.  y = rcp.approx(s) has relative error <= 2^-23, so t = RN(x*y) is within
+// |x/s| * 1.5 * 2^-23 <= 1.5 * 2^-16 of x/s (|x/s| <= 128), and fl(x/s) within 2^-18 of x/s:
+// unless t lies within 2^-15 of a half-integer, x/s, fl(x/s) and t round to the same integer.
+// If any lane of the warp sees such a near-tie (or s / y are not normal), the warp recomputes
+// with the exact __fdiv_rn (rare; warp-uniform branch).
+__device__ __forceinline__ void div_rne8(const float (&x)[8], float s, int (&q)[8]) {
+  float y;
+  asm("rcp.approx.f32 %0, %1;" : "=f"(y) : "f"(s));
+  bool need = !(s >= 1.17549435e-38f && s <= 8.50705917e+37f);
+  float r[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float t = __fmul_rn(x[i], y);
+    r[i] = rintf(t);
+    need |= fabsf(fabsf(__fsub_rn(t, r[i])) - 0.5f) <= 3.0517578125e-05f;
   }
-  return __float2int_rn(__fdiv_rn(x, s));
+  if (__any_sync(0xFFFFFFFFu, need)) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) r[i] = rintf(__fdiv_rn(x[i], s));
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) q[i] = (int)r[i];
 }
-__device__ __forceinline__ bool div_fast_ok(float s) { return s >= 1.17549435e-38f && s <= 8.50705917e+37f; }
 
 // sub(a, b) of R4: fl(a - b) saturated at FLT_MAX (finite inputs whose difference overflows)
 __device__ __forceinline__ float sub_sat(float a, float b) { return fminf(__fsub_rn(a, b), 3.40282347e+38f); }
@@ -99,65 +109,100 @@ __device__ __forceinline__ Geo slab_geo(const QuantParams& p, uint32_t slab_i) {
           p.dst + p.meta_offset + slab_i * p.meta_stride};
 }
 
+// Blocked distribution: warp w of the grid owns chunks [n*w/W, n*(w+1)/W) and walks them in
+// order, advancing (slab, offset) without divisions; the next chunk's load is issued before the
+// current chunk is encoded (two 16-byte loads in flight per lane).
+struct Walker {
+  uint32_t c, c1, slab_i, e0, cps;
+  Geo g;
+  __device__ __forceinline__ void init(const QuantParams& p) {
+    const uint32_t n = p.L * p.Hl * (p.T * p.D / kChunk);
+    const uint32_t warps = gridDim.x * (kQThreads / 32);
+    const uint32_t w = blockIdx.x * (kQThreads / 32) + threadIdx.x / 32;
+    cps = p.T * p.D / kChunk;
+    c = (uint32_t)((uint64_t)n * w / warps);
+    c1 = (uint32_t)((uint64_t)n * (w + 1) / warps);
+    slab_i = c / cps;
+    e0 = (c - slab_i * cps) * kChunk;
+    g = slab_geo(p, slab_i);
+  }
+  __device__ __forceinline__ bool more() const { return c < c1; }
+  __device__ __forceinline__ void next(const QuantParams& p) {
+    ++c;
+    e0 += kChunk;
+    if (e0 == cps * kChunk && c < c1) {
+      e0 = 0;
+      g = slab_geo(p, ++slab_i);
+    }
+  }
+};
+
 // ---------------------------------------------------------------- INT8 / INT4 (G <= 256)
+template <int SCHEME>
+__device__ __forceinline__ void encode_group_chunk(const QuantParams& p, const Geo& g, uint32_t e, const float (&x)[8],
+                                                   uint32_t lane) {
+  const int seg = (int)(p.G >> 3);  // lanes per group (G/8)
+  const uint32_t grp = e >> p.g_shift;
+  const bool leader = (lane & (seg - 1)) == 0;
+  int q[8];
+  if constexpr (SCHEME == HR_S_INT8) {
+    // a3: a = max |x| (exact); s = 1 if a == 0 else fl(a / 127)
+    float a = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a = fmaxf(a, fabsf(x[i]));
+    a = seg_max(a, seg);
+    const float s = (a == 0.f) ? 1.f : __fdiv_rn(a, 127.f);
+    if (leader) reinterpret_cast<float*>(g.meta)[grp] = s;
+    // a4: q = clamp(rne(fl(x / s)), -127, 127)
+    div_rne8(x, s, q);
+    uint32_t w[2] = {0u, 0u};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w[i >> 2] |= ((uint32_t)max(-127, min(127, q[i])) & 0xFFu) << (8 * (i & 3));
+    *reinterpret_cast<uint2*>(g.codes + e) = make_uint2(w[0], w[1]);
+  } else {
+    // a3: mn = min + 0, mx = max + 0 (a zero extreme is +0); s = (mx == mn) ? 1 : fl(sub(mx, mn) / 15)
+    float mn = x[0], mx = x[0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i) mn = fminf(mn, x[i]), mx = fmaxf(mx, x[i]);
+    mn = __fadd_rn(seg_min(mn, seg), 0.f);
+    mx = __fadd_rn(seg_max(mx, seg), 0.f);
+    const float s = (mx == mn) ? 1.f : __fdiv_rn(sub_sat(mx, mn), 15.f);
+    if (leader) reinterpret_cast<float2*>(g.meta)[grp] = make_float2(s, mn);
+    // a4: q = clamp(rne(fl(sub(x, mn) / s)), 0, 15); element 2i -> low nibble (R24)
+    float u[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) u[i] = sub_sat(x[i], mn);
+    div_rne8(u, s, q);
+    uint32_t w = 0u;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) w |= (uint32_t)max(0, min(15, q[i])) << (4 * i);
+    *reinterpret_cast<uint32_t*>(g.codes + e / 2) = w;
+  }
+}
+
 template <int SCHEME, int DT>
 __global__ void __launch_bounds__(kQThreads) quant_group_kernel(QuantParams p) {
   const uint32_t lane = threadIdx.x & 31;
-  const uint64_t slab = (uint64_t)p.T * p.D;
-  const uint64_t chunks_per_slab = slab / kChunk;
-  const uint64_t n_chunks = (uint64_t)p.L * p.Hl * chunks_per_slab;
-  const int seg = (int)(p.G / 8);  // lanes per group
+  Walker wk;
+  wk.init(p);
   bool bad = false;
-  for (uint64_t c = (blockIdx.x * (uint64_t)kQThreads + threadIdx.x) / 32; c < n_chunks;
-       c += (uint64_t)gridDim.x * kQThreads / 32) {
-    const uint32_t slab_i = (uint32_t)(c / chunks_per_slab);
-    const uint32_t e0 = (uint32_t)(c - (uint64_t)slab_i * chunks_per_slab) * kChunk;
-    const Geo g = slab_geo(p, slab_i);
-    const uint32_t e = e0 + lane * 8;
-    float x[8];
-    uint4 raw;
-    load8<DT>(g.src + e, x, raw);
+  if (!wk.more()) return;
+  float x[8];
+  uint4 raw;
+  load8<DT>(wk.g.src + wk.e0 + lane * 8, x, raw);
+  while (true) {
+    const Geo g = wk.g;
+    const uint32_t e = wk.e0 + lane * 8;
+    wk.next(p);
+    float xn[8];
+    uint4 rn;
+    const bool has_next = wk.more();
+    if (has_next) load8<DT>(wk.g.src + wk.e0 + lane * 8, xn, rn);
     bad |= any_nonfinite(x);
-    const uint32_t grp = e / p.G;
-    const bool leader = (lane & (seg - 1)) == 0;
-    if constexpr (SCHEME == HR_S_INT8) {
-      // a3: a = max |x| (exact); s = 1 if a == 0 else fl(a / 127)
-      float a = 0.f;
+    encode_group_chunk<SCHEME>(p, g, e, x, lane);
+    if (!has_next) break;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) a = fmaxf(a, fabsf(x[i]));
-      a = seg_max(a, seg);
-      const float s = (a == 0.f) ? 1.f : __fdiv_rn(a, 127.f);
-      if (leader) reinterpret_cast<float*>(g.meta)[grp] = s;
-      // a4: q = clamp(rne(fl(x / s)), -127, 127)
-      const bool fast = div_fast_ok(s);
-      const float y = __fdiv_rn(1.f, s);
-      uint32_t w[2] = {0u, 0u};
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int q = max(-127, min(127, div_rne(x[i], s, y, fast)));
-        w[i >> 2] |= ((uint32_t)q & 0xFFu) << (8 * (i & 3));
-      }
-      *reinterpret_cast<uint2*>(g.codes + e) = make_uint2(w[0], w[1]);
-    } else {
-      // a3: mn = min + 0, mx = max + 0 (a zero extreme is +0); s = (mx == mn) ? 1 : fl(fl(mx - mn) / 15)
-      float mn = x[0], mx = x[0];
-#pragma unroll
-      for (int i = 1; i < 8; ++i) mn = fminf(mn, x[i]), mx = fmaxf(mx, x[i]);
-      mn = __fadd_rn(seg_min(mn, seg), 0.f);
-      mx = __fadd_rn(seg_max(mx, seg), 0.f);
-      const float s = (mx == mn) ? 1.f : __fdiv_rn(sub_sat(mx, mn), 15.f);
-      if (leader) reinterpret_cast<float2*>(g.meta)[grp] = make_float2(s, mn);
-      // a4: q = clamp(rne(fl(fl(x - mn) / s)), 0, 15); element 2i -> low nibble (R24)
-      const bool fast = div_fast_ok(s);
-      const float y = __fdiv_rn(1.f, s);
-      uint32_t w = 0u;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int q = max(0, min(15, div_rne(sub_sat(x[i], mn), s, y, fast)));
-        w |= (uint32_t)q << (4 * i);
-      }
-      *reinterpret_cast<uint32_t*>(g.codes + e / 2) = w;
-    }
+    for (int i = 0; i < 8; ++i) x[i] = xn[i];
   }
   if (bad) atomicOr(p.err, 1);
 }
@@ -201,21 +246,21 @@ __global__ void __launch_bounds__(kQThreads) quant_biggroup_kernel(QuantParams p
       float x[8];
       uint4 raw;
       load8<DT>(g.src + e, x, raw);
+      int q[8];
       if constexpr (SCHEME == HR_S_INT8) {
+        div_rne8(x, s, q);
         uint32_t w[2] = {0u, 0u};
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int q = max(-127, min(127, __float2int_rn(__fdiv_rn(x[i], s))));
-          w[i >> 2] |= ((uint32_t)q & 0xFFu) << (8 * (i & 3));
-        }
+        for (int i = 0; i < 8; ++i) w[i >> 2] |= ((uint32_t)max(-127, min(127, q[i])) & 0xFFu) << (8 * (i & 3));
         *reinterpret_cast<uint2*>(g.codes + e) = make_uint2(w[0], w[1]);
       } else {
+        float u[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) u[i] = sub_sat(x[i], m0);
+        div_rne8(u, s, q);
         uint32_t w = 0u;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int q = max(0, min(15, __float2int_rn(__fdiv_rn(sub_sat(x[i], m0), s))));
-          w |= (uint32_t)q << (4 * i);
-        }
+        for (int i = 0; i < 8; ++i) w |= (uint32_t)max(0, min(15, q[i])) << (4 * i);
         *reinterpret_cast<uint32_t*>(g.codes + e / 2) = w;
       }
     }
@@ -227,21 +272,17 @@ __global__ void __launch_bounds__(kQThreads) quant_biggroup_kernel(QuantParams p
 template <int SCHEME, int DT>
 __global__ void __launch_bounds__(kQThreads) quant_elementwise_kernel(QuantParams p) {
   const uint32_t lane = threadIdx.x & 31;
-  const uint64_t slab = (uint64_t)p.T * p.D;
-  const uint64_t chunks_per_slab = slab / kChunk;
-  const uint64_t n_chunks = (uint64_t)p.L * p.Hl * chunks_per_slab;
+  Walker wk;
+  wk.init(p);
   bool bad = false;
-  for (uint64_t c = (blockIdx.x * (uint64_t)kQThreads + threadIdx.x) / 32; c < n_chunks;
-       c += (uint64_t)gridDim.x * kQThreads / 32) {
-    const uint32_t slab_i = (uint32_t)(c / chunks_per_slab);
-    const uint32_t e = (uint32_t)(c - (uint64_t)slab_i * chunks_per_slab) * kChunk + lane * 8;
-    const Geo g = slab_geo(p, slab_i);
+  for (; wk.more(); wk.next(p)) {
+    const uint32_t e = wk.e0 + lane * 8;
     float x[8];
     uint4 raw;
-    load8<DT>(g.src + e, x, raw);
+    load8<DT>(wk.g.src + e, x, raw);
     bad |= any_nonfinite(x);
     if constexpr (SCHEME == HR_S_PASS16) {
-      *reinterpret_cast<uint4*>(g.codes + 2ull * e) = raw;
+      *reinterpret_cast<uint4*>(wk.g.codes + 2ull * e) = raw;
     } else {
       constexpr __nv_fp8_interpretation_t kInterp = SCHEME == HR_S_FP8E4M3 ? __NV_E4M3 : __NV_E5M2;
       uint32_t w[2];
@@ -251,7 +292,7 @@ __global__ void __launch_bounds__(kQThreads) quant_elementwise_kernel(QuantParam
         const uint32_t hi = __nv_cvt_float2_to_fp8x2(make_float2(x[4 * i + 2], x[4 * i + 3]), __NV_SATFINITE, kInterp);
         w[i] = (lo & 0xFFFFu) | (hi << 16);
       }
-      *reinterpret_cast<uint2*>(g.codes + e) = make_uint2(w[0], w[1]);
+      *reinterpret_cast<uint2*>(wk.g.codes + e) = make_uint2(w[0], w[1]);
     }
   }
   if (bad) atomicOr(p.err, 1);
@@ -262,35 +303,37 @@ __global__ void __launch_bounds__(kQThreads) quant_elementwise_kernel(QuantParam
 template <int DT>
 __global__ void __launch_bounds__(kQThreads) gse_range_kernel(QuantParams p) {
   const uint32_t lane = threadIdx.x & 31;
-  const uint64_t slab = (uint64_t)p.T * p.D;
-  const uint64_t chunks_per_slab = slab / kChunk;
-  const uint64_t n_chunks = (uint64_t)p.L * p.Hl * chunks_per_slab;
+  Walker wk;
+  wk.init(p);
+  const bool any_chunk = wk.more();
   bool bad = false;
-  for (uint64_t c = (blockIdx.x * (uint64_t)kQThreads + threadIdx.x) / 32; c < n_chunks;
-       c += (uint64_t)gridDim.x * kQThreads / 32) {
-    const uint32_t slab_i = (uint32_t)(c / chunks_per_slab);
-    const uint32_t e = (uint32_t)(c - (uint64_t)slab_i * chunks_per_slab) * kChunk + lane * 8;
-    const Geo g = slab_geo(p, slab_i);
-    float x[8];
-    uint4 raw;
-    load8<DT>(g.src + e, x, raw);
-    bad |= any_nonfinite(x);
-    int emin = 255, emax = 0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int ef = (__float_as_uint(x[i]) >> 23) & 0xFF;
-      if (ef != 0) emin = min(emin, ef), emax = max(emax, ef);
-    }
+  int emin = 255, emax = 0;
+  uint32_t cur = wk.slab_i;
+  auto flush = [&](uint32_t slab_i) {  // warp-reduce and publish the running range of one slab
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
       emin = min(emin, __shfl_xor_sync(0xFFFFFFFFu, emin, o));
       emax = max(emax, __shfl_xor_sync(0xFFFFFFFFu, emax, o));
     }
-    if (lane == 0 && emax != 0) {  // range stored as (255 - min, max) so a zero fill initialises it
+    if (lane == 0 && emax != 0) {  // stored as (255 - min, max) so a zero fill initialises it
       atomicMax(&p.gse_range[2 * slab_i], 255 - emin);
       atomicMax(&p.gse_range[2 * slab_i + 1], emax);
     }
+    emin = 255, emax = 0;
+  };
+  for (; wk.more(); wk.next(p)) {
+    if (wk.slab_i != cur) flush(cur), cur = wk.slab_i;
+    float x[8];
+    uint4 raw;
+    load8<DT>(wk.g.src + wk.e0 + lane * 8, x, raw);
+    bad |= any_nonfinite(x);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int ef = (__float_as_uint(x[i]) >> 23) & 0xFF;
+      if (ef != 0) emin = min(emin, ef), emax = max(emax, ef);
+    }
   }
+  if (any_chunk) flush(cur);
   if (bad) atomicOr(p.err, 1);
 }
 
@@ -298,23 +341,25 @@ __global__ void __launch_bounds__(kQThreads) gse_range_kernel(QuantParams p) {
 template <int DT, int M>
 __global__ void __launch_bounds__(kQThreads) gse_encode_kernel(QuantParams p) {
   const uint32_t lane = threadIdx.x & 31;
-  const uint64_t slab = (uint64_t)p.T * p.D;
-  const uint64_t chunks_per_slab = slab / kChunk;
-  const uint64_t n_chunks = (uint64_t)p.L * p.Hl * chunks_per_slab;
   constexpr int step = M - 1, m = M, nmax = 1 << (7 - M);  // compile-time step: no integer division
-  for (uint64_t c = (blockIdx.x * (uint64_t)kQThreads + threadIdx.x) / 32; c < n_chunks;
-       c += (uint64_t)gridDim.x * kQThreads / 32) {
-    const uint32_t slab_i = (uint32_t)(c / chunks_per_slab);
-    const uint32_t chunk = (uint32_t)(c - (uint64_t)slab_i * chunks_per_slab);
-    const uint32_t e = chunk * kChunk + lane * 8;
-    const Geo g = slab_geo(p, slab_i);
-    const int rmin = 255 - p.gse_range[2 * slab_i], rmax = p.gse_range[2 * slab_i + 1];
-    const bool any = rmax != 0;
-    const int Emin = rmin - 127, Emax = rmax - 127;
-    // lo = max(Emin, Emax - (2^e - 1) * step); G_i = min(lo + i*step, Emax), i < n
-    const int lo = max(Emin, Emax - (nmax - 1) * step);
-    const int n = any ? (Emax - lo + step - 1) / step + 1 : 0;
-    if (chunk == 0) {
+  Walker wk;
+  wk.init(p);
+  uint32_t cur = 0xFFFFFFFFu;
+  int lo = 0, n = 0, Emax = 0;
+  for (; wk.more(); wk.next(p)) {
+    const Geo& g = wk.g;
+    const uint32_t e = wk.e0 + lane * 8;
+    if (wk.slab_i != cur) {
+      cur = wk.slab_i;
+      const int rmin = 255 - p.gse_range[2 * cur], rmax = p.gse_range[2 * cur + 1];
+      const bool any = rmax != 0;
+      const int Emin = rmin - 127;
+      Emax = rmax - 127;
+      // lo = max(Emin, Emax - (2^e - 1) * step); G_i = min(lo + i*step, Emax), i < n
+      lo = max(Emin, Emax - (nmax - 1) * step);
+      n = any ? (Emax - lo + step - 1) / step + 1 : 0;
+    }
+    if (wk.e0 == 0) {
       // meta record: int8 array [2^e] (unused -128), zero pad to 16 B, then the fp32 decode table
       // [2^(e+1)]: entry (sign << e | i) = (-1)^sign 2^(G_i - (m-1)), 0 for unused i
       if (lane < 16) {

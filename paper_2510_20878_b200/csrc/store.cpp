@@ -234,6 +234,7 @@ void Store::build_put(uint32_t doc, const void* k_src, const void* v_src, cudaSt
     q.dst = dst;
     q.L = lay.L, q.H = lay.H, q.Hl = lay.Hl, q.h0 = lay.h0, q.T = lay.T, q.D = lay.D, q.G = lay.G;
     q.gse_e = lay.gse_e, q.gse_m = lay.gse_m, q.dtype = lay.dtype, q.scheme = s;
+    q.g_shift = (uint32_t)__builtin_ctz(lay.G);
     q.code_bytes_slab = lay.code_bytes_slab(s);
     q.meta_offset = lay.meta_offset(s);
     q.meta_stride = lay.meta_stride(s);
