@@ -138,20 +138,57 @@ struct Walker {
 };
 
 // ---------------------------------------------------------------- INT8 / INT4 (G <= 256)
-template <int SCHEME>
+// fl(a / 127) for the INT8 scale without a division: q0 = RN(a * y), y = RN(1/127); the residual
+// r = a - 127*q0 is exact (one FMA) and RN(q0 + r*y) is the correctly rounded quotient (Markstein's
+// correction).  a is always a 16-bit source value, so the identity is checked against __fdiv_rn for
+// every finite bf16 and fp16 magnitude by tests/test_gpu_parity.py::test_int8_scale_all_16bit_values;
+// tiny a (below 2^-100) takes the IEEE division.
+__device__ __forceinline__ float div127(float a) {
+  constexpr float y = 0.007874015718698501587f;  // RN(1/127)
+  if (a < 7.8886090522101181e-31f) return __fdiv_rn(a, 127.f);
+  const float q0 = __fmul_rn(a, y);
+  const float r = __fmaf_rn(-q0, 127.f, a);
+  return __fmaf_rn(r, y, q0);
+}
+
+template <int SEG>
+__device__ __forceinline__ uint32_t seg_max_u32(uint32_t v) {
+#pragma unroll
+  for (int o = SEG >> 1; o; o >>= 1) v = max(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+  return v;
+}
+template <int SEG>
+__device__ __forceinline__ float seg_min_f(float v) {
+#pragma unroll
+  for (int o = SEG >> 1; o; o >>= 1) v = fminf(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+  return v;
+}
+template <int SEG>
+__device__ __forceinline__ float seg_max_f(float v) {
+#pragma unroll
+  for (int o = SEG >> 1; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+  return v;
+}
+
+// largest |x| bit pattern of the 8 16-bit values (magnitude order == integer order, NaN/Inf on top)
+__device__ __forceinline__ uint32_t absmax_bits(const uint4& raw) {
+  const uint32_t m = 0x7FFF7FFFu;
+  const uint32_t v = __vmaxu2(__vmaxu2(raw.x & m, raw.y & m), __vmaxu2(raw.z & m, raw.w & m));
+  return max(v & 0xFFFFu, v >> 16);
+}
+
+template <int SCHEME, int SEG, int DT>
 __device__ __forceinline__ void encode_group_chunk(const QuantParams& p, const Geo& g, uint32_t e, const float (&x)[8],
-                                                   uint32_t lane) {
-  const int seg = (int)(p.G >> 3);  // lanes per group (G/8)
+                                                   const uint4& raw, uint32_t lane, bool& bad) {
   const uint32_t grp = e >> p.g_shift;
-  const bool leader = (lane & (seg - 1)) == 0;
+  const bool leader = (lane & (SEG - 1)) == 0;
   int q[8];
   if constexpr (SCHEME == HR_S_INT8) {
-    // a3: a = max |x| (exact); s = 1 if a == 0 else fl(a / 127)
-    float a = 0.f;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) a = fmaxf(a, fabsf(x[i]));
-    a = seg_max(a, seg);
-    const float s = (a == 0.f) ? 1.f : __fdiv_rn(a, 127.f);
+    // a3: a = max |x| (exact: the largest magnitude bit pattern); s = 1 if a == 0 else fl(a / 127)
+    const uint32_t ab = seg_max_u32<SEG>(absmax_bits(raw));
+    bad |= ab >= (DT == HR_BF16 ? 0x7F80u : 0x7C00u);  // NaN/Inf in the group
+    const float a = to_f32<DT>(ab);
+    const float s = (a == 0.f) ? 1.f : div127(a);
     if (leader) reinterpret_cast<float*>(g.meta)[grp] = s;
     // a4: q = clamp(rne(fl(x / s)), -127, 127)
     div_rne8(x, s, q);
@@ -160,12 +197,13 @@ __device__ __forceinline__ void encode_group_chunk(const QuantParams& p, const G
     for (int i = 0; i < 8; ++i) w[i >> 2] |= ((uint32_t)max(-127, min(127, q[i])) & 0xFFu) << (8 * (i & 3));
     *reinterpret_cast<uint2*>(g.codes + e) = make_uint2(w[0], w[1]);
   } else {
+    bad |= any_nonfinite(x);
     // a3: mn = min + 0, mx = max + 0 (a zero extreme is +0); s = (mx == mn) ? 1 : fl(sub(mx, mn) / 15)
     float mn = x[0], mx = x[0];
 #pragma unroll
     for (int i = 1; i < 8; ++i) mn = fminf(mn, x[i]), mx = fmaxf(mx, x[i]);
-    mn = __fadd_rn(seg_min(mn, seg), 0.f);
-    mx = __fadd_rn(seg_max(mx, seg), 0.f);
+    mn = __fadd_rn(seg_min_f<SEG>(mn), 0.f);
+    mx = __fadd_rn(seg_max_f<SEG>(mx), 0.f);
     const float s = (mx == mn) ? 1.f : __fdiv_rn(sub_sat(mx, mn), 15.f);
     if (leader) reinterpret_cast<float2*>(g.meta)[grp] = make_float2(s, mn);
     // a4: q = clamp(rne(fl(sub(x, mn) / s)), 0, 15); element 2i -> low nibble (R24)
@@ -180,7 +218,7 @@ __device__ __forceinline__ void encode_group_chunk(const QuantParams& p, const G
   }
 }
 
-template <int SCHEME, int DT>
+template <int SCHEME, int SEG, int DT>
 __global__ void __launch_bounds__(kQThreads) quant_group_kernel(QuantParams p) {
   const uint32_t lane = threadIdx.x & 31;
   Walker wk;
@@ -198,11 +236,11 @@ __global__ void __launch_bounds__(kQThreads) quant_group_kernel(QuantParams p) {
     uint4 rn;
     const bool has_next = wk.more();
     if (has_next) load8<DT>(wk.g.src + wk.e0 + lane * 8, xn, rn);
-    bad |= any_nonfinite(x);
-    encode_group_chunk<SCHEME>(p, g, e, x, lane);
+    encode_group_chunk<SCHEME, SEG, DT>(p, g, e, x, raw, lane, bad);
     if (!has_next) break;
 #pragma unroll
     for (int i = 0; i < 8; ++i) x[i] = xn[i];
+    raw = rn;
   }
   if (bad) atomicOr(p.err, 1);
 }
@@ -233,7 +271,7 @@ __global__ void __launch_bounds__(kQThreads) quant_biggroup_kernel(QuantParams p
     float s, m0 = 0.f;
     if constexpr (SCHEME == HR_S_INT8) {
       a = seg_max(a, 32);
-      s = (a == 0.f) ? 1.f : __fdiv_rn(a, 127.f);
+      s = (a == 0.f) ? 1.f : div127(a);
       if (lane == 0) reinterpret_cast<float*>(g.meta)[grp] = s;
     } else {
       mn = __fadd_rn(seg_min(mn, 32), 0.f);
@@ -437,12 +475,19 @@ void launch_dt(const QuantParams& p, cudaStream_t st) {
       const bool small = p.G <= (uint32_t)kChunk;
       const uint64_t work = small ? chunks : (uint64_t)p.L * p.Hl * (slab / p.G);
       const int g = grid_for(work);
-      if (p.scheme == HR_S_INT8) {
-        if (small) quant_group_kernel<HR_S_INT8, DT><<<g, kQThreads, 0, st>>>(p);
-        else quant_biggroup_kernel<HR_S_INT8, DT><<<g, kQThreads, 0, st>>>(p);
+      if (small) {
+        switch ((p.G >> 3) * 16 + (p.scheme == HR_S_INT8 ? 0 : 1)) {
+#define QG(SEGV)                                                                   \
+  case SEGV * 16 + 0: quant_group_kernel<HR_S_INT8, SEGV, DT><<<g, kQThreads, 0, st>>>(p); break; \
+  case SEGV * 16 + 1: quant_group_kernel<HR_S_INT4, SEGV, DT><<<g, kQThreads, 0, st>>>(p); break;
+          QG(4) QG(8) QG(16) QG(32)
+#undef QG
+          default: fail(HR_EINVAL, "group size must be a power of two >= 32");
+        }
+      } else if (p.scheme == HR_S_INT8) {
+        quant_biggroup_kernel<HR_S_INT8, DT><<<g, kQThreads, 0, st>>>(p);
       } else {
-        if (small) quant_group_kernel<HR_S_INT4, DT><<<g, kQThreads, 0, st>>>(p);
-        else quant_biggroup_kernel<HR_S_INT4, DT><<<g, kQThreads, 0, st>>>(p);
+        quant_biggroup_kernel<HR_S_INT4, DT><<<g, kQThreads, 0, st>>>(p);
       }
       break;
     }

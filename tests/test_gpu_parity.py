@@ -536,3 +536,37 @@ def test_edge_values_bitexact(torch_cuda, scheme, dtype):
         want = ost.decode_item(st.export_item(item), NAMES[scheme], lay)
         got = out.cpu().numpy().view(np.uint16).reshape(want.shape)
         assert np.array_equal(got, want), (scheme, dtype, item, np.argwhere(got != want)[:4])
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+def test_int8_scale_all_16bit_values(torch_cuda, dtype):
+    """The INT8 scale fl(a/127) is computed without a division (Markstein
+    correction); a is a 16-bit source value, so checking every
+    finite magnitude covers its whole domain: one group of G = 32 per value
+    (value first, zeros after), scales and codes equal the oracle's."""
+    import paper_2510_20878_b200 as hr
+    torch = torch_cuda
+    top = 0x7F7F if dtype == "bf16" else 0x7BFF
+    mags = np.arange(0, top + 1, dtype=np.uint32).astype(np.uint16)
+    n = mags.size
+    pad = (-n) % 8                       # whole 256-element chunks: T*D % 256 == 0
+    vals = np.concatenate([mags, np.zeros(pad, np.uint16)])
+    groups = np.zeros((vals.size, 32), np.uint16)
+    groups[:, 0] = vals
+    groups[::3, 0] |= 0x8000             # negative maxima too
+    groups[:, 5] = vals >> 1              # a smaller magnitude in the group
+    L, H, D = 1, 1, 128
+    T = groups.size // D
+    bits = groups.reshape(L, H, T, D)
+    lay = ost.Layout(L=L, H=H, T=T, D=D, dtype=dtype, group=32)
+    want = ost.encode_item(bits, ost.INT8, lay)
+    st = hr.Store(L=L, H=H, D=D, T=T, dtype=dtype, group=32, ladder=("INT8",), taus=(),
+                  hbm_budget=2 * lay.item_bytes(ost.INT8) + (1 << 20))
+    src = torch.from_numpy(bits.view(np.int16).reshape(-1).copy()).cuda()
+    st.build_begin(1, np.zeros(2, np.uint64))
+    st.build_put(0, src, src)
+    st.build_end()
+    got = st.export_item(0)
+    mo = lay.meta_offset(ost.INT8)
+    assert np.array_equal(got[mo:mo + 4 * T * D // 32], want[mo:mo + 4 * T * D // 32]), "scales"
+    assert np.array_equal(got, want)
