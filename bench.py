@@ -507,9 +507,11 @@ def run_tiered(ctx, wl, ko, vo, kvb, args):
     torch = ctx.torch
     B, k = wl["batch"], wl["k"]
     per_rank, agg = link_peak(ctx)
+    pageable = bool(getattr(args, "tiered_pageable", False))
     st, h, schemes, build_s, total = build_store(
-        ctx, wl, hbm_budget=wl["hbm_budget"], backing_pinned=True, keep_backing=True, alias_R=wl["alias_R"],
-        decay_shift=wl.get("decay_shift", 0))
+        ctx, wl, hbm_budget=wl["hbm_budget"], backing_pinned=not pageable, keep_backing=True,
+        alias_R=wl["alias_R"], decay_shift=wl.get("decay_shift", 0),
+        pin_budget=(wl.get("pin_budget", 16 << 30) if pageable else 0))
     pool = synth.gen_requests(wl["n_docs"], 8 * B, k, wl["s"], seed=1).reshape(8, B, k)
     steps = max(3, min(args.steps, wl.get("steps", 20)))
     ms_max, tot_bytes, stats, _ = timed_steps(ctx, st, pool, ko, vo, steps, 3, args.epoch_every, sample_clocks=False)
@@ -534,6 +536,8 @@ def run_tiered(ctx, wl, ko, vo, kvb, args):
                                    "formula": "max(HBM alg bytes / hbm_gbs, (H2D + migration bytes) / link peak)"
                                               " / step time"},
            "hbm_budget_bytes": wl["hbm_budget"], "alias_R": wl["alias_R"], "build_seconds": round(build_s, 2),
+           "backing": "pageable (+16 GiB pinned PIN_LIST tier; P:213 pageable -> pinned bounce -> HBM)" if pageable
+                      else "pinned",
            "decay_shift": wl.get("decay_shift", 0),
            "migrations": [stats["migrations_in"], stats["migrations_out"]]}
     st.close()
@@ -553,6 +557,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-tiered", action="store_true", help="skip the host-tier leg")
     ap.add_argument("--no-per-scheme", action="store_true", help="skip the per-scheme decode table")
+    ap.add_argument("--tiered-pageable", action="store_true",
+                    help="host-tier leg with a pageable backing (bounce through pinned memory)")
     ap.add_argument("--ncu-traffic", type=float, default=None,
                     help="dram read+write bytes per launch from an ncu --set full capture (profiles/)")
     args = ap.parse_args()
