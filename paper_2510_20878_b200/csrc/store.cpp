@@ -486,21 +486,30 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
     const bool to_arena = streamed[i].arena_off != FreeList::kNone;
     Slot& sl = ring[(to_arena ? ring_i : ring_i++) % slots];
     const uint8_t* src = nullptr;
+    bool bounce = false;
     if (loc[item].pin_off != FreeList::kNone) {
       src = pin_base + loc[item].pin_off;
     } else {
       require(loc[item].backing_off != FreeList::kNone, HR_ESTATE, "item has no host copy");
       src = backing_base + loc[item].backing_off;
-      if (!backing_is_pinned) {  // pageable data is first copied to pinned memory
-        if (!sl.bounce) HR_CUDA(cudaHostAlloc((void**)&sl.bounce, max_item, cudaHostAllocPortable));
-        if (sl.used) HR_CUDA(cudaEventSynchronize(sl.copied));  // previous DMA out of this bounce buffer done
-        host_copy(sl.bounce, src, bytes[item]);
-        src = sl.bounce;
-      }
+      bounce = !backing_is_pinned;
     }
     if (!to_arena) HR_CUDA(cudaStreamWaitEvent(copy_stream, sl.free_ev, 0));
     if (c0 && i == 0) HR_CUDA(cudaEventRecord(c0, copy_stream));
-    HR_CUDA(cudaMemcpyAsync(dest[i], src, bytes[item], cudaMemcpyHostToDevice, copy_stream));
+    if (bounce) {
+      // pageable data is first copied to pinned memory.  The bounce runs in 4 MiB pieces so
+      // the host copy of piece p+1 overlaps the DMA of piece p.
+      if (!sl.bounce) HR_CUDA(cudaHostAlloc((void**)&sl.bounce, max_item, cudaHostAllocPortable));
+      if (sl.used) HR_CUDA(cudaEventSynchronize(sl.copied));  // previous DMA out of this bounce buffer done
+      constexpr size_t kPiece = 4u << 20;
+      for (size_t off = 0; off < bytes[item]; off += kPiece) {
+        const size_t n = std::min<size_t>(kPiece, bytes[item] - off);
+        host_copy(sl.bounce + off, src + off, n);
+        HR_CUDA(cudaMemcpyAsync(dest[i] + off, sl.bounce + off, n, cudaMemcpyHostToDevice, copy_stream));
+      }
+    } else {
+      HR_CUDA(cudaMemcpyAsync(dest[i], src, bytes[item], cudaMemcpyHostToDevice, copy_stream));
+    }
     HR_CUDA(cudaEventRecord(sl.copied, copy_stream));
     if (c1 && i + 1 == streamed.size()) {
       HR_CUDA(cudaEventRecord(c1, copy_stream));
