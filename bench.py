@@ -584,7 +584,9 @@ def run_ablation(args, wl):
     base = res["turborag_bf16_from_host"]["ms_per_step"]
     for r in res.values():
         r["speedup_vs_turborag"] = round(base / r["ms_per_step"], 2)
-    line = {"ablation": res, "workload": tv["desc"], "batch": B, "k": k,
+    line = {"ablation": res, "workload": "Llama-3-8B KV shape, 10,000-doc store, Zipf(1.1), top-k 10; slow tier = "
+            "pageable host DRAM (backing aliased doc mod 250), HBM hot set 100 GiB, pinned tier 16 GiB where the arm "
+            "has one", "batch": B, "k": k,
             "paper_context": "P:485 MP-only 1.75x, full HA-RAG 2.10x average TTFT over TurboRAG on A100 + disk"}
     if ctx.rank == 0:
         print(json.dumps(line), flush=True)
