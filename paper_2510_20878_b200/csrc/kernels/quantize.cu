@@ -220,27 +220,36 @@ __device__ __forceinline__ void encode_group_chunk(const QuantParams& p, const G
 
 template <int SCHEME, int SEG, int DT>
 __global__ void __launch_bounds__(kQThreads) quant_group_kernel(QuantParams p) {
+  constexpr int kBatch = 4;  // chunks whose loads are in flight together (4 x 16 B per lane)
   const uint32_t lane = threadIdx.x & 31;
   Walker wk;
   wk.init(p);
   bool bad = false;
-  if (!wk.more()) return;
-  float x[8];
-  uint4 raw;
-  load8<DT>(wk.g.src + wk.e0 + lane * 8, x, raw);
-  while (true) {
-    const Geo g = wk.g;
-    const uint32_t e = wk.e0 + lane * 8;
-    wk.next(p);
-    float xn[8];
-    uint4 rn;
-    const bool has_next = wk.more();
-    if (has_next) load8<DT>(wk.g.src + wk.e0 + lane * 8, xn, rn);
-    encode_group_chunk<SCHEME, SEG, DT>(p, g, e, x, raw, lane, bad);
-    if (!has_next) break;
+  while (wk.more()) {
+    uint4 raw[kBatch];
+    Geo g[kBatch];
+    uint32_t e[kBatch];
+    int n = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) x[i] = xn[i];
-    raw = rn;
+    for (int b = 0; b < kBatch; ++b) {
+      if (wk.more()) {  // warp-uniform
+        g[b] = wk.g;
+        e[b] = wk.e0 + lane * 8;
+        raw[b] = __ldg(reinterpret_cast<const uint4*>(wk.g.src + e[b]));
+        wk.next(p);
+        n = b + 1;
+      }
+    }
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b) {
+      if (b < n) {
+        float x[8];
+        const uint32_t w[4] = {raw[b].x, raw[b].y, raw[b].z, raw[b].w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) x[2 * i] = to_f32<DT>(w[i] & 0xFFFFu), x[2 * i + 1] = to_f32<DT>(w[i] >> 16);
+        encode_group_chunk<SCHEME, SEG, DT>(p, g[b], e[b], x, raw[b], lane, bad);
+      }
+    }
   }
   if (bad) atomicOr(p.err, 1);
 }
