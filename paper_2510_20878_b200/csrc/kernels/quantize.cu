@@ -63,25 +63,20 @@ __device__ __forceinline__ bool any_nonfinite(const float (&x)[8]) {
 // division per element.  y = rcp.approx(s) has relative error <= 2^-23, so t = RN(x*y) is within
 // |x/s| * 1.5 * 2^-23 <= 1.5 * 2^-16 of x/s (|x/s| <= 128), and fl(x/s) within 2^-18 of x/s:
 // unless t lies within 2^-15 of a half-integer, x/s, fl(x/s) and t round to the same integer.
-// If any lane of the warp sees such a near-tie (or s / y are not normal), the warp recomputes
-// with the exact __fdiv_rn (rare; warp-uniform branch).
+// Elements near a half-integer (or any element when s / y are not normal) use __fdiv_rn.
 __device__ __forceinline__ void div_rne8(const float (&x)[8], float s, int (&q)[8]) {
   float y;
   asm("rcp.approx.f32 %0, %1;" : "=f"(y) : "f"(s));
-  bool need = !(s >= 1.17549435e-38f && s <= 8.50705917e+37f);
-  float r[8];
+  const bool slow = !(s >= 1.17549435e-38f && s <= 8.50705917e+37f);
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const float t = __fmul_rn(x[i], y);
-    r[i] = rintf(t);
-    need |= fabsf(fabsf(__fsub_rn(t, r[i])) - 0.5f) <= 3.0517578125e-05f;
+    float r = rintf(t);
+    // bf16 data makes exact half-integer quotients common (~0.2% of elements): only the flagged
+    // element takes the IEEE division
+    if (slow || fabsf(fabsf(__fsub_rn(t, r)) - 0.5f) <= 3.0517578125e-05f) r = rintf(__fdiv_rn(x[i], s));
+    q[i] = (int)r;
   }
-  if (__any_sync(0xFFFFFFFFu, need)) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) r[i] = rintf(__fdiv_rn(x[i], s));
-  }
-#pragma unroll
-  for (int i = 0; i < 8; ++i) q[i] = (int)r[i];
 }
 
 // sub(a, b) of R4: fl(a - b) saturated at FLT_MAX (finite inputs whose difference overflows)
