@@ -73,6 +73,12 @@ def build(verbose: bool = False) -> list[str]:
     ssrc = [os.path.join(ROOT, "synth", "csrc", "synth.cu")]
     if _lib(LIBSYNTH, ssrc, [], os.path.join(ROOT, "build", "synth")):
         built.append(LIBSYNTH)
+    # test infrastructure: exhaustive check of the quantizer's division-free arithmetic
+    chk_src = os.path.join(ROOT, "tests", "csrc", "markstein_check.cu")
+    chk = os.path.join(ROOT, "tests", "csrc", "markstein_check")
+    if os.path.exists(chk_src) and (_newer(chk, [chk_src]) or os.environ.get("HARAG_FORCE_BUILD")):
+        _run([NVCC, *ARCH, "-O3", "-o", chk, chk_src])
+        built.append(chk)
     if verbose:
         print("built:", built or "up to date")
     return built
