@@ -25,6 +25,8 @@
 #include "../common.h"
 #include "../kernels.h"
 
+#include <unordered_map>
+
 namespace harag {
 namespace {
 
@@ -461,14 +463,24 @@ __global__ void __launch_bounds__(kQThreads) gse_encode_kernel(QuantParams p) {
 }
 
 int g_num_sms = 0;
-int grid_for(uint64_t warps) {
+// One wave of resident CTAs (the warps walk contiguous chunk blocks): SMs x occupancy of `kernel`.
+template <class K>
+int grid_for(K kernel, uint64_t warps) {
   if (!g_num_sms) {
     int dev = 0;
     HR_CUDA(cudaGetDevice(&dev));
     HR_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
   }
+  static std::unordered_map<const void*, int> cache;  // occupancy per kernel
+  auto it = cache.find((const void*)kernel);
+  if (it == cache.end()) {
+    int o = 0;
+    HR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kernel, kQThreads, 0));
+    it = cache.emplace((const void*)kernel, o).first;
+  }
+  const int occ = it->second;
   const uint64_t want = (warps * 32 + kQThreads - 1) / kQThreads;
-  const uint64_t cap = (uint64_t)g_num_sms * 8;
+  const uint64_t cap = (uint64_t)g_num_sms * (occ > 0 ? occ : 1);
   return (int)(want < cap ? (want ? want : 1) : cap);
 }
 
@@ -476,53 +488,53 @@ template <int DT>
 void launch_dt(const QuantParams& p, cudaStream_t st) {
   const uint64_t slab = (uint64_t)p.T * p.D;
   const uint64_t chunks = (uint64_t)p.L * p.Hl * (slab / kChunk);
-  const int grid = grid_for(chunks);
+#define LAUNCH(KERNEL, WORK) KERNEL<<<grid_for(KERNEL, WORK), kQThreads, 0, st>>>(p)
   switch (p.scheme) {
     case HR_S_PASS16:
-      quant_elementwise_kernel<HR_S_PASS16, DT><<<grid, kQThreads, 0, st>>>(p);
+      LAUNCH((quant_elementwise_kernel<HR_S_PASS16, DT>), chunks);
       break;
     case HR_S_FP8E4M3:
-      quant_elementwise_kernel<HR_S_FP8E4M3, DT><<<grid, kQThreads, 0, st>>>(p);
+      LAUNCH((quant_elementwise_kernel<HR_S_FP8E4M3, DT>), chunks);
       break;
     case HR_S_FP8E5M2:
-      quant_elementwise_kernel<HR_S_FP8E5M2, DT><<<grid, kQThreads, 0, st>>>(p);
+      LAUNCH((quant_elementwise_kernel<HR_S_FP8E5M2, DT>), chunks);
       break;
     case HR_S_INT8:
     case HR_S_INT4: {
-      const bool small = p.G <= (uint32_t)kChunk;
-      const uint64_t work = small ? chunks : (uint64_t)p.L * p.Hl * (slab / p.G);
-      const int g = grid_for(work);
-      if (small) {
+      if (p.G <= (uint32_t)kChunk) {
         switch ((p.G >> 3) * 16 + (p.scheme == HR_S_INT8 ? 0 : 1)) {
-#define QG(SEGV)                                                                   \
-  case SEGV * 16 + 0: quant_group_kernel<HR_S_INT8, SEGV, DT><<<g, kQThreads, 0, st>>>(p); break; \
-  case SEGV * 16 + 1: quant_group_kernel<HR_S_INT4, SEGV, DT><<<g, kQThreads, 0, st>>>(p); break;
+#define QG(SEGV)                                                        \
+  case SEGV * 16 + 0: LAUNCH((quant_group_kernel<HR_S_INT8, SEGV, DT>), chunks); break; \
+  case SEGV * 16 + 1: LAUNCH((quant_group_kernel<HR_S_INT4, SEGV, DT>), chunks); break;
           QG(4) QG(8) QG(16) QG(32)
 #undef QG
           default: fail(HR_EINVAL, "group size must be a power of two >= 32");
         }
-      } else if (p.scheme == HR_S_INT8) {
-        quant_biggroup_kernel<HR_S_INT8, DT><<<g, kQThreads, 0, st>>>(p);
       } else {
-        quant_biggroup_kernel<HR_S_INT4, DT><<<g, kQThreads, 0, st>>>(p);
+        const uint64_t groups = (uint64_t)p.L * p.Hl * (slab / p.G);
+        if (p.scheme == HR_S_INT8)
+          LAUNCH((quant_biggroup_kernel<HR_S_INT8, DT>), groups);
+        else
+          LAUNCH((quant_biggroup_kernel<HR_S_INT4, DT>), groups);
       }
       break;
     }
     case HR_S_GSE8: {
       const uint64_t n_slabs = (uint64_t)p.L * p.Hl;
       HR_CUDA(cudaMemsetAsync(p.gse_range, 0, sizeof(int) * 2 * n_slabs, st));
-      gse_range_kernel<DT><<<grid, kQThreads, 0, st>>>(p);
+      LAUNCH((gse_range_kernel<DT>), chunks);
       if (p.gse_m == 3)
-        gse_encode_kernel<DT, 3><<<grid, kQThreads, 0, st>>>(p);
+        LAUNCH((gse_encode_kernel<DT, 3>), chunks);
       else if (p.gse_m == 4)
-        gse_encode_kernel<DT, 4><<<grid, kQThreads, 0, st>>>(p);
+        LAUNCH((gse_encode_kernel<DT, 4>), chunks);
       else
-        gse_encode_kernel<DT, 5><<<grid, kQThreads, 0, st>>>(p);
+        LAUNCH((gse_encode_kernel<DT, 5>), chunks);
       break;
     }
     default:
       fail(HR_EINVAL, "unknown scheme");
   }
+#undef LAUNCH
   HR_CUDA(cudaGetLastError());
 }
 
