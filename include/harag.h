@@ -88,6 +88,9 @@ typedef struct {
   int32_t  device;         /* CUDA device ordinal */
   int32_t  rank, world;    /* this store owns KV heads [rank*H/world, (rank+1)*H/world) */
   uint32_t staging_slots;  /* host-tier staging ring slots in HBM (0 -> 3) */
+  int32_t  disk_backing;   /* stores built with hr_build_from_file only: 1 = items outside the HBM arena and the
+                              pinned tier stay in the file and are read on every miss (the paper's DISK tier,
+                              P:237; O_DIRECT when available); 0 = the file is loaded into host memory */
 } hr_store_config;
 
 typedef struct {
@@ -181,6 +184,21 @@ hr_status hr_assemble_kv(hr_store* s, uint32_t n_req, uint32_t k, const uint32_t
  * synchronise the others first.  Demand mode: only the lists change. */
 hr_status hr_hotness_delta(hr_store* s, int64_t** dev_ptr, uint32_t* n);
 hr_status hr_replace(hr_store* s, void* stream);
+
+/* ------------------------------------------------------------ persistence
+ * Compress once, load many (compressed chunks are stored on disk).
+ * hr_store_save writes a built store: a 4 KiB-aligned header (magic
+ * "HRSTORE1", the config, n_docs, per-item hotness and scheme) followed by
+ * every item's packed blob at a 4 KiB-aligned offset.
+ * Synchronous; HR_ECUDA/HR_EINVAL (I/O errors carry errno text).
+ * hr_build_from_file builds an EMPTY store from such a file instead of
+ * quantising: schemes are the saved ones (compress once), hotness the saved
+ * vector, placement (Alg. 2 step 1) follows this store's budgets.  The file's
+ * shape (L, H, D, T, dtype, group, GSE layout, rank, world) must equal the
+ * store's config, else HR_EINVAL.  With disk_backing = 1 the file stays open
+ * and backs the cold items. */
+hr_status hr_store_save(const hr_store* s, const char* path);
+hr_status hr_build_from_file(hr_store* s, const char* path, void* stream);
 
 /* ------------------------------------------------------------- inspection */
 /* tier: eager mode -> where the item is served from (HBM arena, pinned tier, backing);

@@ -53,7 +53,8 @@ def _p(a, ct):
 def make_config(*, L, H, D, T, dtype="bf16", group=0, gse=(4, 3),
                 ladder=("INT8", "FP8E4M3", "FP8E5M2", "GSE8"), taus=(0.1, 0.1, 0.1),
                 hbm_budget=0, pin_budget=0, backing_pinned=False, keep_backing=True, decay_shift=1,
-                alias_R=0, device=0, rank=0, world=1, staging_slots=3, demand_mode=False) -> _lib.Config:
+                alias_R=0, device=0, rank=0, world=1, staging_slots=3, demand_mode=False,
+                disk_backing=False) -> _lib.Config:
     c = _lib.default_config()
     c.L, c.H, c.D, c.T = L, H, D, T
     c.dtype = HR_FP16 if dtype == "fp16" else HR_BF16
@@ -69,6 +70,7 @@ def make_config(*, L, H, D, T, dtype="bf16", group=0, gse=(4, 3),
     c.decay_shift, c.bench_alias_R = decay_shift, alias_R
     c.device, c.rank, c.world, c.staging_slots = device, rank, world, staging_slots
     c.demand_mode = int(bool(demand_mode))
+    c.disk_backing = int(bool(disk_backing))
     return c
 
 
@@ -115,6 +117,14 @@ class Store:
 
     def build_end(self, stream=None) -> None:
         check(lib.hr_build_end(self._h, _stream(stream)))
+
+    def save(self, path: str) -> None:
+        """Persist the packed store (hr_store_save)."""
+        check(lib.hr_store_save(self._h, str(path).encode()))
+
+    def build_from_file(self, path: str, stream=None) -> None:
+        """Build this (empty) store from a saved file (hr_build_from_file)."""
+        check(lib.hr_build_from_file(self._h, str(path).encode(), _stream(stream)))
 
     # ----------------------------------------------------------- assemble
     def kv_bytes(self, k: int) -> int:

@@ -30,6 +30,7 @@ class Config(C.Structure):
         ("backing_pinned", C.c_int32), ("keep_backing", C.c_int32), ("demand_mode", C.c_int32),
         ("decay_shift", C.c_uint32), ("bench_alias_R", C.c_uint32),
         ("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("staging_slots", C.c_uint32),
+        ("disk_backing", C.c_int32),
     ]
 
 
@@ -68,6 +69,8 @@ _SIGS = {
     "hr_assemble_kv": (I32, [P, U32, U32, PU32, C.POINTER(P), C.POINTER(P), P]),
     "hr_hotness_delta": (I32, [P, C.POINTER(PI64), PU32]),
     "hr_replace": (I32, [P, P]),
+    "hr_store_save": (I32, [P, C.c_char_p]),
+    "hr_build_from_file": (I32, [P, C.c_char_p, P]),
     "hr_item_info": (I32, [P, U32, PU32, PU32, PU64]),
     "hr_item_rank": (I32, [P, U32, PU32]),
     "hr_export_item": (I32, [P, U32, P, SZ, C.POINTER(SZ)]),

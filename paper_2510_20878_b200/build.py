@@ -4,7 +4,9 @@
                                       runtime (C++), sm_100a kernels
   synth/libharag_synth.so             device copy of the synthetic input generator
 
-Run ``python -m paper_2510_20878_b200.build`` or ``__graft_entry__.build()``.
+Run ``python paper_2510_20878_b200/build.py`` or ``__graft_entry__.build()`` (both
+work before the library exists; ``python -m paper_2510_20878_b200.build`` imports
+the package and so needs a loadable library).
 Rebuilds when any source or header is newer than the library.
 """
 from __future__ import annotations

@@ -130,6 +130,21 @@ hr_status hr_replace(hr_store* s, void* stream) {
   });
 }
 
+hr_status hr_store_save(const hr_store* s, const char* path) {
+  return guard([&] {
+    NONNULL(s);
+    NONNULL(path);
+    s->impl.save(path);
+  });
+}
+hr_status hr_build_from_file(hr_store* s, const char* path, void* stream) {
+  return guard([&] {
+    NONNULL(s);
+    NONNULL(path);
+    s->impl.build_from_file(path, S(stream));
+  });
+}
+
 hr_status hr_item_info(const hr_store* s, uint32_t item, uint32_t* scheme, uint32_t* tier, uint64_t* bytes) {
   return guard([&] {
     NONNULL(s);

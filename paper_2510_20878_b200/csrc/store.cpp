@@ -7,6 +7,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <fcntl.h>
+#include <unistd.h>
+
+#include <atomic>
+#include <cerrno>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -103,6 +108,8 @@ Store::~Store() {
   if (mig_ev) cudaEventDestroy(mig_ev);
   for (auto& p : promos) cudaEventDestroy(p.ev);
   if (copy_stream) cudaStreamDestroy(copy_stream);
+  if (disk_fd >= 0) ::close(disk_fd);
+  if (disk_fd_direct >= 0) ::close(disk_fd_direct);
 }
 
 uint32_t Store::logical_tier(uint32_t item) const {
@@ -116,12 +123,19 @@ void Store::build_begin(uint32_t nd, const uint64_t* hot) {
   require(state == State::Empty, HR_ESTATE, "store already built");
   require(nd > 0, HR_EINVAL, "n_docs must be > 0");
   require(hot != nullptr, HR_EINVAL, "hotness is NULL");
+  // Alg. 1 (P:182-206): schemes by hotness rank
+  setup(nd, hot, assign_schemes(hot, 2 * nd, cfg.ladder, cfg.n_ladder, cfg.tau), false);
+  state = State::Building;
+}
+
+// Placement (Alg. 2 step 1 by bytes, R15) and every allocation of a store whose schemes are known.
+// on_disk: the host backing of the cold items is the store file (hr_build_from_file, disk_backing).
+void Store::setup(uint32_t nd, const uint64_t* hot, std::vector<uint32_t> sc, bool on_disk) {
   HR_CUDA(cudaSetDevice(cfg.device));
   n_docs = nd;
   n_items = 2 * nd;
   h.assign(hot, hot + n_items);
-  // Alg. 1 (P:182-206): schemes by hotness rank
-  scheme = assign_schemes(h.data(), n_items, cfg.ladder, cfg.n_ladder, cfg.tau);
+  scheme = std::move(sc);
   bytes.resize(n_items);
   for (uint32_t i = 0; i < n_items; ++i) bytes[i] = lay.item_bytes(scheme[i]);
   // Alg. 2 step 1 by bytes (R15)
@@ -166,7 +180,7 @@ void Store::build_begin(uint32_t nd, const uint64_t* hot) {
   // host backing: one blob per item that needs one (all if keep_backing), aliased in bench mode
   uint64_t total = 0;
   std::map<uint64_t, uint64_t> alias_off;
-  for (uint32_t i = 0; i < n_items; ++i) {
+  for (uint32_t i = 0; i < n_items && !on_disk; ++i) {
     if (!cfg.keep_backing && tier[i] == HR_T_HBM) continue;
     const uint64_t key = backing_key(i);
     auto it = alias_off.find(key);
@@ -211,7 +225,6 @@ void Store::build_begin(uint32_t nd, const uint64_t* hot) {
   HR_CUDA(cudaMalloc(&gse_range, sizeof(int) * 2 * lay.n_slabs()));
   put_done.assign(n_docs, 0);
   backing_filled.clear();
-  state = State::Building;
 }
 
 uint64_t Store::backing_key(uint32_t item) const {
@@ -425,7 +438,7 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
             const uint64_t off = pin.alloc(bytes[item]);  // queuePIN.put: a pinned copy from the backing
             if (off != FreeList::kNone) {
               loc[item].pin_off = off;
-              host_copy(pin_base + off, backing_base + loc[item].backing_off, bytes[item]);
+              fill_host(item, pin_base + off);
             }
           }
           promote = alg2->contains(Alg2::GPU, item) && loc[item].hbm_off == FreeList::kNone;
@@ -486,20 +499,26 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
     const bool to_arena = streamed[i].arena_off != FreeList::kNone;
     Slot& sl = ring[(to_arena ? ring_i : ring_i++) % slots];
     const uint8_t* src = nullptr;
-    bool bounce = false;
+    bool bounce = false, from_disk = false;
     if (loc[item].pin_off != FreeList::kNone) {
       src = pin_base + loc[item].pin_off;
-    } else {
-      require(loc[item].backing_off != FreeList::kNone, HR_ESTATE, "item has no host copy");
+    } else if (loc[item].backing_off != FreeList::kNone) {
       src = backing_base + loc[item].backing_off;
       bounce = !backing_is_pinned;
+    } else {
+      from_disk = true;  // the DISK tier ("load C_i from Disk"): file -> pinned bounce -> HBM
     }
     if (!to_arena) HR_CUDA(cudaStreamWaitEvent(copy_stream, sl.free_ev, 0));
     if (c0 && i == 0) HR_CUDA(cudaEventRecord(c0, copy_stream));
-    if (bounce) {
+    if (from_disk) {
+      if (!sl.bounce) HR_CUDA(cudaHostAlloc((void**)&sl.bounce, align_up(max_item, 4096), cudaHostAllocPortable));
+      if (sl.used) HR_CUDA(cudaEventSynchronize(sl.copied));
+      read_disk(item, sl.bounce);
+      HR_CUDA(cudaMemcpyAsync(dest[i], sl.bounce, bytes[item], cudaMemcpyHostToDevice, copy_stream));
+    } else if (bounce) {
       // pageable data is first copied to pinned memory.  The bounce runs in 4 MiB pieces so
       // the host copy of piece p+1 overlaps the DMA of piece p.
-      if (!sl.bounce) HR_CUDA(cudaHostAlloc((void**)&sl.bounce, max_item, cudaHostAllocPortable));
+      if (!sl.bounce) HR_CUDA(cudaHostAlloc((void**)&sl.bounce, align_up(max_item, 4096), cudaHostAllocPortable));
       if (sl.used) HR_CUDA(cudaEventSynchronize(sl.copied));  // previous DMA out of this bounce buffer done
       constexpr size_t kPiece = 4u << 20;
       for (size_t off = 0; off < bytes[item]; off += kPiece) {
@@ -530,13 +549,28 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
   stats.requests += n_req;
 }
 
+// A host copy of item's blob at dst (pinned-tier fill): from the in-memory backing or the store file.
+void Store::fill_host(uint32_t item, uint8_t* dst) {
+  if (loc[item].backing_off != FreeList::kNone) {
+    host_copy(dst, backing_base + loc[item].backing_off, bytes[item]);
+  } else {
+    require(disk_fd >= 0, HR_ESTATE, "item has no host copy");
+    uint64_t done = 0;
+    while (done < bytes[item]) {
+      const ssize_t r = ::pread(disk_fd, dst + done, bytes[item] - done, (off_t)(disk_off[item] + done));
+      require(r > 0, HR_EINVAL, "read " + disk_path + ": " + std::strerror(errno));
+      done += (uint64_t)r;
+    }
+  }
+}
+
 void Store::host_copy(void* dst, const void* src, size_t n) {
   if (!copy_pool) {
     unsigned t = std::thread::hardware_concurrency() / 2;
     if (const char* e = std::getenv("HARAG_COPY_THREADS")) t = (unsigned)std::atoi(e);
     copy_pool.reset(new CopyPool(std::min(t, 15u)));
   }
-  copy_pool->copy(dst, src, n);
+  if (n) copy_pool->copy(dst, src, n);
 }
 
 uint64_t Store::bytes_read_alg(uint32_t item) const {
@@ -586,7 +620,7 @@ void Store::replace(cudaStream_t st) {
   poll_promotions(true);  // the previous epoch's copies (normally long done)
   bool any_move = false;
   for (uint32_t i = 0; i < n_items; ++i) any_move |= (nt[i] == HR_T_HBM) != (loc[i].hbm_off != FreeList::kNone);
-  require(!any_move || cfg.keep_backing, HR_ESTATE, "re-placement needs keep_backing = 1");
+  require(!any_move || cfg.keep_backing || disk_fd >= 0, HR_ESTATE, "re-placement needs keep_backing = 1");
   if (!mig_ev) HR_CUDA(cudaEventCreateWithFlags(&mig_ev, cudaEventDisableTiming));
   HR_CUDA(cudaEventRecord(mig_ev, st));
   HR_CUDA(cudaStreamWaitEvent(copy_stream, mig_ev, 0));
@@ -623,8 +657,17 @@ void Store::replace(cudaStream_t st) {
         nt[i] = cfg.backing_pinned ? HR_T_PIN : HR_T_PAGE;
         continue;
       }
-      HR_CUDA(cudaMemcpyAsync(hbm_base + off, backing_base + loc[i].backing_off, bytes[i], cudaMemcpyHostToDevice,
-                              copy_stream));
+      if (loc[i].backing_off != FreeList::kNone) {
+        HR_CUDA(cudaMemcpyAsync(hbm_base + off, backing_base + loc[i].backing_off, bytes[i], cudaMemcpyHostToDevice,
+                                copy_stream));
+      } else {  // disk-backed: through a pinned bounce, one item at a time
+        ensure_ring();
+        Slot& sl = ring[0];
+        if (!sl.bounce) HR_CUDA(cudaHostAlloc((void**)&sl.bounce, align_up(max_item, 4096), cudaHostAllocPortable));
+        HR_CUDA(cudaStreamSynchronize(copy_stream));
+        read_disk(i, sl.bounce);
+        HR_CUDA(cudaMemcpyAsync(hbm_base + off, sl.bounce, bytes[i], cudaMemcpyHostToDevice, copy_stream));
+      }
       Promo pr{i, off, nullptr};
       HR_CUDA(cudaEventCreateWithFlags(&pr.ev, cudaEventDisableTiming));
       HR_CUDA(cudaEventRecord(pr.ev, copy_stream));
@@ -643,7 +686,7 @@ void Store::replace(cudaStream_t st) {
         continue;
       }
       loc[i].pin_off = off;
-      host_copy(pin_base + off, backing_base + loc[i].backing_off, bytes[i]);
+      fill_host(i, pin_base + off);
     }
   }
   tier = nt;  // target placement; HBM promotions become resident as their copies land
@@ -695,6 +738,154 @@ void Store::compact_pin() {  // host-side twin of compact_hbm (no DMA reads the 
   pin.reset_compacted(cursor, pin_cap);
 }
 
+// ------------------------------------------------------------ persistence
+namespace {
+constexpr char kMagic[8] = {'H', 'R', 'S', 'T', 'O', 'R', 'E', '1'};
+struct FileHeader {
+  char magic[8];
+  uint32_t version, n_docs;
+  uint64_t data_offset;
+  hr_store_config cfg;
+};
+std::string errno_msg(const char* what, const std::string& path) { return std::string(what) + " " + path + ": " + std::strerror(errno); }
+void pwrite_all(int fd, const void* buf, size_t n, uint64_t off, const std::string& path) {
+  const uint8_t* p = (const uint8_t*)buf;
+  while (n) {
+    const ssize_t w = ::pwrite(fd, p, n, (off_t)off);
+    require(w > 0, HR_EINVAL, errno_msg("write", path));
+    p += w, n -= (size_t)w, off += (uint64_t)w;
+  }
+}
+void pread_all(int fd, void* buf, size_t n, uint64_t off, const std::string& path) {
+  uint8_t* p = (uint8_t*)buf;
+  while (n) {
+    const ssize_t r = ::pread(fd, p, n, (off_t)off);
+    require(r > 0, HR_EINVAL, errno_msg("read", path));
+    p += r, n -= (size_t)r, off += (uint64_t)r;
+  }
+}
+}  // namespace
+
+std::vector<uint64_t> Store::file_offsets(uint64_t data_offset) const {
+  std::vector<uint64_t> off(n_items);
+  uint64_t o = data_offset;
+  for (uint32_t i = 0; i < n_items; ++i) off[i] = o, o += align_up(bytes[i], 4096);
+  return off;
+}
+
+void Store::save(const char* path) const {
+  require(state == State::Built, HR_ESTATE, "hr_store_save before the store is built");
+  const std::string P(path);
+  const int fd = ::open(path, O_CREAT | O_TRUNC | O_WRONLY, 0644);
+  require(fd >= 0, HR_EINVAL, errno_msg("open", P));
+  FileHeader hd{};
+  std::memcpy(hd.magic, kMagic, 8);
+  hd.version = 1;
+  hd.n_docs = n_docs;
+  hd.cfg = cfg;
+  const uint64_t arrays = sizeof(FileHeader) + n_items * (sizeof(uint64_t) + sizeof(uint32_t));
+  hd.data_offset = align_up(arrays, 4096);
+  std::vector<uint8_t> head(hd.data_offset, 0);
+  std::memcpy(head.data(), &hd, sizeof hd);
+  std::memcpy(head.data() + sizeof hd, h.data(), n_items * sizeof(uint64_t));
+  std::memcpy(head.data() + sizeof hd + n_items * sizeof(uint64_t), scheme.data(), n_items * sizeof(uint32_t));
+  try {
+    pwrite_all(fd, head.data(), head.size(), 0, P);
+    const std::vector<uint64_t> off = file_offsets(hd.data_offset);
+    std::vector<uint8_t> buf(align_up(max_item, 4096));
+    for (uint32_t i = 0; i < n_items; ++i) {
+      std::memset(buf.data() + bytes[i], 0, buf.size() - bytes[i]);
+      size_t len = 0;
+      export_item(i, buf.data(), buf.size(), &len);
+      pwrite_all(fd, buf.data(), align_up(bytes[i], 4096), off[i], P);
+    }
+  } catch (...) {
+    ::close(fd);
+    throw;
+  }
+  require(::close(fd) == 0, HR_EINVAL, errno_msg("close", P));
+}
+
+void Store::build_from_file(const char* path, cudaStream_t st) {
+  require(state == State::Empty, HR_ESTATE, "store already built");
+  const std::string P(path);
+  const int fd = ::open(path, O_RDONLY);
+  require(fd >= 0, HR_EINVAL, errno_msg("open", P));
+  disk_fd = fd;  // owned by the store from here on
+  disk_path = P;
+  FileHeader hd{};
+  pread_all(fd, &hd, sizeof hd, 0, P);
+  require(std::memcmp(hd.magic, kMagic, 8) == 0 && hd.version == 1, HR_ECORRUPT, P + " is not a harag store file");
+  const hr_store_config& f = hd.cfg;
+  require(f.L == cfg.L && f.H == cfg.H && f.D == cfg.D && f.T == cfg.T && f.dtype == cfg.dtype &&
+              (f.group ? f.group : f.D) == (cfg.group ? cfg.group : cfg.D) && f.gse_ebits == cfg.gse_ebits &&
+              f.gse_mbits == cfg.gse_mbits && f.rank == cfg.rank && f.world == cfg.world,
+          HR_EINVAL, "store file shape differs from the store config");
+  const uint32_t nd = hd.n_docs, ni = 2 * nd;
+  std::vector<uint64_t> hot(ni);
+  std::vector<uint32_t> sc(ni);
+  pread_all(fd, hot.data(), ni * sizeof(uint64_t), sizeof hd, P);
+  pread_all(fd, sc.data(), ni * sizeof(uint32_t), sizeof hd + ni * sizeof(uint64_t), P);
+  for (uint32_t v : sc) require(v <= HR_S_INT4, HR_ECORRUPT, "bad scheme in store file");
+  const bool on_disk = cfg.disk_backing != 0;
+  setup(nd, hot.data(), std::move(sc), on_disk);
+  disk_off = file_offsets(hd.data_offset);
+  if (on_disk) {  // cold reads bypass the page cache when the filesystem allows it
+    disk_fd_direct = ::open(path, O_RDONLY | O_DIRECT);
+    if (disk_fd_direct < 0) disk_fd_direct = -1;
+  }
+  ensure_ring();
+  Slot& sl = ring[0];
+  if (!sl.bounce) HR_CUDA(cudaHostAlloc((void**)&sl.bounce, align_up(max_item, 4096), cudaHostAllocPortable));
+  for (uint32_t i = 0; i < n_items; ++i) {
+    const uint64_t rb = align_up(bytes[i], 4096);
+    if (loc[i].hbm_off != FreeList::kNone) {  // GPU_LIST: file -> pinned bounce -> HBM arena
+      HR_CUDA(cudaStreamSynchronize(st));
+      read_disk(i, sl.bounce);
+      HR_CUDA(cudaMemcpyAsync(hbm_ptr(i), sl.bounce, bytes[i], cudaMemcpyHostToDevice, st));
+    }
+    if (loc[i].pin_off != FreeList::kNone) pread_all(fd, pin_base + loc[i].pin_off, bytes[i], disk_off[i], P);
+    if (loc[i].backing_off != FreeList::kNone && !backing_filled.count(loc[i].backing_off)) {
+      pread_all(fd, backing_base + loc[i].backing_off, rb > bytes[i] ? bytes[i] : rb, disk_off[i], P);
+      backing_filled.insert(loc[i].backing_off);
+    }
+  }
+  HR_CUDA(cudaStreamSynchronize(st));
+  n_put = n_docs;
+  cudaFree(scratch);
+  scratch = nullptr;
+  state = State::Built;
+}
+
+// One item's blob from the store file into a page-aligned host buffer (>= align4096(bytes)):
+// O_DIRECT reads of 4 MiB pieces spread over the worker pool.
+void Store::read_disk(uint32_t item, uint8_t* dst) {
+  const int fd = disk_fd_direct >= 0 ? disk_fd_direct : disk_fd;
+  require(fd >= 0, HR_ESTATE, "item has no host copy");
+  const uint64_t n = align_up(bytes[item], 4096), off = disk_off[item];
+  constexpr uint64_t kPiece = 4u << 20;
+  const unsigned pieces = (unsigned)((n + kPiece - 1) / kPiece);
+  if (!copy_pool) host_copy(nullptr, nullptr, 0);  // creates the pool
+  std::atomic<int> err{0};
+  for (unsigned b = 0; b < pieces; b += copy_pool->size()) {
+    copy_pool->parallel_for(std::min(copy_pool->size(), pieces - b), [&](unsigned p) {
+      const uint64_t o = (uint64_t)(b + p) * kPiece;
+      const uint64_t len = std::min(kPiece, n - o);
+      uint8_t* d = dst + o;
+      uint64_t done = 0;
+      while (done < len) {
+        const ssize_t r = ::pread(fd, d + done, len - done, (off_t)(off + o + done));
+        if (r <= 0) {
+          err = errno ? errno : EIO;
+          return;
+        }
+        done += (uint64_t)r;
+      }
+    });
+  }
+  require(err == 0, HR_EINVAL, "read " + disk_path + ": " + std::strerror(err));
+}
+
 void Store::export_item(uint32_t item, void* dst, size_t cap, size_t* len) const {
   require(state == State::Built, HR_ESTATE, "store not built");
   require(item < n_items, HR_ENOTFOUND, "item id out of range");
@@ -706,9 +897,11 @@ void Store::export_item(uint32_t item, void* dst, size_t cap, size_t* len) const
     HR_CUDA(cudaMemcpy(dst, hbm_ptr(item), bytes[item], cudaMemcpyDeviceToHost));
   } else if (loc[item].pin_off != FreeList::kNone) {
     std::memcpy(dst, pin_base + loc[item].pin_off, bytes[item]);
-  } else {
-    require(loc[item].backing_off != FreeList::kNone, HR_ESTATE, "item has no copy");
+  } else if (loc[item].backing_off != FreeList::kNone) {
     std::memcpy(dst, backing_base + loc[item].backing_off, bytes[item]);
+  } else {
+    require(disk_fd >= 0 && !disk_off.empty(), HR_ESTATE, "item has no copy");
+    pread_all(disk_fd, dst, bytes[item], disk_off[item], disk_path);
   }
 }
 

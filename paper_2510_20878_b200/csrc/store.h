@@ -16,6 +16,7 @@
 #include "policy.h"
 
 #include <memory>
+#include <string>
 
 namespace harag {
 
@@ -70,6 +71,11 @@ struct Store {
   ~Store();
 
   void build_begin(uint32_t n_docs, const uint64_t* hotness);
+  void setup(uint32_t n_docs, const uint64_t* hotness, std::vector<uint32_t> schemes, bool on_disk);
+  void save(const char* path) const;
+  void build_from_file(const char* path, cudaStream_t st);
+  void read_disk(uint32_t item, uint8_t* dst);
+  std::vector<uint64_t> file_offsets(uint64_t data_offset) const;
   void build_put(uint32_t doc, const void* k_src, const void* v_src, cudaStream_t st);
   void build_end(cudaStream_t st);
   void build_with_source(uint32_t n_docs, const uint64_t* hotness, hr_src_fn src, void* user, cudaStream_t st);
@@ -90,6 +96,7 @@ struct Store {
                         void* const* v_out) const;
   void release_deferred();
   void host_copy(void* dst, const void* src, size_t n);
+  void fill_host(uint32_t item, uint8_t* dst);
   uint32_t logical_tier(uint32_t item) const;
   void compact_pin();
 
@@ -148,6 +155,10 @@ struct Store {
   };
   std::vector<Promo> promos;
   cudaEvent_t mig_ev = nullptr;
+  // disk tier (hr_build_from_file): the store file backs items without a host copy
+  int disk_fd = -1, disk_fd_direct = -1;
+  std::string disk_path;
+  std::vector<uint64_t> disk_off;
   void poll_promotions(bool wait_all);
   hr_stats stats{};
 };

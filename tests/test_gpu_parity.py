@@ -583,3 +583,47 @@ def test_markstein_division_exhaustive(torch_cuda):
     assert os.path.exists(exe), "build() compiles tests/csrc/markstein_check"
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "mismatches 0" in r.stdout.splitlines()[-1], r.stdout
+
+
+# ----------------------------------------------------- persistence and the DISK tier
+@pytest.mark.parametrize("disk_backing,demand", [(False, False), (True, False), (True, True)])
+def test_save_load_and_disk_tier(torch_cuda, tmp_path, disk_backing, demand):
+    """hr_store_save / hr_build_from_file: compress once, load many.
+    The loaded store keeps the saved schemes, places by its own budgets, and
+    with disk_backing = 1 serves cold items from the file on every miss (the
+    DISK tier); outputs stay bit-exact, re-placement too."""
+    import paper_2510_20878_b200 as hr
+    torch = torch_cuda
+    st, ora, lay, h, sizes = make_pair(torch, L=2, H=2, T=64, D=64, n_docs=16, ladder=NORTH, taus=(0.25, 0.25),
+                                       dtype="fp16")
+    path = str(tmp_path / "store.hr")
+    st.save(path)
+    order = hotness.rank_items(h)
+    hb = sum(sizes[i] for i in order[:6])
+    pb = sum(sizes[i] for i in order[6:10])
+    ld = hr.Store(L=2, H=2, D=64, T=64, dtype="fp16", ladder=("INT8",), taus=(), hbm_budget=hb, pin_budget=pb,
+                  disk_backing=disk_backing, demand_mode=demand, keep_backing=not disk_backing)
+    ld.build_from_file(path)
+    for item in range(32):
+        assert ld.item_info(item)[0] == st.item_info(item)[0]          # saved schemes, not the new ladder
+        assert np.array_equal(ld.export_item(item), ora.blobs[item])
+    if not demand:
+        want = placement.eager_tiers(h, sizes, hb, pb)
+        names = {0: placement.GPU, 1: placement.PIN, 2: placement.PAGE}
+        assert [names[ld.item_info(i)[1]] for i in range(32)] == want
+    for epoch in range(3):
+        reqs = synth.gen_requests(16, 24, 4, 1.1, seed=60 + epoch, perm_seed=70 + epoch)
+        check_requests(torch, ld, ora, lay, reqs)
+        ld.replace()
+    s = ld.stats()
+    assert s["hits"][2] > 0 or s["hits"][1] > 0
+    ld.close()
+    with open(path, "r+b") as f:   # corrupt the magic
+        f.write(b"XXXX")
+    bad = hr.Store(L=2, H=2, D=64, T=64, dtype="fp16", hbm_budget=hb)
+    with pytest.raises(hr.HaragError, match="ECORRUPT"):
+        bad.build_from_file(path)
+    other = hr.Store(L=2, H=2, D=128, T=64, dtype="fp16", hbm_budget=hb)
+    st.save(path)
+    with pytest.raises(hr.HaragError, match="EINVAL"):
+        other.build_from_file(path)
