@@ -592,6 +592,48 @@ def run_ablation(args, wl):
         print(json.dumps(line), flush=True)
 
 
+def run_disk_leg(args, wl):
+    """The DISK tier: a 500-doc store saved to disk, reloaded with disk_backing, a
+    small HBM hot set; every miss is read from the file (O_DIRECT pieces) -> pinned bounce -> HBM."""
+    import tempfile
+
+    import paper_2510_20878_b200 as hr
+    import synth
+    ctx = Ctx(args)
+    torch = ctx.torch
+    w = dict(wl, n_docs=500)
+    st, h, schemes, build_s, total = build_store(ctx, w)
+    d = os.environ.get("HARAG_DISK_DIR", tempfile.gettempdir())
+    path = os.path.join(d, f"harag_store_{os.getpid()}.hr")
+    t0 = time.perf_counter()
+    st.save(path)
+    save_s = time.perf_counter() - t0
+    st.close()
+    geo = dict(L=w["L"], H=w["H"], D=w["D"], T=w["T"], dtype=w["dtype"], rank=ctx.rank, world=ctx.world)
+    ld = hr.Store(ladder=w["ladder"], taus=w["taus"], device=ctx.device, hbm_budget=total // 10, disk_backing=True,
+                  keep_backing=False, decay_shift=0, **geo)
+    t0 = time.perf_counter()
+    ld.build_from_file(path, stream=ctx.stream)
+    load_s = time.perf_counter() - t0
+    B, k = 8, w["k"]
+    kvb = ld.kv_bytes(k)
+    out = torch.empty(2 * B * kvb // 2, dtype=torch.int16, device="cuda")
+    ko = [out[(2 * r) * kvb // 2:(2 * r + 1) * kvb // 2] for r in range(B)]
+    vo = [out[(2 * r + 1) * kvb // 2:(2 * r + 2) * kvb // 2] for r in range(B)]
+    pool = synth.gen_requests(500, 8 * B, k, w["s"], seed=1).reshape(8, B, k)
+    ms, tot, stats, _ = timed_steps(ctx, ld, pool, ko, vo, 5, 3, 0, sample_clocks=False)
+    res = {"disk_leg": {"n_docs": 500, "file_GB": round(total / 1e9, 1), "save_s": round(save_s, 1),
+                        "load_s": round(load_s, 1), "ms_per_step": round(ms / 5, 1), "batch": B, "k": k,
+                        "hits_per_tier": stats["hits"],
+                        "disk_GBps": round(stats["bytes_h2d"] / (stats["h2d_ms"] / 1e3) / 1e9, 2)
+                        if stats["h2d_ms"] else None,
+                        "o_direct_dir": d}}
+    ld.close()
+    os.remove(path)
+    if ctx.rank == 0:
+        print(json.dumps(res), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -608,6 +650,7 @@ def main():
     ap.add_argument("--tiered-pageable", action="store_true",
                     help="host-tier leg with a pageable backing (bounce through pinned memory)")
     ap.add_argument("--ablation", action="store_true", help="run the paper's ablation arms (P:476-485) instead")
+    ap.add_argument("--disk-leg", action="store_true", help="run the DISK-tier leg (save, reload disk-backed) instead")
     ap.add_argument("--ncu-traffic", type=float, default=None,
                     help="dram read+write bytes per launch from an ncu --set full capture (profiles/)")
     args = ap.parse_args()
@@ -620,6 +663,8 @@ def main():
         run_reference(args, wl)
     elif args.ablation:
         run_ablation(args, wl)
+    elif args.disk_leg:
+        run_disk_leg(args, wl)
     else:
         run_ours(args, wl)
 
