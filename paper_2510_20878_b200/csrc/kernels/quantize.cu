@@ -192,20 +192,21 @@ __device__ __forceinline__ void encode_group_chunk(const QuantParams& p, const G
     // (tests/csrc/markstein_check.cu, exhaustive); outside that range the IEEE division.  |x| <= a
     // gives |x/s| <= 127 (1 + 2^-24), so the clamp never binds and is omitted.
     const bool fast = s >= 8.0779356e-28f && s <= 4.2535296e+37f;
-    const float y = __fdiv_rn(1.f, s);
-    uint32_t w[2] = {0u, 0u};
+    int c8[8];
+    if (__all_sync(0xFFFFFFFFu, fast)) {  // warp-uniform: the branch-free path for every normal scale
+      const float y = __fdiv_rn(1.f, s);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      float qf;
-      if (fast) {
+      for (int i = 0; i < 8; ++i) {
         const float q0 = __fmul_rn(x[i], y);
-        qf = __fmaf_rn(__fmaf_rn(-q0, s, x[i]), y, q0);
-      } else {
-        qf = __fdiv_rn(x[i], s);
+        c8[i] = __float2int_rn(__fmaf_rn(__fmaf_rn(-q0, s, x[i]), y, q0));
       }
-      w[i >> 2] |= ((uint32_t)__float2int_rn(qf) & 0xFFu) << (8 * (i & 3));
+    } else {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) c8[i] = __float2int_rn(__fdiv_rn(x[i], s));
     }
-    *reinterpret_cast<uint2*>(g.codes + e) = make_uint2(w[0], w[1]);
+    const uint32_t w0 = __byte_perm(__byte_perm(c8[0], c8[1], 0x0040), __byte_perm(c8[2], c8[3], 0x0040), 0x5410);
+    const uint32_t w1 = __byte_perm(__byte_perm(c8[4], c8[5], 0x0040), __byte_perm(c8[6], c8[7], 0x0040), 0x5410);
+    *reinterpret_cast<uint2*>(g.codes + e) = make_uint2(w0, w1);
   } else {
     bad |= any_nonfinite(x);
     // a3: mn = min + 0, mx = max + 0 (a zero extreme is +0); s = (mx == mn) ? 1 : fl(sub(mx, mn) / 15)
