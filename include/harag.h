@@ -63,7 +63,8 @@ typedef enum {
 typedef enum {
   HR_T_HBM = 0,      /* GPU memory (queueGPU) */
   HR_T_PIN = 1,      /* pinned host memory (queuePIN) */
-  HR_T_PAGE = 2      /* pageable host memory (queuePAGE / backing store) */
+  HR_T_PAGE = 2,     /* pageable host memory (queuePAGE / in-memory backing store) */
+  HR_T_DISK = 3      /* the store file only (disk_backing; DISK_LIST) */
 } hr_tier;
 
 typedef struct {
@@ -91,6 +92,8 @@ typedef struct {
   int32_t  disk_backing;   /* stores built with hr_build_from_file only: 1 = items outside the HBM arena and the
                               pinned tier stay in the file and are read on every miss (the paper's DISK tier,
                               P:237; O_DIRECT when available); 0 = the file is loaded into host memory */
+  uint64_t page_budget;    /* disk_backing only: bytes of pageable cache for PAGE_LIST items (queuePAGE);
+                              items past GPU_LIST + PIN_LIST + PAGE_LIST are DISK_LIST (read on every miss) */
 } hr_store_config;
 
 typedef struct {
@@ -111,6 +114,7 @@ typedef struct {
                                  last copy end, CUDA events on the copy stream) when timing is on */
   uint64_t h2d_items;         /* host-tier items streamed */
   uint64_t bytes_migrated;    /* host -> device bytes of hr_replace promotions (not in bytes_h2d) */
+  uint64_t hits_disk;         /* item accesses served from the store file (HR_T_DISK) */
 } hr_stats;
 
 typedef struct hr_store hr_store;
@@ -220,6 +224,9 @@ hr_status hr_policy_assign(uint32_t n_items, const uint64_t* h, uint32_t n_ladde
 /* Alg. 2 step 1 by bytes (R15): tier per item (0 HBM, 1 PIN, 2 PAGE). */
 hr_status hr_policy_lists_bytes(uint32_t n_items, const uint32_t* order, const uint64_t* sizes,
                                 uint64_t hbm_budget, uint64_t pin_budget, uint32_t* tier_out);
+/* The same with a PAGE budget: 0 HBM, 1 PIN, 2 PAGE, 3 DISK (the rest). */
+hr_status hr_policy_lists_bytes4(uint32_t n_items, const uint32_t* order, const uint64_t* sizes,
+                                 uint64_t hbm_budget, uint64_t pin_budget, uint64_t page_budget, uint32_t* tier_out);
 /* Alg. 2 step 1 by fractions (R13, R14): list per item (0 GPU, 1 PIN, 2 PAGE, 3 DISK). */
 hr_status hr_policy_lists_fraction(uint32_t n_items, const uint32_t* order, double tau_gpu, double tau_pin,
                                    double tau_page, uint32_t* list_out);

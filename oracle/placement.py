@@ -47,11 +47,30 @@ def lists_by_bytes(order, sizes, hbm_budget: int, pin_budget: int):
     return gpu, pin, rest
 
 
-def eager_tiers(h, sizes, hbm_budget: int, pin_budget: int, backing_pinned: bool = False):
+def lists_by_bytes4(order, sizes, hbm_budget: int, pin_budget: int, page_budget: int):
+    """Step 1 with all four lists of P:233-237 by bytes (R15, R26): GPU_LIST,
+    PIN_LIST and PAGE_LIST are consecutive longest rank-prefixes fitting their
+    budgets; DISK_LIST is the rest."""
+    gpu, pin, rest = lists_by_bytes(order, sizes, hbm_budget, pin_budget)
+    page, _, disk = lists_by_bytes(rest, sizes, page_budget, 0)
+    return gpu, pin, page, disk
+
+
+def eager_tiers(h, sizes, hbm_budget: int, pin_budget: int, backing_pinned: bool = False,
+                page_budget=None):
     """Eager placement (R15): GPU_LIST resident in HBM, PIN_LIST in the pinned
     tier, the rest served from the backing (pageable, or pinned when the
-    backing itself is pinned).  Returns tier per item id."""
+    backing itself is pinned).  With page_budget (a disk-backed store, R26)
+    PAGE_LIST is cached in pageable DRAM and DISK_LIST read from the file.
+    Returns tier per item id."""
     order = rank_items(h)
+    if page_budget is not None:
+        gpu, pin, page, disk = lists_by_bytes4(order, sizes, hbm_budget, pin_budget, page_budget)
+        tier = [None] * len(order)
+        for lst, t in ((gpu, GPU), (pin, PIN), (page, PAGE), (disk, DISK)):
+            for i in lst:
+                tier[i] = t
+        return tier
     if backing_pinned:
         pin_budget = 0
     gpu, pin, rest = lists_by_bytes(order, sizes, hbm_budget, pin_budget)

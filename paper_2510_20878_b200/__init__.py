@@ -12,11 +12,11 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
-from ._lib import (FP8E4M3, FP8E5M2, GSE8, HR_BF16, HR_FP16, INT4, INT8, PASS16, SCHEMES, T_HBM, T_PAGE,
-                   T_PIN, HaragError, check, lib)
+from ._lib import (FP8E4M3, FP8E5M2, GSE8, HR_BF16, HR_FP16, INT4, INT8, PASS16, SCHEMES, T_DISK, T_HBM,
+                   T_PAGE, T_PIN, HaragError, check, lib)
 
 __all__ = ["Store", "HaragError", "SCHEMES", "PASS16", "INT8", "FP8E4M3", "FP8E5M2", "GSE8", "INT4",
-           "T_HBM", "T_PIN", "T_PAGE", "policy_rank", "policy_assign", "policy_lists_bytes",
+           "T_HBM", "T_PIN", "T_PAGE", "T_DISK", "policy_rank", "policy_lists_bytes4", "policy_assign", "policy_lists_bytes",
            "policy_lists_fraction", "policy_count", "policy_epoch", "item_bytes", "Alg2"]
 
 
@@ -54,7 +54,7 @@ def make_config(*, L, H, D, T, dtype="bf16", group=0, gse=(4, 3),
                 ladder=("INT8", "FP8E4M3", "FP8E5M2", "GSE8"), taus=(0.1, 0.1, 0.1),
                 hbm_budget=0, pin_budget=0, backing_pinned=False, keep_backing=True, decay_shift=1,
                 alias_R=0, device=0, rank=0, world=1, staging_slots=3, demand_mode=False,
-                disk_backing=False) -> _lib.Config:
+                disk_backing=False, page_budget=0) -> _lib.Config:
     c = _lib.default_config()
     c.L, c.H, c.D, c.T = L, H, D, T
     c.dtype = HR_FP16 if dtype == "fp16" else HR_BF16
@@ -71,6 +71,7 @@ def make_config(*, L, H, D, T, dtype="bf16", group=0, gse=(4, 3),
     c.device, c.rank, c.world, c.staging_slots = device, rank, world, staging_slots
     c.demand_mode = int(bool(demand_mode))
     c.disk_backing = int(bool(disk_backing))
+    c.page_budget = int(page_budget)
     return c
 
 
@@ -189,7 +190,7 @@ class Store:
                 "migrations_out": s.migrations_out, "failed_promotions": s.failed_promotions,
                 "kernel_ms": s.kernel_ms, "timed_launches": s.timed_launches, "hbm_used": s.hbm_used,
                 "pin_used": s.pin_used, "h2d_ms": s.h2d_ms, "h2d_items": s.h2d_items,
-                "bytes_migrated": s.bytes_migrated}
+                "bytes_migrated": s.bytes_migrated, "hits_disk": s.hits_disk}
 
     def close(self) -> None:
         if self._h:
@@ -226,6 +227,14 @@ def policy_lists_bytes(order, sizes, hbm_budget, pin_budget) -> np.ndarray:
     out = np.empty(o.size, np.uint32)
     check(lib.hr_policy_lists_bytes(o.size, _p(o, C.c_uint32), _p(s, C.c_uint64), int(hbm_budget),
                                     int(pin_budget), _p(out, C.c_uint32)))
+    return out
+
+
+def policy_lists_bytes4(order, sizes, hbm_budget, pin_budget, page_budget) -> np.ndarray:
+    o, s = _u32(order), _u64(sizes)
+    out = np.empty(o.size, np.uint32)
+    check(lib.hr_policy_lists_bytes4(o.size, _p(o, C.c_uint32), _p(s, C.c_uint64), int(hbm_budget),
+                                     int(pin_budget), int(page_budget), _p(out, C.c_uint32)))
     return out
 
 

@@ -18,7 +18,7 @@ STATUS_NAMES = {0: "HR_OK", 1: "HR_EINVAL", 2: "HR_ENOMEM", 3: "HR_ECUDA", 4: "H
 HR_BF16, HR_FP16 = 0, 1
 PASS16, INT8, FP8E4M3, FP8E5M2, GSE8, INT4 = range(6)
 SCHEMES = {"PASS16": PASS16, "INT8": INT8, "FP8E4M3": FP8E4M3, "FP8E5M2": FP8E5M2, "GSE8": GSE8, "INT4": INT4}
-T_HBM, T_PIN, T_PAGE = 0, 1, 2
+T_HBM, T_PIN, T_PAGE, T_DISK = 0, 1, 2, 3
 
 
 class Config(C.Structure):
@@ -30,7 +30,7 @@ class Config(C.Structure):
         ("backing_pinned", C.c_int32), ("keep_backing", C.c_int32), ("demand_mode", C.c_int32),
         ("decay_shift", C.c_uint32), ("bench_alias_R", C.c_uint32),
         ("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("staging_slots", C.c_uint32),
-        ("disk_backing", C.c_int32),
+        ("disk_backing", C.c_int32), ("page_budget", C.c_uint64),
     ]
 
 
@@ -41,7 +41,7 @@ class Stats(C.Structure):
         ("migrations_in", C.c_uint64), ("migrations_out", C.c_uint64), ("failed_promotions", C.c_uint64),
         ("kernel_ms", C.c_double), ("timed_launches", C.c_uint64), ("hbm_used", C.c_uint64),
         ("pin_used", C.c_uint64), ("h2d_ms", C.c_double), ("h2d_items", C.c_uint64),
-        ("bytes_migrated", C.c_uint64),
+        ("bytes_migrated", C.c_uint64), ("hits_disk", C.c_uint64),
     ]
 
 
@@ -81,6 +81,7 @@ _SIGS = {
     "hr_policy_assign": (I32, [U32, PU64, U32, PU32, C.POINTER(C.c_double), PU32]),
     "hr_policy_lists_bytes": (I32, [U32, PU32, PU64, U64, U64, PU32]),
     "hr_policy_lists_fraction": (I32, [U32, PU32, DBL, DBL, DBL, PU32]),
+    "hr_policy_lists_bytes4": (I32, [U32, PU32, PU64, U64, U64, U64, PU32]),
     "hr_policy_count": (I32, [U32, U32, PU32, U32, U64, U32, U32, PI64]),
     "hr_policy_epoch": (I32, [U32, PU64, PI64, U32]),
     "hr_item_bytes": (I32, [C.POINTER(Config), U32, PU64]),

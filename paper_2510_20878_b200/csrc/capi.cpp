@@ -227,6 +227,19 @@ hr_status hr_policy_lists_bytes(uint32_t n, const uint32_t* order, const uint64_
     std::memcpy(tier_out, t.data(), sizeof(uint32_t) * n);
   });
 }
+hr_status hr_policy_lists_bytes4(uint32_t n, const uint32_t* order, const uint64_t* sizes, uint64_t hbm_budget,
+                                 uint64_t pin_budget, uint64_t page_budget, uint32_t* tier_out) {
+  return guard([&] {
+    NONNULL(order);
+    NONNULL(sizes);
+    NONNULL(tier_out);
+    std::vector<uint32_t> o(order, order + n);
+    for (uint32_t v : o) harag::require(v < n, HR_EINVAL, "order is not a permutation");
+    harag::require(page_budget != ~0ull, HR_EINVAL, "page_budget must be finite");
+    auto t = harag::lists_by_bytes(o, sizes, hbm_budget, pin_budget, page_budget);
+    std::memcpy(tier_out, t.data(), sizeof(uint32_t) * n);
+  });
+}
 hr_status hr_policy_lists_fraction(uint32_t n, const uint32_t* order, double tau_gpu, double tau_pin,
                                    double tau_page, uint32_t* list_out) {
   return guard([&] {

@@ -41,13 +41,15 @@ std::vector<uint32_t> assign_schemes(const uint64_t* h, uint32_t n, const uint32
 }
 
 std::vector<uint32_t> lists_by_bytes(const std::vector<uint32_t>& order, const uint64_t* sizes, uint64_t hbm_budget,
-                                     uint64_t pin_budget) {
-  std::vector<uint32_t> tier(order.size(), 2);
+                                     uint64_t pin_budget, uint64_t page_budget) {
+  std::vector<uint32_t> tier(order.size(), page_budget == ~0ull ? 2u : 3u);
   size_t i = 0;
-  uint64_t used = 0;
-  while (i < order.size() && used + sizes[order[i]] <= hbm_budget) used += sizes[order[i]], tier[order[i++]] = 0;
-  used = 0;
-  while (i < order.size() && used + sizes[order[i]] <= pin_budget) used += sizes[order[i]], tier[order[i++]] = 1;
+  const uint64_t budget[3] = {hbm_budget, pin_budget, page_budget};
+  for (uint32_t t = 0; t < 3; ++t) {  // longest rank-prefix that fits each budget, no skipping (R15)
+    uint64_t used = 0;
+    while (i < order.size() && (budget[t] == ~0ull || used + sizes[order[i]] <= budget[t]))
+      used += sizes[order[i]], tier[order[i++]] = t;
+  }
   return tier;
 }
 

@@ -22,9 +22,10 @@ std::vector<uint32_t> assign_schemes(const uint64_t* h, uint32_t n, const uint32
                                      const double* tau);
 
 // Alg. 2 step 1 by bytes (R15): longest rank-prefix fitting each budget.
-// Returns tier per item: 0 HBM (GPU_LIST), 1 PIN (PIN_LIST), 2 PAGE.
+// Returns tier per item: 0 HBM (GPU_LIST), 1 PIN (PIN_LIST), 2 PAGE (PAGE_LIST), 3 DISK (the rest,
+// only when page_budget is finite).
 std::vector<uint32_t> lists_by_bytes(const std::vector<uint32_t>& order, const uint64_t* sizes,
-                                     uint64_t hbm_budget, uint64_t pin_budget);
+                                     uint64_t hbm_budget, uint64_t pin_budget, uint64_t page_budget = ~0ull);
 
 // Alg. 2 step 1 by fractions (R13 pairs by name, R14 exclusive end).
 // Returns list per item: 0 GPU, 1 PIN, 2 PAGE, 3 DISK.

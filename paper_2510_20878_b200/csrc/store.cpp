@@ -92,6 +92,7 @@ Store::~Store() {
   copy_pool.reset();
   if (hbm_base) cudaFree(hbm_base);
   if (pin_base) cudaFreeHost(pin_base);
+  if (page_base) free(page_base);
   if (backing_base) {
     if (backing_is_pinned)
       cudaFreeHost(backing_base);
@@ -113,7 +114,12 @@ Store::~Store() {
 }
 
 uint32_t Store::logical_tier(uint32_t item) const {
-  if (alg2) return alg2->contains(Alg2::GPU, item) ? HR_T_HBM : alg2->contains(Alg2::PIN, item) ? HR_T_PIN : HR_T_PAGE;
+  if (alg2)
+    return alg2->contains(Alg2::GPU, item)    ? HR_T_HBM
+           : alg2->contains(Alg2::PIN, item)  ? HR_T_PIN
+           : alg2->contains(Alg2::PAGE, item) ? HR_T_PAGE
+           : on_disk                          ? HR_T_DISK
+                                              : HR_T_PAGE;
   return tier[item];  // eager: the placement target (a promotion may still be in flight)
 }
 
@@ -130,7 +136,18 @@ void Store::build_begin(uint32_t nd, const uint64_t* hot) {
 
 // Placement (Alg. 2 step 1 by bytes, R15) and every allocation of a store whose schemes are known.
 // on_disk: the host backing of the cold items is the store file (hr_build_from_file, disk_backing).
-void Store::setup(uint32_t nd, const uint64_t* hot, std::vector<uint32_t> sc, bool on_disk) {
+std::vector<uint32_t> Store::place_lists() const {
+  // pinned backing: every non-HBM item is served as PIN (no separate PIN_LIST); disk-backed stores add
+  // a PAGE_LIST of page_budget bytes and leave the rest on disk (DISK_LIST)
+  std::vector<uint32_t> t = lists_by_bytes(order, bytes.data(), cfg.hbm_budget,
+                                           cfg.backing_pinned && !on_disk ? 0 : cfg.pin_budget,
+                                           on_disk ? cfg.page_budget : ~0ull);
+  return t;
+}
+
+void Store::setup(uint32_t nd, const uint64_t* hot, std::vector<uint32_t> sc, bool disk) {
+  require(!disk || cfg.page_budget <= (1ull << 46), HR_EINVAL, "page_budget must be a finite byte count");
+  on_disk = disk;
   HR_CUDA(cudaSetDevice(cfg.device));
   n_docs = nd;
   n_items = 2 * nd;
@@ -140,13 +157,13 @@ void Store::setup(uint32_t nd, const uint64_t* hot, std::vector<uint32_t> sc, bo
   for (uint32_t i = 0; i < n_items; ++i) bytes[i] = lay.item_bytes(scheme[i]);
   // Alg. 2 step 1 by bytes (R15)
   order = rank_items(h.data(), n_items);
-  tier = lists_by_bytes(order, bytes.data(), cfg.hbm_budget, cfg.backing_pinned ? 0 : cfg.pin_budget);
+  tier = place_lists();
   if (cfg.demand_mode) {
     // Alg. 2 step 1 gives the lists; the queues start empty and fill on access (step 2)
-    alg2.reset(new Alg2(n_items, tier.data(), bytes.data(), cfg.hbm_budget, cfg.backing_pinned ? 0 : cfg.pin_budget,
-                        0));
-    tier.assign(n_items, HR_T_PAGE);
-  } else if (cfg.backing_pinned) {
+    alg2.reset(new Alg2(n_items, tier.data(), bytes.data(), cfg.hbm_budget,
+                        cfg.backing_pinned && !on_disk ? 0 : cfg.pin_budget, on_disk ? cfg.page_budget : 0));
+    tier.assign(n_items, on_disk ? HR_T_DISK : HR_T_PAGE);
+  } else if (cfg.backing_pinned && !on_disk) {
     for (auto& t : tier)
       if (t == HR_T_PAGE) t = HR_T_PIN;
   }
@@ -168,8 +185,15 @@ void Store::setup(uint32_t nd, const uint64_t* hot, std::vector<uint32_t> sc, bo
     }
     hbm.reset(hbm_cap);
   }
-  // pinned tier (PIN_LIST copies when the backing is pageable)
-  if (!cfg.backing_pinned && cfg.pin_budget) {
+  // pageable PAGE tier cache (disk-backed stores)
+  if (on_disk && cfg.page_budget) {
+    page_cap = align_up(cfg.page_budget, FreeList::kAlign);
+    page_base = (uint8_t*)aligned_alloc(4096, align_up(page_cap, 4096));
+    require(page_base != nullptr, HR_ENOMEM, "PAGE tier allocation failed");
+    page.reset(page_cap);
+  }
+  // pinned tier (PIN_LIST copies when the backing is pageable or on disk)
+  if ((!cfg.backing_pinned || on_disk) && cfg.pin_budget) {
     pin_cap = align_up(cfg.pin_budget, FreeList::kAlign);
     if (cudaHostAlloc((void**)&pin_base, pin_cap, cudaHostAllocPortable) != cudaSuccess) {
       cudaGetLastError();
@@ -180,7 +204,7 @@ void Store::setup(uint32_t nd, const uint64_t* hot, std::vector<uint32_t> sc, bo
   // host backing: one blob per item that needs one (all if keep_backing), aliased in bench mode
   uint64_t total = 0;
   std::map<uint64_t, uint64_t> alias_off;
-  for (uint32_t i = 0; i < n_items && !on_disk; ++i) {
+  for (uint32_t i = 0; i < n_items && !disk; ++i) {
     if (!cfg.keep_backing && tier[i] == HR_T_HBM) continue;
     const uint64_t key = backing_key(i);
     auto it = alias_off.find(key);
@@ -212,9 +236,12 @@ void Store::setup(uint32_t nd, const uint64_t* hot, std::vector<uint32_t> sc, bo
     if (tier[i] == HR_T_HBM) {
       loc[i].hbm_off = hbm.alloc(bytes[i]);
       require(loc[i].hbm_off != FreeList::kNone, HR_ENOMEM, "HBM arena exhausted during placement");
-    } else if (tier[i] == HR_T_PIN && !cfg.backing_pinned) {
+    } else if (tier[i] == HR_T_PIN && pin_base) {
       loc[i].pin_off = pin.alloc(bytes[i]);
       require(loc[i].pin_off != FreeList::kNone, HR_ENOMEM, "pinned tier exhausted during placement");
+    } else if (tier[i] == HR_T_PAGE && page_base) {
+      loc[i].page_off = page.alloc(bytes[i]);
+      require(loc[i].page_off != FreeList::kNone, HR_ENOMEM, "PAGE tier exhausted during placement");
     }
   }
   HR_CUDA(cudaMalloc(&delta, sizeof(int64_t) * n_items));
@@ -380,6 +407,8 @@ void Store::release_deferred() {
   }
   for (auto& f : pending_hbm_free) hbm.release(f.first, f.second);
   pending_hbm_free.clear();
+  for (auto& f : pending_page_free) page.release(f.first, f.second);  // read by the host during its call
+  pending_page_free.clear();
 }
 
 void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* const* k_out, void* const* v_out,
@@ -422,7 +451,10 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
         bool promote = false;
         if (demand) {  // Alg. 2 step 2: one branch per access, inclusive promotion, LRU
           const Alg2::Outcome o = alg2->access(item);
-          stats.hits[o.hit == Alg2::GPU ? HR_T_HBM : o.hit == Alg2::PIN ? HR_T_PIN : HR_T_PAGE]++;
+          if (o.hit == Alg2::DISK && on_disk)
+            stats.hits_disk++;
+          else
+            stats.hits[o.hit == Alg2::GPU ? HR_T_HBM : o.hit == Alg2::PIN ? HR_T_PIN : HR_T_PAGE]++;
           for (const auto& ev : o.evicted) {
             Loc& l = loc[ev.second];
             if (ev.first == Alg2::GPU && l.hbm_off != FreeList::kNone) {
@@ -432,6 +464,16 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
             } else if (ev.first == Alg2::PIN && l.pin_off != FreeList::kNone) {
               pending_pin_free.emplace_back(l.pin_off, bytes[ev.second]);
               l.pin_off = FreeList::kNone;
+            } else if (ev.first == Alg2::PAGE && l.page_off != FreeList::kNone) {
+              pending_page_free.emplace_back(l.page_off, bytes[ev.second]);
+              l.page_off = FreeList::kNone;
+            }
+          }
+          if ((o.put_mask & (1u << Alg2::PAGE)) && loc[item].page_off == FreeList::kNone && page_base) {
+            const uint64_t off = page.alloc(bytes[item]);  // queuePAGE.put: a pageable copy from disk
+            if (off != FreeList::kNone) {
+              loc[item].page_off = off;
+              fill_host(item, page_base + off);
             }
           }
           if ((o.put_mask & (1u << Alg2::PIN)) && loc[item].pin_off == FreeList::kNone && pin_base) {
@@ -443,9 +485,15 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
           }
           promote = alg2->contains(Alg2::GPU, item) && loc[item].hbm_off == FreeList::kNone;
         } else {
-          stats.hits[loc[item].hbm_off != FreeList::kNone                        ? HR_T_HBM
-                     : (loc[item].pin_off != FreeList::kNone || backing_is_pinned) ? HR_T_PIN
-                                                                                   : HR_T_PAGE]++;
+          const Loc& l = loc[item];
+          if (l.hbm_off == FreeList::kNone && l.pin_off == FreeList::kNone && l.page_off == FreeList::kNone &&
+              l.backing_off == FreeList::kNone)
+            stats.hits_disk++;
+          else
+            stats.hits[l.hbm_off != FreeList::kNone                                                    ? HR_T_HBM
+                       : (l.pin_off != FreeList::kNone || (l.backing_off != FreeList::kNone && backing_is_pinned &&
+                                                          l.page_off == FreeList::kNone)) ? HR_T_PIN
+                                                                                           : HR_T_PAGE]++;
         }
         auto it = stream_idx.find(item);
         if (it == stream_idx.end() && loc[item].hbm_off != FreeList::kNone) {
@@ -502,6 +550,9 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
     bool bounce = false, from_disk = false;
     if (loc[item].pin_off != FreeList::kNone) {
       src = pin_base + loc[item].pin_off;
+    } else if (loc[item].page_off != FreeList::kNone) {
+      src = page_base + loc[item].page_off;  // PAGE tier: pageable, through the bounce
+      bounce = true;
     } else if (loc[item].backing_off != FreeList::kNone) {
       src = backing_base + loc[item].backing_off;
       bounce = !backing_is_pinned;
@@ -609,12 +660,12 @@ void Store::replace(cudaStream_t st) {
   epoch_update(h.data(), dh.data(), n_items, cfg.decay_shift);  // a9 (R20)
   HR_CUDA(cudaMemsetAsync(delta, 0, sizeof(int64_t) * n_items, st));
   order = rank_items(h.data(), n_items);
-  std::vector<uint32_t> nt = lists_by_bytes(order, bytes.data(), cfg.hbm_budget, cfg.backing_pinned ? 0 : cfg.pin_budget);
+  std::vector<uint32_t> nt = place_lists();
   if (alg2) {  // demand mode (R20): only the lists change; stale queue entries leave by LRU
     alg2->set_lists(nt.data());
     return;
   }
-  if (cfg.backing_pinned)
+  if (cfg.backing_pinned && !on_disk)
     for (auto& t : nt)
       if (t == HR_T_PAGE) t = HR_T_PIN;
   poll_promotions(true);  // the previous epoch's copies (normally long done)
@@ -637,6 +688,10 @@ void Store::replace(cudaStream_t st) {
       loc[i].pin_off = FreeList::kNone;
       pin_changed = true;
     }
+    if (nt[i] != HR_T_PAGE && loc[i].page_off != FreeList::kNone) {
+      page.release(loc[i].page_off, bytes[i]);
+      loc[i].page_off = FreeList::kNone;
+    }
   }
   // pinned space freed above may still be the source of an in-flight DMA
   if (pin_changed) HR_CUDA(cudaStreamSynchronize(copy_stream));
@@ -654,7 +709,7 @@ void Store::replace(cudaStream_t st) {
       }
       if (off == FreeList::kNone) {
         stats.failed_promotions++;
-        nt[i] = cfg.backing_pinned ? HR_T_PIN : HR_T_PAGE;
+        nt[i] = on_disk ? HR_T_DISK : cfg.backing_pinned ? HR_T_PIN : HR_T_PAGE;
         continue;
       }
       if (loc[i].backing_off != FreeList::kNone) {
@@ -674,7 +729,15 @@ void Store::replace(cudaStream_t st) {
       promos.push_back(pr);
       stats.migrations_in++;
       stats.bytes_migrated += bytes[i];
-    } else if (nt[i] == HR_T_PIN && !cfg.backing_pinned && loc[i].pin_off == FreeList::kNone) {
+    } else if (nt[i] == HR_T_PAGE && page_base && loc[i].page_off == FreeList::kNone) {
+      const uint64_t off = page.alloc(bytes[i]);  // (no compaction: a miss falls back to DISK)
+      if (off == FreeList::kNone) {
+        nt[i] = HR_T_DISK;
+        continue;
+      }
+      loc[i].page_off = off;
+      fill_host(i, page_base + off);
+    } else if (nt[i] == HR_T_PIN && pin_base && loc[i].pin_off == FreeList::kNone) {
       uint64_t off = pin.alloc(bytes[i]);
       if (off == FreeList::kNone && pin_cap - pin.used() >= align_up(bytes[i], FreeList::kAlign)) {
         HR_CUDA(cudaStreamSynchronize(copy_stream));
@@ -682,7 +745,7 @@ void Store::replace(cudaStream_t st) {
         off = pin.alloc(bytes[i]);
       }
       if (off == FreeList::kNone) {
-        nt[i] = HR_T_PAGE;
+        nt[i] = on_disk ? HR_T_DISK : HR_T_PAGE;
         continue;
       }
       loc[i].pin_off = off;
@@ -845,6 +908,7 @@ void Store::build_from_file(const char* path, cudaStream_t st) {
       HR_CUDA(cudaMemcpyAsync(hbm_ptr(i), sl.bounce, bytes[i], cudaMemcpyHostToDevice, st));
     }
     if (loc[i].pin_off != FreeList::kNone) pread_all(fd, pin_base + loc[i].pin_off, bytes[i], disk_off[i], P);
+    if (loc[i].page_off != FreeList::kNone) pread_all(fd, page_base + loc[i].page_off, bytes[i], disk_off[i], P);
     if (loc[i].backing_off != FreeList::kNone && !backing_filled.count(loc[i].backing_off)) {
       pread_all(fd, backing_base + loc[i].backing_off, rb > bytes[i] ? bytes[i] : rb, disk_off[i], P);
       backing_filled.insert(loc[i].backing_off);
@@ -897,6 +961,8 @@ void Store::export_item(uint32_t item, void* dst, size_t cap, size_t* len) const
     HR_CUDA(cudaMemcpy(dst, hbm_ptr(item), bytes[item], cudaMemcpyDeviceToHost));
   } else if (loc[item].pin_off != FreeList::kNone) {
     std::memcpy(dst, pin_base + loc[item].pin_off, bytes[item]);
+  } else if (loc[item].page_off != FreeList::kNone) {
+    std::memcpy(dst, page_base + loc[item].page_off, bytes[item]);
   } else if (loc[item].backing_off != FreeList::kNone) {
     std::memcpy(dst, backing_base + loc[item].backing_off, bytes[item]);
   } else {

@@ -51,6 +51,7 @@ struct Store {
     uint64_t hbm_off = FreeList::kNone;      // HBM arena copy
     uint64_t pin_off = FreeList::kNone;      // pinned-tier copy
     uint64_t backing_off = FreeList::kNone;  // host backing copy
+    uint64_t page_off = FreeList::kNone;     // pageable PAGE-tier cache copy (disk-backed stores)
     bool backing_alias = false;
   };
   struct DescBuf {
@@ -71,7 +72,8 @@ struct Store {
   ~Store();
 
   void build_begin(uint32_t n_docs, const uint64_t* hotness);
-  void setup(uint32_t n_docs, const uint64_t* hotness, std::vector<uint32_t> schemes, bool on_disk);
+  void setup(uint32_t n_docs, const uint64_t* hotness, std::vector<uint32_t> schemes, bool disk);
+  std::vector<uint32_t> place_lists() const;  // Alg. 2 step 1 by bytes for this store's tiers
   void save(const char* path) const;
   void build_from_file(const char* path, cudaStream_t st);
   void read_disk(uint32_t item, uint8_t* dst);
@@ -122,6 +124,10 @@ struct Store {
   uint8_t* pin_base = nullptr;
   uint64_t pin_cap = 0;
   FreeList pin;
+  uint8_t* page_base = nullptr;  // PAGE tier cache of a disk-backed store (pageable)
+  uint64_t page_cap = 0;
+  FreeList page;
+  bool on_disk = false;
   uint8_t* backing_base = nullptr;
   uint64_t backing_bytes = 0;
   bool backing_is_pinned = false;
@@ -145,7 +151,7 @@ struct Store {
   std::unique_ptr<CopyPool> copy_pool;                           // pageable -> pinned bounce workers
   // demand mode (cfg.demand_mode = 1): the paper-literal Alg. 2 step 2 state machine
   std::unique_ptr<Alg2> alg2;
-  std::vector<std::pair<uint64_t, uint64_t>> pending_hbm_free, pending_pin_free;  // (offset, bytes)
+  std::vector<std::pair<uint64_t, uint64_t>> pending_hbm_free, pending_pin_free, pending_page_free;  // (off, bytes)
   cudaEvent_t start_ev = nullptr;
   // eager re-placement: asynchronous promotions (item becomes resident when its copy event completes)
   struct Promo {

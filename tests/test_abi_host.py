@@ -82,6 +82,13 @@ def test_policy_lists_vs_oracle():
         want[g] = 0
         want[p] = 1
         assert tiers.tolist() == want.tolist()
+        gb = int(rng.integers(0, 40)) << 20
+        tiers4 = hr.policy_lists_bytes4(order, sizes, hb, pb, gb)
+        L4 = placement.lists_by_bytes4(order, {i: int(sizes[i]) for i in range(n)}, hb, pb, gb)
+        want = np.empty(n, int)
+        for j, lst in enumerate(L4):
+            want[lst] = j
+        assert tiers4.tolist() == want.tolist()
         f = list(rng.choice([0.0, 0.05, 0.1, 0.2], 3))
         lists = hr.policy_lists_fraction(order, *f)
         L4 = placement.lists_by_fraction(order, *f)

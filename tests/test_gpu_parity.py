@@ -333,6 +333,48 @@ def test_demand_mode_matches_oracle_alg2(torch_cuda, backing_pinned):
     assert s["hbm_used"] <= hb and s["migrations_in"] > 0
 
 
+@pytest.mark.parametrize("page_items", [0, 4])
+def test_demand_mode_four_tiers_matches_oracle(torch_cuda, tmp_path, page_items):
+    """Disk-backed store in demand mode: all four lists and three queues of
+    Alg. 2 — a PAGE_LIST hit serves the pageable cache, a miss
+    reads the file and fills every queue its list names (R16, R26).  Per-tier
+    hit counts (DISK included) and queue contents match the oracle Alg2 after
+    every call; outputs stay bit-exact."""
+    import paper_2510_20878_b200 as hr
+    torch = torch_cuda
+    st, ora, lay, h, sizes = make_pair(torch, L=2, H=2, T=64, D=64, n_docs=16, ladder=NORTH, taus=(0.25, 0.25),
+                                       dtype="fp16")
+    path = str(tmp_path / "store4.hr")
+    st.save(path)
+    st.close()
+    order = hotness.rank_items(h)
+    hb = sum(sizes[i] for i in order[:8]) - 1
+    pb = sum(sizes[i] for i in order[8:12])
+    gb = sum(sizes[i] for i in order[12:12 + page_items])
+    ld = hr.Store(L=2, H=2, D=64, T=64, dtype="fp16", hbm_budget=hb, pin_budget=pb, page_budget=gb,
+                  disk_backing=True, demand_mode=True, keep_backing=False)
+    ld.build_from_file(path)
+    gl, pl, al, dl = placement.lists_by_bytes4(order, sizes, hb, pb, gb)
+    alg = placement.Alg2(gl, pl, al, (hb, pb, gb), sizes)
+    idx = {placement.GPU: 0, placement.PIN: 1, placement.PAGE: 2, placement.DISK: 3}
+    want = [0, 0, 0, 0]
+    for call in range(6):
+        reqs = synth.gen_requests(16, 5, 4, 1.1, seed=80 + call)
+        check_requests(torch, ld, ora, lay, reqs)
+        for req in reqs:
+            for doc in req:
+                for kind in (0, 1):
+                    want[idx[alg.access(2 * int(doc) + kind)[0]]] += 1
+        s = ld.stats()
+        assert s["hits"] == want[:3] and s["hits_disk"] == want[3], call
+        q = [set(alg.resident(t)) for t in (placement.GPU, placement.PIN, placement.PAGE)]
+        got = [ld.item_info(i)[1] for i in range(32)]
+        exp = [0 if i in q[0] else 1 if i in q[1] else 2 if i in q[2] else 3 for i in range(32)]
+        assert got == exp, call
+    assert want[3] > 0 and (page_items == 0 or want[2] > 0)
+    ld.close()
+
+
 # ------------------------------------------- BASELINE configs 2-4 at full shape
 def _sampled_check(torch, st, reqs, outs, lay, schemes, rng, n_slabs=2, src_heads=None):
     """Oracle decode of sampled (request, slot, kind, layer, head) slabs, one by one."""
@@ -586,8 +628,9 @@ def test_markstein_division_exhaustive(torch_cuda):
 
 
 # ----------------------------------------------------- persistence and the DISK tier
-@pytest.mark.parametrize("disk_backing,demand", [(False, False), (True, False), (True, True)])
-def test_save_load_and_disk_tier(torch_cuda, tmp_path, disk_backing, demand):
+@pytest.mark.parametrize("disk_backing,demand,page", [(False, False, 0), (True, False, 0), (True, True, 0),
+                                                       (True, False, 3), (True, True, 3)])
+def test_save_load_and_disk_tier(torch_cuda, tmp_path, disk_backing, demand, page):
     """hr_store_save / hr_build_from_file: compress once, load many.
     The loaded store keeps the saved schemes, places by its own budgets, and
     with disk_backing = 1 serves cold items from the file on every miss (the
@@ -601,15 +644,16 @@ def test_save_load_and_disk_tier(torch_cuda, tmp_path, disk_backing, demand):
     order = hotness.rank_items(h)
     hb = sum(sizes[i] for i in order[:6])
     pb = sum(sizes[i] for i in order[6:10])
+    gb = sum(sizes[i] for i in order[10:10 + page])     # PAGE_LIST cache of the disk-backed store (R26)
     ld = hr.Store(L=2, H=2, D=64, T=64, dtype="fp16", ladder=("INT8",), taus=(), hbm_budget=hb, pin_budget=pb,
-                  disk_backing=disk_backing, demand_mode=demand, keep_backing=not disk_backing)
+                  disk_backing=disk_backing, demand_mode=demand, keep_backing=not disk_backing, page_budget=gb)
     ld.build_from_file(path)
     for item in range(32):
         assert ld.item_info(item)[0] == st.item_info(item)[0]          # saved schemes, not the new ladder
         assert np.array_equal(ld.export_item(item), ora.blobs[item])
     if not demand:
-        want = placement.eager_tiers(h, sizes, hb, pb)
-        names = {0: placement.GPU, 1: placement.PIN, 2: placement.PAGE}
+        want = placement.eager_tiers(h, sizes, hb, pb, page_budget=gb if disk_backing else None)
+        names = {0: placement.GPU, 1: placement.PIN, 2: placement.PAGE, 3: placement.DISK}
         assert [names[ld.item_info(i)[1]] for i in range(32)] == want
     for epoch in range(3):
         reqs = synth.gen_requests(16, 24, 4, 1.1, seed=60 + epoch, perm_seed=70 + epoch)
@@ -617,6 +661,8 @@ def test_save_load_and_disk_tier(torch_cuda, tmp_path, disk_backing, demand):
         ld.replace()
     s = ld.stats()
     assert s["hits"][2] > 0 or s["hits"][1] > 0
+    if disk_backing:
+        assert s["hits_disk"] > 0
     ld.close()
     with open(path, "r+b") as f:   # corrupt the magic
         f.write(b"XXXX")

@@ -98,6 +98,21 @@ def test_lists_by_bytes():
     assert g == [] and p == [] and rest == order
 
 
+def test_lists_by_bytes4():
+    """R26: the PAGE_LIST is the next longest prefix that fits the page budget;
+    DISK_LIST the rest, order kept."""
+    order = [4, 0, 3, 1, 2, 5]
+    sizes = {0: 10, 1: 10, 2: 10, 3: 20, 4: 5, 5: 1}
+    g, p, a, d = placement.lists_by_bytes4(order, sizes, 16, 25, 15)
+    assert (g, p, a, d) == ([4, 0], [3], [1], [2, 5])   # 2 overflows PAGE: 5 (fits) still goes to DISK
+    g, p, a, d = placement.lists_by_bytes4(order, sizes, 0, 0, 0)
+    assert (g, p, a, d) == ([], [], [], order)
+    g, p, a, d = placement.lists_by_bytes4(order, sizes, 0, 0, 10 ** 9)
+    assert a == order and d == []
+    t = placement.eager_tiers([0, 0, 0, 0, 0, 0], [10] * 6, 10, 10, page_budget=20)
+    assert t == ["GPU", "PIN", "PAGE", "PAGE", "DISK", "DISK"]
+
+
 def _mk(n=4):
     g, p, a, _ = placement.lists_by_fraction(list(range(n)), 0.25, 0.25, 0.25)
     return placement.Alg2(g, p, a, (len(g), len(p), len(a)))
