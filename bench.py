@@ -592,6 +592,218 @@ def run_ablation(args, wl):
         print(json.dumps(line), flush=True)
 
 
+def fraction_budgets(hr, h, schemes, geo, t_gpu, t_pin, t_page=None):
+    """Byte budgets equal to Alg. 2's fraction lists: the bytes of the first
+    floor(t_gpu*M) ranked items, of the next floor(t_pin*M), (and of the next floor(t_page*M))."""
+    order = hr.policy_rank(h)
+    sz = {int(c): hr.item_bytes(int(c), **geo) for c in np.unique(schemes)}
+    M = len(order)
+    cuts = np.cumsum([0, int(t_gpu * M), int(t_pin * M)] + ([int(t_page * M)] if t_page is not None else []))
+    by = np.array([sz[int(schemes[i])] for i in order], dtype=np.int64)
+    return [int(by[cuts[j]:cuts[j + 1]].sum()) for j in range(len(cuts) - 1)]
+
+
+def run_tau_sweep(args, wl):
+    """Threshold sweeps of P:401-418 on the loading path: Alg. 1 Param1-4 (tau_1/2/3 = INT8/E4M3/E5M2
+    fractions, the rest GSE-8) at tau_GPU/PIN = 5/5%, then Alg. 2 Param1-2 (tau_GPU/PIN 5/5 vs 5/10)
+    at Alg. 1 Param1.  Corpus, requests and slow tier (pageable host DRAM) as in --ablation; the
+    TurboRAG arm (BF16 always from host) is the speedup denominator."""
+    import paper_2510_20878_b200 as hr
+    import synth
+    ctx = Ctx(args)
+    torch = ctx.torch
+    tv = dict(wl, **wl["tiered_variant"])
+    B, k = tv["batch"], tv["k"]
+    geo = dict(L=tv["L"], H=tv["H"], D=tv["D"], T=tv["T"], dtype=tv["dtype"], rank=ctx.rank, world=ctx.world)
+    pool = synth.gen_requests(tv["n_docs"], 8 * B, k, tv["s"], seed=1).reshape(8, B, k)
+    prof = synth.gen_requests(tv["n_docs"], 4 * tv["n_docs"], k, tv["s"], seed=7)
+    h = hr.policy_count(prof, tv["n_docs"]).astype(np.uint64)
+    alg1 = {"param1": (0.10, 0.05, 0.05), "param2": (0.10, 0.10, 0.05), "param3": (0.10, 0.10, 0.10),
+            "param4": (0.15, 0.10, 0.10)}
+    arms = {"turborag_bf16_from_host": (("PASS16",), (), 0.0, 0.0)}
+    for n, t in alg1.items():
+        arms[f"alg1_{n}"] = (PAPER_LADDER, t, 0.05, 0.05)
+    arms["alg2_param1"] = (PAPER_LADDER, alg1["param1"], 0.05, 0.05)
+    arms["alg2_param2"] = (PAPER_LADDER, alg1["param1"], 0.05, 0.10)
+    ko = vo = None
+    res = {}
+    for name, (ladder, taus, t_gpu, t_pin) in arms.items():
+        schemes = hr.policy_assign(h, ladder, taus)
+        hb, pb = fraction_budgets(hr, h, schemes, geo, t_gpu, t_pin)
+        w = dict(tv, ladder=ladder, taus=taus)
+        st, _, _, build_s, _ = build_store(ctx, w, hbm_budget=hb, pin_budget=pb, backing_pinned=False,
+                                           keep_backing=True, alias_R=tv["alias_R"], decay_shift=0)
+        if ko is None:
+            kvb = st.kv_bytes(k)
+            out = torch.empty(2 * B * kvb // 2, dtype=torch.int16, device="cuda")
+            ko = [out[(2 * r) * kvb // 2:(2 * r + 1) * kvb // 2] for r in range(B)]
+            vo = [out[(2 * r + 1) * kvb // 2:(2 * r + 2) * kvb // 2] for r in range(B)]
+        steps = max(3, min(args.steps, 10))
+        ms, tot, stats, _ = timed_steps(ctx, st, pool, ko, vo, steps, 3, 0, sample_clocks=False)
+        res[name] = {"taus_alg1": list(taus), "tau_gpu": t_gpu, "tau_pin": t_pin, "hbm_budget_GB": round(hb / 1e9, 1),
+                     "pin_budget_GB": round(pb / 1e9, 1), "ms_per_step": round(ms / steps, 2),
+                     "hits_per_tier": stats["hits"], "h2d_GB_per_step": round(stats["bytes_h2d"] / steps / 1e9, 3)}
+        st.close()
+    base = res["turborag_bf16_from_host"]["ms_per_step"]
+    for r in res.values():
+        r["speedup_vs_turborag"] = round(base / r["ms_per_step"], 2)
+    line = {"tau_sweep": res, "workload": "Llama-3-8B KV shape, 10,000-doc store, Zipf(1.1), top-k 10, batch 32; "
+            "slow tier = pageable host DRAM (backing aliased doc mod 250); Alg. 2 fractions turned into byte "
+            "budgets over the ranked items", "paper_context": "P:418 Param3 of Alg. 1 fastest; Alg. 2 Param1 and "
+            "Param2 both ~1.66x TTFT on A100 + disk"}
+    if ctx.rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def run_drift(args, wl):
+    """BASELINE config 5 (hotness drift): 100,000 docs, Zipf skew phases s = 0.6 -> 0.8 -> 1.0 -> 1.2
+    -> 0.6 of 4,096 requests each with a fresh doc permutation per phase, an epoch (hotness
+    all-reduce, decay, re-rank, re-placement) every 256 requests, with decay_shift 1 and 0 (pure
+    accumulation) as two arms.  One process holds the
+    per-rank slice of the 8-GPU run (1 of 8 KV heads: L=32, H=1, D=128, T=512), so per-rank bytes,
+    HBM budget (the hottest 5% of items, tau_GPU P:418) and link traffic are those of one of 8 ranks.
+    Reports the HBM hit rate and migration bytes per epoch and the recovery after each shift."""
+    import paper_2510_20878_b200 as hr
+    import synth
+    ctx = Ctx(args)
+    torch = ctx.torch
+    n_docs, k, B, L, D, T = 100_000, 10, 32, wl["L"], wl["D"], wl["T"]
+    phases = (0.6, 0.8, 1.0, 1.2, 0.6)
+    n_phase, epoch_req = env_int("HARAG_DRIFT_REQS", 4096), 256
+    seed = 5                                          # config index (SURVEY §8d)
+    geo = dict(L=L, H=1, D=D, T=T, dtype=wl["dtype"])
+    prof = synth.gen_requests(n_docs, 16384, k, phases[0], seed=99, perm_seed=seed ^ 0x9E3779B9)
+    h = hr.policy_count(prof, n_docs).astype(np.uint64)
+    schemes = hr.policy_assign(h, PAPER_LADDER, (0.1, 0.1, 0.1))
+    hb, _ = fraction_budgets(hr, h, schemes, geo, 0.05, 0.0)
+    alias = 2000
+    phase_reqs = [synth.gen_requests(n_docs, n_phase, k, s, seed=seed + 16 * p, perm_seed=seed ^ 0x9E3779B9 ^ p)
+                  for p, s in enumerate(phases)]
+
+    def src(doc, kp, vp, strm):
+        synth.gen_item_device(kp, L, 1, T, D, doc, 0, dtype=wl["dtype"], stream=strm, alias_R=alias)
+        synth.gen_item_device(vp, L, 1, T, D, doc, 1, dtype=wl["dtype"], stream=strm, alias_R=alias)
+
+    arms = {}
+    out = ko = vo = None
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for decay in [int(x) for x in os.environ.get("HARAG_DRIFT_DECAYS", "1,0").split(",")]:
+        st = hr.Store(ladder=PAPER_LADDER, taus=(0.1, 0.1, 0.1), device=ctx.device, hbm_budget=hb,
+                      backing_pinned=True, keep_backing=True, alias_R=alias, decay_shift=decay, **geo)
+        t0 = time.perf_counter()
+        st.build(n_docs, h, src, stream=ctx.stream)
+        torch.cuda.synchronize()
+        build_s = time.perf_counter() - t0
+        if out is None:
+            kvb = st.kv_bytes(k)
+            out = torch.empty(2 * B * kvb // 2, dtype=torch.int16, device="cuda")
+            ko = [out[(2 * r) * kvb // 2:(2 * r + 1) * kvb // 2] for r in range(B)]
+            vo = [out[(2 * r + 1) * kvb // 2:(2 * r + 2) * kvb // 2] for r in range(B)]
+        series = []
+        for p, s in enumerate(phases):
+            reqs = phase_reqs[p]
+            for e in range(n_phase // epoch_req):
+                st.reset_stats()
+                e0.record(ctx.stream)
+                for b in range(epoch_req // B):
+                    st.assemble(reqs[e * epoch_req + b * B:e * epoch_req + (b + 1) * B], ko, vo, stream=ctx.stream)
+                e1.record(ctx.stream)
+                e1.synchronize()
+                a_ms = e0.elapsed_time(e1)
+                stt = st.stats()
+                t1 = time.perf_counter()
+                st.replace(stream=ctx.stream)         # a9 (N = 1: the all-reduce is the identity)
+                torch.cuda.synchronize()              # promotions included
+                r_ms = (time.perf_counter() - t1) * 1e3
+                st2 = st.stats()
+                hits = stt["hits"]
+                series.append({"phase": p, "s": s, "epoch": e,
+                               "hbm_hit_rate": round(hits[0] / max(1, sum(hits)), 4),
+                               "assemble_ms": round(a_ms, 2), "ms_per_request": round(a_ms / epoch_req, 3),
+                               "h2d_GB": round(stt["bytes_h2d"] / 1e9, 3), "replace_ms": round(r_ms, 2),
+                               "migrated_GB": round((st2["bytes_migrated"] - stt["bytes_migrated"]) / 1e9, 3),
+                               "promoted": st2["migrations_in"] - stt["migrations_in"]})
+        st.close()
+        per_phase = []
+        for p, s in enumerate(phases):
+            rows = [r for r in series if r["phase"] == p]
+            tail = rows[len(rows) // 2:]
+            steady = statistics.median(r["hbm_hit_rate"] for r in tail)
+            rec = next((i for i, r in enumerate(rows) if r["hbm_hit_rate"] >= 0.95 * steady), len(rows))
+            per_phase.append({"s": s, "steady_hbm_hit_rate": steady, "first_epoch_hit_rate": rows[0]["hbm_hit_rate"],
+                              "recovery_requests": rec * epoch_req,
+                              "ms_per_request_steady": round(statistics.median(r["ms_per_request"] for r in tail), 3),
+                              "migrated_GB_per_epoch": round(statistics.mean(r["migrated_GB"] for r in rows), 3),
+                              "replace_ms_median": round(statistics.median(r["replace_ms"] for r in rows), 1)})
+        arms[f"decay_shift_{decay}"] = {"phases": per_phase, "epochs": series, "build_seconds": round(build_s, 1)}
+    line = {"drift": {"arms": arms, "hbm_budget_GB": round(hb / 1e9, 2), "n_docs": n_docs,
+                      "requests_per_phase": n_phase, "epoch_requests": epoch_req, "batch": B, "k": k},
+            "workload": "BASELINE config 5 per-rank slice: 100,000 docs of Llama-3-8B KV shape, 1 of 8 KV heads "
+                        "(L=32, H=1, D=128, T=512), paper ladder, HBM = hottest 5% of items, cold in pinned host "
+                        "DRAM (backing aliased doc mod 2000), Zipf phases 0.6/0.8/1.0/1.2/0.6; replace_ms includes "
+                        "the promotions' H2D copies"}
+    if ctx.rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def run_analysis(args, wl):
+    """Analysis tooling on the C2 corpus: exponent distribution and top-k
+    coverage per kind, and the RMSE of Eq. per scheme and GSE layout
+    (Fig. rmse_comparison; GSE layouts P:327), over a sample of docs, on the GPU.  Also
+    times the exponent-histogram kernel against the HBM roofline (2 B read per value)."""
+    import paper_2510_20878_b200 as hr
+    import synth
+    ctx = Ctx(args)
+    torch = ctx.torch
+    L, H, D, T = wl["L"], wl["H"], wl["D"], wl["T"]
+    n_docs = env_int("HARAG_ANALYSIS_DOCS", 32)
+    n = L * H * T * D
+    buf = torch.empty(n, dtype=torch.int16, device="cuda")
+    hist = {0: torch.zeros(256, dtype=torch.int64, device="cuda"), 1: torch.zeros(256, dtype=torch.int64, device="cuda")}
+    variants = [("INT8", (4, 3)), ("FP8E4M3", (4, 3)), ("FP8E5M2", (4, 3)), ("GSE8", (4, 3)), ("GSE8", (3, 4)),
+                ("GSE8", (2, 5)), ("INT4", (4, 3))]
+    rm = {(s, g, kind): [] for s, g in variants for kind in (0, 1)}
+    hk_ms, hk_n = 0.0, 0
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    for doc in range(n_docs):
+        for kind in (0, 1):
+            synth.gen_item_device(buf.data_ptr(), L, H, T, D, doc * 37, kind, dtype=wl["dtype"],
+                                  stream=ctx.stream.cuda_stream)
+            e0.record(ctx.stream)
+            hr.exponent_histogram(buf, n, dtype=wl["dtype"], hist=hist[kind], stream=ctx.stream)
+            e1.record(ctx.stream)
+            e1.synchronize()
+            hk_ms += e0.elapsed_time(e1)
+            hk_n += 1
+            for s, g in variants:
+                sse, _ = hr.scheme_error(s, buf, stream=ctx.stream, L=L, H=H, D=D, T=T, dtype=wl["dtype"], gse=g)
+                rm[(s, g, kind)].append(float(np.sqrt(sse / n)))
+    wall = time.perf_counter() - t0
+    cov = {}
+    for kind in (0, 1):
+        h = hist[kind].cpu().numpy().astype(np.float64)
+        h[0] = 0
+        srt = np.sort(h)[::-1] / h.sum()
+        cov["K" if kind == 0 else "V"] = {f"top{k}": round(float(srt[:k].sum()), 4) for k in (4, 6, 8, 10)}
+    rmse = {}
+    for (s, g, kind), v in rm.items():
+        name = s if s != "GSE8" else f"GSE8_1+{g[0]}+{g[1]}"
+        rmse.setdefault(name, {})["K" if kind == 0 else "V"] = {"mean": float(np.mean(v)), "max": float(np.max(v))}
+    peak = measured_hbm_peak()[0]
+    gbs = 2 * n / (hk_ms / hk_n / 1e3) / 1e9
+    line = {"analysis": {"docs": n_docs, "exponent_topk_coverage": cov, "rmse_per_scheme": rmse,
+                         "exponent_hist_kernel": {"GBps": round(gbs, 1), "frac_of_hbm_peak": round(gbs / peak, 3),
+                                                  "avg_ms": round(hk_ms / hk_n, 4), "bytes_per_launch": 2 * n},
+                         "wall_s": round(wall, 1)},
+            "workload": f"Llama-3-8B KV shape items (L={L}, H={H}, T={T}, D={D}, {wl['dtype']}), {n_docs} docs x K/V, "
+                        "synthetic generator (SURVEY §8d)",
+            "paper_context": "P:133 top-8 exponents cover 96-97% (K) / 95-96% (V) on MS MARCO; P:349 RMSE order "
+                             "INT8 < E4M3 < E5M2 < GSE-8"}
+    if ctx.rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def run_disk_leg(args, wl):
     """The DISK tier: a 500-doc store saved to disk, reloaded with disk_backing, a
     small HBM hot set; every miss is read from the file (O_DIRECT pieces) -> pinned bounce -> HBM."""
@@ -610,25 +822,34 @@ def run_disk_leg(args, wl):
     save_s = time.perf_counter() - t0
     st.close()
     geo = dict(L=w["L"], H=w["H"], D=w["D"], T=w["T"], dtype=w["dtype"], rank=ctx.rank, world=ctx.world)
-    ld = hr.Store(ladder=w["ladder"], taus=w["taus"], device=ctx.device, hbm_budget=total // 10, disk_backing=True,
-                  keep_backing=False, decay_shift=0, **geo)
-    t0 = time.perf_counter()
-    ld.build_from_file(path, stream=ctx.stream)
-    load_s = time.perf_counter() - t0
     B, k = 8, w["k"]
-    kvb = ld.kv_bytes(k)
-    out = torch.empty(2 * B * kvb // 2, dtype=torch.int16, device="cuda")
-    ko = [out[(2 * r) * kvb // 2:(2 * r + 1) * kvb // 2] for r in range(B)]
-    vo = [out[(2 * r + 1) * kvb // 2:(2 * r + 2) * kvb // 2] for r in range(B)]
     pool = synth.gen_requests(500, 8 * B, k, w["s"], seed=1).reshape(8, B, k)
-    ms, tot, stats, _ = timed_steps(ctx, ld, pool, ko, vo, 5, 3, 0, sample_clocks=False)
-    res = {"disk_leg": {"n_docs": 500, "file_GB": round(total / 1e9, 1), "save_s": round(save_s, 1),
-                        "load_s": round(load_s, 1), "ms_per_step": round(ms / 5, 1), "batch": B, "k": k,
-                        "hits_per_tier": stats["hits"],
-                        "disk_GBps": round(stats["bytes_h2d"] / (stats["h2d_ms"] / 1e3) / 1e9, 2)
-                        if stats["h2d_ms"] else None,
-                        "o_direct_dir": d}}
-    ld.close()
+    res = {"disk_leg": {"n_docs": 500, "file_GB": round(total / 1e9, 1), "save_s": round(save_s, 1), "batch": B,
+                        "k": k, "o_direct_dir": d}}
+    arms = {  # eager HBM + DISK; paper-literal 4-tier Alg. 2 (R26): HBM / pinned / pageable PAGE cache / DISK
+        "eager_hbm_disk": dict(hbm_budget=total // 10),
+        "demand_4tier": dict(hbm_budget=total // 10, pin_budget=total // 10, page_budget=total // 5,
+                             demand_mode=True),
+    }
+    out = ko = vo = None
+    for name, over in arms.items():
+        ld = hr.Store(ladder=w["ladder"], taus=w["taus"], device=ctx.device, disk_backing=True, keep_backing=False,
+                      decay_shift=0, **over, **geo)
+        t0 = time.perf_counter()
+        ld.build_from_file(path, stream=ctx.stream)
+        load_s = time.perf_counter() - t0
+        if out is None:
+            kvb = ld.kv_bytes(k)
+            out = torch.empty(2 * B * kvb // 2, dtype=torch.int16, device="cuda")
+            ko = [out[(2 * r) * kvb // 2:(2 * r + 1) * kvb // 2] for r in range(B)]
+            vo = [out[(2 * r + 1) * kvb // 2:(2 * r + 2) * kvb // 2] for r in range(B)]
+        ms, tot, stats, _ = timed_steps(ctx, ld, pool, ko, vo, 5, 3, 0, sample_clocks=False)
+        res["disk_leg"][name] = {
+            "load_s": round(load_s, 1), "ms_per_step": round(ms / 5, 1),
+            "hits_per_tier": stats["hits"] + [stats["hits_disk"]],
+            "host_GBps": round(stats["bytes_h2d"] / (stats["h2d_ms"] / 1e3) / 1e9, 2) if stats["h2d_ms"] else None,
+            "budgets_GB": {kk: round(v / 1e9, 2) for kk, v in over.items() if kk.endswith("budget")}}
+        ld.close()
     os.remove(path)
     if ctx.rank == 0:
         print(json.dumps(res), flush=True)
@@ -651,6 +872,9 @@ def main():
                     help="host-tier leg with a pageable backing (bounce through pinned memory)")
     ap.add_argument("--ablation", action="store_true", help="run the paper's ablation arms (P:476-485) instead")
     ap.add_argument("--disk-leg", action="store_true", help="run the DISK-tier leg (save, reload disk-backed) instead")
+    ap.add_argument("--tau-sweep", action="store_true", help="run the threshold sweeps of P:401-418 instead")
+    ap.add_argument("--drift", action="store_true", help="run BASELINE config 5 (hotness drift) instead")
+    ap.add_argument("--analysis", action="store_true", help="run the exponent / RMSE analysis leg instead")
     ap.add_argument("--ncu-traffic", type=float, default=None,
                     help="dram read+write bytes per launch from an ncu --set full capture (profiles/)")
     args = ap.parse_args()
@@ -665,6 +889,12 @@ def main():
         run_ablation(args, wl)
     elif args.disk_leg:
         run_disk_leg(args, wl)
+    elif args.tau_sweep:
+        run_tau_sweep(args, wl)
+    elif args.drift:
+        run_drift(args, wl)
+    elif args.analysis:
+        run_analysis(args, wl)
     else:
         run_ours(args, wl)
 

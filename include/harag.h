@@ -189,6 +189,31 @@ hr_status hr_assemble_kv(hr_store* s, uint32_t n_req, uint32_t k, const uint32_t
 hr_status hr_hotness_delta(hr_store* s, int64_t** dev_ptr, uint32_t* n);
 hr_status hr_replace(hr_store* s, void* stream);
 
+/* Consumer of the assembled KV: for each request r the
+ * attention of its query rows over its k retrieved chunks — the cross-attention
+ * a TurboRAG / HA-RAG prefill runs over the precomputed chunk KV —
+ * computed straight from the packed codes (gather + dequantise fused into the
+ * kernel; the KV cache of hr_assemble_kv is never materialised):
+ *   O[r][l][hq][i][:] = sum_j softmax_j(scale * <Q[r][l][hq][i], K_j>) V_j,
+ *   lse[r][l][hq][i]  = log sum_j exp(scale * <Q[r][l][hq][i], K_j>)  (natural log),
+ * j over the k*T keys of docs ids[r][0..k) in request order, K_j / V_j the
+ * decoded values of hr_assemble_kv (bit for bit), query head hq of this rank
+ * reading local KV head hq / g (GQA).
+ *   q_dev:   device [n_req][L][Hl*g][n_q][D] of cfg->dtype (16-byte aligned);
+ *   o_dev:   device, same layout and dtype; lse_dev: device float32
+ *            [n_req][L][Hl*g][n_q], or NULL;
+ *   scale:   softmax scale (<= 0 -> 1/sqrt(D));
+ *   kv_dump: NULL (test hook: device [n_req][2][L][Hl][k*T][D], receives the
+ *            decoded K and V exactly as hr_assemble_kv would write them).
+ * Needs g * n_q <= 128, D in {64, 128}, T a multiple of 64, eager placement and
+ * every requested item resident in HBM (HR_ESTATE otherwise, before any launch);
+ * duplicate / unknown ids as hr_assemble_kv.  Stream-ordered; counts hotness
+ * like hr_assemble_kv (a1).  Arithmetic: bf16/fp16 tensor-core products, fp32
+ * accumulation, probabilities rounded to the dtype before P.V. */
+hr_status hr_attend(hr_store* s, uint32_t n_req, uint32_t k, const uint32_t* doc_ids, const void* q_dev,
+                    uint32_t n_q, uint32_t g, void* o_dev, float* lse_dev, float scale, void* kv_dump,
+                    void* stream);
+
 /* ------------------------------------------------------------ persistence
  * Compress once, load many (compressed chunks are stored on disk).
  * hr_store_save writes a built store: a 4 KiB-aligned header (magic
@@ -237,6 +262,24 @@ hr_status hr_policy_count(uint32_t n_req, uint32_t k, const uint32_t* ids, uint3
 hr_status hr_policy_epoch(uint32_t n_items, uint64_t* h_inout, const int64_t* delta, uint32_t decay_shift);
 /* Packed blob size of one item for a config and scheme. */
 hr_status hr_item_bytes(const hr_store_config* cfg, uint32_t scheme, uint64_t* bytes);
+
+/* ---- analysis tooling -------------------------------
+ * hr_exponent_histogram: hist_dev[b] += number of the n 16-bit values at src_dev
+ * (device, dtype hr_dtype) whose biased exponent field is b (bf16: bits 14..7,
+ * 256 bins; fp16: bits 14..10, 32 bins used) — the exponent distribution of
+ * P:131-133 (Fig. KV-exponent-range); zeros/subnormals land in bin 0.
+ * hist_dev: device uint64[256], accumulated (the caller zeroes it).  Stream-
+ * ordered; src_dev 16-byte aligned for full speed (any alignment is correct). */
+hr_status hr_exponent_histogram(uint32_t dtype, const void* src_dev, uint64_t n, uint64_t* hist_dev, void* stream);
+/* hr_scheme_error: compress one item with `scheme` exactly as hr_build_store
+ * would (cfg's geometry, group, GSE layout and this rank's heads of src_dev,
+ * device [L][H][T][D] of cfg->dtype), decode it with the assemble kernel, and
+ * write out_host[0] = sum over elements of (x_i - x^_i)^2 (fp64), out_host[1] =
+ * max |x_i - x^_i|; RMSE of Eq. = sqrt(out_host[0] / (L*Hl*T*D)).
+ * Synchronous (returns after the stream drains).  HR_EINVAL on NaN/Inf input or
+ * a bad config / scheme; temporary device memory is freed before returning. */
+hr_status hr_scheme_error(const hr_store_config* cfg, uint32_t scheme, const void* src_dev, double* out_host,
+                          void* stream);
 
 /* Alg. 2 step 2 demand-mode state machine.  list_of_item: 0 GPU,
  * 1 PIN, 2 PAGE, 3 DISK; sizes: bytes per item (NULL = 1 each); caps in the

@@ -17,7 +17,8 @@ from ._lib import (FP8E4M3, FP8E5M2, GSE8, HR_BF16, HR_FP16, INT4, INT8, PASS16,
 
 __all__ = ["Store", "HaragError", "SCHEMES", "PASS16", "INT8", "FP8E4M3", "FP8E5M2", "GSE8", "INT4",
            "T_HBM", "T_PIN", "T_PAGE", "T_DISK", "policy_rank", "policy_lists_bytes4", "policy_assign", "policy_lists_bytes",
-           "policy_lists_fraction", "policy_count", "policy_epoch", "item_bytes", "Alg2"]
+           "policy_lists_fraction", "policy_count", "policy_epoch", "item_bytes", "Alg2",
+           "exponent_histogram", "scheme_error"]
 
 
 def _ptr(x) -> int:
@@ -140,6 +141,18 @@ class Store:
         kp = (C.c_void_p * n_req)(*[_ptr(x) for x in k_out])
         vp = (C.c_void_p * n_req)(*[_ptr(x) for x in v_out])
         check(lib.hr_assemble_kv(self._h, n_req, k, _p(ids, C.c_uint32), kp, vp, _stream(stream)))
+
+    def attend(self, ids, q, o, n_q: int, g: int, lse=None, scale: float = 0.0, kv_dump=None,
+               stream=None) -> None:
+        """Attention of each request's query rows over its retrieved chunks, straight from the
+        packed codes (hr_attend).  q / o: device [n_req][L][Hl*g][n_q][D]; lse: device float32
+        [n_req][L][Hl*g][n_q] or None; scale <= 0 -> 1/sqrt(D)."""
+        ids = _u32(ids)
+        if ids.ndim != 2:
+            raise ValueError("ids must be [n_req][k]")
+        n_req, k = ids.shape
+        check(lib.hr_attend(self._h, n_req, k, _p(ids, C.c_uint32), _ptr(q), int(n_q), int(g), _ptr(o),
+                            _ptr(lse), float(scale), _ptr(kv_dump), _stream(stream)))
 
     # ------------------------------------------------------------ epochs
     def hotness_delta_ptr(self) -> tuple[int, int]:
@@ -267,6 +280,29 @@ def item_bytes(scheme, **cfg) -> int:
     b = C.c_uint64()
     check(lib.hr_item_bytes(C.byref(c), SCHEMES[scheme] if isinstance(scheme, str) else scheme, C.byref(b)))
     return b.value
+
+
+def exponent_histogram(src, n: int, dtype: str = "bf16", hist=None, stream=None):
+    """hist[b] += count of the n 16-bit values at device address/tensor `src` whose biased
+    exponent field is b.  `hist`: device uint64[256] (int64 tensor) to accumulate
+    into; a fresh zeroed torch tensor on src's device when None (returned)."""
+    if hist is None:
+        import torch
+        hist = torch.zeros(256, dtype=torch.int64, device=src.device)
+    check(lib.hr_exponent_histogram(HR_BF16 if dtype == "bf16" else HR_FP16, _ptr(src), int(n), _ptr(hist),
+                                    _stream(stream)))
+    return hist
+
+
+def scheme_error(scheme, src, stream=None, **cfg) -> tuple[float, float]:
+    """(sum of squared errors, max |error|) of one item (device [L][H][T][D], this rank's heads)
+    compressed with `scheme` and decoded by the assemble kernel — Eq. before the
+    1/N and the square root.  Synchronous."""
+    c = make_config(**cfg)
+    out = (C.c_double * 2)()
+    check(lib.hr_scheme_error(C.byref(c), SCHEMES[scheme] if isinstance(scheme, str) else scheme, _ptr(src), out,
+                              _stream(stream)))
+    return float(out[0]), float(out[1])
 
 
 class Alg2:

@@ -69,6 +69,7 @@ _SIGS = {
     "hr_assemble_kv": (I32, [P, U32, U32, PU32, C.POINTER(P), C.POINTER(P), P]),
     "hr_hotness_delta": (I32, [P, C.POINTER(PI64), PU32]),
     "hr_replace": (I32, [P, P]),
+    "hr_attend": (I32, [P, U32, U32, PU32, P, U32, U32, P, P, C.c_float, P, P]),
     "hr_store_save": (I32, [P, C.c_char_p]),
     "hr_build_from_file": (I32, [P, C.c_char_p, P]),
     "hr_item_info": (I32, [P, U32, PU32, PU32, PU64]),
@@ -85,6 +86,8 @@ _SIGS = {
     "hr_policy_count": (I32, [U32, U32, PU32, U32, U64, U32, U32, PI64]),
     "hr_policy_epoch": (I32, [U32, PU64, PI64, U32]),
     "hr_item_bytes": (I32, [C.POINTER(Config), U32, PU64]),
+    "hr_exponent_histogram": (I32, [U32, P, U64, P, P]),
+    "hr_scheme_error": (I32, [C.POINTER(Config), U32, P, C.POINTER(C.c_double), P]),
     "hr_alg2_create": (I32, [U32, PU32, PU64, U64, U64, U64, C.POINTER(P)]),
     "hr_alg2_access": (I32, [P, U32, PU32, PU32, PU32, U32, PU32]),
     "hr_alg2_set_lists": (I32, [P, PU32]),

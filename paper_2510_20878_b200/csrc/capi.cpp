@@ -7,6 +7,7 @@
 #include <new>
 #include <string>
 
+#include "analysis.h"
 #include "harag.h"
 #include "layout.h"
 #include "policy.h"
@@ -123,6 +124,15 @@ hr_status hr_hotness_delta(hr_store* s, int64_t** dev_ptr, uint32_t* n) {
     *n = s->impl.n_items;
   });
 }
+hr_status hr_attend(hr_store* s, uint32_t n_req, uint32_t k, const uint32_t* doc_ids, const void* q_dev,
+                    uint32_t n_q, uint32_t g, void* o_dev, float* lse_dev, float scale, void* kv_dump,
+                    void* stream) {
+  return guard([&] {
+    NONNULL(s);
+    s->impl.attend(n_req, k, doc_ids, q_dev, n_q, g, o_dev, lse_dev, scale, kv_dump, S(stream));
+  });
+}
+
 hr_status hr_replace(hr_store* s, void* stream) {
   return guard([&] {
     NONNULL(s);
@@ -272,6 +282,25 @@ hr_status hr_item_bytes(const hr_store_config* cfg, uint32_t scheme, uint64_t* b
     NONNULL(bytes);
     harag::require(scheme <= HR_S_INT4, HR_EINVAL, "unknown scheme");
     *bytes = harag::make_layout(*cfg).item_bytes(scheme);
+  });
+}
+
+hr_status hr_exponent_histogram(uint32_t dtype, const void* src_dev, uint64_t n, uint64_t* hist_dev, void* stream) {
+  return guard([&] {
+    NONNULL(hist_dev);
+    harag::require(dtype == HR_BF16 || dtype == HR_FP16, HR_EINVAL, "dtype must be HR_BF16 or HR_FP16");
+    if (n == 0) return;
+    NONNULL(src_dev);
+    harag::launch_exponent_hist(dtype, src_dev, n, reinterpret_cast<unsigned long long*>(hist_dev), S(stream));
+    HR_CUDA(cudaGetLastError());
+  });
+}
+
+hr_status hr_scheme_error(const hr_store_config* cfg, uint32_t scheme, const void* src_dev, double* out_host,
+                          void* stream) {
+  return guard([&] {
+    NONNULL(cfg);
+    harag::scheme_error(*cfg, scheme, src_dev, out_host, S(stream));
   });
 }
 

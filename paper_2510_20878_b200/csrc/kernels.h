@@ -67,4 +67,20 @@ struct QuantParams {
 // a3 + a4: one CTA per (layer, local head) slab.
 void launch_quantize(const QuantParams& p, cudaStream_t stream);
 
+// Consumer: attention of each request's query rows over its retrieved
+// chunks, decoding the packed codes inside the kernel (kernels/attend.cu).
+struct AttnParams {
+  const AsmDesc* descs;      // [n_req][k][2] (K, V) of HBM-resident items; count = hotness counter or nullptr
+  const uint16_t* q;         // [n_req][L][Hl*g][n_q][D]
+  uint16_t* o;               // same layout as q
+  float* lse;                // [n_req][L][Hl*g][n_q] natural-log sum of exp of the scaled scores, or nullptr
+  uint16_t* kv_dump;         // test hook: decoded KV [n_req][2][L][Hl][k*T][D], or nullptr
+  uint32_t n_req, k, L, Hl, T, D, g, n_q, M;  // M = g * n_q <= 128
+  uint32_t G, g_shift, gse_e, gse_m, dtype;
+  float scale_log2;          // softmax scale * log2(e)
+  uint64_t code_slab[6];     // per scheme, code bytes per slab
+  uint32_t meta_stride[6];   // per scheme, bytes per slab meta record
+};
+void launch_attend(const AttnParams& p, cudaStream_t stream);
+
 }  // namespace harag

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <fcntl.h>
 #include <unistd.h>
 
@@ -651,6 +652,90 @@ void Store::poll_promotions(bool wait_all) {
 // launch reads an evicted item from HBM.  Promotions are asynchronous: an item becomes resident
 // when its copy event has completed (polled at the next hr_assemble_kv), and until then it is
 // streamed from the host like any host-tier item — requests never wait for a migration.
+// Consumer: attention over the request's packed chunks (kernels/attend.cu).
+// Every requested item must be resident in the HBM arena (eager placement).
+void Store::attend(uint32_t n_req, uint32_t k, const uint32_t* ids, const void* q, uint32_t n_q, uint32_t g,
+                   void* o, float* lse, float scale, void* kv_dump, cudaStream_t st) {
+  require(state == State::Built, HR_ESTATE, "hr_attend before the store is built");
+  require(!alg2, HR_ESTATE, "hr_attend needs eager placement (demand_mode = 0)");
+  require(q && o, HR_EINVAL, "NULL query or output pointer");
+  require(((uintptr_t)q & 15) == 0 && ((uintptr_t)o & 15) == 0 && ((uintptr_t)kv_dump & 15) == 0, HR_EINVAL,
+          "query / output pointers must be 16-byte aligned");
+  require(g >= 1 && n_q >= 1 && (uint64_t)g * n_q <= 128, HR_EINVAL, "g * n_q must be in [1, 128]");
+  require(lay.D == 64 || lay.D == 128, HR_EINVAL, "hr_attend: head_dim must be 64 or 128");
+  require(lay.T % 64 == 0, HR_EINVAL, "hr_attend: tokens per chunk must be a multiple of 64");
+  require(n_req == 0 || (k >= 1 && ids), HR_EINVAL, "bad request");
+  std::vector<uint32_t> tmp(k);
+  for (uint32_t r = 0; r < n_req; ++r) {
+    for (uint32_t j = 0; j < k; ++j) {
+      tmp[j] = ids[(uint64_t)r * k + j];
+      require(tmp[j] < n_docs, HR_ENOTFOUND, "unknown doc id " + std::to_string(tmp[j]));
+    }
+    std::sort(tmp.begin(), tmp.end());
+    require(std::adjacent_find(tmp.begin(), tmp.end()) == tmp.end(), HR_EINVAL,
+            "duplicate doc id in request " + std::to_string(r) + " (R19)");
+  }
+  HR_CUDA(cudaSetDevice(cfg.device));
+  if (!promos.empty()) poll_promotions(false);
+  for (uint64_t i = 0; i < (uint64_t)n_req * k; ++i)
+    for (uint32_t kind = 0; kind < 2; ++kind)
+      require(loc[2 * ids[i] + kind].hbm_off != FreeList::kNone, HR_ESTATE,
+              "hr_attend: item " + std::to_string(2 * ids[i] + kind) + " is not resident in HBM");
+  if (n_req == 0) return;
+  const size_t n_desc = 2ull * n_req * k;
+  DescBuf& db = desc_buffer(n_desc);
+  for (uint32_t r = 0; r < n_req; ++r) {
+    const bool counted = ((req_counter + r) % (uint64_t)cfg.world) == (uint64_t)cfg.rank;
+    for (uint32_t j = 0; j < k; ++j)
+      for (uint32_t kind = 0; kind < 2; ++kind) {
+        const uint32_t item = 2 * ids[(uint64_t)r * k + j] + kind;
+        AsmDesc d{};
+        d.codes = hbm_ptr(item);
+        d.meta = d.codes + lay.meta_offset(scheme[item]);
+        d.count = counted ? reinterpret_cast<unsigned long long*>(delta + item) : nullptr;
+        d.slot = j;
+        d.scheme = scheme[item];
+        db.host[((uint64_t)r * k + j) * 2 + kind] = d;
+        stats.hits[HR_T_HBM]++;
+        stats.bytes_hbm_alg += bytes_read_alg(item);
+      }
+  }
+  HR_CUDA(cudaMemcpyAsync(db.dev, db.host, n_desc * sizeof(AsmDesc), cudaMemcpyHostToDevice, st));
+  AttnParams p{};
+  p.descs = db.dev;
+  p.q = static_cast<const uint16_t*>(q);
+  p.o = static_cast<uint16_t*>(o);
+  p.lse = lse;
+  p.kv_dump = static_cast<uint16_t*>(kv_dump);
+  p.n_req = n_req, p.k = k, p.L = lay.L, p.Hl = lay.Hl, p.T = lay.T, p.D = lay.D, p.g = g, p.n_q = n_q;
+  p.M = g * n_q;
+  p.G = lay.G, p.g_shift = (uint32_t)__builtin_ctz(lay.G), p.gse_e = lay.gse_e, p.gse_m = lay.gse_m;
+  p.dtype = lay.dtype;
+  const float sc = scale > 0.f ? scale : 1.f / std::sqrt((float)lay.D);
+  p.scale_log2 = sc * 1.4426950408889634f;
+  for (uint32_t s = 0; s <= HR_S_INT4; ++s) {
+    p.code_slab[s] = lay.code_bytes_slab(s);
+    p.meta_stride[s] = (uint32_t)lay.meta_stride(s);
+  }
+  // q read + o written (algorithmic), beside the codes + meta counted above
+  stats.bytes_hbm_alg += 2ull * 2 * n_req * lay.L * lay.Hl * g * n_q * lay.D;
+  cudaEvent_t a = nullptr, b = nullptr;
+  if (timing) {
+    HR_CUDA(cudaEventCreate(&a));
+    HR_CUDA(cudaEventCreate(&b));
+    HR_CUDA(cudaEventRecord(a, st));
+  }
+  launch_attend(p, st);
+  if (timing) {
+    HR_CUDA(cudaEventRecord(b, st));
+    timers.emplace_back(a, b);
+  }
+  stats.kernel_launches++;
+  HR_CUDA(cudaEventRecord(db.done, st));
+  req_counter += n_req;
+  stats.requests += n_req;
+}
+
 void Store::replace(cudaStream_t st) {
   require(state == State::Built, HR_ESTATE, "hr_replace before the store is built");
   HR_CUDA(cudaSetDevice(cfg.device));

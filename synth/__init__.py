@@ -92,6 +92,29 @@ def gen_item(L: int, H: int, T: int, D: int, doc: int, kind: int, *,
     raise ValueError(dtype)
 
 
+QUERY_SEED = 0x51554552  # "QUER"
+Q_UNIT = np.float32(1.0 / 37837.0)
+
+
+def gen_query(n_req: int, L: int, HQ: int, n_q: int, D: int, *, seed: int = QUERY_SEED,
+              dtype: str = "bf16") -> np.ndarray:
+    """Bit patterns (uint16) of synthetic query rows [n_req][L][HQ][n_q][D] for the attention
+    consumer: the same Irwin-Hall counter recipe as gen_item with unit
+    standard deviation (scores s = <q, k>/sqrt(D) then have the spread of K's values)."""
+    idx = np.arange(n_req * L * HQ * n_q * D, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        u = splitmix64(np.uint64(seed) ^ idx)
+    m16 = np.uint64(0xFFFF)
+    b = ((u & m16) + ((u >> np.uint64(16)) & m16) + ((u >> np.uint64(32)) & m16)
+         + (u >> np.uint64(48))).astype(np.int64) - 131070
+    x = (b.astype(np.float32) * Q_UNIT).astype(np.float32).reshape(n_req, L, HQ, n_q, D)
+    if dtype == "bf16":
+        return _f32_to_bf16_bits_gen(x)
+    if dtype == "fp16":
+        return x.astype(np.float16).view(np.uint16)
+    raise ValueError(dtype)
+
+
 def zipf_permutation(n_docs: int, seed: int) -> np.ndarray:
     return np.random.Generator(np.random.PCG64(seed ^ 0x9E3779B9)).permutation(n_docs)
 

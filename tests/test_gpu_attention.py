@@ -1,0 +1,190 @@
+"""GPU parity of the attention consumer (hr_attend) against
+the oracle (oracle/attention.py over oracle.store.assemble).
+
+The decoded K/V the kernel feeds its tensor cores are compared BIT-EXACTLY with
+the oracle's assembled KV (kv_dump hook).  O and LSE are floating-point results
+of a different summation (tensor-core fp32 accumulation, probabilities rounded
+to the 16-bit dtype before P.V) and are held to the bound DESIGN.md R28 derives:
+|O - O*| <= 2^-8 * max_j |v_j - O*| + 2^-8 |O*| (bf16; 2^-10 for fp16 P) per
+element, |LSE - LSE*| <= 2^-8."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import attention, hotness
+from oracle import store as ost
+
+pytestmark = pytest.mark.gpu
+
+NAMES = {"PASS16": ost.PASS16, "INT8": ost.INT8, "FP8E4M3": ost.FP8E4M3, "FP8E5M2": ost.FP8E5M2,
+         "GSE8": ost.GSE8, "INT4": ost.INT4}
+PAPER = ("INT8", "FP8E4M3", "FP8E5M2", "GSE8")
+NORTH = ("PASS16", "INT8", "INT4")
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+def build(torch, *, L, H, T, D, n_docs, ladder, taus, dtype, group=0, rank=0, world=1, demand=False,
+          hbm_items=None):
+    import paper_2510_20878_b200 as hr
+    prof = synth.gen_requests(n_docs, 4 * n_docs, min(4, n_docs), 1.1, seed=7)
+    h = hotness.count_requests(prof, n_docs).astype(np.uint64)
+    lay = ost.Layout(L=L, H=H, T=T, D=D, dtype=dtype, group=group, rank=rank, world=world)
+    schemes = hotness.assign_schemes(h.tolist(), [NAMES[s] for s in ladder], taus)
+    sizes = [lay.item_bytes(s) for s in schemes]
+    order = hotness.rank_items(h)
+    hb = sum(sizes) + 4096 if hbm_items is None else sum(sizes[i] for i in order[:hbm_items])
+    st = hr.Store(L=L, H=H, D=D, T=T, dtype=dtype, group=group, ladder=ladder, taus=taus, hbm_budget=hb,
+                  rank=rank, world=world, demand_mode=demand)
+
+    def src(doc, kp, vp, stream):
+        synth.gen_item_device(kp, L, H, T, D, doc, 0, dtype=dtype, stream=stream)
+        synth.gen_item_device(vp, L, H, T, D, doc, 1, dtype=dtype, stream=stream)
+
+    st.build(n_docs, h, src)
+    ora = ost.OracleStore(lay, [NAMES[s] for s in ladder], taus)
+    ora.build(n_docs, h, lambda d, k: synth.gen_item(L, H, T, D, d, k, heads=lay.heads, dtype=dtype))
+    return st, ora, lay
+
+
+def check_bound(O_gpu, lse_gpu, O, lse, V_range, dtype):
+    eps = 2.0 ** -8 if dtype == "bf16" else 2.0 ** -10
+    tol = eps * V_range + 2.0 ** -8 * np.abs(O) + 1e-6
+    err = np.abs(O_gpu - O)
+    assert np.all(err <= tol), f"max err {err.max()} vs tol {tol[np.unravel_index(np.argmax(err - tol), err.shape)]}"
+    assert np.max(np.abs(lse_gpu - lse)) <= 2.0 ** -8, np.max(np.abs(lse_gpu - lse))
+
+
+def run_case(torch, st, ora, lay, reqs, n_q, g, dtype, scale=None):
+    import paper_2510_20878_b200 as hr  # noqa: F401
+    n_req, k = reqs.shape
+    HQ = lay.Hl * g
+    Qb = synth.gen_query(n_req, lay.L, HQ, n_q, lay.D, dtype=dtype)
+    q = torch.from_numpy(Qb.view(np.int16)).cuda()
+    o = torch.full_like(q, 0x7FFF)
+    lse = torch.full((n_req, lay.L, HQ, n_q), float("nan"), dtype=torch.float32, device="cuda")
+    dump = torch.empty(n_req * 2 * lay.L * lay.Hl * k * lay.T * lay.D, dtype=torch.int16, device="cuda")
+    st.attend(reqs, q, o, n_q, g, lse=lse, scale=scale or 0.0, kv_dump=dump)
+    torch.cuda.synchronize()
+    Og = o.cpu().numpy().view(np.uint16)
+    Ogf = (Og.astype(np.uint32) << 16).view(np.float32) if dtype == "bf16" else Og.view(np.float16).astype(np.float32)
+    lg = lse.cpu().numpy()
+    dmp = dump.cpu().numpy().view(np.uint16).reshape(n_req, 2, lay.L, lay.Hl, k * lay.T, lay.D)
+    for r, req in enumerate(reqs):
+        K, V = ora.assemble(list(req))
+        assert np.array_equal(dmp[r, 0], K), f"decoded K differs, request {r}"
+        assert np.array_equal(dmp[r, 1], V), f"decoded V differs, request {r}"
+        O, L_ = attention.attend_request(Qb[r], K, V, g, dtype, scale)
+        from oracle import numerics
+        v = numerics.to_f32(V, dtype).astype(np.float64)
+        vr = np.empty_like(O)   # max_j |v_j - O| per (layer, query head, row, column)
+        for l in range(lay.L):
+            for hq in range(HQ):
+                vr[l, hq] = np.max(np.abs(v[l, hq // g][None, :, :] - O[l, hq][:, None, :]), axis=1)
+        check_bound(Ogf[r].astype(np.float64), lg[r].astype(np.float64), O, L_, vr, dtype)
+
+
+@pytest.mark.parametrize("ladder,dtype,D,T,g,n_q,group", [
+    (NORTH, "fp16", 64, 64, 2, 4, 32),
+    (PAPER, "bf16", 128, 128, 4, 32, 0),       # M = 128
+    (PAPER, "bf16", 128, 64, 3, 5, 64),        # ragged M = 15
+    (("GSE8", "INT4"), "bf16", 64, 128, 1, 1, 0),  # decode-shaped M = 1
+])
+def test_attend_matches_oracle(torch_cuda, ladder, dtype, D, T, g, n_q, group):
+    taus = (0.3,) * (len(ladder) - 1)
+    st, ora, lay = build(torch_cuda, L=2, H=2, T=T, D=D, n_docs=8, ladder=ladder, taus=taus, dtype=dtype,
+                         group=group)
+    reqs = synth.gen_requests(8, 3, 3, 1.1, seed=11)
+    run_case(torch_cuda, st, ora, lay, reqs, n_q, g, dtype)
+    st.close()
+
+
+def test_attend_head_sharded_and_scale(torch_cuda):
+    st, ora, lay = build(torch_cuda, L=2, H=4, T=64, D=128, n_docs=6, ladder=PAPER, taus=(0.2, 0.2, 0.2),
+                         dtype="bf16", rank=1, world=2)
+    reqs = synth.gen_requests(6, 2, 4, 1.1, seed=12)
+    run_case(torch_cuda, st, ora, lay, reqs, 8, 4, "bf16", scale=0.05)
+    st.close()
+
+
+def test_attend_counts_hotness_and_validates(torch_cuda):
+    import paper_2510_20878_b200 as hr
+    torch = torch_cuda
+    st, ora, lay = build(torch, L=2, H=2, T=64, D=64, n_docs=8, ladder=NORTH, taus=(0.25, 0.25), dtype="fp16",
+                         hbm_items=6)
+    hot = [i // 2 for i in range(16) if st.item_info(i)[1] == 0]
+    docs = sorted({d for d in hot if st.item_info(2 * d)[1] == 0 and st.item_info(2 * d + 1)[1] == 0})
+    assert len(docs) >= 2
+    reqs = np.array([docs[:2]], np.uint32)
+    q = torch.zeros(2 * 2 * 4 * 64, dtype=torch.int16, device="cuda")
+    o = torch.empty_like(q)
+    st.attend(reqs, q, o, 4, 1)
+    torch.cuda.synchronize()
+    delta = st.hotness_delta().cpu().numpy()
+    assert np.array_equal(delta, hotness.count_requests(reqs, 8))
+    cold = next(d for d in range(8) if st.item_info(2 * d)[1] != 0)
+    with pytest.raises(hr.HaragError, match="ESTATE"):
+        st.attend(np.array([[docs[0], cold]], np.uint32), q, o, 4, 1)
+    with pytest.raises(hr.HaragError, match="EINVAL"):
+        st.attend(reqs, q, o, 65, 2)                     # g * n_q > 128
+    with pytest.raises(hr.HaragError, match="EINVAL"):
+        st.attend(np.array([[docs[0], docs[0]]], np.uint32), q, o, 4, 1)
+    st.close()
+    dm, _, _ = build(torch, L=2, H=2, T=64, D=64, n_docs=4, ladder=NORTH, taus=(0.25, 0.25), dtype="fp16",
+                     demand=True)
+    with pytest.raises(hr.HaragError, match="ESTATE"):
+        dm.attend(np.array([[0]], np.uint32), q, o, 4, 1)
+    dm.close()
+
+
+def test_attend_full_shape_sampled(torch_cuda):
+    """Llama-3-8B KV shape (32 x 8 x 512 x 128), k = 10, GQA g = 4, n_q = 32 (M = 128): decoded KV
+    of every (layer, head) bit-exact; O / LSE of sampled (layer, query head) pairs vs the oracle."""
+    import paper_2510_20878_b200 as hr  # noqa: F401
+    torch = torch_cuda
+    L, H, T, D, n_docs, k, g, n_q = 32, 8, 512, 128, 12, 10, 4, 32
+    prof = synth.gen_requests(n_docs, 4 * n_docs, 4, 1.1, seed=7)
+    h = hotness.count_requests(prof, n_docs).astype(np.uint64)
+    lay = ost.Layout(L=L, H=H, T=T, D=D)
+    import paper_2510_20878_b200 as hr
+    schemes = hotness.assign_schemes(h.tolist(), [NAMES[s] for s in PAPER], (0.1, 0.1, 0.1))
+    st = hr.Store(L=L, H=H, D=D, T=T, hbm_budget=sum(lay.item_bytes(s) for s in schemes) + 4096)
+
+    def src(doc, kp, vp, stream):
+        synth.gen_item_device(kp, L, H, T, D, doc, 0, stream=stream)
+        synth.gen_item_device(vp, L, H, T, D, doc, 1, stream=stream)
+
+    st.build(n_docs, h, src)
+    reqs = synth.gen_requests(n_docs, 1, k, 1.1, seed=13)
+    Qb = synth.gen_query(1, L, H * g, n_q, D)
+    q = torch.from_numpy(Qb.view(np.int16)).cuda()
+    o = torch.empty_like(q)
+    lse = torch.empty((1, L, H * g, n_q), dtype=torch.float32, device="cuda")
+    st.attend(reqs, q, o, n_q, g, lse=lse)
+    torch.cuda.synchronize()
+    Og = (o.cpu().numpy().view(np.uint16).astype(np.uint32) << 16).view(np.float32)
+    lg = lse.cpu().numpy()
+    rng = np.random.default_rng(0)
+    from oracle import numerics
+    for (l, hq) in [(0, 0), (31, 31)] + [tuple(x) for x in rng.integers(0, [L, H * g], (2, 2))]:
+        hh = hq // g
+        Ks, Vs = [], []
+        for doc in reqs[0]:
+            for kind, acc in ((0, Ks), (1, Vs)):
+                x = synth.gen_item(L, H, T, D, int(doc), kind, heads=(hh, hh + 1))[l, 0]
+                c, m = ost.encode_slab(x, schemes[2 * int(doc) + kind], lay)
+                acc.append(ost.decode_slab(c, m, schemes[2 * int(doc) + kind], lay).reshape(T, D))
+        K, V = np.concatenate(Ks), np.concatenate(Vs)
+        O, L_ = attention.attention(numerics.to_f32(Qb[0, l, hq], "bf16").astype(np.float64),
+                                    numerics.to_f32(K, "bf16").astype(np.float64),
+                                    numerics.to_f32(V, "bf16").astype(np.float64), 1 / np.sqrt(D))
+        v = numerics.to_f32(V, "bf16").astype(np.float64)
+        vr = np.max(np.abs(v[None, :, :] - O[:, None, :]), axis=1)
+        check_bound(Og[0, l, hq].astype(np.float64), lg[0, l, hq].astype(np.float64), O, L_, vr, "bf16")
+    st.close()
