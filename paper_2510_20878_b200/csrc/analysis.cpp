@@ -47,7 +47,7 @@ void scheme_error(const hr_store_config& cfg, uint32_t scheme, const void* src, 
   q.meta_stride = lay.meta_stride(scheme);
   q.err = err.as<int>();
   q.gse_range = gse.as<int>();
-  launch_quantize(q, st);
+  launch_quantize(&q, 1, st);
   AsmDesc d{};
   d.codes = blob.as<uint8_t>();
   d.meta = blob.as<uint8_t>() + lay.meta_offset(scheme);

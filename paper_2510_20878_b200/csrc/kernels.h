@@ -61,11 +61,13 @@ struct QuantParams {
   uint32_t g_shift;          // log2(G)
   uint64_t code_bytes_slab, meta_offset, meta_stride;
   int* err;                  // set to 1 on NaN/Inf
-  int* gse_range;            // device scratch int[2 * L * Hl] (GSE-8 per-slab exponent range)
+  int* gse_range;            // GSE-8: device scratch int[2 * L * Hl] of THIS item (per-slab exponent range)
 };
 
-// a3 + a4: one CTA per (layer, local head) slab.
-void launch_quantize(const QuantParams& p, cudaStream_t stream);
+// a3 + a4 for a batch of items sharing one layout (any scheme mix): one TMA-staged launch per
+// batch of up to 32 items (+ a read-only GSE-8 range pass when the batch holds GSE-8 items).
+// Padding bytes of the blobs are not written (the caller zero-fills them).
+void launch_quantize(const QuantParams* items, int n, cudaStream_t stream);
 
 // Consumer: attention of each request's query rows over its retrieved
 // chunks, decoding the packed codes inside the kernel (kernels/attend.cu).

@@ -1,5 +1,5 @@
 // a3 + a4 of the HA-RAG hot path on sm_100a: per-group statistics and
-// encode + bit-pack of one item's (layer, head) slabs into the packed blob of
+// encode + bit-pack of items' (layer, head) slabs into the packed blob of
 // DESIGN.md §4.  Compress-once (Alg. 1 step 3); schemes:
 //   INT8   P:144, symmetric absmax per group of G (R1-R3)
 //   INT4   north_star, min-max per group, two codes per byte (R4)
@@ -7,32 +7,109 @@
 //   GSE-8  P:155-172: per-slab exponent range -> shared-exponent array
 //          ("rule C", R6), then the three steps of P:157-161 (truncation, R9)
 //   PASS16 source bits unchanged
-// Every fp decision is one IEEE fp32 operation with round-to-nearest-even
-// (__fdiv_rn, __fsub_rn, __fadd_rn; no reciprocal, no contraction, R3).
+// Every integer-deciding fp decision equals one IEEE fp32 operation with
+// round-to-nearest-even (R3); where the kernel avoids a division it proves
+// equality (Markstein's correction, exhaustively checked) or falls back to
+// __fdiv_rn near a rounding tie.
 //
-// Work decomposition: a warp owns a 256-element chunk (8 elements = one
-// 16-byte load per lane) of one slab and grid-strides over the item.  For
-// G <= 256 a group is G/8 consecutive lanes and its statistics are a segmented
-// warp-shuffle reduction — one read of the source, one write of codes + meta.
-// G > 256 (e.g. the paper-ratio mode G = T*D): one warp per group, two passes
-// (the second read hits L2).  GSE-8 needs the slab-wide exponent range first:
-// a reduction kernel (warp shuffles + one atomicMin/Max per warp) then the
-// encode kernel, which rebuilds the shared-exponent array per warp.
+// Structure (warp-specialised, persistent, batched): one launch quantises a
+// batch of items (the K and V of a doc, or more), possibly of different
+// schemes.  Work unit = tile of kQTileE consecutive source elements of one
+// (item, layer, head) slab.  CTA = 1 producer warp + kQWarps consumer warps,
+// one CTA per SM, CTA b owns a contiguous block of tiles.  The producer's lane
+// 0 has the TMA engine bulk-copy each tile's 16-bit source into a kQStages-deep
+// shared-memory ring (mbarrier full / empty); for GSE-8 the whole producer
+// warp also builds the tile's 256-entry exponent -> code-template table from
+// the slab's exponent range and writes the slab's meta record.  Consumer warps
+// encode 256-element chunks straight from shared memory (segmented warp-shuffle
+// group statistics for INT8 / INT4: the source is read from HBM once) and store
+// codes and scales; PASS16 tiles are written back by the bulk-copy engine.
+// GSE-8 needs the slab-wide exponent range before any code: a range pass
+// (same kernel, RANGE mode: read-only) precedes the encode launch; for a K+V
+// batch (67 MB at Llama-3-8B shape) the encode's re-read hits the 126 MB L2.
+//
+// Group sizes G > 256 (the "paper-ratio" mode G = T*D) use
+// quant_biggroup_kernel: one warp per group, two passes.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_fp8.h>
 
 #include "../common.h"
 #include "../kernels.h"
+#include "ptx.h"
 
-#include <unordered_map>
+#include <algorithm>
 
 namespace harag {
 namespace {
 
-constexpr int kQThreads = 256;
-constexpr int kChunk = 256;  // elements per warp iteration
+using namespace ptx;
 
+#ifndef HARAG_Q_WARPS
+#define HARAG_Q_WARPS 16
+#endif
+#ifndef HARAG_Q_STAGES
+#define HARAG_Q_STAGES 4
+#endif
+#ifndef HARAG_Q_TILE
+#define HARAG_Q_TILE 16384
+#endif
+constexpr int kQWarps = HARAG_Q_WARPS;           // consumer warps per CTA
+constexpr int kQThreadsB = 32 * (1 + kQWarps);   // + 1 producer warp
+constexpr int kQStages = HARAG_Q_STAGES;         // ring depth
+constexpr uint32_t kQTileE = HARAG_Q_TILE;       // source elements per tile (2 B each)
+constexpr int kQMaxJobs = 32;                    // items per launch
+constexpr int kChunk = 256;                      // elements per warp step (8 per lane)
+constexpr float kMagic = 12582912.f;             // 1.5 * 2^23: fl(v + kMagic) = rne(v) in the low bits, |v| < 2^22
+
+enum { MODE_ENCODE = 0, MODE_RANGE = 1 };
+
+struct QJob {
+  const uint16_t* src;  // [L][H][T][D] all heads
+  uint8_t* dst;         // item blob
+  int* range;           // GSE-8: int[2 * L * Hl] (255 - min, max) biased exponents, zero-initialised
+  uint32_t scheme;
+  uint32_t pad;
+};
+
+struct QBatch {
+  QJob jobs[kQMaxJobs];
+  uint32_t n_jobs;
+  uint32_t L, H, Hl, h0, T, D, G, g_shift, gse_e, gse_m, dtype;
+  uint32_t slab, tile_e, tiles_per_slab;
+  uint64_t n_tiles;
+  uint64_t code_slab[6], meta_off[6];
+  uint32_t meta_stride[6];
+  int* err;
+};
+
+struct QHdr {
+  uint8_t* codes;   // first code byte of the tile
+  uint8_t* meta;    // INT8 / INT4: the tile's first group record; GSE-8: slab record
+  int* range;       // RANGE mode: the slab's exponent-range pair
+  uint32_t n_el;    // elements in the tile (multiple of 256)
+  uint32_t scheme;
+};
+
+// Dynamic shared memory: [tile ring | GSE tables | headers | full | empty]
+struct QSmem {
+  uint8_t* base;
+  __device__ __forceinline__ uint8_t* tile(int s) const { return base + (size_t)s * kQTileE * 2; }
+  __device__ __forceinline__ uint32_t* gtab(int s) const {
+    return reinterpret_cast<uint32_t*>(base + (size_t)kQStages * kQTileE * 2) + 256 * s;
+  }
+  __device__ __forceinline__ QHdr* hdr() const { return reinterpret_cast<QHdr*>(gtab(kQStages)); }
+  __device__ __forceinline__ uint64_t* full() const { return reinterpret_cast<uint64_t*>(hdr() + kQStages); }
+  __device__ __forceinline__ uint64_t* empty() const { return full() + kQStages; }
+};
+constexpr size_t kQSmemBytes =
+    (size_t)kQStages * kQTileE * 2 + (size_t)kQStages * 1024 + kQStages * sizeof(QHdr) + 2 * kQStages * 8;
+
+__device__ __forceinline__ uint32_t code_bytes(uint32_t scheme, uint32_t n_el) {
+  return scheme == HR_S_PASS16 ? 2 * n_el : scheme == HR_S_INT4 ? n_el / 2 : n_el;
+}
+
+// ------------------------------------------------------------------ element helpers
 template <int DT>
 __device__ __forceinline__ float to_f32(uint32_t bits16) {
   if constexpr (DT == HR_BF16) {
@@ -41,111 +118,36 @@ __device__ __forceinline__ float to_f32(uint32_t bits16) {
     return __half2float(__ushort_as_half((unsigned short)bits16));
   }
 }
-
-// 8 source elements (one 16-byte vector) -> fp32
+// 8 16-bit source elements -> fp32 pairs (element 2i in .x)
 template <int DT>
-__device__ __forceinline__ void load8(const uint16_t* p, float (&x)[8], uint4& raw) {
-  raw = __ldg(reinterpret_cast<const uint4*>(p));
+__device__ __forceinline__ void unpack8(const uint4& raw, float2 (&x)[4]) {
   const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    x[2 * i] = to_f32<DT>(w[i] & 0xFFFFu);
-    x[2 * i + 1] = to_f32<DT>(w[i] >> 16);
-  }
-}
-
-__device__ __forceinline__ bool any_nonfinite(const float (&x)[8]) {
-  bool bad = false;
-#pragma unroll
-  for (int i = 0; i < 8; ++i) bad |= !isfinite(x[i]);
-  return bad;
-}
-
-// rne(fl(x / s)) for 8 elements of one group — the quantised codes of R3 — without an IEEE
-// division per element.  y = rcp.approx(s) has relative error <= 2^-23, so t = RN(x*y) is within
-// |x/s| * 1.5 * 2^-23 <= 1.5 * 2^-16 of x/s (|x/s| <= 128), and fl(x/s) within 2^-18 of x/s:
-// unless t lies within 2^-15 of a half-integer, x/s, fl(x/s) and t round to the same integer.
-// Elements near a half-integer (or any element when s / y are not normal) use __fdiv_rn.
-__device__ __forceinline__ void div_rne8(const float (&x)[8], float s, int (&q)[8]) {
-  float y;
-  asm("rcp.approx.f32 %0, %1;" : "=f"(y) : "f"(s));
-  const bool slow = !(s >= 1.17549435e-38f && s <= 8.50705917e+37f);
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const float t = __fmul_rn(x[i], y);
-    float r = rintf(t);
-    // bf16 data makes exact half-integer quotients common (~0.2% of elements): only the flagged
-    // element takes the IEEE division
-    if (slow || fabsf(fabsf(__fsub_rn(t, r)) - 0.5f) <= 3.0517578125e-05f) r = rintf(__fdiv_rn(x[i], s));
-    q[i] = (int)r;
-  }
-}
-
-// sub(a, b) of R4: fl(a - b) saturated at FLT_MAX (finite inputs whose difference overflows)
-__device__ __forceinline__ float sub_sat(float a, float b) { return fminf(__fsub_rn(a, b), 3.40282347e+38f); }
-
-// segmented reductions over `seg` consecutive lanes (seg a power of two <= 32)
-__device__ __forceinline__ float seg_max(float v, int seg) {
-  for (int o = seg >> 1; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
-  return v;
-}
-__device__ __forceinline__ float seg_min(float v, int seg) {
-  for (int o = seg >> 1; o; o >>= 1) v = fminf(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
-  return v;
-}
-
-struct Geo {  // slab addressing shared by the kernels
-  const uint16_t* src;
-  uint8_t* codes;
-  uint8_t* meta;
-};
-__device__ __forceinline__ Geo slab_geo(const QuantParams& p, uint32_t slab_i) {
-  const uint32_t l = slab_i / p.Hl, hl = slab_i - l * p.Hl;
-  const uint64_t slab = (uint64_t)p.T * p.D;
-  return {p.src + ((uint64_t)l * p.H + p.h0 + hl) * slab, p.dst + slab_i * p.code_bytes_slab,
-          p.dst + p.meta_offset + slab_i * p.meta_stride};
-}
-
-// Blocked distribution: warp w of the grid owns chunks [n*w/W, n*(w+1)/W) and walks them in
-// order, advancing (slab, offset) without divisions; the next chunk's load is issued before the
-// current chunk is encoded (two 16-byte loads in flight per lane).
-struct Walker {
-  uint32_t c, c1, slab_i, e0, cps;
-  Geo g;
-  __device__ __forceinline__ void init(const QuantParams& p) {
-    const uint32_t n = p.L * p.Hl * (p.T * p.D / kChunk);
-    const uint32_t warps = gridDim.x * (kQThreads / 32);
-    const uint32_t w = blockIdx.x * (kQThreads / 32) + threadIdx.x / 32;
-    cps = p.T * p.D / kChunk;
-    c = (uint32_t)((uint64_t)n * w / warps);
-    c1 = (uint32_t)((uint64_t)n * (w + 1) / warps);
-    slab_i = c / cps;
-    e0 = (c - slab_i * cps) * kChunk;
-    g = slab_geo(p, slab_i);
-  }
-  __device__ __forceinline__ bool more() const { return c < c1; }
-  __device__ __forceinline__ void next(const QuantParams& p) {
-    ++c;
-    e0 += kChunk;
-    if (e0 == cps * kChunk && c < c1) {
-      e0 = 0;
-      g = slab_geo(p, ++slab_i);
+    if constexpr (DT == HR_BF16) {
+      x[i] = make_float2(__uint_as_float(w[i] << 16), __uint_as_float(w[i] & 0xFFFF0000u));
+    } else {
+      x[i] = __half22float2(*reinterpret_cast<const __half2*>(&w[i]));
     }
   }
-};
-
-// ---------------------------------------------------------------- INT8 / INT4 (G <= 256)
-// fl(a / 127) for the INT8 scale without a division: q0 = RN(a * y), y = RN(1/127); the residual
-// r = a - 127*q0 is exact (one FMA) and RN(q0 + r*y) is the correctly rounded quotient (Markstein's
-// correction).  a is always a 16-bit source value, so the identity is checked against __fdiv_rn for
-// every finite bf16 and fp16 magnitude by tests/test_gpu_parity.py::test_int8_scale_all_16bit_values;
-// tiny a (below 2^-100) takes the IEEE division.
-__device__ __forceinline__ float div127(float a) {
-  constexpr float y = 0.007874015718698501587f;  // RN(1/127)
-  if (a < 7.8886090522101181e-31f) return __fdiv_rn(a, 127.f);
-  const float q0 = __fmul_rn(a, y);
-  const float r = __fmaf_rn(-q0, 127.f, a);
-  return __fmaf_rn(r, y, q0);
+}
+// magnitude bit patterns, max over the 8 values (NaN/Inf on top); 16-bit patterns in both halves
+__device__ __forceinline__ uint32_t absmax_pair(const uint4& raw) {
+  const uint32_t m = 0x7FFF7FFFu;
+  return __vmaxu2(__vmaxu2(raw.x & m, raw.y & m), __vmaxu2(raw.z & m, raw.w & m));
+}
+template <int DT>
+__device__ __forceinline__ bool pattern_nonfinite(uint32_t pair_max) {
+  const uint32_t v = max(pair_max & 0xFFFFu, pair_max >> 16);
+  return v >= (DT == HR_BF16 ? 0x7F80u : 0x7C00u);
+}
+// bytes 0 of four words -> one word
+__device__ __forceinline__ uint32_t gather_b0(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  return __byte_perm(__byte_perm(a, b, 0x0040), __byte_perm(c, d, 0x0040), 0x5410);
+}
+// bytes 3 of four words -> one word
+__device__ __forceinline__ uint32_t gather_b3(uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+  return __byte_perm(__byte_perm(a, b, 0x0073), __byte_perm(c, d, 0x0073), 0x5410);
 }
 
 template <int SEG>
@@ -167,150 +169,565 @@ __device__ __forceinline__ float seg_max_f(float v) {
   return v;
 }
 
-// largest |x| bit pattern of the 8 16-bit values (magnitude order == integer order, NaN/Inf on top)
-__device__ __forceinline__ uint32_t absmax_bits(const uint4& raw) {
-  const uint32_t m = 0x7FFF7FFFu;
-  const uint32_t v = __vmaxu2(__vmaxu2(raw.x & m, raw.y & m), __vmaxu2(raw.z & m, raw.w & m));
-  return max(v & 0xFFFFu, v >> 16);
+// fl(a / 127) for the INT8 scale without a division: q0 = RN(a * y), y = RN(1/127); the residual
+// r = a - 127*q0 is exact (one FMA) and RN(q0 + r*y) is the correctly rounded quotient (Markstein's
+// correction).  a is always a 16-bit source value, so the identity is checked against __fdiv_rn for
+// every finite bf16 and fp16 magnitude by tests/test_gpu_parity.py::test_int8_scale_all_16bit_values;
+// tiny a (below 2^-100) takes the IEEE division.
+__device__ __forceinline__ float div127(float a) {
+  constexpr float y = 0.007874015718698501587f;  // RN(1/127)
+  if (a < 7.8886090522101181e-31f) return __fdiv_rn(a, 127.f);
+  const float q0 = __fmul_rn(a, y);
+  const float r = __fmaf_rn(-q0, 127.f, a);
+  return __fmaf_rn(r, y, q0);
 }
 
-template <int SCHEME, int SEG, int DT>
-__device__ __forceinline__ void encode_group_chunk(const QuantParams& p, const Geo& g, uint32_t e, const float (&x)[8],
-                                                   const uint4& raw, uint32_t lane, bool& bad) {
-  const uint32_t grp = e >> p.g_shift;
-  const bool leader = (lane & (SEG - 1)) == 0;
-  int q[8];
-  if constexpr (SCHEME == HR_S_INT8) {
-    // a3: a = max |x| (exact: the largest magnitude bit pattern); s = 1 if a == 0 else fl(a / 127)
-    const uint32_t ab = seg_max_u32<SEG>(absmax_bits(raw));
-    bad |= ab >= (DT == HR_BF16 ? 0x7F80u : 0x7C00u);  // NaN/Inf in the group
-    const float a = to_f32<DT>(ab);
-    const float s = (a == 0.f) ? 1.f : div127(a);
-    if (leader) reinterpret_cast<float*>(g.meta)[grp] = s;
-    // a4: q = clamp(rne(fl(x / s)), -127, 127).  fl(x/s) by Markstein's correction with y = RN(1/s):
-    // equal to IEEE division for every (a, x) pair of 16-bit values when s is in [2^-90, 2^125]
-    // (tests/csrc/markstein_check.cu, exhaustive); outside that range the IEEE division.  |x| <= a
-    // gives |x/s| <= 127 (1 + 2^-24), so the clamp never binds and is omitted.
-    const bool fast = s >= 8.0779356e-28f && s <= 4.2535296e+37f;
-    int c8[8];
-    if (__all_sync(0xFFFFFFFFu, fast)) {  // warp-uniform: the branch-free path for every normal scale
-      const float y = __fdiv_rn(1.f, s);
+// sub(a, b) of R4: fl(a - b) saturated at FLT_MAX (finite inputs whose difference overflows)
+__device__ __forceinline__ float sub_sat(float a, float b) { return fminf(__fsub_rn(a, b), 3.40282347e+38f); }
+
+// ------------------------------------------------------------------ INT8 / INT4 (G <= 256)
+// A warp step covers 1024 consecutive elements; lane L owns the 32 elements [32L, 32L + 32), so a
+// group of G is SEGL = G/32 lanes: the per-lane statistics are plain min/max chains, the cross-lane
+// reduction is log2(SEGL) <= 3 shuffles, and the group scalars are computed by SEGL lanes only.
+// Shared-memory reads: the lane's four 16-B chunks are read in the rotated order
+// c = (j + (L >> 1)) & 3, which makes every quarter-warp load cover 32 distinct banks; the codes are
+// rotated back in registers before the 16-B stores.
+constexpr uint32_t kStep = 1024;  // elements per warp step
+constexpr uint32_t kLaneE = 32;   // elements per lane and step
+
+template <int DT>
+__device__ __forceinline__ bool load_lane32(const uint8_t* tile, uint32_t e0, uint32_t n_el, uint32_t rot,
+                                            uint4 (&raw)[4]) {
+  const bool valid = e0 < n_el;  // n_el is a multiple of 256: a lane's 32 elements are all valid or none
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float q0 = __fmul_rn(x[i], y);
-        c8[i] = __float2int_rn(__fmaf_rn(__fmaf_rn(-q0, s, x[i]), y, q0));
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) c8[i] = __float2int_rn(__fdiv_rn(x[i], s));
-    }
-    const uint32_t w0 = __byte_perm(__byte_perm(c8[0], c8[1], 0x0040), __byte_perm(c8[2], c8[3], 0x0040), 0x5410);
-    const uint32_t w1 = __byte_perm(__byte_perm(c8[4], c8[5], 0x0040), __byte_perm(c8[6], c8[7], 0x0040), 0x5410);
-    *reinterpret_cast<uint2*>(g.codes + e) = make_uint2(w0, w1);
-  } else {
-    bad |= any_nonfinite(x);
-    // a3: mn = min + 0, mx = max + 0 (a zero extreme is +0); s = (mx == mn) ? 1 : fl(sub(mx, mn) / 15)
-    float mn = x[0], mx = x[0];
-#pragma unroll
-    for (int i = 1; i < 8; ++i) mn = fminf(mn, x[i]), mx = fmaxf(mx, x[i]);
-    mn = __fadd_rn(seg_min_f<SEG>(mn), 0.f);
-    mx = __fadd_rn(seg_max_f<SEG>(mx), 0.f);
-    const float s = (mx == mn) ? 1.f : __fdiv_rn(sub_sat(mx, mn), 15.f);
-    if (leader) reinterpret_cast<float2*>(g.meta)[grp] = make_float2(s, mn);
-    // a4: q = clamp(rne(fl(sub(x, mn) / s)), 0, 15); element 2i -> low nibble (R24)
-    float u[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) u[i] = sub_sat(x[i], mn);
-    div_rne8(u, s, q);
-    uint32_t w = 0u;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) w |= (uint32_t)max(0, min(15, q[i])) << (4 * i);
-    *reinterpret_cast<uint32_t*>(g.codes + e / 2) = w;
+  for (uint32_t j = 0; j < 4; ++j)
+    raw[j] = valid ? *reinterpret_cast<const uint4*>(tile + 2 * (e0 + ((j + rot) & 3) * 8)) : make_uint4(0, 0, 0, 0);
+  return valid;
+}
+// slot j holds chunk (j + rot) & 3: put chunk c back at position c
+template <class V>
+__device__ __forceinline__ void unrotate4(V (&w)[4], uint32_t rot) {
+  if (rot & 1) {
+    const V t = w[3];
+    w[3] = w[2], w[2] = w[1], w[1] = w[0], w[0] = t;
+  }
+  if (rot & 2) {
+    V t = w[0];
+    w[0] = w[2], w[2] = t;
+    t = w[1];
+    w[1] = w[3], w[3] = t;
   }
 }
 
-template <int SCHEME, int SEG, int DT>
-__global__ void __launch_bounds__(kQThreads) quant_group_kernel(QuantParams p) {
-  constexpr int kBatch = 4;  // chunks whose loads are in flight together (4 x 16 B per lane)
-  const uint32_t lane = threadIdx.x & 31;
-  Walker wk;
-  wk.init(p);
+// a3: a = max |x| (exact: the largest magnitude bit pattern); s = 1 if a == 0 else fl(a / 127).
+// a4: q = rne(fl(x / s)) with fl(x/s) by Markstein's correction, y = RN(1/s): equal to the IEEE quotient
+// for every (a, x) pair of 16-bit values when s is in [2^-90, 2^125] (tests/csrc/markstein_check.cu,
+// exhaustive); outside that range the IEEE division.  |x| <= a gives |x/s| <= 127 (1 + 2^-24), so the
+// clamp to [-127, 127] never binds and is omitted; rne comes from fl(v + 1.5*2^23), whose low byte is
+// the two's-complement code.
+template <int SEGL, int DT>
+__device__ __forceinline__ void enc_int8_step(const uint8_t* tile, uint32_t eb, uint32_t n_el, uint8_t* codes,
+                                              float* meta, uint32_t g_shift, uint32_t lane, uint32_t& nan_acc) {
+  const uint32_t e0 = eb + lane * kLaneE, rot = (lane >> 1) & 3;
+  uint4 raw[4];
+  const bool valid = load_lane32<DT>(tile, e0, n_el, rot, raw);
+  const uint32_t pm = __vmaxu2(__vmaxu2(absmax_pair(raw[0]), absmax_pair(raw[1])),
+                               __vmaxu2(absmax_pair(raw[2]), absmax_pair(raw[3])));
+  const uint32_t ab = seg_max_u32<SEGL>(max(pm & 0xFFFFu, pm >> 16));
+  nan_acc = __vmaxu2(nan_acc, ab);  // NaN/Inf
+  const float a = to_f32<DT>(ab);
+  const float s = (a == 0.f) ? 1.f : div127(a);
+  if ((lane & (SEGL - 1)) == 0 && valid) meta[e0 >> g_shift] = s;
+  const bool fast = s >= 8.0779356e-28f && s <= 4.2535296e+37f;
+  uint2 w[4];
+  if (__all_sync(0xFFFFFFFFu, fast)) {  // warp-uniform: the branch-free path for every normal scale
+    const float y = __fdiv_rn(1.f, s);
+    const float2 yy = make_float2(y, y), ns = make_float2(-s, -s), mg = make_float2(kMagic, kMagic);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float2 x[4];
+      unpack8<DT>(raw[j], x);
+      uint32_t v[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 q0 = __fmul2_rn(x[i], yy);
+        const float2 qf = __ffma2_rn(__ffma2_rn(q0, ns, x[i]), yy, q0);  // fl(x / s)
+        const float2 rr = __fadd2_rn(qf, mg);
+        v[2 * i] = __float_as_uint(rr.x), v[2 * i + 1] = __float_as_uint(rr.y);
+      }
+      w[j] = make_uint2(gather_b0(v[0], v[1], v[2], v[3]), gather_b0(v[4], v[5], v[6], v[7]));
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float2 x[4];
+      unpack8<DT>(raw[j], x);
+      uint32_t v[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        v[2 * i] = (uint32_t)__float2int_rn(__fdiv_rn(x[i].x, s));
+        v[2 * i + 1] = (uint32_t)__float2int_rn(__fdiv_rn(x[i].y, s));
+      }
+      w[j] = make_uint2(gather_b0(v[0], v[1], v[2], v[3]), gather_b0(v[4], v[5], v[6], v[7]));
+    }
+  }
+  unrotate4(w, rot);
+  if (valid) {
+    uint4* dst = reinterpret_cast<uint4*>(codes + e0);
+    dst[0] = make_uint4(w[0].x, w[0].y, w[1].x, w[1].y);
+    dst[1] = make_uint4(w[2].x, w[2].y, w[3].x, w[3].y);
+  }
+}
+
+// a3: mn = min + 0, mx = max + 0 (a zero extreme is +0); s = (mx == mn) ? 1 : fl(sub(mx, mn) / 15).
+// a4: q = clamp(rne(fl(sub(x, mn) / s)), 0, 15); element 2i -> low nibble (R24).  u = sub(x, mn) is in
+// [0, sub(mx, mn)], so fl(u / s) is in [0, 15 (1 + 2^-23)] and the clamp never binds.  fl(u / s) without
+// a division: y = RN(1/s), q0 = RN(u*y) (within 2 ulps), one Markstein correction q1 = RN(q0 + r0*y),
+// r0 = u - s*q0 (FMA), makes q1 faithful, and a second one, q2 = RN(q1 + r1*y), is the correctly
+// rounded quotient (Markstein's theorem: y within 1/2 ulp of 1/s, q1 within 1 ulp of u/s).  Checked
+// against IEEE division on 2^33 sampled (x, mn, mx) triples per source dtype by
+// tests/csrc/markstein_check.cu.  Scales outside [2^-90, 2^125] (or a group whose range overflows) take
+// __fdiv_rn per element (warp-uniform).
+template <int SEGL, int DT>
+__device__ __forceinline__ void enc_int4_step(const uint8_t* tile, uint32_t eb, uint32_t n_el, uint8_t* codes,
+                                              float2* meta, uint32_t g_shift, uint32_t lane, uint32_t& nan_acc) {
+  const uint32_t e0 = eb + lane * kLaneE, rot = (lane >> 1) & 3;
+  uint4 raw[4];
+  const bool valid = load_lane32<DT>(tile, e0, n_el, rot, raw);
+  nan_acc = __vmaxu2(nan_acc, __vmaxu2(__vmaxu2(absmax_pair(raw[0]), absmax_pair(raw[1])),
+                                       __vmaxu2(absmax_pair(raw[2]), absmax_pair(raw[3]))));
+  float2 x[4][4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) unpack8<DT>(raw[j], x[j]);
+  float mn = x[0][0].x, mx = x[0][0].x;
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) mn = fminf(mn, fminf(x[j][i].x, x[j][i].y)), mx = fmaxf(mx, fmaxf(x[j][i].x, x[j][i].y));
+  mn = __fadd_rn(seg_min_f<SEGL>(mn), 0.f);
+  mx = __fadd_rn(seg_max_f<SEGL>(mx), 0.f);
+  const float dm = __fsub_rn(mx, mn);
+  const float s = (mx == mn) ? 1.f : __fdiv_rn(fminf(dm, 3.40282347e+38f), 15.f);
+  if ((lane & (SEGL - 1)) == 0 && valid) meta[e0 >> g_shift] = make_float2(s, mn);
+  const bool fast = s >= 8.0779356e-28f && s <= 4.2535296e+37f && dm <= 3.40282347e+38f;
+  uint32_t w[4];
+  if (__all_sync(0xFFFFFFFFu, fast)) {  // warp-uniform
+    const float y = __fdiv_rn(1.f, s);
+    const float2 yy = make_float2(y, y), ns = make_float2(-s, -s), nm = make_float2(-mn, -mn);
+    const float2 mg = make_float2(kMagic, kMagic);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint32_t v[8];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float2 u = __fadd2_rn(x[j][i], nm);
+        const float2 q0 = __fmul2_rn(u, yy);
+        const float2 q1 = __ffma2_rn(__ffma2_rn(q0, ns, u), yy, q0);
+        const float2 q2 = __ffma2_rn(__ffma2_rn(q1, ns, u), yy, q1);  // fl(u / s)
+        const float2 rr = __fadd2_rn(q2, mg);                          // low bits: rne
+        v[2 * i] = __float_as_uint(rr.x), v[2 * i + 1] = __float_as_uint(rr.y);
+      }
+      // even elements -> low nibbles, odd -> high nibbles
+      w[j] = (gather_b0(v[0], v[2], v[4], v[6]) & 0x0F0F0F0Fu) | ((gather_b0(v[1], v[3], v[5], v[7]) & 0x0F0F0F0Fu) << 4);
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint32_t v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        v[i] = (uint32_t)__float2int_rn(__fdiv_rn(sub_sat(i & 1 ? x[j][i >> 1].y : x[j][i >> 1].x, mn), s));
+      w[j] = (gather_b0(v[0], v[2], v[4], v[6]) & 0x0F0F0F0Fu) | ((gather_b0(v[1], v[3], v[5], v[7]) & 0x0F0F0F0Fu) << 4);
+    }
+  }
+  unrotate4(w, rot);
+  if (valid) *reinterpret_cast<uint4*>(codes + e0 / 2) = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// ------------------------------------------------------------------ FP8 (nearest, ties to even, saturating: R5)
+template <int SCHEME, int DT>
+__device__ __forceinline__ void enc_fp8(const uint4& raw, uint8_t* codes, uint32_t e, uint32_t& nan_acc) {
+  constexpr __nv_fp8_interpretation_t kInterp = SCHEME == HR_S_FP8E4M3 ? __NV_E4M3 : __NV_E5M2;
+  nan_acc = __vmaxu2(nan_acc, absmax_pair(raw));
+  float2 x[4];
+  unpack8<DT>(raw, x);
+  uint32_t c[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) c[i] = __nv_cvt_float2_to_fp8x2(x[i], __NV_SATFINITE, kInterp);
+  *reinterpret_cast<uint2*>(codes + e) = make_uint2(__byte_perm(c[0], c[1], 0x5410), __byte_perm(c[2], c[3], 0x5410));
+}
+
+// ------------------------------------------------------------------ GSE-8
+// Table entry per fp32 biased exponent ef of the slab (built by the producer warp):
+//   bits 24..30 and 8..14   idx << m   (idx: smallest G_i >= E)
+//   bits 31 and 15          1 (sign kept) — 0 for codes that flush (zero, subnormal, E below the array's reach)
+//   bits 0..4               31 - keep  keep = m - 1 - d fraction bits after the marker, d = G_idx - E
+// The code of x (fp32 bits b) is byte 3 of ((b | 0x7FFFFFFF) & ent) | ({m24 : 0} >> (31 - keep)), with
+// m24 = 1.fraction (24 bits): the funnel shift puts the marker 1 and the top keep fraction bits (the
+// rest truncated, R9) in byte 3 below idx.  A flushed entry is 0: both terms vanish.  For a bf16 pair
+// word w the high element is exactly that with b = w; the low element assembles its code in byte 1
+// ((w | 0xFFFF7FFF) & ent keeps its sign bit 15, and {m8 : 0} >> (31 - keep) with m8 = 1.fraction
+// (8 bits) puts the field in byte 1), so no unpacking to fp32 is needed.
+template <int DT>
+__device__ __forceinline__ void enc_gse(const uint4& raw, uint8_t* codes, uint32_t tab, uint32_t e,
+                                        uint32_t& nan_acc) {
+  nan_acc = __vmaxu2(nan_acc, absmax_pair(raw));
+  uint32_t c[8];
+  if constexpr (DT == HR_BF16) {
+    const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t eh = lds32(tab | ((w[i] >> 21) & 0x3FCu));
+      const uint32_t el = lds32(tab | ((w[i] >> 5) & 0x3FCu));
+      c[2 * i + 1] = ((w[i] | 0x7FFFFFFFu) & eh) | __funnelshift_r(0u, (w[i] & 0x007F0000u) | 0x00800000u, eh);
+      c[2 * i] = ((w[i] | 0xFFFF7FFFu) & el) | __funnelshift_r(0u, (w[i] & 0x7Fu) | 0x80u, el);
+    }
+    *reinterpret_cast<uint2*>(codes + e) = make_uint2(__byte_perm(__byte_perm(c[0], c[1], 0x0071), __byte_perm(c[2], c[3], 0x0071), 0x5410),
+                                                      __byte_perm(__byte_perm(c[4], c[5], 0x0071), __byte_perm(c[6], c[7], 0x0071), 0x5410));
+  } else {
+    float2 x[4];
+    unpack8<DT>(raw, x);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const uint32_t b = __float_as_uint(i & 1 ? x[i >> 1].y : x[i >> 1].x);
+      const uint32_t ent = lds32(tab | ((b >> 21) & 0x3FCu));
+      c[i] = ((b | 0x7FFFFFFFu) & ent) | __funnelshift_r(0u, (b & 0x007FFFFFu) | 0x00800000u, ent);
+    }
+    *reinterpret_cast<uint2*>(codes + e) = make_uint2(gather_b3(c[0], c[1], c[2], c[3]), gather_b3(c[4], c[5], c[6], c[7]));
+  }
+}
+
+// the slab's array parameters from its exponent range (rule C, R6): lo, Emax, n entries
+struct GseArr {
+  int lo, Emax, n, rmin, rmax;  // rmin / rmax: biased exponent range of the slab's nonzero normals
+};
+__device__ __forceinline__ GseArr gse_array(const int* range, int m, int nmax) {
+  const int step = m - 1;
+  const int rmin = 255 - range[0], rmax = range[1];
+  GseArr a;
+  a.Emax = rmax - 127;
+  a.lo = max(rmin - 127, a.Emax - (nmax - 1) * step);
+  a.n = rmax != 0 ? (a.Emax - a.lo + step - 1) / step + 1 : 0;
+  a.rmin = rmin, a.rmax = rmax;
+  return a;
+}
+
+// producer warp: the code-template table of one slab.  Only exponents that occur in the slab
+// ([rmin, rmax], and 0 for zeros / subnormals) are written; other entries are never read (a NaN/Inf
+// input, ef = 255, is rejected through the error flag).
+__device__ __forceinline__ void gse_build_table(uint32_t* tab, const GseArr& a, int m, int lane) {
+  const int step = m - 1;
+  if (lane == 0) tab[0] = 0u;
+  if (a.n == 0) return;
+  for (int ef = a.rmin + lane; ef <= min(a.rmax, 254); ef += 32) {
+    const int E = ef - 127;
+    const int idx = (E <= a.lo) ? 0 : (E - a.lo + step - 1) / step;
+    const int d = min(a.lo + idx * step, a.Emax) - E;
+    uint32_t ent = 0;
+    if (d <= m - 1) {
+      const uint32_t t = 0x80u | ((uint32_t)idx << m);  // sign enable | idx << m
+      ent = (t << 24) | (t << 8) | (uint32_t)(31 - (m - 1 - d));
+    }
+    tab[ef] = ent;
+  }
+}
+
+// producer warp: the slab's meta record — int8 array [2^e] (unused -128), zero pad to 16 B, then the fp32
+// decode table [2^(e+1)]: entry (sign << e | i) = (-1)^sign 2^(G_i - (m-1)), 0 for unused i
+__device__ __forceinline__ void gse_write_record(uint8_t* meta, uint32_t stride, const GseArr& a, int m, int nmax,
+                                                 int lane) {
+  const int step = m - 1;
+  if (lane < 16) {
+    int v = 0;
+    if (lane < nmax) v = (lane < a.n) ? min(a.lo + lane * step, a.Emax) : -128;
+    meta[lane] = (uint8_t)(int8_t)v;
+  }
+  for (uint32_t w = lane; w < (stride - 16) / 4; w += 32) {
+    float v = 0.f;
+    const int i = (int)w & (nmax - 1);
+    if ((int)w < 2 * nmax && i < a.n) {
+      const int k = min(a.lo + i * step, a.Emax) - step;
+      v = k >= -126 ? __int_as_float((k + 127) << 23) : (k >= -149 ? __int_as_float(1 << (k + 149)) : 0.f);
+      if ((int)w >= nmax) v = -v;
+    }
+    reinterpret_cast<float*>(meta + 16)[w] = v;
+  }
+}
+
+// ------------------------------------------------------------------ producer
+template <int MODE>
+__device__ __forceinline__ void q_produce(const QBatch& p, const QSmem& sm, int lane) {
+  const uint64_t t0 = p.n_tiles * blockIdx.x / gridDim.x, t1 = p.n_tiles * (blockIdx.x + 1) / gridDim.x;
+  const uint32_t per_job = p.L * p.Hl * p.tiles_per_slab;
+  uint32_t j = (uint32_t)(t0 / per_job);
+  uint32_t r = (uint32_t)(t0 - (uint64_t)j * per_job);
+  uint32_t slab_i = r / p.tiles_per_slab, sub = r - slab_i * p.tiles_per_slab;
+  uint32_t l = slab_i / p.Hl, hl = slab_i - l * p.Hl;
+  const int m = (int)p.gse_m, nmax = 1 << (7 - m);
+  for (uint64_t i = 0; i < t1 - t0; ++i) {
+    const int stage = (int)(i % kQStages);
+    if (i >= kQStages) mbar_wait(&sm.empty()[stage], (uint32_t)(((i / kQStages) - 1) & 1));
+    const QJob& jb = p.jobs[j];
+    const uint32_t scheme = jb.scheme;
+    const uint32_t e0 = sub * p.tile_e;
+    const uint32_t n_el = min(p.tile_e, p.slab - e0);
+    uint8_t* meta = jb.dst + p.meta_off[scheme] + (uint64_t)slab_i * p.meta_stride[scheme];
+    if (MODE == MODE_ENCODE && scheme == HR_S_GSE8) {
+      const GseArr a = gse_array(jb.range + 2 * slab_i, m, nmax);
+      gse_build_table(sm.gtab(stage), a, m, lane);
+      if (sub == 0) gse_write_record(meta, p.meta_stride[HR_S_GSE8], a, m, nmax, lane);
+      __syncwarp();
+    }
+    if (lane == 0) {
+      QHdr& h = sm.hdr()[stage];
+      h.codes = jb.dst + (uint64_t)slab_i * p.code_slab[scheme] + code_bytes(scheme, e0);
+      h.meta = scheme == HR_S_INT8 ? meta + 4 * (e0 >> p.g_shift) : scheme == HR_S_INT4 ? meta + 8 * (e0 >> p.g_shift) : meta;
+      h.range = jb.range ? jb.range + 2 * slab_i : nullptr;
+      h.n_el = n_el;
+      h.scheme = scheme;
+      uint64_t* full = &sm.full()[stage];
+      mbar_arrive_expect_tx(full, 2 * n_el);  // release: header and table visible with the phase flip
+      bulk_g2s(sm.tile(stage), jb.src + ((uint64_t)(l * p.H + p.h0 + hl) * p.slab + e0), 2 * n_el, full);
+    }
+    if (++sub == p.tiles_per_slab) {  // advance (sub, head, layer, job) without divisions
+      sub = 0;
+      ++slab_i;
+      if (++hl == p.Hl) {
+        hl = 0;
+        if (++l == p.L) l = 0, slab_i = 0, ++j;
+      }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ consumers
+template <int DT, int SEG>
+__device__ __forceinline__ void q_consume_encode(const QBatch& p, const QSmem& sm, int cw, int lane) {
+  const uint64_t t0 = p.n_tiles * blockIdx.x / gridDim.x, t1 = p.n_tiles * (blockIdx.x + 1) / gridDim.x;
+  uint32_t nan_acc = 0;
+  for (uint64_t i = 0; i < t1 - t0; ++i) {
+    const int stage = (int)(i % kQStages);
+    mbar_wait(&sm.full()[stage], (uint32_t)((i / kQStages) & 1));
+    const QHdr h = sm.hdr()[stage];
+    const uint8_t* tile = sm.tile(stage);
+    const uint32_t n_ch = h.n_el / kChunk;
+    switch (h.scheme) {
+      case HR_S_PASS16:
+        if (cw == 0 && lane == 0) bulk_s2g(h.codes, tile, 2 * h.n_el);
+        for (uint32_t c = cw; c < n_ch; c += kQWarps)
+          nan_acc = __vmaxu2(nan_acc, absmax_pair(*reinterpret_cast<const uint4*>(tile + 2 * (c * kChunk + lane * 8))));
+        if (cw == 0 && lane == 0) bulk_wait_read_all();  // the stage is released below
+        break;
+      case HR_S_INT8:
+        for (uint32_t eb = cw * kStep; eb < h.n_el; eb += kQWarps * kStep)
+          enc_int8_step<SEG / 4, DT>(tile, eb, h.n_el, h.codes, reinterpret_cast<float*>(h.meta), p.g_shift, lane,
+                                     nan_acc);
+        break;
+      case HR_S_INT4:
+        for (uint32_t eb = cw * kStep; eb < h.n_el; eb += kQWarps * kStep)
+          enc_int4_step<SEG / 4, DT>(tile, eb, h.n_el, h.codes, reinterpret_cast<float2*>(h.meta), p.g_shift, lane,
+                                     nan_acc);
+        break;
+      case HR_S_FP8E4M3:
+#pragma unroll 2
+        for (uint32_t c = cw; c < n_ch; c += kQWarps) {
+          const uint32_t e = c * kChunk + lane * 8;
+          enc_fp8<HR_S_FP8E4M3, DT>(*reinterpret_cast<const uint4*>(tile + 2 * e), h.codes, e, nan_acc);
+        }
+        break;
+      case HR_S_FP8E5M2:
+#pragma unroll 2
+        for (uint32_t c = cw; c < n_ch; c += kQWarps) {
+          const uint32_t e = c * kChunk + lane * 8;
+          enc_fp8<HR_S_FP8E5M2, DT>(*reinterpret_cast<const uint4*>(tile + 2 * e), h.codes, e, nan_acc);
+        }
+        break;
+      case HR_S_GSE8: {
+        const uint32_t tab = smem_addr(sm.gtab(stage));  // 1-KB aligned: entry address = tab | 4*ef
+#pragma unroll 2
+        for (uint32_t c = cw; c < n_ch; c += kQWarps) {
+          const uint32_t e = c * kChunk + lane * 8;
+          enc_gse<DT>(*reinterpret_cast<const uint4*>(tile + 2 * e), h.codes, tab, e, nan_acc);
+        }
+        break;
+      }
+      default:
+        break;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty()[stage]);
+  }
+  if (cw == 0 && lane == 0) bulk_wait_all();
+  if (pattern_nonfinite<DT>(nan_acc)) atomicOr(p.err, 1);
+}
+
+// RANGE mode: per-slab min / max biased fp32 exponent over nonzero normal values (R8, R9).
+// bf16: from 16-bit patterns two at a time — max magnitude pattern -> Emax; for Emin the key
+// (mag + 0x7F80) ^ 0x8000 maps normals (mag >= 0x80) to mag - 0x80 and zeros / subnormals above 0x7FFF,
+// so the minimum key is the smallest normal.  fp16: per element in fp32 (fp16 subnormals are fp32
+// normals).
+template <int DT>
+__device__ __forceinline__ void q_consume_range(const QBatch& p, const QSmem& sm, int cw, int lane) {
+  const uint64_t t0 = p.n_tiles * blockIdx.x / gridDim.x, t1 = p.n_tiles * (blockIdx.x + 1) / gridDim.x;
   bool bad = false;
-  while (wk.more()) {
-    uint4 raw[kBatch];
-    Geo g[kBatch];
-    uint32_t e[kBatch];
-    int n = 0;
+  for (uint64_t i = 0; i < t1 - t0; ++i) {
+    const int stage = (int)(i % kQStages);
+    mbar_wait(&sm.full()[stage], (uint32_t)((i / kQStages) & 1));
+    const QHdr h = sm.hdr()[stage];
+    const uint8_t* tile = sm.tile(stage);
+    const uint32_t n_ch = h.n_el / kChunk;
+    int emin = 255, emax = 0;
+    if constexpr (DT == HR_BF16) {
+      uint32_t mx = 0u, mn = 0xFFFFFFFFu;
+      for (uint32_t c = cw; c < n_ch; c += kQWarps) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(tile + 2 * (c * kChunk + lane * 8));
+        const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
 #pragma unroll
-    for (int b = 0; b < kBatch; ++b) {
-      if (wk.more()) {  // warp-uniform
-        g[b] = wk.g;
-        e[b] = wk.e0 + lane * 8;
-        raw[b] = __ldg(reinterpret_cast<const uint4*>(wk.g.src + e[b]));
-        wk.next(p);
-        n = b + 1;
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t mag = w[k] & 0x7FFF7FFFu;
+          mx = __vmaxu2(mx, mag);
+          mn = __vminu2(mn, (mag + 0x7F807F80u) ^ 0x80008000u);
+        }
+      }
+      const uint32_t pmax = max(mx & 0xFFFFu, mx >> 16), kmin = min(mn & 0xFFFFu, mn >> 16);
+      bad |= pmax >= 0x7F80u;
+      emax = (int)(pmax >> 7);
+      if (kmin < 0x8000u) emin = (int)((kmin + 0x80u) >> 7);
+    } else {
+      for (uint32_t c = cw; c < n_ch; c += kQWarps) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(tile + 2 * (c * kChunk + lane * 8));
+        float2 x[4];
+        unpack8<DT>(raw, x);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t b = __float_as_uint(k & 1 ? x[k >> 1].y : x[k >> 1].x);
+          const int ef = (b >> 23) & 0xFF;
+          bad |= ef == 255;
+          if (ef != 0) emin = min(emin, ef), emax = max(emax, ef);
+        }
       }
     }
 #pragma unroll
-    for (int b = 0; b < kBatch; ++b) {
-      if (b < n) {
-        float x[8];
-        const uint32_t w[4] = {raw[b].x, raw[b].y, raw[b].z, raw[b].w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) x[2 * i] = to_f32<DT>(w[i] & 0xFFFFu), x[2 * i + 1] = to_f32<DT>(w[i] >> 16);
-        encode_group_chunk<SCHEME, SEG, DT>(p, g[b], e[b], x, raw[b], lane, bad);
-      }
+    for (int o = 16; o; o >>= 1) {
+      emin = min(emin, __shfl_xor_sync(0xFFFFFFFFu, emin, o));
+      emax = max(emax, __shfl_xor_sync(0xFFFFFFFFu, emax, o));
     }
+    if (lane == 0 && emax != 0) {  // stored as (255 - min, max) so a zero fill initialises it
+      atomicMax(&h.range[0], 255 - emin);
+      atomicMax(&h.range[1], emax);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty()[stage]);
   }
   if (bad) atomicOr(p.err, 1);
 }
 
+template <int DT, int SEG, int MODE>
+__global__ void __launch_bounds__(kQThreadsB, 1) quantize_batch_kernel(const __grid_constant__ QBatch p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const QSmem sm{smem_raw};
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    if (smem_addr(smem_raw) & 1023u) __trap();  // GSE-8 table addressing (tab | 4*ef) needs 1-KB alignment
+    for (int s = 0; s < kQStages; ++s) {
+      mbar_init(&sm.full()[s], 1);
+      mbar_init(&sm.empty()[s], kQWarps);
+    }
+    mbar_init_fence();
+  }
+  __syncthreads();
+  if (warp == 0) {
+    q_produce<MODE>(p, sm, lane);
+  } else if (MODE == MODE_RANGE) {
+    q_consume_range<DT>(p, sm, warp - 1, lane);
+  } else {
+    q_consume_encode<DT, SEG>(p, sm, warp - 1, lane);
+  }
+}
+
 // ---------------------------------------------------------------- INT8 / INT4 (G > 256): warp per group
-template <int SCHEME, int DT>
-__global__ void __launch_bounds__(kQThreads) quant_biggroup_kernel(QuantParams p) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t slab = (uint64_t)p.T * p.D;
-  const uint32_t groups_per_slab = (uint32_t)(slab / p.G);
-  const uint64_t n_groups = (uint64_t)p.L * p.Hl * groups_per_slab;
+__device__ __forceinline__ void load8(const uint16_t* p, int dt, float (&x)[8]) {
+  const uint4 raw = __ldg(reinterpret_cast<const uint4*>(p));
+  const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    x[2 * i] = dt == HR_BF16 ? to_f32<HR_BF16>(w[i] & 0xFFFFu) : to_f32<HR_FP16>(w[i] & 0xFFFFu);
+    x[2 * i + 1] = dt == HR_BF16 ? to_f32<HR_BF16>(w[i] >> 16) : to_f32<HR_FP16>(w[i] >> 16);
+  }
+}
+__device__ __forceinline__ bool any_nonfinite(const float (&x)[8]) {
   bool bad = false;
-  for (uint64_t gi = (blockIdx.x * (uint64_t)kQThreads + threadIdx.x) / 32; gi < n_groups;
-       gi += (uint64_t)gridDim.x * kQThreads / 32) {
-    const uint32_t slab_i = (uint32_t)(gi / groups_per_slab);
-    const uint32_t grp = (uint32_t)(gi - (uint64_t)slab_i * groups_per_slab);
-    const Geo g = slab_geo(p, slab_i);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) bad |= !isfinite(x[i]);
+  return bad;
+}
+// rne(fl(x / s)) for 8 elements (the argument of enc_int4, per element)
+__device__ __forceinline__ void div_rne8(const float (&x)[8], float s, int (&q)[8]) {
+  float y;
+  asm("rcp.approx.f32 %0, %1;" : "=f"(y) : "f"(s));
+  const bool slow = !(s >= 1.17549435e-38f && s <= 8.50705917e+37f);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float t = __fmul_rn(x[i], y);
+    float r = rintf(t);
+    if (slow || fabsf(fabsf(__fsub_rn(t, r)) - 0.5f) <= 3.0517578125e-05f) r = rintf(__fdiv_rn(x[i], s));
+    q[i] = (int)r;
+  }
+}
+
+__global__ void __launch_bounds__(256) quant_biggroup_kernel(const __grid_constant__ QBatch p) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t slab = p.slab;
+  const uint32_t groups_per_slab = (uint32_t)(slab / p.G);
+  const uint64_t per_job = (uint64_t)p.L * p.Hl * groups_per_slab;
+  const uint64_t n_groups = per_job * p.n_jobs;
+  bool bad = false;
+  for (uint64_t gi = (blockIdx.x * 256ull + threadIdx.x) / 32; gi < n_groups; gi += (uint64_t)gridDim.x * 8) {
+    const uint32_t j = (uint32_t)(gi / per_job);
+    const uint64_t gj = gi - j * per_job;
+    const QJob& jb = p.jobs[j];
+    const uint32_t slab_i = (uint32_t)(gj / groups_per_slab);
+    const uint32_t grp = (uint32_t)(gj - (uint64_t)slab_i * groups_per_slab);
+    const uint32_t l = slab_i / p.Hl, hl = slab_i - l * p.Hl;
+    const uint16_t* src = jb.src + ((uint64_t)l * p.H + p.h0 + hl) * slab;
+    uint8_t* codes = jb.dst + slab_i * p.code_slab[jb.scheme];
+    uint8_t* meta = jb.dst + p.meta_off[jb.scheme] + (uint64_t)slab_i * p.meta_stride[jb.scheme];
     const uint32_t base = grp * p.G;
     float a = 0.f, mn = INFINITY, mx = -INFINITY;
     for (uint32_t e = base + lane * 8; e < base + p.G; e += kChunk) {  // pass 1: statistics
       float x[8];
-      uint4 raw;
-      load8<DT>(g.src + e, x, raw);
+      load8(src + e, p.dtype, x);
       bad |= any_nonfinite(x);
 #pragma unroll
       for (int i = 0; i < 8; ++i) a = fmaxf(a, fabsf(x[i])), mn = fminf(mn, x[i]), mx = fmaxf(mx, x[i]);
     }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      a = fmaxf(a, __shfl_xor_sync(0xFFFFFFFFu, a, o));
+      mn = fminf(mn, __shfl_xor_sync(0xFFFFFFFFu, mn, o));
+      mx = fmaxf(mx, __shfl_xor_sync(0xFFFFFFFFu, mx, o));
+    }
     float s, m0 = 0.f;
-    if constexpr (SCHEME == HR_S_INT8) {
-      a = seg_max(a, 32);
+    if (jb.scheme == HR_S_INT8) {
       s = (a == 0.f) ? 1.f : div127(a);
-      if (lane == 0) reinterpret_cast<float*>(g.meta)[grp] = s;
+      if (lane == 0) reinterpret_cast<float*>(meta)[grp] = s;
     } else {
-      mn = __fadd_rn(seg_min(mn, 32), 0.f);
-      mx = __fadd_rn(seg_max(mx, 32), 0.f);
+      mn = __fadd_rn(mn, 0.f);
+      mx = __fadd_rn(mx, 0.f);
       s = (mx == mn) ? 1.f : __fdiv_rn(sub_sat(mx, mn), 15.f);
       m0 = mn;
-      if (lane == 0) reinterpret_cast<float2*>(g.meta)[grp] = make_float2(s, mn);
+      if (lane == 0) reinterpret_cast<float2*>(meta)[grp] = make_float2(s, mn);
     }
     for (uint32_t e = base + lane * 8; e < base + p.G; e += kChunk) {  // pass 2: encode (L2 re-read)
       float x[8];
-      uint4 raw;
-      load8<DT>(g.src + e, x, raw);
+      load8(src + e, p.dtype, x);
       int q[8];
-      if constexpr (SCHEME == HR_S_INT8) {
+      if (jb.scheme == HR_S_INT8) {
         div_rne8(x, s, q);
         uint32_t w[2] = {0u, 0u};
 #pragma unroll
         for (int i = 0; i < 8; ++i) w[i >> 2] |= ((uint32_t)max(-127, min(127, q[i])) & 0xFFu) << (8 * (i & 3));
-        *reinterpret_cast<uint2*>(g.codes + e) = make_uint2(w[0], w[1]);
+        *reinterpret_cast<uint2*>(codes + e) = make_uint2(w[0], w[1]);
       } else {
         float u[8];
 #pragma unroll
@@ -319,234 +736,107 @@ __global__ void __launch_bounds__(kQThreads) quant_biggroup_kernel(QuantParams p
         uint32_t w = 0u;
 #pragma unroll
         for (int i = 0; i < 8; ++i) w |= (uint32_t)max(0, min(15, q[i])) << (4 * i);
-        *reinterpret_cast<uint32_t*>(g.codes + e / 2) = w;
+        *reinterpret_cast<uint32_t*>(codes + e / 2) = w;
       }
     }
   }
   if (bad) atomicOr(p.err, 1);
 }
 
-// ---------------------------------------------------------------- FP8 / PASS16: elementwise
-template <int SCHEME, int DT>
-__global__ void __launch_bounds__(kQThreads) quant_elementwise_kernel(QuantParams p) {
-  const uint32_t lane = threadIdx.x & 31;
-  Walker wk;
-  wk.init(p);
-  bool bad = false;
-  for (; wk.more(); wk.next(p)) {
-    const uint32_t e = wk.e0 + lane * 8;
-    float x[8];
-    uint4 raw;
-    load8<DT>(wk.g.src + e, x, raw);
-    bad |= any_nonfinite(x);
-    if constexpr (SCHEME == HR_S_PASS16) {
-      *reinterpret_cast<uint4*>(wk.g.codes + 2ull * e) = raw;
-    } else {
-      constexpr __nv_fp8_interpretation_t kInterp = SCHEME == HR_S_FP8E4M3 ? __NV_E4M3 : __NV_E5M2;
-      uint32_t w[2];
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {  // nearest code, ties to even, saturating (R5)
-        const uint32_t lo = __nv_cvt_float2_to_fp8x2(make_float2(x[4 * i], x[4 * i + 1]), __NV_SATFINITE, kInterp);
-        const uint32_t hi = __nv_cvt_float2_to_fp8x2(make_float2(x[4 * i + 2], x[4 * i + 3]), __NV_SATFINITE, kInterp);
-        w[i] = (lo & 0xFFFFu) | (hi << 16);
-      }
-      *reinterpret_cast<uint2*>(wk.g.codes + e) = make_uint2(w[0], w[1]);
-    }
-  }
-  if (bad) atomicOr(p.err, 1);
-}
-
-// ---------------------------------------------------------------- GSE-8
-// pass A: per-slab min/max biased exponent over nonzero normal values (R8, R9)
-template <int DT>
-__global__ void __launch_bounds__(kQThreads) gse_range_kernel(QuantParams p) {
-  const uint32_t lane = threadIdx.x & 31;
-  Walker wk;
-  wk.init(p);
-  const bool any_chunk = wk.more();
-  bool bad = false;
-  int emin = 255, emax = 0;
-  uint32_t cur = wk.slab_i;
-  auto flush = [&](uint32_t slab_i) {  // warp-reduce and publish the running range of one slab
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      emin = min(emin, __shfl_xor_sync(0xFFFFFFFFu, emin, o));
-      emax = max(emax, __shfl_xor_sync(0xFFFFFFFFu, emax, o));
-    }
-    if (lane == 0 && emax != 0) {  // stored as (255 - min, max) so a zero fill initialises it
-      atomicMax(&p.gse_range[2 * slab_i], 255 - emin);
-      atomicMax(&p.gse_range[2 * slab_i + 1], emax);
-    }
-    emin = 255, emax = 0;
-  };
-  for (; wk.more(); wk.next(p)) {
-    if (wk.slab_i != cur) flush(cur), cur = wk.slab_i;
-    float x[8];
-    uint4 raw;
-    load8<DT>(wk.g.src + wk.e0 + lane * 8, x, raw);
-    bad |= any_nonfinite(x);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int ef = (__float_as_uint(x[i]) >> 23) & 0xFF;
-      if (ef != 0) emin = min(emin, ef), emax = max(emax, ef);
-    }
-  }
-  if (any_chunk) flush(cur);
-  if (bad) atomicOr(p.err, 1);
-}
-
-// pass B: shared-exponent array from the range (R6) and the three steps of P:157-161
-template <int DT, int M>
-__global__ void __launch_bounds__(kQThreads) gse_encode_kernel(QuantParams p) {
-  const uint32_t lane = threadIdx.x & 31;
-  constexpr int step = M - 1, m = M, nmax = 1 << (7 - M);  // compile-time step: no integer division
-  Walker wk;
-  wk.init(p);
-  uint32_t cur = 0xFFFFFFFFu;
-  int lo = 0, n = 0, Emax = 0;
-  for (; wk.more(); wk.next(p)) {
-    const Geo& g = wk.g;
-    const uint32_t e = wk.e0 + lane * 8;
-    if (wk.slab_i != cur) {
-      cur = wk.slab_i;
-      const int rmin = 255 - p.gse_range[2 * cur], rmax = p.gse_range[2 * cur + 1];
-      const bool any = rmax != 0;
-      const int Emin = rmin - 127;
-      Emax = rmax - 127;
-      // lo = max(Emin, Emax - (2^e - 1) * step); G_i = min(lo + i*step, Emax), i < n
-      lo = max(Emin, Emax - (nmax - 1) * step);
-      n = any ? (Emax - lo + step - 1) / step + 1 : 0;
-    }
-    if (wk.e0 == 0) {
-      // meta record: int8 array [2^e] (unused -128), zero pad to 16 B, then the fp32 decode table
-      // [2^(e+1)]: entry (sign << e | i) = (-1)^sign 2^(G_i - (m-1)), 0 for unused i
-      if (lane < 16) {
-        int v = 0;
-        if ((int)lane < nmax) v = ((int)lane < n) ? min(lo + (int)lane * step, Emax) : -128;
-        g.meta[lane] = (uint8_t)(int8_t)v;
-      }
-      for (uint32_t w = lane; w < (p.meta_stride - 16) / 4; w += 32) {
-        float v = 0.f;
-        const int i = (int)w & (nmax - 1);
-        if ((int)w < 2 * nmax && i < n) {
-          const int k = min(lo + i * step, Emax) - step;
-          v = k >= -126 ? __int_as_float((k + 127) << 23) : (k >= -149 ? __int_as_float(1 << (k + 149)) : 0.f);
-          if ((int)w >= nmax) v = -v;
-        }
-        reinterpret_cast<float*>(g.meta + 16)[w] = v;
-      }
-    }
-    float x[8];
-    uint4 raw;
-    load8<DT>(g.src + e, x, raw);
-    uint32_t w[2] = {0u, 0u};
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const uint32_t b = __float_as_uint(x[i]);
-      const int ef = (b >> 23) & 0xFF;
-      uint32_t byte = 0u;
-      if (ef != 0) {
-        const int E = ef - 127;
-        const int idx = (E <= lo) ? 0 : (E - lo + step - 1) / step;  // smallest G_i >= E
-        const int G = min(lo + idx * step, Emax);
-        const int d = G - E;
-        if (d <= m - 1) {  // else below the array's reach: flush (R9)
-          const int keep = m - 1 - d;
-          // marker 1 at position d+1 from the MSB, then the top fraction bits (truncated)
-          const uint32_t field = (1u << keep) | ((b & 0x7FFFFFu) >> (23 - keep));
-          byte = ((b >> 31) << 7) | ((uint32_t)idx << m) | field;
-        }
-      }
-      w[i >> 2] |= byte << (8 * (i & 3));
-    }
-    *reinterpret_cast<uint2*>(g.codes + e) = make_uint2(w[0], w[1]);
-  }
-}
-
+// ---------------------------------------------------------------- launch
 int g_num_sms = 0;
-// One wave of resident CTAs (the warps walk contiguous chunk blocks): SMs x occupancy of `kernel`.
-template <class K>
-int grid_for(K kernel, uint64_t warps) {
+
+template <int DT, int SEG, int MODE>
+void launch_b(const QBatch& b, cudaStream_t st) {
+  static bool init = false;
+  if (!init) {
+    HR_CUDA(cudaFuncSetAttribute(quantize_batch_kernel<DT, SEG, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)kQSmemBytes));
+    init = true;
+  }
+  const uint64_t grid = std::min<uint64_t>(b.n_tiles, (uint64_t)g_num_sms);
+  quantize_batch_kernel<DT, SEG, MODE><<<(unsigned)grid, kQThreadsB, kQSmemBytes, st>>>(b);
+}
+
+template <int DT>
+void launch_seg(const QBatch& b, int mode, cudaStream_t st) {
+  if (mode == MODE_RANGE) return launch_b<DT, 16, MODE_RANGE>(b, st);
+  switch (b.G) {  // SEG = G / 8 lanes per group
+    case 32: return launch_b<DT, 4, MODE_ENCODE>(b, st);
+    case 64: return launch_b<DT, 8, MODE_ENCODE>(b, st);
+    case 128: return launch_b<DT, 16, MODE_ENCODE>(b, st);
+    case 256: return launch_b<DT, 32, MODE_ENCODE>(b, st);
+    default:  // G > 256: the batch holds no INT8 / INT4 job (they take quant_biggroup_kernel)
+      require(b.G > 256, HR_EINVAL, "group size must be a power of two >= 32");
+      return launch_b<DT, 32, MODE_ENCODE>(b, st);
+  }
+}
+
+void run_batch(QBatch& b, int mode, cudaStream_t st) {
+  b.tile_e = std::min<uint32_t>(kQTileE, b.slab);
+  b.tiles_per_slab = (b.slab + b.tile_e - 1) / b.tile_e;
+  b.n_tiles = (uint64_t)b.n_jobs * b.L * b.Hl * b.tiles_per_slab;
+  if (!b.n_tiles) return;
+  if (b.dtype == HR_BF16)
+    launch_seg<HR_BF16>(b, mode, st);
+  else
+    launch_seg<HR_FP16>(b, mode, st);
+}
+
+}  // namespace
+
+void launch_quantize(const QuantParams* items, int n, cudaStream_t st) {
+  if (n <= 0) return;
   if (!g_num_sms) {
     int dev = 0;
     HR_CUDA(cudaGetDevice(&dev));
     HR_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev));
   }
-  static std::unordered_map<const void*, int> cache;  // occupancy per kernel
-  auto it = cache.find((const void*)kernel);
-  if (it == cache.end()) {
-    int o = 0;
-    HR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kernel, kQThreads, 0));
-    it = cache.emplace((const void*)kernel, o).first;
+  const QuantParams& q0 = items[0];
+  const uint64_t slab = (uint64_t)q0.T * q0.D;
+  require(slab % kChunk == 0, HR_EINVAL, "T*D must be a multiple of 256");
+  require(slab <= (1ull << 31), HR_EINVAL, "slab too large");
+  QBatch base{};
+  base.L = q0.L, base.H = q0.H, base.Hl = q0.Hl, base.h0 = q0.h0, base.T = q0.T, base.D = q0.D, base.G = q0.G;
+  base.g_shift = q0.g_shift, base.gse_e = q0.gse_e, base.gse_m = q0.gse_m, base.dtype = q0.dtype;
+  base.slab = (uint32_t)slab;
+  base.err = q0.err;
+  for (int i = 0; i < n; ++i) {
+    const QuantParams& q = items[i];
+    require(q.scheme <= HR_S_INT4, HR_EINVAL, "unknown scheme");
+    require(q.L == q0.L && q.H == q0.H && q.Hl == q0.Hl && q.h0 == q0.h0 && q.T == q0.T && q.D == q0.D &&
+                q.G == q0.G && q.dtype == q0.dtype && q.gse_m == q0.gse_m && q.err == q0.err,
+            HR_EINVAL, "a quantize batch shares one layout");
+    base.code_slab[q.scheme] = q.code_bytes_slab;
+    base.meta_off[q.scheme] = q.meta_offset;
+    base.meta_stride[q.scheme] = (uint32_t)q.meta_stride;
   }
-  const int occ = it->second;
-  const uint64_t want = (warps * 32 + kQThreads - 1) / kQThreads;
-  const uint64_t cap = (uint64_t)g_num_sms * (occ > 0 ? occ : 1);
-  return (int)(want < cap ? (want ? want : 1) : cap);
-}
-
-template <int DT>
-void launch_dt(const QuantParams& p, cudaStream_t st) {
-  const uint64_t slab = (uint64_t)p.T * p.D;
-  const uint64_t chunks = (uint64_t)p.L * p.Hl * (slab / kChunk);
-#define LAUNCH(KERNEL, WORK) KERNEL<<<grid_for(KERNEL, WORK), kQThreads, 0, st>>>(p)
-  switch (p.scheme) {
-    case HR_S_PASS16:
-      LAUNCH((quant_elementwise_kernel<HR_S_PASS16, DT>), chunks);
-      break;
-    case HR_S_FP8E4M3:
-      LAUNCH((quant_elementwise_kernel<HR_S_FP8E4M3, DT>), chunks);
-      break;
-    case HR_S_FP8E5M2:
-      LAUNCH((quant_elementwise_kernel<HR_S_FP8E5M2, DT>), chunks);
-      break;
-    case HR_S_INT8:
-    case HR_S_INT4: {
-      if (p.G <= (uint32_t)kChunk) {
-        switch ((p.G >> 3) * 16 + (p.scheme == HR_S_INT8 ? 0 : 1)) {
-#define QG(SEGV)                                                        \
-  case SEGV * 16 + 0: LAUNCH((quant_group_kernel<HR_S_INT8, SEGV, DT>), chunks); break; \
-  case SEGV * 16 + 1: LAUNCH((quant_group_kernel<HR_S_INT4, SEGV, DT>), chunks); break;
-          QG(4) QG(8) QG(16) QG(32)
-#undef QG
-          default: fail(HR_EINVAL, "group size must be a power of two >= 32");
-        }
-      } else {
-        const uint64_t groups = (uint64_t)p.L * p.Hl * (slab / p.G);
-        if (p.scheme == HR_S_INT8)
-          LAUNCH((quant_biggroup_kernel<HR_S_INT8, DT>), groups);
-        else
-          LAUNCH((quant_biggroup_kernel<HR_S_INT4, DT>), groups);
+  const uint64_t n_slabs = (uint64_t)q0.L * q0.Hl;
+  // pass 1: GSE-8 exponent ranges; big groups
+  QBatch rng = base, big = base, enc = base;
+  for (int i = 0; i < n; ++i) {
+    const QuantParams& q = items[i];
+    const QJob job{q.src, q.dst, q.gse_range, q.scheme, 0};
+    const bool is_big = (q.scheme == HR_S_INT8 || q.scheme == HR_S_INT4) && q.G > (uint32_t)kChunk;
+    if (q.scheme == HR_S_GSE8) {
+      require(q.gse_range != nullptr, HR_EINVAL, "GSE-8 quantize needs range scratch");
+      HR_CUDA(cudaMemsetAsync(q.gse_range, 0, sizeof(int) * 2 * n_slabs, st));
+      rng.jobs[rng.n_jobs++] = job;
+    }
+    (is_big ? big : enc).jobs[(is_big ? big : enc).n_jobs++] = job;
+    const bool last = i + 1 == n;
+    if (rng.n_jobs == kQMaxJobs || enc.n_jobs == kQMaxJobs || big.n_jobs == kQMaxJobs || last) {
+      run_batch(rng, MODE_RANGE, st);
+      run_batch(enc, MODE_ENCODE, st);
+      if (big.n_jobs) {
+        const uint64_t warps = (uint64_t)big.n_jobs * n_slabs * (slab / q0.G);
+        const uint64_t grid = std::min<uint64_t>((warps + 7) / 8, (uint64_t)g_num_sms * 8);
+        quant_biggroup_kernel<<<(unsigned)grid, 256, 0, st>>>(big);
       }
-      break;
+      rng.n_jobs = enc.n_jobs = big.n_jobs = 0;
     }
-    case HR_S_GSE8: {
-      const uint64_t n_slabs = (uint64_t)p.L * p.Hl;
-      HR_CUDA(cudaMemsetAsync(p.gse_range, 0, sizeof(int) * 2 * n_slabs, st));
-      LAUNCH((gse_range_kernel<DT>), chunks);
-      if (p.gse_m == 3)
-        LAUNCH((gse_encode_kernel<DT, 3>), chunks);
-      else if (p.gse_m == 4)
-        LAUNCH((gse_encode_kernel<DT, 4>), chunks);
-      else
-        LAUNCH((gse_encode_kernel<DT, 5>), chunks);
-      break;
-    }
-    default:
-      fail(HR_EINVAL, "unknown scheme");
   }
-#undef LAUNCH
   HR_CUDA(cudaGetLastError());
-}
-
-}  // namespace
-
-void launch_quantize(const QuantParams& p, cudaStream_t st) {
-  require(((uint64_t)p.T * p.D) % kChunk == 0, HR_EINVAL, "T*D must be a multiple of 256");
-  if (p.dtype == HR_BF16)
-    launch_dt<HR_BF16>(p, st);
-  else
-    launch_dt<HR_FP16>(p, st);
 }
 
 }  // namespace harag

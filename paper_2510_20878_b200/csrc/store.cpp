@@ -250,7 +250,7 @@ void Store::setup(uint32_t nd, const uint64_t* hot, std::vector<uint32_t> sc, bo
   HR_CUDA(cudaMalloc(&err_flag, sizeof(int)));
   HR_CUDA(cudaMemset(err_flag, 0, sizeof(int)));
   HR_CUDA(cudaMalloc(&scratch, 2 * max_item));
-  HR_CUDA(cudaMalloc(&gse_range, sizeof(int) * 2 * lay.n_slabs()));
+  HR_CUDA(cudaMalloc(&gse_range, sizeof(int) * 4 * lay.n_slabs()));  // K and V of a put
   put_done.assign(n_docs, 0);
   backing_filled.clear();
 }
@@ -266,25 +266,38 @@ void Store::build_put(uint32_t doc, const void* k_src, const void* v_src, cudaSt
   require(state == State::Building, HR_ESTATE, "hr_build_put outside begin/end");
   require(doc < n_docs, HR_ENOTFOUND, "doc id out of range");
   require(k_src && v_src, HR_EINVAL, "source pointer is NULL");
+  QuantParams q[2]{};
+  uint8_t* dsts[2];
   for (uint32_t kind = 0; kind < 2; ++kind) {
     const uint32_t item = 2 * doc + kind;
     const uint32_t s = scheme[item];
     uint8_t* dst = tier[item] == HR_T_HBM ? hbm_ptr(item) : scratch + kind * max_item;
-    QuantParams q{};
-    q.src = (const uint16_t*)(kind ? v_src : k_src);
-    q.dst = dst;
-    q.L = lay.L, q.H = lay.H, q.Hl = lay.Hl, q.h0 = lay.h0, q.T = lay.T, q.D = lay.D, q.G = lay.G;
-    q.gse_e = lay.gse_e, q.gse_m = lay.gse_m, q.dtype = lay.dtype, q.scheme = s;
-    q.g_shift = (uint32_t)__builtin_ctz(lay.G);
-    q.code_bytes_slab = lay.code_bytes_slab(s);
-    q.meta_offset = lay.meta_offset(s);
-    q.meta_stride = lay.meta_stride(s);
-    q.err = err_flag;
-    q.gse_range = gse_range;
-    // zero padding and meta (records may end in padding) so exported blobs are deterministic
-    const uint64_t cend = lay.n_slabs() * q.code_bytes_slab;
-    if (bytes[item] > cend) HR_CUDA(cudaMemsetAsync(dst + cend, 0, bytes[item] - cend, st));
-    launch_quantize(q, st);
+    dsts[kind] = dst;
+    QuantParams& qk = q[kind];
+    qk.src = (const uint16_t*)(kind ? v_src : k_src);
+    qk.dst = dst;
+    qk.L = lay.L, qk.H = lay.H, qk.Hl = lay.Hl, qk.h0 = lay.h0, qk.T = lay.T, qk.D = lay.D, qk.G = lay.G;
+    qk.gse_e = lay.gse_e, qk.gse_m = lay.gse_m, qk.dtype = lay.dtype, qk.scheme = s;
+    qk.g_shift = (uint32_t)__builtin_ctz(lay.G);
+    qk.code_bytes_slab = lay.code_bytes_slab(s);
+    qk.meta_offset = lay.meta_offset(s);
+    qk.meta_stride = lay.meta_stride(s);
+    qk.err = err_flag;
+    qk.gse_range = gse_range + kind * 2 * lay.n_slabs();
+    // zero the padding (the kernels write codes and meta records only) so exported blobs are deterministic
+    const uint64_t cend = lay.n_slabs() * qk.code_bytes_slab;
+    const uint64_t mend = qk.meta_offset + lay.n_slabs() * qk.meta_stride;
+    if (qk.meta_stride > lay.meta_raw_slab(s)) {  // padded records: zero the whole meta section
+      HR_CUDA(cudaMemsetAsync(dst + cend, 0, bytes[item] - cend, st));
+    } else {
+      if (qk.meta_offset > cend) HR_CUDA(cudaMemsetAsync(dst + cend, 0, qk.meta_offset - cend, st));
+      if (bytes[item] > mend) HR_CUDA(cudaMemsetAsync(dst + mend, 0, bytes[item] - mend, st));
+    }
+  }
+  launch_quantize(q, 2, st);
+  for (uint32_t kind = 0; kind < 2; ++kind) {
+    const uint32_t item = 2 * doc + kind;
+    uint8_t* dst = dsts[kind];
     if (loc[item].backing_off != FreeList::kNone && !backing_filled.count(loc[item].backing_off)) {
       // bench aliasing: a shared blob is written once (its docs have identical sources by contract)
       HR_CUDA(cudaMemcpyAsync(backing_base + loc[item].backing_off, dst, bytes[item], cudaMemcpyDeviceToHost, st));

@@ -615,10 +615,12 @@ def test_int8_scale_all_16bit_values(torch_cuda, dtype):
 
 
 def test_markstein_division_exhaustive(torch_cuda):
-    """The INT8 quantizer computes fl(x/s) without a division (Markstein's FMA
-    correction).  tests/csrc/markstein_check.cu compares it with
-    IEEE division for every pair of 16-bit values (a, x), |x| <= a, bf16 and
-    fp16 (2.07e9 pairs): zero mismatches required."""
+    """The INT8 / INT4 quantizers compute fl(x/s) without a division
+    (Markstein's FMA correction).  tests/csrc/markstein_check.cu
+    compares INT8 with IEEE division for every pair of 16-bit values (a, x),
+    |x| <= a, bf16 and fp16 (2.07e9 pairs), and INT4's two-correction variant
+    on 2^36 sampled (x, mn, mx) triples per dtype, half of them steered onto
+    quantisation ties: zero mismatches required."""
     import os
     import subprocess
     exe = os.path.join(os.path.dirname(__file__), "csrc", "markstein_check")
