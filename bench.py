@@ -335,21 +335,25 @@ def run_per_scheme(ctx, wl, args):
     B, k, n_docs = 16, wl["k"], 400
     L, H, D, T = wl["L"], wl["H"], wl["D"], wl["T"]
     geo = dict(L=L, H=H, D=D, T=T, dtype=wl["dtype"], rank=ctx.rank, world=ctx.world)
-    src = torch.empty(2, L * H * T * D, dtype=torch.int16, device="cuda")
-    synth.gen_item_device(src[0].data_ptr(), L, H, T, D, 0, 0, dtype=wl["dtype"])
-    synth.gen_item_device(src[1].data_ptr(), L, H, T, D, 0, 1, dtype=wl["dtype"])
+    NS = 8   # distinct source docs cycled through the puts: 8 x K+V >> L2, so every source read is an HBM read
+    src = torch.empty(NS, 2, L * H * T * D, dtype=torch.int16, device="cuda")
+    for i in range(NS):
+        synth.gen_item_device(src[i, 0].data_ptr(), L, H, T, D, i, 0, dtype=wl["dtype"])
+        synth.gen_item_device(src[i, 1].data_ptr(), L, H, T, D, i, 1, dtype=wl["dtype"])
     for scheme in ("PASS16", "INT8", "FP8E4M3", "FP8E5M2", "GSE8", "INT4"):
         item = hr.item_bytes(scheme, **geo)
         st = hr.Store(ladder=(scheme,), taus=(), device=ctx.device, keep_backing=False,
                       hbm_budget=2 * n_docs * item + (1 << 20), **geo)
         st.build_begin(n_docs, np.zeros(2 * n_docs, np.uint64))
-        for d in range(3):
-            st.build_put(d, src[0], src[1], stream=ctx.stream)
+        st.build_put_batch(range(3), [src[i, 0] for i in range(3)], [src[i, 1] for i in range(3)], stream=ctx.stream)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record(ctx.stream)
-        for d in range(n_docs):   # every doc quantised from the same resident source (identical items)
-            st.build_put(d, src[0], src[1], stream=ctx.stream)
+        QB = 8   # docs per hr_build_put_batch call (one quantize launch of 16 items)
+        for d in range(0, n_docs, QB):
+            nd = min(QB, n_docs - d)
+            st.build_put_batch(range(d, d + nd), [src[(d + i) % NS, 0] for i in range(nd)],
+                               [src[(d + i) % NS, 1] for i in range(nd)], stream=ctx.stream)
         e1.record(ctx.stream)
         st.build_end(stream=ctx.stream)
         q_ms = e0.elapsed_time(e1)

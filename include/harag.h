@@ -154,6 +154,12 @@ hr_status hr_build_store(hr_store* s, uint32_t n_docs, const uint64_t* hotness,
  * seen, else HR_EINVAL). */
 hr_status hr_build_begin(hr_store* s, uint32_t n_docs, const uint64_t* hotness);
 hr_status hr_build_put(hr_store* s, uint32_t doc, const void* k_src, const void* v_src, void* stream);
+/* hr_build_put for n <= 16 distinct docs in one quantize launch (all 2n items, any scheme mix):
+ * docs host uint32[n], k_srcs / v_srcs host arrays of n DEVICE pointers (same rules as hr_build_put).
+ * HR_EINVAL for n > 16, a NULL pointer or a repeated doc; HR_ENOTFOUND for a doc >= n_docs; checks
+ * precede any launch. */
+hr_status hr_build_put_batch(hr_store* s, uint32_t n, const uint32_t* docs, const void* const* k_srcs,
+                             const void* const* v_srcs, void* stream);
 hr_status hr_build_end(hr_store* s, void* stream);
 
 /* --------------------------------------------------------------- assemble

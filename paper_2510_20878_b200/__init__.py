@@ -117,6 +117,14 @@ class Store:
     def build_put(self, doc: int, k_src, v_src, stream=None) -> None:
         check(lib.hr_build_put(self._h, doc, _ptr(k_src), _ptr(v_src), _stream(stream)))
 
+    def build_put_batch(self, docs, k_srcs, v_srcs, stream=None) -> None:
+        """hr_build_put_batch: up to 16 docs quantised in one launch."""
+        n = len(docs)
+        d = (C.c_uint32 * n)(*[int(x) for x in docs])
+        ks = (C.c_void_p * n)(*[_ptr(x) for x in k_srcs])
+        vs = (C.c_void_p * n)(*[_ptr(x) for x in v_srcs])
+        check(lib.hr_build_put_batch(self._h, n, d, ks, vs, _stream(stream)))
+
     def build_end(self, stream=None) -> None:
         check(lib.hr_build_end(self._h, _stream(stream)))
 

@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libharag.so")
+LIB_PATH = os.environ.get("HARAG_LIB") or os.path.join(_HERE, "libharag.so")  # HARAG_LIB: tuning variants only
 
 HR_OK, HR_EINVAL, HR_ENOMEM, HR_ECUDA, HR_ENOTFOUND, HR_ECORRUPT, HR_ESTATE = range(7)
 STATUS_NAMES = {0: "HR_OK", 1: "HR_EINVAL", 2: "HR_ENOMEM", 3: "HR_ECUDA", 4: "HR_ENOTFOUND",
@@ -54,6 +54,7 @@ lib = C.CDLL(LIB_PATH)
 
 P, U32, U64, I32, DBL, SZ = C.c_void_p, C.c_uint32, C.c_uint64, C.c_int, C.c_double, C.c_size_t
 PU32, PU64, PI64 = C.POINTER(C.c_uint32), C.POINTER(C.c_uint64), C.POINTER(C.c_int64)
+PP = C.POINTER(C.c_void_p)
 
 _SIGS = {
     "hr_last_error": (C.c_char_p, []),
@@ -64,6 +65,7 @@ _SIGS = {
     "hr_build_store": (I32, [P, U32, PU64, SRC_FN, P, P]),
     "hr_build_begin": (I32, [P, U32, PU64]),
     "hr_build_put": (I32, [P, U32, P, P, P]),
+    "hr_build_put_batch": (I32, [P, U32, PU32, PP, PP, P]),
     "hr_build_end": (I32, [P, P]),
     "hr_kv_bytes": (SZ, [P, U32]),
     "hr_assemble_kv": (I32, [P, U32, U32, PU32, C.POINTER(P), C.POINTER(P), P]),

@@ -68,7 +68,7 @@ def build(verbose: bool = False) -> list[str]:
     """Compile every CUDA/C++ library in-tree; returns the libraries rebuilt."""
     csrc = os.path.join(PKG, "csrc")
     srcs = sorted(glob.glob(os.path.join(csrc, "*.cpp")) + glob.glob(os.path.join(csrc, "kernels", "*.cu")))
-    hdrs = sorted(glob.glob(os.path.join(csrc, "*.h")) + [os.path.join(ROOT, "include", "harag.h")])
+    hdrs = sorted(glob.glob(os.path.join(csrc, "*.h")) + glob.glob(os.path.join(csrc, "kernels", "*.h")) + [os.path.join(ROOT, "include", "harag.h")])
     built = []
     if _lib(LIBHARAG, srcs, hdrs, os.path.join(ROOT, "build", "harag")):
         built.append(LIBHARAG)

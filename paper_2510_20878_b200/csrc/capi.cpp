@@ -97,6 +97,13 @@ hr_status hr_build_put(hr_store* s, uint32_t doc, const void* k_src, const void*
     s->impl.build_put(doc, k_src, v_src, S(stream));
   });
 }
+hr_status hr_build_put_batch(hr_store* s, uint32_t n, const uint32_t* docs, const void* const* k_srcs,
+                             const void* const* v_srcs, void* stream) {
+  return guard([&] {
+    NONNULL(s);
+    s->impl.build_put_batch(n, docs, k_srcs, v_srcs, S(stream));
+  });
+}
 hr_status hr_build_end(hr_store* s, void* stream) {
   return guard([&] {
     NONNULL(s);

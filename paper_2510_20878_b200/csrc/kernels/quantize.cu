@@ -555,7 +555,7 @@ __device__ __forceinline__ void q_consume_encode(const QBatch& p, const QSmem& s
         break;
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty()[stage]);
+    if (lane == 0) mbar_arrive_relaxed(&sm.empty()[stage]);
   }
   if (cw == 0 && lane == 0) bulk_wait_all();
   if (pattern_nonfinite<DT>(nan_acc)) atomicOr(p.err, 1);
@@ -570,13 +570,30 @@ template <int DT>
 __device__ __forceinline__ void q_consume_range(const QBatch& p, const QSmem& sm, int cw, int lane) {
   const uint64_t t0 = p.n_tiles * blockIdx.x / gridDim.x, t1 = p.n_tiles * (blockIdx.x + 1) / gridDim.x;
   bool bad = false;
+  int emin = 255, emax = 0;  // running range of the current slab (this warp's chunks)
+  int* cur = nullptr;
+  auto flush = [&] {  // warp-reduce and publish the running range of slab `cur`
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      emin = min(emin, __shfl_xor_sync(0xFFFFFFFFu, emin, o));
+      emax = max(emax, __shfl_xor_sync(0xFFFFFFFFu, emax, o));
+    }
+    if (lane == 0 && emax != 0) {  // stored as (255 - min, max) so a zero fill initialises it
+      atomicMax(&cur[0], 255 - emin);
+      atomicMax(&cur[1], emax);
+    }
+    emin = 255, emax = 0;
+  };
   for (uint64_t i = 0; i < t1 - t0; ++i) {
     const int stage = (int)(i % kQStages);
     mbar_wait(&sm.full()[stage], (uint32_t)((i / kQStages) & 1));
     const QHdr h = sm.hdr()[stage];
     const uint8_t* tile = sm.tile(stage);
     const uint32_t n_ch = h.n_el / kChunk;
-    int emin = 255, emax = 0;
+    if (h.range != cur) {
+      if (cur) flush();
+      cur = h.range;
+    }
     if constexpr (DT == HR_BF16) {
       uint32_t mx = 0u, mn = 0xFFFFFFFFu;
       for (uint32_t c = cw; c < n_ch; c += kQWarps) {
@@ -591,8 +608,8 @@ __device__ __forceinline__ void q_consume_range(const QBatch& p, const QSmem& sm
       }
       const uint32_t pmax = max(mx & 0xFFFFu, mx >> 16), kmin = min(mn & 0xFFFFu, mn >> 16);
       bad |= pmax >= 0x7F80u;
-      emax = (int)(pmax >> 7);
-      if (kmin < 0x8000u) emin = (int)((kmin + 0x80u) >> 7);
+      emax = max(emax, (int)(pmax >> 7));
+      if (kmin < 0x8000u) emin = min(emin, (int)((kmin + 0x80u) >> 7));
     } else {
       for (uint32_t c = cw; c < n_ch; c += kQWarps) {
         const uint4 raw = *reinterpret_cast<const uint4*>(tile + 2 * (c * kChunk + lane * 8));
@@ -607,18 +624,10 @@ __device__ __forceinline__ void q_consume_range(const QBatch& p, const QSmem& sm
         }
       }
     }
-#pragma unroll
-    for (int o = 16; o; o >>= 1) {
-      emin = min(emin, __shfl_xor_sync(0xFFFFFFFFu, emin, o));
-      emax = max(emax, __shfl_xor_sync(0xFFFFFFFFu, emax, o));
-    }
-    if (lane == 0 && emax != 0) {  // stored as (255 - min, max) so a zero fill initialises it
-      atomicMax(&h.range[0], 255 - emin);
-      atomicMax(&h.range[1], emax);
-    }
     __syncwarp();
-    if (lane == 0) mbar_arrive(&sm.empty()[stage]);
+    if (lane == 0) mbar_arrive_relaxed(&sm.empty()[stage]);
   }
+  if (cur) flush();
   if (bad) atomicOr(p.err, 1);
 }
 
@@ -812,30 +821,46 @@ void launch_quantize(const QuantParams* items, int n, cudaStream_t st) {
     base.meta_stride[q.scheme] = (uint32_t)q.meta_stride;
   }
   const uint64_t n_slabs = (uint64_t)q0.L * q0.Hl;
-  // pass 1: GSE-8 exponent ranges; big groups
-  QBatch rng = base, big = base, enc = base;
+  // GSE-8 items go in pairs (range pass, then encode while the pair's source is still in L2: a Llama-3-8B
+  // K+V pair is 67 MB of the 126 MB L2); every other item of the call shares one encode launch per
+  // kQMaxJobs; INT8 / INT4 with G > 256 take the big-group kernel.
+  QBatch rng = base, big = base, enc = base, gse = base;
+  auto flush_gse = [&] {
+    if (!gse.n_jobs) return;
+    rng.n_jobs = 0;
+    for (uint32_t j = 0; j < gse.n_jobs; ++j) {
+      HR_CUDA(cudaMemsetAsync(gse.jobs[j].range, 0, sizeof(int) * 2 * n_slabs, st));
+      rng.jobs[rng.n_jobs++] = gse.jobs[j];
+    }
+    run_batch(rng, MODE_RANGE, st);
+    run_batch(gse, MODE_ENCODE, st);
+    gse.n_jobs = 0;
+  };
+  auto flush_big = [&] {
+    if (!big.n_jobs) return;
+    const uint64_t warps = (uint64_t)big.n_jobs * n_slabs * (slab / q0.G);
+    const uint64_t grid = std::min<uint64_t>((warps + 7) / 8, (uint64_t)g_num_sms * 8);
+    quant_biggroup_kernel<<<(unsigned)grid, 256, 0, st>>>(big);
+    big.n_jobs = 0;
+  };
   for (int i = 0; i < n; ++i) {
     const QuantParams& q = items[i];
     const QJob job{q.src, q.dst, q.gse_range, q.scheme, 0};
-    const bool is_big = (q.scheme == HR_S_INT8 || q.scheme == HR_S_INT4) && q.G > (uint32_t)kChunk;
     if (q.scheme == HR_S_GSE8) {
       require(q.gse_range != nullptr, HR_EINVAL, "GSE-8 quantize needs range scratch");
-      HR_CUDA(cudaMemsetAsync(q.gse_range, 0, sizeof(int) * 2 * n_slabs, st));
-      rng.jobs[rng.n_jobs++] = job;
-    }
-    (is_big ? big : enc).jobs[(is_big ? big : enc).n_jobs++] = job;
-    const bool last = i + 1 == n;
-    if (rng.n_jobs == kQMaxJobs || enc.n_jobs == kQMaxJobs || big.n_jobs == kQMaxJobs || last) {
-      run_batch(rng, MODE_RANGE, st);
-      run_batch(enc, MODE_ENCODE, st);
-      if (big.n_jobs) {
-        const uint64_t warps = (uint64_t)big.n_jobs * n_slabs * (slab / q0.G);
-        const uint64_t grid = std::min<uint64_t>((warps + 7) / 8, (uint64_t)g_num_sms * 8);
-        quant_biggroup_kernel<<<(unsigned)grid, 256, 0, st>>>(big);
-      }
-      rng.n_jobs = enc.n_jobs = big.n_jobs = 0;
+      gse.jobs[gse.n_jobs++] = job;
+      if (gse.n_jobs == 2) flush_gse();
+    } else if ((q.scheme == HR_S_INT8 || q.scheme == HR_S_INT4) && q.G > (uint32_t)kChunk) {
+      big.jobs[big.n_jobs++] = job;
+      if (big.n_jobs == kQMaxJobs) flush_big();
+    } else {
+      enc.jobs[enc.n_jobs++] = job;
+      if (enc.n_jobs == kQMaxJobs) run_batch(enc, MODE_ENCODE, st), enc.n_jobs = 0;
     }
   }
+  flush_gse();
+  flush_big();
+  run_batch(enc, MODE_ENCODE, st);
   HR_CUDA(cudaGetLastError());
 }
 

@@ -249,8 +249,8 @@ void Store::setup(uint32_t nd, const uint64_t* hot, std::vector<uint32_t> sc, bo
   HR_CUDA(cudaMemset(delta, 0, sizeof(int64_t) * n_items));
   HR_CUDA(cudaMalloc(&err_flag, sizeof(int)));
   HR_CUDA(cudaMemset(err_flag, 0, sizeof(int)));
-  HR_CUDA(cudaMalloc(&scratch, 2 * max_item));
-  HR_CUDA(cudaMalloc(&gse_range, sizeof(int) * 4 * lay.n_slabs()));  // K and V of a put
+  scratch = nullptr, scratch_items = 0;  // allocated by the first put that needs it
+  HR_CUDA(cudaMalloc(&gse_range, sizeof(int) * 2 * 2 * kPutBatch * lay.n_slabs()));  // every item of a put batch
   put_done.assign(n_docs, 0);
   backing_filled.clear();
 }
@@ -263,18 +263,41 @@ uint64_t Store::backing_key(uint32_t item) const {
 }
 
 void Store::build_put(uint32_t doc, const void* k_src, const void* v_src, cudaStream_t st) {
+  build_put_batch(1, &doc, &k_src, &v_src, st);
+}
+
+void Store::build_put_batch(uint32_t n, const uint32_t* docs, const void* const* k_srcs, const void* const* v_srcs,
+                            cudaStream_t st) {
   require(state == State::Building, HR_ESTATE, "hr_build_put outside begin/end");
-  require(doc < n_docs, HR_ENOTFOUND, "doc id out of range");
-  require(k_src && v_src, HR_EINVAL, "source pointer is NULL");
-  QuantParams q[2]{};
-  uint8_t* dsts[2];
-  for (uint32_t kind = 0; kind < 2; ++kind) {
-    const uint32_t item = 2 * doc + kind;
+  require(n <= kPutBatch, HR_EINVAL, "hr_build_put_batch: at most 16 docs per call");
+  require(n == 0 || (docs && k_srcs && v_srcs), HR_EINVAL, "NULL array");
+  for (uint32_t i = 0; i < n; ++i) {
+    require(docs[i] < n_docs, HR_ENOTFOUND, "doc id out of range");
+    require(k_srcs[i] && v_srcs[i], HR_EINVAL, "source pointer is NULL");
+    for (uint32_t j = 0; j < i; ++j) require(docs[j] != docs[i], HR_EINVAL, "duplicate doc in a put batch");
+  }
+  // items headed for the host only (not in the HBM arena) are quantised into scratch first
+  uint32_t n_host = 0;
+  for (uint32_t i = 0; i < 2 * n; ++i) n_host += tier[2 * docs[i / 2] + i % 2] != HR_T_HBM;
+  if (n_host > scratch_items) {
+    if (scratch) {  // a previous put may still be writing it
+      HR_CUDA(cudaStreamSynchronize(st));
+      cudaFree(scratch);
+      scratch = nullptr;
+    }
+    HR_CUDA(cudaMalloc(&scratch, (size_t)n_host * max_item));
+    scratch_items = n_host;
+  }
+  QuantParams q[2 * kPutBatch]{};
+  uint8_t* dsts[2 * kPutBatch];
+  uint32_t h = 0;
+  for (uint32_t i = 0; i < 2 * n; ++i) {
+    const uint32_t kind = i % 2, item = 2 * docs[i / 2] + kind;
     const uint32_t s = scheme[item];
-    uint8_t* dst = tier[item] == HR_T_HBM ? hbm_ptr(item) : scratch + kind * max_item;
-    dsts[kind] = dst;
-    QuantParams& qk = q[kind];
-    qk.src = (const uint16_t*)(kind ? v_src : k_src);
+    uint8_t* dst = tier[item] == HR_T_HBM ? hbm_ptr(item) : scratch + (size_t)(h++) * max_item;
+    dsts[i] = dst;
+    QuantParams& qk = q[i];
+    qk.src = (const uint16_t*)(kind ? v_srcs[i / 2] : k_srcs[i / 2]);
     qk.dst = dst;
     qk.L = lay.L, qk.H = lay.H, qk.Hl = lay.Hl, qk.h0 = lay.h0, qk.T = lay.T, qk.D = lay.D, qk.G = lay.G;
     qk.gse_e = lay.gse_e, qk.gse_m = lay.gse_m, qk.dtype = lay.dtype, qk.scheme = s;
@@ -283,7 +306,7 @@ void Store::build_put(uint32_t doc, const void* k_src, const void* v_src, cudaSt
     qk.meta_offset = lay.meta_offset(s);
     qk.meta_stride = lay.meta_stride(s);
     qk.err = err_flag;
-    qk.gse_range = gse_range + kind * 2 * lay.n_slabs();
+    qk.gse_range = gse_range + (size_t)i * 2 * lay.n_slabs();
     // zero the padding (the kernels write codes and meta records only) so exported blobs are deterministic
     const uint64_t cend = lay.n_slabs() * qk.code_bytes_slab;
     const uint64_t mend = qk.meta_offset + lay.n_slabs() * qk.meta_stride;
@@ -294,10 +317,10 @@ void Store::build_put(uint32_t doc, const void* k_src, const void* v_src, cudaSt
       if (bytes[item] > mend) HR_CUDA(cudaMemsetAsync(dst + mend, 0, bytes[item] - mend, st));
     }
   }
-  launch_quantize(q, 2, st);
-  for (uint32_t kind = 0; kind < 2; ++kind) {
-    const uint32_t item = 2 * doc + kind;
-    uint8_t* dst = dsts[kind];
+  launch_quantize(q, (int)(2 * n), st);
+  for (uint32_t i = 0; i < 2 * n; ++i) {
+    const uint32_t item = 2 * docs[i / 2] + i % 2;
+    uint8_t* dst = dsts[i];
     if (loc[item].backing_off != FreeList::kNone && !backing_filled.count(loc[item].backing_off)) {
       // bench aliasing: a shared blob is written once (its docs have identical sources by contract)
       HR_CUDA(cudaMemcpyAsync(backing_base + loc[item].backing_off, dst, bytes[item], cudaMemcpyDeviceToHost, st));
@@ -306,8 +329,10 @@ void Store::build_put(uint32_t doc, const void* k_src, const void* v_src, cudaSt
     if (loc[item].pin_off != FreeList::kNone)
       HR_CUDA(cudaMemcpyAsync(pin_base + loc[item].pin_off, dst, bytes[item], cudaMemcpyDeviceToHost, st));
   }
-  if (!put_done[doc]) ++n_put;
-  put_done[doc] = 1;
+  for (uint32_t i = 0; i < n; ++i) {
+    if (!put_done[docs[i]]) ++n_put;
+    put_done[docs[i]] = 1;
+  }
 }
 
 void Store::build_end(cudaStream_t st) {
@@ -319,19 +344,30 @@ void Store::build_end(cudaStream_t st) {
   require(err == 0, HR_EINVAL, "NaN/Inf in the source chunks (rejected at ingestion, S:30)");
   cudaFree(scratch);
   scratch = nullptr;
+  scratch_items = 0;
   state = State::Built;
 }
 
 void Store::build_with_source(uint32_t nd, const uint64_t* hot, hr_src_fn src, void* user, cudaStream_t st) {
   require(src != nullptr, HR_EINVAL, "source callback is NULL");
   build_begin(nd, hot);
+  // kSrcBatch docs per quantize launch: the source callback fills one buffer pair per doc
   const uint64_t full = 2ull * lay.L * lay.H * lay.T * lay.D;
-  HR_CUDA(cudaMalloc(&src_k, full));
-  HR_CUDA(cudaMalloc(&src_v, full));
-  for (uint32_t d = 0; d < nd; ++d) {
-    const int rc = src(user, d, src_k, src_v, (void*)st);
-    require(rc == HR_OK, (hr_status)rc, "source callback failed for doc " + std::to_string(d));
-    build_put(d, src_k, src_v, st);
+  const uint32_t nb = std::max<uint32_t>(1, std::min<uint32_t>(kSrcBatch, nd));
+  HR_CUDA(cudaMalloc(&src_k, full * nb));
+  HR_CUDA(cudaMalloc(&src_v, full * nb));
+  uint32_t docs[kPutBatch];
+  const void *ks[kPutBatch], *vs[kPutBatch];
+  for (uint32_t d0 = 0; d0 < nd; d0 += nb) {
+    const uint32_t n = std::min(nb, nd - d0);
+    for (uint32_t i = 0; i < n; ++i) {
+      docs[i] = d0 + i;
+      ks[i] = (uint8_t*)src_k + full * i;
+      vs[i] = (uint8_t*)src_v + full * i;
+      const int rc = src(user, docs[i], (void*)ks[i], (void*)vs[i], (void*)st);
+      require(rc == HR_OK, (hr_status)rc, "source callback failed for doc " + std::to_string(docs[i]));
+    }
+    build_put_batch(n, docs, ks, vs, st);
   }
   build_end(st);
   cudaFree(src_k);
@@ -1016,6 +1052,7 @@ void Store::build_from_file(const char* path, cudaStream_t st) {
   n_put = n_docs;
   cudaFree(scratch);
   scratch = nullptr;
+  scratch_items = 0;
   state = State::Built;
 }
 

@@ -79,6 +79,8 @@ struct Store {
   void read_disk(uint32_t item, uint8_t* dst);
   std::vector<uint64_t> file_offsets(uint64_t data_offset) const;
   void build_put(uint32_t doc, const void* k_src, const void* v_src, cudaStream_t st);
+  void build_put_batch(uint32_t n, const uint32_t* docs, const void* const* k_srcs, const void* const* v_srcs,
+                       cudaStream_t st);
   void build_end(cudaStream_t st);
   void build_with_source(uint32_t n_docs, const uint64_t* hotness, hr_src_fn src, void* user, cudaStream_t st);
   void assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* const* k_out, void* const* v_out,
@@ -137,6 +139,9 @@ struct Store {
   int64_t* delta = nullptr;  // device int64[n_items] hotness delta (a1)
   int* err_flag = nullptr;
   uint8_t* scratch = nullptr;  // build: quantised blobs headed for the host
+  uint32_t scratch_items = 0;  // capacity of scratch in items of max_item bytes
+  static constexpr uint32_t kPutBatch = 16;  // docs per hr_build_put_batch call (one quantize launch)
+  static constexpr uint32_t kSrcBatch = 4;   // docs per launch in hr_build_store (source buffers: 4 x K+V)
   int* gse_range = nullptr;    // build: GSE-8 per-slab exponent range scratch
   void* src_k = nullptr;
   void* src_v = nullptr;

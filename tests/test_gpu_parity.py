@@ -288,6 +288,47 @@ def test_validation_before_any_write(torch_cuda):
         st2.assemble(np.array([[0]]), ko[:1], vo[:1])
 
 
+def test_put_batch_mixed_tiers_and_validation(torch_cuda):
+    """hr_build_put_batch: docs in any order, items of every scheme of the
+    north-star ladder and of all tiers (HBM arena, pinned tier, host backing)
+    quantised in one launch; blobs equal the oracle's.  Bad batches (repeated
+    doc, unknown doc, > 16 docs) fail before any launch."""
+    import paper_2510_20878_b200 as hr
+    torch = torch_cuda
+    L, H, T, D, n_docs = 2, 2, 64, 64, 12
+    prof = synth.gen_requests(n_docs, 4 * n_docs, 4, 1.1, seed=7)
+    h = hotness.count_requests(prof, n_docs).astype(np.uint64)
+    lay = ost.Layout(L=L, H=H, T=T, D=D, dtype="fp16")
+    schemes = hotness.assign_schemes(h.tolist(), [NAMES[x] for x in NORTH], (0.25, 0.25))
+    sizes = [lay.item_bytes(x) for x in schemes]
+    order = hotness.rank_items(h)
+    st = hr.Store(L=L, H=H, D=D, T=T, dtype="fp16", ladder=NORTH, taus=(0.25, 0.25),
+                  hbm_budget=sum(sizes[i] for i in order[:6]), pin_budget=sum(sizes[i] for i in order[6:10]))
+    src = [(torch.from_numpy(synth.gen_item(L, H, T, D, d, 0, dtype="fp16").view(np.int16).reshape(-1).copy()).cuda(),
+            torch.from_numpy(synth.gen_item(L, H, T, D, d, 1, dtype="fp16").view(np.int16).reshape(-1).copy()).cuda())
+           for d in range(n_docs)]
+    st.build_begin(n_docs, h)
+    with pytest.raises(hr.HaragError, match="EINVAL"):
+        st.build_put_batch([1, 1], [src[1][0]] * 2, [src[1][1]] * 2)
+    with pytest.raises(hr.HaragError, match="ENOTFOUND"):
+        st.build_put_batch([0, n_docs], [src[0][0]] * 2, [src[0][1]] * 2)
+    with pytest.raises(hr.HaragError, match="EINVAL"):
+        st.build_put_batch(list(range(17)), [src[0][0]] * 17, [src[0][1]] * 17)
+    perm = [7, 3, 11, 0, 5, 9, 1]
+    st.build_put_batch(perm, [src[d][0] for d in perm], [src[d][1] for d in perm])
+    rest = [d for d in range(n_docs) if d not in perm]
+    st.build_put_batch(rest, [src[d][0] for d in rest], [src[d][1] for d in rest])
+    st.build_end()
+    ora = ost.OracleStore(lay, [NAMES[x] for x in NORTH], (0.25, 0.25))
+    ora.build(n_docs, h, lambda d, k: synth.gen_item(L, H, T, D, d, k, dtype="fp16"))
+    tiers = set()
+    for item in range(2 * n_docs):
+        s_, tier, _ = st.item_info(item)
+        tiers.add(tier)
+        assert np.array_equal(st.export_item(item), ora.blobs[item]), item
+    assert len(tiers) == 3
+
+
 # ------------------------------------------------- demand mode (paper-literal Alg. 2)
 @pytest.mark.parametrize("backing_pinned", [False, True])
 def test_demand_mode_matches_oracle_alg2(torch_cuda, backing_pinned):
