@@ -808,6 +808,92 @@ def run_analysis(args, wl):
         print(json.dumps(line), flush=True)
 
 
+def run_attend(args, wl):
+    """Consumer prefill: attention of each request's question rows over its k
+    retrieved chunks, (a) fused — hr_attend decodes the packed codes inside a tcgen05 attention
+    kernel, no 2 B/element KV is materialised — and (b) unfused — hr_assemble_kv writes the bf16 KV,
+    then torch SDPA (library flash/cuDNN attention) reads it.  C2 shape, paper ladder, HBM-resident
+    store; GQA g = 4 (Llama-3-8B: 32 query heads over 8 KV heads), n_q question tokens per request."""
+    import paper_2510_20878_b200 as hr
+    import synth
+    ctx = Ctx(args)
+    torch = ctx.torch
+    wl = dict(wl, n_docs=env_int("HARAG_ATT_DOCS", 200))
+    L, H, D, T, k = wl["L"], wl["H"], wl["D"], wl["T"], wl["k"]
+    Hl, g = H // ctx.world, 4
+    n_q = env_int("HARAG_ATT_NQ", 32)
+    B = env_int("HARAG_ATT_BATCH", 8)
+    reps = max(3, args.steps)
+    st, h, schemes, build_s, total = build_store(ctx, wl)
+    reqs = synth.gen_requests(wl["n_docs"], B, k, wl["s"], seed=3).astype(np.uint32)
+    HQ, M = Hl * g, g * n_q
+    q = torch.from_numpy(synth.gen_query(B, L, HQ, n_q, D, dtype=wl["dtype"]).view(np.int16)).cuda()
+    o = torch.empty_like(q)
+    lse = torch.empty((B, L, HQ, n_q), dtype=torch.float32, device="cuda")
+    # algorithmic traffic: every retrieved item's packed blob once, Q read, O + LSE written
+    code_bytes = sum(st.item_info(2 * int(d) + kind)[2] for req in reqs for d in req for kind in (0, 1))
+    io_bytes = 2 * q.numel() * 2 + lse.numel() * 4
+    flops = 4.0 * B * L * Hl * M * (k * T) * D
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+
+    def timed(fn):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        ev[0].record(ctx.stream)
+        for _ in range(reps):
+            fn()
+        ev[1].record(ctx.stream)
+        ev[1].synchronize()
+        return ev[0].elapsed_time(ev[1]) / reps
+
+    fused_ms = timed(lambda: st.attend(reqs, q, o, n_q, g, lse=lse))
+    # unfused: materialise the KV (hr_assemble_kv), then library attention over it
+    kvb = st.kv_bytes(k)
+    ko = [torch.empty(kvb // 2, dtype=torch.bfloat16, device="cuda") for _ in range(B)]
+    vo = [torch.empty(kvb // 2, dtype=torch.bfloat16, device="cuda") for _ in range(B)]
+    qf = q.view(torch.bfloat16).view(B, L, Hl, g * n_q, D)
+    o2 = torch.empty_like(qf)
+
+    def unfused():
+        st.assemble(reqs, ko, vo)
+        for r in range(B):
+            K = ko[r].view(L, Hl, k * T, D)
+            V = vo[r].view(L, Hl, k * T, D)
+            o2[r] = torch.nn.functional.scaled_dot_product_attention(qf[r], K, V)
+    unf_ms = timed(unfused)
+    st.attend(reqs, q, o, n_q, g)
+    unfused()
+    torch.cuda.synchronize()
+    diff = (o.view(torch.bfloat16).view(B, L, Hl, g * n_q, D).float() - o2.float()).abs().max().item()
+    hbm_peak, _ = measured_hbm_peak()
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            tc_peak = float(json.load(f)["bf16_tflops"])
+        tc_src = "MEASURED_PEAKS.json bf16_tflops (cuBLAS 8192^3, burst)"
+    except (OSError, KeyError, ValueError):
+        tc_peak, tc_src = 2250.0, "nominal dense bf16"
+    t_hbm = (code_bytes + io_bytes) / (hbm_peak * 1e9) * 1e3
+    t_tc = flops / (tc_peak * 1e12) * 1e3
+    bound = "tensor" if t_tc > t_hbm else "hbm"
+    line = {"attend": {
+        "workload": f"Llama-3-8B KV shape, {wl['n_docs']}-doc HBM-resident store, paper ladder, batch {B} requests x "
+                    f"k={k} x {T}-token chunks, {n_q} question tokens, GQA g={g} (M = {M} query rows per KV head)",
+        "fused_ms": round(fused_ms, 4), "unfused_ms": round(unf_ms, 4),
+        "speedup_fused_vs_unfused": round(unf_ms / fused_ms, 3),
+        "fused_TFLOPs": round(flops / (fused_ms / 1e3) / 1e12, 1),
+        "fused_code_GBps": round((code_bytes + io_bytes) / (fused_ms / 1e3) / 1e9, 1),
+        "roofline": {"bound": bound, "t_hbm_ms": round(t_hbm, 4), "t_tensor_ms": round(t_tc, 4),
+                     "frac": round(max(t_hbm, t_tc) / fused_ms, 4), "hbm_peak_GBps": hbm_peak,
+                     "tensor_peak_TFLOPs": tc_peak, "tensor_peak_source": tc_src},
+        "flops_per_batch": flops, "code_bytes_per_batch": code_bytes,
+        "max_abs_diff_fused_vs_unfused": diff,
+        "unfused_path": "hr_assemble_kv (bf16 KV in HBM) + torch.nn.functional.scaled_dot_product_attention"}}
+    st.close()
+    if ctx.rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def run_disk_leg(args, wl):
     """The DISK tier: a 500-doc store saved to disk, reloaded with disk_backing, a
     small HBM hot set; every miss is read from the file (O_DIRECT pieces) -> pinned bounce -> HBM."""
@@ -878,6 +964,7 @@ def main():
     ap.add_argument("--disk-leg", action="store_true", help="run the DISK-tier leg (save, reload disk-backed) instead")
     ap.add_argument("--tau-sweep", action="store_true", help="run the threshold sweeps of P:401-418 instead")
     ap.add_argument("--drift", action="store_true", help="run BASELINE config 5 (hotness drift) instead")
+    ap.add_argument("--attend", action="store_true", help="run the fused packed-code attention leg instead")
     ap.add_argument("--analysis", action="store_true", help="run the exponent / RMSE analysis leg instead")
     ap.add_argument("--ncu-traffic", type=float, default=None,
                     help="dram read+write bytes per launch from an ncu --set full capture (profiles/)")
@@ -899,6 +986,8 @@ def main():
         run_drift(args, wl)
     elif args.analysis:
         run_analysis(args, wl)
+    elif args.attend:
+        run_attend(args, wl)
     else:
         run_ours(args, wl)
 

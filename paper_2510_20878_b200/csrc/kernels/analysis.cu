@@ -27,11 +27,13 @@ __device__ __forceinline__ uint32_t exp_field(uint32_t bits16) {
 }
 
 // Lane-private 16-bit counters, two bins per word: word w = bin / 2 of lane L lives at
-// cnt[w * 32 + (L ^ (w & 31))] — no atomics (each lane owns its column) and, because the column
-// is XOR-swizzled by the row, lanes counting the same bin hit 32 different banks.
+// cnt[w * 32 + (L ^ (w & 31))] — no inter-lane conflicts (each lane owns its column) and, because
+// the column is XOR-swizzled by the row, lanes counting the same bin hit 32 different banks.  The
+// increment is a shared-memory reduction (no return value), so consecutive values of one lane that
+// land in the same bin do not form a load -> add -> store dependency chain.
 __device__ __forceinline__ void hist_add(uint32_t* cnt, uint32_t lane, uint32_t bin) {
   const uint32_t w = bin >> 1;
-  cnt[w * 32 + (lane ^ (w & 31))] += 1u << ((bin & 1) * 16);
+  atomicAdd(&cnt[w * 32 + (lane ^ (w & 31))], 1u << ((bin & 1) * 16));
 }
 
 // Sum the warp's lane counters into the block histogram and clear them: lane i reads rows i,
