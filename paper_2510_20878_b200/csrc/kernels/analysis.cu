@@ -17,7 +17,7 @@ namespace {
 
 constexpr int kHistThreads = 256;
 constexpr int kHistWarps = kHistThreads / 32;
-constexpr int kHistBatch = 8;        // 16-byte loads in flight per lane
+constexpr int kHistBatch = 16;       // 16-byte loads in flight per lane (256 B: 64 KB per SM)
 constexpr uint32_t kFlushVecs = 8000;  // 16-bit lane counters: flush before 65535 (8 elements per vector)
 
 // Biased exponent field of a 16-bit float: bf16 bits 14..7 (8 bits), fp16 bits 14..10 (5 bits).
