@@ -30,7 +30,6 @@
 namespace harag {
 namespace {
 
-constexpr int kAttThreads = 128;  // 4 warps: thread t owns query row t (TMEM lane t)
 constexpr int kKT = 64;           // keys per tile
 constexpr int kRows = 128;        // MMA M
 
@@ -117,40 +116,58 @@ template <int DT>
 __device__ __forceinline__ float hi_f(uint32_t w) {
   return DT == HR_BF16 ? __uint_as_float(w & 0xFFFF0000u) : __half2float(__ushort_as_half((unsigned short)(w >> 16)));
 }
-__device__ __forceinline__ float s8f(uint32_t w, int byte) { return (float)(int8_t)(w >> (8 * byte)); }
-__device__ __forceinline__ float u8f(uint32_t w, int byte) { return (float)(uint8_t)(w >> (8 * byte)); }
 
-// Decode the 8 elements [e, e+8) of one slab — the decode rules of hr_assemble_kv (R3-R5, R9) bit for bit.
+constexpr int kSoftWarps = 4, kDecWarps = 4, kDecGroups = 2;
+constexpr int kAttThreads2 = 32 * (kSoftWarps + kDecGroups * kDecWarps + 1);
+constexpr uint32_t kDecChunks = kKT * 128 / 8 / (32 * kDecWarps);  // 8-element chunks per decoder thread at D = 128
+// per decoder group: codes slots [K, V][kDecChunks][thread] x 16 B, meta slots x 8 B
+constexpr uint32_t kStageBytes = 2 * kDecChunks * 32 * kDecWarps * (16 + 8);
+
+// The four bytes of w as exact floats (minus `bias`): 0x4B0000bb is 2^23 + bb, so one PRMT and one
+// (packed) subtraction replace an I2F per element.  bias 2^23 for unsigned bytes; 2^23 + 128 for
+// two's-complement bytes pre-XORed with 0x80.
+__device__ __forceinline__ void bytes_to_f2(uint32_t w, float bias, float2& a, float2& b) {
+  const float2 nb = make_float2(-bias, -bias);
+  a = __fadd2_rn(make_float2(__uint_as_float(__byte_perm(w, 0x4B000000u, 0x7650)), __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7651))), nb);
+  b = __fadd2_rn(make_float2(__uint_as_float(__byte_perm(w, 0x4B000000u, 0x7652)), __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7653))), nb);
+}
+
+// Decode phase: the rules of decode8 / hr_assemble_kv (R3-R5, R9) from loaded codes and meta.
 template <int DT>
-__device__ __forceinline__ uint4 decode8(uint32_t scheme, const uint8_t* codes, const uint8_t* meta, uint32_t e,
-                                         uint32_t g_shift, uint32_t gse_m, const float* gtab) {
+__device__ __forceinline__ uint4 dec_raw8(uint32_t scheme, const uint4& c, const float2& m, uint32_t gse_m,
+                                          const float* gtab) {
   switch (scheme) {
     case HR_S_PASS16:
-      return __ldg(reinterpret_cast<const uint4*>(codes + 2ull * e));
-    case HR_S_INT8: {
-      const uint2 c = __ldg(reinterpret_cast<const uint2*>(codes + e));
-      const float s = __ldg(reinterpret_cast<const float*>(meta) + (e >> g_shift));
-      return make_uint4(pack2<DT>(__fmul_rn(s8f(c.x, 0), s), __fmul_rn(s8f(c.x, 1), s)),
-                        pack2<DT>(__fmul_rn(s8f(c.x, 2), s), __fmul_rn(s8f(c.x, 3), s)),
-                        pack2<DT>(__fmul_rn(s8f(c.y, 0), s), __fmul_rn(s8f(c.y, 1), s)),
-                        pack2<DT>(__fmul_rn(s8f(c.y, 2), s), __fmul_rn(s8f(c.y, 3), s)));
-    }
-    case HR_S_INT4: {
-      const uint32_t c = __ldg(reinterpret_cast<const uint32_t*>(codes + e / 2));
-      const uint32_t lo = c & 0x0F0F0F0Fu, hi = (c >> 4) & 0x0F0F0F0Fu;
-      const float2 q = __ldg(reinterpret_cast<const float2*>(meta) + (e >> g_shift));
-      float f[8];
+      return c;
+    case HR_S_INT8: {  // q = byte ^ 0x80 - 128 exactly (magic-number conversion, no I2F), then fl(q * s)
+      const float2 s2 = make_float2(m.x, m.x);
+      float2 q[4];
+      bytes_to_f2(c.x ^ 0x80808080u, 8388736.f, q[0], q[1]);
+      bytes_to_f2(c.y ^ 0x80808080u, 8388736.f, q[2], q[3]);
+      uint32_t o[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        f[2 * i] = __fadd_rn(__fmul_rn(u8f(lo, i), q.x), q.y);
-        f[2 * i + 1] = __fadd_rn(__fmul_rn(u8f(hi, i), q.x), q.y);
+        const float2 f = __fmul2_rn(q[i], s2);
+        o[i] = pack2<DT>(f.x, f.y);
       }
-      return make_uint4(pack2<DT>(f[0], f[1]), pack2<DT>(f[2], f[3]), pack2<DT>(f[4], f[5]), pack2<DT>(f[6], f[7]));
+      return make_uint4(o[0], o[1], o[2], o[3]);
+    }
+    case HR_S_INT4: {  // fl(fl(q * s) + mn), q the nibble (element 2i = low nibble of byte i); scalar _rn
+      // operations: the product must be rounded before the add (no FMA contraction, R4)
+      const uint32_t lo = c.x & 0x0F0F0F0Fu, hi = (c.x >> 4) & 0x0F0F0F0Fu;
+      const uint32_t ev01 = __byte_perm(lo, hi, 0x5140), ev23 = __byte_perm(lo, hi, 0x7362);  // e0 e1 e2 e3 | e4..e7
+      float2 q[4];
+      bytes_to_f2(ev01, 8388608.f, q[0], q[1]);
+      bytes_to_f2(ev23, 8388608.f, q[2], q[3]);
+      uint32_t o[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        o[i] = pack2<DT>(__fadd_rn(__fmul_rn(q[i].x, m.x), m.y), __fadd_rn(__fmul_rn(q[i].y, m.x), m.y));
+      return make_uint4(o[0], o[1], o[2], o[3]);
     }
     case HR_S_FP8E4M3:
     case HR_S_FP8E5M2: {
       const __nv_fp8_interpretation_t it = scheme == HR_S_FP8E4M3 ? __NV_E4M3 : __NV_E5M2;
-      const uint2 c = __ldg(reinterpret_cast<const uint2*>(codes + e));
       const uint32_t w[4] = {c.x & 0xFFFFu, c.x >> 16, c.y & 0xFFFFu, c.y >> 16};
       uint32_t o[4];
 #pragma unroll
@@ -166,46 +183,138 @@ __device__ __forceinline__ uint4 decode8(uint32_t scheme, const uint8_t* codes, 
       return make_uint4(o[0], o[1], o[2], o[3]);
     }
     default: {  // GSE-8: +-f * 2^(G_idx - (m-1)) from the slab's fp32 table (staged in shared memory)
-      const uint2 c = __ldg(reinterpret_cast<const uint2*>(codes + e));
-      const uint32_t fm = (1u << gse_m) - 1u;
-      float f[8];
+      const uint32_t fm = ((1u << gse_m) - 1u) * 0x01010101u;
+      float2 q[4];
+      bytes_to_f2(c.x & fm, 8388608.f, q[0], q[1]);  // the fields f, exact
+      bytes_to_f2(c.y & fm, 8388608.f, q[2], q[3]);
+      float t[8];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const uint32_t b = ((i < 4 ? c.x : c.y) >> (8 * (i & 3))) & 0xFFu;
-        f[i] = __fmaf_rn((float)(b & fm), gtab[b >> gse_m], 0.f);
+      for (int i = 0; i < 8; ++i) t[i] = gtab[(((i < 4 ? c.x : c.y) >> (8 * (i & 3))) & 0xFFu) >> gse_m];
+      uint32_t o[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {  // fma(f, T, +0): the exact product; a (sign 1, field 0) byte gives +0
+        const float2 f = __ffma2_rn(q[i], make_float2(t[2 * i], t[2 * i + 1]), make_float2(0.f, 0.f));
+        o[i] = pack2<DT>(f.x, f.y);
       }
-      return make_uint4(pack2<DT>(f[0], f[1]), pack2<DT>(f[2], f[3]), pack2<DT>(f[4], f[5]), pack2<DT>(f[6], f[7]));
+      return make_uint4(o[0], o[1], o[2], o[3]);
     }
   }
 }
 
-struct AttSmem {
-  uint8_t* q;  // [128 rows][D] K-major core layout: (dc * 16 + row / 8) * 128 + (row % 8) * 16
-  uint8_t* k;  // [64 keys][D]  K-major (B of S = Q K^T)
-  uint8_t* v;  // [64 keys][D]  MN-major (B of O += P V): (key / 8 * (D / 8) + dc) * 128 + (key % 8) * 16
-  uint8_t* p;  // [128 rows][64 keys] K-major (A of O += P V)
-  float* gtab; // [2][32] GSE decode tables of the current K and V slab
-  uint64_t* bar;  // [2]: S done, O done
-  uint32_t* tmem; // TMEM base written by tcgen05.alloc
-};
-
-size_t att_smem_bytes(uint32_t D) {
-  return (size_t)kRows * D * 2 + 2 * (size_t)kKT * D * 2 + (size_t)kRows * kKT * 2 + 2 * 32 * 4 + 2 * 8 + 16;
+// Decode one operand tile (this decoder thread's kDecChunks chunks of 8 elements) with the scheme
+// resolved ONCE per tile: a runtime switch over compile-time-specialised loops (a per-chunk switch
+// made the decode loop branch-bound).  VMAJ: V's MN-major layout, else K's K-major layout.
+template <int DT, int SCH, bool VMAJ, uint32_t D>
+__device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, const uint8_t* __restrict__ stm,
+                                           const float* __restrict__ gt, uint32_t gse_m, uint8_t* __restrict__ dst,
+                                           uint32_t dt, uint16_t* __restrict__ dump) {
+  constexpr uint32_t dcs = D / 8, nch = kKT * dcs / (32 * kDecWarps);
+#pragma unroll
+  for (uint32_t i = 0; i < nch; ++i) {
+    const uint32_t cc = dt + i * 32 * kDecWarps;
+    {
+      const uint32_t gI = cc >> 5, ii = cc & 7, jj = (cc >> 3) & 3;
+      const uint32_t key = (gI % (kKT / 8)) * 8 + ii, dc = (gI / (kKT / 8)) * 4 + jj;
+      const uint4 raw = *reinterpret_cast<const uint4*>(stc + (i * 32 * kDecWarps + dt) * 16);
+      const float2 m = *reinterpret_cast<const float2*>(stm + (i * 32 * kDecWarps + dt) * 8);
+      const uint4 v = dec_raw8<DT>(SCH, raw, m, gse_m, gt);
+      if (VMAJ)
+        *reinterpret_cast<uint4*>(dst + ((key / 8) * dcs + dc) * 128 + (key % 8) * 16) = v;
+      else
+        *reinterpret_cast<uint4*>(dst + (dc * (kKT / 8) + key / 8) * 128 + (key % 8) * 16) = v;
+      if (dump) *reinterpret_cast<uint4*>(dump + key * D + dc * 8) = v;
+    }
+  }
+}
+template <int DT, bool VMAJ, uint32_t D>
+__device__ __forceinline__ void dec_tile(uint32_t scheme, const uint8_t* stc, const uint8_t* stm, const float* gt,
+                                         uint32_t gse_m, uint8_t* dst, uint32_t dt, uint16_t* dump) {
+  switch (scheme) {
+    case HR_S_PASS16: return dec_tile_s<DT, HR_S_PASS16, VMAJ, D>(stc, stm, gt, gse_m, dst, dt, dump);
+    case HR_S_INT8: return dec_tile_s<DT, HR_S_INT8, VMAJ, D>(stc, stm, gt, gse_m, dst, dt, dump);
+    case HR_S_FP8E4M3: return dec_tile_s<DT, HR_S_FP8E4M3, VMAJ, D>(stc, stm, gt, gse_m, dst, dt, dump);
+    case HR_S_FP8E5M2: return dec_tile_s<DT, HR_S_FP8E5M2, VMAJ, D>(stc, stm, gt, gse_m, dst, dt, dump);
+    case HR_S_INT4: return dec_tile_s<DT, HR_S_INT4, VMAJ, D>(stc, stm, gt, gse_m, dst, dt, dump);
+    default: return dec_tile_s<DT, HR_S_GSE8, VMAJ, D>(stc, stm, gt, gse_m, dst, dt, dump);
+  }
 }
 
-template <int DT>
-__global__ void __launch_bounds__(kAttThreads) attend_kernel(AttnParams p) {
+// cp.async (LDGSTS) of one chunk's codes / group meta into this thread's staging slot: the loads of a
+// whole tile are in flight at once without holding registers
+template <int N>
+__device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(saddr(smem)), "l"(gmem), "n"(N) : "memory");
+}
+__device__ __forceinline__ void stage_chunk(uint32_t scheme, const uint8_t* codes, const uint8_t* meta, uint32_t e,
+                                            uint32_t g_shift, uint8_t* sc, uint8_t* sm) {
+  if (scheme == HR_S_PASS16) {
+    cp_async<16>(sc, codes + 2ull * e);
+  } else if (scheme == HR_S_INT4) {
+    cp_async<4>(sc, codes + e / 2);
+    cp_async<8>(sm, meta + 8ull * (e >> g_shift));
+  } else {
+    cp_async<8>(sc, codes + e);
+    if (scheme == HR_S_INT8) cp_async<4>(sm, meta + 4ull * (e >> g_shift));
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// Warp-specialised pipeline, one CTA per (request, layer, KV head) unit:
+//   warps 0-3  softmax: thread t owns query row t (TMEM lane t); loads Q; online softmax of S_j,
+//              lazy O rescale, P_j -> shared memory; epilogue O / l and LSE
+//   warps 4-11 decoders, two groups of 4: group b decodes the tiles j with j&1 == b into operand
+//              buffer b — tile j's K and V codes (L2-prefetched kPF tiles ahead; all of a thread's
+//              loads in flight before it decodes) -> bf16/fp16 operand tiles in shared memory, the
+//              assemble decode bit for bit; two groups so decode latency overlaps across tiles
+//   warp 12    MMA issuer (one lane): S_j = Q K_j^T into TMEM buffer j&1, then O += P_{j-1} V_{j-1}
+// so the tensor core computes S_{j+1} while the softmax warps work on S_j and the decoders fill
+// tile j+2.  mbarriers: sf (S ready), pf (P ready), kvf (operands ready), kve (operands and P free:
+// committed after PV), od (PV done, for the lazy rescale and the epilogue), qf (Q ready).
+constexpr uint32_t kPF = 4;  // L2 prefetch distance in tiles
+
+size_t att_smem_bytes(uint32_t D) {
+  return (size_t)kRows * D * 2 + 4 * (size_t)kKT * D * 2 + 2 * (size_t)kRows * kKT * 2 + 4 * 32 * 4 + 16 * 8 + 16 +
+         kDecGroups * kStageBytes;
+}
+
+// 2^x on the SFU (MUFU.EX2, relative error ~2^-22, far inside R28's 2^-9 budget)
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void named_bar(uint32_t id, uint32_t n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive1(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(bar)) : "memory");
+}
+__device__ __forceinline__ uint32_t code_bytes_of(uint32_t scheme, uint32_t n_el) {
+  return scheme == HR_S_PASS16 ? 2 * n_el : scheme == HR_S_INT4 ? n_el / 2 : n_el;
+}
+
+#ifdef HARAG_ATT_TRACE
+__device__ long long g_tr[9][96];  // per-tile event clocks of CTA 0 (pipeline study builds only)
+#define TR(ev, j) do { if (blockIdx.x == 0 && (j) < 96) g_tr[ev][j] = clock64(); } while (0)
+#else
+#define TR(ev, j) do { } while (0)
+#endif
+
+template <int DT, uint32_t D>
+__global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_constant__ AttnParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  const uint32_t D = p.D;
-  AttSmem sm;
-  sm.q = smem_raw;
-  sm.k = sm.q + kRows * D * 2;
-  sm.v = sm.k + kKT * D * 2;
-  sm.p = sm.v + kKT * D * 2;
-  sm.gtab = reinterpret_cast<float*>(sm.p + kRows * kKT * 2);
-  sm.bar = reinterpret_cast<uint64_t*>(sm.gtab + 64);
-  sm.tmem = reinterpret_cast<uint32_t*>(sm.bar + 2);
-  const int tid = threadIdx.x, warp = tid >> 5;
+  constexpr uint32_t dcs = D / 8;
+  uint8_t* sq = smem_raw;                          // [128 rows][D] K-major core layout
+  uint8_t* skb = sq + kRows * D * 2;               // 2 x [64 keys][D] K-major (B of S = Q K^T)
+  uint8_t* svb = skb + 2 * kKT * D * 2;            // 2 x [64 keys][D] MN-major (B of O += P V)
+  uint8_t* spb = svb + 2 * kKT * D * 2;            // 2 x [128 rows][64 keys] K-major (A of O += P V)
+  float* gtab = reinterpret_cast<float*>(spb + 2 * kRows * kKT * 2);  // [group][2][32] GSE tables (K, V)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(gtab + 128);
+  uint64_t *sf = bar, *pf = bar + 2, *kvf = bar + 4, *kve = bar + 6, *od = bar + 8, *qf = bar + 9;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
+  uint8_t* stage0 = reinterpret_cast<uint8_t*>(bar + 18);  // 16-B aligned decoder staging
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   const uint32_t unit = blockIdx.x;  // (request, layer, head)
   const uint32_t r = unit / (p.L * p.Hl), lh = unit - r * (p.L * p.Hl);
@@ -213,14 +322,22 @@ __global__ void __launch_bounds__(kAttThreads) attend_kernel(AttnParams p) {
   const uint32_t slab_i = l * p.Hl + h;
   const uint32_t hq = p.Hl * p.g;  // query heads on this rank
   const uint64_t row0 = (((uint64_t)r * p.L + l) * hq + (uint64_t)h * p.g) * p.n_q;  // first query row of the unit
+  const uint32_t tiles_per_doc = p.T / kKT;
+  const uint32_t n_tiles = p.k * tiles_per_doc;
 
-  if (warp == 0) {  // TMEM: S at columns [0, 64), O at [128, 128 + D)
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(saddr(sm.tmem)));
+  if (warp == 0) {  // TMEM: S buffers at columns [0, 64) and [64, 128), O at [128, 128 + D)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(saddr(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    mbar_init(&sm.bar[0], 1);
-    mbar_init(&sm.bar[1], 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&sf[b], 1);
+      mbar_init(&pf[b], kSoftWarps);
+      mbar_init(&kvf[b], kDecWarps);
+      mbar_init(&kve[b], 1);
+    }
+    mbar_init(od, 1);
+    mbar_init(qf, kSoftWarps);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (p.descs[0].count != nullptr && l == 0 && h == 0) {  // a1: hotness of this request's items
       for (uint32_t j = 0; j < 2 * p.k; ++j) {
@@ -229,155 +346,236 @@ __global__ void __launch_bounds__(kAttThreads) attend_kernel(AttnParams p) {
       }
     }
   }
-  // Q tile: rows >= M are zero.  Thread mapping per 32 chunks: 8 rows x 4 column chunks (coalesced
-  // 64-B row reads, conflict-free 16-B shared stores).
-  const uint32_t dcs = D / 8;
-  for (uint32_t c = tid; c < kRows * dcs; c += kAttThreads) {
-    const uint32_t gI = c >> 5, i = c & 7, jj = (c >> 3) & 3;
-    const uint32_t row = (gI % (kRows / 8)) * 8 + i, dc = (gI / (kRows / 8)) * 4 + jj;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (row < p.M) v = __ldg(reinterpret_cast<const uint4*>(p.q + (row0 + row) * D) + dc);
-    *reinterpret_cast<uint4*>(sm.q + (dc * (kRows / 8) + row / 8) * 128 + (row % 8) * 16) = v;
-  }
   tc_before();
   __syncthreads();
   tc_after();
-  const uint32_t tmem = *sm.tmem;
-  const uint32_t t_s = tmem, t_o = tmem + 128;
-  const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t t_o = tmem + 128;
 
-  const uint32_t fmt = DT == HR_BF16 ? 1u : 0u;
-  const uint32_t id_s = idesc(fmt, 0, 0, kKT, kRows);  // S[128 x 64] = Q[128 x D] . K[64 x D]^T
-  const uint32_t id_o = idesc(fmt, 0, 1, D, kRows);    // O[128 x D] += P[128 x 64] . V[64 x D] (V MN-major)
-  const uint32_t tiles_per_doc = p.T / kKT;
-  const uint32_t n_tiles = p.k * tiles_per_doc;
-  const float c = p.scale_log2;
-  float m_ref = -INFINITY, lsum = 0.f;
-
-  for (uint32_t j = 0; j < n_tiles; ++j) {
-    const uint32_t slot = j / tiles_per_doc, t0 = (j - slot * tiles_per_doc) * kKT;
-    const AsmDesc& dk = p.descs[((uint64_t)r * p.k + slot) * 2];
-    const AsmDesc& dv = p.descs[((uint64_t)r * p.k + slot) * 2 + 1];
-    const uint8_t* kc = dk.codes + (uint64_t)slab_i * p.code_slab[dk.scheme];
-    const uint8_t* vc = dv.codes + (uint64_t)slab_i * p.code_slab[dv.scheme];
-    const uint8_t* km = dk.meta + (uint64_t)slab_i * p.meta_stride[dk.scheme];
-    const uint8_t* vm = dv.meta + (uint64_t)slab_i * p.meta_stride[dv.scheme];
-    if (t0 == 0) {  // new doc: stage the GSE decode tables of its K and V slab
-      __syncthreads();
-      if (tid < 64) {
-        const bool isv = tid >= 32;
-        const AsmDesc& d = isv ? dv : dk;
-        const uint8_t* m = isv ? vm : km;
-        const uint32_t i = tid & 31;
-        sm.gtab[tid] = (d.scheme == HR_S_GSE8 && i < (2u << p.gse_e)) ? reinterpret_cast<const float*>(m + 16)[i] : 0.f;
-      }
-      __syncthreads();
-    }
-    // decode the K and V tiles (64 keys x D) into the operand layouts
-    for (uint32_t cc = tid; cc < kKT * dcs; cc += kAttThreads) {
-      const uint32_t gI = cc >> 5, i = cc & 7, jj = (cc >> 3) & 3;
-      const uint32_t key = (gI % (kKT / 8)) * 8 + i, dc = (gI / (kKT / 8)) * 4 + jj;
-      const uint32_t e = (t0 + key) * D + dc * 8;
-      const uint4 kv = decode8<DT>(dk.scheme, kc, km, e, p.g_shift, p.gse_m, sm.gtab);
-      const uint4 vv = decode8<DT>(dv.scheme, vc, vm, e, p.g_shift, p.gse_m, sm.gtab + 32);
-      *reinterpret_cast<uint4*>(sm.k + (dc * (kKT / 8) + key / 8) * 128 + (key % 8) * 16) = kv;
-      *reinterpret_cast<uint4*>(sm.v + ((key / 8) * dcs + dc) * 128 + (key % 8) * 16) = vv;
-      if (p.kv_dump) {  // test hook: the assembled KV [r][2][l][h][k*T][D]
-        const uint64_t base = ((((uint64_t)r * 2) * p.L + l) * p.Hl + h) * p.k * p.T * D;
-        const uint64_t kvoff = (uint64_t)p.L * p.Hl * p.k * p.T * D;
-        const uint64_t o = base + ((uint64_t)slot * p.T + t0 + key) * D + dc * 8;
-        *reinterpret_cast<uint4*>(p.kv_dump + o) = kv;
-        *reinterpret_cast<uint4*>(p.kv_dump + kvoff + o) = vv;
-      }
+  if (warp < kSoftWarps) {
+    // ------------------------------------------------------------------ softmax warps
+    // Q tile: rows >= M are zero.  Thread mapping per 32 chunks: 8 rows x 4 column chunks.
+    for (uint32_t c = tid; c < kRows * dcs; c += 32 * kSoftWarps) {
+      const uint32_t gI = c >> 5, i = c & 7, jj = (c >> 3) & 3;
+      const uint32_t row = (gI % (kRows / 8)) * 8 + i, dc = (gI / (kRows / 8)) * 4 + jj;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (row < p.M) v = __ldg(reinterpret_cast<const uint4*>(p.q + (row0 + row) * D) + dc);
+      *reinterpret_cast<uint4*>(sq + (dc * (kRows / 8) + row / 8) * 128 + (row % 8) * 16) = v;
     }
     fence_async_smem();
-    tc_before();
-    __syncthreads();
-    if (tid == 0) {
+    __syncwarp();
+    if (lane == 0) mbar_arrive1(qf);
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    const float c = p.scale_log2;
+    float m_ref = -INFINITY, lsum = 0.f;
+    for (uint32_t j = 0; j < n_tiles; ++j) {
+      const uint32_t b = j & 1;
+      mbar_wait(&sf[b], (j >> 1) & 1);
+      if (tid == 0) TR(0, j);
       tc_after();
-      const uint32_t qa = saddr(sm.q), ka = saddr(sm.k);
-      for (uint32_t s = 0; s < D / 16; ++s)  // K-major: one k-step = 2 core matrices along K
-        mma_f16(t_s, sdesc(qa + s * 2 * (kRows / 8) * 128, (kRows / 8) * 128, 128),
-                sdesc(ka + s * 2 * (kKT / 8) * 128, (kKT / 8) * 128, 128), id_s, s > 0);
-      mma_commit(&sm.bar[0]);
-    }
-    mbar_wait(&sm.bar[0], j & 1);
-    tc_after();
-    // online softmax on this thread's row
-    uint32_t sv[2][32];
-    tmem_ld32(t_s + lane_base, sv[0]);
-    tmem_ld32(t_s + lane_base + 32, sv[1]);
-    float mt = -INFINITY;
+      uint32_t sv[2][32];
+      tmem_ld32(tmem + b * kKT + lane_base, sv[0]);
+      tmem_ld32(tmem + b * kKT + 32 + lane_base, sv[1]);
+      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // independent chains (ILP)
 #pragma unroll
-    for (int a = 0; a < 2; ++a)
+      for (int a = 0; a < 2; ++a)
 #pragma unroll
-      for (int b = 0; b < 32; ++b) mt = fmaxf(mt, __uint_as_float(sv[a][b]) * c);
-    const bool grow = mt > m_ref + 8.f;  // lazy rescale: p stays <= 2^8 between rescales
-    const float m_new = grow ? mt : m_ref;
-    if (__any_sync(0xFFFFFFFFu, grow) && j > 0) {
-      const float alpha = grow ? exp2f(m_ref - m_new) : 1.f;
-      for (uint32_t cb = 0; cb < D; cb += 32) {
-        uint32_t ov[32];
-        tmem_ld32(t_o + lane_base + cb, ov);
+        for (int q = 0; q < 32; ++q) mx4[q & 3] = fmaxf(mx4[q & 3], __uint_as_float(sv[a][q]));
+      const float mt = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * c;  // c > 0: max(s) c = max(s c)
+      const bool grow = mt > m_ref + 8.f;  // lazy rescale: p stays <= 2^8 between rescales
+      if (j >= 2) mbar_wait(&kve[b], ((j >> 1) - 1) & 1);  // PV_{j-2} done: P[b] free, O at most one PV behind
+      if (__any_sync(0xFFFFFFFFu, grow) && j > 0) {
+        mbar_wait(od, (j - 1) & 1);  // PV_{j-1} done: O may be read and rewritten
+        tc_after();
+        const float alpha = grow ? ex2(m_ref - mt) : 1.f;
+        for (uint32_t cb = 0; cb < D; cb += 32) {
+          uint32_t ov[32];
+          tmem_ld32(t_o + lane_base + cb, ov);
 #pragma unroll
-        for (int b = 0; b < 32; ++b) ov[b] = __float_as_uint(__uint_as_float(ov[b]) * alpha);
-        tmem_st32(t_o + lane_base + cb, ov);
-      }
-      lsum *= alpha;
-    }
-    m_ref = m_new;
-    uint8_t* prow = sm.p + (tid / 8) * 128 + (tid % 8) * 16;
-#pragma unroll
-    for (int a = 0; a < 2; ++a) {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {  // 8 keys -> one 16-B core-matrix row
-        uint32_t w[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float p0 = exp2f(__uint_as_float(sv[a][q * 8 + 2 * u]) * c - m_ref);
-          const float p1 = exp2f(__uint_as_float(sv[a][q * 8 + 2 * u + 1]) * c - m_ref);
-          w[u] = pack2<DT>(p0, p1);
-          lsum += lo_f<DT>(w[u]) + hi_f<DT>(w[u]);  // normalise by the rounded weights actually used
+          for (int q = 0; q < 32; ++q) ov[q] = __float_as_uint(__uint_as_float(ov[q]) * alpha);
+          tmem_st32(t_o + lane_base + cb, ov);
         }
-        const uint32_t kc8 = a * 4 + q;  // key chunk
-        *reinterpret_cast<uint4*>(prow + kc8 * (kRows / 8) * 128) = make_uint4(w[0], w[1], w[2], w[3]);
+        lsum *= alpha;
+      }
+      if (grow) m_ref = mt;
+      uint8_t* prow = spb + b * (kRows * kKT * 2) + (tid / 8) * 128 + (tid % 8) * 16;
+      float ls4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {  // 8 keys -> one 16-B core-matrix row
+          uint32_t w[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const float p0 = ex2(__fmaf_rn(__uint_as_float(sv[a][q * 8 + 2 * u]), c, -m_ref));
+            const float p1 = ex2(__fmaf_rn(__uint_as_float(sv[a][q * 8 + 2 * u + 1]), c, -m_ref));
+            w[u] = pack2<DT>(p0, p1);
+            ls4[u] += lo_f<DT>(w[u]) + hi_f<DT>(w[u]);  // normalise by the rounded weights actually used
+          }
+          const uint32_t kc8 = a * 4 + q;  // key chunk
+          *reinterpret_cast<uint4*>(prow + kc8 * (kRows / 8) * 128) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+      lsum += (ls4[0] + ls4[1]) + (ls4[2] + ls4[3]);
+      fence_async_smem();
+      tc_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive1(&pf[b]);
+      if (tid == 0) TR(1, j);
+    }
+    // epilogue: O / l -> output dtype; LSE (natural log) = ln 2 * (m_ref + log2 l)
+    if (n_tiles >= 2) mbar_wait(od, (n_tiles - 2) & 1);
+    mbar_wait(od, (n_tiles - 1) & 1);
+    tc_after();
+    const float inv = 1.f / lsum;
+    for (uint32_t cb = 0; cb < D; cb += 32) {
+      uint32_t ov[32];
+      tmem_ld32(t_o + lane_base + cb, ov);
+      if ((uint32_t)tid < p.M) {
+        uint4* dst = reinterpret_cast<uint4*>(p.o + (row0 + tid) * D + cb);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t w[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            w[u] = pack2<DT>(__uint_as_float(ov[q * 8 + 2 * u]) * inv, __uint_as_float(ov[q * 8 + 2 * u + 1]) * inv);
+          dst[q] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
       }
     }
-    fence_async_smem();
-    tc_before();
-    __syncthreads();
-    if (tid == 0) {
+    if ((uint32_t)tid < p.M && p.lse) p.lse[row0 + tid] = 0.69314718055994531f * (m_ref + __log2f(lsum));
+  } else if (warp < kSoftWarps + kDecGroups * kDecWarps) {
+    // ------------------------------------------------------------------ decoder warps
+    const uint32_t grp = (uint32_t)(warp - kSoftWarps) / kDecWarps;   // tiles j with j & 1 == grp
+    const uint32_t dt = tid - 32 * kSoftWarps - 32 * kDecWarps * grp;  // 0..127 within the group
+    float* gt = gtab + 64 * grp;
+    auto tile_src = [&](uint32_t j, const AsmDesc*& dk, const AsmDesc*& dv, uint32_t& t0) {
+      const uint32_t slot = j / tiles_per_doc;
+      t0 = (j - slot * tiles_per_doc) * kKT;
+      dk = &p.descs[((uint64_t)r * p.k + slot) * 2];
+      dv = dk + 1;
+    };
+    auto prefetch = [&](uint32_t j) {
+      const AsmDesc *dk, *dv;
+      uint32_t t0;
+      tile_src(j, dk, dv, t0);
+      const uint32_t n_el = kKT * D;
+      prefetch_l2(dk->codes + (uint64_t)slab_i * p.code_slab[dk->scheme] + code_bytes_of(dk->scheme, t0 * D),
+                  code_bytes_of(dk->scheme, n_el));
+      prefetch_l2(dv->codes + (uint64_t)slab_i * p.code_slab[dv->scheme] + code_bytes_of(dv->scheme, t0 * D),
+                  code_bytes_of(dv->scheme, n_el));
+    };
+    if (dt == 0)
+      for (uint32_t j = grp; j < kPF && j < n_tiles; j += kDecGroups) prefetch(j);
+    uint32_t cur_slot = 0xFFFFFFFFu;
+    for (uint32_t j = grp; j < n_tiles; j += kDecGroups) {
+      const uint32_t b = grp, use = j >> 1;  // use-th fill of buffer b
+      const AsmDesc *dkp, *dvp;
+      uint32_t t0;
+      tile_src(j, dkp, dvp, t0);
+      const AsmDesc dk = *dkp, dv = *dvp;
+      if (dt == 0 && j + kPF < n_tiles) prefetch(j + kPF);
+      const uint8_t* kc = dk.codes + (uint64_t)slab_i * p.code_slab[dk.scheme];
+      const uint8_t* vc = dv.codes + (uint64_t)slab_i * p.code_slab[dv.scheme];
+      const uint8_t* km = dk.meta + (uint64_t)slab_i * p.meta_stride[dk.scheme];
+      const uint8_t* vm = dv.meta + (uint64_t)slab_i * p.meta_stride[dv.scheme];
+      const uint32_t slot = j / tiles_per_doc;
+      // all of this thread's loads in flight at once: cp.async into its own staging slots
+      uint8_t* stc = stage0 + grp * kStageBytes;                         // [K, V][i][dt] x 16 B
+      uint8_t* stm = stc + 2 * kDecChunks * 32 * kDecWarps * 16;          // [K, V][i][dt] x 8 B
+#pragma unroll
+      for (uint32_t i = 0; i < kKT * dcs / (32 * kDecWarps); ++i) {
+        const uint32_t cc = dt + i * 32 * kDecWarps;
+        {
+          const uint32_t gI = cc >> 5, ii = cc & 7, jj = (cc >> 3) & 3;
+          const uint32_t key = (gI % (kKT / 8)) * 8 + ii, dc = (gI / (kKT / 8)) * 4 + jj;
+          const uint32_t e = (t0 + key) * D + dc * 8;
+          const uint32_t sl = i * 32 * kDecWarps + dt;
+          stage_chunk(dk.scheme, kc, km, e, p.g_shift, stc + sl * 16, stm + sl * 8);
+          stage_chunk(dv.scheme, vc, vm, e, p.g_shift, stc + (kDecChunks * 32 * kDecWarps + sl) * 16,
+                      stm + (kDecChunks * 32 * kDecWarps + sl) * 8);
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+      if (slot != cur_slot) {  // new doc: stage the GSE decode tables of its K and V slab (this group only)
+        cur_slot = slot;
+        named_bar(1 + grp, 32 * kDecWarps);
+        if (dt < 64) {
+          const bool isv = dt >= 32;
+          const AsmDesc& d = isv ? dv : dk;
+          const uint8_t* m = isv ? vm : km;
+          const uint32_t i = dt & 31;
+          gt[dt] = (d.scheme == HR_S_GSE8 && i < (2u << p.gse_e)) ? reinterpret_cast<const float*>(m + 16)[i] : 0.f;
+        }
+        named_bar(1 + grp, 32 * kDecWarps);
+      }
+      if (dt == 0) TR(6, j);
+      if (use >= 1) mbar_wait(&kve[b], (use - 1) & 1);  // PV_{j-2} (and S_{j-2}) done: buffer b free
+      if (dt == 0) TR(2, j);
+      asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's staged chunks have landed
+      if (dt == 0) TR(7, j);
+      uint8_t* skd = skb + b * (kKT * D * 2);
+      uint8_t* svd = svb + b * (kKT * D * 2);
+      {
+        uint16_t* dump = nullptr;  // test hook: the assembled KV [r][2][l][h][k*T][D]
+        if (p.kv_dump)
+          dump = p.kv_dump + ((((uint64_t)r * 2) * p.L + l) * p.Hl + h) * p.k * p.T * D + ((uint64_t)slot * p.T + t0) * D;
+        const uint64_t kvoff = (uint64_t)p.L * p.Hl * p.k * p.T * D;
+        const uint32_t vo = kDecChunks * 32 * kDecWarps;
+        dec_tile<DT, false, D>(dk.scheme, stc, stm, gt, p.gse_m, skd, dt, dump);
+        dec_tile<DT, true, D>(dv.scheme, stc + vo * 16, stm + vo * 8, gt + 32, p.gse_m, svd, dt,
+                              dump ? dump + kvoff : nullptr);
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive1(&kvf[b]);
+      if (dt == 0) TR(3, j);
+    }
+  } else if (lane == 0) {
+    // ------------------------------------------------------------------ MMA issuer
+    const uint32_t fmt = DT == HR_BF16 ? 1u : 0u;
+    const uint32_t id_s = idesc(fmt, 0, 0, kKT, kRows);  // S[128 x 64] = Q[128 x D] . K[64 x D]^T
+    const uint32_t id_o = idesc(fmt, 0, 1, D, kRows);    // O[128 x D] += P[128 x 64] . V[64 x D] (V MN-major)
+    const uint32_t qa = saddr(sq);
+    auto pv = [&](uint32_t jj) {
+      const uint32_t bb = jj & 1;
+      mbar_wait(&pf[bb], (jj >> 1) & 1);
+      TR(5, jj);
       tc_after();
-      const uint32_t pa = saddr(sm.p), va = saddr(sm.v);
+      const uint32_t pa = saddr(spb + bb * (kRows * kKT * 2)), va = saddr(svb + bb * (kKT * D * 2));
       for (uint32_t s = 0; s < kKT / 16; ++s)
         mma_f16(t_o, sdesc(pa + s * 2 * (kRows / 8) * 128, (kRows / 8) * 128, 128),
-                sdesc(va + s * 2 * dcs * 128, dcs * 128, 128), id_o, (j > 0 || s > 0) ? 1u : 0u);
-      mma_commit(&sm.bar[1]);
+                sdesc(va + s * 2 * dcs * 128, dcs * 128, 128), id_o, (jj > 0 || s > 0) ? 1u : 0u);
+      mma_commit(&kve[bb]);
+      mma_commit(od);
+    };
+    mbar_wait(qf, 0);
+    for (uint32_t j = 0; j < n_tiles; ++j) {
+      const uint32_t b = j & 1;
+      mbar_wait(&kvf[b], (j >> 1) & 1);
+      TR(4, j);
+      tc_after();
+      const uint32_t ka = saddr(skb + b * (kKT * D * 2));
+      for (uint32_t s = 0; s < D / 16; ++s)  // K-major: one k-step = 2 core matrices along K
+        mma_f16(tmem + b * kKT, sdesc(qa + s * 2 * (kRows / 8) * 128, (kRows / 8) * 128, 128),
+                sdesc(ka + s * 2 * (kKT / 8) * 128, (kKT / 8) * 128, 128), id_s, s > 0);
+      mma_commit(&sf[b]);
+      if (j >= 1) pv(j - 1);
     }
-    mbar_wait(&sm.bar[1], j & 1);
-    tc_after();
+    if (n_tiles) pv(n_tiles - 1);
   }
-  // epilogue: O / l -> output dtype; LSE (natural log) = ln 2 * (m_ref + log2 l)
-  const float inv = 1.f / lsum;
-  for (uint32_t cb = 0; cb < D; cb += 32) {
-    uint32_t ov[32];
-    tmem_ld32(t_o + lane_base + cb, ov);
-    if ((uint32_t)tid < p.M) {
-      uint4* dst = reinterpret_cast<uint4*>(p.o + (row0 + tid) * D + cb);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint32_t w[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          w[u] = pack2<DT>(__uint_as_float(ov[q * 8 + 2 * u]) * inv, __uint_as_float(ov[q * 8 + 2 * u + 1]) * inv);
-        dst[q] = make_uint4(w[0], w[1], w[2], w[3]);
-      }
-    }
-  }
-  if ((uint32_t)tid < p.M && p.lse) p.lse[row0 + tid] = 0.69314718055994531f * (m_ref + __log2f(lsum));
   tc_before();
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+#ifdef HARAG_ATT_TRACE
+  if (blockIdx.x == 0 && tid == 0) {
+    const long long t0 = g_tr[6][0];
+    printf("tile sfwait pfarr kvewait kvfarr Sissue PVissue decstart loadsin (cycles from decode start of tile 0)\n");
+    for (uint32_t j = 0; j < n_tiles && j < 96; ++j)
+      printf("%u %lld %lld %lld %lld %lld %lld %lld %lld\n", j, g_tr[0][j] - t0, g_tr[1][j] - t0, g_tr[2][j] - t0,
+             g_tr[3][j] - t0, g_tr[4][j] - t0, g_tr[5][j] - t0, g_tr[6][j] - t0, g_tr[7][j] - t0);
+  }
+#endif
 }
 
 }  // namespace
@@ -390,23 +588,18 @@ void launch_attend(const AttnParams& p, cudaStream_t st) {
   const uint64_t units = (uint64_t)p.n_req * p.L * p.Hl;
   if (!units) return;
   require(units < (1ull << 31), HR_EINVAL, "attend: too many units");
-  if (p.dtype == HR_BF16) {
-    static bool init = false;
-    if (!init) {
-      HR_CUDA(cudaFuncSetAttribute(attend_kernel<HR_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)att_smem_bytes(128)));
-      init = true;
+  static bool init[4] = {false, false, false, false};  // per (dtype, D) instantiation
+  auto go = [&](void (*kern)(AttnParams), int slot) {
+    if (!init[slot]) {
+      HR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)att_smem_bytes(128)));
+      init[slot] = true;
     }
-    attend_kernel<HR_BF16><<<(unsigned)units, kAttThreads, smem, st>>>(p);
-  } else {
-    static bool init = false;
-    if (!init) {
-      HR_CUDA(cudaFuncSetAttribute(attend_kernel<HR_FP16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)att_smem_bytes(128)));
-      init = true;
-    }
-    attend_kernel<HR_FP16><<<(unsigned)units, kAttThreads, smem, st>>>(p);
-  }
+    kern<<<(unsigned)units, kAttThreads2, smem, st>>>(p);
+  };
+  if (p.dtype == HR_BF16)
+    p.D == 128 ? go(attend_kernel<HR_BF16, 128>, 0) : go(attend_kernel<HR_BF16, 64>, 1);
+  else
+    p.D == 128 ? go(attend_kernel<HR_FP16, 128>, 2) : go(attend_kernel<HR_FP16, 64>, 3);
   HR_CUDA(cudaGetLastError());
 }
 

@@ -78,7 +78,9 @@ def run_case(torch, st, ora, lay, reqs, n_q, g, dtype, scale=None):
     dmp = dump.cpu().numpy().view(np.uint16).reshape(n_req, 2, lay.L, lay.Hl, k * lay.T, lay.D)
     for r, req in enumerate(reqs):
         K, V = ora.assemble(list(req))
-        assert np.array_equal(dmp[r, 0], K), f"decoded K differs, request {r}"
+        bad = np.argwhere(dmp[r, 0] != K)
+        assert bad.size == 0, f"decoded K differs, request {r}: {len(bad)} at {bad[:4].tolist()} " \
+            f"got {[hex(int(dmp[r, 0][tuple(i)])) for i in bad[:4]]} want {[hex(int(K[tuple(i)])) for i in bad[:4]]}"
         assert np.array_equal(dmp[r, 1], V), f"decoded V differs, request {r}"
         O, L_ = attention.attend_request(Qb[r], K, V, g, dtype, scale)
         from oracle import numerics
