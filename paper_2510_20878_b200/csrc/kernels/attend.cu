@@ -121,7 +121,8 @@ constexpr int kSoftWarps = 4, kDecWarps = 4, kDecGroups = 2;
 constexpr int kAttThreads2 = 32 * (kSoftWarps + kDecGroups * kDecWarps + 1);
 constexpr uint32_t kDecChunks = kKT * 128 / 8 / (32 * kDecWarps);  // 8-element chunks per decoder thread at D = 128
 // per decoder group: codes slots [K, V][kDecChunks][thread] x 16 B, meta slots x 8 B
-constexpr uint32_t kStageBytes = 2 * kDecChunks * 32 * kDecWarps * (16 + 8);
+constexpr uint32_t kStageBytes = 2 * kDecChunks * 32 * kDecWarps * (8 + 8);  // 8-B code + 8-B meta slots
+constexpr uint32_t kOpBufs = 3;  // K/V operand buffers: decode of tile j waits for PV_{j-3} only
 
 // The four bytes of w as exact floats (minus `bias`): 0x4B0000bb is 2^23 + bb, so one PRMT and one
 // (packed) subtraction replace an I2F per element.  bias 2^23 for unsigned bytes; 2^23 + 128 for
@@ -207,7 +208,8 @@ __device__ __forceinline__ uint4 dec_raw8(uint32_t scheme, const uint4& c, const
 template <int DT, int SCH, bool VMAJ, uint32_t D>
 __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, const uint8_t* __restrict__ stm,
                                            const float* __restrict__ gt, uint32_t gse_m, uint8_t* __restrict__ dst,
-                                           uint32_t dt, uint16_t* __restrict__ dump) {
+                                           uint32_t dt, uint16_t* __restrict__ dump, const uint8_t* __restrict__ g16,
+                                           uint32_t t0) {
   constexpr uint32_t dcs = D / 8, nch = kKT * dcs / (32 * kDecWarps);
 #pragma unroll
   for (uint32_t i = 0; i < nch; ++i) {
@@ -215,9 +217,14 @@ __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, cons
     {
       const uint32_t gI = cc >> 5, ii = cc & 7, jj = (cc >> 3) & 3;
       const uint32_t key = (gI % (kKT / 8)) * 8 + ii, dc = (gI / (kKT / 8)) * 4 + jj;
-      const uint4 raw = *reinterpret_cast<const uint4*>(stc + (i * 32 * kDecWarps + dt) * 16);
-      const float2 m = *reinterpret_cast<const float2*>(stm + (i * 32 * kDecWarps + dt) * 8);
-      const uint4 v = dec_raw8<DT>(SCH, raw, m, gse_m, gt);
+      uint4 v;
+      if (SCH == HR_S_PASS16) {  // bits unchanged: straight from global (L2-prefetched) into the operand tile
+        v = __ldg(reinterpret_cast<const uint4*>(g16 + 2ull * ((t0 + key) * D + dc * 8)));
+      } else {
+        const uint2 raw = *reinterpret_cast<const uint2*>(stc + (i * 32 * kDecWarps + dt) * 8);
+        const float2 m = *reinterpret_cast<const float2*>(stm + (i * 32 * kDecWarps + dt) * 8);
+        v = dec_raw8<DT>(SCH, make_uint4(raw.x, raw.y, 0u, 0u), m, gse_m, gt);
+      }
       if (VMAJ)
         *reinterpret_cast<uint4*>(dst + ((key / 8) * dcs + dc) * 128 + (key % 8) * 16) = v;
       else
@@ -228,14 +235,15 @@ __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, cons
 }
 template <int DT, bool VMAJ, uint32_t D>
 __device__ __forceinline__ void dec_tile(uint32_t scheme, const uint8_t* stc, const uint8_t* stm, const float* gt,
-                                         uint32_t gse_m, uint8_t* dst, uint32_t dt, uint16_t* dump) {
+                                         uint32_t gse_m, uint8_t* dst, uint32_t dt, uint16_t* dump,
+                                         const uint8_t* g16, uint32_t t0) {
   switch (scheme) {
-    case HR_S_PASS16: return dec_tile_s<DT, HR_S_PASS16, VMAJ, D>(stc, stm, gt, gse_m, dst, dt, dump);
-    case HR_S_INT8: return dec_tile_s<DT, HR_S_INT8, VMAJ, D>(stc, stm, gt, gse_m, dst, dt, dump);
-    case HR_S_FP8E4M3: return dec_tile_s<DT, HR_S_FP8E4M3, VMAJ, D>(stc, stm, gt, gse_m, dst, dt, dump);
-    case HR_S_FP8E5M2: return dec_tile_s<DT, HR_S_FP8E5M2, VMAJ, D>(stc, stm, gt, gse_m, dst, dt, dump);
-    case HR_S_INT4: return dec_tile_s<DT, HR_S_INT4, VMAJ, D>(stc, stm, gt, gse_m, dst, dt, dump);
-    default: return dec_tile_s<DT, HR_S_GSE8, VMAJ, D>(stc, stm, gt, gse_m, dst, dt, dump);
+    case HR_S_PASS16: return dec_tile_s<DT, HR_S_PASS16, VMAJ, D>(stc, stm, gt, gse_m, dst, dt, dump, g16, t0);
+    case HR_S_INT8: return dec_tile_s<DT, HR_S_INT8, VMAJ, D>(stc, stm, gt, gse_m, dst, dt, dump, g16, t0);
+    case HR_S_FP8E4M3: return dec_tile_s<DT, HR_S_FP8E4M3, VMAJ, D>(stc, stm, gt, gse_m, dst, dt, dump, g16, t0);
+    case HR_S_FP8E5M2: return dec_tile_s<DT, HR_S_FP8E5M2, VMAJ, D>(stc, stm, gt, gse_m, dst, dt, dump, g16, t0);
+    case HR_S_INT4: return dec_tile_s<DT, HR_S_INT4, VMAJ, D>(stc, stm, gt, gse_m, dst, dt, dump, g16, t0);
+    default: return dec_tile_s<DT, HR_S_GSE8, VMAJ, D>(stc, stm, gt, gse_m, dst, dt, dump, g16, t0);
   }
 }
 
@@ -248,7 +256,7 @@ __device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
 __device__ __forceinline__ void stage_chunk(uint32_t scheme, const uint8_t* codes, const uint8_t* meta, uint32_t e,
                                             uint32_t g_shift, uint8_t* sc, uint8_t* sm) {
   if (scheme == HR_S_PASS16) {
-    cp_async<16>(sc, codes + 2ull * e);
+    // copied straight into the operand buffer once it is free (dec_tile_s<PASS16>)
   } else if (scheme == HR_S_INT4) {
     cp_async<4>(sc, codes + e / 2);
     cp_async<8>(sm, meta + 8ull * (e >> g_shift));
@@ -274,14 +282,30 @@ constexpr uint32_t kPF = 4;  // L2 prefetch distance in tiles
 
 size_t att_smem_bytes(uint32_t D) {
   return (size_t)kRows * D * 2 + 4 * (size_t)kKT * D * 2 + 2 * (size_t)kRows * kKT * 2 + 4 * 32 * 4 + 16 * 8 + 16 +
-         kDecGroups * kStageBytes;
+         kDecGroups * kStageBytes + (kOpBufs - 2) * 2 * (size_t)kKT * D * 2;
 }
 
 // 2^x on the SFU (MUFU.EX2, relative error ~2^-22, far inside R28's 2^-9 budget)
 __device__ __forceinline__ float ex2(float x) {
+#ifdef HARAG_ATT_NOEXP
+  return x;  // pipeline study only
+#else
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+#endif
+}
+// non-blocking: has the phase with parity `parity` completed?
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(saddr(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
 }
 __device__ __forceinline__ void named_bar(uint32_t id, uint32_t n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
@@ -306,12 +330,13 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   constexpr uint32_t dcs = D / 8;
   uint8_t* sq = smem_raw;                          // [128 rows][D] K-major core layout
-  uint8_t* skb = sq + kRows * D * 2;               // 2 x [64 keys][D] K-major (B of S = Q K^T)
-  uint8_t* svb = skb + 2 * kKT * D * 2;            // 2 x [64 keys][D] MN-major (B of O += P V)
-  uint8_t* spb = svb + 2 * kKT * D * 2;            // 2 x [128 rows][64 keys] K-major (A of O += P V)
+  uint8_t* skb = sq + kRows * D * 2;               // kOpBufs x [64 keys][D] K-major (B of S = Q K^T)
+  uint8_t* svb = skb + kOpBufs * kKT * D * 2;      // kOpBufs x [64 keys][D] MN-major (B of O += P V)
+  uint8_t* spb = svb + kOpBufs * kKT * D * 2;      // 2 x [128 rows][64 keys] K-major (A of O += P V)
   float* gtab = reinterpret_cast<float*>(spb + 2 * kRows * kKT * 2);  // [group][2][32] GSE tables (K, V)
   uint64_t* bar = reinterpret_cast<uint64_t*>(gtab + 128);
-  uint64_t *sf = bar, *pf = bar + 2, *kvf = bar + 4, *kve = bar + 6, *od = bar + 8, *qf = bar + 9;
+  uint64_t *sf = bar, *pf = bar + 2, *kvf = bar + 4, *kve = bar + 7, *od = bar + 10, *qf = bar + 11;
+  uint64_t* pfree = bar + 12;  // [2]: PV_j done -> P buffer j & 1 free
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
   uint8_t* stage0 = reinterpret_cast<uint8_t*>(bar + 18);  // 16-B aligned decoder staging
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -333,6 +358,9 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     for (int b = 0; b < 2; ++b) {
       mbar_init(&sf[b], 1);
       mbar_init(&pf[b], kSoftWarps);
+      mbar_init(&pfree[b], 1);
+    }
+    for (uint32_t b = 0; b < kOpBufs; ++b) {
       mbar_init(&kvf[b], kDecWarps);
       mbar_init(&kve[b], 1);
     }
@@ -383,7 +411,9 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         for (int q = 0; q < 32; ++q) mx4[q & 3] = fmaxf(mx4[q & 3], __uint_as_float(sv[a][q]));
       const float mt = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * c;  // c > 0: max(s) c = max(s c)
       const bool grow = mt > m_ref + 8.f;  // lazy rescale: p stays <= 2^8 between rescales
-      if (j >= 2) mbar_wait(&kve[b], ((j >> 1) - 1) & 1);  // PV_{j-2} done: P[b] free, O at most one PV behind
+      // PV_{j-2} done: P[b] free and O at most one PV behind (a per-buffer barrier: od itself may already
+      // be past PV_{j-1}, which would alias its parity)
+      if (j >= 2) mbar_wait(&pfree[b], ((j >> 1) - 1) & 1);
       if (__any_sync(0xFFFFFFFFu, grow) && j > 0) {
         mbar_wait(od, (j - 1) & 1);  // PV_{j-1} done: O may be read and rewritten
         tc_after();
@@ -424,8 +454,9 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       if (tid == 0) TR(1, j);
     }
     // epilogue: O / l -> output dtype; LSE (natural log) = ln 2 * (m_ref + log2 l)
-    if (n_tiles >= 2) mbar_wait(od, (n_tiles - 2) & 1);
-    mbar_wait(od, (n_tiles - 1) & 1);
+    // PV_{n-1} done (its commit covers every earlier MMA); the per-buffer barrier has completed at least
+    // PV_{n-3}'s phase, so its parity cannot alias
+    if (n_tiles) mbar_wait(&pfree[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
     tc_after();
     const float inv = 1.f / lsum;
     for (uint32_t cb = 0; cb < D; cb += 32) {
@@ -469,7 +500,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       for (uint32_t j = grp; j < kPF && j < n_tiles; j += kDecGroups) prefetch(j);
     uint32_t cur_slot = 0xFFFFFFFFu;
     for (uint32_t j = grp; j < n_tiles; j += kDecGroups) {
-      const uint32_t b = grp, use = j >> 1;  // use-th fill of buffer b
+      const uint32_t b = j % kOpBufs, use = j / kOpBufs;  // use-th fill of operand buffer b
       const AsmDesc *dkp, *dvp;
       uint32_t t0;
       tile_src(j, dkp, dvp, t0);
@@ -481,8 +512,8 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       const uint8_t* vm = dv.meta + (uint64_t)slab_i * p.meta_stride[dv.scheme];
       const uint32_t slot = j / tiles_per_doc;
       // all of this thread's loads in flight at once: cp.async into its own staging slots
-      uint8_t* stc = stage0 + grp * kStageBytes;                         // [K, V][i][dt] x 16 B
-      uint8_t* stm = stc + 2 * kDecChunks * 32 * kDecWarps * 16;          // [K, V][i][dt] x 8 B
+      uint8_t* stc = stage0 + grp * kStageBytes;                         // [K, V][i][dt] x 8 B codes
+      uint8_t* stm = stc + 2 * kDecChunks * 32 * kDecWarps * 8;           // [K, V][i][dt] x 8 B meta
 #pragma unroll
       for (uint32_t i = 0; i < kKT * dcs / (32 * kDecWarps); ++i) {
         const uint32_t cc = dt + i * 32 * kDecWarps;
@@ -491,8 +522,8 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
           const uint32_t key = (gI % (kKT / 8)) * 8 + ii, dc = (gI / (kKT / 8)) * 4 + jj;
           const uint32_t e = (t0 + key) * D + dc * 8;
           const uint32_t sl = i * 32 * kDecWarps + dt;
-          stage_chunk(dk.scheme, kc, km, e, p.g_shift, stc + sl * 16, stm + sl * 8);
-          stage_chunk(dv.scheme, vc, vm, e, p.g_shift, stc + (kDecChunks * 32 * kDecWarps + sl) * 16,
+          stage_chunk(dk.scheme, kc, km, e, p.g_shift, stc + sl * 8, stm + sl * 8);
+          stage_chunk(dv.scheme, vc, vm, e, p.g_shift, stc + (kDecChunks * 32 * kDecWarps + sl) * 8,
                       stm + (kDecChunks * 32 * kDecWarps + sl) * 8);
         }
       }
@@ -510,7 +541,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         named_bar(1 + grp, 32 * kDecWarps);
       }
       if (dt == 0) TR(6, j);
-      if (use >= 1) mbar_wait(&kve[b], (use - 1) & 1);  // PV_{j-2} (and S_{j-2}) done: buffer b free
+      if (use >= 1) mbar_wait(&kve[b], (use - 1) & 1);  // PV_{j-3} (and S_{j-3}) done: buffer b free
       if (dt == 0) TR(2, j);
       asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's staged chunks have landed
       if (dt == 0) TR(7, j);
@@ -522,9 +553,9 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
           dump = p.kv_dump + ((((uint64_t)r * 2) * p.L + l) * p.Hl + h) * p.k * p.T * D + ((uint64_t)slot * p.T + t0) * D;
         const uint64_t kvoff = (uint64_t)p.L * p.Hl * p.k * p.T * D;
         const uint32_t vo = kDecChunks * 32 * kDecWarps;
-        dec_tile<DT, false, D>(dk.scheme, stc, stm, gt, p.gse_m, skd, dt, dump);
-        dec_tile<DT, true, D>(dv.scheme, stc + vo * 16, stm + vo * 8, gt + 32, p.gse_m, svd, dt,
-                              dump ? dump + kvoff : nullptr);
+        dec_tile<DT, false, D>(dk.scheme, stc, stm, gt, p.gse_m, skd, dt, dump, kc, t0);
+        dec_tile<DT, true, D>(dv.scheme, stc + vo * 8, stm + vo * 8, gt + 32, p.gse_m, svd, dt,
+                              dump ? dump + kvoff : nullptr, vc, t0);
       }
       fence_async_smem();
       __syncwarp();
@@ -537,32 +568,36 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     const uint32_t id_s = idesc(fmt, 0, 0, kKT, kRows);  // S[128 x 64] = Q[128 x D] . K[64 x D]^T
     const uint32_t id_o = idesc(fmt, 0, 1, D, kRows);    // O[128 x D] += P[128 x 64] . V[64 x D] (V MN-major)
     const uint32_t qa = saddr(sq);
-    auto pv = [&](uint32_t jj) {
-      const uint32_t bb = jj & 1;
-      mbar_wait(&pf[bb], (jj >> 1) & 1);
-      TR(5, jj);
-      tc_after();
-      const uint32_t pa = saddr(spb + bb * (kRows * kKT * 2)), va = saddr(svb + bb * (kKT * D * 2));
-      for (uint32_t s = 0; s < kKT / 16; ++s)
-        mma_f16(t_o, sdesc(pa + s * 2 * (kRows / 8) * 128, (kRows / 8) * 128, 128),
-                sdesc(va + s * 2 * dcs * 128, dcs * 128, 128), id_o, (jj > 0 || s > 0) ? 1u : 0u);
-      mma_commit(&kve[bb]);
-      mma_commit(od);
-    };
+    // Event-driven issue: S_j needs operands j (kvf) and its TMEM buffer free (softmax of j-2 done, i.e.
+    // PV_{j-2} already issued); PV_j needs P_j (pf).  Whichever is ready goes first, so PV_{j-1} (which
+    // frees the operand buffer decode j+1 waits for) never waits behind the decode of tile j.
+    uint32_t ns = 0, npv = 0;
     mbar_wait(qf, 0);
-    for (uint32_t j = 0; j < n_tiles; ++j) {
-      const uint32_t b = j & 1;
-      mbar_wait(&kvf[b], (j >> 1) & 1);
-      TR(4, j);
-      tc_after();
-      const uint32_t ka = saddr(skb + b * (kKT * D * 2));
-      for (uint32_t s = 0; s < D / 16; ++s)  // K-major: one k-step = 2 core matrices along K
-        mma_f16(tmem + b * kKT, sdesc(qa + s * 2 * (kRows / 8) * 128, (kRows / 8) * 128, 128),
-                sdesc(ka + s * 2 * (kKT / 8) * 128, (kKT / 8) * 128, 128), id_s, s > 0);
-      mma_commit(&sf[b]);
-      if (j >= 1) pv(j - 1);
+    while (npv < n_tiles) {
+      if (ns < n_tiles && ns <= npv + 1 && mbar_test(&kvf[ns % kOpBufs], (ns / kOpBufs) & 1)) {
+        const uint32_t b = ns & 1, ob = ns % kOpBufs;
+        TR(4, ns);
+        tc_after();
+        const uint32_t ka = saddr(skb + ob * (kKT * D * 2));
+        for (uint32_t s = 0; s < D / 16; ++s)  // K-major: one k-step = 2 core matrices along K
+          mma_f16(tmem + b * kKT, sdesc(qa + s * 2 * (kRows / 8) * 128, (kRows / 8) * 128, 128),
+                  sdesc(ka + s * 2 * (kKT / 8) * 128, (kKT / 8) * 128, 128), id_s, s > 0);
+        mma_commit(&sf[b]);
+        ++ns;
+      } else if (npv < ns && mbar_test(&pf[npv & 1], (npv >> 1) & 1)) {
+        const uint32_t bb = npv & 1, ob = npv % kOpBufs;
+        TR(5, npv);
+        tc_after();
+        const uint32_t pa = saddr(spb + bb * (kRows * kKT * 2)), va = saddr(svb + ob * (kKT * D * 2));
+        for (uint32_t s = 0; s < kKT / 16; ++s)
+          mma_f16(t_o, sdesc(pa + s * 2 * (kRows / 8) * 128, (kRows / 8) * 128, 128),
+                  sdesc(va + s * 2 * dcs * 128, dcs * 128, 128), id_o, (npv > 0 || s > 0) ? 1u : 0u);
+        mma_commit(&kve[ob]);
+        mma_commit(&pfree[bb]);
+        mma_commit(od);
+        ++npv;
+      }
     }
-    if (n_tiles) pv(n_tiles - 1);
   }
   tc_before();
   __syncthreads();
