@@ -117,7 +117,7 @@ __device__ __forceinline__ float hi_f(uint32_t w) {
   return DT == HR_BF16 ? __uint_as_float(w & 0xFFFF0000u) : __half2float(__ushort_as_half((unsigned short)(w >> 16)));
 }
 
-constexpr int kSoftWarps = 4, kDecWarps = 4, kDecGroups = 2;
+constexpr int kSoftWarps = 8, kDecWarps = 4, kDecGroups = 2;
 constexpr int kAttThreads2 = 32 * (kSoftWarps + kDecGroups * kDecWarps + 1);
 constexpr uint32_t kDecChunks = kKT * 128 / 8 / (32 * kDecWarps);  // 8-element chunks per decoder thread at D = 128
 // per decoder group: codes slots [K, V][kDecChunks][thread] x 16 B, meta slots x 8 B
@@ -282,7 +282,7 @@ constexpr uint32_t kPF = 4;  // L2 prefetch distance in tiles
 
 size_t att_smem_bytes(uint32_t D) {
   return (size_t)kRows * D * 2 + 4 * (size_t)kKT * D * 2 + 2 * (size_t)kRows * kKT * 2 + 4 * 32 * 4 + 16 * 8 + 16 +
-         kDecGroups * kStageBytes + (kOpBufs - 2) * 2 * (size_t)kKT * D * 2;
+         kDecGroups * kStageBytes + (kOpBufs - 2) * 2 * (size_t)kKT * D * 2 + 2 * 2 * kRows * 4;
 }
 
 // 2^x on the SFU (MUFU.EX2, relative error ~2^-22, far inside R28's 2^-9 budget)
@@ -319,7 +319,7 @@ __device__ __forceinline__ uint32_t code_bytes_of(uint32_t scheme, uint32_t n_el
 }
 
 #ifdef HARAG_ATT_TRACE
-__device__ long long g_tr[9][96];  // per-tile event clocks of CTA 0 (pipeline study builds only)
+__device__ long long g_tr[14][96];  // per-tile event clocks of CTA 0 (pipeline study builds only)
 #define TR(ev, j) do { if (blockIdx.x == 0 && (j) < 96) g_tr[ev][j] = clock64(); } while (0)
 #else
 #define TR(ev, j) do { } while (0)
@@ -339,6 +339,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
   uint64_t* pfree = bar + 12;  // [2]: PV_j done -> P buffer j & 1 free
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
   uint8_t* stage0 = reinterpret_cast<uint8_t*>(bar + 18);  // 16-B aligned decoder staging
+  float* rmax = reinterpret_cast<float*>(stage0 + kDecGroups * kStageBytes);  // [2 slots][2 halves][128 rows]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   const uint32_t unit = blockIdx.x;  // (request, layer, head)
@@ -365,7 +366,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       mbar_init(&kve[b], 1);
     }
     mbar_init(od, 1);
-    mbar_init(qf, kSoftWarps);
+    mbar_init(qf, kSoftWarps);  // every softmax warp loads a share of Q
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (p.descs[0].count != nullptr && l == 0 && h == 0) {  // a1: hotness of this request's items
       for (uint32_t j = 0; j < 2 * p.k; ++j) {
@@ -382,6 +383,10 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
 
   if (warp < kSoftWarps) {
     // ------------------------------------------------------------------ softmax warps
+    // warp w: TMEM lane quadrant w & 3 (rows 32 (w & 3) .. + 31), column half hf = w >> 2 of S (keys
+    // 32 hf .. + 31) and of O (columns D/2 hf ..).  The two warps of a quadrant exchange their partial
+    // row maxima through shared memory (named barrier 3) so both take identical rescale decisions.
+    const uint32_t quad = warp & 3, hf = warp >> 2, t = quad * 32 + lane;  // t: query row
     // Q tile: rows >= M are zero.  Thread mapping per 32 chunks: 8 rows x 4 column chunks.
     for (uint32_t c = tid; c < kRows * dcs; c += 32 * kSoftWarps) {
       const uint32_t gI = c >> 5, i = c & 7, jj = (c >> 3) & 3;
@@ -393,7 +398,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     fence_async_smem();
     __syncwarp();
     if (lane == 0) mbar_arrive1(qf);
-    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    const uint32_t lane_base = (quad * 32) << 16;
     const float c = p.scale_log2;
     float m_ref = -INFINITY, lsum = 0.f;
     for (uint32_t j = 0; j < n_tiles; ++j) {
@@ -401,24 +406,26 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       mbar_wait(&sf[b], (j >> 1) & 1);
       if (tid == 0) TR(0, j);
       tc_after();
-      uint32_t sv[2][32];
-      tmem_ld32(tmem + b * kKT + lane_base, sv[0]);
-      tmem_ld32(tmem + b * kKT + 32 + lane_base, sv[1]);
+      uint32_t sv[32];
+      tmem_ld32(tmem + b * kKT + hf * 32 + lane_base, sv);
+      if (tid == 0) TR(8, j);
       float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // independent chains (ILP)
 #pragma unroll
-      for (int a = 0; a < 2; ++a)
-#pragma unroll
-        for (int q = 0; q < 32; ++q) mx4[q & 3] = fmaxf(mx4[q & 3], __uint_as_float(sv[a][q]));
-      const float mt = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * c;  // c > 0: max(s) c = max(s c)
+      for (int q = 0; q < 32; ++q) mx4[q & 3] = fmaxf(mx4[q & 3], __uint_as_float(sv[q]));
+      rmax[(j & 1) * 256 + hf * 128 + t] = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
+      named_bar(3, 32 * kSoftWarps);  // double-buffered slots: a warp cannot overwrite before its partner read
+      if (tid == 0) TR(9, j);
+      const float mt = fmaxf(rmax[(j & 1) * 256 + t], rmax[(j & 1) * 256 + 128 + t]) * c;  // c > 0
       const bool grow = mt > m_ref + 8.f;  // lazy rescale: p stays <= 2^8 between rescales
       // PV_{j-2} done: P[b] free and O at most one PV behind (a per-buffer barrier: od itself may already
       // be past PV_{j-1}, which would alias its parity)
       if (j >= 2) mbar_wait(&pfree[b], ((j >> 1) - 1) & 1);
+      if (tid == 0) TR(10, j);
       if (__any_sync(0xFFFFFFFFu, grow) && j > 0) {
         mbar_wait(od, (j - 1) & 1);  // PV_{j-1} done: O may be read and rewritten
         tc_after();
         const float alpha = grow ? ex2(m_ref - mt) : 1.f;
-        for (uint32_t cb = 0; cb < D; cb += 32) {
+        for (uint32_t cb = hf * (D / 2); cb < (hf + 1) * (D / 2); cb += 32) {
           uint32_t ov[32];
           tmem_ld32(t_o + lane_base + cb, ov);
 #pragma unroll
@@ -428,42 +435,44 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         lsum *= alpha;
       }
       if (grow) m_ref = mt;
-      uint8_t* prow = spb + b * (kRows * kKT * 2) + (tid / 8) * 128 + (tid % 8) * 16;
+      uint8_t* prow = spb + b * (kRows * kKT * 2) + (t / 8) * 128 + (t % 8) * 16;
       float ls4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int a = 0; a < 2; ++a) {
+      for (int q = 0; q < 4; ++q) {  // 8 keys -> one 16-B core-matrix row
+        uint32_t w[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {  // 8 keys -> one 16-B core-matrix row
-          uint32_t w[4];
-#pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const float p0 = ex2(__fmaf_rn(__uint_as_float(sv[a][q * 8 + 2 * u]), c, -m_ref));
-            const float p1 = ex2(__fmaf_rn(__uint_as_float(sv[a][q * 8 + 2 * u + 1]), c, -m_ref));
-            w[u] = pack2<DT>(p0, p1);
-            ls4[u] += lo_f<DT>(w[u]) + hi_f<DT>(w[u]);  // normalise by the rounded weights actually used
-          }
-          const uint32_t kc8 = a * 4 + q;  // key chunk
-          *reinterpret_cast<uint4*>(prow + kc8 * (kRows / 8) * 128) = make_uint4(w[0], w[1], w[2], w[3]);
+        for (int u = 0; u < 4; ++u) {
+          const float p0 = ex2(__fmaf_rn(__uint_as_float(sv[q * 8 + 2 * u]), c, -m_ref));
+          const float p1 = ex2(__fmaf_rn(__uint_as_float(sv[q * 8 + 2 * u + 1]), c, -m_ref));
+          w[u] = pack2<DT>(p0, p1);
+          ls4[u] += lo_f<DT>(w[u]) + hi_f<DT>(w[u]);  // normalise by the rounded weights actually used
         }
+        const uint32_t kc8 = hf * 4 + q;  // key chunk
+        *reinterpret_cast<uint4*>(prow + kc8 * (kRows / 8) * 128) = make_uint4(w[0], w[1], w[2], w[3]);
       }
       lsum += (ls4[0] + ls4[1]) + (ls4[2] + ls4[3]);
+      if (tid == 0) TR(11, j);
       fence_async_smem();
       tc_before();
       __syncwarp();
       if (lane == 0) mbar_arrive1(&pf[b]);
       if (tid == 0) TR(1, j);
     }
-    // epilogue: O / l -> output dtype; LSE (natural log) = ln 2 * (m_ref + log2 l)
+    // epilogue: O / l -> output dtype; LSE (natural log) = ln 2 * (m_ref + log2 l), l = sum of both halves
+    const uint32_t es = (n_tiles & 1) * 256;  // the slot the last tile's exchange did not use
+    rmax[es + hf * 128 + t] = lsum;
+    named_bar(3, 32 * kSoftWarps);
+    const float ltot = rmax[es + t] + rmax[es + 128 + t];
     // PV_{n-1} done (its commit covers every earlier MMA); the per-buffer barrier has completed at least
     // PV_{n-3}'s phase, so its parity cannot alias
     if (n_tiles) mbar_wait(&pfree[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
     tc_after();
-    const float inv = 1.f / lsum;
-    for (uint32_t cb = 0; cb < D; cb += 32) {
+    const float inv = 1.f / ltot;
+    for (uint32_t cb = hf * (D / 2); cb < (hf + 1) * (D / 2); cb += 32) {
       uint32_t ov[32];
       tmem_ld32(t_o + lane_base + cb, ov);
-      if ((uint32_t)tid < p.M) {
-        uint4* dst = reinterpret_cast<uint4*>(p.o + (row0 + tid) * D + cb);
+      if (t < p.M) {
+        uint4* dst = reinterpret_cast<uint4*>(p.o + (row0 + t) * D + cb);
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           uint32_t w[4];
@@ -474,7 +483,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         }
       }
     }
-    if ((uint32_t)tid < p.M && p.lse) p.lse[row0 + tid] = 0.69314718055994531f * (m_ref + __log2f(lsum));
+    if (hf == 0 && t < p.M && p.lse) p.lse[row0 + t] = 0.69314718055994531f * (m_ref + __log2f(ltot));
   } else if (warp < kSoftWarps + kDecGroups * kDecWarps) {
     // ------------------------------------------------------------------ decoder warps
     const uint32_t grp = (uint32_t)(warp - kSoftWarps) / kDecWarps;   // tiles j with j & 1 == grp
@@ -583,6 +592,10 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
           mma_f16(tmem + b * kKT, sdesc(qa + s * 2 * (kRows / 8) * 128, (kRows / 8) * 128, 128),
                   sdesc(ka + s * 2 * (kKT / 8) * 128, (kKT / 8) * 128, 128), id_s, s > 0);
         mma_commit(&sf[b]);
+#ifdef HARAG_ATT_MMASYNC
+        mbar_wait(&sf[b], (ns >> 1) & 1);  // pipeline study: time the MMA alone
+        TR(12, ns);
+#endif
         ++ns;
       } else if (npv < ns && mbar_test(&pf[npv & 1], (npv >> 1) & 1)) {
         const uint32_t bb = npv & 1, ob = npv % kOpBufs;
@@ -595,6 +608,10 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         mma_commit(&kve[ob]);
         mma_commit(&pfree[bb]);
         mma_commit(od);
+#ifdef HARAG_ATT_MMASYNC
+        mbar_wait(&pfree[bb], (npv >> 1) & 1);
+        TR(13, npv);
+#endif
         ++npv;
       }
     }
@@ -605,10 +622,12 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
 #ifdef HARAG_ATT_TRACE
   if (blockIdx.x == 0 && tid == 0) {
     const long long t0 = g_tr[6][0];
-    printf("tile sfwait pfarr kvewait kvfarr Sissue PVissue decstart loadsin (cycles from decode start of tile 0)\n");
+    printf("tile sfwait pfarr kvewait kvfarr Sissue PVissue decstart loadsin | tmemld xchg pfree expdone | Sdone PVdone\n");
     for (uint32_t j = 0; j < n_tiles && j < 96; ++j)
-      printf("%u %lld %lld %lld %lld %lld %lld %lld %lld\n", j, g_tr[0][j] - t0, g_tr[1][j] - t0, g_tr[2][j] - t0,
-             g_tr[3][j] - t0, g_tr[4][j] - t0, g_tr[5][j] - t0, g_tr[6][j] - t0, g_tr[7][j] - t0);
+      printf("%u %lld %lld %lld %lld %lld %lld %lld %lld | %lld %lld %lld %lld | %lld %lld\n", j, g_tr[0][j] - t0,
+             g_tr[1][j] - t0, g_tr[2][j] - t0, g_tr[3][j] - t0, g_tr[4][j] - t0, g_tr[5][j] - t0, g_tr[6][j] - t0,
+             g_tr[7][j] - t0, g_tr[8][j] - t0, g_tr[9][j] - t0, g_tr[10][j] - t0, g_tr[11][j] - t0,
+             g_tr[12][j] - t0, g_tr[13][j] - t0);
   }
 #endif
 }
