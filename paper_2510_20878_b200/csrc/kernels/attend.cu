@@ -18,7 +18,7 @@
 // into TMEM; each thread owns one query row for the online softmax (tcgen05.ld
 // of its S row, exp2, lazy rescale of O only when the running max grows by
 // more than 2^8), writes P to shared memory; one thread issues O += P V into
-// TMEM.  Operand tiles use the canonical no-swizzle core-matrix layouts
+// TMEM.  Q, K and P use 128-byte-swizzled K-major tiles, V the canonical no-swizzle MN-major layout
 // (8 rows x 16 B per core matrix).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
@@ -53,6 +53,17 @@ __device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_
 
 // Shared-memory matrix descriptor, no swizzle (canonical core-matrix layout): start address,
 // LBO = byte distance between core matrices adjacent in K, SBO = adjacent in M/N; version 1.
+// K-major operand with the 128-byte swizzle: rows of 64 16-bit elements (128 B), 8-row atoms of 1024 B
+// (SBO), 16-B chunk c of row r stored at chunk c ^ (r & 7); K beyond 64 elements = the next 64-column block.
+// One MMA k-step (16 elements = 32 B) advances the start address by 32 B inside the atom.  The swizzle
+// is a function of the absolute shared-memory address, so every block is 1024-B aligned.
+__device__ __forceinline__ uint64_t sdesc_sw128(uint32_t addr) {
+  return (uint64_t)((addr >> 4) & 0x3FFFu) | (1ull << 16) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
+}
+// byte offset of 16-B chunk dc (8 elements) of row `row` in a SW128 K-major tile of `rows` rows
+__device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t dc, uint32_t rows) {
+  return (dc >> 3) * (rows * 128) + (row >> 3) * 1024 + (row & 7) * 128 + (((dc & 7) ^ (row & 7)) << 4);
+}
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
   return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
@@ -228,7 +239,7 @@ __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, cons
       if (VMAJ)
         *reinterpret_cast<uint4*>(dst + ((key / 8) * dcs + dc) * 128 + (key % 8) * 16) = v;
       else
-        *reinterpret_cast<uint4*>(dst + (dc * (kKT / 8) + key / 8) * 128 + (key % 8) * 16) = v;
+        *reinterpret_cast<uint4*>(dst + sw128_off(key, dc, kKT)) = v;
       if (dump) *reinterpret_cast<uint4*>(dump + key * D + dc * 8) = v;
     }
   }
@@ -356,6 +367,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
+    if (saddr(smem_raw) & 1023u) __trap();  // 128-B-swizzled operand tiles need 1024-B-aligned atoms
     for (int b = 0; b < 2; ++b) {
       mbar_init(&sf[b], 1);
       mbar_init(&pf[b], kSoftWarps);
@@ -393,7 +405,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       const uint32_t row = (gI % (kRows / 8)) * 8 + i, dc = (gI / (kRows / 8)) * 4 + jj;
       uint4 v = make_uint4(0, 0, 0, 0);
       if (row < p.M) v = __ldg(reinterpret_cast<const uint4*>(p.q + (row0 + row) * D) + dc);
-      *reinterpret_cast<uint4*>(sq + (dc * (kRows / 8) + row / 8) * 128 + (row % 8) * 16) = v;
+      *reinterpret_cast<uint4*>(sq + sw128_off(row, dc, kRows)) = v;
     }
     fence_async_smem();
     __syncwarp();
@@ -435,7 +447,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         lsum *= alpha;
       }
       if (grow) m_ref = mt;
-      uint8_t* prow = spb + b * (kRows * kKT * 2) + (t / 8) * 128 + (t % 8) * 16;
+      uint8_t* pbuf = spb + b * (kRows * kKT * 2);
       float ls4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (int q = 0; q < 4; ++q) {  // 8 keys -> one 16-B core-matrix row
@@ -448,7 +460,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
           ls4[u] += lo_f<DT>(w[u]) + hi_f<DT>(w[u]);  // normalise by the rounded weights actually used
         }
         const uint32_t kc8 = hf * 4 + q;  // key chunk
-        *reinterpret_cast<uint4*>(prow + kc8 * (kRows / 8) * 128) = make_uint4(w[0], w[1], w[2], w[3]);
+        *reinterpret_cast<uint4*>(pbuf + sw128_off(t, kc8, kRows)) = make_uint4(w[0], w[1], w[2], w[3]);
       }
       lsum += (ls4[0] + ls4[1]) + (ls4[2] + ls4[3]);
       if (tid == 0) TR(11, j);
@@ -589,8 +601,8 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         tc_after();
         const uint32_t ka = saddr(skb + ob * (kKT * D * 2));
         for (uint32_t s = 0; s < D / 16; ++s)  // K-major: one k-step = 2 core matrices along K
-          mma_f16(tmem + b * kKT, sdesc(qa + s * 2 * (kRows / 8) * 128, (kRows / 8) * 128, 128),
-                  sdesc(ka + s * 2 * (kKT / 8) * 128, (kKT / 8) * 128, 128), id_s, s > 0);
+          mma_f16(tmem + b * kKT, sdesc_sw128(qa + (s >> 2) * (kRows * 128) + (s & 3) * 32),
+                  sdesc_sw128(ka + (s >> 2) * (kKT * 128) + (s & 3) * 32), id_s, s > 0);
         mma_commit(&sf[b]);
 #ifdef HARAG_ATT_MMASYNC
         mbar_wait(&sf[b], (ns >> 1) & 1);  // pipeline study: time the MMA alone
@@ -603,8 +615,8 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         tc_after();
         const uint32_t pa = saddr(spb + bb * (kRows * kKT * 2)), va = saddr(svb + ob * (kKT * D * 2));
         for (uint32_t s = 0; s < kKT / 16; ++s)
-          mma_f16(t_o, sdesc(pa + s * 2 * (kRows / 8) * 128, (kRows / 8) * 128, 128),
-                  sdesc(va + s * 2 * dcs * 128, dcs * 128, 128), id_o, (npv > 0 || s > 0) ? 1u : 0u);
+          mma_f16(t_o, sdesc_sw128(pa + s * 32), sdesc(va + s * 2 * dcs * 128, dcs * 128, 128), id_o,
+                  (npv > 0 || s > 0) ? 1u : 0u);
         mma_commit(&kve[ob]);
         mma_commit(&pfree[bb]);
         mma_commit(od);
