@@ -10,16 +10,20 @@
 // to the precomputed chunk KV that TurboRAG / HA-RAG prefill performs (P:41,
 // P:316); LSE lets a caller merge it with the question's own causal part.
 //
-// sm_100a design: one CTA per (request, layer, KV head) unit; the unit's
-// M = g*n_q query rows (<= 128) form the A operand of tcgen05.mma (M = 128,
-// rows past M are zero).  Per 64-key tile: all threads decode the K and V
-// codes straight from HBM into bf16/fp16 operand tiles in shared memory
-// (the decode of hr_assemble_kv, bit for bit); one thread issues S = Q K^T
-// into TMEM; each thread owns one query row for the online softmax (tcgen05.ld
-// of its S row, exp2, lazy rescale of O only when the running max grows by
-// more than 2^8), writes P to shared memory; one thread issues O += P V into
-// TMEM.  Q, K and P use 128-byte-swizzled K-major tiles, V the canonical no-swizzle MN-major layout
-// (8 rows x 16 B per core matrix).
+// sm_100a design: one CTA per (request, layer, KV head) unit,
+// warp-specialised — 8 softmax warps, 2 groups of 4 decoder warps and one MMA
+// issuer lane.  The unit's M = g*n_q <= 128 query rows are the A operand of
+// tcgen05.mma (M = 128, rows past M zero); per 64-key tile the decoders stage
+// the packed codes with cp.async (L2-prefetched ahead) and decode them, bit
+// for bit as hr_assemble_kv, into one of four K/V operand buffers; S = Q K^T
+// accumulates in one of two TMEM buffers; the softmax warps (thread = row,
+// two warps per row quadrant splitting the columns) run the online softmax
+// with a lazy O rescale and write P (16-bit) back into the S buffer's TMEM
+// columns; O += P V takes A from TMEM.  Q and K use 128-byte-swizzled K-major
+// shared-memory tiles, V the canonical no-swizzle MN-major layout (8 rows x
+// 16 B per core matrix).  Debug builds: -DHARAG_ATT_TRACE (per-tile clock64
+// events of CTA 0), -DHARAG_ATT_WATCHDOG (mbarrier waits that report and trap),
+// -DHARAG_ATT_MMASYNC (MMA latency in isolation).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_fp8.h>
@@ -106,8 +110,25 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
       : "memory");
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
+// 16 consecutive 32-bit columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      HR_W8(0), HR_W8(8)
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
 #undef HR_R8
 #undef HR_W8
+// D (TMEM) += A (TMEM: lanes = rows, 32-bit columns = pairs of 16-bit K elements) . B (shared memory)
+__device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b), "r"(id), "r"(acc)
+      : "memory");
+}
 
 template <int DT>
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
@@ -133,7 +154,7 @@ constexpr int kAttThreads2 = 32 * (kSoftWarps + kDecGroups * kDecWarps + 1);
 constexpr uint32_t kDecChunks = kKT * 128 / 8 / (32 * kDecWarps);  // 8-element chunks per decoder thread at D = 128
 // per decoder group: codes slots [K, V][kDecChunks][thread] x 16 B, meta slots x 8 B
 constexpr uint32_t kStageBytes = 2 * kDecChunks * 32 * kDecWarps * (8 + 8);  // 8-B code + 8-B meta slots
-constexpr uint32_t kOpBufs = 3;  // K/V operand buffers: decode of tile j waits for PV_{j-3} only
+constexpr uint32_t kOpBufs = 4;  // K/V operand buffers: decode of tile j waits for PV_{j-4} only
 
 // The four bytes of w as exact floats (minus `bias`): 0x4B0000bb is 2^23 + bb, so one PRMT and one
 // (packed) subtraction replace an I2F per element.  bias 2^23 for unsigned bytes; 2^23 + 128 for
@@ -292,20 +313,42 @@ __device__ __forceinline__ void stage_chunk(uint32_t scheme, const uint8_t* code
 constexpr uint32_t kPF = 4;  // L2 prefetch distance in tiles
 
 size_t att_smem_bytes(uint32_t D) {
-  return (size_t)kRows * D * 2 + 4 * (size_t)kKT * D * 2 + 2 * (size_t)kRows * kKT * 2 + 4 * 32 * 4 + 16 * 8 + 16 +
-         kDecGroups * kStageBytes + (kOpBufs - 2) * 2 * (size_t)kKT * D * 2 + 2 * 2 * kRows * 4;
+  return (size_t)kRows * D * 2 + kOpBufs * 2 * (size_t)kKT * D * 2 + 4 * 32 * 4 + 16 * 8 + 16 +
+         kDecGroups * kStageBytes + 2 * 2 * kRows * 4;
 }
 
 // 2^x on the SFU (MUFU.EX2, relative error ~2^-22, far inside R28's 2^-9 budget)
 __device__ __forceinline__ float ex2(float x) {
-#ifdef HARAG_ATT_NOEXP
-  return x;  // pipeline study only
-#else
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
-#endif
 }
+#ifdef HARAG_ATT_WATCHDOG
+// debug builds: a wait that reports (block, warp, site, parity) and traps after ~2^31 cycles
+__device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, int site, uint32_t j) {
+  const long long t0 = clock64();
+  while (true) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(saddr(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (clock64() - t0 > (1ll << 31)) {
+      printf("WATCHDOG block %d warp %d lane %d site %d parity %u tile %u\n", (int)blockIdx.x, (int)(threadIdx.x / 32),
+             (int)(threadIdx.x % 32), site, parity, j);
+      __trap();
+    }
+  }
+}
+#define MBW(bar, par, site, j) mbar_wait_wd(bar, par, site, j)
+#else
+#define MBW(bar, par, site, j) mbar_wait(bar, par)
+#endif
+
 // non-blocking: has the phase with parity `parity` completed?
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
@@ -343,11 +386,12 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
   uint8_t* sq = smem_raw;                          // [128 rows][D] K-major core layout
   uint8_t* skb = sq + kRows * D * 2;               // kOpBufs x [64 keys][D] K-major (B of S = Q K^T)
   uint8_t* svb = skb + kOpBufs * kKT * D * 2;      // kOpBufs x [64 keys][D] MN-major (B of O += P V)
-  uint8_t* spb = svb + kOpBufs * kKT * D * 2;      // 2 x [128 rows][64 keys] K-major (A of O += P V)
-  float* gtab = reinterpret_cast<float*>(spb + 2 * kRows * kKT * 2);  // [group][2][32] GSE tables (K, V)
+  // P_j lives in TMEM, packed over the first 32 columns of S buffer j & 1 (the A operand of O += P V)
+  float* gtab = reinterpret_cast<float*>(svb + kOpBufs * kKT * D * 2);  // [group][2][32] GSE tables (K, V)
   uint64_t* bar = reinterpret_cast<uint64_t*>(gtab + 128);
-  uint64_t *sf = bar, *pf = bar + 2, *kvf = bar + 4, *kve = bar + 7, *od = bar + 10, *qf = bar + 11;
-  uint64_t* pfree = bar + 12;  // [2]: PV_j done -> P buffer j & 1 free
+  static_assert(4 + 2 * kOpBufs + 4 <= 16, "mbarrier slots");
+  uint64_t *sf = bar, *pf = bar + 2, *kvf = bar + 4, *kve = kvf + kOpBufs, *od = kve + kOpBufs, *qf = od + 1;
+  uint64_t* pfree = qf + 1;  // [2]: PV_j done (P_j consumed)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
   uint8_t* stage0 = reinterpret_cast<uint8_t*>(bar + 18);  // 16-B aligned decoder staging
   float* rmax = reinterpret_cast<float*>(stage0 + kDecGroups * kStageBytes);  // [2 slots][2 halves][128 rows]
@@ -415,7 +459,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     float m_ref = -INFINITY, lsum = 0.f;
     for (uint32_t j = 0; j < n_tiles; ++j) {
       const uint32_t b = j & 1;
-      mbar_wait(&sf[b], (j >> 1) & 1);
+      MBW(&sf[b], (j >> 1) & 1, 1, j);
       if (tid == 0) TR(0, j);
       tc_after();
       uint32_t sv[32];
@@ -429,12 +473,12 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       if (tid == 0) TR(9, j);
       const float mt = fmaxf(rmax[(j & 1) * 256 + t], rmax[(j & 1) * 256 + 128 + t]) * c;  // c > 0
       const bool grow = mt > m_ref + 8.f;  // lazy rescale: p stays <= 2^8 between rescales
-      // PV_{j-2} done: P[b] free and O at most one PV behind (a per-buffer barrier: od itself may already
-      // be past PV_{j-1}, which would alias its parity)
-      if (j >= 2) mbar_wait(&pfree[b], ((j >> 1) - 1) & 1);
       if (tid == 0) TR(10, j);
       if (__any_sync(0xFFFFFFFFu, grow) && j > 0) {
-        mbar_wait(od, (j - 1) & 1);  // PV_{j-1} done: O may be read and rewritten
+        // O may be read and rewritten once PV_{j-1} is done.  First PV_{j-2} on its per-buffer barrier, so
+        // that "PV done" (od) is at most one phase behind and its parity wait cannot alias.
+        if (j >= 2) MBW(&pfree[b], ((j >> 1) - 1) & 1, 7, j);
+        MBW(od, (j - 1) & 1, 2, j);
         tc_after();
         const float alpha = grow ? ex2(m_ref - mt) : 1.f;
         for (uint32_t cb = hf * (D / 2); cb < (hf + 1) * (D / 2); cb += 32) {
@@ -447,24 +491,18 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         lsum *= alpha;
       }
       if (grow) m_ref = mt;
-      uint8_t* pbuf = spb + b * (kRows * kKT * 2);
-      float ls4[4] = {0.f, 0.f, 0.f, 0.f};
+      uint32_t w[16];  // keys 32 hf + 2i, + 1 packed in column 16 hf + i of the S buffer (S reads are done:
+      float ls4[4] = {0.f, 0.f, 0.f, 0.f};  // both halves passed the max exchange)
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {  // 8 keys -> one 16-B core-matrix row
-        uint32_t w[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const float p0 = ex2(__fmaf_rn(__uint_as_float(sv[q * 8 + 2 * u]), c, -m_ref));
-          const float p1 = ex2(__fmaf_rn(__uint_as_float(sv[q * 8 + 2 * u + 1]), c, -m_ref));
-          w[u] = pack2<DT>(p0, p1);
-          ls4[u] += lo_f<DT>(w[u]) + hi_f<DT>(w[u]);  // normalise by the rounded weights actually used
-        }
-        const uint32_t kc8 = hf * 4 + q;  // key chunk
-        *reinterpret_cast<uint4*>(pbuf + sw128_off(t, kc8, kRows)) = make_uint4(w[0], w[1], w[2], w[3]);
+      for (int i = 0; i < 16; ++i) {
+        const float p0 = ex2(__fmaf_rn(__uint_as_float(sv[2 * i]), c, -m_ref));
+        const float p1 = ex2(__fmaf_rn(__uint_as_float(sv[2 * i + 1]), c, -m_ref));
+        w[i] = pack2<DT>(p0, p1);
+        ls4[i & 3] += lo_f<DT>(w[i]) + hi_f<DT>(w[i]);  // normalise by the rounded weights actually used
       }
+      tmem_st16(tmem + b * kKT + hf * 16 + lane_base, w);
       lsum += (ls4[0] + ls4[1]) + (ls4[2] + ls4[3]);
       if (tid == 0) TR(11, j);
-      fence_async_smem();
       tc_before();
       __syncwarp();
       if (lane == 0) mbar_arrive1(&pf[b]);
@@ -477,7 +515,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     const float ltot = rmax[es + t] + rmax[es + 128 + t];
     // PV_{n-1} done (its commit covers every earlier MMA); the per-buffer barrier has completed at least
     // PV_{n-3}'s phase, so its parity cannot alias
-    if (n_tiles) mbar_wait(&pfree[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
+    if (n_tiles) MBW(&pfree[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1, 8, n_tiles);
     tc_after();
     const float inv = 1.f / ltot;
     for (uint32_t cb = hf * (D / 2); cb < (hf + 1) * (D / 2); cb += 32) {
@@ -562,7 +600,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         named_bar(1 + grp, 32 * kDecWarps);
       }
       if (dt == 0) TR(6, j);
-      if (use >= 1) mbar_wait(&kve[b], (use - 1) & 1);  // PV_{j-3} (and S_{j-3}) done: buffer b free
+      if (use >= 1) MBW(&kve[b], (use - 1) & 1, 3, j);  // PV_{j-3} (and S_{j-3}) done: buffer b free
       if (dt == 0) TR(2, j);
       asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's staged chunks have landed
       if (dt == 0) TR(7, j);
@@ -593,8 +631,17 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     // PV_{j-2} already issued); PV_j needs P_j (pf).  Whichever is ready goes first, so PV_{j-1} (which
     // frees the operand buffer decode j+1 waits for) never waits behind the decode of tile j.
     uint32_t ns = 0, npv = 0;
-    mbar_wait(qf, 0);
+    MBW(qf, 0, 4, 0);
+#ifdef HARAG_ATT_WATCHDOG
+    long long wd0 = clock64();
+#endif
     while (npv < n_tiles) {
+#ifdef HARAG_ATT_WATCHDOG
+      if (clock64() - wd0 > (1ll << 33)) {
+        printf("WATCHDOG MMA block %d ns %u npv %u n %u\n", (int)blockIdx.x, ns, npv, n_tiles);
+        __trap();
+      }
+#endif
       if (ns < n_tiles && ns <= npv + 1 && mbar_test(&kvf[ns % kOpBufs], (ns / kOpBufs) & 1)) {
         const uint32_t b = ns & 1, ob = ns % kOpBufs;
         TR(4, ns);
@@ -604,8 +651,11 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
           mma_f16(tmem + b * kKT, sdesc_sw128(qa + (s >> 2) * (kRows * 128) + (s & 3) * 32),
                   sdesc_sw128(ka + (s >> 2) * (kKT * 128) + (s & 3) * 32), id_s, s > 0);
         mma_commit(&sf[b]);
+#ifdef HARAG_ATT_WATCHDOG
+        wd0 = clock64();
+#endif
 #ifdef HARAG_ATT_MMASYNC
-        mbar_wait(&sf[b], (ns >> 1) & 1);  // pipeline study: time the MMA alone
+        MBW(&sf[b], (ns >> 1) & 1, 5, ns);  // pipeline study: time the MMA alone
         TR(12, ns);
 #endif
         ++ns;
@@ -613,15 +663,18 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         const uint32_t bb = npv & 1, ob = npv % kOpBufs;
         TR(5, npv);
         tc_after();
-        const uint32_t pa = saddr(spb + bb * (kRows * kKT * 2)), va = saddr(svb + ob * (kKT * D * 2));
+        const uint32_t va = saddr(svb + ob * (kKT * D * 2));
         for (uint32_t s = 0; s < kKT / 16; ++s)
-          mma_f16(t_o, sdesc_sw128(pa + s * 32), sdesc(va + s * 2 * dcs * 128, dcs * 128, 128), id_o,
-                  (npv > 0 || s > 0) ? 1u : 0u);
+          mma_f16_ts(t_o, tmem + bb * kKT + s * 8, sdesc(va + s * 2 * dcs * 128, dcs * 128, 128), id_o,
+                     (npv > 0 || s > 0) ? 1u : 0u);  // A = P_npv from TMEM: 16 keys = 8 columns per k-step
         mma_commit(&kve[ob]);
         mma_commit(&pfree[bb]);
         mma_commit(od);
+#ifdef HARAG_ATT_WATCHDOG
+        wd0 = clock64();
+#endif
 #ifdef HARAG_ATT_MMASYNC
-        mbar_wait(&pfree[bb], (npv >> 1) & 1);
+        MBW(&pfree[bb], (npv >> 1) & 1, 6, npv);
         TR(13, npv);
 #endif
         ++npv;
