@@ -654,6 +654,169 @@ __global__ void __launch_bounds__(kQThreadsB, 1) quantize_batch_kernel(const __g
   }
 }
 
+// ---------------------------------------------------------------- GSE-8, single pass: a slab per cluster
+// A cluster of kGseQ CTAs owns one (item, layer, head) slab; CTA q bulk-copies quarter q of the slab's
+// source into its shared memory (one TMA copy), computes the quarter's exponent range, writes it into
+// every peer's shared memory (DSMEM, st.shared::cluster), and after one cluster barrier each CTA has
+// the slab-wide range, builds the code-template table (one entry per thread) and encodes its quarter
+// from shared memory.  The source is read from HBM once; many small CTAs per SM overlap the copies
+// with the encode.  Used when a quarter slab fits kGseQMaxBytes (every Llama shape).
+constexpr int kGseQ = 4;                  // CTAs per cluster (= slab quarters)
+constexpr int kGseThreads = 256;
+constexpr uint32_t kGseQMaxBytes = 64 * 1024;
+constexpr uint32_t kGseHdr = 8192;  // table + exchange + barrier
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void st_cluster_v2(uint32_t local_addr, uint32_t rank, int a, int b) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_addr), "r"(rank));
+  asm volatile("st.shared::cluster.v2.s32 [%0], {%1, %2};" ::"r"(remote), "r"(a), "r"(b) : "memory");
+}
+
+// (a & imm) | b with b a register (one LOP3; the compiler would spend two with two immediates)
+__device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(d) : "r"(a), "r"(0x007F007Fu), "r"(b));  // (a & b) | c
+  return d;
+}
+// GSE-8 codes of 8 bf16 values with a 512-entry table indexed by sign|exponent (9 bits): the entry of a
+// negative value already carries its sign bit (bits 31 and 15), so the code of the high bf16 of a word w
+// is byte 3 of ent | ({1.fraction : 0} >> (31 - keep)), of the low bf16 byte 1 of the same with the
+// 8-bit significand.  A flushed value's entry is 0 for either sign.
+__device__ __forceinline__ void enc_gse_sx(const uint4& raw, uint8_t* codes, uint32_t tab, uint32_t e) {
+  const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+  uint32_t c[8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t eh = lds32(tab | ((w[i] >> 21) & 0x7FCu));
+    const uint32_t el = lds32(tab | ((w[i] >> 5) & 0x7FCu));
+    // bits 16..23 = 1.fraction of the high value, 0..7 of the low one, zeros elsewhere: each funnel shift
+    // only moves its own value's bits into the byte it reads (3 for high, 1 for low)
+    const uint32_t mm = and_or(w[i], 0x00800080u);
+    c[2 * i + 1] = eh | __funnelshift_r(0u, mm, eh);
+    c[2 * i] = el | __funnelshift_r(0u, mm, el);
+  }
+  *reinterpret_cast<uint2*>(codes + e) = make_uint2(
+      __byte_perm(__byte_perm(c[0], c[1], 0x0071), __byte_perm(c[2], c[3], 0x0071), 0x5410),
+      __byte_perm(__byte_perm(c[4], c[5], 0x0071), __byte_perm(c[6], c[7], 0x0071), 0x5410));
+}
+
+template <int DT>
+__global__ void __cluster_dims__(kGseQ, 1, 1) __launch_bounds__(kGseThreads, 5)
+    gse_slab_kernel(const __grid_constant__ QBatch p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  // [code-template table, 2 KB at a 2-KB-aligned address inside the first 4 KB][part | red | bar][source]
+  uint32_t* tab = reinterpret_cast<uint32_t*>(smem_raw + ((2048u - (smem_addr(smem_raw) & 2047u)) & 2047u));
+  int* part = reinterpret_cast<int*>(smem_raw + 4096);               // [kGseQ][2] quarter ranges (biased)
+  int* red = part + 2 * kGseQ;                                       // [warps][2] block reduction
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem_raw + 4096 + 256);
+  uint8_t* src_s = smem_raw + kGseHdr;                               // quarter of the slab's source
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t q = cluster_rank();
+  const uint32_t n_slabs = p.L * p.Hl;
+  const uint32_t cid = blockIdx.x / kGseQ, j = cid / n_slabs, slab_i = cid - j * n_slabs;
+  const uint32_t l = slab_i / p.Hl, hl = slab_i - l * p.Hl;
+  const uint32_t qe = p.slab / kGseQ;  // elements per quarter (multiple of 64)
+  const QJob& jb = p.jobs[j];
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    mbar_arrive_expect_tx(bar, 2 * qe);
+    bulk_g2s(src_s, jb.src + ((uint64_t)(l * p.H + p.h0 + hl) * p.slab + (uint64_t)q * qe), 2 * qe, bar);
+  }
+  mbar_wait(bar, 0);
+  // quarter range: min / max biased fp32 exponent over nonzero normals (as q_consume_range)
+  int emin = 255, emax = 0;
+  bool bad = false;
+  for (uint32_t e = tid * 8; e < qe; e += kGseThreads * 8) {
+    const uint4 raw = *reinterpret_cast<const uint4*>(src_s + 2 * e);
+    if constexpr (DT == HR_BF16) {
+      const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
+      uint32_t mx = 0u, mn = 0xFFFFFFFFu;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t mag = w[k] & 0x7FFF7FFFu;
+        mx = __vmaxu2(mx, mag);
+        mn = __vminu2(mn, (mag + 0x7F807F80u) ^ 0x80008000u);
+      }
+      const uint32_t pmax = max(mx & 0xFFFFu, mx >> 16), kmin = min(mn & 0xFFFFu, mn >> 16);
+      bad |= pmax >= 0x7F80u;
+      emax = max(emax, (int)(pmax >> 7));
+      if (kmin < 0x8000u) emin = min(emin, (int)((kmin + 0x80u) >> 7));
+    } else {
+      float2 x[4];
+      unpack8<DT>(raw, x);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t b = __float_as_uint(k & 1 ? x[k >> 1].y : x[k >> 1].x);
+        const int ef = (b >> 23) & 0xFF;
+        bad |= ef == 255;
+        if (ef != 0) emin = min(emin, ef), emax = max(emax, ef);
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    emin = min(emin, __shfl_xor_sync(0xFFFFFFFFu, emin, o));
+    emax = max(emax, __shfl_xor_sync(0xFFFFFFFFu, emax, o));
+  }
+  if (lane == 0) red[2 * warp] = emin, red[2 * warp + 1] = emax;
+  __syncthreads();
+  if (tid == 0) {
+    for (uint32_t w = 1; w < kGseThreads / 32; ++w) emin = min(emin, red[2 * w]), emax = max(emax, red[2 * w + 1]);
+    // (255 - min, max) as the range pass stores it: a quarter without normals contributes (0, 0)
+    const int a = emax != 0 ? 255 - emin : 0, b = emax;
+    for (uint32_t r = 0; r < kGseQ; ++r) st_cluster_v2(smem_addr(part + 2 * q), r, a, b);
+  }
+  cluster_sync();  // every quarter's range is in every CTA's `part`
+  int rng[2] = {0, 0};
+#pragma unroll
+  for (int r = 0; r < kGseQ; ++r) rng[0] = max(rng[0], part[2 * r]), rng[1] = max(rng[1], part[2 * r + 1]);
+  const int m = (int)p.gse_m, nmax = 1 << (7 - m);
+  const GseArr ga = gse_array(rng, m, nmax);
+  {  // code-template table, indexed by sign|exponent (512 entries, thread t builds t and 256 + t)
+    const int ef = (int)tid, step = m - 1;
+    uint32_t ent = 0;
+    if (ga.n > 0 && ef >= ga.rmin && ef <= min(ga.rmax, 254)) {
+      const int E = ef - 127;
+      const int idx = (E <= ga.lo) ? 0 : (E - ga.lo + step - 1) / step;
+      const int d = min(ga.lo + idx * step, ga.Emax) - E;
+      if (d <= m - 1) {
+        // bf16: sign-free template (the negative half of the table adds the sign); fp16 (enc_gse through
+        // fp32, sign combined per element): the "sign kept" bit of gse_build_table
+        const uint32_t t7 = (DT == HR_BF16 ? 0u : 0x80u) | ((uint32_t)idx << m);
+        ent = (t7 << 24) | (t7 << 8) | (uint32_t)(31 - (m - 1 - d));
+      }
+    }
+    tab[tid] = ent;                                   // positive (and ef = 0: 0)
+    tab[256 + tid] = ent ? ent | 0x80008000u : 0u;    // negative: the sign bit rides in the entry
+  }
+  uint8_t* meta = jb.dst + p.meta_off[HR_S_GSE8] + (uint64_t)slab_i * p.meta_stride[HR_S_GSE8];
+  if (q == 0 && warp == 0) gse_write_record(meta, p.meta_stride[HR_S_GSE8], ga, m, nmax, (int)lane);
+  __syncthreads();
+  uint8_t* codes = jb.dst + (uint64_t)slab_i * p.code_slab[HR_S_GSE8] + (uint64_t)q * qe;
+  const uint32_t taddr = smem_addr(tab);
+  if constexpr (DT == HR_BF16) {
+    for (uint32_t e = tid * 8; e < qe; e += kGseThreads * 8)
+      enc_gse_sx(*reinterpret_cast<const uint4*>(src_s + 2 * e), codes, taddr, e);
+  } else {  // fp16: through fp32 with the first 256 (sign-free) entries, signs combined per element
+    uint32_t nan_acc = 0;
+    for (uint32_t e = tid * 8; e < qe; e += kGseThreads * 8)
+      enc_gse<DT>(*reinterpret_cast<const uint4*>(src_s + 2 * e), codes, taddr, e, nan_acc);
+  }
+  if (bad) atomicOr(p.err, 1);
+}
+
 // ---------------------------------------------------------------- INT8 / INT4 (G > 256): warp per group
 __device__ __forceinline__ void load8(const uint16_t* p, int dt, float (&x)[8]) {
   const uint4 raw = __ldg(reinterpret_cast<const uint4*>(p));
@@ -825,8 +988,21 @@ void launch_quantize(const QuantParams* items, int n, cudaStream_t st) {
   // K+V pair is 67 MB of the 126 MB L2); every other item of the call shares one encode launch per
   // kQMaxJobs; INT8 / INT4 with G > 256 take the big-group kernel.
   QBatch rng = base, big = base, enc = base, gse = base;
+  const bool gse_single = 2ull * (slab / kGseQ) <= kGseQMaxBytes && ((slab / kGseQ) % 8) == 0;
   auto flush_gse = [&] {
     if (!gse.n_jobs) return;
+    if (gse_single) {  // one pass: a cluster of kGseQ CTAs per slab
+      const size_t smem = kGseHdr + 2 * (slab / kGseQ);
+      auto kern = gse.dtype == HR_BF16 ? gse_slab_kernel<HR_BF16> : gse_slab_kernel<HR_FP16>;
+      static bool init[2] = {false, false};
+      if (!init[gse.dtype == HR_BF16]) {
+        HR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kGseHdr + kGseQMaxBytes)));
+        init[gse.dtype == HR_BF16] = true;
+      }
+      kern<<<(unsigned)(gse.n_jobs * n_slabs * kGseQ), kGseThreads, smem, st>>>(gse);
+      gse.n_jobs = 0;
+      return;
+    }
     rng.n_jobs = 0;
     for (uint32_t j = 0; j < gse.n_jobs; ++j) {
       HR_CUDA(cudaMemsetAsync(gse.jobs[j].range, 0, sizeof(int) * 2 * n_slabs, st));
@@ -849,7 +1025,7 @@ void launch_quantize(const QuantParams* items, int n, cudaStream_t st) {
     if (q.scheme == HR_S_GSE8) {
       require(q.gse_range != nullptr, HR_EINVAL, "GSE-8 quantize needs range scratch");
       gse.jobs[gse.n_jobs++] = job;
-      if (gse.n_jobs == 2) flush_gse();
+      if (gse.n_jobs == (gse_single ? (uint32_t)kQMaxJobs : 2u)) flush_gse();
     } else if ((q.scheme == HR_S_INT8 || q.scheme == HR_S_INT4) && q.G > (uint32_t)kChunk) {
       big.jobs[big.n_jobs++] = job;
       if (big.n_jobs == kQMaxJobs) flush_big();
