@@ -153,7 +153,10 @@ constexpr int kSoftWarps = 8, kDecWarps = 4, kDecGroups = 2;
 constexpr int kAttThreads2 = 32 * (kSoftWarps + kDecGroups * kDecWarps + 1);
 constexpr uint32_t kDecChunks = kKT * 128 / 8 / (32 * kDecWarps);  // 8-element chunks per decoder thread at D = 128
 // per decoder group: codes slots [K, V][kDecChunks][thread] x 16 B, meta slots x 8 B
-constexpr uint32_t kStageBytes = 2 * kDecChunks * 32 * kDecWarps * (8 + 8);  // 8-B code + 8-B meta slots
+// per decoder group: codes slots [K, V][kDecChunks][thread] x 8 B, the tile's meta windows [K, V] x 2 KB
+// (<= 256 groups x 8 B), the doc's GSE-8 value tables [K, V][256] x 16-bit
+constexpr uint32_t kMetaWin = 2048;
+constexpr uint32_t kStageBytes = 2 * kDecChunks * 32 * kDecWarps * 8 + 2 * kMetaWin + 2 * 256 * 2;
 constexpr uint32_t kOpBufs = 4;  // K/V operand buffers: decode of tile j waits for PV_{j-4} only
 
 // The four bytes of w as exact floats (minus `bias`): 0x4B0000bb is 2^23 + bb, so one PRMT and one
@@ -238,10 +241,10 @@ __device__ __forceinline__ uint4 dec_raw8(uint32_t scheme, const uint4& c, const
 // resolved ONCE per tile: a runtime switch over compile-time-specialised loops (a per-chunk switch
 // made the decode loop branch-bound).  VMAJ: V's MN-major layout, else K's K-major layout.
 template <int DT, int SCH, bool VMAJ, uint32_t D>
-__device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, const uint8_t* __restrict__ stm,
-                                           const float* __restrict__ gt, uint32_t gse_m, uint8_t* __restrict__ dst,
-                                           uint32_t dt, uint16_t* __restrict__ dump, const uint8_t* __restrict__ g16,
-                                           uint32_t t0) {
+__device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, const uint8_t* __restrict__ smeta,
+                                           const uint16_t* __restrict__ vt, uint32_t g_shift, uint32_t g0,
+                                           uint8_t* __restrict__ dst, uint32_t dt, uint16_t* __restrict__ dump,
+                                           const uint8_t* __restrict__ g16, uint32_t t0) {
   constexpr uint32_t dcs = D / 8, nch = kKT * dcs / (32 * kDecWarps);
 #pragma unroll
   for (uint32_t i = 0; i < nch; ++i) {
@@ -250,12 +253,22 @@ __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, cons
       const uint32_t gI = cc >> 5, ii = cc & 7, jj = (cc >> 3) & 3;
       const uint32_t key = (gI % (kKT / 8)) * 8 + ii, dc = (gI / (kKT / 8)) * 4 + jj;
       uint4 v;
-      if (SCH == HR_S_PASS16) {  // bits unchanged: straight from global (L2-prefetched) into the operand tile
+      if constexpr (SCH == HR_S_PASS16) {  // bits unchanged: straight from global (L2-prefetched) into the operand tile
         v = __ldg(reinterpret_cast<const uint4*>(g16 + 2ull * ((t0 + key) * D + dc * 8)));
       } else {
         const uint2 raw = *reinterpret_cast<const uint2*>(stc + (i * 32 * kDecWarps + dt) * 8);
-        const float2 m = *reinterpret_cast<const float2*>(stm + (i * 32 * kDecWarps + dt) * 8);
-        v = dec_raw8<DT>(SCH, make_uint4(raw.x, raw.y, 0u, 0u), m, gse_m, gt);
+        if constexpr (SCH == HR_S_GSE8) {  // the slab's 256-entry table of decoded 16-bit values: one LDS.U16 per element
+          uint32_t h[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) h[k] = vt[((k < 4 ? raw.x : raw.y) >> (8 * (k & 3))) & 0xFFu];
+          v = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
+        } else {
+          float2 m = make_float2(0.f, 0.f);
+          const uint32_t g = ((((t0 + key) * D + dc * 8)) >> g_shift) - g0;  // group index in the tile window
+          if (SCH == HR_S_INT8) m.x = reinterpret_cast<const float*>(smeta)[g];
+          if (SCH == HR_S_INT4) m = reinterpret_cast<const float2*>(smeta)[g];
+          v = dec_raw8<DT>(SCH, make_uint4(raw.x, raw.y, 0u, 0u), m, 0u, nullptr);
+        }
       }
       if (VMAJ)
         *reinterpret_cast<uint4*>(dst + ((key / 8) * dcs + dc) * 128 + (key % 8) * 16) = v;
@@ -266,17 +279,19 @@ __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, cons
   }
 }
 template <int DT, bool VMAJ, uint32_t D>
-__device__ __forceinline__ void dec_tile(uint32_t scheme, const uint8_t* stc, const uint8_t* stm, const float* gt,
-                                         uint32_t gse_m, uint8_t* dst, uint32_t dt, uint16_t* dump,
+__device__ __forceinline__ void dec_tile(uint32_t scheme, const uint8_t* stc, const uint8_t* smeta, const uint16_t* vt,
+                                         uint32_t g_shift, uint32_t g0, uint8_t* dst, uint32_t dt, uint16_t* dump,
                                          const uint8_t* g16, uint32_t t0) {
+#define HR_DT(S) dec_tile_s<DT, S, VMAJ, D>(stc, smeta, vt, g_shift, g0, dst, dt, dump, g16, t0)
   switch (scheme) {
-    case HR_S_PASS16: return dec_tile_s<DT, HR_S_PASS16, VMAJ, D>(stc, stm, gt, gse_m, dst, dt, dump, g16, t0);
-    case HR_S_INT8: return dec_tile_s<DT, HR_S_INT8, VMAJ, D>(stc, stm, gt, gse_m, dst, dt, dump, g16, t0);
-    case HR_S_FP8E4M3: return dec_tile_s<DT, HR_S_FP8E4M3, VMAJ, D>(stc, stm, gt, gse_m, dst, dt, dump, g16, t0);
-    case HR_S_FP8E5M2: return dec_tile_s<DT, HR_S_FP8E5M2, VMAJ, D>(stc, stm, gt, gse_m, dst, dt, dump, g16, t0);
-    case HR_S_INT4: return dec_tile_s<DT, HR_S_INT4, VMAJ, D>(stc, stm, gt, gse_m, dst, dt, dump, g16, t0);
-    default: return dec_tile_s<DT, HR_S_GSE8, VMAJ, D>(stc, stm, gt, gse_m, dst, dt, dump, g16, t0);
+    case HR_S_PASS16: return HR_DT(HR_S_PASS16);
+    case HR_S_INT8: return HR_DT(HR_S_INT8);
+    case HR_S_FP8E4M3: return HR_DT(HR_S_FP8E4M3);
+    case HR_S_FP8E5M2: return HR_DT(HR_S_FP8E5M2);
+    case HR_S_INT4: return HR_DT(HR_S_INT4);
+    default: return HR_DT(HR_S_GSE8);
   }
+#undef HR_DT
 }
 
 // cp.async (LDGSTS) of one chunk's codes / group meta into this thread's staging slot: the loads of a
@@ -285,17 +300,26 @@ template <int N>
 __device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(saddr(smem)), "l"(gmem), "n"(N) : "memory");
 }
-__device__ __forceinline__ void stage_chunk(uint32_t scheme, const uint8_t* codes, const uint8_t* meta, uint32_t e,
-                                            uint32_t g_shift, uint8_t* sc, uint8_t* sm) {
+__device__ __forceinline__ void stage_chunk(uint32_t scheme, const uint8_t* codes, uint32_t e, uint8_t* sc) {
   if (scheme == HR_S_PASS16) {
     // copied straight into the operand buffer once it is free (dec_tile_s<PASS16>)
   } else if (scheme == HR_S_INT4) {
     cp_async<4>(sc, codes + e / 2);
-    cp_async<8>(sm, meta + 8ull * (e >> g_shift));
   } else {
     cp_async<8>(sc, codes + e);
-    if (scheme == HR_S_INT8) cp_async<4>(sm, meta + 4ull * (e >> g_shift));
   }
+}
+// the tile's window of group meta (INT8: fp32 scale, INT4: (scale, min) per group) -> shared memory,
+// 4-byte copies spread over the group's threads; returns the first group index of the window
+__device__ __forceinline__ uint32_t stage_meta(uint32_t scheme, const uint8_t* meta, uint32_t t0, uint32_t D,
+                                               uint32_t g_shift, uint8_t* sm, uint32_t dt) {
+  const uint32_t g0 = (t0 * D) >> g_shift;
+  if (scheme != HR_S_INT8 && scheme != HR_S_INT4) return g0;
+  const uint32_t me = scheme == HR_S_INT8 ? 4u : 8u;
+  const uint32_t g1 = ((t0 + kKT) * D - 1) >> g_shift;  // last group of the tile
+  const uint32_t words = (g1 - g0 + 1) * me / 4;
+  for (uint32_t w = dt; w < words; w += 32 * kDecWarps) cp_async<4>(sm + 4 * w, meta + (uint64_t)g0 * me + 4 * w);
+  return g0;
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -313,8 +337,8 @@ __device__ __forceinline__ void stage_chunk(uint32_t scheme, const uint8_t* code
 constexpr uint32_t kPF = 4;  // L2 prefetch distance in tiles
 
 size_t att_smem_bytes(uint32_t D) {
-  return (size_t)kRows * D * 2 + kOpBufs * 2 * (size_t)kKT * D * 2 + 4 * 32 * 4 + 16 * 8 + 16 +
-         kDecGroups * kStageBytes + 2 * 2 * kRows * 4;
+  return (size_t)kRows * D * 2 + kOpBufs * 2 * (size_t)kKT * D * 2 + 16 * 8 + 16 + kDecGroups * kStageBytes +
+         2 * 2 * kRows * 4;
 }
 
 // 2^x on the SFU (MUFU.EX2, relative error ~2^-22, far inside R28's 2^-9 budget)
@@ -387,8 +411,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
   uint8_t* skb = sq + kRows * D * 2;               // kOpBufs x [64 keys][D] K-major (B of S = Q K^T)
   uint8_t* svb = skb + kOpBufs * kKT * D * 2;      // kOpBufs x [64 keys][D] MN-major (B of O += P V)
   // P_j lives in TMEM, packed over the first 32 columns of S buffer j & 1 (the A operand of O += P V)
-  float* gtab = reinterpret_cast<float*>(svb + kOpBufs * kKT * D * 2);  // [group][2][32] GSE tables (K, V)
-  uint64_t* bar = reinterpret_cast<uint64_t*>(gtab + 128);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(svb + kOpBufs * kKT * D * 2);
   static_assert(4 + 2 * kOpBufs + 4 <= 16, "mbarrier slots");
   uint64_t *sf = bar, *pf = bar + 2, *kvf = bar + 4, *kve = kvf + kOpBufs, *od = kve + kOpBufs, *qf = od + 1;
   uint64_t* pfree = qf + 1;  // [2]: PV_j done (P_j consumed)
@@ -538,7 +561,6 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     // ------------------------------------------------------------------ decoder warps
     const uint32_t grp = (uint32_t)(warp - kSoftWarps) / kDecWarps;   // tiles j with j & 1 == grp
     const uint32_t dt = tid - 32 * kSoftWarps - 32 * kDecWarps * grp;  // 0..127 within the group
-    float* gt = gtab + 64 * grp;
     auto tile_src = [&](uint32_t j, const AsmDesc*& dk, const AsmDesc*& dv, uint32_t& t0) {
       const uint32_t slot = j / tiles_per_doc;
       t0 = (j - slot * tiles_per_doc) * kKT;
@@ -572,7 +594,10 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       const uint32_t slot = j / tiles_per_doc;
       // all of this thread's loads in flight at once: cp.async into its own staging slots
       uint8_t* stc = stage0 + grp * kStageBytes;                         // [K, V][i][dt] x 8 B codes
-      uint8_t* stm = stc + 2 * kDecChunks * 32 * kDecWarps * 8;           // [K, V][i][dt] x 8 B meta
+      uint8_t* smk = stc + 2 * kDecChunks * 32 * kDecWarps * 8;           // K meta window
+      uint8_t* smv = smk + kMetaWin;                                      // V meta window
+      uint16_t* vtk = reinterpret_cast<uint16_t*>(smv + kMetaWin);        // [256] K value table
+      uint16_t* vtv = vtk + 256;                                          // [256] V value table
 #pragma unroll
       for (uint32_t i = 0; i < kKT * dcs / (32 * kDecWarps); ++i) {
         const uint32_t cc = dt + i * 32 * kDecWarps;
@@ -581,28 +606,38 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
           const uint32_t key = (gI % (kKT / 8)) * 8 + ii, dc = (gI / (kKT / 8)) * 4 + jj;
           const uint32_t e = (t0 + key) * D + dc * 8;
           const uint32_t sl = i * 32 * kDecWarps + dt;
-          stage_chunk(dk.scheme, kc, km, e, p.g_shift, stc + sl * 8, stm + sl * 8);
-          stage_chunk(dv.scheme, vc, vm, e, p.g_shift, stc + (kDecChunks * 32 * kDecWarps + sl) * 8,
-                      stm + (kDecChunks * 32 * kDecWarps + sl) * 8);
+          stage_chunk(dk.scheme, kc, e, stc + sl * 8);
+          stage_chunk(dv.scheme, vc, e, stc + (kDecChunks * 32 * kDecWarps + sl) * 8);
         }
       }
+      // (the previous tile's decode is done with the meta windows: the kvf arrive of that tile followed it
+      // in every thread, and the named barrier below orders the group)
+      named_bar(1 + grp, 32 * kDecWarps);
+      const uint32_t gk0 = stage_meta(dk.scheme, km, t0, D, p.g_shift, smk, dt);
+      const uint32_t gv0 = stage_meta(dv.scheme, vm, t0, D, p.g_shift, smv, dt);
       asm volatile("cp.async.commit_group;" ::: "memory");
-      if (slot != cur_slot) {  // new doc: stage the GSE decode tables of its K and V slab (this group only)
+      if (slot != cur_slot) {  // new doc: the GSE-8 value tables of its K and V slab (this group only)
         cur_slot = slot;
-        named_bar(1 + grp, 32 * kDecWarps);
-        if (dt < 64) {
-          const bool isv = dt >= 32;
-          const AsmDesc& d = isv ? dv : dk;
-          const uint8_t* m = isv ? vm : km;
-          const uint32_t i = dt & 31;
-          gt[dt] = (d.scheme == HR_S_GSE8 && i < (2u << p.gse_e)) ? reinterpret_cast<const float*>(m + 16)[i] : 0.f;
+        const uint32_t fm = (1u << p.gse_m) - 1u;
+#pragma unroll
+        for (uint32_t x = 0; x < 2; ++x) {  // thread dt builds bytes dt and dt + 128 of K and of V
+          const uint32_t byte = dt + 128 * x;
+#pragma unroll
+          for (uint32_t kv = 0; kv < 2; ++kv) {
+            const AsmDesc& d = kv ? dv : dk;
+            if (d.scheme != HR_S_GSE8) continue;
+            const float T = __ldg(reinterpret_cast<const float*>((kv ? vm : km) + 16) + (byte >> p.gse_m));
+            // fma(f, T, +0): the decode of hr_assemble_kv (a (sign 1, field 0) byte gives +0), then RNE
+            const float f = __fmaf_rn((float)(byte & fm), T, 0.f);
+            (kv ? vtv : vtk)[byte] = (uint16_t)(pack2<DT>(f, 0.f) & 0xFFFFu);
+          }
         }
-        named_bar(1 + grp, 32 * kDecWarps);
       }
       if (dt == 0) TR(6, j);
       if (use >= 1) MBW(&kve[b], (use - 1) & 1, 3, j);  // PV_{j-3} (and S_{j-3}) done: buffer b free
       if (dt == 0) TR(2, j);
       asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's staged chunks have landed
+      named_bar(1 + grp, 32 * kDecWarps);               // ... and every thread's meta / value-table share
       if (dt == 0) TR(7, j);
       uint8_t* skd = skb + b * (kKT * D * 2);
       uint8_t* svd = svb + b * (kKT * D * 2);
@@ -612,8 +647,8 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
           dump = p.kv_dump + ((((uint64_t)r * 2) * p.L + l) * p.Hl + h) * p.k * p.T * D + ((uint64_t)slot * p.T + t0) * D;
         const uint64_t kvoff = (uint64_t)p.L * p.Hl * p.k * p.T * D;
         const uint32_t vo = kDecChunks * 32 * kDecWarps;
-        dec_tile<DT, false, D>(dk.scheme, stc, stm, gt, p.gse_m, skd, dt, dump, kc, t0);
-        dec_tile<DT, true, D>(dv.scheme, stc + vo * 8, stm + vo * 8, gt + 32, p.gse_m, svd, dt,
+        dec_tile<DT, false, D>(dk.scheme, stc, smk, vtk, p.g_shift, gk0, skd, dt, dump, kc, t0);
+        dec_tile<DT, true, D>(dv.scheme, stc + vo * 8, smv, vtv, p.g_shift, gv0, svd, dt,
                               dump ? dump + kvoff : nullptr, vc, t0);
       }
       fence_async_smem();
