@@ -349,7 +349,7 @@ def run_per_scheme(ctx, wl, args):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         e0.record(ctx.stream)
-        QB = 8   # docs per hr_build_put_batch call (one quantize launch of 16 items)
+        QB = 16  # docs per hr_build_put_batch call (one quantize launch of 32 items)
         for d in range(0, n_docs, QB):
             nd = min(QB, n_docs - d)
             st.build_put_batch(range(d, d + nd), [src[(d + i) % NS, 0] for i in range(nd)],

@@ -22,7 +22,7 @@ st = hr.Store(L=L, H=H, D=D, T=T, ladder=(scheme,), taus=(), keep_backing=False,
               hbm_budget=2 * n_docs * item + (1 << 20))
 st.build_begin(n_docs, np.zeros(2 * n_docs, np.uint64))
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-QB = int(os.environ.get("HARAG_PUT_BATCH", "8"))  # docs per hr_build_put_batch (one launch)
+QB = int(os.environ.get("HARAG_PUT_BATCH", "16"))  # docs per hr_build_put_batch (one launch)
 st.build_put_batch(range(min(QB, n_docs)), [src[i % NS, 0] for i in range(min(QB, n_docs))],
                    [src[i % NS, 1] for i in range(min(QB, n_docs))])  # warm-up (module load, first touch)
 torch.cuda.synchronize()
