@@ -706,7 +706,7 @@ __global__ void __launch_bounds__(kQThreadsB, 1) quantize_batch_kernel(const __g
 // from shared memory.  The source is read from HBM once; many small CTAs per SM overlap the copies
 // with the encode.  Used when a quarter slab fits kGseQMaxBytes (every Llama shape).
 constexpr int kGseQ = 4;                  // CTAs per cluster (= slab quarters)
-constexpr int kGseThreads = 256;
+constexpr int kGseThreads = 128;  // 128 elements per thread at Llama shapes: amortises the per-slab setup
 constexpr uint32_t kGseQMaxBytes = 64 * 1024;
 constexpr uint32_t kGseHdr = 8192;  // table + exchange + barrier
 
@@ -782,21 +782,17 @@ __global__ void __cluster_dims__(kGseQ, 1, 1) __launch_bounds__(kGseThreads, 5)
   // quarter range: min / max biased fp32 exponent over nonzero normals (as q_consume_range)
   int emin = 255, emax = 0;
   bool bad = false;
+  uint32_t mx = 0u, mn = 0xFFFFFFFFu;  // bf16: running 16-bit-pair max magnitude / min normal key
   for (uint32_t e = tid * 8; e < qe; e += kGseThreads * 8) {
     const uint4 raw = *reinterpret_cast<const uint4*>(src_s + 2 * e);
     if constexpr (DT == HR_BF16) {
       const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
-      uint32_t mx = 0u, mn = 0xFFFFFFFFu;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         const uint32_t mag = w[k] & 0x7FFF7FFFu;
         mx = __vmaxu2(mx, mag);
         mn = __vminu2(mn, (mag + 0x7F807F80u) ^ 0x80008000u);
       }
-      const uint32_t pmax = max(mx & 0xFFFFu, mx >> 16), kmin = min(mn & 0xFFFFu, mn >> 16);
-      bad |= pmax >= 0x7F80u;
-      emax = max(emax, (int)(pmax >> 7));
-      if (kmin < 0x8000u) emin = min(emin, (int)((kmin + 0x80u) >> 7));
     } else {
       float2 x[4];
       unpack8<DT>(raw, x);
@@ -808,6 +804,12 @@ __global__ void __cluster_dims__(kGseQ, 1, 1) __launch_bounds__(kGseThreads, 5)
         if (ef != 0) emin = min(emin, ef), emax = max(emax, ef);
       }
     }
+  }
+  if constexpr (DT == HR_BF16) {
+    const uint32_t pmax = max(mx & 0xFFFFu, mx >> 16), kmin = min(mn & 0xFFFFu, mn >> 16);
+    bad |= pmax >= 0x7F80u;
+    emax = (int)(pmax >> 7);
+    if (kmin < 0x8000u) emin = (int)((kmin + 0x80u) >> 7);
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
@@ -828,12 +830,16 @@ __global__ void __cluster_dims__(kGseQ, 1, 1) __launch_bounds__(kGseThreads, 5)
   for (int r = 0; r < kGseQ; ++r) rng[0] = max(rng[0], part[2 * r]), rng[1] = max(rng[1], part[2 * r + 1]);
   const int m = (int)p.gse_m, nmax = 1 << (7 - m);
   const GseArr ga = gse_array(rng, m, nmax);
-  {  // code-template table, indexed by sign|exponent (512 entries, thread t builds t and 256 + t)
-    const int ef = (int)tid, step = m - 1;
+  // code-template table, indexed by sign|exponent (512 entries; thread t builds exponents t, t + 128, ...
+  // and their negative copies).  idx = ceil((E - lo) / step) by a multiply-shift (exact for numerators
+  // below 4096 and step 2..4, checked exhaustively offline)
+  const uint32_t inv_step = (65536u + (uint32_t)(m - 1) - 1u) / (uint32_t)(m - 1);
+  for (int ef = (int)tid; ef < 256; ef += kGseThreads) {
+    const int step = m - 1;
     uint32_t ent = 0;
     if (ga.n > 0 && ef >= ga.rmin && ef <= min(ga.rmax, 254)) {
       const int E = ef - 127;
-      const int idx = (E <= ga.lo) ? 0 : (E - ga.lo + step - 1) / step;
+      const int idx = (E <= ga.lo) ? 0 : (int)(((uint32_t)(E - ga.lo + step - 1) * inv_step) >> 16);
       const int d = min(ga.lo + idx * step, ga.Emax) - E;
       if (d <= m - 1) {
         // bf16: sign-free template (the negative half of the table adds the sign); fp16 (enc_gse through
@@ -842,8 +848,8 @@ __global__ void __cluster_dims__(kGseQ, 1, 1) __launch_bounds__(kGseThreads, 5)
         ent = (t7 << 24) | (t7 << 8) | (uint32_t)(31 - (m - 1 - d));
       }
     }
-    tab[tid] = ent;                                   // positive (and ef = 0: 0)
-    tab[256 + tid] = ent ? ent | 0x80008000u : 0u;    // negative: the sign bit rides in the entry
+    tab[ef] = ent;                                    // positive (and ef = 0: 0)
+    tab[256 + ef] = ent ? ent | 0x80008000u : 0u;     // negative: the sign bit rides in the entry
   }
   uint8_t* meta = jb.dst + p.meta_off[HR_S_GSE8] + (uint64_t)slab_i * p.meta_stride[HR_S_GSE8];
   if (q == 0 && warp == 0) gse_write_record(meta, p.meta_stride[HR_S_GSE8], ga, m, nmax, (int)lane);
