@@ -149,7 +149,24 @@ __device__ __forceinline__ float hi_f(uint32_t w) {
   return DT == HR_BF16 ? __uint_as_float(w & 0xFFFF0000u) : __half2float(__ushort_as_half((unsigned short)(w >> 16)));
 }
 
-constexpr int kSoftWarps = 8, kDecWarps = 4, kDecGroups = 2;
+#ifndef HARAG_ATT_SOFT_WARPS
+#define HARAG_ATT_SOFT_WARPS 4
+#endif
+#ifndef HARAG_ATT_DEC_WARPS
+#define HARAG_ATT_DEC_WARPS 8
+#endif
+#ifndef HARAG_ATT_DEC_GROUPS
+#define HARAG_ATT_DEC_GROUPS 2
+#endif
+// measured (tools/prof_attend.py 8, C2 shape): 4 softmax + 2 x 8 decoder warps 2.40 ms; 4 + 2 x 4: 2.53 ms;
+// 8 + 2 x 4: 2.63 ms; 4 + 1 x 8: 2.89 ms;
+// 4 + 3 x 4: 2.59 ms (more warps = fewer registers per thread)
+constexpr int kSoftWarps = HARAG_ATT_SOFT_WARPS, kDecWarps = HARAG_ATT_DEC_WARPS, kDecGroups = HARAG_ATT_DEC_GROUPS;
+constexpr int kNH = kSoftWarps / 4;        // column parts per 32-row quadrant (1 or 2)
+constexpr uint32_t kCW = 64 / kNH;         // S columns per softmax warp (kKT = 64)
+// The P pass reloads S 32 columns at a time and writes P over the S buffer's first 32 columns: with one
+// column part per row quadrant a warp only overwrites S columns it has already consumed.
+static_assert(kNH == 1, "two column parts would overwrite each other's S columns before the reload");
 constexpr int kAttThreads2 = 32 * (kSoftWarps + kDecGroups * kDecWarps + 1);
 constexpr uint32_t kDecChunks = kKT * 128 / 8 / (32 * kDecWarps);  // 8-element chunks per decoder thread at D = 128
 // per decoder group: codes slots [K, V][kDecChunks][thread] x 16 B, meta slots x 8 B
@@ -485,16 +502,25 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       MBW(&sf[b], (j >> 1) & 1, 1, j);
       if (tid == 0) TR(0, j);
       tc_after();
-      uint32_t sv[32];
-      tmem_ld32(tmem + b * kKT + hf * 32 + lane_base, sv);
-      if (tid == 0) TR(8, j);
-      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // independent chains (ILP)
+      // row max over this warp's kCW columns, 32 at a time (register pressure: the P pass reloads them)
+      float pm = -INFINITY;
 #pragma unroll
-      for (int q = 0; q < 32; ++q) mx4[q & 3] = fmaxf(mx4[q & 3], __uint_as_float(sv[q]));
-      rmax[(j & 1) * 256 + hf * 128 + t] = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
-      named_bar(3, 32 * kSoftWarps);  // double-buffered slots: a warp cannot overwrite before its partner read
+      for (uint32_t q = 0; q < kCW / 32; ++q) {
+        uint32_t sv[32];
+        tmem_ld32(tmem + b * kKT + hf * kCW + 32 * q + lane_base, sv);
+        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // independent chains (ILP)
+#pragma unroll
+        for (uint32_t u = 0; u < 32; ++u) mx4[u & 3] = fmaxf(mx4[u & 3], __uint_as_float(sv[u]));
+        pm = fmaxf(pm, fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])));
+      }
+      if (tid == 0) TR(8, j);
+      if constexpr (kNH > 1) {
+        rmax[(j & 1) * 256 + hf * 128 + t] = pm;
+        named_bar(15, 32 * kSoftWarps);  // double-buffered slots: a warp cannot overwrite before its partner read
+        pm = fmaxf(rmax[(j & 1) * 256 + t], rmax[(j & 1) * 256 + 128 + t]);
+      }
       if (tid == 0) TR(9, j);
-      const float mt = fmaxf(rmax[(j & 1) * 256 + t], rmax[(j & 1) * 256 + 128 + t]) * c;  // c > 0
+      const float mt = pm * c;  // c > 0: max(s) c = max(s c)
       const bool grow = mt > m_ref + 8.f;  // lazy rescale: p stays <= 2^8 between rescales
       if (tid == 0) TR(10, j);
       if (__any_sync(0xFFFFFFFFu, grow) && j > 0) {
@@ -504,7 +530,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         MBW(od, (j - 1) & 1, 2, j);
         tc_after();
         const float alpha = grow ? ex2(m_ref - mt) : 1.f;
-        for (uint32_t cb = hf * (D / 2); cb < (hf + 1) * (D / 2); cb += 32) {
+        for (uint32_t cb = hf * (D / kNH); cb < (hf + 1) * (D / kNH); cb += 32) {
           uint32_t ov[32];
           tmem_ld32(t_o + lane_base + cb, ov);
 #pragma unroll
@@ -514,16 +540,22 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         lsum *= alpha;
       }
       if (grow) m_ref = mt;
-      uint32_t w[16];  // keys 32 hf + 2i, + 1 packed in column 16 hf + i of the S buffer (S reads are done:
-      float ls4[4] = {0.f, 0.f, 0.f, 0.f};  // both halves passed the max exchange)
+      // keys kCW hf + 2i, + 1 packed in column kCW/2 hf + i of the S buffer (S reads are done: with two
+      // column parts both passed the max exchange; within a warp the chunk q reload precedes its store)
+      float ls4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const float p0 = ex2(__fmaf_rn(__uint_as_float(sv[2 * i]), c, -m_ref));
-        const float p1 = ex2(__fmaf_rn(__uint_as_float(sv[2 * i + 1]), c, -m_ref));
-        w[i] = pack2<DT>(p0, p1);
-        ls4[i & 3] += lo_f<DT>(w[i]) + hi_f<DT>(w[i]);  // normalise by the rounded weights actually used
+      for (uint32_t q = 0; q < kCW / 32; ++q) {
+        uint32_t sv[32], w[16];
+        tmem_ld32(tmem + b * kKT + hf * kCW + 32 * q + lane_base, sv);
+#pragma unroll
+        for (uint32_t i = 0; i < 16; ++i) {
+          const float p0 = ex2(__fmaf_rn(__uint_as_float(sv[2 * i]), c, -m_ref));
+          const float p1 = ex2(__fmaf_rn(__uint_as_float(sv[2 * i + 1]), c, -m_ref));
+          w[i] = pack2<DT>(p0, p1);
+          ls4[i & 3] += lo_f<DT>(w[i]) + hi_f<DT>(w[i]);  // normalise by the rounded weights actually used
+        }
+        tmem_st16(tmem + b * kKT + hf * (kCW / 2) + 16 * q + lane_base, w);
       }
-      tmem_st16(tmem + b * kKT + hf * 16 + lane_base, w);
       lsum += (ls4[0] + ls4[1]) + (ls4[2] + ls4[3]);
       if (tid == 0) TR(11, j);
       tc_before();
@@ -532,16 +564,19 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       if (tid == 0) TR(1, j);
     }
     // epilogue: O / l -> output dtype; LSE (natural log) = ln 2 * (m_ref + log2 l), l = sum of both halves
-    const uint32_t es = (n_tiles & 1) * 256;  // the slot the last tile's exchange did not use
-    rmax[es + hf * 128 + t] = lsum;
-    named_bar(3, 32 * kSoftWarps);
-    const float ltot = rmax[es + t] + rmax[es + 128 + t];
+    float ltot = lsum;
+    if constexpr (kNH > 1) {
+      const uint32_t es = (n_tiles & 1) * 256;  // the slot the last tile's exchange did not use
+      rmax[es + hf * 128 + t] = lsum;
+      named_bar(15, 32 * kSoftWarps);
+      ltot = rmax[es + t] + rmax[es + 128 + t];
+    }
     // PV_{n-1} done (its commit covers every earlier MMA); the per-buffer barrier has completed at least
     // PV_{n-3}'s phase, so its parity cannot alias
     if (n_tiles) MBW(&pfree[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1, 8, n_tiles);
     tc_after();
     const float inv = 1.f / ltot;
-    for (uint32_t cb = hf * (D / 2); cb < (hf + 1) * (D / 2); cb += 32) {
+    for (uint32_t cb = hf * (D / kNH); cb < (hf + 1) * (D / kNH); cb += 32) {
       uint32_t ov[32];
       tmem_ld32(t_o + lane_base + cb, ov);
       if (t < p.M) {
@@ -559,7 +594,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     if (hf == 0 && t < p.M && p.lse) p.lse[row0 + t] = 0.69314718055994531f * (m_ref + __log2f(ltot));
   } else if (warp < kSoftWarps + kDecGroups * kDecWarps) {
     // ------------------------------------------------------------------ decoder warps
-    const uint32_t grp = (uint32_t)(warp - kSoftWarps) / kDecWarps;   // tiles j with j & 1 == grp
+    const uint32_t grp = (uint32_t)(warp - kSoftWarps) / kDecWarps;   // tiles j with j % kDecGroups == grp
     const uint32_t dt = tid - 32 * kSoftWarps - 32 * kDecWarps * grp;  // 0..127 within the group
     auto tile_src = [&](uint32_t j, const AsmDesc*& dk, const AsmDesc*& dv, uint32_t& t0) {
       const uint32_t slot = j / tiles_per_doc;
@@ -619,9 +654,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       if (slot != cur_slot) {  // new doc: the GSE-8 value tables of its K and V slab (this group only)
         cur_slot = slot;
         const uint32_t fm = (1u << p.gse_m) - 1u;
-#pragma unroll
-        for (uint32_t x = 0; x < 2; ++x) {  // thread dt builds bytes dt and dt + 128 of K and of V
-          const uint32_t byte = dt + 128 * x;
+        for (uint32_t byte = dt; byte < 256; byte += 32 * kDecWarps) {  // bytes dt, dt + group size, ...
 #pragma unroll
           for (uint32_t kv = 0; kv < 2; ++kv) {
             const AsmDesc& d = kv ? dv : dk;
