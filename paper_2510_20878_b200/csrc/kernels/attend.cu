@@ -156,9 +156,10 @@ __device__ __forceinline__ float hi_f(uint32_t w) {
 #define HARAG_ATT_DEC_WARPS 8
 #endif
 #ifndef HARAG_ATT_DEC_GROUPS
-#define HARAG_ATT_DEC_GROUPS 2
+#define HARAG_ATT_DEC_GROUPS 3
 #endif
-// measured (tools/prof_attend.py 8, C2 shape): 4 softmax + 2 x 8 decoder warps 2.40 ms; 4 + 2 x 4: 2.53 ms;
+// measured (tools/prof_attend.py 8, C2 shape): 4 softmax + 3 x 8 decoder warps 2.14 ms; 4 + 2 x 8: 2.38 ms;
+// 4 + 2 x 4: 2.53 ms;
 // 8 + 2 x 4: 2.63 ms; 4 + 1 x 8: 2.89 ms;
 // 4 + 3 x 4: 2.59 ms (more warps = fewer registers per thread)
 constexpr int kSoftWarps = HARAG_ATT_SOFT_WARPS, kDecWarps = HARAG_ATT_DEC_WARPS, kDecGroups = HARAG_ATT_DEC_GROUPS;
