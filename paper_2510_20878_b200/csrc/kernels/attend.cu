@@ -11,17 +11,16 @@
 // P:316); LSE lets a caller merge it with the question's own causal part.
 //
 // sm_100a design: one CTA per (request, layer, KV head) unit,
-// warp-specialised — 8 softmax warps, 2 groups of 4 decoder warps and one MMA
+// warp-specialised — 4 softmax warps, 3 groups of 8 decoder warps and one MMA
 // issuer lane.  The unit's M = g*n_q <= 128 query rows are the A operand of
 // tcgen05.mma (M = 128, rows past M zero); per 64-key tile the decoders stage
 // the packed codes with cp.async (L2-prefetched ahead) and decode them, bit
 // for bit as hr_assemble_kv, into one of four K/V operand buffers; S = Q K^T
-// accumulates in one of two TMEM buffers; the softmax warps (thread = row,
-// two warps per row quadrant splitting the columns) run the online softmax
-// with a lazy O rescale and write P (16-bit) back into the S buffer's TMEM
-// columns; O += P V takes A from TMEM.  Q and K use 128-byte-swizzled K-major
-// shared-memory tiles, V the canonical no-swizzle MN-major layout (8 rows x
-// 16 B per core matrix).  Debug builds: -DHARAG_ATT_TRACE (per-tile clock64
+// accumulates in one of two TMEM buffers; the softmax warps (thread = row)
+// run the online softmax with a lazy O rescale and write P (16-bit) back into
+// the S buffer's TMEM columns; O += P V takes A from TMEM.  Q and K use
+// 128-byte-swizzled K-major shared-memory tiles, V the canonical no-swizzle
+// MN-major layout (8 rows x // 16 B per core matrix).  Debug builds: -DHARAG_ATT_TRACE (per-tile clock64
 // events of CTA 0), -DHARAG_ATT_WATCHDOG (mbarrier waits that report and trap),
 // -DHARAG_ATT_MMASYNC (MMA latency in isolation).
 #include <cuda_bf16.h>
