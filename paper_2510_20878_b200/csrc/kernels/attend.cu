@@ -20,9 +20,10 @@
 // run the online softmax with a lazy O rescale and write P (16-bit) back into
 // the S buffer's TMEM columns; O += P V takes A from TMEM.  Q and K use
 // 128-byte-swizzled K-major shared-memory tiles, V the canonical no-swizzle
-// MN-major layout (8 rows x // 16 B per core matrix).  Debug builds: -DHARAG_ATT_TRACE (per-tile clock64
-// events of CTA 0), -DHARAG_ATT_WATCHDOG (mbarrier waits that report and trap),
-// -DHARAG_ATT_MMASYNC (MMA latency in isolation).
+// MN-major layout (8 rows x 16 B per core matrix).  Debug builds:
+// -DHARAG_ATT_TRACE (per-tile clock64 events of CTA 0), -DHARAG_ATT_WATCHDOG
+// (mbarrier waits that report and trap), -DHARAG_ATT_MMASYNC (MMA latency in
+// isolation).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_fp8.h>
