@@ -165,9 +165,10 @@ __device__ __forceinline__ float hi_f(uint32_t w) {
 constexpr int kSoftWarps = HARAG_ATT_SOFT_WARPS, kDecWarps = HARAG_ATT_DEC_WARPS, kDecGroups = HARAG_ATT_DEC_GROUPS;
 constexpr int kNH = kSoftWarps / 4;        // column parts per 32-row quadrant (1 or 2)
 constexpr uint32_t kCW = 64 / kNH;         // S columns per softmax warp (kKT = 64)
-// The P pass reloads S 32 columns at a time and writes P over the S buffer's first 32 columns: with one
-// column part per row quadrant a warp only overwrites S columns it has already consumed.
-static_assert(kNH == 1, "two column parts would overwrite each other's S columns before the reload");
+// With one column part per row quadrant (kNH = 1) the P pass reloads S 32 columns at a time (fewer
+// registers) and writes P over the S buffer's first 32 columns, which only this warp has read.  With two
+// parts each warp keeps its 32 S columns in registers: P is stored only after both passed the max
+// exchange, i.e. after every S read of the tile.
 constexpr int kAttThreads2 = 32 * (kSoftWarps + kDecGroups * kDecWarps + 1);
 constexpr uint32_t kDecChunks = kKT * 128 / 8 / (32 * kDecWarps);  // 8-element chunks per decoder thread at D = 128
 // per decoder group: codes slots [K, V][kDecChunks][thread] x 16 B, meta slots x 8 B
@@ -503,11 +504,11 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       MBW(&sf[b], (j >> 1) & 1, 1, j);
       if (tid == 0) TR(0, j);
       tc_after();
-      // row max over this warp's kCW columns, 32 at a time (register pressure: the P pass reloads them)
+      // row max over this warp's kCW columns, 32 at a time (kNH = 1: the P pass reloads them)
       float pm = -INFINITY;
+      uint32_t sv[32];
 #pragma unroll
       for (uint32_t q = 0; q < kCW / 32; ++q) {
-        uint32_t sv[32];
         tmem_ld32(tmem + b * kKT + hf * kCW + 32 * q + lane_base, sv);
         float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // independent chains (ILP)
 #pragma unroll
@@ -546,8 +547,8 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       float ls4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
       for (uint32_t q = 0; q < kCW / 32; ++q) {
-        uint32_t sv[32], w[16];
-        tmem_ld32(tmem + b * kKT + hf * kCW + 32 * q + lane_base, sv);
+        uint32_t w[16];
+        if (kNH == 1) tmem_ld32(tmem + b * kKT + hf * kCW + 32 * q + lane_base, sv);
 #pragma unroll
         for (uint32_t i = 0; i < 16; ++i) {
           const float p0 = ex2(__fmaf_rn(__uint_as_float(sv[2 * i]), c, -m_ref));
