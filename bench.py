@@ -335,7 +335,7 @@ def run_per_scheme(ctx, wl, args):
     B, k, n_docs = 16, wl["k"], 400
     L, H, D, T = wl["L"], wl["H"], wl["D"], wl["T"]
     geo = dict(L=L, H=H, D=D, T=T, dtype=wl["dtype"], rank=ctx.rank, world=ctx.world)
-    NS = 8   # distinct source docs cycled through the puts: 8 x K+V >> L2, so every source read is an HBM read
+    NS = 16  # distinct source docs = docs per launch (16 x K+V = 2.1 GB >> L2): no two jobs of a launch share a source, every source read is an HBM read
     src = torch.empty(NS, 2, L * H * T * D, dtype=torch.int16, device="cuda")
     for i in range(NS):
         synth.gen_item_device(src[i, 0].data_ptr(), L, H, T, D, i, 0, dtype=wl["dtype"])
