@@ -544,21 +544,22 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       if (grow) m_ref = mt;
       // keys kCW hf + 2i, + 1 packed in column kCW/2 hf + i of the S buffer (S reads are done: with two
       // column parts both passed the max exchange; within a warp the chunk q reload precedes its store)
-      float ls4[4] = {0.f, 0.f, 0.f, 0.f};
+      float2 ls2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};  // (even, odd) keys, two chains
+      const float2 c2 = make_float2(c, c), nm2 = make_float2(-m_ref, -m_ref);
 #pragma unroll
       for (uint32_t q = 0; q < kCW / 32; ++q) {
         uint32_t w[16];
         if (kNH == 1) tmem_ld32(tmem + b * kKT + hf * kCW + 32 * q + lane_base, sv);
 #pragma unroll
         for (uint32_t i = 0; i < 16; ++i) {
-          const float p0 = ex2(__fmaf_rn(__uint_as_float(sv[2 * i]), c, -m_ref));
-          const float p1 = ex2(__fmaf_rn(__uint_as_float(sv[2 * i + 1]), c, -m_ref));
-          w[i] = pack2<DT>(p0, p1);
-          ls4[i & 3] += lo_f<DT>(w[i]) + hi_f<DT>(w[i]);  // normalise by the rounded weights actually used
+          const float2 x = __ffma2_rn(make_float2(__uint_as_float(sv[2 * i]), __uint_as_float(sv[2 * i + 1])), c2, nm2);
+          w[i] = pack2<DT>(ex2(x.x), ex2(x.y));
+          // normalise by the rounded weights actually used: both 16-bit halves as exact fp32 values
+          ls2[i & 1] = __fadd2_rn(ls2[i & 1], make_float2(lo_f<DT>(w[i]), hi_f<DT>(w[i])));
         }
         tmem_st16(tmem + b * kKT + hf * (kCW / 2) + 16 * q + lane_base, w);
       }
-      lsum += (ls4[0] + ls4[1]) + (ls4[2] + ls4[3]);
+      lsum += (ls2[0].x + ls2[0].y) + (ls2[1].x + ls2[1].y);
       if (tid == 0) TR(11, j);
       tc_before();
       __syncwarp();
