@@ -261,7 +261,7 @@ __device__ __forceinline__ uint4 dec_raw8(uint32_t scheme, const uint4& c, const
 // made the decode loop branch-bound).  VMAJ: V's MN-major layout, else K's K-major layout.
 template <int DT, int SCH, bool VMAJ, uint32_t D>
 __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, const uint8_t* __restrict__ smeta,
-                                           const uint16_t* __restrict__ vt, uint32_t g_shift, uint32_t g0,
+                                           const uint16_t* __restrict__ vt, uint32_t gse_m, uint32_t g_shift, uint32_t g0,
                                            uint8_t* __restrict__ dst, uint32_t dt, uint16_t* __restrict__ dump,
                                            const uint8_t* __restrict__ g16, uint32_t t0) {
   constexpr uint32_t dcs = D / 8, nch = kKT * dcs / (32 * kDecWarps);
@@ -276,11 +276,19 @@ __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, cons
         v = __ldg(reinterpret_cast<const uint4*>(g16 + 2ull * ((t0 + key) * D + dc * 8)));
       } else {
         const uint2 raw = *reinterpret_cast<const uint2*>(stc + (i * 32 * kDecWarps + dt) * 8);
-        if constexpr (SCH == HR_S_GSE8) {  // the slab's 256-entry table of decoded 16-bit values: one LDS.U16 per element
+        if constexpr (SCH == HR_S_GSE8) {
+#ifdef HARAG_ATT_GSE_VALUE_TABLE
+          // the slab's 256-entry table of decoded 16-bit values: one LDS.U16 per element (bank conflicts)
           uint32_t h[8];
 #pragma unroll
           for (int k = 0; k < 8; ++k) h[k] = vt[((k < 4 ? raw.x : raw.y) >> (8 * (k & 3))) & 0xFFu];
           v = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
+#else
+          // fields by the magic-number conversion, scale from the slab's 2^(e+1)-entry fp32 table (at most
+          // 32 entries: distinct entries sit in distinct banks), fma(f, T, +0) as hr_assemble_kv
+          v = dec_raw8<DT>(SCH, make_uint4(raw.x, raw.y, 0u, 0u), make_float2(0.f, 0.f), gse_m,
+                           reinterpret_cast<const float*>(vt));
+#endif
         } else {
           float2 m = make_float2(0.f, 0.f);
           const uint32_t g = ((((t0 + key) * D + dc * 8)) >> g_shift) - g0;  // group index in the tile window
@@ -299,9 +307,9 @@ __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, cons
 }
 template <int DT, bool VMAJ, uint32_t D>
 __device__ __forceinline__ void dec_tile(uint32_t scheme, const uint8_t* stc, const uint8_t* smeta, const uint16_t* vt,
-                                         uint32_t g_shift, uint32_t g0, uint8_t* dst, uint32_t dt, uint16_t* dump,
-                                         const uint8_t* g16, uint32_t t0) {
-#define HR_DT(S) dec_tile_s<DT, S, VMAJ, D>(stc, smeta, vt, g_shift, g0, dst, dt, dump, g16, t0)
+                                         uint32_t gse_m, uint32_t g_shift, uint32_t g0, uint8_t* dst, uint32_t dt,
+                                         uint16_t* dump, const uint8_t* g16, uint32_t t0) {
+#define HR_DT(S) dec_tile_s<DT, S, VMAJ, D>(stc, smeta, vt, gse_m, g_shift, g0, dst, dt, dump, g16, t0)
   switch (scheme) {
     case HR_S_PASS16: return HR_DT(HR_S_PASS16);
     case HR_S_INT8: return HR_DT(HR_S_INT8);
@@ -657,6 +665,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       if (slot != cur_slot) {  // new doc: the GSE-8 value tables of its K and V slab (this group only)
         cur_slot = slot;
         const uint32_t fm = (1u << p.gse_m) - 1u;
+#ifdef HARAG_ATT_GSE_VALUE_TABLE
         for (uint32_t byte = dt; byte < 256; byte += 32 * kDecWarps) {  // bytes dt, dt + group size, ...
 #pragma unroll
           for (uint32_t kv = 0; kv < 2; ++kv) {
@@ -668,6 +677,16 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
             (kv ? vtv : vtk)[byte] = (uint16_t)(pack2<DT>(f, 0.f) & 0xFFFFu);
           }
         }
+#else
+        (void)fm;
+        if (dt < 64) {  // the fp32 scale tables (2^(e+1) entries, zero-filled to 32) of its K and V slab
+          const uint32_t kv = dt >> 5, i = dt & 31;
+          const AsmDesc& d = kv ? dv : dk;
+          reinterpret_cast<float*>(kv ? vtv : vtk)[i] =
+              (d.scheme == HR_S_GSE8 && i < (2u << p.gse_e)) ? __ldg(reinterpret_cast<const float*>((kv ? vm : km) + 16) + i)
+                                                               : 0.f;
+        }
+#endif
       }
       if (dt == 0) TR(6, j);
       if (use >= 1) MBW(&kve[b], (use - 1) & 1, 3, j);  // PV_{j-3} (and S_{j-3}) done: buffer b free
@@ -683,8 +702,8 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
           dump = p.kv_dump + ((((uint64_t)r * 2) * p.L + l) * p.Hl + h) * p.k * p.T * D + ((uint64_t)slot * p.T + t0) * D;
         const uint64_t kvoff = (uint64_t)p.L * p.Hl * p.k * p.T * D;
         const uint32_t vo = kDecChunks * 32 * kDecWarps;
-        dec_tile<DT, false, D>(dk.scheme, stc, smk, vtk, p.g_shift, gk0, skd, dt, dump, kc, t0);
-        dec_tile<DT, true, D>(dv.scheme, stc + vo * 8, smv, vtv, p.g_shift, gv0, svd, dt,
+        dec_tile<DT, false, D>(dk.scheme, stc, smk, vtk, p.gse_m, p.g_shift, gk0, skd, dt, dump, kc, t0);
+        dec_tile<DT, true, D>(dv.scheme, stc + vo * 8, smv, vtv, p.gse_m, p.g_shift, gv0, svd, dt,
                               dump ? dump + kvoff : nullptr, vc, t0);
       }
       fence_async_smem();
