@@ -18,9 +18,10 @@
 // for bit as hr_assemble_kv, into one of four K/V operand buffers; S = Q K^T
 // accumulates in one of two TMEM buffers; the softmax warps (thread = row)
 // run the online softmax with a lazy O rescale and write P (16-bit) back into
-// the S buffer's TMEM columns; O += P V takes A from TMEM.  Q and K use
-// 128-byte-swizzled K-major shared-memory tiles, V the canonical no-swizzle
-// MN-major layout (8 rows x 16 B per core matrix).  Debug builds:
+// the S buffer's TMEM columns.  Both MMAs take A from TMEM (Q loaded once per
+// unit, P per tile), so shared memory feeds only the B operands: K as a
+// 128-byte-swizzled K-major tile, V the canonical no-swizzle MN-major layout
+// (8 rows x 16 B per core matrix).  Debug builds:
 // -DHARAG_ATT_TRACE (per-tile clock64 events of CTA 0), -DHARAG_ATT_WATCHDOG
 // (mbarrier waits that report and trap), -DHARAG_ATT_MMASYNC (MMA latency in
 // isolation).
@@ -75,14 +76,6 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t 
 // Instruction descriptor, kind::f16: fp32 accumulate, A/B format (0 fp16, 1 bf16), majors, N, M.
 __host__ __device__ constexpr uint32_t idesc(uint32_t fmt, uint32_t a_mn, uint32_t b_mn, uint32_t n, uint32_t m) {
   return (1u << 4) | (fmt << 7) | (fmt << 10) | (a_mn << 15) | (b_mn << 16) | ((n >> 3) << 17) | ((m >> 4) << 24);
-}
-__device__ __forceinline__ void mma_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(a), "l"(b), "r"(id), "r"(acc)
-      : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(saddr(bar))
@@ -362,9 +355,10 @@ __device__ __forceinline__ uint32_t stage_meta(uint32_t scheme, const uint8_t* m
 // tile j+2.  mbarriers: sf (S ready), pf (P ready), kvf (operands ready), kve (operands and P free:
 // committed after PV), od (PV done, for the lazy rescale and the epilogue), qf (Q ready).
 constexpr uint32_t kPF = 4;  // L2 prefetch distance in tiles
+constexpr uint32_t kTQ = 256, kTmemCols = 512;  // Q's first TMEM column; columns allocated (power of two)
 
 size_t att_smem_bytes(uint32_t D) {
-  return (size_t)kRows * D * 2 + kOpBufs * 2 * (size_t)kKT * D * 2 + 16 * 8 + 16 + kDecGroups * kStageBytes +
+  return kOpBufs * 2 * (size_t)kKT * D * 2 + 16 * 8 + 16 + kDecGroups * kStageBytes +
          2 * 2 * kRows * 4;
 }
 
@@ -434,8 +428,8 @@ template <int DT, uint32_t D>
 __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_constant__ AttnParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   constexpr uint32_t dcs = D / 8;
-  uint8_t* sq = smem_raw;                          // [128 rows][D] K-major core layout
-  uint8_t* skb = sq + kRows * D * 2;               // kOpBufs x [64 keys][D] K-major (B of S = Q K^T)
+  // Q (A of S = Q K^T) lives in TMEM columns [kTQ, kTQ + D/2): lane = query row, column c = elements 2c, 2c+1
+  uint8_t* skb = smem_raw;                         // kOpBufs x [64 keys][D] K-major (B of S = Q K^T)
   uint8_t* svb = skb + kOpBufs * kKT * D * 2;      // kOpBufs x [64 keys][D] MN-major (B of O += P V)
   // P_j lives in TMEM, packed over the first 32 columns of S buffer j & 1 (the A operand of O += P V)
   uint64_t* bar = reinterpret_cast<uint64_t*>(svb + kOpBufs * kKT * D * 2);
@@ -456,8 +450,8 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
   const uint32_t tiles_per_doc = p.T / kKT;
   const uint32_t n_tiles = p.k * tiles_per_doc;
 
-  if (warp == 0) {  // TMEM: S buffers at columns [0, 64) and [64, 128), O at [128, 128 + D)
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(saddr(tmem_slot)));
+  if (warp == 0) {  // TMEM: S buffers at columns [0, 64) and [64, 128), O at [128, 128 + D), Q at [kTQ, kTQ + D/2)
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(tmem_slot)), "n"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
@@ -493,18 +487,21 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     // 32 hf .. + 31) and of O (columns D/2 hf ..).  The two warps of a quadrant exchange their partial
     // row maxima through shared memory (named barrier 3) so both take identical rescale decisions.
     const uint32_t quad = warp & 3, hf = warp >> 2, t = quad * 32 + lane;  // t: query row
-    // Q tile: rows >= M are zero.  Thread mapping per 32 chunks: 8 rows x 4 column chunks.
-    for (uint32_t c = tid; c < kRows * dcs; c += 32 * kSoftWarps) {
-      const uint32_t gI = c >> 5, i = c & 7, jj = (c >> 3) & 3;
-      const uint32_t row = (gI % (kRows / 8)) * 8 + i, dc = (gI / (kRows / 8)) * 4 + jj;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (row < p.M) v = __ldg(reinterpret_cast<const uint4*>(p.q + (row0 + row) * D) + dc);
-      *reinterpret_cast<uint4*>(sq + sw128_off(row, dc, kRows)) = v;
+    const uint32_t lane_base = (quad * 32) << 16;
+    // Q row t (zero for t >= M) -> this thread's TMEM lane, 64 elements per tcgen05.st
+    for (uint32_t cb = 0; hf == 0 && cb < D / 2; cb += 32) {  // (with two column parts: one warp per quadrant)
+      uint32_t qv[32];
+      const uint4* src = reinterpret_cast<const uint4*>(p.q + (row0 + t) * D + 2 * cb);
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const uint4 w = t < p.M ? __ldg(src + u) : make_uint4(0, 0, 0, 0);
+        qv[4 * u] = w.x, qv[4 * u + 1] = w.y, qv[4 * u + 2] = w.z, qv[4 * u + 3] = w.w;
+      }
+      tmem_st32(tmem + kTQ + cb + lane_base, qv);
     }
-    fence_async_smem();
+    tc_before();
     __syncwarp();
     if (lane == 0) mbar_arrive1(qf);
-    const uint32_t lane_base = (quad * 32) << 16;
     const float c = p.scale_log2;
     float m_ref = -INFINITY, lsum = 0.f;
     for (uint32_t j = 0; j < n_tiles; ++j) {
@@ -716,7 +713,6 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     const uint32_t fmt = DT == HR_BF16 ? 1u : 0u;
     const uint32_t id_s = idesc(fmt, 0, 0, kKT, kRows);  // S[128 x 64] = Q[128 x D] . K[64 x D]^T
     const uint32_t id_o = idesc(fmt, 0, 1, D, kRows);    // O[128 x D] += P[128 x 64] . V[64 x D] (V MN-major)
-    const uint32_t qa = saddr(sq);
     // Event-driven issue: S_j needs operands j (kvf) and its TMEM buffer free (softmax of j-2 done, i.e.
     // PV_{j-2} already issued); PV_j needs P_j (pf).  Whichever is ready goes first, so PV_{j-1} (which
     // frees the operand buffer decode j+1 waits for) never waits behind the decode of tile j.
@@ -737,9 +733,9 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         TR(4, ns);
         tc_after();
         const uint32_t ka = saddr(skb + ob * (kKT * D * 2));
-        for (uint32_t s = 0; s < D / 16; ++s)  // K-major: one k-step = 2 core matrices along K
-          mma_f16(tmem + b * kKT, sdesc_sw128(qa + (s >> 2) * (kRows * 128) + (s & 3) * 32),
-                  sdesc_sw128(ka + (s >> 2) * (kKT * 128) + (s & 3) * 32), id_s, s > 0);
+        for (uint32_t s = 0; s < D / 16; ++s)  // A = Q from TMEM (8 columns per k-step); K-major SW128 K
+          mma_f16_ts(tmem + b * kKT, tmem + kTQ + s * 8, sdesc_sw128(ka + (s >> 2) * (kKT * 128) + (s & 3) * 32),
+                     id_s, s > 0);
         mma_commit(&sf[b]);
 #ifdef HARAG_ATT_WATCHDOG
         wd0 = clock64();
@@ -773,7 +769,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
   }
   tc_before();
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(kTmemCols));
 #ifdef HARAG_ATT_TRACE
   if (blockIdx.x == 0 && tid == 0) {
     const long long t0 = g_tr[6][0];
