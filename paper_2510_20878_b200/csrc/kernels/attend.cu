@@ -113,6 +113,16 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16
 }
 #undef HR_R8
 #undef HR_W8
+__device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
+  uint32_t v;
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+  return v;
+}
+__device__ __forceinline__ void tmem_st1(uint32_t taddr, uint32_t v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v) : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
 // D (TMEM) += A (TMEM: lanes = rows, 32-bit columns = pairs of 16-bit K elements) . B (shared memory)
 __device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t id, uint32_t acc) {
   asm volatile(
@@ -290,8 +300,8 @@ __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, cons
           v = dec_raw8<DT>(SCH, make_uint4(raw.x, raw.y, 0u, 0u), m, 0u, nullptr);
         }
       }
-      if (VMAJ)
-        *reinterpret_cast<uint4*>(dst + ((key / 8) * dcs + dc) * 128 + (key % 8) * 16) = v;
+      if (VMAJ)  // V: D/8 + 2 chunks per 8-key group (the ones / zero columns follow the D/8 of the head)
+        *reinterpret_cast<uint4*>(dst + ((key / 8) * (dcs + 2) + dc) * 128 + (key % 8) * 16) = v;
       else
         *reinterpret_cast<uint4*>(dst + sw128_off(key, dc, kKT)) = v;
       if (dump) *reinterpret_cast<uint4*>(dump + key * D + dc * 8) = v;
@@ -355,10 +365,11 @@ __device__ __forceinline__ uint32_t stage_meta(uint32_t scheme, const uint8_t* m
 // tile j+2.  mbarriers: sf (S ready), pf (P ready), kvf (operands ready), kve (operands and P free:
 // committed after PV), od (PV done, for the lazy rescale and the epilogue), qf (Q ready).
 constexpr uint32_t kPF = 4;  // L2 prefetch distance in tiles
-constexpr uint32_t kTQ = 256, kTmemCols = 512;  // Q's first TMEM column; columns allocated (power of two)
+// TMEM columns: S buffers [0, 128), O [128, 128 + D + 16) (column 128 + D: the row sum), Q [kTQ, kTQ + D/2)
+constexpr uint32_t kTQ = 384, kTmemCols = 512;
 
 size_t att_smem_bytes(uint32_t D) {
-  return kOpBufs * 2 * (size_t)kKT * D * 2 + 16 * 8 + 16 + kDecGroups * kStageBytes +
+  return kOpBufs * (size_t)kKT * (2 * D + 16) * 2 + 16 * 8 + 16 + kDecGroups * kStageBytes +
          2 * 2 * kRows * 4;
 }
 
@@ -430,9 +441,13 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
   constexpr uint32_t dcs = D / 8;
   // Q (A of S = Q K^T) lives in TMEM columns [kTQ, kTQ + D/2): lane = query row, column c = elements 2c, 2c+1
   uint8_t* skb = smem_raw;                         // kOpBufs x [64 keys][D] K-major (B of S = Q K^T)
-  uint8_t* svb = skb + kOpBufs * kKT * D * 2;      // kOpBufs x [64 keys][D] MN-major (B of O += P V)
+  // kOpBufs x [64 keys][D + 16] MN-major (B of O += P V): column D is all ones, D + 1 .. D + 15 zero, so
+  // the PV MMA also accumulates the row sum of P — the rounded 16-bit weights actually used — in O's
+  // column D (fp32 on the tensor core: no per-element sum in the softmax warps)
+  constexpr uint32_t vdcs = D / 8 + 2, vbuf = kKT * (D + 16) * 2;
+  uint8_t* svb = skb + kOpBufs * kKT * D * 2;
   // P_j lives in TMEM, packed over the first 32 columns of S buffer j & 1 (the A operand of O += P V)
-  uint64_t* bar = reinterpret_cast<uint64_t*>(svb + kOpBufs * kKT * D * 2);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(svb + kOpBufs * vbuf);
   static_assert(4 + 2 * kOpBufs + 4 <= 16, "mbarrier slots");
   uint64_t *sf = bar, *pf = bar + 2, *kvf = bar + 4, *kve = kvf + kOpBufs, *od = kve + kOpBufs, *qf = od + 1;
   uint64_t* pfree = qf + 1;  // [2]: PV_j done (P_j consumed)
@@ -475,6 +490,13 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       }
     }
   }
+  for (uint32_t c = tid; c < kOpBufs * kKT * 2; c += blockDim.x) {  // the ones / zero chunks of every V buffer
+    const uint32_t b = c / (2 * kKT), key = (c / 2) % kKT, dc = D / 8 + (c & 1);
+    const uint32_t one = DT == HR_BF16 ? 0x3F80u : 0x3C00u;
+    *reinterpret_cast<uint4*>(svb + b * vbuf + ((key / 8) * vdcs + dc) * 128 + (key % 8) * 16) =
+        make_uint4((c & 1) ? 0u : one, 0u, 0u, 0u);
+  }
+  fence_async_smem();
   tc_before();
   __syncthreads();
   tc_after();
@@ -503,7 +525,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     __syncwarp();
     if (lane == 0) mbar_arrive1(qf);
     const float c = p.scale_log2;
-    float m_ref = -INFINITY, lsum = 0.f;
+    float m_ref = -INFINITY;
     for (uint32_t j = 0; j < n_tiles; ++j) {
       const uint32_t b = j & 1;
       MBW(&sf[b], (j >> 1) & 1, 1, j);
@@ -544,12 +566,11 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
           for (int q = 0; q < 32; ++q) ov[q] = __float_as_uint(__uint_as_float(ov[q]) * alpha);
           tmem_st32(t_o + lane_base + cb, ov);
         }
-        lsum *= alpha;
+        if (hf == kNH - 1) tmem_st1(t_o + lane_base + D, __float_as_uint(__uint_as_float(tmem_ld1(t_o + lane_base + D)) * alpha));
       }
       if (grow) m_ref = mt;
       // keys kCW hf + 2i, + 1 packed in column kCW/2 hf + i of the S buffer (S reads are done: with two
       // column parts both passed the max exchange; within a warp the chunk q reload precedes its store)
-      float2 ls2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};  // (even, odd) keys, two chains
       const float2 c2 = make_float2(c, c), nm2 = make_float2(-m_ref, -m_ref);
 #pragma unroll
       for (uint32_t q = 0; q < kCW / 32; ++q) {
@@ -559,12 +580,9 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         for (uint32_t i = 0; i < 16; ++i) {
           const float2 x = __ffma2_rn(make_float2(__uint_as_float(sv[2 * i]), __uint_as_float(sv[2 * i + 1])), c2, nm2);
           w[i] = pack2<DT>(ex2(x.x), ex2(x.y));
-          // normalise by the rounded weights actually used: both 16-bit halves as exact fp32 values
-          ls2[i & 1] = __fadd2_rn(ls2[i & 1], make_float2(lo_f<DT>(w[i]), hi_f<DT>(w[i])));
         }
         tmem_st16(tmem + b * kKT + hf * (kCW / 2) + 16 * q + lane_base, w);
       }
-      lsum += (ls2[0].x + ls2[0].y) + (ls2[1].x + ls2[1].y);
       if (tid == 0) TR(11, j);
       tc_before();
       __syncwarp();
@@ -572,18 +590,12 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       if (tid == 0) TR(1, j);
     }
     // epilogue: O / l -> output dtype; LSE (natural log) = ln 2 * (m_ref + log2 l), l = sum of both halves
-    float ltot = lsum;
-    if constexpr (kNH > 1) {
-      const uint32_t es = (n_tiles & 1) * 256;  // the slot the last tile's exchange did not use
-      rmax[es + hf * 128 + t] = lsum;
-      named_bar(15, 32 * kSoftWarps);
-      ltot = rmax[es + t] + rmax[es + 128 + t];
-    }
     // PV_{n-1} done (its commit covers every earlier MMA); the per-buffer barrier has completed at least
     // PV_{n-3}'s phase, so its parity cannot alias
     if (n_tiles) MBW(&pfree[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1, 8, n_tiles);
     tc_after();
-    const float inv = 1.f / ltot;
+    // l = sum of the rounded weights (O's ones column); every row has l >= 1 (its maximum contributes 2^0)
+    const float ltot = __uint_as_float(tmem_ld1(t_o + lane_base + D)), inv = 1.f / ltot;
     for (uint32_t cb = hf * (D / kNH); cb < (hf + 1) * (D / kNH); cb += 32) {
       uint32_t ov[32];
       tmem_ld32(t_o + lane_base + cb, ov);
@@ -692,7 +704,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       named_bar(1 + grp, 32 * kDecWarps);               // ... and every thread's meta / value-table share
       if (dt == 0) TR(7, j);
       uint8_t* skd = skb + b * (kKT * D * 2);
-      uint8_t* svd = svb + b * (kKT * D * 2);
+      uint8_t* svd = svb + b * vbuf;
       {
         uint16_t* dump = nullptr;  // test hook: the assembled KV [r][2][l][h][k*T][D]
         if (p.kv_dump)
@@ -712,7 +724,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     // ------------------------------------------------------------------ MMA issuer
     const uint32_t fmt = DT == HR_BF16 ? 1u : 0u;
     const uint32_t id_s = idesc(fmt, 0, 0, kKT, kRows);  // S[128 x 64] = Q[128 x D] . K[64 x D]^T
-    const uint32_t id_o = idesc(fmt, 0, 1, D, kRows);    // O[128 x D] += P[128 x 64] . V[64 x D] (V MN-major)
+    const uint32_t id_o = idesc(fmt, 0, 1, D + 16, kRows);  // O[128 x D+16] += P[128 x 64] . V[64 x D+16] (MN-major)
     // Event-driven issue: S_j needs operands j (kvf) and its TMEM buffer free (softmax of j-2 done, i.e.
     // PV_{j-2} already issued); PV_j needs P_j (pf).  Whichever is ready goes first, so PV_{j-1} (which
     // frees the operand buffer decode j+1 waits for) never waits behind the decode of tile j.
@@ -749,9 +761,9 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         const uint32_t bb = npv & 1, ob = npv % kOpBufs;
         TR(5, npv);
         tc_after();
-        const uint32_t va = saddr(svb + ob * (kKT * D * 2));
+        const uint32_t va = saddr(svb + ob * vbuf);
         for (uint32_t s = 0; s < kKT / 16; ++s)
-          mma_f16_ts(t_o, tmem + bb * kKT + s * 8, sdesc(va + s * 2 * dcs * 128, dcs * 128, 128), id_o,
+          mma_f16_ts(t_o, tmem + bb * kKT + s * 8, sdesc(va + s * 2 * vdcs * 128, vdcs * 128, 128), id_o,
                      (npv > 0 || s > 0) ? 1u : 0u);  // A = P_npv from TMEM: 16 keys = 8 columns per k-step
         mma_commit(&kve[ob]);
         mma_commit(&pfree[bb]);

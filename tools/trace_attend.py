@@ -6,6 +6,7 @@ import numpy as np
 
 rows = [l.split() for l in open(sys.argv[1]) if l[:1].isdigit() and "|" in l]
 a = np.array([[float(x) for x in r if x != "|"] for r in rows])
+a = a[np.nonzero(a[:, 0] == 0)[0][-1]:]  # the last launch's trace
 lo, hi = (int(sys.argv[2]), int(sys.argv[3])) if len(sys.argv) > 3 else (len(a) // 4, 3 * len(a) // 4)
 s = slice(lo, hi)
 sf, pf, kve, kvf, si, pv, ds, li, tl, ex = (a[:, i] for i in (1, 2, 3, 4, 5, 6, 7, 8, 9, 12))
