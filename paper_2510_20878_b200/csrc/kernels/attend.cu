@@ -103,16 +103,16 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
       : "memory");
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
-// 16 consecutive 32-bit columns of this thread's TMEM lane
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
-      HR_W8(0), HR_W8(8)
-      : "memory");
-  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-}
 #undef HR_R8
 #undef HR_W8
+// 16 columns, no completion wait (one tcgen05.wait::st before the data is published)
+__device__ __forceinline__ void tmem_st16_nw(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
 __device__ __forceinline__ uint32_t tmem_ld1(uint32_t taddr) {
   uint32_t v;
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr));
@@ -143,6 +143,17 @@ __device__ __forceinline__ uint32_t pack2(float a, float b) {
     return *reinterpret_cast<uint32_t*>(&h);
   }
 }
+// lane-wise maximum of two pairs of non-negative 16-bit floats
+template <int DT>
+__device__ __forceinline__ uint32_t hmax2u(uint32_t a, uint32_t b) {
+  if constexpr (DT == HR_BF16) {
+    __nv_bfloat162 r = __hmax2(*reinterpret_cast<__nv_bfloat162*>(&a), *reinterpret_cast<__nv_bfloat162*>(&b));
+    return *reinterpret_cast<uint32_t*>(&r);
+  } else {
+    __half2 r = __hmax2(*reinterpret_cast<__half2*>(&a), *reinterpret_cast<__half2*>(&b));
+    return *reinterpret_cast<uint32_t*>(&r);
+  }
+}
 template <int DT>
 __device__ __forceinline__ float lo_f(uint32_t w) {
   return DT == HR_BF16 ? __uint_as_float(w << 16) : __half2float(__ushort_as_half((unsigned short)(w & 0xFFFFu)));
@@ -161,17 +172,10 @@ __device__ __forceinline__ float hi_f(uint32_t w) {
 #ifndef HARAG_ATT_DEC_GROUPS
 #define HARAG_ATT_DEC_GROUPS 3
 #endif
-// measured (tools/prof_attend.py 8, C2 shape): 4 softmax + 3 x 8 decoder warps 2.14 ms; 4 + 2 x 8: 2.38 ms;
-// 4 + 2 x 4: 2.53 ms;
-// 8 + 2 x 4: 2.63 ms; 4 + 1 x 8: 2.89 ms;
-// 4 + 3 x 4: 2.59 ms (more warps = fewer registers per thread)
+// measured (tools/prof_attend.py 8, C2 shape, session-2 kernel): 4 softmax + 3 x 8 decoder warps 2.14 ms;
+// 4 + 2 x 8: 2.38 ms; 4 + 2 x 4: 2.53 ms; 8 + 2 x 4: 2.63 ms; 4 + 1 x 8: 2.89 ms; 4 + 3 x 4: 2.59 ms
 constexpr int kSoftWarps = HARAG_ATT_SOFT_WARPS, kDecWarps = HARAG_ATT_DEC_WARPS, kDecGroups = HARAG_ATT_DEC_GROUPS;
-constexpr int kNH = kSoftWarps / 4;        // column parts per 32-row quadrant (1 or 2)
-constexpr uint32_t kCW = 64 / kNH;         // S columns per softmax warp (kKT = 64)
-// With one column part per row quadrant (kNH = 1) the P pass reloads S 32 columns at a time (fewer
-// registers) and writes P over the S buffer's first 32 columns, which only this warp has read.  With two
-// parts each warp keeps its 32 S columns in registers: P is stored only after both passed the max
-// exchange, i.e. after every S read of the tile.
+static_assert(kSoftWarps == 4, "one softmax warp per TMEM lane quadrant");
 constexpr int kAttThreads2 = 32 * (kSoftWarps + kDecGroups * kDecWarps + 1);
 constexpr uint32_t kDecChunks = kKT * 128 / 8 / (32 * kDecWarps);  // 8-element chunks per decoder thread at D = 128
 // per decoder group: codes slots [K, V][kDecChunks][thread] x 16 B, meta slots x 8 B
@@ -365,12 +369,12 @@ __device__ __forceinline__ uint32_t stage_meta(uint32_t scheme, const uint8_t* m
 // tile j+2.  mbarriers: sf (S ready), pf (P ready), kvf (operands ready), kve (operands and P free:
 // committed after PV), od (PV done, for the lazy rescale and the epilogue), qf (Q ready).
 constexpr uint32_t kPF = 4;  // L2 prefetch distance in tiles
-// TMEM columns: S buffers [0, 128), O [128, 128 + D + 16) (column 128 + D: the row sum), Q [kTQ, kTQ + D/2)
-constexpr uint32_t kTQ = 384, kTmemCols = 512;
+// TMEM columns: S buffers [0, 128), O [128, 128 + D + 16) (column 128 + D: the row sum), Q [kTQ, kTQ + D/2),
+// P buffers [kTP, kTP + 64) (32 columns of 16-bit pairs each)
+constexpr uint32_t kTQ = 320, kTP = 448, kTmemCols = 512;
 
 size_t att_smem_bytes(uint32_t D) {
-  return kOpBufs * (size_t)kKT * (2 * D + 16) * 2 + 16 * 8 + 16 + kDecGroups * kStageBytes +
-         2 * 2 * kRows * 4;
+  return kOpBufs * (size_t)kKT * (2 * D + 16) * 2 + 16 * 8 + 16 + kDecGroups * kStageBytes;
 }
 
 // 2^x on the SFU (MUFU.EX2, relative error ~2^-22, far inside R28's 2^-9 budget)
@@ -453,7 +457,6 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
   uint64_t* pfree = qf + 1;  // [2]: PV_j done (P_j consumed)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
   uint8_t* stage0 = reinterpret_cast<uint8_t*>(bar + 18);  // 16-B aligned decoder staging
-  float* rmax = reinterpret_cast<float*>(stage0 + kDecGroups * kStageBytes);  // [2 slots][2 halves][128 rows]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   const uint32_t unit = blockIdx.x;  // (request, layer, head)
@@ -505,13 +508,11 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
 
   if (warp < kSoftWarps) {
     // ------------------------------------------------------------------ softmax warps
-    // warp w: TMEM lane quadrant w & 3 (rows 32 (w & 3) .. + 31), column half hf = w >> 2 of S (keys
-    // 32 hf .. + 31) and of O (columns D/2 hf ..).  The two warps of a quadrant exchange their partial
-    // row maxima through shared memory (named barrier 3) so both take identical rescale decisions.
-    const uint32_t quad = warp & 3, hf = warp >> 2, t = quad * 32 + lane;  // t: query row
+    // warp w: TMEM lane quadrant w (rows 32 w .. + 31), every column of S, P and O of its rows
+    const uint32_t quad = warp, t = quad * 32 + lane;  // t: query row
     const uint32_t lane_base = (quad * 32) << 16;
     // Q row t (zero for t >= M) -> this thread's TMEM lane, 64 elements per tcgen05.st
-    for (uint32_t cb = 0; hf == 0 && cb < D / 2; cb += 32) {  // (with two column parts: one warp per quadrant)
+    for (uint32_t cb = 0; cb < D / 2; cb += 32) {
       uint32_t qv[32];
       const uint4* src = reinterpret_cast<const uint4*>(p.q + (row0 + t) * D + 2 * cb);
 #pragma unroll
@@ -526,64 +527,68 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     if (lane == 0) mbar_arrive1(qf);
     const float c = p.scale_log2;
     float m_ref = -INFINITY;
-    for (uint32_t j = 0; j < n_tiles; ++j) {
-      const uint32_t b = j & 1;
-      MBW(&sf[b], (j >> 1) & 1, 1, j);
-      if (tid == 0) TR(0, j);
-      tc_after();
-      // row max over this warp's kCW columns, 32 at a time (kNH = 1: the P pass reloads them)
-      float pm = -INFINITY;
-      uint32_t sv[32];
-#pragma unroll
-      for (uint32_t q = 0; q < kCW / 32; ++q) {
-        tmem_ld32(tmem + b * kKT + hf * kCW + 32 * q + lane_base, sv);
-        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // independent chains (ILP)
-#pragma unroll
-        for (uint32_t u = 0; u < 32; ++u) mx4[u & 3] = fmaxf(mx4[u & 3], __uint_as_float(sv[u]));
-        pm = fmaxf(pm, fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])));
-      }
-      if (tid == 0) TR(8, j);
-      if constexpr (kNH > 1) {
-        rmax[(j & 1) * 256 + hf * 128 + t] = pm;
-        named_bar(15, 32 * kSoftWarps);  // double-buffered slots: a warp cannot overwrite before its partner read
-        pm = fmaxf(rmax[(j & 1) * 256 + t], rmax[(j & 1) * 256 + 128 + t]);
-      }
-      if (tid == 0) TR(9, j);
-      const float mt = pm * c;  // c > 0: max(s) c = max(s c)
-      const bool grow = mt > m_ref + 8.f;  // lazy rescale: p stays <= 2^8 between rescales
-      if (tid == 0) TR(10, j);
-      if (__any_sync(0xFFFFFFFFu, grow) && j > 0) {
-        // O may be read and rewritten once PV_{j-1} is done.  First PV_{j-2} on its per-buffer barrier, so
-        // that "PV done" (od) is at most one phase behind and its parity wait cannot alias.
-        if (j >= 2) MBW(&pfree[b], ((j >> 1) - 1) & 1, 7, j);
-        MBW(od, (j - 1) & 1, 2, j);
-        tc_after();
-        const float alpha = grow ? ex2(m_ref - mt) : 1.f;
-        for (uint32_t cb = hf * (D / kNH); cb < (hf + 1) * (D / kNH); cb += 32) {
-          uint32_t ov[32];
-          tmem_ld32(t_o + lane_base + cb, ov);
-#pragma unroll
-          for (int q = 0; q < 32; ++q) ov[q] = __float_as_uint(__uint_as_float(ov[q]) * alpha);
-          tmem_st32(t_o + lane_base + cb, ov);
-        }
-        if (hf == kNH - 1) tmem_st1(t_o + lane_base + D, __float_as_uint(__uint_as_float(tmem_ld1(t_o + lane_base + D)) * alpha));
-      }
-      if (grow) m_ref = mt;
-      // keys kCW hf + 2i, + 1 packed in column kCW/2 hf + i of the S buffer (S reads are done: with two
-      // column parts both passed the max exchange; within a warp the chunk q reload precedes its store)
+    // P_j = 2^(s c - m_ref) for the 64 keys of tile j -> 16-bit pairs in this lane of P buffer j & 1 (column i:
+    // keys 2i, 2i + 1); returns whether some weight exceeds 2^8 (s c > m_ref + 8: the running maximum grew)
+    auto p_pass = [&](uint32_t s_col, uint32_t p_col) -> bool {
       const float2 c2 = make_float2(c, c), nm2 = make_float2(-m_ref, -m_ref);
+      uint32_t hm = 0u;  // packed running maximum of the weights (all >= +0)
 #pragma unroll
-      for (uint32_t q = 0; q < kCW / 32; ++q) {
-        uint32_t w[16];
-        if (kNH == 1) tmem_ld32(tmem + b * kKT + hf * kCW + 32 * q + lane_base, sv);
+      for (uint32_t q = 0; q < kKT / 32; ++q) {
+        uint32_t sv[32], w[16];
+        tmem_ld32(s_col + 32 * q, sv);
 #pragma unroll
         for (uint32_t i = 0; i < 16; ++i) {
           const float2 x = __ffma2_rn(make_float2(__uint_as_float(sv[2 * i]), __uint_as_float(sv[2 * i + 1])), c2, nm2);
           w[i] = pack2<DT>(ex2(x.x), ex2(x.y));
+          hm = hmax2u<DT>(hm, w[i]);
         }
-        tmem_st16(tmem + b * kKT + hf * (kCW / 2) + 16 * q + lane_base, w);
+        tmem_st16_nw(p_col + 16 * q, w);
+      }
+      return fmaxf(lo_f<DT>(hm), hi_f<DT>(hm)) > 256.f;
+    };
+    for (uint32_t j = 0; j < n_tiles; ++j) {
+      const uint32_t b = j & 1;
+      const uint32_t s_col = tmem + b * kKT + lane_base, p_col = tmem + kTP + b * (kKT / 2) + lane_base;
+      MBW(&sf[b], (j >> 1) & 1, 1, j);
+      if (tid == 0) TR(0, j);
+      tc_after();
+      // one pass at the running reference m_ref (the common case: the row maximum did not grow by > 2^8)
+      bool grow = p_pass(s_col, p_col);
+      if (tid == 0) TR(8, j);
+      if (__any_sync(0xFFFFFFFFu, grow)) {
+        // the maximum of some row grew (always on tile 0): its row max, the O rescale, P again.  S is
+        // intact (P has its own TMEM columns); the first pass's P stores complete before P is rewritten.
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};  // independent chains (ILP)
+#pragma unroll
+        for (uint32_t q = 0; q < kKT / 32; ++q) {
+          uint32_t sv[32];
+          tmem_ld32(s_col + 32 * q, sv);
+#pragma unroll
+          for (uint32_t u = 0; u < 32; ++u) mx4[u & 3] = fmaxf(mx4[u & 3], __uint_as_float(sv[u]));
+        }
+        const float mt = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * c;  // c > 0: max(s) c = max(s c)
+        if (j > 0) {
+          // O may be read and rewritten once PV_{j-1} is done.  First PV_{j-2} on its per-buffer barrier, so
+          // that "PV done" (od) is at most one phase behind and its parity wait cannot alias.
+          if (j >= 2) MBW(&pfree[b], ((j >> 1) - 1) & 1, 7, j);
+          MBW(od, (j - 1) & 1, 2, j);
+          tc_after();
+          const float alpha = grow ? ex2(m_ref - mt) : 1.f;
+          for (uint32_t cb = 0; cb < D; cb += 32) {
+            uint32_t ov[32];
+            tmem_ld32(t_o + lane_base + cb, ov);
+#pragma unroll
+            for (int q = 0; q < 32; ++q) ov[q] = __float_as_uint(__uint_as_float(ov[q]) * alpha);
+            tmem_st32(t_o + lane_base + cb, ov);
+          }
+          tmem_st1(t_o + lane_base + D, __float_as_uint(__uint_as_float(tmem_ld1(t_o + lane_base + D)) * alpha));
+        }
+        if (grow) m_ref = mt;
+        p_pass(s_col, p_col);
       }
       if (tid == 0) TR(11, j);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_before();
       __syncwarp();
       if (lane == 0) mbar_arrive1(&pf[b]);
@@ -596,7 +601,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     tc_after();
     // l = sum of the rounded weights (O's ones column); every row has l >= 1 (its maximum contributes 2^0)
     const float ltot = __uint_as_float(tmem_ld1(t_o + lane_base + D)), inv = 1.f / ltot;
-    for (uint32_t cb = hf * (D / kNH); cb < (hf + 1) * (D / kNH); cb += 32) {
+    for (uint32_t cb = 0; cb < D; cb += 32) {
       uint32_t ov[32];
       tmem_ld32(t_o + lane_base + cb, ov);
       if (t < p.M) {
@@ -611,7 +616,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         }
       }
     }
-    if (hf == 0 && t < p.M && p.lse) p.lse[row0 + t] = 0.69314718055994531f * (m_ref + __log2f(ltot));
+    if (t < p.M && p.lse) p.lse[row0 + t] = 0.69314718055994531f * (m_ref + __log2f(ltot));
   } else if (warp < kSoftWarps + kDecGroups * kDecWarps) {
     // ------------------------------------------------------------------ decoder warps
     const uint32_t grp = (uint32_t)(warp - kSoftWarps) / kDecWarps;   // tiles j with j % kDecGroups == grp
@@ -763,7 +768,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         tc_after();
         const uint32_t va = saddr(svb + ob * vbuf);
         for (uint32_t s = 0; s < kKT / 16; ++s)
-          mma_f16_ts(t_o, tmem + bb * kKT + s * 8, sdesc(va + s * 2 * vdcs * 128, vdcs * 128, 128), id_o,
+          mma_f16_ts(t_o, tmem + kTP + bb * (kKT / 2) + s * 8, sdesc(va + s * 2 * vdcs * 128, vdcs * 128, 128), id_o,
                      (npv > 0 || s > 0) ? 1u : 0u);  // A = P_npv from TMEM: 16 keys = 8 columns per k-step
         mma_commit(&kve[ob]);
         mma_commit(&pfree[bb]);
