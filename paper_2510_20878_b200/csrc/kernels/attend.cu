@@ -77,9 +77,14 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t 
 __host__ __device__ constexpr uint32_t idesc(uint32_t fmt, uint32_t a_mn, uint32_t b_mn, uint32_t n, uint32_t m) {
   return (1u << 4) | (fmt << 7) | (fmt << 10) | (a_mn << 15) | (b_mn << 16) | ((n >> 3) << 17) | ((m >> 4) << 24);
 }
+// MMA issue is warp-uniform: the whole issuer warp runs the loop and elect.sync picks the one issuing
+// lane inside the instruction sequence (issue from a divergent single-lane branch wraps every tcgen05
+// instruction in an elect loop and measured twice the completion time: tools/ubench/mma_lat.cu)
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(saddr(bar))
-               : "memory");
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(saddr(bar))
+      : "memory");
 }
 
 #define HR_R8(i) "=r"(v[i]), "=r"(v[i + 1]), "=r"(v[i + 2]), "=r"(v[i + 3]), "=r"(v[i + 4]), "=r"(v[i + 5]), \
@@ -126,9 +131,10 @@ __device__ __forceinline__ void tmem_st1(uint32_t taddr, uint32_t v) {
 // D (TMEM) += A (TMEM: lanes = rows, 32-bit columns = pairs of 16-bit K elements) . B (shared memory)
 __device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t id, uint32_t acc) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\t"
+      "{\n\t.reg .pred p, e;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b), "r"(id), "r"(acc)
       : "memory");
 }
@@ -420,6 +426,10 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
       : "r"(saddr(bar)), "r"(parity)
       : "memory");
   return ok != 0;
+}
+// warp-uniform mbar_test (lane 0's observation)
+__device__ __forceinline__ bool mbar_test_u(uint64_t* bar, uint32_t parity) {
+  return __shfl_sync(0xFFFFFFFFu, (int)mbar_test(bar, parity), 0) != 0;
 }
 __device__ __forceinline__ void named_bar(uint32_t id, uint32_t n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
@@ -725,7 +735,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       if (lane == 0) mbar_arrive1(&kvf[b]);
       if (dt == 0) TR(3, j);
     }
-  } else if (lane == 0) {
+  } else {
     // ------------------------------------------------------------------ MMA issuer
     const uint32_t fmt = DT == HR_BF16 ? 1u : 0u;
     const uint32_t id_s = idesc(fmt, 0, 0, kKT, kRows);  // S[128 x 64] = Q[128 x D] . K[64 x D]^T
@@ -745,7 +755,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         __trap();
       }
 #endif
-      if (ns < n_tiles && ns <= npv + 1 && mbar_test(&kvf[ns % kOpBufs], (ns / kOpBufs) & 1)) {
+      if (ns < n_tiles && ns <= npv + 1 && mbar_test_u(&kvf[ns % kOpBufs], (ns / kOpBufs) & 1)) {
         const uint32_t b = ns & 1, ob = ns % kOpBufs;
         TR(4, ns);
         tc_after();
@@ -762,7 +772,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         TR(12, ns);
 #endif
         ++ns;
-      } else if (npv < ns && mbar_test(&pf[npv & 1], (npv >> 1) & 1)) {
+      } else if (npv < ns && mbar_test_u(&pf[npv & 1], (npv >> 1) & 1)) {
         const uint32_t bb = npv & 1, ob = npv % kOpBufs;
         TR(5, npv);
         tc_after();
