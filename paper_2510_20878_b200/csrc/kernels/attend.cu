@@ -200,6 +200,36 @@ __device__ __forceinline__ void bytes_to_f2(uint32_t w, float bias, float2& a, f
   b = __fadd2_rn(make_float2(__uint_as_float(__byte_perm(w, 0x4B000000u, 0x7652)), __uint_as_float(__byte_perm(w, 0x4B000000u, 0x7653))), nb);
 }
 
+// high 16-bit halves of two fp32 values as a pair (lo = a): the bf16 value of an fp32 that is exactly
+// representable in bf16, or bf16 by truncation
+__device__ __forceinline__ uint32_t hi_pair(float a, float b) {
+  return __byte_perm(__float_as_uint(a), __float_as_uint(b), 0x7632);
+}
+// Two FP8 codes of word w (bytes picked by `sel_m`) -> an exact 16-bit pair, without the conversion pipe
+// (XU: cvt / F2FP run at 16 lanes per clock per SM).  The 7 exponent+mantissa bits are placed as the top
+// of a 16-bit float's exponent+mantissa field (shift sh), the sign at bit 15 (`sel_s` picks the sign
+// bytes into bytes 1 and 3), and one packed multiply by 2^(bias difference) rebiases — exact, including
+// subnormal codes (16-bit multiplies keep subnormals).  E4M3: bf16 sh 4, x 2^120; fp16 sh 7, x 2^8.
+// E5M2: bf16 sh 5, x 2^112; fp16: the code is the high byte of the fp16 value.  The quantizer's
+// satfinite conversions never emit the E4M3 NaN or E5M2 inf/NaN codes; those decode as finite values here.
+template <int DT, int E5>
+__device__ __forceinline__ uint32_t fp8_pair(uint32_t w, uint32_t sel_m, uint32_t sel_s) {
+  if constexpr (DT == HR_FP16 && E5) return __byte_perm(w, 0u, sel_s);  // [0, b0, 0, b1]
+  const uint32_t xm = __byte_perm(w & 0x7F7F7F7Fu, 0u, sel_m);         // b & 0x7f in the low byte of each half
+  const uint32_t xs = __byte_perm(w & 0x80808080u, 0u, sel_s);         // sign bits at 15 and 31
+  constexpr int sh = DT == HR_BF16 ? (E5 ? 5 : 4) : 7;
+  const uint32_t r = (xm << sh) | xs;
+  if constexpr (DT == HR_BF16) {
+    const __nv_bfloat162 k = E5 ? __floats2bfloat162_rn(0x1p112f, 0x1p112f) : __floats2bfloat162_rn(0x1p120f, 0x1p120f);
+    __nv_bfloat162 v = __hmul2(*reinterpret_cast<const __nv_bfloat162*>(&r), k);
+    return *reinterpret_cast<uint32_t*>(&v);
+  } else {
+    const __half2 k = __floats2half2_rn(256.f, 256.f);
+    __half2 v = __hmul2(*reinterpret_cast<const __half2*>(&r), k);
+    return *reinterpret_cast<uint32_t*>(&v);
+  }
+}
+
 // Decode phase: the rules of decode8 / hr_assemble_kv (R3-R5, R9) from loaded codes and meta.
 template <int DT>
 __device__ __forceinline__ uint4 dec_raw8(uint32_t scheme, const uint4& c, const float2& m, uint32_t gse_m,
@@ -234,22 +264,11 @@ __device__ __forceinline__ uint4 dec_raw8(uint32_t scheme, const uint4& c, const
       return make_uint4(o[0], o[1], o[2], o[3]);
     }
     case HR_S_FP8E4M3:
-    case HR_S_FP8E5M2: {
-      const __nv_fp8_interpretation_t it = scheme == HR_S_FP8E4M3 ? __NV_E4M3 : __NV_E5M2;
-      const uint32_t w[4] = {c.x & 0xFFFFu, c.x >> 16, c.y & 0xFFFFu, c.y >> 16};
-      uint32_t o[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        __half2_raw hr = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)w[i], it);  // exact
-        if constexpr (DT == HR_FP16) {
-          o[i] = (uint32_t)hr.x | ((uint32_t)hr.y << 16);
-        } else {
-          const float2 f = __half22float2(*reinterpret_cast<__half2*>(&hr));
-          o[i] = pack2<DT>(f.x, f.y);  // exact in bf16
-        }
-      }
-      return make_uint4(o[0], o[1], o[2], o[3]);
-    }
+      return make_uint4(fp8_pair<DT, 0>(c.x, 0x4140u, 0x1404u), fp8_pair<DT, 0>(c.x, 0x4342u, 0x3424u),
+                        fp8_pair<DT, 0>(c.y, 0x4140u, 0x1404u), fp8_pair<DT, 0>(c.y, 0x4342u, 0x3424u));
+    case HR_S_FP8E5M2:
+      return make_uint4(fp8_pair<DT, 1>(c.x, 0x4140u, 0x1404u), fp8_pair<DT, 1>(c.x, 0x4342u, 0x3424u),
+                        fp8_pair<DT, 1>(c.y, 0x4140u, 0x1404u), fp8_pair<DT, 1>(c.y, 0x4342u, 0x3424u));
     default: {  // GSE-8: +-f * 2^(G_idx - (m-1)) from the slab's fp32 table (staged in shared memory)
       const uint32_t fm = ((1u << gse_m) - 1u) * 0x01010101u;
       float2 q[4];
@@ -262,7 +281,9 @@ __device__ __forceinline__ uint4 dec_raw8(uint32_t scheme, const uint4& c, const
 #pragma unroll
       for (int i = 0; i < 4; ++i) {  // fma(f, T, +0): the exact product; a (sign 1, field 0) byte gives +0
         const float2 f = __ffma2_rn(q[i], make_float2(t[2 * i], t[2 * i + 1]), make_float2(0.f, 0.f));
-        o[i] = pack2<DT>(f.x, f.y);
+        // bf16: f (< 2^m <= 2^7) times a power of two has at most 8 significant bits, so the high half of
+        // the fp32 value IS the rounded bf16 (one PRMT per pair, no F2FP on the conversion pipe)
+        o[i] = DT == HR_BF16 ? hi_pair(f.x, f.y) : pack2<DT>(f.x, f.y);
       }
       return make_uint4(o[0], o[1], o[2], o[3]);
     }
@@ -378,6 +399,12 @@ constexpr uint32_t kPF = 4;  // L2 prefetch distance in tiles
 // TMEM columns: S buffers [0, 128), O [128, 128 + D + 16) (column 128 + D: the row sum), Q [kTQ, kTQ + D/2),
 // P buffers [kTP, kTP + 64) (32 columns of 16-bit pairs each)
 constexpr uint32_t kTQ = 320, kTP = 448, kTmemCols = 512;
+// Lazy rescale threshold tau (log2 units): weights p = 2^(s c - m_ref) may reach 2^tau before the reference
+// moves (O rescaled).  fp16 P must stay below 65504: tau 8.  bf16 P has fp32's exponent range: tau 32 keeps
+// O and its row sum (<= 2^tau * n * |v|) far inside fp32 and makes rescales rare.
+#ifndef HARAG_ATT_TAU_BF16
+#define HARAG_ATT_TAU_BF16 32
+#endif
 
 size_t att_smem_bytes(uint32_t D) {
   return kOpBufs * (size_t)kKT * (2 * D + 16) * 2 + 16 * 8 + 16 + kDecGroups * kStageBytes;
@@ -536,9 +563,10 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     __syncwarp();
     if (lane == 0) mbar_arrive1(qf);
     const float c = p.scale_log2;
+    constexpr float kPMax = DT == HR_BF16 ? (float)(1ull << HARAG_ATT_TAU_BF16) : 256.f;  // 2^tau
     float m_ref = -INFINITY;
     // P_j = 2^(s c - m_ref) for the 64 keys of tile j -> 16-bit pairs in this lane of P buffer j & 1 (column i:
-    // keys 2i, 2i + 1); returns whether some weight exceeds 2^8 (s c > m_ref + 8: the running maximum grew)
+    // keys 2i, 2i + 1); returns whether some weight exceeds 2^tau (s c > m_ref + tau: the running maximum grew)
     auto p_pass = [&](uint32_t s_col, uint32_t p_col) -> bool {
       const float2 c2 = make_float2(c, c), nm2 = make_float2(-m_ref, -m_ref);
       uint32_t hm = 0u;  // packed running maximum of the weights (all >= +0)
@@ -554,7 +582,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         }
         tmem_st16_nw(p_col + 16 * q, w);
       }
-      return fmaxf(lo_f<DT>(hm), hi_f<DT>(hm)) > 256.f;
+      return fmaxf(lo_f<DT>(hm), hi_f<DT>(hm)) > kPMax;
     };
     for (uint32_t j = 0; j < n_tiles; ++j) {
       const uint32_t b = j & 1;
@@ -562,7 +590,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       MBW(&sf[b], (j >> 1) & 1, 1, j);
       if (tid == 0) TR(0, j);
       tc_after();
-      // one pass at the running reference m_ref (the common case: the row maximum did not grow by > 2^8)
+      // one pass at the running reference m_ref (the common case: the row maximum did not grow by > tau)
       bool grow = p_pass(s_col, p_col);
       if (tid == 0) TR(8, j);
       if (__any_sync(0xFFFFFFFFu, grow)) {
