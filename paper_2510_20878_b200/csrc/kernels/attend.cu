@@ -108,6 +108,21 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32
       : "memory");
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
+// 32 columns, no completion wait (tcgen05.wait::ld / ::st issued by the caller)
+__device__ __forceinline__ void tmem_ld32_nw(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : HR_R8(0), HR_R8(8), HR_R8(16), HR_R8(24)
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st32_nw(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+      "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      HR_W8(0), HR_W8(8), HR_W8(16), HR_W8(24)
+      : "memory");
+}
 #undef HR_R8
 #undef HR_W8
 // 16 columns, no completion wait (one tcgen05.wait::st before the data is published)
@@ -182,6 +197,8 @@ __device__ __forceinline__ float hi_f(uint32_t w) {
 // 4 + 2 x 8: 2.38 ms; 4 + 2 x 4: 2.53 ms; 8 + 2 x 4: 2.63 ms; 4 + 1 x 8: 2.89 ms; 4 + 3 x 4: 2.59 ms
 constexpr int kSoftWarps = HARAG_ATT_SOFT_WARPS, kDecWarps = HARAG_ATT_DEC_WARPS, kDecGroups = HARAG_ATT_DEC_GROUPS;
 static_assert(kSoftWarps == 4, "one softmax warp per TMEM lane quadrant");
+// with <= 17 warps per CTA (>= 120 registers per thread) a softmax thread holds its whole 64-column S row
+constexpr bool kWideSoftmax = kDecGroups * kDecWarps <= 16;
 constexpr int kAttThreads2 = 32 * (kSoftWarps + kDecGroups * kDecWarps + 1);
 constexpr uint32_t kDecChunks = kKT * 128 / 8 / (32 * kDecWarps);  // 8-element chunks per decoder thread at D = 128
 // per decoder group: codes slots [K, V][kDecChunks][thread] x 16 B, meta slots x 8 B
@@ -189,7 +206,11 @@ constexpr uint32_t kDecChunks = kKT * 128 / 8 / (32 * kDecWarps);  // 8-element 
 // (<= 256 groups x 8 B), the doc's GSE-8 value tables [K, V][256] x 16-bit
 constexpr uint32_t kMetaWin = 2048;
 constexpr uint32_t kStageBytes = 2 * kDecChunks * 32 * kDecWarps * 8 + 2 * kMetaWin + 2 * 256 * 2;
-constexpr uint32_t kOpBufs = 4;  // K/V operand buffers: decode of tile j waits for PV_{j-4} only
+#ifndef HARAG_ATT_OPBUFS
+#define HARAG_ATT_OPBUFS 4
+#endif
+constexpr uint32_t kOpBufs = HARAG_ATT_OPBUFS;  // K/V operand buffers: decode of tile j waits for PV_{j-kOpBufs}
+constexpr uint32_t kBarSlots = 24;             // mbarrier slots (8 B each) ahead of the TMEM slot
 
 // The four bytes of w as exact floats (minus `bias`): 0x4B0000bb is 2^23 + bb, so one PRMT and one
 // (packed) subtraction replace an I2F per element.  bias 2^23 for unsigned bytes; 2^23 + 128 for
@@ -290,6 +311,18 @@ __device__ __forceinline__ uint4 dec_raw8(uint32_t scheme, const uint4& c, const
   }
 }
 
+// Byte offset of chunk (key, dc) — 8 elements, 8 B of 1-byte codes or 4 B of INT4 — in a staged code tile.
+// Each key's row of D/8 chunks is stored contiguously but with its chunks permuted (XOR swizzle), so that
+// (a) the cp.async copies, where a warp's 32 lanes take 32 consecutive chunks of the contiguous global
+// tile, write whole 128-B lines, and (b) the decode reads, where a warp's lanes take 8 keys x 4 chunk
+// columns, hit distinct banks (2 wavefronts per LDS.64, 1 per LDS.32).
+template <uint32_t D>
+__device__ __forceinline__ uint32_t stage_off(bool int4, uint32_t key, uint32_t dc) {
+  constexpr uint32_t dcs = D / 8;
+  if (int4) return (key * dcs + (dc ^ (D == 128 ? ((key >> 1) & 3u) << 2 : ((key >> 2) & 1u) << 2))) * 4;
+  return (key * dcs + (dc ^ (D == 128 ? (key & 7u) << 1 : ((key >> 1) & 3u) << 1))) * 8;
+}
+
 // Decode one operand tile (this decoder thread's kDecChunks chunks of 8 elements) with the scheme
 // resolved ONCE per tile: a runtime switch over compile-time-specialised loops (a per-chunk switch
 // made the decode loop branch-bound).  VMAJ: V's MN-major layout, else K's K-major layout.
@@ -309,7 +342,9 @@ __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, cons
       if constexpr (SCH == HR_S_PASS16) {  // bits unchanged: straight from global (L2-prefetched) into the operand tile
         v = __ldg(reinterpret_cast<const uint4*>(g16 + 2ull * ((t0 + key) * D + dc * 8)));
       } else {
-        const uint2 raw = *reinterpret_cast<const uint2*>(stc + (i * 32 * kDecWarps + dt) * 8);
+        uint2 raw;
+        if constexpr (SCH == HR_S_INT4) raw.x = *reinterpret_cast<const uint32_t*>(stc + stage_off<D>(true, key, dc));
+        else raw = *reinterpret_cast<const uint2*>(stc + stage_off<D>(false, key, dc));
         if constexpr (SCH == HR_S_GSE8) {
 #ifdef HARAG_ATT_GSE_VALUE_TABLE
           // the slab's 256-entry table of decoded 16-bit values: one LDS.U16 per element (bank conflicts)
@@ -407,7 +442,7 @@ constexpr uint32_t kTQ = 320, kTP = 448, kTmemCols = 512;
 #endif
 
 size_t att_smem_bytes(uint32_t D) {
-  return kOpBufs * (size_t)kKT * (2 * D + 16) * 2 + 16 * 8 + 16 + kDecGroups * kStageBytes;
+  return kOpBufs * (size_t)kKT * (2 * D + 16) * 2 + kBarSlots * 8 + 16 + kDecGroups * kStageBytes;
 }
 
 // 2^x on the SFU (MUFU.EX2, relative error ~2^-22, far inside R28's 2^-9 budget)
@@ -489,11 +524,11 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
   uint8_t* svb = skb + kOpBufs * kKT * D * 2;
   // P_j lives in TMEM, packed over the first 32 columns of S buffer j & 1 (the A operand of O += P V)
   uint64_t* bar = reinterpret_cast<uint64_t*>(svb + kOpBufs * vbuf);
-  static_assert(4 + 2 * kOpBufs + 4 <= 16, "mbarrier slots");
+  static_assert(4 + 2 * kOpBufs + 4 <= kBarSlots, "mbarrier slots");
   uint64_t *sf = bar, *pf = bar + 2, *kvf = bar + 4, *kve = kvf + kOpBufs, *od = kve + kOpBufs, *qf = od + 1;
   uint64_t* pfree = qf + 1;  // [2]: PV_j done (P_j consumed)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 16);
-  uint8_t* stage0 = reinterpret_cast<uint8_t*>(bar + 18);  // 16-B aligned decoder staging
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + kBarSlots);
+  uint8_t* stage0 = reinterpret_cast<uint8_t*>(bar + kBarSlots + 2);  // 16-B aligned decoder staging
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   const uint32_t unit = blockIdx.x;  // (request, layer, head)
@@ -570,6 +605,22 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     auto p_pass = [&](uint32_t s_col, uint32_t p_col) -> bool {
       const float2 c2 = make_float2(c, c), nm2 = make_float2(-m_ref, -m_ref);
       uint32_t hm = 0u;  // packed running maximum of the weights (all >= +0)
+      if constexpr (kWideSoftmax) {  // the whole 64-column row in registers: both loads in flight, 32 independent pairs
+        uint32_t sv[64], w[32];
+        tmem_ld32_nw(s_col, *reinterpret_cast<uint32_t(*)[32]>(&sv[0]));
+        tmem_ld32_nw(s_col + 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[32]));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        uint32_t hm1 = 0u;
+#pragma unroll
+        for (uint32_t i = 0; i < 32; ++i) {
+          const float2 x = __ffma2_rn(make_float2(__uint_as_float(sv[2 * i]), __uint_as_float(sv[2 * i + 1])), c2, nm2);
+          w[i] = pack2<DT>(ex2(x.x), ex2(x.y));
+          if (i & 1) hm1 = hmax2u<DT>(hm1, w[i]); else hm = hmax2u<DT>(hm, w[i]);
+        }
+        tmem_st32_nw(p_col, w);
+        hm = hmax2u<DT>(hm, hm1);
+        return fmaxf(lo_f<DT>(hm), hi_f<DT>(hm)) > kPMax;
+      }
 #pragma unroll
       for (uint32_t q = 0; q < kKT / 32; ++q) {
         uint32_t sv[32], w[16];
@@ -691,22 +742,17 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       const uint8_t* vm = dv.meta + (uint64_t)slab_i * p.meta_stride[dv.scheme];
       const uint32_t slot = j / tiles_per_doc;
       // all of this thread's loads in flight at once: cp.async into its own staging slots
-      uint8_t* stc = stage0 + grp * kStageBytes;                         // [K, V][i][dt] x 8 B codes
+      uint8_t* stc = stage0 + grp * kStageBytes;                         // [K, V] staged code tiles (stage_off)
       uint8_t* smk = stc + 2 * kDecChunks * 32 * kDecWarps * 8;           // K meta window
       uint8_t* smv = smk + kMetaWin;                                      // V meta window
       uint16_t* vtk = reinterpret_cast<uint16_t*>(smv + kMetaWin);        // [256] K value table
       uint16_t* vtv = vtk + 256;                                          // [256] V value table
 #pragma unroll
-      for (uint32_t i = 0; i < kKT * dcs / (32 * kDecWarps); ++i) {
-        const uint32_t cc = dt + i * 32 * kDecWarps;
-        {
-          const uint32_t gI = cc >> 5, ii = cc & 7, jj = (cc >> 3) & 3;
-          const uint32_t key = (gI % (kKT / 8)) * 8 + ii, dc = (gI / (kKT / 8)) * 4 + jj;
-          const uint32_t e = (t0 + key) * D + dc * 8;
-          const uint32_t sl = i * 32 * kDecWarps + dt;
-          stage_chunk(dk.scheme, kc, e, stc + sl * 8);
-          stage_chunk(dv.scheme, vc, e, stc + (kDecChunks * 32 * kDecWarps + sl) * 8);
-        }
+      for (uint32_t i = 0; i < kKT * dcs / (32 * kDecWarps); ++i) {  // a warp copies 32 consecutive chunks
+        const uint32_t c = dt + i * 32 * kDecWarps, key = c / dcs, dc = c % dcs;
+        const uint32_t e = (t0 + key) * D + dc * 8;
+        stage_chunk(dk.scheme, kc, e, stc + stage_off<D>(dk.scheme == HR_S_INT4, key, dc));
+        stage_chunk(dv.scheme, vc, e, stc + kDecChunks * 32 * kDecWarps * 8 + stage_off<D>(dv.scheme == HR_S_INT4, key, dc));
       }
       // (the previous tile's decode is done with the meta windows: the kvf arrive of that tile followed it
       // in every thread, and the named barrier below orders the group)

@@ -10,7 +10,8 @@ import paper_2510_20878_b200 as hr  # noqa: E402
 import synth  # noqa: E402
 
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 4
-L, H, T, D, k, n_docs, g, n_q = 32, 8, 512, 128, 10, 40, 4, 32
+K_OVERRIDE = int(os.environ.get("HARAG_PROF_K", "10"))
+L, H, T, D, k, n_docs, g, n_q = 32, 8, 512, 128, K_OVERRIDE, 40, 4, 32
 h = hr.policy_count(synth.gen_requests(n_docs, 160, k, 1.1, seed=7), n_docs).astype(np.uint64)
 ladder, taus = ("INT8", "FP8E4M3", "FP8E5M2", "GSE8"), (0.1, 0.1, 0.1)
 total = sum(hr.item_bytes(int(s), L=L, H=H, D=D, T=T) for s in hr.policy_assign(h, ladder, taus))
