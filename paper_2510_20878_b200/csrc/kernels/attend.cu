@@ -346,7 +346,7 @@ __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, cons
         if constexpr (SCH == HR_S_INT4) raw.x = *reinterpret_cast<const uint32_t*>(stc + stage_off<D>(true, key, dc));
         else raw = *reinterpret_cast<const uint2*>(stc + stage_off<D>(false, key, dc));
         if constexpr (SCH == HR_S_GSE8) {
-#ifdef HARAG_ATT_GSE_VALUE_TABLE
+#ifndef HARAG_ATT_GSE_ARITH
           // the slab's 256-entry table of decoded 16-bit values: one LDS.U16 per element (bank conflicts)
           uint32_t h[8];
 #pragma unroll
@@ -488,6 +488,19 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
       : "r"(saddr(bar)), "r"(parity)
       : "memory");
   return ok != 0;
+}
+// wait for the phase with parity `parity` for at most ~`ns` nanoseconds (suspended, not spinning);
+// warp-uniform (lane 0's observation)
+__device__ __forceinline__ bool mbar_wait_hint_u(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(saddr(bar)), "r"(parity), "r"(ns)
+      : "memory");
+  return __shfl_sync(0xFFFFFFFFu, (int)ok, 0) != 0;
 }
 // warp-uniform mbar_test (lane 0's observation)
 __device__ __forceinline__ bool mbar_test_u(uint64_t* bar, uint32_t parity) {
@@ -763,7 +776,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       if (slot != cur_slot) {  // new doc: the GSE-8 value tables of its K and V slab (this group only)
         cur_slot = slot;
         const uint32_t fm = (1u << p.gse_m) - 1u;
-#ifdef HARAG_ATT_GSE_VALUE_TABLE
+#ifndef HARAG_ATT_GSE_ARITH
         for (uint32_t byte = dt; byte < 256; byte += 32 * kDecWarps) {  // bytes dt, dt + group size, ...
 #pragma unroll
           for (uint32_t kv = 0; kv < 2; ++kv) {
@@ -829,7 +842,24 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         __trap();
       }
 #endif
-      if (ns < n_tiles && ns <= npv + 1 && mbar_test_u(&kvf[ns % kOpBufs], (ns / kOpBufs) & 1)) {
+      // Blocking waits where only one event can come next (no polling: a spinning issuer took 10% of the
+      // SM's issue slots): after S_{j+1} only PV_j can follow; with every issued S matched by its PV only
+      // S can.  With both possible (after PV_j: S_{j+2} or PV_{j+1}), S operands are usually ready already.
+      const bool s_ok = ns < n_tiles && ns <= npv + 1, pv_ok = npv < ns;
+      bool do_s;
+      if (!pv_ok) {
+        MBW(&kvf[ns % kOpBufs], (ns / kOpBufs) & 1, 9, ns);
+        do_s = true;
+      } else if (!s_ok) {
+        MBW(&pf[npv & 1], (npv >> 1) & 1, 10, npv);
+        do_s = false;
+      } else {
+        while (true) {
+          if (mbar_test_u(&kvf[ns % kOpBufs], (ns / kOpBufs) & 1)) { do_s = true; break; }
+          if (mbar_wait_hint_u(&pf[npv & 1], (npv >> 1) & 1, 100)) { do_s = false; break; }
+        }
+      }
+      if (do_s) {
         const uint32_t b = ns & 1, ob = ns % kOpBufs;
         TR(4, ns);
         tc_after();
@@ -846,7 +876,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         TR(12, ns);
 #endif
         ++ns;
-      } else if (npv < ns && mbar_test_u(&pf[npv & 1], (npv >> 1) & 1)) {
+      } else {
         const uint32_t bb = npv & 1, ob = npv % kOpBufs;
         TR(5, npv);
         tc_after();
