@@ -429,11 +429,15 @@ __device__ __forceinline__ uint32_t stage_meta(uint32_t scheme, const uint8_t* m
 //   warp 12    MMA issuer (one lane): S_j = Q K_j^T into TMEM buffer j&1, then O += P_{j-1} V_{j-1}
 // so the tensor core computes S_{j+1} while the softmax warps work on S_j and the decoders fill
 // tile j+2.  mbarriers: sf (S ready), pf (P ready), kvf (operands ready), kve (operands and P free:
-// committed after PV), od (PV done, for the lazy rescale and the epilogue), qf (Q ready).
+// committed after PV), pfree (PV done per P buffer: lazy rescale, epilogue), qf (Q ready).
 constexpr uint32_t kPF = 4;  // L2 prefetch distance in tiles
-// TMEM columns: S buffers [0, 128), O [128, 128 + D + 16) (column 128 + D: the row sum), Q [kTQ, kTQ + D/2),
-// P buffers [kTP, kTP + 64) (32 columns of 16-bit pairs each)
-constexpr uint32_t kTQ = 320, kTP = 448, kTmemCols = 512;
+// kSB S buffers and kSB P buffers in TMEM: S_j = Q K_j^T may be computed while softmax works on S_{j-2}
+// and S_{j-1} waits — the tensor core runs S_{j+2} ahead of PV_j.
+// TMEM columns: S buffers [0, 64 kSB), O [kTO, kTO + D + 16) (column kTO + D: the row sum),
+// Q [kTQ, kTQ + D/2), P buffers [kTP, kTP + 32 kSB) (32 columns of 16-bit pairs each)
+constexpr uint32_t kSB = 3;
+constexpr uint32_t kTO = 64 * kSB, kTQ = kTO + 144, kTP = kTQ + 64, kTmemCols = 512;
+static_assert(kTP + 32 * kSB <= kTmemCols, "TMEM columns");
 // Lazy rescale threshold tau (log2 units): weights p = 2^(s c - m_ref) may reach 2^tau before the reference
 // moves (O rescaled).  fp16 P must stay below 65504: tau 8.  bf16 P has fp32's exponent range: tau 32 keeps
 // O and its row sum (<= 2^tau * n * |v|) far inside fp32 and makes rescales rare.
@@ -535,11 +539,10 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
   // column D (fp32 on the tensor core: no per-element sum in the softmax warps)
   constexpr uint32_t vdcs = D / 8 + 2, vbuf = kKT * (D + 16) * 2;
   uint8_t* svb = skb + kOpBufs * kKT * D * 2;
-  // P_j lives in TMEM, packed over the first 32 columns of S buffer j & 1 (the A operand of O += P V)
   uint64_t* bar = reinterpret_cast<uint64_t*>(svb + kOpBufs * vbuf);
-  static_assert(4 + 2 * kOpBufs + 4 <= kBarSlots, "mbarrier slots");
-  uint64_t *sf = bar, *pf = bar + 2, *kvf = bar + 4, *kve = kvf + kOpBufs, *od = kve + kOpBufs, *qf = od + 1;
-  uint64_t* pfree = qf + 1;  // [2]: PV_j done (P_j consumed)
+  static_assert(3 * kSB + 2 * kOpBufs + 1 <= kBarSlots, "mbarrier slots");
+  uint64_t *sf = bar, *pf = sf + kSB, *pfree = pf + kSB;  // per S/P buffer: S ready, P ready, PV done
+  uint64_t *kvf = pfree + kSB, *kve = kvf + kOpBufs, *qf = kve + kOpBufs;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + kBarSlots);
   uint8_t* stage0 = reinterpret_cast<uint8_t*>(bar + kBarSlots + 2);  // 16-B aligned decoder staging
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -553,13 +556,13 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
   const uint32_t tiles_per_doc = p.T / kKT;
   const uint32_t n_tiles = p.k * tiles_per_doc;
 
-  if (warp == 0) {  // TMEM: S buffers at columns [0, 64) and [64, 128), O at [128, 128 + D), Q at [kTQ, kTQ + D/2)
+  if (warp == 0) {  // TMEM: S, O, Q and P buffers (kTO, kTQ, kTP)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(tmem_slot)), "n"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
     if (saddr(smem_raw) & 1023u) __trap();  // 128-B-swizzled operand tiles need 1024-B-aligned atoms
-    for (int b = 0; b < 2; ++b) {
+    for (uint32_t b = 0; b < kSB; ++b) {
       mbar_init(&sf[b], 1);
       mbar_init(&pf[b], kSoftWarps);
       mbar_init(&pfree[b], 1);
@@ -568,7 +571,6 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       mbar_init(&kvf[b], kDecWarps);
       mbar_init(&kve[b], 1);
     }
-    mbar_init(od, 1);
     mbar_init(qf, kSoftWarps);  // every softmax warp loads a share of Q
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (p.descs[0].count != nullptr && l == 0 && h == 0) {  // a1: hotness of this request's items
@@ -589,7 +591,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
   __syncthreads();
   tc_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t t_o = tmem + 128;
+  const uint32_t t_o = tmem + kTO;
 
   if (warp < kSoftWarps) {
     // ------------------------------------------------------------------ softmax warps
@@ -649,9 +651,9 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       return fmaxf(lo_f<DT>(hm), hi_f<DT>(hm)) > kPMax;
     };
     for (uint32_t j = 0; j < n_tiles; ++j) {
-      const uint32_t b = j & 1;
+      const uint32_t b = j % kSB, ph = (j / kSB) & 1;  // buffer, phase parity of its use
       const uint32_t s_col = tmem + b * kKT + lane_base, p_col = tmem + kTP + b * (kKT / 2) + lane_base;
-      MBW(&sf[b], (j >> 1) & 1, 1, j);
+      MBW(&sf[b], ph, 1, j);
       if (tid == 0) TR(0, j);
       tc_after();
       // one pass at the running reference m_ref (the common case: the row maximum did not grow by > tau)
@@ -671,10 +673,9 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         }
         const float mt = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * c;  // c > 0: max(s) c = max(s c)
         if (j > 0) {
-          // O may be read and rewritten once PV_{j-1} is done.  First PV_{j-2} on its per-buffer barrier, so
-          // that "PV done" (od) is at most one phase behind and its parity wait cannot alias.
-          if (j >= 2) MBW(&pfree[b], ((j >> 1) - 1) & 1, 7, j);
-          MBW(od, (j - 1) & 1, 2, j);
+          // O may be read and rewritten once PV_{j-1} is done (its commit covers every earlier MMA).  Its
+          // per-buffer barrier cannot have run ahead: PV_{j-1+kSB} needs P of a later tile.
+          MBW(&pfree[(j - 1) % kSB], ((j - 1) / kSB) & 1, 2, j);
           tc_after();
           const float alpha = grow ? ex2(m_ref - mt) : 1.f;
           for (uint32_t cb = 0; cb < D; cb += 32) {
@@ -699,7 +700,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     // epilogue: O / l -> output dtype; LSE (natural log) = ln 2 * (m_ref + log2 l), l = sum of both halves
     // PV_{n-1} done (its commit covers every earlier MMA); the per-buffer barrier has completed at least
     // PV_{n-3}'s phase, so its parity cannot alias
-    if (n_tiles) MBW(&pfree[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1, 8, n_tiles);
+    if (n_tiles) MBW(&pfree[(n_tiles - 1) % kSB], ((n_tiles - 1) / kSB) & 1, 8, n_tiles);
     tc_after();
     // l = sum of the rounded weights (O's ones column); every row has l >= 1 (its maximum contributes 2^0)
     const float ltot = __uint_as_float(tmem_ld1(t_o + lane_base + D)), inv = 1.f / ltot;
@@ -845,22 +846,22 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       // Blocking waits where only one event can come next (no polling: a spinning issuer took 10% of the
       // SM's issue slots): after S_{j+1} only PV_j can follow; with every issued S matched by its PV only
       // S can.  With both possible (after PV_j: S_{j+2} or PV_{j+1}), S operands are usually ready already.
-      const bool s_ok = ns < n_tiles && ns <= npv + 1, pv_ok = npv < ns;
+      const bool s_ok = ns < n_tiles && ns <= npv + kSB - 1, pv_ok = npv < ns;
       bool do_s;
       if (!pv_ok) {
         MBW(&kvf[ns % kOpBufs], (ns / kOpBufs) & 1, 9, ns);
         do_s = true;
       } else if (!s_ok) {
-        MBW(&pf[npv & 1], (npv >> 1) & 1, 10, npv);
+        MBW(&pf[npv % kSB], (npv / kSB) & 1, 10, npv);
         do_s = false;
       } else {
         while (true) {
           if (mbar_test_u(&kvf[ns % kOpBufs], (ns / kOpBufs) & 1)) { do_s = true; break; }
-          if (mbar_wait_hint_u(&pf[npv & 1], (npv >> 1) & 1, 100)) { do_s = false; break; }
+          if (mbar_wait_hint_u(&pf[npv % kSB], (npv / kSB) & 1, 100)) { do_s = false; break; }
         }
       }
       if (do_s) {
-        const uint32_t b = ns & 1, ob = ns % kOpBufs;
+        const uint32_t b = ns % kSB, ob = ns % kOpBufs;
         TR(4, ns);
         tc_after();
         const uint32_t ka = saddr(skb + ob * (kKT * D * 2));
@@ -872,12 +873,12 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         wd0 = clock64();
 #endif
 #ifdef HARAG_ATT_MMASYNC
-        MBW(&sf[b], (ns >> 1) & 1, 5, ns);  // pipeline study: time the MMA alone
+        MBW(&sf[b], (ns / kSB) & 1, 5, ns);  // pipeline study: time the MMA alone
         TR(12, ns);
 #endif
         ++ns;
       } else {
-        const uint32_t bb = npv & 1, ob = npv % kOpBufs;
+        const uint32_t bb = npv % kSB, ob = npv % kOpBufs;
         TR(5, npv);
         tc_after();
         const uint32_t va = saddr(svb + ob * vbuf);
@@ -886,12 +887,11 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
                      (npv > 0 || s > 0) ? 1u : 0u);  // A = P_npv from TMEM: 16 keys = 8 columns per k-step
         mma_commit(&kve[ob]);
         mma_commit(&pfree[bb]);
-        mma_commit(od);
 #ifdef HARAG_ATT_WATCHDOG
         wd0 = clock64();
 #endif
 #ifdef HARAG_ATT_MMASYNC
-        MBW(&pfree[bb], (npv >> 1) & 1, 6, npv);
+        MBW(&pfree[bb], (npv / kSB) & 1, 6, npv);
         TR(13, npv);
 #endif
         ++npv;
