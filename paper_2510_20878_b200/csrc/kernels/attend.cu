@@ -445,8 +445,20 @@ static_assert(kTP + 32 * kSB <= kTmemCols, "TMEM columns");
 #define HARAG_ATT_TAU_BF16 32
 #endif
 
+// a retrieved doc's code / meta pointers for this unit's slab and its K, V schemes, staged in shared memory
+// once per CTA (the per-tile descriptor reads were dependent global loads ahead of every staging copy)
+struct DocSrc {
+  const uint8_t *kc, *vc, *km, *vm;
+  uint32_t ks, vs;
+};
+constexpr uint32_t kMaxDocs = 64;  // k <= 64 retrieved chunks per request
+struct SchemeOf {
+  uint32_t scheme;
+};
+
 size_t att_smem_bytes(uint32_t D) {
-  return kOpBufs * (size_t)kKT * (2 * D + 16) * 2 + kBarSlots * 8 + 16 + kDecGroups * kStageBytes;
+  return kOpBufs * (size_t)kKT * (2 * D + 16) * 2 + kBarSlots * 8 + 16 + kDecGroups * kStageBytes +
+         kMaxDocs * sizeof(DocSrc);
 }
 
 // 2^x on the SFU (MUFU.EX2, relative error ~2^-22, far inside R28's 2^-9 budget)
@@ -545,6 +557,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
   uint64_t *kvf = pfree + kSB, *kve = kvf + kOpBufs, *qf = kve + kOpBufs;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + kBarSlots);
   uint8_t* stage0 = reinterpret_cast<uint8_t*>(bar + kBarSlots + 2);  // 16-B aligned decoder staging
+  DocSrc* dsrc = reinterpret_cast<DocSrc*>(stage0 + kDecGroups * kStageBytes);  // [k]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   const uint32_t unit = blockIdx.x;  // (request, layer, head)
@@ -724,37 +737,36 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     // ------------------------------------------------------------------ decoder warps
     const uint32_t grp = (uint32_t)(warp - kSoftWarps) / kDecWarps;   // tiles j with j % kDecGroups == grp
     const uint32_t dt = tid - 32 * kSoftWarps - 32 * kDecWarps * grp;  // 0..127 within the group
-    auto tile_src = [&](uint32_t j, const AsmDesc*& dk, const AsmDesc*& dv, uint32_t& t0) {
-      const uint32_t slot = j / tiles_per_doc;
-      t0 = (j - slot * tiles_per_doc) * kKT;
-      dk = &p.descs[((uint64_t)r * p.k + slot) * 2];
-      dv = dk + 1;
-    };
+    {
+      const uint32_t nd = 32 * kDecGroups * kDecWarps, di = tid - 32 * kSoftWarps;
+      for (uint32_t slot = di; slot < p.k; slot += nd) {
+        const AsmDesc dk = p.descs[((uint64_t)r * p.k + slot) * 2], dv = p.descs[((uint64_t)r * p.k + slot) * 2 + 1];
+        DocSrc d;
+        d.kc = dk.codes + (uint64_t)slab_i * p.code_slab[dk.scheme];
+        d.vc = dv.codes + (uint64_t)slab_i * p.code_slab[dv.scheme];
+        d.km = dk.meta + (uint64_t)slab_i * p.meta_stride[dk.scheme];
+        d.vm = dv.meta + (uint64_t)slab_i * p.meta_stride[dv.scheme];
+        d.ks = dk.scheme, d.vs = dv.scheme;
+        dsrc[slot] = d;
+      }
+      named_bar(8, nd);
+    }
     auto prefetch = [&](uint32_t j) {
-      const AsmDesc *dk, *dv;
-      uint32_t t0;
-      tile_src(j, dk, dv, t0);
-      const uint32_t n_el = kKT * D;
-      prefetch_l2(dk->codes + (uint64_t)slab_i * p.code_slab[dk->scheme] + code_bytes_of(dk->scheme, t0 * D),
-                  code_bytes_of(dk->scheme, n_el));
-      prefetch_l2(dv->codes + (uint64_t)slab_i * p.code_slab[dv->scheme] + code_bytes_of(dv->scheme, t0 * D),
-                  code_bytes_of(dv->scheme, n_el));
+      const uint32_t slot = j / tiles_per_doc, t0 = (j - slot * tiles_per_doc) * kKT;
+      const DocSrc& d = dsrc[slot];
+      prefetch_l2(d.kc + code_bytes_of(d.ks, t0 * D), code_bytes_of(d.ks, kKT * D));
+      prefetch_l2(d.vc + code_bytes_of(d.vs, t0 * D), code_bytes_of(d.vs, kKT * D));
     };
     if (dt == 0)
       for (uint32_t j = grp; j < kPF && j < n_tiles; j += kDecGroups) prefetch(j);
     uint32_t cur_slot = 0xFFFFFFFFu;
     for (uint32_t j = grp; j < n_tiles; j += kDecGroups) {
       const uint32_t b = j % kOpBufs, use = j / kOpBufs;  // use-th fill of operand buffer b
-      const AsmDesc *dkp, *dvp;
-      uint32_t t0;
-      tile_src(j, dkp, dvp, t0);
-      const AsmDesc dk = *dkp, dv = *dvp;
+      const uint32_t slot = j / tiles_per_doc, t0 = (j - slot * tiles_per_doc) * kKT;
+      const DocSrc ds = dsrc[slot];
+      const SchemeOf dk{ds.ks}, dv{ds.vs};
       if (dt == 0 && j + kPF < n_tiles) prefetch(j + kPF);
-      const uint8_t* kc = dk.codes + (uint64_t)slab_i * p.code_slab[dk.scheme];
-      const uint8_t* vc = dv.codes + (uint64_t)slab_i * p.code_slab[dv.scheme];
-      const uint8_t* km = dk.meta + (uint64_t)slab_i * p.meta_stride[dk.scheme];
-      const uint8_t* vm = dv.meta + (uint64_t)slab_i * p.meta_stride[dv.scheme];
-      const uint32_t slot = j / tiles_per_doc;
+      const uint8_t *kc = ds.kc, *vc = ds.vc, *km = ds.km, *vm = ds.vm;
       // all of this thread's loads in flight at once: cp.async into its own staging slots
       uint8_t* stc = stage0 + grp * kStageBytes;                         // [K, V] staged code tiles (stage_off)
       uint8_t* smk = stc + 2 * kDecChunks * 32 * kDecWarps * 8;           // K meta window
@@ -781,7 +793,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         for (uint32_t byte = dt; byte < 256; byte += 32 * kDecWarps) {  // bytes dt, dt + group size, ...
 #pragma unroll
           for (uint32_t kv = 0; kv < 2; ++kv) {
-            const AsmDesc& d = kv ? dv : dk;
+            const SchemeOf& d = kv ? dv : dk;
             if (d.scheme != HR_S_GSE8) continue;
             const float T = __ldg(reinterpret_cast<const float*>((kv ? vm : km) + 16) + (byte >> p.gse_m));
             // fma(f, T, +0): the decode of hr_assemble_kv (a (sign 1, field 0) byte gives +0), then RNE
@@ -793,7 +805,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         (void)fm;
         if (dt < 64) {  // the fp32 scale tables (2^(e+1) entries, zero-filled to 32) of its K and V slab
           const uint32_t kv = dt >> 5, i = dt & 31;
-          const AsmDesc& d = kv ? dv : dk;
+          const SchemeOf& d = kv ? dv : dk;
           reinterpret_cast<float*>(kv ? vtv : vtk)[i] =
               (d.scheme == HR_S_GSE8 && i < (2u << p.gse_e)) ? __ldg(reinterpret_cast<const float*>((kv ? vm : km) + 16) + i)
                                                                : 0.f;
@@ -920,6 +932,7 @@ void launch_attend(const AttnParams& p, cudaStream_t st) {
   require(p.D == 64 || p.D == 128, HR_EINVAL, "attend: head_dim must be 64 or 128");
   require(p.T % kKT == 0, HR_EINVAL, "attend: tokens per chunk must be a multiple of 64");
   require(p.M >= 1 && p.M <= kRows, HR_EINVAL, "attend: g * n_q must be in [1, 128]");
+  require(p.k >= 1 && p.k <= kMaxDocs, HR_EINVAL, "attend: k must be in [1, 64]");
   const size_t smem = att_smem_bytes(p.D);
   const uint64_t units = (uint64_t)p.n_req * p.L * p.Hl;
   if (!units) return;
