@@ -199,18 +199,23 @@ constexpr int kSoftWarps = HARAG_ATT_SOFT_WARPS, kDecWarps = HARAG_ATT_DEC_WARPS
 static_assert(kSoftWarps == 4, "one softmax warp per TMEM lane quadrant");
 // with <= 17 warps per CTA (>= 120 registers per thread) a softmax thread holds its whole 64-column S row
 constexpr bool kWideSoftmax = kDecGroups * kDecWarps <= 16;
-constexpr int kAttThreads2 = 32 * (kSoftWarps + kDecGroups * kDecWarps + 1);
+// + one MMA issuer warp + one producer warp (TMA bulk copies of the code tiles into the stage ring)
+constexpr int kAttThreads2 = 32 * (kSoftWarps + kDecGroups * kDecWarps + 2);
+constexpr int kIssuerWarp = kSoftWarps + kDecGroups * kDecWarps, kProducerWarp = kIssuerWarp + 1;
 constexpr uint32_t kDecChunks = kKT * 128 / 8 / (32 * kDecWarps);  // 8-element chunks per decoder thread at D = 128
 // per decoder group: codes slots [K, V][kDecChunks][thread] x 16 B, meta slots x 8 B
 // per decoder group: codes slots [K, V][kDecChunks][thread] x 8 B, the tile's meta windows [K, V] x 2 KB
 // (<= 256 groups x 8 B), the doc's GSE-8 value tables [K, V][256] x 16-bit
 constexpr uint32_t kMetaWin = 2048;
-constexpr uint32_t kStageBytes = 2 * kDecChunks * 32 * kDecWarps * 8 + 2 * kMetaWin + 2 * 256 * 2;
+constexpr uint32_t kStageBytes = 2 * kMetaWin + 2 * 256 * 2;  // per decoder group: meta windows, value tables
+// Stage ring of code tiles, filled by the producer warp with TMA bulk copies (cp.async.bulk): slot =
+// [K codes, 8 KB][V codes, 8 KB], each the tile's contiguous [64 keys][D] codes (1 B, or 1/2 B for INT4)
+constexpr uint32_t kStages = 4, kSlotBytes = 2 * kKT * 128, kSlotV = kKT * 128;
 #ifndef HARAG_ATT_OPBUFS
 #define HARAG_ATT_OPBUFS 4
 #endif
 constexpr uint32_t kOpBufs = HARAG_ATT_OPBUFS;  // K/V operand buffers: decode of tile j waits for PV_{j-kOpBufs}
-constexpr uint32_t kBarSlots = 24;             // mbarrier slots (8 B each) ahead of the TMEM slot
+constexpr uint32_t kBarSlots = 32;             // mbarrier slots (8 B each) ahead of the TMEM slot
 
 // The four bytes of w as exact floats (minus `bias`): 0x4B0000bb is 2^23 + bb, so one PRMT and one
 // (packed) subtraction replace an I2F per element.  bias 2^23 for unsigned bytes; 2^23 + 128 for
@@ -311,18 +316,6 @@ __device__ __forceinline__ uint4 dec_raw8(uint32_t scheme, const uint4& c, const
   }
 }
 
-// Byte offset of chunk (key, dc) — 8 elements, 8 B of 1-byte codes or 4 B of INT4 — in a staged code tile.
-// Each key's row of D/8 chunks is stored contiguously but with its chunks permuted (XOR swizzle), so that
-// (a) the cp.async copies, where a warp's 32 lanes take 32 consecutive chunks of the contiguous global
-// tile, write whole 128-B lines, and (b) the decode reads, where a warp's lanes take 8 keys x 4 chunk
-// columns, hit distinct banks (2 wavefronts per LDS.64, 1 per LDS.32).
-template <uint32_t D>
-__device__ __forceinline__ uint32_t stage_off(bool int4, uint32_t key, uint32_t dc) {
-  constexpr uint32_t dcs = D / 8;
-  if (int4) return (key * dcs + (dc ^ (D == 128 ? ((key >> 1) & 3u) << 2 : ((key >> 2) & 1u) << 2))) * 4;
-  return (key * dcs + (dc ^ (D == 128 ? (key & 7u) << 1 : ((key >> 1) & 3u) << 1))) * 8;
-}
-
 // Decode one operand tile (this decoder thread's kDecChunks chunks of 8 elements) with the scheme
 // resolved ONCE per tile: a runtime switch over compile-time-specialised loops (a per-chunk switch
 // made the decode loop branch-bound).  VMAJ: V's MN-major layout, else K's K-major layout.
@@ -336,15 +329,24 @@ __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, cons
   for (uint32_t i = 0; i < nch; ++i) {
     const uint32_t cc = dt + i * 32 * kDecWarps;
     {
-      const uint32_t gI = cc >> 5, ii = cc & 7, jj = (cc >> 3) & 3;
-      const uint32_t key = (gI % (kKT / 8)) * 8 + ii, dc = (gI / (kKT / 8)) * 4 + jj;
+      // K: a warp takes whole key rows (conflict-free reads of the contiguous stage slot; a quarter warp
+      // writes one 128-B swizzled row of the K-major tile).  V: a warp takes 8 keys x 4 chunk columns (a
+      // quarter warp writes 8 rows of one MN-major core matrix; the stage reads conflict 4-way).
+      uint32_t key, dc;
+      if (VMAJ) {
+        const uint32_t gI = cc >> 5, ii = cc & 7, jj = (cc >> 3) & 3;
+        key = (gI % (kKT / 8)) * 8 + ii, dc = (gI / (kKT / 8)) * 4 + jj;
+      } else {
+        key = cc / dcs, dc = cc % dcs;
+      }
       uint4 v;
       if constexpr (SCH == HR_S_PASS16) {  // bits unchanged: straight from global (L2-prefetched) into the operand tile
         v = __ldg(reinterpret_cast<const uint4*>(g16 + 2ull * ((t0 + key) * D + dc * 8)));
       } else {
         uint2 raw;
-        if constexpr (SCH == HR_S_INT4) raw.x = *reinterpret_cast<const uint32_t*>(stc + stage_off<D>(true, key, dc));
-        else raw = *reinterpret_cast<const uint2*>(stc + stage_off<D>(false, key, dc));
+        // the stage slot holds the tile's codes contiguously: [key][D] (1 B, or 1/2 B for INT4)
+        if constexpr (SCH == HR_S_INT4) raw.x = *reinterpret_cast<const uint32_t*>(stc + (key * dcs + dc) * 4);
+        else raw = *reinterpret_cast<const uint2*>(stc + (key * dcs + dc) * 8);
         if constexpr (SCH == HR_S_GSE8) {
 #ifndef HARAG_ATT_GSE_ARITH
           // the slab's 256-entry table of decoded 16-bit values: one LDS.U16 per element (bank conflicts)
@@ -396,15 +398,7 @@ template <int N>
 __device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(saddr(smem)), "l"(gmem), "n"(N) : "memory");
 }
-__device__ __forceinline__ void stage_chunk(uint32_t scheme, const uint8_t* codes, uint32_t e, uint8_t* sc) {
-  if (scheme == HR_S_PASS16) {
-    // copied straight into the operand buffer once it is free (dec_tile_s<PASS16>)
-  } else if (scheme == HR_S_INT4) {
-    cp_async<4>(sc, codes + e / 2);
-  } else {
-    cp_async<8>(sc, codes + e);
-  }
-}
+
 // the tile's window of group meta (INT8: fp32 scale, INT4: (scale, min) per group) -> shared memory,
 // 4-byte copies spread over the group's threads; returns the first group index of the window
 __device__ __forceinline__ uint32_t stage_meta(uint32_t scheme, const uint8_t* meta, uint32_t t0, uint32_t D,
@@ -457,7 +451,7 @@ struct SchemeOf {
 };
 
 size_t att_smem_bytes(uint32_t D) {
-  return kOpBufs * (size_t)kKT * (2 * D + 16) * 2 + kBarSlots * 8 + 16 + kDecGroups * kStageBytes +
+  return kOpBufs * (size_t)kKT * (2 * D + 16) * 2 + kBarSlots * 8 + 16 + kStages * kSlotBytes + kDecGroups * kStageBytes +
          kMaxDocs * sizeof(DocSrc);
 }
 
@@ -522,6 +516,16 @@ __device__ __forceinline__ bool mbar_wait_hint_u(uint64_t* bar, uint32_t parity,
 __device__ __forceinline__ bool mbar_test_u(uint64_t* bar, uint32_t parity) {
   return __shfl_sync(0xFFFFFFFFu, (int)mbar_test(bar, parity), 0) != 0;
 }
+__device__ __forceinline__ void ptx_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)), "r"(bytes) : "memory");
+}
+// TMA 1-D bulk copy global -> shared (bytes: multiple of 16, both addresses 16-B aligned)
+__device__ __forceinline__ void ptx_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   saddr(dst)),
+               "l"(src), "r"(bytes), "r"(saddr(bar))
+               : "memory");
+}
 __device__ __forceinline__ void named_bar(uint32_t id, uint32_t n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
@@ -552,11 +556,13 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
   constexpr uint32_t vdcs = D / 8 + 2, vbuf = kKT * (D + 16) * 2;
   uint8_t* svb = skb + kOpBufs * kKT * D * 2;
   uint64_t* bar = reinterpret_cast<uint64_t*>(svb + kOpBufs * vbuf);
-  static_assert(3 * kSB + 2 * kOpBufs + 1 <= kBarSlots, "mbarrier slots");
+  static_assert(3 * kSB + 2 * kOpBufs + 1 + 2 * kStages <= kBarSlots, "mbarrier slots");
   uint64_t *sf = bar, *pf = sf + kSB, *pfree = pf + kSB;  // per S/P buffer: S ready, P ready, PV done
   uint64_t *kvf = pfree + kSB, *kve = kvf + kOpBufs, *qf = kve + kOpBufs;
+  uint64_t *stf = qf + 1, *ste = stf + kStages;  // stage ring: full (TMA bytes landed), empty (decoded)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + kBarSlots);
-  uint8_t* stage0 = reinterpret_cast<uint8_t*>(bar + kBarSlots + 2);  // 16-B aligned decoder staging
+  uint8_t* ring = reinterpret_cast<uint8_t*>(bar + kBarSlots + 2);     // 16-B aligned stage ring
+  uint8_t* stage0 = ring + kStages * kSlotBytes;                        // per-group meta windows / tables
   DocSrc* dsrc = reinterpret_cast<DocSrc*>(stage0 + kDecGroups * kStageBytes);  // [k]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
@@ -585,6 +591,10 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       mbar_init(&kve[b], 1);
     }
     mbar_init(qf, kSoftWarps);  // every softmax warp loads a share of Q
+    for (uint32_t s = 0; s < kStages; ++s) {
+      mbar_init(&stf[s], 1);
+      mbar_init(&ste[s], kDecWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (p.descs[0].count != nullptr && l == 0 && h == 0) {  // a1: hotness of this request's items
       for (uint32_t j = 0; j < 2 * p.k; ++j) {
@@ -751,35 +761,18 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       }
       named_bar(8, nd);
     }
-    auto prefetch = [&](uint32_t j) {
-      const uint32_t slot = j / tiles_per_doc, t0 = (j - slot * tiles_per_doc) * kKT;
-      const DocSrc& d = dsrc[slot];
-      prefetch_l2(d.kc + code_bytes_of(d.ks, t0 * D), code_bytes_of(d.ks, kKT * D));
-      prefetch_l2(d.vc + code_bytes_of(d.vs, t0 * D), code_bytes_of(d.vs, kKT * D));
-    };
-    if (dt == 0)
-      for (uint32_t j = grp; j < kPF && j < n_tiles; j += kDecGroups) prefetch(j);
     uint32_t cur_slot = 0xFFFFFFFFu;
     for (uint32_t j = grp; j < n_tiles; j += kDecGroups) {
       const uint32_t b = j % kOpBufs, use = j / kOpBufs;  // use-th fill of operand buffer b
       const uint32_t slot = j / tiles_per_doc, t0 = (j - slot * tiles_per_doc) * kKT;
       const DocSrc ds = dsrc[slot];
       const SchemeOf dk{ds.ks}, dv{ds.vs};
-      if (dt == 0 && j + kPF < n_tiles) prefetch(j + kPF);
       const uint8_t *kc = ds.kc, *vc = ds.vc, *km = ds.km, *vm = ds.vm;
-      // all of this thread's loads in flight at once: cp.async into its own staging slots
-      uint8_t* stc = stage0 + grp * kStageBytes;                         // [K, V] staged code tiles (stage_off)
-      uint8_t* smk = stc + 2 * kDecChunks * 32 * kDecWarps * 8;           // K meta window
+      uint8_t* stc = ring + (j % kStages) * kSlotBytes;                  // [K, V] code tiles (producer's TMA)
+      uint8_t* smk = stage0 + grp * kStageBytes;                          // K meta window
       uint8_t* smv = smk + kMetaWin;                                      // V meta window
       uint16_t* vtk = reinterpret_cast<uint16_t*>(smv + kMetaWin);        // [256] K value table
       uint16_t* vtv = vtk + 256;                                          // [256] V value table
-#pragma unroll
-      for (uint32_t i = 0; i < kKT * dcs / (32 * kDecWarps); ++i) {  // a warp copies 32 consecutive chunks
-        const uint32_t c = dt + i * 32 * kDecWarps, key = c / dcs, dc = c % dcs;
-        const uint32_t e = (t0 + key) * D + dc * 8;
-        stage_chunk(dk.scheme, kc, e, stc + stage_off<D>(dk.scheme == HR_S_INT4, key, dc));
-        stage_chunk(dv.scheme, vc, e, stc + kDecChunks * 32 * kDecWarps * 8 + stage_off<D>(dv.scheme == HR_S_INT4, key, dc));
-      }
       // (the previous tile's decode is done with the meta windows: the kvf arrive of that tile followed it
       // in every thread, and the named barrier below orders the group)
       named_bar(1 + grp, 32 * kDecWarps);
@@ -815,8 +808,9 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       if (dt == 0) TR(6, j);
       if (use >= 1) MBW(&kve[b], (use - 1) & 1, 3, j);  // PV_{j-3} (and S_{j-3}) done: buffer b free
       if (dt == 0) TR(2, j);
-      asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's staged chunks have landed
+      asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's meta share has landed
       named_bar(1 + grp, 32 * kDecWarps);               // ... and every thread's meta / value-table share
+      MBW(&stf[j % kStages], (j / kStages) & 1, 11, j);  // the code tiles have landed
       if (dt == 0) TR(7, j);
       uint8_t* skd = skb + b * (kKT * D * 2);
       uint8_t* svd = svb + b * vbuf;
@@ -825,15 +819,57 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         if (p.kv_dump)
           dump = p.kv_dump + ((((uint64_t)r * 2) * p.L + l) * p.Hl + h) * p.k * p.T * D + ((uint64_t)slot * p.T + t0) * D;
         const uint64_t kvoff = (uint64_t)p.L * p.Hl * p.k * p.T * D;
-        const uint32_t vo = kDecChunks * 32 * kDecWarps;
         dec_tile<DT, false, D>(dk.scheme, stc, smk, vtk, p.gse_m, p.g_shift, gk0, skd, dt, dump, kc, t0);
-        dec_tile<DT, true, D>(dv.scheme, stc + vo * 8, smv, vtv, p.gse_m, p.g_shift, gv0, svd, dt,
+        dec_tile<DT, true, D>(dv.scheme, stc + kSlotV, smv, vtv, p.gse_m, p.g_shift, gv0, svd, dt,
                               dump ? dump + kvoff : nullptr, vc, t0);
       }
       fence_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive1(&kvf[b]);
+      if (lane == 0) {
+        mbar_arrive1(&kvf[b]);
+        mbar_arrive1(&ste[j % kStages]);  // this warp's reads of the stage slot are done
+      }
       if (dt == 0) TR(3, j);
+    }
+  } else if (warp == kProducerWarp) {
+    // ------------------------------------------------------------------ producer (one lane)
+    // tile j's K and V code tiles -> stage slot j % kStages (TMA bulk copies, completion counted in bytes on
+    // stf), once the decoder group of tile j - kStages has released the slot; L2 prefetch kPF tiles ahead
+    if (lane == 0) {
+      auto tile_ptrs = [&](uint32_t j, const uint8_t*& kp, const uint8_t*& vp, uint32_t& kb, uint32_t& vb) {
+        const uint32_t slot = j / tiles_per_doc, t0 = (j - slot * tiles_per_doc) * kKT;
+        const AsmDesc* d = &p.descs[((uint64_t)r * p.k + slot) * 2];
+        const uint32_t ks = d[0].scheme, vs = d[1].scheme;
+        kp = d[0].codes + (uint64_t)slab_i * p.code_slab[ks] + code_bytes_of(ks, t0 * D);
+        vp = d[1].codes + (uint64_t)slab_i * p.code_slab[vs] + code_bytes_of(vs, t0 * D);
+        kb = ks == HR_S_PASS16 ? 0u : code_bytes_of(ks, kKT * D);  // PASS16 tiles are read in place
+        vb = vs == HR_S_PASS16 ? 0u : code_bytes_of(vs, kKT * D);
+      };
+      for (uint32_t j = 0; j < kPF && j < n_tiles; ++j) {
+        const uint8_t *kp, *vp;
+        uint32_t kb, vb;
+        tile_ptrs(j, kp, vp, kb, vb);
+        if (kb) prefetch_l2(kp, kb);
+        if (vb) prefetch_l2(vp, vb);
+      }
+      for (uint32_t j = 0; j < n_tiles; ++j) {
+        const uint32_t sl = j % kStages, u = j / kStages;
+        if (j + kPF < n_tiles) {
+          const uint8_t *kp, *vp;
+          uint32_t kb, vb;
+          tile_ptrs(j + kPF, kp, vp, kb, vb);
+          if (kb) prefetch_l2(kp, kb);
+          if (vb) prefetch_l2(vp, vb);
+        }
+        const uint8_t *kp, *vp;
+        uint32_t kb, vb;
+        tile_ptrs(j, kp, vp, kb, vb);
+        if (u >= 1) MBW(&ste[sl], (u - 1) & 1, 12, j);
+        ptx_arrive_expect_tx(&stf[sl], kb + vb);
+        uint8_t* dst = ring + sl * kSlotBytes;
+        if (kb) ptx_bulk_g2s(dst, kp, kb, &stf[sl]);
+        if (vb) ptx_bulk_g2s(dst + kSlotV, vp, vb, &stf[sl]);
+      }
     }
   } else {
     // ------------------------------------------------------------------ MMA issuer
