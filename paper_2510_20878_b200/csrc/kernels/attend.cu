@@ -87,6 +87,42 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
       : "memory");
 }
 
+
+// N back-to-back MMAs D += A_i . B_i (A from TMEM, B from shared memory) under ONE elect.sync: the first
+// accumulates iff acc0, the rest always (fewer issue slots per MMA than one elect per instruction)
+template <int N>
+__device__ __forceinline__ void mma_ts_batch(uint32_t d, const uint32_t (&a)[N], const uint64_t (&b)[N], uint32_t id,
+                                             uint32_t acc0);
+template <>
+__device__ __forceinline__ void mma_ts_batch<4>(uint32_t d, const uint32_t (&a)[4], const uint64_t (&b)[4], uint32_t id,
+                                                uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %10, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %5, %9, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %6, %9, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%3], %7, %9, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%4], %8, %9, 1;\n\t}" ::"r"(d),
+      "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "l"(b[0]), "l"(b[1]), "l"(b[2]), "l"(b[3]), "r"(id), "r"(acc0)
+      : "memory");
+}
+template <>
+__device__ __forceinline__ void mma_ts_batch<8>(uint32_t d, const uint32_t (&a)[8], const uint64_t (&b)[8], uint32_t id,
+                                                uint32_t acc0) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\tsetp.ne.b32 p, %18, 0;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %9, %17, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%2], %10, %17, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%3], %11, %17, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%4], %12, %17, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%5], %13, %17, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%6], %14, %17, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%7], %15, %17, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%8], %16, %17, 1;\n\t}" ::"r"(d),
+      "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(a[4]), "r"(a[5]), "r"(a[6]), "r"(a[7]), "l"(b[0]), "l"(b[1]),
+      "l"(b[2]), "l"(b[3]), "l"(b[4]), "l"(b[5]), "l"(b[6]), "l"(b[7]), "r"(id), "r"(acc0)
+      : "memory");
+}
+
 #define HR_R8(i) "=r"(v[i]), "=r"(v[i + 1]), "=r"(v[i + 2]), "=r"(v[i + 3]), "=r"(v[i + 4]), "=r"(v[i + 5]), \
                  "=r"(v[i + 6]), "=r"(v[i + 7])
 #define HR_W8(i) "r"(v[i]), "r"(v[i + 1]), "r"(v[i + 2]), "r"(v[i + 3]), "r"(v[i + 4]), "r"(v[i + 5]), \
@@ -144,15 +180,6 @@ __device__ __forceinline__ void tmem_st1(uint32_t taddr, uint32_t v) {
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 // D (TMEM) += A (TMEM: lanes = rows, 32-bit columns = pairs of 16-bit K elements) . B (shared memory)
-__device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b, uint32_t id, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "r"(a_tmem), "l"(b), "r"(id), "r"(acc)
-      : "memory");
-}
 
 template <int DT>
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
@@ -202,9 +229,7 @@ constexpr bool kWideSoftmax = kDecGroups * kDecWarps <= 16;
 // + one MMA issuer warp + one producer warp (TMA bulk copies of the code tiles into the stage ring)
 constexpr int kAttThreads2 = 32 * (kSoftWarps + kDecGroups * kDecWarps + 2);
 constexpr int kIssuerWarp = kSoftWarps + kDecGroups * kDecWarps, kProducerWarp = kIssuerWarp + 1;
-constexpr uint32_t kDecChunks = kKT * 128 / 8 / (32 * kDecWarps);  // 8-element chunks per decoder thread at D = 128
-// per decoder group: codes slots [K, V][kDecChunks][thread] x 16 B, meta slots x 8 B
-// per decoder group: codes slots [K, V][kDecChunks][thread] x 8 B, the tile's meta windows [K, V] x 2 KB
+// per decoder group: the tile's meta windows [K, V] x 2 KB
 // (<= 256 groups x 8 B), the doc's GSE-8 value tables [K, V][256] x 16-bit
 constexpr uint32_t kMetaWin = 2048;
 constexpr uint32_t kStageBytes = 2 * kMetaWin + 2 * 256 * 2;  // per decoder group: meta windows, value tables
@@ -547,7 +572,6 @@ __device__ long long g_tr[14][96];  // per-tile event clocks of CTA 0 (pipeline 
 template <int DT, uint32_t D>
 __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_constant__ AttnParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  constexpr uint32_t dcs = D / 8;
   // Q (A of S = Q K^T) lives in TMEM columns [kTQ, kTQ + D/2): lane = query row, column c = elements 2c, 2c+1
   uint8_t* skb = smem_raw;                         // kOpBufs x [64 keys][D] K-major (B of S = Q K^T)
   // kOpBufs x [64 keys][D + 16] MN-major (B of O += P V): column D is all ones, D + 1 .. D + 15 zero, so
@@ -913,9 +937,16 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         TR(4, ns);
         tc_after();
         const uint32_t ka = saddr(skb + ob * (kKT * D * 2));
-        for (uint32_t s = 0; s < D / 16; ++s)  // A = Q from TMEM (8 columns per k-step); K-major SW128 K
-          mma_f16_ts(tmem + b * kKT, tmem + kTQ + s * 8, sdesc_sw128(ka + (s >> 2) * (kKT * 128) + (s & 3) * 32),
-                     id_s, s > 0);
+        {  // A = Q from TMEM (8 columns per k-step); K-major SW128 K
+          uint32_t a[D / 16];
+          uint64_t bd[D / 16];
+#pragma unroll
+          for (uint32_t s = 0; s < D / 16; ++s) {
+            a[s] = tmem + kTQ + s * 8;
+            bd[s] = sdesc_sw128(ka + (s >> 2) * (kKT * 128) + (s & 3) * 32);
+          }
+          mma_ts_batch<D / 16>(tmem + b * kKT, a, bd, id_s, 0u);
+        }
         mma_commit(&sf[b]);
 #ifdef HARAG_ATT_WATCHDOG
         wd0 = clock64();
@@ -930,9 +961,16 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         TR(5, npv);
         tc_after();
         const uint32_t va = saddr(svb + ob * vbuf);
-        for (uint32_t s = 0; s < kKT / 16; ++s)
-          mma_f16_ts(t_o, tmem + kTP + bb * (kKT / 2) + s * 8, sdesc(va + s * 2 * vdcs * 128, vdcs * 128, 128), id_o,
-                     (npv > 0 || s > 0) ? 1u : 0u);  // A = P_npv from TMEM: 16 keys = 8 columns per k-step
+        {  // A = P_npv from TMEM: 16 keys = 8 columns per k-step
+          uint32_t a[kKT / 16];
+          uint64_t bd[kKT / 16];
+#pragma unroll
+          for (uint32_t s = 0; s < kKT / 16; ++s) {
+            a[s] = tmem + kTP + bb * (kKT / 2) + s * 8;
+            bd[s] = sdesc(va + s * 2 * vdcs * 128, vdcs * 128, 128);
+          }
+          mma_ts_batch<kKT / 16>(t_o, a, bd, id_o, npv > 0 ? 1u : 0u);
+        }
         mma_commit(&kve[ob]);
         mma_commit(&pfree[bb]);
 #ifdef HARAG_ATT_WATCHDOG
