@@ -215,13 +215,13 @@ __device__ __forceinline__ float hi_f(uint32_t w) {
 #define HARAG_ATT_SOFT_WARPS 4
 #endif
 #ifndef HARAG_ATT_DEC_WARPS
-#define HARAG_ATT_DEC_WARPS 8
+#define HARAG_ATT_DEC_WARPS 4
 #endif
 #ifndef HARAG_ATT_DEC_GROUPS
 #define HARAG_ATT_DEC_GROUPS 3
 #endif
-// measured (tools/prof_attend.py 8, C2 shape, session-2 kernel): 4 softmax + 3 x 8 decoder warps 2.14 ms;
-// 4 + 2 x 8: 2.38 ms; 4 + 2 x 4: 2.53 ms; 8 + 2 x 4: 2.63 ms; 4 + 1 x 8: 2.89 ms; 4 + 3 x 4: 2.59 ms
+// measured (tools/prof_attend.py 8, C2 shape, TMA stage ring): 3 x 4 decoder warps 1.447 ms (default: 18 warps,
+// so the softmax threads hold a whole S row), 4 x 4 1.455, 3 x 8 1.477, 2 x 8 1.624 ms
 constexpr int kSoftWarps = HARAG_ATT_SOFT_WARPS, kDecWarps = HARAG_ATT_DEC_WARPS, kDecGroups = HARAG_ATT_DEC_GROUPS;
 static_assert(kSoftWarps == 4, "one softmax warp per TMEM lane quadrant");
 // with <= 17 warps per CTA (>= 120 registers per thread) a softmax thread holds its whole 64-column S row
@@ -662,7 +662,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     const float c = p.scale_log2;
     constexpr float kPMax = DT == HR_BF16 ? (float)(1ull << HARAG_ATT_TAU_BF16) : 256.f;  // 2^tau
     float m_ref = -INFINITY;
-    // P_j = 2^(s c - m_ref) for the 64 keys of tile j -> 16-bit pairs in this lane of P buffer j & 1 (column i:
+    // P_j = 2^(s c - m_ref) for the 64 keys of tile j -> 16-bit pairs in this lane of P buffer j % kSB (column i:
     // keys 2i, 2i + 1); returns whether some weight exceeds 2^tau (s c > m_ref + tau: the running maximum grew)
     auto p_pass = [&](uint32_t s_col, uint32_t p_col) -> bool {
       const float2 c2 = make_float2(c, c), nm2 = make_float2(-m_ref, -m_ref);
@@ -681,19 +681,19 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         }
         tmem_st32_nw(p_col, w);
         hm = hmax2u<DT>(hm, hm1);
-        return fmaxf(lo_f<DT>(hm), hi_f<DT>(hm)) > kPMax;
-      }
+      } else {  // 32 columns at a time (<= 64 registers per thread)
 #pragma unroll
-      for (uint32_t q = 0; q < kKT / 32; ++q) {
-        uint32_t sv[32], w[16];
-        tmem_ld32(s_col + 32 * q, sv);
+        for (uint32_t q = 0; q < kKT / 32; ++q) {
+          uint32_t sv[32], w[16];
+          tmem_ld32(s_col + 32 * q, sv);
 #pragma unroll
-        for (uint32_t i = 0; i < 16; ++i) {
-          const float2 x = __ffma2_rn(make_float2(__uint_as_float(sv[2 * i]), __uint_as_float(sv[2 * i + 1])), c2, nm2);
-          w[i] = pack2<DT>(ex2(x.x), ex2(x.y));
-          hm = hmax2u<DT>(hm, w[i]);
+          for (uint32_t i = 0; i < 16; ++i) {
+            const float2 x = __ffma2_rn(make_float2(__uint_as_float(sv[2 * i]), __uint_as_float(sv[2 * i + 1])), c2, nm2);
+            w[i] = pack2<DT>(ex2(x.x), ex2(x.y));
+            hm = hmax2u<DT>(hm, w[i]);
+          }
+          tmem_st16_nw(p_col + 16 * q, w);
         }
-        tmem_st16_nw(p_col + 16 * q, w);
       }
       return fmaxf(lo_f<DT>(hm), hi_f<DT>(hm)) > kPMax;
     };
