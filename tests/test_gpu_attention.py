@@ -143,6 +143,15 @@ def test_attend_counts_hotness_and_validates(torch_cuda):
     with pytest.raises(hr.HaragError, match="ESTATE"):
         dm.attend(np.array([[0]], np.uint32), q, o, 4, 1)
     dm.close()
+    # k is bounded by the kernel's per-CTA table of retrieved docs (64)
+    big, _, _ = build(torch, L=1, H=1, T=64, D=64, n_docs=66, ladder=NORTH, taus=(0.25, 0.25), dtype="fp16")
+    q1 = torch.zeros(1 * 1 * 4 * 64, dtype=torch.int16, device="cuda")
+    o1 = torch.empty_like(q1)
+    big.attend(np.arange(64, dtype=np.uint32)[None], q1, o1, 4, 1)
+    torch.cuda.synchronize()
+    with pytest.raises(hr.HaragError, match="EINVAL"):
+        big.attend(np.arange(65, dtype=np.uint32)[None], q1, o1, 4, 1)
+    big.close()
 
 
 def test_attend_full_shape_sampled(torch_cuda):
