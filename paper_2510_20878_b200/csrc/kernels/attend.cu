@@ -65,6 +65,12 @@ __device__ __forceinline__ void tc_after() { asm volatile("tcgen05.fence::after_
 __device__ __forceinline__ uint64_t sdesc_sw128(uint32_t addr) {
   return (uint64_t)((addr >> 4) & 0x3FFFu) | (1ull << 16) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) | (2ull << 61);
 }
+// MN-major operand with the 128-byte swizzle: rows = K index (keys) of 64 N-elements (128 B), 8-row atoms of
+// 1024 B (SBO: next 8 rows along K), LBO = byte distance between 64-element blocks along N
+__device__ __forceinline__ uint64_t sdesc_sw128_mn(uint32_t addr, uint32_t lbo) {
+  return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)((lbo >> 4) & 0x3FFFu) << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         (1ull << 46) | (2ull << 61);
+}
 // byte offset of 16-B chunk dc (8 elements) of row `row` in a SW128 K-major tile of `rows` rows
 __device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t dc, uint32_t rows) {
   return (dc >> 3) * (rows * 128) + (row >> 3) * 1024 + (row & 7) * 128 + (((dc & 7) ^ (row & 7)) << 4);
@@ -354,16 +360,9 @@ __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, cons
   for (uint32_t i = 0; i < nch; ++i) {
     const uint32_t cc = dt + i * 32 * kDecWarps;
     {
-      // K: a warp takes whole key rows (conflict-free reads of the contiguous stage slot; a quarter warp
-      // writes one 128-B swizzled row of the K-major tile).  V: a warp takes 8 keys x 4 chunk columns (a
-      // quarter warp writes 8 rows of one MN-major core matrix; the stage reads conflict 4-way).
-      uint32_t key, dc;
-      if (VMAJ) {
-        const uint32_t gI = cc >> 5, ii = cc & 7, jj = (cc >> 3) & 3;
-        key = (gI % (kKT / 8)) * 8 + ii, dc = (gI / (kKT / 8)) * 4 + jj;
-      } else {
-        key = cc / dcs, dc = cc % dcs;
-      }
+      // a warp takes whole key rows: conflict-free reads of the contiguous stage slot, and a quarter warp
+      // writes one 128-B swizzled row (K: K-major, V: MN-major — the same physical SW128 layout)
+      const uint32_t key = cc / dcs, dc = cc % dcs;
       uint4 v;
       if constexpr (SCH == HR_S_PASS16) {  // bits unchanged: straight from global (L2-prefetched) into the operand tile
         v = __ldg(reinterpret_cast<const uint4*>(g16 + 2ull * ((t0 + key) * D + dc * 8)));
@@ -393,10 +392,7 @@ __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, cons
           v = dec_raw8<DT>(SCH, make_uint4(raw.x, raw.y, 0u, 0u), m, 0u, nullptr);
         }
       }
-      if (VMAJ)  // V: D/8 + 2 chunks per 8-key group (the ones / zero columns follow the D/8 of the head)
-        *reinterpret_cast<uint4*>(dst + ((key / 8) * (dcs + 2) + dc) * 128 + (key % 8) * 16) = v;
-      else
-        *reinterpret_cast<uint4*>(dst + sw128_off(key, dc, kKT)) = v;
+      *reinterpret_cast<uint4*>(dst + sw128_off(key, dc, kKT)) = v;
       if (dump) *reinterpret_cast<uint4*>(dump + key * D + dc * 8) = v;
     }
   }
@@ -476,7 +472,7 @@ struct SchemeOf {
 };
 
 size_t att_smem_bytes(uint32_t D) {
-  return kOpBufs * (size_t)kKT * (2 * D + 16) * 2 + kBarSlots * 8 + 16 + kStages * kSlotBytes + kDecGroups * kStageBytes +
+  return kOpBufs * (size_t)kKT * (2 * D) * 2 + kKT * 16 * 2 + kBarSlots * 8 + 16 + kStages * kSlotBytes + kDecGroups * kStageBytes +
          kMaxDocs * sizeof(DocSrc);
 }
 
@@ -574,12 +570,14 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // Q (A of S = Q K^T) lives in TMEM columns [kTQ, kTQ + D/2): lane = query row, column c = elements 2c, 2c+1
   uint8_t* skb = smem_raw;                         // kOpBufs x [64 keys][D] K-major (B of S = Q K^T)
-  // kOpBufs x [64 keys][D + 16] MN-major (B of O += P V): column D is all ones, D + 1 .. D + 15 zero, so
-  // the PV MMA also accumulates the row sum of P — the rounded 16-bit weights actually used — in O's
-  // column D (fp32 on the tensor core: no per-element sum in the softmax warps)
-  constexpr uint32_t vdcs = D / 8 + 2, vbuf = kKT * (D + 16) * 2;
+  // kOpBufs x [64 keys][D] MN-major SW128 (B of O += P V; 64-dim atoms of 64 keys x 128 B)
+  constexpr uint32_t vbuf = kKT * D * 2;
   uint8_t* svb = skb + kOpBufs * kKT * D * 2;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(svb + kOpBufs * vbuf);
+  // [64 keys][16] MN-major no-swizzle tile: column 0 all ones, 1..15 zero.  O[:, D..D+15] += P . ones gives
+  // the row sum of P — the rounded 16-bit weights actually used — in O's column D (fp32, on the tensor
+  // core: no per-element sum in the softmax warps)
+  uint8_t* sones = svb + kOpBufs * vbuf;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sones + kKT * 16 * 2);
   static_assert(3 * kSB + 2 * kOpBufs + 1 + 2 * kStages <= kBarSlots, "mbarrier slots");
   uint64_t *sf = bar, *pf = sf + kSB, *pfree = pf + kSB;  // per S/P buffer: S ready, P ready, PV done
   uint64_t *kvf = pfree + kSB, *kve = kvf + kOpBufs, *qf = kve + kOpBufs;
@@ -627,11 +625,10 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       }
     }
   }
-  for (uint32_t c = tid; c < kOpBufs * kKT * 2; c += blockDim.x) {  // the ones / zero chunks of every V buffer
-    const uint32_t b = c / (2 * kKT), key = (c / 2) % kKT, dc = D / 8 + (c & 1);
+  for (uint32_t c = tid; c < kKT * 2; c += blockDim.x) {  // the ones tile: 2 core-matrix columns
+    const uint32_t key = c / 2, dc = c & 1;
     const uint32_t one = DT == HR_BF16 ? 0x3F80u : 0x3C00u;
-    *reinterpret_cast<uint4*>(svb + b * vbuf + ((key / 8) * vdcs + dc) * 128 + (key % 8) * 16) =
-        make_uint4((c & 1) ? 0u : one, 0u, 0u, 0u);
+    *reinterpret_cast<uint4*>(sones + ((key / 8) * 2 + dc) * 128 + (key % 8) * 16) = make_uint4(dc ? 0u : one, 0u, 0u, 0u);
   }
   fence_async_smem();
   tc_before();
@@ -899,7 +896,9 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     // ------------------------------------------------------------------ MMA issuer
     const uint32_t fmt = DT == HR_BF16 ? 1u : 0u;
     const uint32_t id_s = idesc(fmt, 0, 0, kKT, kRows);  // S[128 x 64] = Q[128 x D] . K[64 x D]^T
-    const uint32_t id_o = idesc(fmt, 0, 1, D + 16, kRows);  // O[128 x D+16] += P[128 x 64] . V[64 x D+16] (MN-major)
+    const uint32_t id_o = idesc(fmt, 0, 1, D, kRows);    // O[128 x D] += P[128 x 64] . V[64 x D] (V MN-major SW128)
+    const uint32_t id_1 = idesc(fmt, 0, 1, 16, kRows);   // O[128 x D..D+15] += P . ones
+    const uint32_t oa = saddr(sones);
     // Event-driven issue: S_j needs operands j (kvf) and its TMEM buffer free (softmax of j-2 done, i.e.
     // PV_{j-2} already issued); PV_j needs P_j (pf).  Whichever is ready goes first, so PV_{j-1} (which
     // frees the operand buffer decode j+1 waits for) never waits behind the decode of tile j.
@@ -967,9 +966,12 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
 #pragma unroll
           for (uint32_t s = 0; s < kKT / 16; ++s) {
             a[s] = tmem + kTP + bb * (kKT / 2) + s * 8;
-            bd[s] = sdesc(va + s * 2 * vdcs * 128, vdcs * 128, 128);
+            bd[s] = sdesc_sw128_mn(va + s * 2048, kKT * 128);  // 16 keys = two 8-key row groups
           }
           mma_ts_batch<kKT / 16>(t_o, a, bd, id_o, npv > 0 ? 1u : 0u);
+#pragma unroll
+          for (uint32_t s = 0; s < kKT / 16; ++s) bd[s] = sdesc(oa + s * 2 * 2 * 128, 2 * 128, 128);
+          mma_ts_batch<kKT / 16>(t_o + D, a, bd, id_1, npv > 0 ? 1u : 0u);
         }
         mma_commit(&kve[ob]);
         mma_commit(&pfree[bb]);
