@@ -241,7 +241,10 @@ constexpr uint32_t kMetaWin = 2048;
 constexpr uint32_t kStageBytes = 2 * kMetaWin + 2 * 256 * 2;  // per decoder group: meta windows, value tables
 // Stage ring of code tiles, filled by the producer warp with TMA bulk copies (cp.async.bulk): slot =
 // [K codes, 8 KB][V codes, 8 KB], each the tile's contiguous [64 keys][D] codes (1 B, or 1/2 B for INT4)
-constexpr uint32_t kStages = 4, kSlotBytes = 2 * kKT * 128, kSlotV = kKT * 128;
+#ifndef HARAG_ATT_STAGES
+#define HARAG_ATT_STAGES 4
+#endif
+constexpr uint32_t kStages = HARAG_ATT_STAGES, kSlotBytes = 2 * kKT * 128, kSlotV = kKT * 128;
 #ifndef HARAG_ATT_OPBUFS
 #define HARAG_ATT_OPBUFS 4
 #endif
@@ -445,7 +448,10 @@ __device__ __forceinline__ uint32_t stage_meta(uint32_t scheme, const uint8_t* m
 // so the tensor core computes S_{j+1} while the softmax warps work on S_j and the decoders fill
 // tile j+2.  mbarriers: sf (S ready), pf (P ready), kvf (operands ready), kve (operands and P free:
 // committed after PV), pfree (PV done per P buffer: lazy rescale, epilogue), qf (Q ready).
-constexpr uint32_t kPF = 4;  // L2 prefetch distance in tiles
+#ifndef HARAG_ATT_PF
+#define HARAG_ATT_PF 4
+#endif
+constexpr uint32_t kPF = HARAG_ATT_PF;  // L2 prefetch distance in tiles
 // kSB S buffers and kSB P buffers in TMEM: S_j = Q K_j^T may be computed while softmax works on S_{j-2}
 // and S_{j-1} waits — the tensor core runs S_{j+2} ahead of PV_j.
 // TMEM columns: S buffers [0, 64 kSB), O [kTO, kTO + D + 16) (column kTO + D: the row sum),
