@@ -667,6 +667,10 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     float m_ref = -INFINITY;
     // P_j = 2^(s c - m_ref) for the 64 keys of tile j -> 16-bit pairs in this lane of P buffer j % kSB (column i:
     // keys 2i, 2i + 1); returns whether some weight exceeds 2^tau (s c > m_ref + tau: the running maximum grew)
+#ifdef HARAG_ATT_SOFTMAX_SUM
+    static_assert(kWideSoftmax, "softmax-side row sum: wide pass only");
+    float psum = 0.f, lsum = 0.f;  // this tile's sum of the rounded weights; running row sum
+#endif
     auto p_pass = [&](uint32_t s_col, uint32_t p_col) -> bool {
       const float2 c2 = make_float2(c, c), nm2 = make_float2(-m_ref, -m_ref);
       uint32_t hm = 0u;  // packed running maximum of the weights (all >= +0)
@@ -676,12 +680,21 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         tmem_ld32_nw(s_col + 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[32]));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         uint32_t hm1 = 0u;
+#ifdef HARAG_ATT_SOFTMAX_SUM
+        float2 ls2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#endif
 #pragma unroll
         for (uint32_t i = 0; i < 32; ++i) {
           const float2 x = __ffma2_rn(make_float2(__uint_as_float(sv[2 * i]), __uint_as_float(sv[2 * i + 1])), c2, nm2);
           w[i] = pack2<DT>(ex2(x.x), ex2(x.y));
           if (i & 1) hm1 = hmax2u<DT>(hm1, w[i]); else hm = hmax2u<DT>(hm, w[i]);
+#ifdef HARAG_ATT_SOFTMAX_SUM
+          ls2[i & 1] = __fadd2_rn(ls2[i & 1], make_float2(lo_f<DT>(w[i]), hi_f<DT>(w[i])));
+#endif
         }
+#ifdef HARAG_ATT_SOFTMAX_SUM
+        psum = (ls2[0].x + ls2[0].y) + (ls2[1].x + ls2[1].y);
+#endif
         tmem_st32_nw(p_col, w);
         hm = hmax2u<DT>(hm, hm1);
       } else {  // 32 columns at a time (<= 64 registers per thread)
@@ -735,11 +748,18 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
             for (int q = 0; q < 32; ++q) ov[q] = __float_as_uint(__uint_as_float(ov[q]) * alpha);
             tmem_st32(t_o + lane_base + cb, ov);
           }
+#ifdef HARAG_ATT_SOFTMAX_SUM
+          lsum *= alpha;
+#else
           tmem_st1(t_o + lane_base + D, __float_as_uint(__uint_as_float(tmem_ld1(t_o + lane_base + D)) * alpha));
+#endif
         }
         if (grow) m_ref = mt;
         p_pass(s_col, p_col);
       }
+#ifdef HARAG_ATT_SOFTMAX_SUM
+      lsum += psum;
+#endif
       if (tid == 0) TR(11, j);
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       tc_before();
@@ -753,7 +773,11 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     if (n_tiles) MBW(&pfree[(n_tiles - 1) % kSB], ((n_tiles - 1) / kSB) & 1, 8, n_tiles);
     tc_after();
     // l = sum of the rounded weights (O's ones column); every row has l >= 1 (its maximum contributes 2^0)
+#ifdef HARAG_ATT_SOFTMAX_SUM
+    const float ltot = lsum, inv = 1.f / ltot;
+#else
     const float ltot = __uint_as_float(tmem_ld1(t_o + lane_base + D)), inv = 1.f / ltot;
+#endif
     for (uint32_t cb = 0; cb < D; cb += 32) {
       uint32_t ov[32];
       tmem_ld32(t_o + lane_base + cb, ov);
@@ -977,7 +1001,9 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
           mma_ts_batch<kKT / 16>(t_o, a, bd, id_o, npv > 0 ? 1u : 0u);
 #pragma unroll
           for (uint32_t s = 0; s < kKT / 16; ++s) bd[s] = sdesc(oa + s * 2 * 2 * 128, 2 * 128, 128);
+#ifndef HARAG_ATT_SOFTMAX_SUM
           mma_ts_batch<kKT / 16>(t_o + D, a, bd, id_1, npv > 0 ? 1u : 0u);
+#endif
         }
         mma_commit(&kve[ob]);
         mma_commit(&pfree[bb]);
