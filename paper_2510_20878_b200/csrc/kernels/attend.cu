@@ -43,13 +43,17 @@ __device__ __forceinline__ uint32_t saddr(const void* p) { return static_cast<ui
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(bar)), "r"(count) : "memory");
 }
+// suspended wait (the thread sleeps until the phase completes or the hint elapses, instead of re-polling)
+#ifndef HARAG_ATT_WAIT_HINT
+#define HARAG_ATT_WAIT_HINT 0x989680
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n}" ::"r"(saddr(bar)),
-      "r"(parity)
+      "r"(parity), "n"(HARAG_ATT_WAIT_HINT)
       : "memory");
 }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
