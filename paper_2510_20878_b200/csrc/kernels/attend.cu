@@ -460,7 +460,10 @@ constexpr uint32_t kPF = HARAG_ATT_PF;  // L2 prefetch distance in tiles
 // and S_{j-1} waits — the tensor core runs S_{j+2} ahead of PV_j.
 // TMEM columns: S buffers [0, 64 kSB), O [kTO, kTO + D + 16) (column kTO + D: the row sum),
 // Q [kTQ, kTQ + D/2), P buffers [kTP, kTP + 32 kSB) (32 columns of 16-bit pairs each)
-constexpr uint32_t kSB = 3;
+#ifndef HARAG_ATT_SBUFS
+#define HARAG_ATT_SBUFS 2
+#endif
+constexpr uint32_t kSB = HARAG_ATT_SBUFS;
 constexpr uint32_t kTO = 64 * kSB, kTQ = kTO + 144, kTP = kTQ + 64, kTmemCols = 512;
 static_assert(kTP + 32 * kSB <= kTmemCols, "TMEM columns");
 // Lazy rescale threshold tau (log2 units): weights p = 2^(s c - m_ref) may reach 2^tau before the reference
