@@ -953,7 +953,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
 #endif
       // Blocking waits where only one event can come next (no polling: a spinning issuer took 10% of the
       // SM's issue slots): after S_{j+1} only PV_j can follow; with every issued S matched by its PV only
-      // S can.  With both possible (after PV_j: S_{j+2} or PV_{j+1}), S operands are usually ready already.
+      // S can.  With both possible, PV goes first if P is ready, else whichever event comes first.
       const bool s_ok = ns < n_tiles && ns <= npv + kSB - 1, pv_ok = npv < ns;
       bool do_s;
       if (!pv_ok) {
@@ -964,8 +964,13 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         do_s = false;
       } else {
         while (true) {
+#ifndef HARAG_ATT_S_FIRST  // PV_j first when P_j is ready (measured 1.30 vs 1.32 ms for S-first)
+          if (mbar_test_u(&pf[npv % kSB], (npv / kSB) & 1)) { do_s = false; break; }
+          if (mbar_wait_hint_u(&kvf[ns % kOpBufs], (ns / kOpBufs) & 1, 100)) { do_s = true; break; }
+#else
           if (mbar_test_u(&kvf[ns % kOpBufs], (ns / kOpBufs) & 1)) { do_s = true; break; }
           if (mbar_wait_hint_u(&pf[npv % kSB], (npv / kSB) & 1, 100)) { do_s = false; break; }
+#endif
         }
       }
       if (do_s) {
