@@ -240,9 +240,22 @@ hr_status hr_build_from_file(hr_store* s, const char* path, void* stream);
  * demand mode -> the Alg. 2 queue holding it (queueGPU -> HBM, queuePIN -> PIN, none -> PAGE/backing). */
 hr_status hr_item_info(const hr_store* s, uint32_t item, uint32_t* scheme, uint32_t* tier, uint64_t* bytes);
 hr_status hr_item_rank(const hr_store* s, uint32_t item, uint32_t* rank);   /* position in the hotness order */
+/* Physical copies of an item right now (hr_item_info reports the logical tier): *mask |= HR_R_HBM when
+ * the item's blob is in the HBM arena (or its promotion copy is enqueued there; stream-ordered), HR_R_PIN
+ * pinned-tier copy, HR_R_PAGE pageable PAGE-tier cache copy, HR_R_BACKING in-memory host backing,
+ * HR_R_FILE in the store file of a disk-backed store.  Demand mode keeps HR_R_HBM == queueGPU of Alg. 2
+ * after every hr_assemble_kv.  HR_ENOTFOUND for an unknown item, HR_ESTATE before build. */
+enum { HR_R_HBM = 1, HR_R_PIN = 2, HR_R_PAGE = 4, HR_R_BACKING = 8, HR_R_FILE = 16 };
+hr_status hr_item_residency(const hr_store* s, uint32_t item, uint32_t* mask);
 hr_status hr_export_item(const hr_store* s, uint32_t item, void* host_dst, size_t cap, size_t* len); /* packed blob; synchronous */
 hr_status hr_store_stats(const hr_store* s, hr_stats* out);                 /* synchronises pending timing events */
-hr_status hr_set_timing(hr_store* s, int enable);                           /* 1: time every assemble launch with CUDA events */
+hr_status hr_set_timing(hr_store* s, int enable);  /* bit 0: time every assemble launch with CUDA events (stats.kernel_ms);
+                                                     bit 1: time every hr_assemble_kv call (hr_last_call_ms); 0..3 */
+/* Per-request assemble latency: device time from the entry of the last hr_assemble_kv call made with
+ * timing bit 1 (an event recorded on its stream before any of its work) to the end of its last launch —
+ * planning, descriptor upload, host-tier copies and kernels included.  Waits for that call to finish.
+ * HR_ESTATE when no call was timed. */
+hr_status hr_last_call_ms(hr_store* s, double* ms);
 hr_status hr_reset_stats(hr_store* s);
 
 /* ------------------------------------------ host policy (no GPU needed)

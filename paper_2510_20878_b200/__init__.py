@@ -12,11 +12,11 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
-from ._lib import (FP8E4M3, FP8E5M2, GSE8, HR_BF16, HR_FP16, INT4, INT8, PASS16, SCHEMES, T_DISK, T_HBM,
-                   T_PAGE, T_PIN, HaragError, check, lib)
+from ._lib import (FP8E4M3, FP8E5M2, GSE8, HR_BF16, HR_FP16, INT4, INT8, PASS16, R_BACKING, R_FILE, R_HBM,
+                   R_PAGE, R_PIN, SCHEMES, T_DISK, T_HBM, T_PAGE, T_PIN, HaragError, check, lib)
 
 __all__ = ["Store", "HaragError", "SCHEMES", "PASS16", "INT8", "FP8E4M3", "FP8E5M2", "GSE8", "INT4",
-           "T_HBM", "T_PIN", "T_PAGE", "T_DISK", "policy_rank", "policy_lists_bytes4", "policy_assign", "policy_lists_bytes",
+           "T_HBM", "T_PIN", "T_PAGE", "T_DISK", "R_HBM", "R_PIN", "R_PAGE", "R_BACKING", "R_FILE", "policy_rank", "policy_lists_bytes4", "policy_assign", "policy_lists_bytes",
            "policy_lists_fraction", "policy_count", "policy_epoch", "item_bytes", "Alg2",
            "exponent_histogram", "scheme_error"]
 
@@ -61,6 +61,10 @@ def make_config(*, L, H, D, T, dtype="bf16", group=0, gse=(4, 3),
     c.dtype = HR_FP16 if dtype == "fp16" else HR_BF16
     c.group = group
     c.gse_ebits, c.gse_mbits = gse
+    if not 1 <= len(ladder) <= 6:
+        raise ValueError("ladder must hold 1..6 schemes")
+    if len(taus) != len(ladder) - 1:
+        raise ValueError(f"need len(ladder) - 1 = {len(ladder) - 1} taus, got {len(taus)} (Alg. 1, P:190)")
     c.n_ladder = len(ladder)
     for j, s in enumerate(ladder):
         c.ladder[j] = SCHEMES[s] if isinstance(s, str) else int(s)
@@ -189,6 +193,12 @@ class Store:
         check(lib.hr_item_rank(self._h, item, C.byref(r)))
         return r.value
 
+    def item_residency(self, item: int) -> int:
+        """Bit mask of the item's physical copies (hr_item_residency: R_HBM, R_PIN, R_PAGE, R_BACKING, R_FILE)."""
+        m = C.c_uint32()
+        check(lib.hr_item_residency(self._h, item, C.byref(m)))
+        return m.value
+
     def export_item(self, item: int) -> np.ndarray:
         _, _, nbytes = self.item_info(item)
         buf = np.zeros(nbytes, dtype=np.uint8)
@@ -196,8 +206,15 @@ class Store:
         check(lib.hr_export_item(self._h, item, buf.ctypes.data, nbytes, C.byref(ln)))
         return buf[: ln.value]
 
-    def set_timing(self, on: bool) -> None:
-        check(lib.hr_set_timing(self._h, int(bool(on))))
+    def set_timing(self, on: bool, calls: bool = False) -> None:
+        """on: CUDA events around every assemble launch; calls: around every hr_assemble_kv call."""
+        check(lib.hr_set_timing(self._h, int(bool(on)) | (2 if calls else 0)))
+
+    def last_call_ms(self) -> float:
+        """Device time of the last timed hr_assemble_kv call (entry -> last launch done)."""
+        v = C.c_double()
+        check(lib.hr_last_call_ms(self._h, C.byref(v)))
+        return v.value
 
     def reset_stats(self) -> None:
         check(lib.hr_reset_stats(self._h))
@@ -235,6 +252,10 @@ def policy_rank(h) -> np.ndarray:
 
 def policy_assign(h, ladder, taus) -> np.ndarray:
     h = _u64(h)
+    if not 1 <= len(ladder) <= 6:
+        raise ValueError("ladder must hold 1..6 schemes")
+    if len(taus) != len(ladder) - 1:
+        raise ValueError(f"need len(ladder) - 1 = {len(ladder) - 1} taus, got {len(taus)} (Alg. 1, P:190)")
     lad = _u32([SCHEMES[s] if isinstance(s, str) else s for s in ladder])
     tau = np.ascontiguousarray(np.asarray(list(taus) + [0.0], dtype=np.float64))
     out = np.empty(h.size, np.uint32)

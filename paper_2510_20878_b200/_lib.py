@@ -19,6 +19,7 @@ HR_BF16, HR_FP16 = 0, 1
 PASS16, INT8, FP8E4M3, FP8E5M2, GSE8, INT4 = range(6)
 SCHEMES = {"PASS16": PASS16, "INT8": INT8, "FP8E4M3": FP8E4M3, "FP8E5M2": FP8E5M2, "GSE8": GSE8, "INT4": INT4}
 T_HBM, T_PIN, T_PAGE, T_DISK = 0, 1, 2, 3
+R_HBM, R_PIN, R_PAGE, R_BACKING, R_FILE = 1, 2, 4, 8, 16
 
 
 class Config(C.Structure):
@@ -76,9 +77,11 @@ _SIGS = {
     "hr_build_from_file": (I32, [P, C.c_char_p, P]),
     "hr_item_info": (I32, [P, U32, PU32, PU32, PU64]),
     "hr_item_rank": (I32, [P, U32, PU32]),
+    "hr_item_residency": (I32, [P, U32, PU32]),
     "hr_export_item": (I32, [P, U32, P, SZ, C.POINTER(SZ)]),
     "hr_store_stats": (I32, [P, C.POINTER(Stats)]),
     "hr_set_timing": (I32, [P, I32]),
+    "hr_last_call_ms": (I32, [P, C.POINTER(C.c_double)]),
     "hr_reset_stats": (I32, [P]),
     "hr_policy_rank": (I32, [U32, PU64, PU32]),
     "hr_policy_assign": (I32, [U32, PU64, U32, PU32, C.POINTER(C.c_double), PU32]),

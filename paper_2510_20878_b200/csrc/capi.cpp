@@ -173,6 +173,20 @@ hr_status hr_item_info(const hr_store* s, uint32_t item, uint32_t* scheme, uint3
     if (bytes) *bytes = st.bytes[item];
   });
 }
+hr_status hr_item_residency(const hr_store* s, uint32_t item, uint32_t* mask) {
+  return guard([&] {
+    NONNULL(s);
+    NONNULL(mask);
+    const auto& st = s->impl;
+    harag::require(st.state != harag::Store::State::Empty, HR_ESTATE, "store not built");
+    harag::require(item < st.n_items, HR_ENOTFOUND, "item id out of range");
+    const auto& l = st.loc[item];
+    const uint64_t none = harag::FreeList::kNone;
+    *mask = (l.hbm_off != none ? HR_R_HBM : 0) | (l.pin_off != none ? HR_R_PIN : 0) |
+            (l.page_off != none ? HR_R_PAGE : 0) | (l.backing_off != none ? HR_R_BACKING : 0) |
+            (st.disk_fd >= 0 && !st.disk_off.empty() ? HR_R_FILE : 0);
+  });
+}
 hr_status hr_item_rank(const hr_store* s, uint32_t item, uint32_t* rank) {
   return guard([&] {
     NONNULL(s);
@@ -200,7 +214,16 @@ hr_status hr_store_stats(const hr_store* s, hr_stats* out) {
 hr_status hr_set_timing(hr_store* s, int enable) {
   return guard([&] {
     NONNULL(s);
-    s->impl.timing = enable != 0;
+    harag::require(enable >= 0 && enable <= 3, HR_EINVAL, "enable must be 0..3");
+    s->impl.timing = (enable & 1) != 0;
+    s->impl.call_timing = (enable & 2) != 0;
+  });
+}
+hr_status hr_last_call_ms(hr_store* s, double* ms) {
+  return guard([&] {
+    NONNULL(s);
+    NONNULL(ms);
+    *ms = s->impl.last_call_ms();
   });
 }
 hr_status hr_reset_stats(hr_store* s) {

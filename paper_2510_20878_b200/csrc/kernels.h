@@ -32,8 +32,10 @@ constexpr int kAsmStages = HARAG_STAGES;         // shared-memory ring depth
 constexpr int kAsmCodeStage = HARAG_CODE_STAGE;  // bytes of packed codes per stage (every scheme mix)
 constexpr int kAsmMaxTileE = kAsmCodeStage;      // elements per tile (half when a launch holds PASS16 items)
 
+constexpr int kAsmInline = 64;  // launches of <= kAsmInline descriptors carry them in the kernel parameters
+
 struct AsmParams {
-  const AsmDesc* descs;
+  const AsmDesc* descs;      // device array, or nullptr: the descriptors are inl[0..n_desc)
   uint32_t n_desc;
   uint32_t L, Hl, T, D, k, G;
   uint32_t g_shift;          // log2(G) (G is a power of two)
@@ -45,6 +47,7 @@ struct AsmParams {
   uint32_t meta_stage;       // bytes of meta window per stage (multiple of 128)
   uint64_t n_tiles;          // n_desc * L * Hl * tiles_per_slab
   uint32_t meta_stride[6];   // per scheme, bytes per slab record
+  AsmDesc inl[kAsmInline];   // small launches (a single request, a streamed item): no descriptor H2D copy
 };
 
 // Launch the fused gather -> unpack -> dequantise -> scatter (+ hotness count).

@@ -151,7 +151,7 @@ __device__ __forceinline__ void produce(const AsmParams& p, const Smem& sm) {
   uint32_t r = (uint32_t)(t0 - (uint64_t)di * per_desc);
   uint32_t slab_i = r / p.tiles_per_slab;
   uint32_t sub = r - slab_i * p.tiles_per_slab;
-  AsmDesc d = p.descs[di];
+  AsmDesc d = p.descs ? p.descs[di] : p.inl[di];
   for (uint64_t i = 0; i < t1 - t0; ++i) {
     const int stage = (int)(i % kAsmStages);
     if (i >= kAsmStages) mbar_wait(&sm.empty()[stage], (uint32_t)(((i / kAsmStages) - 1) & 1));
@@ -187,7 +187,10 @@ __device__ __forceinline__ void produce(const AsmParams& p, const Smem& sm) {
       sub = 0;
       if (++slab_i == n_slabs) {
         slab_i = 0;
-        if (i + 1 < t1 - t0) d = p.descs[++di];
+        if (i + 1 < t1 - t0) {
+          ++di;
+          d = p.descs ? p.descs[di] : p.inl[di];
+        }
       }
     }
   }

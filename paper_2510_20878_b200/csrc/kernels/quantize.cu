@@ -718,6 +718,10 @@ __device__ __forceinline__ uint32_t cluster_rank() {
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
 __device__ __forceinline__ void st_cluster_v2(uint32_t local_addr, uint32_t rank, int a, int b) {
   uint32_t remote;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_addr), "r"(rank));
@@ -774,6 +778,9 @@ __global__ void __cluster_dims__(kGseQ, 1, 1) __launch_bounds__(kGseThreads, 5)
     mbar_init_fence();
   }
   __syncthreads();
+  // split cluster barrier: every CTA of the cluster must have started before a peer writes into its
+  // shared memory (the DSMEM stores below); the wait is placed after the load and the range pass
+  cluster_arrive_relaxed();
   if (tid == 0) {
     mbar_arrive_expect_tx(bar, 2 * qe);
     bulk_g2s(src_s, jb.src + ((uint64_t)(l * p.H + p.h0 + hl) * p.slab + (uint64_t)q * qe), 2 * qe, bar);
@@ -818,6 +825,7 @@ __global__ void __cluster_dims__(kGseQ, 1, 1) __launch_bounds__(kGseThreads, 5)
   }
   if (lane == 0) red[2 * warp] = emin, red[2 * warp + 1] = emax;
   __syncthreads();
+  cluster_wait();  // every peer CTA is running (pairs with cluster_arrive_relaxed above)
   if (tid == 0) {
     for (uint32_t w = 1; w < kGseThreads / 32; ++w) emin = min(emin, red[2 * w]), emax = max(emax, red[2 * w + 1]);
     // (255 - min, max) as the range pass stores it: a quarter without normals contributes (0, 0)

@@ -107,6 +107,9 @@ Store::~Store() {
   if (src_k) cudaFree(src_k);
   if (src_v) cudaFree(src_v);
   if (start_ev) cudaEventDestroy(start_ev);
+  if (after_a_ev) cudaEventDestroy(after_a_ev);
+  for (auto& e : call_ev)
+    if (e) cudaEventDestroy(e);
   if (mig_ev) cudaEventDestroy(mig_ev);
   for (auto& p : promos) cudaEventDestroy(p.ev);
   if (copy_stream) cudaStreamDestroy(copy_stream);
@@ -358,17 +361,38 @@ void Store::build_with_source(uint32_t nd, const uint64_t* hot, hr_src_fn src, v
   HR_CUDA(cudaMalloc(&src_v, full * nb));
   uint32_t docs[kPutBatch];
   const void *ks[kPutBatch], *vs[kPutBatch];
-  for (uint32_t d0 = 0; d0 < nd; d0 += nb) {
-    const uint32_t n = std::min(nb, nd - d0);
-    for (uint32_t i = 0; i < n; ++i) {
-      docs[i] = d0 + i;
-      ks[i] = (uint8_t*)src_k + full * i;
-      vs[i] = (uint8_t*)src_v + full * i;
-      const int rc = src(user, docs[i], (void*)ks[i], (void*)vs[i], (void*)st);
-      require(rc == HR_OK, (hr_status)rc, "source callback failed for doc " + std::to_string(docs[i]));
+  // bench aliasing (bench_alias_R > 0): a doc whose items all live only in a host backing blob that
+  // an earlier doc with the same source already filled needs no quantisation (the blob would be
+  // written with identical bytes) — only HBM-arena and pinned-tier items and first fills are built
+  auto needed = [&](uint32_t doc) {
+    if (!cfg.bench_alias_R) return true;
+    for (uint32_t kind = 0; kind < 2; ++kind) {
+      const Loc& l = loc[2 * doc + kind];
+      if (tier[2 * doc + kind] == HR_T_HBM || l.pin_off != FreeList::kNone || l.page_off != FreeList::kNone ||
+          l.backing_off == FreeList::kNone || !backing_filled.count(l.backing_off))
+        return true;
     }
-    build_put_batch(n, docs, ks, vs, st);
+    return false;
+  };
+  uint32_t n = 0;
+  auto flush = [&] {
+    if (n) build_put_batch(n, docs, ks, vs, st);
+    n = 0;
+  };
+  for (uint32_t doc = 0; doc < nd; ++doc) {
+    if (!needed(doc)) {
+      if (!put_done[doc]) ++n_put;
+      put_done[doc] = 1;
+      continue;
+    }
+    docs[n] = doc;
+    ks[n] = (uint8_t*)src_k + full * n;
+    vs[n] = (uint8_t*)src_v + full * n;
+    const int rc = src(user, doc, (void*)ks[n], (void*)vs[n], (void*)st);
+    require(rc == HR_OK, (hr_status)rc, "source callback failed for doc " + std::to_string(doc));
+    if (++n == nb) flush();
   }
+  flush();
   build_end(st);
   cudaFree(src_k);
   cudaFree(src_v);
@@ -402,10 +426,16 @@ void Store::ensure_ring() {
   }
 }
 
-void Store::launch(const AsmDesc* dev_descs, uint32_t n, uint32_t k, uint32_t scheme_mask, cudaStream_t st) {
+void Store::launch(const AsmDesc* dev_descs, const AsmDesc* host_descs, uint32_t n, uint32_t k, uint32_t scheme_mask,
+                   cudaStream_t st) {
   AsmParams p{};
-  p.descs = dev_descs;
   p.n_desc = n;
+  if (n <= (uint32_t)kAsmInline) {  // carried in the kernel parameters: no descriptor copy ahead of the launch
+    p.descs = nullptr;
+    std::memcpy(p.inl, host_descs, n * sizeof(AsmDesc));
+  } else {
+    p.descs = dev_descs;
+  }
   p.L = lay.L, p.Hl = lay.Hl, p.T = lay.T, p.D = lay.D, p.k = k, p.G = lay.G;
   p.g_shift = (uint32_t)__builtin_ctz(lay.G);
   p.gse_m = lay.gse_m;
@@ -446,17 +476,16 @@ void Store::validate_request(uint32_t n_req, uint32_t k, const uint32_t* ids, vo
   }
 }
 
-// Demand mode (paper-literal Alg. 2 step 2): space freed by evictions of the previous call is
-// released now — its readers are ordered before this call's promotion copies by `start_ev`, and
-// the copy stream is drained before pinned space is rewritten by the host.
+// Demand mode (paper-literal Alg. 2 step 2): pinned / pageable space freed by evictions of the
+// previous call is released now — the copy stream is drained before pinned space is rewritten by
+// the host.  (HBM arena space is released inside the call that evicts; promotion copies are
+// ordered after its readers by `start_ev` and `after_a_ev`.)
 void Store::release_deferred() {
   if (!pending_pin_free.empty()) {
     HR_CUDA(cudaStreamSynchronize(copy_stream));
     for (auto& f : pending_pin_free) pin.release(f.first, f.second);
     pending_pin_free.clear();
   }
-  for (auto& f : pending_hbm_free) hbm.release(f.first, f.second);
-  pending_hbm_free.clear();
   for (auto& f : pending_page_free) page.release(f.first, f.second);  // read by the host during its call
   pending_page_free.clear();
 }
@@ -465,6 +494,13 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
                      cudaStream_t st) {
   validate_request(n_req, k, ids, k_out, v_out);  // before any device work: no partial writes
   HR_CUDA(cudaSetDevice(cfg.device));
+  if (call_timing) {  // per-call latency: this event -> the end of the call's last launch (device clock)
+    if (!call_ev[0]) {
+      HR_CUDA(cudaEventCreate(&call_ev[0]));
+      HR_CUDA(cudaEventCreate(&call_ev[1]));
+    }
+    HR_CUDA(cudaEventRecord(call_ev[0], st));
+  }
   if (!promos.empty()) poll_promotions(false);
   const bool demand = alg2 != nullptr;
   if (demand) {
@@ -475,30 +511,22 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
   }
   const size_t n_desc = 2ull * n_req * k;
   DescBuf& db = desc_buffer(n_desc);
-  // a6 planning.  Resident items (physically in the HBM arena when the call starts, or promoted in
-  // eager mode) go to launch A; the rest are streamed, each item once per call.
-  struct Stream {
-    uint32_t item;
-    uint64_t arena_off;  // != kNone: promotion target (demand mode), else a staging-ring slot
-    std::vector<AsmDesc> descs;
-  };
-  std::vector<Stream> streamed;
-  std::unordered_map<uint32_t, size_t> stream_idx;
-  size_t nh = 0;
-  uint32_t hbm_mask = 0;
+  // a6 planning, in three passes.
+  //  1. Every access in request order: Alg. 2 step 2 (demand mode: one branch per access, the hit
+  //     counted where Alg. 2 finds the item, host-queue fills done at once) or the tier lookup (eager).
+  //  2. Demand mode: physical HBM residency := queueGPU as it stands after the call's accesses.
+  //     Blocks of items that left the queue are freed first (their launch-A readers of this call are
+  //     ordered before any promotion copy that reuses the space: `after_a`), then the newcomers that
+  //     this call accessed get their arena blocks; their DMA lands there instead of a ring slot.
+  //  3. Descriptors: items resident when the call started go to launch A (from their block as it was
+  //     at the start), the rest are streamed, each item once per call.
+  std::vector<uint32_t> evicted_gpu;
   for (uint32_t r = 0; r < n_req; ++r) {
-    const bool counted = ((req_counter + r) % (uint64_t)cfg.world) == (uint64_t)cfg.rank;
     for (uint32_t j = 0; j < k; ++j) {
       for (uint32_t kind = 0; kind < 2; ++kind) {
         const uint32_t item = 2 * ids[(uint64_t)r * k + j] + kind;
-        AsmDesc d{};
-        d.out = (uint8_t*)(kind ? v_out[r] : k_out[r]);
-        d.count = counted ? reinterpret_cast<unsigned long long*>(delta + item) : nullptr;
-        d.slot = j;
-        d.scheme = scheme[item];
         stats.bytes_out += lay.n_slabs() * lay.slab() * 2;
         stats.bytes_hbm_alg += lay.n_slabs() * lay.slab() * 2 + bytes_read_alg(item);
-        bool promote = false;
         if (demand) {  // Alg. 2 step 2: one branch per access, inclusive promotion, LRU
           const Alg2::Outcome o = alg2->access(item);
           if (o.hit == Alg2::DISK && on_disk)
@@ -507,10 +535,8 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
             stats.hits[o.hit == Alg2::GPU ? HR_T_HBM : o.hit == Alg2::PIN ? HR_T_PIN : HR_T_PAGE]++;
           for (const auto& ev : o.evicted) {
             Loc& l = loc[ev.second];
-            if (ev.first == Alg2::GPU && l.hbm_off != FreeList::kNone) {
-              pending_hbm_free.emplace_back(l.hbm_off, bytes[ev.second]);  // readers may still be in flight
-              l.hbm_off = FreeList::kNone;
-              stats.migrations_out++;
+            if (ev.first == Alg2::GPU) {
+              evicted_gpu.push_back(ev.second);  // pass 2 frees its block unless it is back in the queue
             } else if (ev.first == Alg2::PIN && l.pin_off != FreeList::kNone) {
               pending_pin_free.emplace_back(l.pin_off, bytes[ev.second]);
               l.pin_off = FreeList::kNone;
@@ -533,7 +559,6 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
               fill_host(item, pin_base + off);
             }
           }
-          promote = alg2->contains(Alg2::GPU, item) && loc[item].hbm_off == FreeList::kNone;
         } else {
           const Loc& l = loc[item];
           if (l.hbm_off == FreeList::kNone && l.pin_off == FreeList::kNone && l.page_off == FreeList::kNone &&
@@ -545,19 +570,87 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
                                                           l.page_off == FreeList::kNone)) ? HR_T_PIN
                                                                                            : HR_T_PAGE]++;
         }
-        auto it = stream_idx.find(item);
-        if (it == stream_idx.end() && loc[item].hbm_off != FreeList::kNone) {
-          d.codes = hbm_ptr(item);
+      }
+    }
+  }
+  // pass 2 (demand mode): HBM arena := queueGPU
+  std::unordered_map<uint32_t, uint64_t> start_off;  // items resident at the call's start whose block was freed
+  std::unordered_map<uint32_t, bool> promoted;       // item -> its arena block reuses space freed in this call
+  if (demand) {
+    std::vector<std::pair<uint64_t, uint64_t>> freed;  // [off, off + size) freed in this call
+    for (uint32_t item : evicted_gpu) {
+      Loc& l = loc[item];
+      if (l.hbm_off == FreeList::kNone || alg2->contains(Alg2::GPU, item)) continue;
+      start_off.emplace(item, l.hbm_off);
+      freed.emplace_back(l.hbm_off, l.hbm_off + align_up(bytes[item], FreeList::kAlign));
+      hbm.release(l.hbm_off, bytes[item]);
+      l.hbm_off = FreeList::kNone;
+      stats.migrations_out++;
+    }
+    for (uint64_t a = 0; a < 2ull * n_req * k; ++a) {
+      const uint32_t item = 2 * ids[a / 2] + (uint32_t)(a % 2);
+      if (loc[item].hbm_off != FreeList::kNone || !alg2->contains(Alg2::GPU, item)) continue;
+      uint64_t off = hbm.alloc(bytes[item]);
+      if (off == FreeList::kNone && hbm_cap - hbm.used() >= align_up(bytes[item], FreeList::kAlign)) {
+        // queueGPU fits the budget by construction: defragment (needs an idle device) and retry.  The
+        // moved blocks overwrite the space of items freed above, so those are streamed instead.
+        HR_CUDA(cudaDeviceSynchronize());
+        compact_hbm();
+        start_off.clear();
+        freed.clear();
+        for (auto& p : promoted) p.second = false;
+        off = hbm.alloc(bytes[item]);
+      }
+      if (off == FreeList::kNone) {
+        stats.failed_promotions++;
+        continue;
+      }
+      bool reuse = false;
+      const uint64_t end = off + align_up(bytes[item], FreeList::kAlign);
+      for (const auto& f : freed) reuse |= off < f.second && f.first < end;
+      loc[item].hbm_off = off;  // "put C_i in queueGPU": resident once its copy (ordered below) lands
+      promoted.emplace(item, reuse);
+      stats.migrations_in++;
+    }
+  }
+  // pass 3: descriptors
+  struct Stream {
+    uint32_t item;
+    uint64_t arena_off;  // != kNone: promotion target (demand mode), else a staging-ring slot
+    bool after_a;        // the arena block reuses space a launch-A descriptor of this call reads
+    std::vector<AsmDesc> descs;
+  };
+  std::vector<Stream> streamed;
+  std::unordered_map<uint32_t, size_t> stream_idx;
+  size_t nh = 0;
+  uint32_t hbm_mask = 0;
+  bool any_after_a = false;
+  for (uint32_t r = 0; r < n_req; ++r) {
+    const bool counted = ((req_counter + r) % (uint64_t)cfg.world) == (uint64_t)cfg.rank;
+    for (uint32_t j = 0; j < k; ++j) {
+      for (uint32_t kind = 0; kind < 2; ++kind) {
+        const uint32_t item = 2 * ids[(uint64_t)r * k + j] + kind;
+        AsmDesc d{};
+        d.out = (uint8_t*)(kind ? v_out[r] : k_out[r]);
+        d.count = counted ? reinterpret_cast<unsigned long long*>(delta + item) : nullptr;
+        d.slot = j;
+        d.scheme = scheme[item];
+        const auto pr = promoted.find(item);
+        const auto so = start_off.find(item);
+        if (pr == promoted.end() && (loc[item].hbm_off != FreeList::kNone || so != start_off.end())) {
+          d.codes = hbm_base + (so != start_off.end() ? so->second : loc[item].hbm_off);
           d.meta = d.codes + lay.meta_offset(d.scheme);
           db.host[nh++] = d;
           hbm_mask |= 1u << d.scheme;
           continue;
         }
+        auto it = stream_idx.find(item);
         if (it == stream_idx.end()) {
-          Stream s{item, FreeList::kNone, {}};
-          if (promote) {  // "put C_i in queueGPU": the DMA lands in the arena instead of the ring
-            s.arena_off = hbm.alloc(bytes[item]);
-            if (s.arena_off != FreeList::kNone) stats.migrations_in++;
+          Stream s{item, FreeList::kNone, false, {}};
+          if (pr != promoted.end()) {
+            s.arena_off = loc[item].hbm_off;
+            s.after_a = pr->second;
+            any_after_a |= pr->second;
           }
           it = stream_idx.emplace(item, streamed.size()).first;
           streamed.push_back(std::move(s));
@@ -582,9 +675,15 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
     }
     range[i] = {b, pos - b};
   }
-  HR_CUDA(cudaMemcpyAsync(db.dev, db.host, pos * sizeof(AsmDesc), cudaMemcpyHostToDevice, st));
+  bool need_dev = nh > (size_t)kAsmInline;
+  for (const auto& rg : range) need_dev |= rg.second > (size_t)kAsmInline;
+  if (need_dev) HR_CUDA(cudaMemcpyAsync(db.dev, db.host, pos * sizeof(AsmDesc), cudaMemcpyHostToDevice, st));
   // launch A: every resident (request, slot, kind)
-  if (nh) launch(db.dev, (uint32_t)nh, k, hbm_mask, st);
+  if (nh) launch(db.dev, db.host, (uint32_t)nh, k, hbm_mask, st);
+  if (any_after_a && nh) {
+    if (!after_a_ev) HR_CUDA(cudaEventCreateWithFlags(&after_a_ev, cudaEventDisableTiming));
+    HR_CUDA(cudaEventRecord(after_a_ev, st));
+  }
   // a7: host-tier items -> (pinned, or pageable -> pinned bounce) -> HBM (ring slot or arena) -> launch B
   cudaEvent_t c0 = nullptr, c1 = nullptr;
   if (timing && !streamed.empty()) {
@@ -610,6 +709,7 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
       from_disk = true;  // the DISK tier ("load C_i from Disk"): file -> pinned bounce -> HBM
     }
     if (!to_arena) HR_CUDA(cudaStreamWaitEvent(copy_stream, sl.free_ev, 0));
+    if (to_arena && streamed[i].after_a && nh) HR_CUDA(cudaStreamWaitEvent(copy_stream, after_a_ev, 0));
     if (c0 && i == 0) HR_CUDA(cudaEventRecord(c0, copy_stream));
     if (from_disk) {
       if (!sl.bounce) HR_CUDA(cudaHostAlloc((void**)&sl.bounce, align_up(max_item, 4096), cudaHostAllocPortable));
@@ -639,15 +739,24 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
     sl.used = true;
     stats.bytes_h2d += bytes[item];
     HR_CUDA(cudaStreamWaitEvent(st, sl.copied, 0));
-    launch(db.dev + range[i].first, (uint32_t)range[i].second, k, 1u << scheme[item], st);
-    if (to_arena)
-      loc[item].hbm_off = streamed[i].arena_off;  // resident from now on (stream-ordered)
-    else
-      HR_CUDA(cudaEventRecord(sl.free_ev, st));
+    launch(db.dev + range[i].first, db.host + range[i].first, (uint32_t)range[i].second, k, 1u << scheme[item], st);
+    if (!to_arena) HR_CUDA(cudaEventRecord(sl.free_ev, st));
   }
   HR_CUDA(cudaEventRecord(db.done, st));
+  if (call_timing) {
+    HR_CUDA(cudaEventRecord(call_ev[1], st));
+    call_recorded = true;
+  }
   req_counter += n_req;
   stats.requests += n_req;
+}
+
+double Store::last_call_ms() {
+  require(call_recorded, HR_ESTATE, "no timed hr_assemble_kv call (hr_set_timing bit 1)");
+  HR_CUDA(cudaEventSynchronize(call_ev[1]));
+  float ms = 0;
+  HR_CUDA(cudaEventElapsedTime(&ms, call_ev[0], call_ev[1]));
+  return ms;
 }
 
 // A host copy of item's blob at dst (pinned-tier fill): from the in-memory backing or the store file.
@@ -791,21 +900,30 @@ void Store::replace(cudaStream_t st) {
   std::vector<int64_t> dh(n_items);
   HR_CUDA(cudaMemcpyAsync(dh.data(), delta, sizeof(int64_t) * n_items, cudaMemcpyDeviceToHost, st));
   HR_CUDA(cudaStreamSynchronize(st));
-  epoch_update(h.data(), dh.data(), n_items, cfg.decay_shift);  // a9 (R20)
+  // the epoch is computed on copies and committed only once it is known to be applicable, so a
+  // refused re-placement (HR_ESTATE) leaves hotness, rank order and delta untouched
+  std::vector<uint64_t> h_new(h);
+  epoch_update(h_new.data(), dh.data(), n_items, cfg.decay_shift);  // a9 (R20)
+  std::vector<uint32_t> order_new = rank_items(h_new.data(), n_items);
+  std::swap(order, order_new);
+  std::vector<uint32_t> nt = place_lists();  // Alg. 2 step 1 over the new order
+  std::swap(order, order_new);
+  if (!alg2) {
+    if (cfg.backing_pinned && !on_disk)
+      for (auto& t : nt)
+        if (t == HR_T_PAGE) t = HR_T_PIN;
+    poll_promotions(true);  // the previous epoch's copies (normally long done)
+    bool any_move = false;
+    for (uint32_t i = 0; i < n_items; ++i) any_move |= (nt[i] == HR_T_HBM) != (loc[i].hbm_off != FreeList::kNone);
+    require(!any_move || cfg.keep_backing || disk_fd >= 0, HR_ESTATE, "re-placement needs keep_backing = 1");
+  }
+  h.swap(h_new);
+  order.swap(order_new);
   HR_CUDA(cudaMemsetAsync(delta, 0, sizeof(int64_t) * n_items, st));
-  order = rank_items(h.data(), n_items);
-  std::vector<uint32_t> nt = place_lists();
   if (alg2) {  // demand mode (R20): only the lists change; stale queue entries leave by LRU
     alg2->set_lists(nt.data());
     return;
   }
-  if (cfg.backing_pinned && !on_disk)
-    for (auto& t : nt)
-      if (t == HR_T_PAGE) t = HR_T_PIN;
-  poll_promotions(true);  // the previous epoch's copies (normally long done)
-  bool any_move = false;
-  for (uint32_t i = 0; i < n_items; ++i) any_move |= (nt[i] == HR_T_HBM) != (loc[i].hbm_off != FreeList::kNone);
-  require(!any_move || cfg.keep_backing || disk_fd >= 0, HR_ESTATE, "re-placement needs keep_backing = 1");
   if (!mig_ev) HR_CUDA(cudaEventCreateWithFlags(&mig_ev, cudaEventDisableTiming));
   HR_CUDA(cudaEventRecord(mig_ev, st));
   HR_CUDA(cudaStreamWaitEvent(copy_stream, mig_ev, 0));
@@ -856,6 +974,9 @@ void Store::replace(cudaStream_t st) {
         HR_CUDA(cudaStreamSynchronize(copy_stream));
         read_disk(i, sl.bounce);
         HR_CUDA(cudaMemcpyAsync(hbm_base + off, sl.bounce, bytes[i], cudaMemcpyHostToDevice, copy_stream));
+        // the next user of this bounce buffer (a streamed item of hr_assemble_kv) waits for the DMA
+        HR_CUDA(cudaEventRecord(sl.copied, copy_stream));
+        sl.used = true;
       }
       Promo pr{i, off, nullptr};
       HR_CUDA(cudaEventCreateWithFlags(&pr.ev, cudaEventDisableTiming));

@@ -96,7 +96,8 @@ struct Store {
   uint64_t bytes_read_alg(uint32_t item) const;
   DescBuf& desc_buffer(size_t n);
   void ensure_ring();
-  void launch(const AsmDesc* dev_descs, uint32_t n, uint32_t k, uint32_t scheme_mask, cudaStream_t st);
+  void launch(const AsmDesc* dev_descs, const AsmDesc* host_descs, uint32_t n, uint32_t k, uint32_t scheme_mask,
+              cudaStream_t st);
   void compact_hbm();
   void validate_request(uint32_t n_req, uint32_t k, const uint32_t* ids, void* const* k_out,
                         void* const* v_out) const;
@@ -151,15 +152,20 @@ struct Store {
   std::vector<Slot> ring;
   uint64_t req_counter = 0;
 
-  bool timing = false;
+  bool timing = false;       // CUDA events around every assemble launch (stats.kernel_ms)
+  bool call_timing = false;  // CUDA events around every hr_assemble_kv call (hr_last_call_ms)
+  bool call_recorded = false;
+  cudaEvent_t call_ev[2] = {nullptr, nullptr};
+  double last_call_ms();
   int grid_override = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timers;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> h2d_timers;  // copy-stream window per assemble call
   std::unique_ptr<CopyPool> copy_pool;                           // pageable -> pinned bounce workers
   // demand mode (cfg.demand_mode = 1): the paper-literal Alg. 2 step 2 state machine
   std::unique_ptr<Alg2> alg2;
-  std::vector<std::pair<uint64_t, uint64_t>> pending_hbm_free, pending_pin_free, pending_page_free;  // (off, bytes)
+  std::vector<std::pair<uint64_t, uint64_t>> pending_pin_free, pending_page_free;  // (off, bytes)
   cudaEvent_t start_ev = nullptr;
+  cudaEvent_t after_a_ev = nullptr;  // recorded after launch A when a promotion reuses space it reads
   // eager re-placement: asynchronous promotions (item becomes resident when its copy event completes)
   struct Promo {
     uint32_t item;

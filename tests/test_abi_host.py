@@ -41,6 +41,15 @@ def test_config_validation():
         hr.item_bytes("INT8", L=2, H=2, D=64, T=64, group=48)  # power of two
     with pytest.raises(hr.HaragError):
         hr.item_bytes("GSE8", L=2, H=2, D=64, T=64, gse=(5, 2))
+    # Alg. 1 needs exactly one tau per ladder boundary; a short list must not leave
+    # hr_config_default's thresholds in place or let the C side read past the array
+    with pytest.raises(ValueError):
+        hr.make_config(L=2, H=2, D=64, T=64, ladder=("INT8", "FP8E4M3", "GSE8"), taus=(0.1,))
+    with pytest.raises(ValueError):
+        hr.make_config(L=2, H=2, D=64, T=64, ladder=("INT8",) * 7, taus=(0.1,) * 6)
+    with pytest.raises(ValueError):
+        hr.policy_assign(np.arange(8), ["INT8", "GSE8"], [])
+    assert list(hr.policy_assign(np.arange(8), ["INT8", "GSE8"], [0.25])) == [4] * 6 + [1] * 2
 
 
 @pytest.mark.parametrize("scheme", ["PASS16", "INT8", "FP8E4M3", "FP8E5M2", "GSE8", "INT4"])

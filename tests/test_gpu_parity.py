@@ -370,8 +370,13 @@ def test_demand_mode_matches_oracle_alg2(torch_cuda, backing_pinned):
         got = [st.item_info(i)[1] for i in range(2 * n_docs)]
         assert {i for i in range(2 * n_docs) if got[i] == 0} == gpu_q, call
         assert {i for i in range(2 * n_docs) if got[i] == 1} == pin_q - gpu_q, call
+        # physical residency follows queueGPU: the HBM arena holds exactly its items (no leaked or
+        # lagging arena blocks) and nothing else
+        res = [st.item_residency(i) for i in range(2 * n_docs)]
+        assert {i for i in range(2 * n_docs) if res[i] & hr.R_HBM} == gpu_q, call
+        assert st.stats()["hbm_used"] == sum((sizes[i] + 255) // 256 * 256 for i in gpu_q), call
     s = st.stats()
-    assert s["hbm_used"] <= hb and s["migrations_in"] > 0
+    assert s["hbm_used"] <= hb and s["migrations_in"] > 0 and s["failed_promotions"] == 0
 
 
 @pytest.mark.parametrize("page_items", [0, 4])
@@ -412,6 +417,9 @@ def test_demand_mode_four_tiers_matches_oracle(torch_cuda, tmp_path, page_items)
         got = [ld.item_info(i)[1] for i in range(32)]
         exp = [0 if i in q[0] else 1 if i in q[1] else 2 if i in q[2] else 3 for i in range(32)]
         assert got == exp, call
+        res = [ld.item_residency(i) for i in range(32)]
+        assert {i for i in range(32) if res[i] & hr.R_HBM} == q[0], call
+        assert all(r & hr.R_FILE for r in res)
     assert want[3] > 0 and (page_items == 0 or want[2] > 0)
     ld.close()
 
@@ -716,3 +724,23 @@ def test_save_load_and_disk_tier(torch_cuda, tmp_path, disk_backing, demand, pag
     st.save(path)
     with pytest.raises(hr.HaragError, match="EINVAL"):
         other.build_from_file(path)
+
+
+def test_refused_replace_leaves_epoch_state(torch_cuda):
+    """hr_replace that cannot migrate (keep_backing = 0 and the lists move) returns HR_ESTATE and
+    leaves hotness, rank order and the accumulated delta exactly as they were."""
+    import paper_2510_20878_b200 as hr
+    torch = torch_cuda
+    st, ora, lay, h, sizes = make_pair(torch, L=2, H=2, T=64, D=64, n_docs=8, ladder=NORTH, taus=(0.25, 0.25),
+                                       dtype="fp16", hbm_items=4, keep_backing=False)
+    ranks = [st.item_rank(i) for i in range(16)]
+    cold = [i for i in range(16) if ranks[i] >= 8]
+    delta = np.zeros(16, np.int64)
+    delta[cold] = 1000                                   # the cold items would take over the HBM set
+    st.hotness_delta().copy_(torch.from_numpy(delta).cuda())
+    with pytest.raises(hr.HaragError, match="ESTATE"):
+        st.replace()
+    assert [st.item_rank(i) for i in range(16)] == ranks
+    assert np.array_equal(st.hotness_delta().cpu().numpy(), delta)
+    reqs = synth.gen_requests(8, 6, 3, 1.1, seed=9)
+    check_requests(torch, st, ora, lay, reqs)
