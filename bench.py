@@ -46,6 +46,14 @@ WORKLOADS = {
                                    desc="Llama-3-8B KV shape, full 10,000-doc store: hottest items in a 100 GiB HBM "
                                         "arena, the rest in pinned host DRAM (backing aliased doc mod 250 to fit "
                                         "host RAM; every miss still crosses the link), Zipf(1.1), top-k 10, batch 32")),
+    # BASELINE.json configs[2]: Llama-2-7B MHA KV shape (the paper's model), 50k docs (legs only)
+    "c3": dict(L=32, H=32, D=128, T=512, n_docs=50000, k=10, batch=32, s=1.1, dtype="bf16",
+               ladder=PAPER_LADDER, taus=(0.1, 0.1, 0.1), desc="Llama-2-7B MHA KV shape (32 layers x 32 heads x "
+               "head_dim 128), 50,000 docs of 512 tokens, paper ladder, Zipf(1.1), top-k 10, batch 32"),
+    # BASELINE.json configs[3]: Llama-3-70B KV shape, 10k docs (legs only; all-HBM sub-store of 1,000 docs)
+    "c4": dict(L=80, H=8, D=128, T=512, n_docs=10000, k=10, batch=32, s=1.1, dtype="bf16",
+               ladder=PAPER_LADDER, taus=(0.1, 0.1, 0.1), desc="Llama-3-70B KV shape (80 layers x 8 KV heads x "
+               "head_dim 128), 512-token chunks, paper ladder, Zipf(1.1), top-k 10, batch 32"),
     # BASELINE.json configs[0]
     "tiny": dict(L=2, H=2, D=64, T=64, n_docs=16, k=4, batch=8, s=1.1, dtype="fp16", ladder=NORTH_LADDER,
                  taus=(0.25, 0.25), desc="tiny store: 16 chunks x 64 tokens, 2 layers, 2 KV heads, head_dim 64, "
@@ -115,71 +123,128 @@ def alg_bytes_per_elem(scheme: str, G: int) -> float:
 
 
 # ------------------------------------------------------------------ oracle
-class OracleSample:
-    """The CPU oracle on a bounded sample of the workload: request 0 of the
-    first batch, restricted to the first `layers` layers (all heads).  Packed
-    blobs are prepared once (compression is offline); what is timed is the
-    oracle's assemble = decode + scatter, the same work the GPU step does."""
+# The cpu_baseline leg and --impl reference: the CPU oracle as it stands (oracle/), timed on the
+# host cores.  These are the only places bench.py runs oracle code.
+def _oracle_prepare(args):
+    """Worker: packed blob of one item (offline compression: gen_item -> encode_item)."""
+    from oracle import store as ost
+    import synth
+    (L, H, T, D, dtype, doc, kind, scheme) = args
+    lay = ost.Layout(L=L, H=H, T=T, D=D, dtype=dtype)
+    return ost.encode_item(synth.gen_item(L, H, T, D, doc, kind, dtype=dtype), scheme, lay)
 
-    def __init__(self, wl, req, layers: int):
+
+def _oracle_decode(args):
+    """Worker: the oracle's decode of one packed item (oracle.store.decode_item)."""
+    from oracle import store as ost
+    (L, H, T, D, dtype, blob, scheme) = args
+    return ost.decode_item(blob, scheme, ost.Layout(L=L, H=H, T=T, D=D, dtype=dtype))
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+class OracleSample:
+    """The CPU oracle on one WHOLE request of the workload (request 0 of the first batch: k docs,
+    K and V, every layer and head).  Packed blobs are prepared once (compression is offline,
+    P:107); what is timed is the oracle's assemble = decode of every item + scatter into the
+    request's KV cache (oracle.store.decode_item, oracle.store.assemble) — the work the GPU step
+    does per request.  Two ways: one thread (numpy in this process), and all host cores (the same
+    oracle functions in a pool of nproc processes, one item per task, results gathered and
+    scattered here)."""
+
+    def __init__(self, wl, req, pool=None):
         from oracle import hotness
         from oracle import store as ost
         import synth
         L, H, D, T, k = wl["L"], wl["H"], wl["D"], wl["T"], wl["k"]
-        self.ost, self.wl, self.layers = ost, wl, layers
-        self.lay = ost.Layout(L=layers, H=H, T=T, D=D, dtype=wl["dtype"])
-        prof = synth.gen_requests(wl["n_docs"], 4 * wl["n_docs"], k, wl["s"], seed=7)
+        self.ost, self.wl = ost, wl
+        self.lay = ost.Layout(L=L, H=H, T=T, D=D, dtype=wl["dtype"])
+        prof = synth.gen_requests(wl["n_docs"], 4 * wl["n_docs"], k, wl["s"], seed=7, perm_seed=1)
         h = hotness.count_requests(prof, wl["n_docs"]).astype(np.uint64)
         names = {"PASS16": ost.PASS16, "INT8": ost.INT8, "FP8E4M3": ost.FP8E4M3, "FP8E5M2": ost.FP8E5M2,
                  "GSE8": ost.GSE8, "INT4": ost.INT4}
         self.schemes = hotness.assign_schemes(h.tolist(), [names[s] for s in wl["ladder"]], wl["taus"])
         self.req = [int(d) for d in req]
-        self.blobs = {}
-        for d in self.req:
-            for kind in (0, 1):
-                x = synth.gen_item(layers, H, T, D, d, kind, dtype=wl["dtype"])
-                self.blobs[2 * d + kind] = ost.encode_item(x, self.schemes[2 * d + kind], self.lay)
+        self.items = [2 * d + kind for d in self.req for kind in (0, 1)]
+        self.nproc = os.cpu_count() or 1
+        self.pool = pool
+        jobs = [(L, H, T, D, wl["dtype"], i // 2, i % 2, self.schemes[i]) for i in self.items]
+        blobs = list(pool.map(_oracle_prepare, jobs)) if pool else [_oracle_prepare(j) for j in jobs]
+        self.blobs = dict(zip(self.items, blobs))
 
-    def run_once(self) -> tuple[int, float]:
+    def _jobs(self):
+        w = self.wl
+        return [(w["L"], w["H"], w["T"], w["D"], w["dtype"], self.blobs[i], self.schemes[i]) for i in self.items]
+
+    def run_once(self, parallel: bool) -> tuple[int, float]:
         t0 = time.perf_counter()
-        dec = {i: self.ost.decode_item(b, self.schemes[i], self.lay) for i, b in self.blobs.items()}
+        if parallel:
+            dec = dict(zip(self.items, self.pool.map(_oracle_decode, self._jobs())))
+        else:
+            dec = {i: self.ost.decode_item(self.blobs[i], self.schemes[i], self.lay) for i in self.items}
         K, V = self.ost.assemble(dec, self.req, self.lay)
         return K.nbytes + V.nbytes, time.perf_counter() - t0
 
-    def describe(self, reps: int, nbytes: int) -> str:
+    def describe(self, reps: int, nbytes: int, parallel: bool) -> str:
         wl = self.wl
-        return (f"assemble (decode + scatter) of request 0 (k={wl['k']}) restricted to layer(s) 0..{self.layers - 1} "
-                f"of {wl['L']} (all {wl['H']} heads), {reps} repetition(s), {nbytes / 1e6:.0f} MB of "
-                f"{wl['dtype']} KV output; numpy, single-threaded")
+        how = (f"{self.nproc} processes (oracle.store.decode_item per item over a process pool)" if parallel
+               else "1 thread (numpy)")
+        return (f"assemble (decode + scatter) of one whole request (k={wl['k']} docs, K and V, all {wl['L']} layers x "
+                f"{wl['H']} heads x {wl['T']} tokens x {wl['D']}), {reps} repetition(s), {nbytes / 1e6:.0f} MB of "
+                f"{wl['dtype']} KV output; {how}; CPU: {cpu_model()}")
 
 
-def oracle_baseline(wl, req, budget_s: float = 10.0, layers: int = 2):
-    smp = OracleSample(wl, req, layers)
-    total_b, total_t, reps = 0, 0.0, 0
-    while reps < 1 or (total_t < budget_s and reps < 5):
-        b, t = smp.run_once()
-        total_b, total_t, reps = total_b + b, total_t + t, reps + 1
-    return {"value": round(total_b / total_t / 1e9, 5), "unit": "GB/s", "cores": 1, "kind": "oracle",
-            "sample": smp.describe(reps, total_b)}
+def oracle_pool():
+    import multiprocessing as mp
+    from concurrent.futures import ProcessPoolExecutor
+    return ProcessPoolExecutor(os.cpu_count() or 1, mp_context=mp.get_context("spawn"))
+
+
+def oracle_baseline(wl, req):
+    """cpu_baseline: the oracle on one whole request, single-threaded and on all host cores."""
+    with oracle_pool() as pool:
+        smp = OracleSample(wl, req, pool)
+        smp.run_once(True)                               # pool warm-up (imports in the workers)
+        b1, t1 = smp.run_once(False)
+        bn, tn, reps = 0, 0.0, 0
+        while reps < 3:
+            b, t = smp.run_once(True)
+            bn, tn, reps = bn + b, tn + t, reps + 1
+    return {"value": round(bn / tn / 1e9, 5), "unit": "GB/s", "cores": smp.nproc, "kind": "oracle",
+            "sample": smp.describe(reps, bn, True), "cpu_model": cpu_model(), "nproc": smp.nproc,
+            "single_thread": {"value": round(b1 / t1 / 1e9, 5), "unit": "GB/s", "cores": 1,
+                              "sample": smp.describe(1, b1, False)}}
 
 
 def run_reference(args, wl):
-    """--impl reference: the CPU oracle as it stands, on rank 0 only."""
+    """--impl reference: the CPU oracle as it stands on the box's host cores, rank 0 only; a step
+    = the oracle's assemble of one whole request of the workload on all cores."""
     if env_int("RANK", 0) != 0:
         return
     import synth
     reqs = synth.gen_requests(wl["n_docs"], wl["batch"], wl["k"], wl["s"], seed=1)
-    smp = OracleSample(wl, reqs[0], layers=1)
-    for _ in range(args.warmup):
-        smp.run_once()
-    times, nb = [], 0
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        b, t = smp.run_once()
-        times.append(t)
-        nb = b
-        if time.perf_counter() - t0 > 150:  # keep the whole arm within a few minutes
-            break
+    with oracle_pool() as pool:
+        smp = OracleSample(wl, reqs[0], pool)
+        for _ in range(args.warmup):
+            smp.run_once(True)
+        times, nb = [], 0
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            b, t = smp.run_once(True)
+            times.append(t)
+            nb = b
+            if time.perf_counter() - t0 > 150:  # keep the whole arm within a few minutes
+                break
     tot = sum(times)
     v = nb * len(times) / tot / 1e9
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 5), "unit": "GB/s", "n_gpus": args.gpus,
@@ -187,9 +252,9 @@ def run_reference(args, wl):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": wl["desc"], "global_batch": wl["batch"], "k": wl["k"],
-                       "step": "one bounded sample: " + smp.describe(1, nb)},
-            "cpu_baseline": {"value": round(v, 5), "unit": "GB/s", "cores": 1, "kind": "oracle",
-                             "sample": smp.describe(len(times), nb * len(times))},
+                       "step": "one bounded sample: " + smp.describe(1, nb, True)},
+            "cpu_baseline": {"value": round(v, 5), "unit": "GB/s", "cores": smp.nproc, "kind": "oracle",
+                             "sample": smp.describe(len(times), nb * len(times), True), "cpu_model": cpu_model()},
             "e2e": {"value": round(v, 5), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -218,12 +283,27 @@ class Ctx:
             else:
                 dist.init_process_group(backend)
         self.stream = torch.cuda.current_stream()
+        self.placement_checks = 0
 
     def barrier(self):
         self.torch.cuda.synchronize()
         if self.world > 1:
             self.dist.barrier()
             self.torch.cuda.synchronize()
+
+    def check_placement(self, st):
+        """Debug consistency check after an epoch: every rank's placement digest
+        (hr_placement_hash) must be identical — MIN == MAX over ranks."""
+        if self.world == 1:
+            return
+        hv = st.placement_hash()
+        t = self.torch.tensor([hv - (1 << 64) if hv >= 1 << 63 else hv] * 2, dtype=self.torch.int64, device="cuda")
+        self.dist.all_reduce(t[0:1], op=self.dist.ReduceOp.MIN)
+        self.dist.all_reduce(t[1:2], op=self.dist.ReduceOp.MAX)
+        lo, hi = t.tolist()
+        if lo != hi:
+            raise RuntimeError(f"rank {self.rank}: placement diverged across ranks after hr_replace ({lo} != {hi})")
+        self.placement_checks += 1
 
     def allreduce(self, vals, op="max"):
         t = self.torch.tensor([float(v) for v in vals], dtype=self.torch.float64, device="cuda")
@@ -237,8 +317,10 @@ def build_store(ctx, wl, **over):
     import paper_2510_20878_b200 as hr
     import synth
     L, H, D, T, k = wl["L"], wl["H"], wl["D"], wl["T"], wl["k"]
-    prof = synth.gen_requests(wl["n_docs"], 4 * wl["n_docs"], k, wl["s"], seed=7)
-    h = hr.policy_count(prof, wl["n_docs"]).astype(np.uint64)   # offline profile
+    # offline profile: a trace of the same popularity ranking as the served requests (their doc
+    # permutation, perm seed 1) drawn independently (seed 7) — the profile predicts, it does not replay
+    prof = synth.gen_requests(wl["n_docs"], 4 * wl["n_docs"], k, wl["s"], seed=7, perm_seed=1)
+    h = hr.policy_count(prof, wl["n_docs"]).astype(np.uint64)
     schemes = hr.policy_assign(h, wl["ladder"], wl["taus"])
     geo = dict(L=L, H=H, D=D, T=T, dtype=wl["dtype"], rank=ctx.rank, world=ctx.world)
     total = sum(hr.item_bytes(int(sc), **geo) for sc in schemes)
@@ -269,6 +351,7 @@ def timed_steps(ctx, st, pool, ko, vo, steps, warmup, epoch_every, sample_clocks
             if ctx.world > 1:
                 dist.all_reduce(st.hotness_delta(), op=dist.ReduceOp.SUM)   # a9: the one collective
             st.replace(stream=ctx.stream)
+            ctx.check_placement(st)
 
     for i in range(warmup):
         step(i)
@@ -292,6 +375,35 @@ def timed_steps(ctx, st, pool, ko, vo, steps, warmup, epoch_every, sample_clocks
     ms_max, = ctx.allreduce([ms], "max")
     tot_bytes, = ctx.allreduce([stats["bytes_out"]], "sum")
     return ms_max, tot_bytes, stats, clocks
+
+
+def request_latency(ctx, st, reqs, ko1, vo1, n=256):
+    """Per-request assemble latency (one request of k docs per call), device clock: from the
+    hr_assemble_kv entry (an event the library records on the stream before any of the call's
+    work) to the end of its last launch — planning, descriptor upload, host-tier copies and
+    kernels included, the Python binding's argument marshalling excluded.  Also reported: the
+    same calls bracketed from Python (CUDA events around the binding call).  p50/p99 over n
+    calls on an idle stream, max over ranks."""
+    torch = ctx.torch
+    st.set_timing(False, calls=True)
+    st.reset_stats()
+    lat, lat_py = [], []
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for i in range(n + 8):
+        req = reqs[i % len(reqs):i % len(reqs) + 1]
+        e0.record(ctx.stream)
+        st.assemble(req, ko1, vo1, stream=ctx.stream)
+        e1.record(ctx.stream)
+        ms = st.last_call_ms()
+        e1.synchronize()
+        if i >= 8:   # warm-up calls excluded
+            lat.append(ms * 1e3)
+            lat_py.append(e0.elapsed_time(e1) * 1e3)
+    st.set_timing(False, calls=False)
+    host_us = st.stats()["host_ms"] * 1e3 / (n + 8)
+    p50, p99, q50, q99 = ctx.allreduce([np.percentile(lat, 50), np.percentile(lat, 99),
+                                        np.percentile(lat_py, 50), np.percentile(lat_py, 99)], "max")
+    return p50, p99, {"p50": round(q50, 1), "p99": round(q99, 1), "library_host_us_mean": round(host_us, 1)}
 
 
 def link_peak(ctx, gib=1, reps=10):
@@ -376,8 +488,117 @@ def run_per_scheme(ctx, wl, args):
     return res
 
 
+LEGS = {
+    # name: base workload, tier mix, budgets.  "pinned": hot set in the HBM arena, every other item
+    # in a pinned host backing; "pageable": hot set in HBM, PIN_LIST in a 16 GiB pinned tier, the rest
+    # in a pageable backing (staged through pinned bounce buffers); "hbm": every item in HBM.
+    # Host backings are aliased (docs with equal doc mod R and scheme share one blob) to fit host RAM;
+    # every miss still crosses the host link.
+    "c2_tiered_pinned": dict(base="c2", n_docs=10000, tier="pinned", hbm_budget=100 << 30, alias_R=250, steps=20,
+                             desc="Llama-3-8B KV shape, full 10,000-doc store: hottest items in a 100 GiB HBM arena, "
+                                  "the rest in pinned host DRAM, Zipf(1.1), top-k 10, batch 32"),
+    "c2_tiered_pageable": dict(base="c2", n_docs=10000, tier="pageable", hbm_budget=100 << 30, pin_budget=16 << 30,
+                               alias_R=250, steps=20,
+                               desc="Llama-3-8B KV shape, full 10,000-doc store: 100 GiB HBM hot set, next items in "
+                                    "a 16 GiB pinned tier, the rest in PAGEABLE host DRAM (host-staged cold: "
+                                    "pageable -> pinned bounce -> HBM, P:213), Zipf(1.1), top-k 10, batch 32"),
+    "c3_llama2_7b_mha": dict(base="c3", tier="pinned", hbm_budget=80 * 10 ** 9, alias_R=100, steps=5,
+                             desc="BASELINE config 2: Llama-2-7B MHA KV shape (32 layers x 32 heads x 128), 50,000 "
+                                  "docs of 512 tokens, hot set in an HBM arena of up to 80 GB, cold in pinned host "
+                                  "DRAM, Zipf(1.1), top-k 10, batch 32 requests (86 GB of KV per batch)"),
+    "c4_llama3_70b_hbm": dict(base="c4", n_docs=1000, tier="hbm", steps=10,
+                              desc="BASELINE config 3: Llama-3-70B KV shape (80 layers x 8 KV heads x 128), "
+                                   "1,000-doc all-HBM sub-store, Zipf(1.1), top-k 10, batch 32"),
+    "c4_llama3_70b_tiered": dict(base="c4", tier="pinned", hbm_budget=80 * 10 ** 9, alias_R=100, steps=5,
+                                 desc="BASELINE config 3: Llama-3-70B KV shape, 10,000 docs, hot set in an HBM arena "
+                                      "of up to 80 GB, cold in pinned host DRAM, Zipf(1.1), top-k 10, batch 32"),
+}
+
+
+def kernel_roofline(stats, peak, peak_src, traffic=None):
+    """Assemble kernels of the timed region: algorithmic HBM bytes (codes + meta read, KV written) over
+    their summed CUDA-event durations (library events on the launching stream)."""
+    launches = max(1, stats["timed_launches"])
+    avg_ms = stats["kernel_ms"] / launches
+    alg_per_launch = stats["bytes_hbm_alg"] / max(1, stats["kernel_launches"])
+    achieved = alg_per_launch / (avg_ms / 1e3) / 1e9 if avg_ms else 0.0
+    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+            "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": "assemble_kv_kernel",
+            "avg_launch_ms": round(avg_ms, 4), "alg_bytes_per_launch": int(alg_per_launch),
+            "launches": int(stats["kernel_launches"]), "peak_source": peak_src}
+
+
+def run_leg(ctx, name, spec, args):
+    """One measurement leg (LEGS): build the store, time `steps` batches (W = 3), report assembled
+    GB/s, the assemble kernels' HBM roofline, the host link and overlapped rooflines (tiered legs)
+    and single-request latency p50/p99 (mixed tiers in tiered legs)."""
+    import synth
+    torch = ctx.torch
+    base = WORKLOADS[spec["base"]]
+    wl = dict(base, **{k_: v for k_, v in spec.items() if k_ in ("n_docs", "batch", "k", "s")})
+    B, k = wl["batch"], wl["k"]
+    L, H, D, T = wl["L"], wl["H"], wl["D"], wl["T"]
+    Hl = H // ctx.world
+    kvb = L * Hl * k * T * D * 2
+    tier = spec["tier"]
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    out = torch.empty(B * kvb, dtype=torch.int16, device="cuda")     # 2*B*kvb bytes
+    ko = [out[(2 * r) * kvb // 2:(2 * r + 1) * kvb // 2] for r in range(B)]
+    vo = [out[(2 * r + 1) * kvb // 2:(2 * r + 2) * kvb // 2] for r in range(B)]
+    free, _ = torch.cuda.mem_get_info()
+    over = dict(decay_shift=0)
+    link = None
+    if tier == "hbm":
+        over.update(keep_backing=False)
+    else:
+        link = link_peak(ctx)
+        ring = 3 * L * Hl * T * D * 2 + (2 << 30)
+        hb = int(min(spec["hbm_budget"] // ctx.world, free - ring - (6 << 30)))
+        over.update(hbm_budget=hb, keep_backing=True, alias_R=spec["alias_R"], backing_pinned=(tier == "pinned"),
+                    pin_budget=(spec.get("pin_budget", 0) // ctx.world if tier == "pageable" else 0))
+    st, h, schemes, build_s, total = build_store(ctx, wl, **over)
+    pool = synth.gen_requests(wl["n_docs"], 8 * B, k, wl["s"], seed=1).reshape(8, B, k)
+    steps = max(3, min(args.steps, spec.get("steps", 20)))
+    ms_max, tot_bytes, stats, _ = timed_steps(ctx, st, pool, ko, vo, steps, 3, args.epoch_every, sample_clocks=False)
+    peak, peak_src = measured_hbm_peak()
+    step_s = ms_max / steps / 1e3
+    res = {"workload": spec["desc"], "value": round(tot_bytes / (ms_max / 1e3) / 1e9, 2), "unit": "GB/s",
+           "ms_per_step": round(ms_max / steps, 3), "steps": steps, "warmup": 3, "batch": B, "k": k,
+           "n_docs": wl["n_docs"], "roofline": kernel_roofline(stats, peak, peak_src),
+           "hits_per_tier": stats["hits"], "store_bytes_per_rank": int(total), "build_seconds": round(build_s, 2)}
+    if link is not None:
+        per_rank, agg = link
+        h2d_GBps = stats["bytes_h2d"] / (stats["h2d_ms"] / 1e3) / 1e9 if stats["h2d_ms"] else None
+        hbm_alg_per_step = stats["bytes_hbm_alg"] / steps
+        h2d_per_step = stats["bytes_h2d"] / steps
+        mig_per_step = stats["bytes_migrated"] / steps
+        t_star = max(hbm_alg_per_step / (peak * 1e9), (h2d_per_step + mig_per_step) / (per_rank * 1e9))
+        res.update({
+            "h2d_bytes_per_step": int(h2d_per_step), "migration_bytes_per_step": int(mig_per_step),
+            "h2d_items_per_step": stats["h2d_items"] / steps,
+            "link": {"achieved_GBps": round(h2d_GBps, 2) if h2d_GBps else None,
+                     "peak_GBps": round(per_rank, 2), "peak_all_ranks_GBps": round(agg, 2),
+                     "frac": round(h2d_GBps / per_rank, 4) if h2d_GBps else None,
+                     "window": "first host-tier copy start -> last copy end per call (copy-stream events)",
+                     "peak_source": "pinned H2D 1 GiB cudaMemcpyAsync best of 10, measured in this run"},
+            "overlapped_roofline": {"t_star_ms": round(t_star * 1e3, 3), "frac": round(t_star / step_s, 4),
+                                    "formula": "max(HBM alg bytes / hbm_gbs, (H2D + migration bytes) / link peak)"
+                                               " / step time"},
+            "hbm_budget_bytes": over["hbm_budget"], "alias_R": spec["alias_R"],
+            "backing": tier, "migrations": [stats["migrations_in"], stats["migrations_out"]]})
+    p50, p99, lat_py = request_latency(ctx, st, pool.reshape(-1, k), ko[:1], vo[:1], n=64 if tier == "hbm" else 32)
+    res["request_latency_us"] = {"p50": round(p50, 1), "p99": round(p99, 1), "bytes_out": int(2 * kvb),
+                                 "tiers": "HBM-resident" if tier == "hbm" else "mixed (misses streamed)"}
+    st.close()
+    del st, out, ko, vo
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return res
+
+
 def run_ours(args, wl):
-    import paper_2510_20878_b200 as hr
+    import paper_2510_20878_b200 as hr  # noqa: F401  (fails loudly without the native library)
     import synth
     from paper_2510_20878_b200 import SCHEMES
 
@@ -389,11 +610,7 @@ def run_ours(args, wl):
         raise SystemExit(f"H={H} not divisible by {world} GPUs")
     n_batches = 8
     pool = synth.gen_requests(wl["n_docs"], n_batches * B, k, wl["s"], seed=1).reshape(n_batches, B, k)
-
-    over = {}
-    if wl.get("tiered"):
-        over = dict(hbm_budget=wl["hbm_budget"], backing_pinned=True, keep_backing=True, alias_R=wl["alias_R"])
-    st, h, schemes, build_s, total = build_store(ctx, wl, **over)
+    st, h, schemes, build_s, total = build_store(ctx, wl)
 
     # ---- outputs: one [L][Hl][k*T][D] K and V buffer per request
     kvb = st.kv_bytes(k)
@@ -406,31 +623,15 @@ def run_ours(args, wl):
 
     # ---- roofline of the dominant kernel (assemble_kv_kernel), live CUDA events
     peak, peak_src = measured_hbm_peak()
-    launches = max(1, stats["timed_launches"])
-    avg_ms = stats["kernel_ms"] / launches
-    alg_per_launch = stats["bytes_hbm_alg"] / max(1, stats["kernel_launches"])
-    achieved = alg_per_launch / (avg_ms / 1e3) / 1e9
     traffic = args.ncu_traffic
     tfile = os.path.join(ROOT, "profiles", f"traffic_{args.workload}_b{B}_n{world}.json")
     if traffic is None and os.path.exists(tfile):
         with open(tfile) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
-    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-            "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": "assemble_kv_kernel",
-            "avg_launch_ms": round(avg_ms, 4), "alg_bytes_per_launch": int(alg_per_launch),
-            "peak_source": peak_src}
+    roof = kernel_roofline(stats, peak, peak_src, traffic)
 
     # ---- per-request assemble latency (one request of k docs), through the C ABI
-    lat = []
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for i in range(min(64, n_batches * B)):
-        req = pool.reshape(-1, k)[i:i + 1]
-        e0.record(ctx.stream)
-        st.assemble(req, ko[:1], vo[:1], stream=ctx.stream)
-        e1.record(ctx.stream)
-        e1.synchronize()
-        lat.append(e0.elapsed_time(e1) * 1e3)
-    p50, p99 = ctx.allreduce([np.percentile(lat, 50), np.percentile(lat, 99)], "max")
+    p50, p99, lat_py = request_latency(ctx, st, pool.reshape(-1, k), ko[:1], vo[:1])
 
     # ---- e2e through the C ABI with HOST buffers: ids from host, KV back to pinned host memory
     e2e = None
@@ -452,7 +653,7 @@ def run_ours(args, wl):
         e2e_ms, = ctx.allreduce([t_e0.elapsed_time(t_e1)], "max")
         e2e_bytes = 2 * B * kvb * e2e_steps * world
         e2e = {"value": round(e2e_bytes / (e2e_ms / 1e3) / 1e9, 2), "unit": "GB/s",
-               "h2d_bytes_per_step": int(B * k * 4 + 2 * B * k * 40), "d2h_bytes_per_step": int(d2h // e2e_steps),
+               "h2d_bytes_per_step": int(B * k * 4), "d2h_bytes_per_step": int(d2h // e2e_steps),
                "path": "hr_assemble_kv(host ids) -> device KV -> cudaMemcpyAsync D2H into pinned host buffers"}
         del host_out
 
@@ -463,38 +664,50 @@ def run_ours(args, wl):
     sch_hist = {name: int(np.sum(schemes == code)) for name, code in SCHEMES.items() if np.sum(schemes == code)}
     hits = stats["hits"]
     st.close()
-    del st
+    del st, out, ko, vo
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = oracle_baseline(wl, pool[0][0], budget_s=10.0, layers=2)
+        cpu = oracle_baseline(wl, pool[0][0])
 
     per_scheme = None
-    if not args.no_per_scheme and wl.get("tiered_variant"):
+    if not args.no_per_scheme and args.workload == "c2":
         per_scheme = run_per_scheme(ctx, wl, args)
 
-    # ---- host-tier leg (a7): HBM hot set + pinned cold set, streamed over the host link
-    tiered = None
-    if not args.no_tiered and wl.get("tiered_variant"):
-        tiered = run_tiered(ctx, dict(wl, **wl["tiered_variant"]), ko, vo, kvb, args)
+    # ---- the other BASELINE configs and the host tiers, each its own leg
+    legs = {}
+    names = [] if args.legs == "none" or args.workload != "c2" else (
+        list(LEGS) if args.legs == "all" else args.legs.split(","))
+    for name in names:
+        try:
+            legs[name] = run_leg(ctx, name, LEGS[name], args)
+        except Exception as e:  # noqa: BLE001 - a failed leg is reported, the headline still prints
+            legs[name] = {"error": f"{type(e).__name__}: {e}"}
+            torch.cuda.synchronize()
+            torch.cuda.empty_cache()
 
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": wl["dtype"], "data": "synthetic",
+        "request_latency_us": {"p50": round(p50, 1), "p99": round(p99, 1), "k": k, "bytes_out": int(2 * kvb),
+                               "calls": 256, "from": "hr_assemble_kv entry (library event) to last launch done",
+                               "incl_python_binding": lat_py},
+        "roofline": roof,
+        "e2e": e2e,
+        "gpu_launches": int(stats["kernel_launches"]),
+        "clocks": clocks,
+        "cpu_baseline": cpu,
         "config": {"workload": wl["desc"], "global_batch": B, "k": k, "seq_len_per_request": k * T,
                    "parallelism": f"kv-head shard x{world}" if world > 1 else "single GPU",
                    "n_docs": wl["n_docs"], "items_per_scheme": sch_hist, "epoch_every_steps": args.epoch_every,
                    "l2": "inputs larger than L2 (store and per-step output each >> 126 MB)",
-                   "store_bytes_per_rank": int(total), "hits_per_tier": hits},
-        "request_latency_us": {"p50": round(p50, 1), "p99": round(p99, 1), "k": k, "bytes_out": int(2 * kvb)},
-        "roofline": roof,
-        "cpu_baseline": cpu,
-        "e2e": e2e,
-        "gpu_launches": int(stats["kernel_launches"]),
-        "clocks": clocks,
+                   "store_bytes_per_rank": int(total), "hits_per_tier": hits,
+                   "placement_checks": ctx.placement_checks},
         "build": build,
-        "tiered": tiered,
+        "legs": legs,
         "per_scheme": per_scheme,
         "impl": "ours",
     }
@@ -502,50 +715,6 @@ def run_ours(args, wl):
         print(json.dumps(line), flush=True)
     if world > 1:
         ctx.dist.destroy_process_group()
-
-
-def run_tiered(ctx, wl, ko, vo, kvb, args):
-    """HBM-resident hot set + pinned-host cold set: per step the cold items of the batch are
-    streamed over the host link into the staging ring, overlapped with the HBM-resident launch."""
-    import synth
-    torch = ctx.torch
-    B, k = wl["batch"], wl["k"]
-    per_rank, agg = link_peak(ctx)
-    pageable = bool(getattr(args, "tiered_pageable", False))
-    st, h, schemes, build_s, total = build_store(
-        ctx, wl, hbm_budget=wl["hbm_budget"], backing_pinned=not pageable, keep_backing=True,
-        alias_R=wl["alias_R"], decay_shift=wl.get("decay_shift", 0),
-        pin_budget=(wl.get("pin_budget", 16 << 30) if pageable else 0))
-    pool = synth.gen_requests(wl["n_docs"], 8 * B, k, wl["s"], seed=1).reshape(8, B, k)
-    steps = max(3, min(args.steps, wl.get("steps", 20)))
-    ms_max, tot_bytes, stats, _ = timed_steps(ctx, st, pool, ko, vo, steps, 3, args.epoch_every, sample_clocks=False)
-    h2d_GBps = stats["bytes_h2d"] / (stats["h2d_ms"] / 1e3) / 1e9 if stats["h2d_ms"] else None
-    step_s = ms_max / steps / 1e3
-    hbm_alg_per_step = stats["bytes_hbm_alg"] / steps
-    h2d_per_step = stats["bytes_h2d"] / steps
-    mig_per_step = stats["bytes_migrated"] / steps
-    peak = measured_hbm_peak()[0]
-    t_star = max(hbm_alg_per_step / (peak * 1e9), (h2d_per_step + mig_per_step) / (per_rank * 1e9))
-    res = {"workload": wl["desc"], "value": round(tot_bytes / (ms_max / 1e3) / 1e9, 2), "unit": "GB/s",
-           "ms_per_step": round(ms_max / steps, 3), "steps": steps,
-           "hits_per_tier": stats["hits"], "h2d_bytes_per_step": int(h2d_per_step),
-           "migration_bytes_per_step": int(mig_per_step),
-           "h2d_items_per_step": stats["h2d_items"] / steps,
-           "link": {"achieved_GBps": round(h2d_GBps, 2) if h2d_GBps else None,
-                    "peak_GBps": round(per_rank, 2), "peak_all_ranks_GBps": round(agg, 2),
-                    "frac": round(h2d_GBps / per_rank, 4) if h2d_GBps else None,
-                    "peak_source": "pinned H2D 1 GiB cudaMemcpyAsync best of 10, measured in this run"},
-           "overlapped_roofline": {"t_star_ms": round(t_star * 1e3, 3),
-                                   "frac": round(t_star / step_s, 4),
-                                   "formula": "max(HBM alg bytes / hbm_gbs, (H2D + migration bytes) / link peak)"
-                                              " / step time"},
-           "hbm_budget_bytes": wl["hbm_budget"], "alias_R": wl["alias_R"], "build_seconds": round(build_s, 2),
-           "backing": "pageable (+16 GiB pinned PIN_LIST tier; P:213 pageable -> pinned bounce -> HBM)" if pageable
-                      else "pinned",
-           "decay_shift": wl.get("decay_shift", 0),
-           "migrations": [stats["migrations_in"], stats["migrations_out"]]}
-    st.close()
-    return res
 
 
 def run_ablation(args, wl):
@@ -620,7 +789,7 @@ def run_tau_sweep(args, wl):
     B, k = tv["batch"], tv["k"]
     geo = dict(L=tv["L"], H=tv["H"], D=tv["D"], T=tv["T"], dtype=tv["dtype"], rank=ctx.rank, world=ctx.world)
     pool = synth.gen_requests(tv["n_docs"], 8 * B, k, tv["s"], seed=1).reshape(8, B, k)
-    prof = synth.gen_requests(tv["n_docs"], 4 * tv["n_docs"], k, tv["s"], seed=7)
+    prof = synth.gen_requests(tv["n_docs"], 4 * tv["n_docs"], k, tv["s"], seed=7, perm_seed=1)
     h = hr.policy_count(prof, tv["n_docs"]).astype(np.uint64)
     alg1 = {"param1": (0.10, 0.05, 0.05), "param2": (0.10, 0.10, 0.05), "param3": (0.10, 0.10, 0.10),
             "param4": (0.15, 0.10, 0.10)}
@@ -672,21 +841,28 @@ def run_drift(args, wl):
     ctx = Ctx(args)
     torch = ctx.torch
     n_docs, k, B, L, D, T = 100_000, 10, 32, wl["L"], wl["D"], wl["T"]
+    # N = 1: one process holds the per-rank slice of the 8-GPU run (1 of 8 KV heads).  N > 1: the
+    # real sharded run — all 8 KV heads split over the ranks, each rank counting its requests
+    # (q mod N), the deltas all-reduced (NCCL SUM) every epoch and the placement digests compared.
+    H = 1 if ctx.world == 1 else wl["H"]
+    if H % ctx.world:
+        raise SystemExit(f"H={H} not divisible by {ctx.world} GPUs")
+    Hl = H // ctx.world
     phases = (0.6, 0.8, 1.0, 1.2, 0.6)
     n_phase, epoch_req = env_int("HARAG_DRIFT_REQS", 4096), 256
     seed = 5                                          # config index
-    geo = dict(L=L, H=1, D=D, T=T, dtype=wl["dtype"])
+    geo = dict(L=L, H=H, D=D, T=T, dtype=wl["dtype"], rank=ctx.rank, world=ctx.world)
     prof = synth.gen_requests(n_docs, 16384, k, phases[0], seed=99, perm_seed=seed ^ 0x9E3779B9)
     h = hr.policy_count(prof, n_docs).astype(np.uint64)
     schemes = hr.policy_assign(h, PAPER_LADDER, (0.1, 0.1, 0.1))
     hb, _ = fraction_budgets(hr, h, schemes, geo, 0.05, 0.0)
-    alias = 2000
+    alias = max(250, 2000 // Hl)    # host backing ~17 GB per rank whatever the shard
     phase_reqs = [synth.gen_requests(n_docs, n_phase, k, s, seed=seed + 16 * p, perm_seed=seed ^ 0x9E3779B9 ^ p)
                   for p, s in enumerate(phases)]
 
     def src(doc, kp, vp, strm):
-        synth.gen_item_device(kp, L, 1, T, D, doc, 0, dtype=wl["dtype"], stream=strm, alias_R=alias)
-        synth.gen_item_device(vp, L, 1, T, D, doc, 1, dtype=wl["dtype"], stream=strm, alias_R=alias)
+        synth.gen_item_device(kp, L, H, T, D, doc, 0, dtype=wl["dtype"], stream=strm, alias_R=alias)
+        synth.gen_item_device(vp, L, H, T, D, doc, 1, dtype=wl["dtype"], stream=strm, alias_R=alias)
 
     arms = {}
     out = ko = vo = None
@@ -713,18 +889,27 @@ def run_drift(args, wl):
                     st.assemble(reqs[e * epoch_req + b * B:e * epoch_req + (b + 1) * B], ko, vo, stream=ctx.stream)
                 e1.record(ctx.stream)
                 e1.synchronize()
-                a_ms = e0.elapsed_time(e1)
+                a_ms, = ctx.allreduce([e0.elapsed_time(e1)], "max")
                 stt = st.stats()
                 t1 = time.perf_counter()
-                st.replace(stream=ctx.stream)         # a9 (N = 1: the all-reduce is the identity)
+                ar_ms = 0.0
+                if ctx.world > 1:                     # a9: the one collective (NCCL SUM of int64 deltas)
+                    ctx.barrier()
+                    ta = time.perf_counter()
+                    ctx.dist.all_reduce(st.hotness_delta(), op=ctx.dist.ReduceOp.SUM)
+                    torch.cuda.synchronize()
+                    ar_ms = (time.perf_counter() - ta) * 1e3
+                st.replace(stream=ctx.stream)
+                ctx.check_placement(st)
                 torch.cuda.synchronize()              # promotions included
-                r_ms = (time.perf_counter() - t1) * 1e3
+                r_ms, ar_ms = ctx.allreduce([(time.perf_counter() - t1) * 1e3, ar_ms], "max")
                 st2 = st.stats()
                 hits = stt["hits"]
                 series.append({"phase": p, "s": s, "epoch": e,
                                "hbm_hit_rate": round(hits[0] / max(1, sum(hits)), 4),
                                "assemble_ms": round(a_ms, 2), "ms_per_request": round(a_ms / epoch_req, 3),
                                "h2d_GB": round(stt["bytes_h2d"] / 1e9, 3), "replace_ms": round(r_ms, 2),
+                               "allreduce_ms": round(ar_ms, 3),
                                "migrated_GB": round((st2["bytes_migrated"] - stt["bytes_migrated"]) / 1e9, 3),
                                "promoted": st2["migrations_in"] - stt["migrations_in"]})
         st.close()
@@ -741,11 +926,15 @@ def run_drift(args, wl):
                               "replace_ms_median": round(statistics.median(r["replace_ms"] for r in rows), 1)})
         arms[f"decay_shift_{decay}"] = {"phases": per_phase, "epochs": series, "build_seconds": round(build_s, 1)}
     line = {"drift": {"arms": arms, "hbm_budget_GB": round(hb / 1e9, 2), "n_docs": n_docs,
-                      "requests_per_phase": n_phase, "epoch_requests": epoch_req, "batch": B, "k": k},
-            "workload": "BASELINE config 5 per-rank slice: 100,000 docs of Llama-3-8B KV shape, 1 of 8 KV heads "
-                        "(L=32, H=1, D=128, T=512), paper ladder, HBM = hottest 5% of items, cold in pinned host "
-                        "DRAM (backing aliased doc mod 2000), Zipf phases 0.6/0.8/1.0/1.2/0.6; replace_ms includes "
-                        "the promotions' H2D copies"}
+                      "requests_per_phase": n_phase, "epoch_requests": epoch_req, "batch": B, "k": k,
+                      "n_gpus": ctx.world, "kv_heads_per_rank": Hl, "placement_checks": ctx.placement_checks},
+            "workload": (("BASELINE config 5 per-rank slice: 100,000 docs of Llama-3-8B KV shape, 1 of 8 KV heads "
+                          "(L=32, H=1, D=128, T=512)") if ctx.world == 1 else
+                         (f"BASELINE config 5 on {ctx.world} GPUs: 100,000 docs of Llama-3-8B KV shape (L=32, H=8, "
+                          f"D=128, T=512), {Hl} KV head(s) per rank, deltas all-reduced (NCCL SUM) every epoch")) +
+                        f", paper ladder, HBM = hottest 5% of items, cold in pinned host DRAM (backing aliased doc "
+                        f"mod {alias}), Zipf phases 0.6/0.8/1.0/1.2/0.6; replace_ms includes the all-reduce and "
+                        "the promotions' H2D copies (max over ranks)"}
     if ctx.rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -956,15 +1145,14 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="c2", choices=["c2", "tiny"], help="headline workload (c3, c4: legs)")
     ap.add_argument("--epoch-every", type=int, default=8)
     ap.add_argument("--batch", type=int, default=0, help="override the workload's batch (profiling runs)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--no-tiered", action="store_true", help="skip the host-tier leg")
+    ap.add_argument("--legs", default="all",
+                    help="measurement legs after the headline (c2 only): all | none | comma list of " + ",".join(LEGS))
     ap.add_argument("--no-per-scheme", action="store_true", help="skip the per-scheme decode table")
-    ap.add_argument("--tiered-pageable", action="store_true",
-                    help="host-tier leg with a pageable backing (bounce through pinned memory)")
     ap.add_argument("--ablation", action="store_true", help="run the paper's ablation arms (P:476-485) instead")
     ap.add_argument("--disk-leg", action="store_true", help="run the DISK-tier leg (save, reload disk-backed) instead")
     ap.add_argument("--tau-sweep", action="store_true", help="run the threshold sweeps of P:401-418 instead")

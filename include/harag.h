@@ -88,12 +88,15 @@ typedef struct {
   uint32_t bench_alias_R;  /* 0 = off; >0: docs d and d' with d % R == d' % R and equal scheme share one host backing blob (bench only) */
   int32_t  device;         /* CUDA device ordinal */
   int32_t  rank, world;    /* this store owns KV heads [rank*H/world, (rank+1)*H/world) */
-  uint32_t staging_slots;  /* host-tier staging ring slots in HBM (0 -> 3) */
+  uint32_t staging_slots;  /* host-tier staging ring slots in HBM, one item each (0 -> ~2 GiB worth, 3..64) */
   int32_t  disk_backing;   /* stores built with hr_build_from_file only: 1 = items outside the HBM arena and the
                               pinned tier stay in the file and are read on every miss (the paper's DISK tier,
                               P:237; O_DIRECT when available); 0 = the file is loaded into host memory */
   uint64_t page_budget;    /* disk_backing only: bytes of pageable cache for PAGE_LIST items (queuePAGE);
                               items past GPU_LIST + PIN_LIST + PAGE_LIST are DISK_LIST (read on every miss) */
+  int32_t  numa_bind;      /* 1 (default): host tiers (pinned tier, backing, bounce buffers) are allocated and
+                              first touched by a thread running on the CPUs NVML reports local to `device`, and
+                              the bounce / disk workers run there (hr_store_local_cpus); 0: no binding */
 } hr_store_config;
 
 typedef struct {
@@ -115,6 +118,7 @@ typedef struct {
   uint64_t h2d_items;         /* host-tier items streamed */
   uint64_t bytes_migrated;    /* host -> device bytes of hr_replace promotions (not in bytes_h2d) */
   uint64_t hits_disk;         /* item accesses served from the store file (HR_T_DISK) */
+  double   host_ms;           /* host time inside hr_assemble_kv (entry -> last launch enqueued), summed */
 } hr_stats;
 
 typedef struct hr_store hr_store;
@@ -247,6 +251,14 @@ hr_status hr_item_rank(const hr_store* s, uint32_t item, uint32_t* rank);   /* p
  * after every hr_assemble_kv.  HR_ENOTFOUND for an unknown item, HR_ESTATE before build. */
 enum { HR_R_HBM = 1, HR_R_PIN = 2, HR_R_PAGE = 4, HR_R_BACKING = 8, HR_R_FILE = 16 };
 hr_status hr_item_residency(const hr_store* s, uint32_t item, uint32_t* mask);
+/* CPUs the store binds its host-tier allocations and workers to (numa_bind): *n of them written to
+ * cpus[0..cap); *n = 0 when nothing is bound (no NVML, numa_bind = 0, or every allowed CPU is local). */
+hr_status hr_store_local_cpus(const hr_store* s, int32_t* cpus, uint32_t cap, uint32_t* n);
+/* Digest of the placement state every rank must agree on after an epoch (SURVEY §8(e) consistency
+ * check): FNV-1a over, per item in id order, its hotness h, scheme and target tier (eager) / queue
+ * (demand mode), and over the hotness rank order.  Ranks of one job compare it with a MIN/MAX
+ * all-reduce; a mismatch means their hotness vectors or policies diverged. */
+hr_status hr_placement_hash(const hr_store* s, uint64_t* hash);
 hr_status hr_export_item(const hr_store* s, uint32_t item, void* host_dst, size_t cap, size_t* len); /* packed blob; synchronous */
 hr_status hr_store_stats(const hr_store* s, hr_stats* out);                 /* synchronises pending timing events */
 hr_status hr_set_timing(hr_store* s, int enable);  /* bit 0: time every assemble launch with CUDA events (stats.kernel_ms);

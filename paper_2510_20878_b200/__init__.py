@@ -54,8 +54,8 @@ def _p(a, ct):
 def make_config(*, L, H, D, T, dtype="bf16", group=0, gse=(4, 3),
                 ladder=("INT8", "FP8E4M3", "FP8E5M2", "GSE8"), taus=(0.1, 0.1, 0.1),
                 hbm_budget=0, pin_budget=0, backing_pinned=False, keep_backing=True, decay_shift=1,
-                alias_R=0, device=0, rank=0, world=1, staging_slots=3, demand_mode=False,
-                disk_backing=False, page_budget=0) -> _lib.Config:
+                alias_R=0, device=0, rank=0, world=1, staging_slots=0, demand_mode=False,
+                disk_backing=False, page_budget=0, numa_bind=True) -> _lib.Config:
     c = _lib.default_config()
     c.L, c.H, c.D, c.T = L, H, D, T
     c.dtype = HR_FP16 if dtype == "fp16" else HR_BF16
@@ -77,6 +77,7 @@ def make_config(*, L, H, D, T, dtype="bf16", group=0, gse=(4, 3),
     c.demand_mode = int(bool(demand_mode))
     c.disk_backing = int(bool(disk_backing))
     c.page_budget = int(page_budget)
+    c.numa_bind = int(bool(numa_bind))
     return c
 
 
@@ -199,6 +200,19 @@ class Store:
         check(lib.hr_item_residency(self._h, item, C.byref(m)))
         return m.value
 
+    def local_cpus(self) -> list[int]:
+        """CPUs the host tiers and bounce workers are bound to (hr_store_local_cpus; [] = unbound)."""
+        buf = (C.c_int32 * 4096)()
+        n = C.c_uint32()
+        check(lib.hr_store_local_cpus(self._h, buf, 4096, C.byref(n)))
+        return [buf[i] for i in range(n.value)]
+
+    def placement_hash(self) -> int:
+        """hr_placement_hash: digest of hotness, schemes and placement (compare across ranks)."""
+        v = C.c_uint64()
+        check(lib.hr_placement_hash(self._h, C.byref(v)))
+        return v.value
+
     def export_item(self, item: int) -> np.ndarray:
         _, _, nbytes = self.item_info(item)
         buf = np.zeros(nbytes, dtype=np.uint8)
@@ -228,7 +242,7 @@ class Store:
                 "migrations_out": s.migrations_out, "failed_promotions": s.failed_promotions,
                 "kernel_ms": s.kernel_ms, "timed_launches": s.timed_launches, "hbm_used": s.hbm_used,
                 "pin_used": s.pin_used, "h2d_ms": s.h2d_ms, "h2d_items": s.h2d_items,
-                "bytes_migrated": s.bytes_migrated, "hits_disk": s.hits_disk}
+                "bytes_migrated": s.bytes_migrated, "hits_disk": s.hits_disk, "host_ms": s.host_ms}
 
     def close(self) -> None:
         if self._h:

@@ -31,7 +31,7 @@ class Config(C.Structure):
         ("backing_pinned", C.c_int32), ("keep_backing", C.c_int32), ("demand_mode", C.c_int32),
         ("decay_shift", C.c_uint32), ("bench_alias_R", C.c_uint32),
         ("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("staging_slots", C.c_uint32),
-        ("disk_backing", C.c_int32), ("page_budget", C.c_uint64),
+        ("disk_backing", C.c_int32), ("page_budget", C.c_uint64), ("numa_bind", C.c_int32),
     ]
 
 
@@ -42,7 +42,7 @@ class Stats(C.Structure):
         ("migrations_in", C.c_uint64), ("migrations_out", C.c_uint64), ("failed_promotions", C.c_uint64),
         ("kernel_ms", C.c_double), ("timed_launches", C.c_uint64), ("hbm_used", C.c_uint64),
         ("pin_used", C.c_uint64), ("h2d_ms", C.c_double), ("h2d_items", C.c_uint64),
-        ("bytes_migrated", C.c_uint64), ("hits_disk", C.c_uint64),
+        ("bytes_migrated", C.c_uint64), ("hits_disk", C.c_uint64), ("host_ms", C.c_double),
     ]
 
 
@@ -78,6 +78,8 @@ _SIGS = {
     "hr_item_info": (I32, [P, U32, PU32, PU32, PU64]),
     "hr_item_rank": (I32, [P, U32, PU32]),
     "hr_item_residency": (I32, [P, U32, PU32]),
+    "hr_store_local_cpus": (I32, [P, C.POINTER(C.c_int32), U32, PU32]),
+    "hr_placement_hash": (I32, [P, PU64]),
     "hr_export_item": (I32, [P, U32, P, SZ, C.POINTER(SZ)]),
     "hr_store_stats": (I32, [P, C.POINTER(Stats)]),
     "hr_set_timing": (I32, [P, I32]),

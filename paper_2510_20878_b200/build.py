@@ -59,7 +59,7 @@ def _lib(target: str, sources: list[str], headers: list[str], objdir: str, extra
     with cf.ThreadPoolExecutor(max_workers=min(8, len(jobs))) as ex:
         list(ex.map(_run, jobs))
     tmp = target + ".tmp"
-    _run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lpthread"])
+    _run([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lpthread", "-ldl"])
     os.replace(tmp, target)
     return True
 

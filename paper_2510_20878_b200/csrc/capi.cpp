@@ -64,7 +64,8 @@ void hr_config_default(hr_store_config* c) {
   c->keep_backing = 1;
   c->decay_shift = 1;
   c->world = 1;
-  c->staging_slots = 3;
+  c->staging_slots = 0;
+  c->numa_bind = 1;
 }
 
 hr_status hr_store_create(const hr_store_config* cfg, hr_store** out) {
@@ -185,6 +186,23 @@ hr_status hr_item_residency(const hr_store* s, uint32_t item, uint32_t* mask) {
     *mask = (l.hbm_off != none ? HR_R_HBM : 0) | (l.pin_off != none ? HR_R_PIN : 0) |
             (l.page_off != none ? HR_R_PAGE : 0) | (l.backing_off != none ? HR_R_BACKING : 0) |
             (st.disk_fd >= 0 && !st.disk_off.empty() ? HR_R_FILE : 0);
+  });
+}
+hr_status hr_store_local_cpus(const hr_store* s, int32_t* cpus, uint32_t cap, uint32_t* n) {
+  return guard([&] {
+    NONNULL(s);
+    NONNULL(n);
+    const auto& c = s->impl.local_cpus;
+    *n = (uint32_t)c.size();
+    harag::require(!cpus || c.size() <= cap, HR_EINVAL, "cpus buffer too small");
+    for (size_t i = 0; cpus && i < c.size(); ++i) cpus[i] = c[i];
+  });
+}
+hr_status hr_placement_hash(const hr_store* s, uint64_t* hash) {
+  return guard([&] {
+    NONNULL(s);
+    NONNULL(hash);
+    *hash = s->impl.placement_hash();
   });
 }
 hr_status hr_item_rank(const hr_store* s, uint32_t item, uint32_t* rank) {

@@ -12,8 +12,9 @@
 //   PASS16 bytes unchanged (TMA bulk copy both ways)
 // then one round-to-nearest-even to the output dtype (R25).
 //
-// Structure (warp-specialised, persistent): CTA = 1 producer warp + 8
-// consumer warps; CTA b owns a contiguous block of tiles.  A tile = p.tile_e
+// Structure (warp-specialised, persistent): CTA = 1 producer warp + 28
+// consumer warps (HARAG_CONSUMER_WARPS, kernels.h; one CTA per SM); CTA b owns
+// a contiguous block of tiles.  A tile = p.tile_e
 // consecutive elements of one (request, slot, kind, layer, head) slab.  The
 // producer lane resolves the tile (descriptor, addresses, hotness count),
 // writes a small header to shared memory and has the TMA engine bulk-copy
@@ -114,6 +115,9 @@ struct TileHdr {
   uint32_t goff;     // e0 mod G: group of element e is (goff + e) >> g_shift
 };
 
+// Descriptors: launches of <= kAsmInline (64) descriptors (a single request, a streamed item) carry
+// them in the kernel parameters (p.descs == nullptr), larger ones read a device array.
+//
 // Dynamic shared memory: [codes ring | meta ring | headers | full barriers | empty barriers];
 // every meta stage starts 256-B aligned
 struct Smem {
@@ -197,7 +201,7 @@ __device__ __forceinline__ void produce(const AsmParams& p, const Smem& sm) {
 }
 
 // ------------------------------------------------------------------ consumers
-// Consumer thread ctid handles the 8-element chunks ctid, ctid + 256, ... of a tile.
+// Consumer thread ctid handles the 8-element chunks ctid, ctid + 32*kConsumerWarps, ... of a tile.
 constexpr uint32_t kChunkStride = kConsumerWarps * 32 * 8;
 
 template <int DT>

@@ -11,20 +11,24 @@
 // P:316); LSE lets a caller merge it with the question's own causal part.
 //
 // sm_100a design: one CTA per (request, layer, KV head) unit,
-// warp-specialised — 4 softmax warps, 3 groups of 8 decoder warps and one MMA
-// issuer lane.  The unit's M = g*n_q <= 128 query rows are the A operand of
-// tcgen05.mma (M = 128, rows past M zero); per 64-key tile the decoders stage
-// the packed codes with cp.async (L2-prefetched ahead) and decode them, bit
-// for bit as hr_assemble_kv, into one of four K/V operand buffers; S = Q K^T
-// accumulates in one of two TMEM buffers; the softmax warps (thread = row)
-// run the online softmax with a lazy O rescale and write P (16-bit) back into
-// the S buffer's TMEM columns.  Both MMAs take A from TMEM (Q loaded once per
-// unit, P per tile), so shared memory feeds only the B operands: K as a
-// 128-byte-swizzled K-major tile, V the canonical no-swizzle MN-major layout
-// (8 rows x 16 B per core matrix).  Debug builds:
-// -DHARAG_ATT_TRACE (per-tile clock64 events of CTA 0), -DHARAG_ATT_WATCHDOG
-// (mbarrier waits that report and trap), -DHARAG_ATT_MMASYNC (MMA latency in
-// isolation).
+// warp-specialised — 4 softmax warps (thread = query row = TMEM lane), 3 groups
+// of 4 decoder warps (tiles round-robin), one MMA-issuer warp and one producer
+// warp.  The unit's M = g*n_q <= 128 query rows are the A operand of
+// tcgen05.mma (M = 128, rows past M zero), loaded into TMEM once.  Per 64-key
+// tile the producer lane bulk-copies (TMA, cp.async.bulk) the tile's contiguous
+// K and V code runs into a 4-slot stage ring (mbarrier complete_tx); a decoder
+// group decodes them, bit for bit as hr_assemble_kv, into one of four K/V
+// operand buffers — K a 128-byte-swizzled K-major tile, V a 128-byte-swizzled
+// MN-major tile (the same physical layout), both written row-wise from the
+// contiguous stage slot, so stage reads and operand writes are conflict-free.
+// S = Q K^T accumulates in one of two TMEM buffers; the softmax warps run a
+// one-pass online softmax at a running reference max (rescale of O only when a
+// row max grows past a threshold) and write P (16-bit) back into the S
+// buffer's TMEM columns; O += P V takes A = P from TMEM, and the row sum of the
+// rounded P is accumulated by the tensor core (an N = 16 MMA against a ones
+// tile).  Debug builds: -DHARAG_ATT_TRACE (per-tile clock64 events of CTA 0),
+// -DHARAG_ATT_WATCHDOG (mbarrier waits that report and trap),
+// -DHARAG_ATT_MMASYNC (MMA latency in isolation).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_fp8.h>

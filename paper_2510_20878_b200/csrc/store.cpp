@@ -12,7 +12,9 @@
 #include <unistd.h>
 
 #include <atomic>
+#include <chrono>
 #include <cerrno>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -68,13 +70,20 @@ Store::Store(const hr_store_config& c) : cfg(c), lay(make_layout(c)) {
   require(sum <= 1.0 + 1e-12, HR_EINVAL, "taus sum above 1");
   require(cfg.demand_mode == 0 || cfg.demand_mode == 1, HR_EINVAL, "demand_mode must be 0 or 1");
   if (cfg.demand_mode) cfg.keep_backing = 1;  // the backing plays the paper's disk: every item has a copy
-  slots = cfg.staging_slots ? cfg.staging_slots : 3;
+  slots = cfg.staging_slots;  // 0: sized in ensure_ring once the largest item is known
   if (const char* g = std::getenv("HARAG_ASM_GRID")) grid_override = std::atoi(g);  // tuning experiments
   HR_CUDA(cudaSetDevice(cfg.device));
   HR_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
+  if (cfg.numa_bind) local_cpus = gpu_local_cpus(cfg.device);
+  host_prof = std::getenv("HARAG_HOST_PROF") != nullptr;
 }
 
 Store::~Store() {
+  if (host_prof && prof_calls)
+    std::fprintf(stderr, "[harag host prof] %llu calls, us/call: entry+validate %.2f desc_buffer %.2f pass1 %.2f "
+                 "pass2-3 %.2f launchA %.2f tail %.2f\n", (unsigned long long)prof_calls,
+                 1e3 * prof_ms[0] / prof_calls, 1e3 * prof_ms[1] / prof_calls, 1e3 * prof_ms[2] / prof_calls,
+                 1e3 * prof_ms[3] / prof_calls, 1e3 * prof_ms[4] / prof_calls, 1e3 * prof_ms[5] / prof_calls);
   cudaSetDevice(cfg.device);
   cudaDeviceSynchronize();
   for (auto& d : dbuf) {
@@ -151,6 +160,7 @@ std::vector<uint32_t> Store::place_lists() const {
 
 void Store::setup(uint32_t nd, const uint64_t* hot, std::vector<uint32_t> sc, bool disk) {
   require(!disk || cfg.page_budget <= (1ull << 46), HR_EINVAL, "page_budget must be a finite byte count");
+  const CpuBind bind(local_cpus);  // host tiers are allocated (and pinned pages touched) on the GPU's node
   on_disk = disk;
   HR_CUDA(cudaSetDevice(cfg.device));
   n_docs = nd;
@@ -272,6 +282,7 @@ void Store::build_put(uint32_t doc, const void* k_src, const void* v_src, cudaSt
 void Store::build_put_batch(uint32_t n, const uint32_t* docs, const void* const* k_srcs, const void* const* v_srcs,
                             cudaStream_t st) {
   require(state == State::Building, HR_ESTATE, "hr_build_put outside begin/end");
+  const CpuBind bind(local_cpus);  // the D2H fills first-touch the pageable backing pages
   require(n <= kPutBatch, HR_EINVAL, "hr_build_put_batch: at most 16 docs per call");
   require(n == 0 || (docs && k_srcs && v_srcs), HR_EINVAL, "NULL array");
   for (uint32_t i = 0; i < n; ++i) {
@@ -418,6 +429,10 @@ Store::DescBuf& Store::desc_buffer(size_t n) {
 
 void Store::ensure_ring() {
   if (!ring.empty()) return;
+  // Default depth: ~2 GiB of slots (3..64).  Launch B of a streamed item runs on the request stream
+  // behind launch A, so a slot is recycled only after launch A; the ring must hold what the link
+  // delivers meanwhile (Llama-3-8B batch 32: launch A ~5 ms = ~280 MB at 55 GB/s) or the copies stall.
+  if (!slots) slots = (uint32_t)std::min<uint64_t>(64, std::max<uint64_t>(3, ((2ull << 30) + max_item - 1) / max_item));
   ring.resize(slots);
   for (auto& r : ring) {
     HR_CUDA(cudaMalloc(&r.dev, max_item));
@@ -492,6 +507,14 @@ void Store::release_deferred() {
 
 void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* const* k_out, void* const* v_out,
                      cudaStream_t st) {
+  const auto host_t0 = std::chrono::steady_clock::now();
+  auto tick = [&](int i) {
+    if (!host_prof) return;
+    const auto now = std::chrono::steady_clock::now();
+    prof_ms[i] += std::chrono::duration<double, std::milli>(now - prof_t).count();
+    prof_t = now;
+  };
+  if (host_prof) prof_t = host_t0;
   validate_request(n_req, k, ids, k_out, v_out);  // before any device work: no partial writes
   HR_CUDA(cudaSetDevice(cfg.device));
   if (call_timing) {  // per-call latency: this event -> the end of the call's last launch (device clock)
@@ -501,6 +524,7 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
     }
     HR_CUDA(cudaEventRecord(call_ev[0], st));
   }
+  tick(0);
   if (!promos.empty()) poll_promotions(false);
   const bool demand = alg2 != nullptr;
   if (demand) {
@@ -510,7 +534,8 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
     HR_CUDA(cudaStreamWaitEvent(copy_stream, start_ev, 0));
   }
   const size_t n_desc = 2ull * n_req * k;
-  DescBuf& db = desc_buffer(n_desc);
+  if (hdesc.size() < n_desc) hdesc.resize(n_desc);  // host descriptors (pageable scratch)
+  tick(1);
   // a6 planning, in three passes.
   //  1. Every access in request order: Alg. 2 step 2 (demand mode: one branch per access, the hit
   //     counted where Alg. 2 finds the item, host-queue fills done at once) or the tier lookup (eager).
@@ -574,6 +599,7 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
     }
   }
   // pass 2 (demand mode): HBM arena := queueGPU
+  tick(2);
   std::unordered_map<uint32_t, uint64_t> start_off;  // items resident at the call's start whose block was freed
   std::unordered_map<uint32_t, bool> promoted;       // item -> its arena block reuses space freed in this call
   if (demand) {
@@ -640,7 +666,7 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
         if (pr == promoted.end() && (loc[item].hbm_off != FreeList::kNone || so != start_off.end())) {
           d.codes = hbm_base + (so != start_off.end() ? so->second : loc[item].hbm_off);
           d.meta = d.codes + lay.meta_offset(d.scheme);
-          db.host[nh++] = d;
+          hdesc[nh++] = d;
           hbm_mask |= 1u << d.scheme;
           continue;
         }
@@ -671,15 +697,26 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
     for (AsmDesc d : s.descs) {
       d.codes = dest[i];
       d.meta = dest[i] + lay.meta_offset(d.scheme);
-      db.host[pos++] = d;
+      hdesc[pos++] = d;
     }
     range[i] = {b, pos - b};
   }
+  tick(3);
   bool need_dev = nh > (size_t)kAsmInline;
   for (const auto& rg : range) need_dev |= rg.second > (size_t)kAsmInline;
-  if (need_dev) HR_CUDA(cudaMemcpyAsync(db.dev, db.host, pos * sizeof(AsmDesc), cudaMemcpyHostToDevice, st));
+  // launches of <= kAsmInline descriptors carry them as kernel parameters; only larger ones need the
+  // device array (a pinned staging buffer, recycled once the call's launches are done)
+  DescBuf* db = nullptr;
+  const AsmDesc* ddesc = nullptr;
+  if (need_dev) {
+    db = &desc_buffer(pos);
+    std::memcpy(db->host, hdesc.data(), pos * sizeof(AsmDesc));
+    HR_CUDA(cudaMemcpyAsync(db->dev, db->host, pos * sizeof(AsmDesc), cudaMemcpyHostToDevice, st));
+    ddesc = db->dev;
+  }
   // launch A: every resident (request, slot, kind)
-  if (nh) launch(db.dev, db.host, (uint32_t)nh, k, hbm_mask, st);
+  if (nh) launch(ddesc, hdesc.data(), (uint32_t)nh, k, hbm_mask, st);
+  tick(4);
   if (any_after_a && nh) {
     if (!after_a_ev) HR_CUDA(cudaEventCreateWithFlags(&after_a_ev, cudaEventDisableTiming));
     HR_CUDA(cudaEventRecord(after_a_ev, st));
@@ -717,11 +754,11 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
       read_disk(item, sl.bounce);
       HR_CUDA(cudaMemcpyAsync(dest[i], sl.bounce, bytes[item], cudaMemcpyHostToDevice, copy_stream));
     } else if (bounce) {
-      // pageable data is first copied to pinned memory.  The bounce runs in 4 MiB pieces so
-      // the host copy of piece p+1 overlaps the DMA of piece p.
+      // pageable data is first copied to pinned memory.  The bounce runs in 8 MiB pieces so
+      // the host copy of piece p+1 overlaps the DMA of piece p (and item i+1's copy item i's DMA).
       if (!sl.bounce) HR_CUDA(cudaHostAlloc((void**)&sl.bounce, align_up(max_item, 4096), cudaHostAllocPortable));
       if (sl.used) HR_CUDA(cudaEventSynchronize(sl.copied));  // previous DMA out of this bounce buffer done
-      constexpr size_t kPiece = 4u << 20;
+      constexpr size_t kPiece = 8u << 20;
       for (size_t off = 0; off < bytes[item]; off += kPiece) {
         const size_t n = std::min<size_t>(kPiece, bytes[item] - off);
         host_copy(sl.bounce + off, src + off, n);
@@ -739,14 +776,18 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
     sl.used = true;
     stats.bytes_h2d += bytes[item];
     HR_CUDA(cudaStreamWaitEvent(st, sl.copied, 0));
-    launch(db.dev + range[i].first, db.host + range[i].first, (uint32_t)range[i].second, k, 1u << scheme[item], st);
+    launch(ddesc ? ddesc + range[i].first : nullptr, hdesc.data() + range[i].first, (uint32_t)range[i].second, k,
+           1u << scheme[item], st);
     if (!to_arena) HR_CUDA(cudaEventRecord(sl.free_ev, st));
   }
-  HR_CUDA(cudaEventRecord(db.done, st));
+  if (db) HR_CUDA(cudaEventRecord(db->done, st));
   if (call_timing) {
     HR_CUDA(cudaEventRecord(call_ev[1], st));
     call_recorded = true;
   }
+  tick(5);
+  prof_calls++;
+  stats.host_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0).count();
   req_counter += n_req;
   stats.requests += n_req;
 }
@@ -776,9 +817,13 @@ void Store::fill_host(uint32_t item, uint8_t* dst) {
 
 void Store::host_copy(void* dst, const void* src, size_t n) {
   if (!copy_pool) {
-    unsigned t = std::thread::hardware_concurrency() / 2;
+    // every host core but the calling thread's (measured: one thread copies pageable -> pinned at
+    // ~8.6 GB/s on the B200 host, 16 threads at ~88 GB/s, tools/hostcopy.cpp)
+    unsigned t = std::max(1u, std::thread::hardware_concurrency()) - 1;
     if (const char* e = std::getenv("HARAG_COPY_THREADS")) t = (unsigned)std::atoi(e);
-    copy_pool.reset(new CopyPool(std::min(t, 15u)));
+    const int spin = std::getenv("HARAG_POOL_SPIN") ? std::atoi(std::getenv("HARAG_POOL_SPIN")) : 2000;
+    copy_pool.reset(new CopyPool(std::min(t, 31u), spin));
+    copy_pool->set_affinity(local_cpus);
   }
   if (n) copy_pool->copy(dst, src, n);
 }
@@ -896,6 +941,7 @@ void Store::attend(uint32_t n_req, uint32_t k, const uint32_t* ids, const void* 
 
 void Store::replace(cudaStream_t st) {
   require(state == State::Built, HR_ESTATE, "hr_replace before the store is built");
+  const CpuBind bind(local_cpus);  // pinned-tier fills
   HR_CUDA(cudaSetDevice(cfg.device));
   std::vector<int64_t> dh(n_items);
   HR_CUDA(cudaMemcpyAsync(dh.data(), delta, sizeof(int64_t) * n_items, cudaMemcpyDeviceToHost, st));
@@ -1126,6 +1172,7 @@ void Store::save(const char* path) const {
 
 void Store::build_from_file(const char* path, cudaStream_t st) {
   require(state == State::Empty, HR_ESTATE, "store already built");
+  const CpuBind bind(local_cpus);
   const std::string P(path);
   const int fd = ::open(path, O_RDONLY);
   require(fd >= 0, HR_EINVAL, errno_msg("open", P));
@@ -1225,6 +1272,22 @@ void Store::export_item(uint32_t item, void* dst, size_t cap, size_t* len) const
     require(disk_fd >= 0 && !disk_off.empty(), HR_ESTATE, "item has no copy");
     pread_all(disk_fd, dst, bytes[item], disk_off[item], disk_path);
   }
+}
+
+uint64_t Store::placement_hash() const {
+  require(state == State::Built, HR_ESTATE, "store not built");
+  uint64_t x = 0xcbf29ce484222325ull;  // FNV-1a, 64-bit
+  auto mix = [&x](uint64_t v) {
+    for (int b = 0; b < 8; ++b) x = (x ^ ((v >> (8 * b)) & 0xFF)) * 0x100000001b3ull;
+  };
+  mix(n_items);
+  for (uint32_t i = 0; i < n_items; ++i) {
+    mix(h[i]);
+    mix(scheme[i]);
+    mix(logical_tier(i));
+  }
+  for (uint32_t i = 0; i < n_items; ++i) mix(order[i]);
+  return x;
 }
 
 void Store::get_stats(hr_stats* out) {

@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <chrono>
 #include <cstdint>
 #include <map>
 #include <unordered_set>
@@ -12,6 +13,7 @@
 #include "common.h"
 #include "kernels.h"
 #include "layout.h"
+#include "numa.h"
 #include "pool.h"
 #include "policy.h"
 
@@ -107,8 +109,11 @@ struct Store {
   uint32_t logical_tier(uint32_t item) const;
   void compact_pin();
 
+  uint64_t placement_hash() const;
+
   hr_store_config cfg;
   Layout lay;
+  std::vector<int> local_cpus;  // numa_bind: CPUs local to the device (empty: unbound)
   State state = State::Empty;
   uint32_t n_docs = 0, n_items = 0, n_put = 0;
   uint32_t slots = 3;
@@ -148,6 +153,7 @@ struct Store {
   void* src_v = nullptr;
   cudaStream_t copy_stream = nullptr;
   std::vector<DescBuf> dbuf;
+  std::vector<AsmDesc> hdesc;  // host copy of an assemble call's descriptors
   int dbuf_next = 0;
   std::vector<Slot> ring;
   uint64_t req_counter = 0;
@@ -157,6 +163,11 @@ struct Store {
   bool call_recorded = false;
   cudaEvent_t call_ev[2] = {nullptr, nullptr};
   double last_call_ms();
+  // HARAG_HOST_PROF=1: host-time breakdown of hr_assemble_kv, printed when the store is destroyed
+  bool host_prof = false;
+  double prof_ms[6] = {0, 0, 0, 0, 0, 0};
+  uint64_t prof_calls = 0;
+  std::chrono::steady_clock::time_point prof_t;
   int grid_override = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timers;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> h2d_timers;  // copy-stream window per assemble call

@@ -156,7 +156,7 @@ def test_bench_store_full_request_and_batch32(torch_cuda):
     torch = torch_cuda
     n_docs, k, B = 2000, 10, 32
     lay = ost.Layout(L=L, H=H, T=T, D=D)
-    prof = synth.gen_requests(n_docs, 4 * n_docs, k, 1.1, seed=7)       # bench.build_store's profile
+    prof = synth.gen_requests(n_docs, 4 * n_docs, k, 1.1, seed=7, perm_seed=1)   # bench.build_store's profile
     h = hotness.count_requests(prof, n_docs).astype(np.uint64)
     taus = (0.1, 0.1, 0.1)
     schemes = hotness.assign_schemes(h.tolist(), [NAMES[s] for s in PAPER], taus)
