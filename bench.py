@@ -512,6 +512,8 @@ LEGS = {
     "c4_llama3_70b_tiered": dict(base="c4", tier="pinned", hbm_budget=80 * 10 ** 9, alias_R=100, steps=5,
                                  desc="BASELINE config 3: Llama-3-70B KV shape, 10,000 docs, hot set in an HBM arena "
                                       "of up to 80 GB, cold in pinned host DRAM, Zipf(1.1), top-k 10, batch 32"),
+    # the consumer: TTFT-like prefill over the retrieved chunks, fused vs unfused
+    "c2_ttft": dict(kind="ttft"),
 }
 
 
@@ -528,12 +530,179 @@ def kernel_roofline(stats, peak, peak_src, traffic=None):
             "launches": int(stats["kernel_launches"]), "peak_source": peak_src}
 
 
+class RandomLlama:
+    """Llama-3-8B-shaped decoder with RANDOM weights (bf16, N(0, 0.02^2)), for a TTFT-like number of
+    the consumer (the paper's metric is TTFT): the question tokens of each
+    request are prefilled through every layer, attending to the request's retrieved chunk KV
+    (TurboRAG: precomputed chunk KV) and causally to themselves, then the LM head gives
+    the first token.  Only the shapes matter here (no checkpoint exists offline); the GEMMs are torch
+    (cuBLAS), the chunk attention is either
+      fused:   hr_attend_layers (packed codes decoded inside the tcgen05 kernel, one launch per layer)
+               + the question's own causal block, merged by log-sum-exp, or
+      unfused: hr_assemble_kv once (bf16 KV of every layer materialised) + torch SDPA per layer over
+               [chunk KV ; own KV] with the causal mask on the own block."""
+
+    def __init__(self, torch, L, Hq, Hkv, D, hidden=4096, inter=14336, vocab=128256, seed=0):
+        self.torch, self.L, self.Hq, self.Hkv, self.D = torch, L, Hq, Hkv, D
+        g = torch.Generator(device="cuda").manual_seed(seed)
+
+        def w(*shape):
+            return (torch.randn(*shape, generator=g, device="cuda", dtype=torch.float32) * 0.02).to(torch.bfloat16)
+        self.wqkv = [w(hidden, (Hq + 2 * Hkv) * D) for _ in range(L)]
+        self.wo = [w(Hq * D, hidden) for _ in range(L)]
+        self.wgu = [w(hidden, 2 * inter) for _ in range(L)]
+        self.wd = [w(inter, hidden) for _ in range(L)]
+        self.lm = w(hidden, vocab)
+        self.emb = w(vocab, hidden)
+        self.hidden, self.inter = hidden, inter
+
+    def rms(self, x):
+        t = self.torch
+        return (x.float() * t.rsqrt(x.float().pow(2).mean(-1, keepdim=True) + 1e-5)).to(t.bfloat16)
+
+    def rope(self, x, pos0):
+        """Rotary embedding of the question tokens at positions pos0 .. pos0 + n - 1 (x [B][H][n][D])."""
+        t = self.torch
+        n, D = x.shape[2], x.shape[3]
+        inv = 500000.0 ** (-t.arange(0, D, 2, device="cuda", dtype=t.float32) / D)
+        ang = t.arange(pos0, pos0 + n, device="cuda", dtype=t.float32)[:, None] * inv[None, :]
+        c, s = ang.cos(), ang.sin()
+        x1, x2 = x[..., 0::2].float(), x[..., 1::2].float()
+        out = t.empty_like(x)
+        out[..., 0::2] = (x1 * c - x2 * s).to(x.dtype)
+        out[..., 1::2] = (x1 * s + x2 * c).to(x.dtype)
+        return out
+
+    def own_attention(self, q, k, v):
+        """Causal attention of the question block on itself: O [B][Hq][n][D] and LSE [B][Hq][n] (fp32)."""
+        t = self.torch
+        B, Hq, n, D = q.shape
+        g = Hq // k.shape[1]
+        kk = k.repeat_interleave(g, dim=1).float()
+        vv = v.repeat_interleave(g, dim=1).float()
+        s = (q.float() @ kk.transpose(-1, -2)) / D ** 0.5
+        s = s.masked_fill(t.ones(n, n, device="cuda", dtype=t.bool).triu(1), float("-inf"))
+        lse = t.logsumexp(s, dim=-1)
+        return (t.softmax(s, dim=-1) @ vv), lse
+
+    def prefill(self, tokens, attend_chunks, pos0):
+        """tokens [B][n] -> first token ids [B].  attend_chunks(l, q, k_own, v_own) -> O [B][Hq][n][D]."""
+        t = self.torch
+        B, n = tokens.shape
+        x = self.emb[tokens]                                     # [B][n][hidden]
+        Hq, Hkv, D = self.Hq, self.Hkv, self.D
+        for l in range(self.L):
+            h = self.rms(x)
+            qkv = (h.reshape(B * n, -1) @ self.wqkv[l]).reshape(B, n, Hq + 2 * Hkv, D).transpose(1, 2)
+            q = self.rope(qkv[:, :Hq], pos0)
+            k = self.rope(qkv[:, Hq:Hq + Hkv], pos0)
+            v = qkv[:, Hq + Hkv:]
+            o = attend_chunks(l, q.contiguous(), k.contiguous(), v.contiguous())   # [B][Hq][n][D] bf16
+            x = x + (o.transpose(1, 2).reshape(B * n, Hq * D) @ self.wo[l]).reshape(B, n, -1)
+            h = self.rms(x).reshape(B * n, -1)
+            gu = h @ self.wgu[l]
+            a = t.nn.functional.silu(gu[:, :self.inter].float()) * gu[:, self.inter:].float()
+            x = x + (a.to(t.bfloat16) @ self.wd[l]).reshape(B, n, -1)
+        logits = self.rms(x[:, -1]) @ self.lm
+        return logits.argmax(-1)
+
+
+def run_ttft(ctx, args, n_docs=2000, B=8, n_q=32, reps=5):
+    """TTFT-like number: retrieved chunk KV from the HBM-resident C2 store, question
+    prefill through 32 random-weight Llama-3-8B layers, first token.  Fused (hr_attend_layers) vs
+    unfused (hr_assemble_kv + SDPA); CUDA-event time per batch."""
+    import synth
+    torch = ctx.torch
+    wl = dict(WORKLOADS["c2"], n_docs=n_docs)
+    L, H, D, T, k = wl["L"], wl["H"], wl["D"], wl["T"], wl["k"]
+    Hl = H // ctx.world
+    g = 4                                                        # Llama-3-8B: 32 query heads over 8 KV heads
+    st, h, schemes, build_s, total = build_store(ctx, wl)
+    model = RandomLlama(torch, L, Hl * g, Hl, D)
+    reqs = synth.gen_requests(n_docs, B, k, wl["s"], seed=3).astype(np.uint32)
+    tokens = torch.randint(0, 128256, (B, n_q), device="cuda", generator=torch.Generator(device="cuda").manual_seed(1))
+    pos0 = k * T
+    kvb = st.kv_bytes(k)
+    ko = [torch.empty(kvb // 2, dtype=torch.bfloat16, device="cuda") for _ in range(B)]
+    vo = [torch.empty(kvb // 2, dtype=torch.bfloat16, device="cuda") for _ in range(B)]
+    o_c = torch.empty((B, 1, Hl * g, n_q, D), dtype=torch.bfloat16, device="cuda")
+    lse_c = torch.empty((B, 1, Hl * g, n_q), dtype=torch.float32, device="cuda")
+    maskf = torch.zeros(n_q, k * T + n_q, device="cuda", dtype=torch.bool)
+    maskf[:, :k * T] = True
+    maskf[:, k * T:] = torch.ones(n_q, n_q, device="cuda", dtype=torch.bool).tril()
+
+    def fused_attn(l, q, k_own, v_own):
+        st.attend(reqs, q, o_c, n_q, g, lse=lse_c, layers=(l, 1))
+        o_s, lse_s = model.own_attention(q, k_own, v_own)
+        lc = lse_c[:, 0]
+        m = torch.maximum(lc, lse_s)
+        wc, ws = torch.exp(lc - m), torch.exp(lse_s - m)
+        o = (o_c[:, 0].float() * wc[..., None] + o_s * ws[..., None]) / (wc + ws)[..., None]
+        return o.to(torch.bfloat16)
+
+    def unfused_attn(l, q, k_own, v_own):
+        out = torch.empty_like(q)
+        for r in range(B):
+            Kc = ko[r].view(L, Hl, k * T, D)[l]
+            Vc = vo[r].view(L, Hl, k * T, D)[l]
+            Kf = torch.cat([Kc, k_own[r]], dim=1)
+            Vf = torch.cat([Vc, v_own[r]], dim=1)
+            out[r] = torch.nn.functional.scaled_dot_product_attention(
+                q[r], Kf, Vf, attn_mask=maskf, enable_gqa=True)
+        return out
+
+    def fused():
+        return model.prefill(tokens, fused_attn, pos0)
+
+    def unfused():
+        st.assemble(reqs, ko, vo)
+        return model.prefill(tokens, unfused_attn, pos0)
+
+    def no_chunks():   # the question alone: the compute floor that no KV loading can remove
+        return model.prefill(tokens, lambda l, q, kk, vv: model.own_attention(q, kk, vv)[0].to(torch.bfloat16), pos0)
+
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+
+    def timed(fn):
+        for _ in range(2):
+            fn()
+        torch.cuda.synchronize()
+        ev[0].record(ctx.stream)
+        for _ in range(reps):
+            out = fn()
+        ev[1].record(ctx.stream)
+        ev[1].synchronize()
+        return ev[0].elapsed_time(ev[1]) / reps, out
+
+    f_ms, f_tok = timed(fused)
+    u_ms, u_tok = timed(unfused)
+    n_ms, _ = timed(no_chunks)
+    agree = float((f_tok == u_tok).float().mean().item())
+    res = {"workload": f"Llama-3-8B-shaped decoder with random bf16 weights (32 layers, 32 query / 8 KV heads, hidden "
+                       f"4096, MLP 14336, vocab 128256), batch {B} requests x {n_q} question tokens, k={k} retrieved "
+                       f"512-token chunks each from the {n_docs}-doc HBM-resident C2 store (paper ladder)",
+           "ttft_ms_fused": round(f_ms, 3), "ttft_ms_unfused": round(u_ms, 3), "prefill_only_ms": round(n_ms, 3),
+           "speedup_fused_vs_unfused": round(u_ms / f_ms, 3),
+           "chunk_attention_ms_fused": round(f_ms - n_ms, 3), "chunk_attention_ms_unfused": round(u_ms - n_ms, 3),
+           "first_token_agreement_fused_vs_unfused": agree,
+           "fused": "hr_attend_layers per layer (packed codes, no KV materialised) + own causal block, LSE merge",
+           "unfused": "hr_assemble_kv (bf16 KV of all layers) + torch SDPA per layer over [chunk ; own] KV",
+           "timing": f"CUDA events over {reps} batches after 2 warm-up batches"}
+    st.close()
+    del model
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return res
+
+
 def run_leg(ctx, name, spec, args):
     """One measurement leg (LEGS): build the store, time `steps` batches (W = 3), report assembled
     GB/s, the assemble kernels' HBM roofline, the host link and overlapped rooflines (tiered legs)
     and single-request latency p50/p99 (mixed tiers in tiered legs)."""
     import synth
     torch = ctx.torch
+    if spec.get("kind") == "ttft":
+        return run_ttft(ctx, args)
     base = WORKLOADS[spec["base"]]
     wl = dict(base, **{k_: v for k_, v in spec.items() if k_ in ("n_docs", "batch", "k", "s")})
     B, k = wl["batch"], wl["k"]

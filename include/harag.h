@@ -215,14 +215,24 @@ hr_status hr_replace(hr_store* s, void* stream);
  *   scale:   softmax scale (<= 0 -> 1/sqrt(D));
  *   kv_dump: NULL (test hook: device [n_req][2][L][Hl][k*T][D], receives the
  *            decoded K and V exactly as hr_assemble_kv would write them).
- * Needs g * n_q <= 128, D in {64, 128}, T a multiple of 64, eager placement and
- * every requested item resident in HBM (HR_ESTATE otherwise, before any launch);
+ * Needs g * n_q <= 128, D in {64, 128}, T a multiple of 64 and eager placement (HR_ESTATE otherwise,
+ * before any launch); host-tier items are staged as in hr_attend_layers;
  * duplicate / unknown ids as hr_assemble_kv.  Stream-ordered; counts hotness
  * like hr_assemble_kv (a1).  Arithmetic: bf16/fp16 tensor-core products, fp32
  * accumulation, probabilities rounded to the dtype before P.V. */
 hr_status hr_attend(hr_store* s, uint32_t n_req, uint32_t k, const uint32_t* doc_ids, const void* q_dev,
                     uint32_t n_q, uint32_t g, void* o_dev, float* lse_dev, float scale, void* kv_dump,
                     void* stream);
+/* hr_attend over the layer window [layer0, layer0 + n_layers) only — one layer at a time is what a
+ * prefill needs, since layer l's queries come out of layer l-1.  q_dev / o_dev / lse_dev / kv_dump are
+ * laid out as for hr_attend with n_layers in place of L.  Items outside the HBM arena are accepted:
+ * the window's code and meta slabs are copied from the pinned tier / host backing (pageable through a
+ * pinned bounce; the DISK tier through a read of the blob) into staging-ring slots, and the
+ * launch waits for them; a call's host-tier items must fit the ring at once (HR_ESTATE otherwise,
+ * before any work).  hr_attend == hr_attend_layers(s, ..., 0, L, ...). */
+hr_status hr_attend_layers(hr_store* s, uint32_t n_req, uint32_t k, const uint32_t* doc_ids, uint32_t layer0,
+                           uint32_t n_layers, const void* q_dev, uint32_t n_q, uint32_t g, void* o_dev, float* lse_dev,
+                           float scale, void* kv_dump, void* stream);
 
 /* ------------------------------------------------------------ persistence
  * Compress once, load many (compressed chunks are stored on disk).

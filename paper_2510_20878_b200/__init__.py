@@ -156,16 +156,22 @@ class Store:
         check(lib.hr_assemble_kv(self._h, n_req, k, _p(ids, C.c_uint32), kp, vp, _stream(stream)))
 
     def attend(self, ids, q, o, n_q: int, g: int, lse=None, scale: float = 0.0, kv_dump=None,
-               stream=None) -> None:
+               stream=None, layers=None) -> None:
         """Attention of each request's query rows over its retrieved chunks, straight from the
-        packed codes (hr_attend).  q / o: device [n_req][L][Hl*g][n_q][D]; lse: device float32
-        [n_req][L][Hl*g][n_q] or None; scale <= 0 -> 1/sqrt(D)."""
+        packed codes (hr_attend; hr_attend_layers for layers=(l0, n)).  q / o: device
+        [n_req][L or n][Hl*g][n_q][D]; lse: device float32 [n_req][L or n][Hl*g][n_q] or None;
+        scale <= 0 -> 1/sqrt(D)."""
         ids = _u32(ids)
         if ids.ndim != 2:
             raise ValueError("ids must be [n_req][k]")
         n_req, k = ids.shape
-        check(lib.hr_attend(self._h, n_req, k, _p(ids, C.c_uint32), _ptr(q), int(n_q), int(g), _ptr(o),
-                            _ptr(lse), float(scale), _ptr(kv_dump), _stream(stream)))
+        if layers is None:
+            check(lib.hr_attend(self._h, n_req, k, _p(ids, C.c_uint32), _ptr(q), int(n_q), int(g), _ptr(o),
+                                _ptr(lse), float(scale), _ptr(kv_dump), _stream(stream)))
+        else:
+            check(lib.hr_attend_layers(self._h, n_req, k, _p(ids, C.c_uint32), int(layers[0]), int(layers[1]),
+                                       _ptr(q), int(n_q), int(g), _ptr(o), _ptr(lse), float(scale),
+                                       _ptr(kv_dump), _stream(stream)))
 
     # ------------------------------------------------------------ epochs
     def hotness_delta_ptr(self) -> tuple[int, int]:

@@ -73,6 +73,7 @@ _SIGS = {
     "hr_hotness_delta": (I32, [P, C.POINTER(PI64), PU32]),
     "hr_replace": (I32, [P, P]),
     "hr_attend": (I32, [P, U32, U32, PU32, P, U32, U32, P, P, C.c_float, P, P]),
+    "hr_attend_layers": (I32, [P, U32, U32, PU32, U32, U32, P, U32, U32, P, P, C.c_float, P, P]),
     "hr_store_save": (I32, [P, C.c_char_p]),
     "hr_build_from_file": (I32, [P, C.c_char_p, P]),
     "hr_item_info": (I32, [P, U32, PU32, PU32, PU64]),

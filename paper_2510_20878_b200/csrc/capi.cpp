@@ -137,7 +137,15 @@ hr_status hr_attend(hr_store* s, uint32_t n_req, uint32_t k, const uint32_t* doc
                     void* stream) {
   return guard([&] {
     NONNULL(s);
-    s->impl.attend(n_req, k, doc_ids, q_dev, n_q, g, o_dev, lse_dev, scale, kv_dump, S(stream));
+    s->impl.attend(n_req, k, doc_ids, 0, s->impl.lay.L, q_dev, n_q, g, o_dev, lse_dev, scale, kv_dump, S(stream));
+  });
+}
+hr_status hr_attend_layers(hr_store* s, uint32_t n_req, uint32_t k, const uint32_t* doc_ids, uint32_t layer0,
+                           uint32_t n_layers, const void* q_dev, uint32_t n_q, uint32_t g, void* o_dev, float* lse_dev,
+                           float scale, void* kv_dump, void* stream) {
+  return guard([&] {
+    NONNULL(s);
+    s->impl.attend(n_req, k, doc_ids, layer0, n_layers, q_dev, n_q, g, o_dev, lse_dev, scale, kv_dump, S(stream));
   });
 }
 

@@ -80,7 +80,8 @@ struct AttnParams {
   uint16_t* o;               // same layout as q
   float* lse;                // [n_req][L][Hl*g][n_q] natural-log sum of exp of the scaled scores, or nullptr
   uint16_t* kv_dump;         // test hook: decoded KV [n_req][2][L][Hl][k*T][D], or nullptr
-  uint32_t n_req, k, L, Hl, T, D, g, n_q, M;  // M = g * n_q <= 128
+  uint32_t n_req, k, L, Hl, T, D, g, n_q, M;  // M = g * n_q <= 128; L = layers of this call (window)
+  uint32_t l0;               // first store layer of the window (q / o / lse / kv_dump index layers 0..L-1)
   uint32_t G, g_shift, gse_e, gse_m, dtype;
   float scale_log2;          // softmax scale * log2(e)
   uint64_t code_slab[6];     // per scheme, code bytes per slab

@@ -611,7 +611,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
   const uint32_t unit = blockIdx.x;  // (request, layer, head)
   const uint32_t r = unit / (p.L * p.Hl), lh = unit - r * (p.L * p.Hl);
   const uint32_t l = lh / p.Hl, h = lh - l * p.Hl;
-  const uint32_t slab_i = l * p.Hl + h;
+  const uint32_t slab_i = (p.l0 + l) * p.Hl + h;  // the store's slab: layer l0 + l of the call's window
   const uint32_t hq = p.Hl * p.g;  // query heads on this rank
   const uint64_t row0 = (((uint64_t)r * p.L + l) * hq + (uint64_t)h * p.g) * p.n_q;  // first query row of the unit
   const uint32_t tiles_per_doc = p.T / kKT;
@@ -1036,6 +1036,11 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         ++npv;
       }
     }
+    // consume the last phase of every operand buffer's "PV done" barrier: the decoders only wait for a
+    // buffer they reuse, so without this the final tcgen05.commit arrivals would have no waiter when the
+    // CTA exits (compute-sanitizer synccheck: "missing wait")
+    for (uint32_t b = 0; b < kOpBufs && b < n_tiles; ++b)
+      MBW(&kve[b], ((n_tiles - 1 - b) / kOpBufs) & 1, 11, n_tiles);
   }
   tc_before();
   __syncthreads();

@@ -18,10 +18,12 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <optional>
 #include <unordered_set>
 
 #include "kernels.h"
 #include "policy.h"
+#include "trace.h"
 
 namespace harag {
 
@@ -363,6 +365,7 @@ void Store::build_end(cudaStream_t st) {
 }
 
 void Store::build_with_source(uint32_t nd, const uint64_t* hot, hr_src_fn src, void* user, cudaStream_t st) {
+  const NvtxRange nvtx_call("hr_build");
   require(src != nullptr, HR_EINVAL, "source callback is NULL");
   build_begin(nd, hot);
   // kSrcBatch docs per quantize launch: the source callback fills one buffer pair per doc
@@ -508,6 +511,7 @@ void Store::release_deferred() {
 void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* const* k_out, void* const* v_out,
                      cudaStream_t st) {
   const auto host_t0 = std::chrono::steady_clock::now();
+  const NvtxRange nvtx_call("hr_assemble_kv");
   auto tick = [&](int i) {
     if (!host_prof) return;
     const auto now = std::chrono::steady_clock::now();
@@ -536,6 +540,7 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
   const size_t n_desc = 2ull * n_req * k;
   if (hdesc.size() < n_desc) hdesc.resize(n_desc);  // host descriptors (pageable scratch)
   tick(1);
+  std::optional<NvtxRange> nvtx_plan(std::in_place, "plan");
   // a6 planning, in three passes.
   //  1. Every access in request order: Alg. 2 step 2 (demand mode: one branch per access, the hit
   //     counted where Alg. 2 finds the item, host-queue fills done at once) or the tier lookup (eager).
@@ -702,6 +707,7 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
     range[i] = {b, pos - b};
   }
   tick(3);
+  nvtx_plan.reset();
   bool need_dev = nh > (size_t)kAsmInline;
   for (const auto& rg : range) need_dev |= rg.second > (size_t)kAsmInline;
   // launches of <= kAsmInline descriptors carry them as kernel parameters; only larger ones need the
@@ -715,7 +721,10 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
     ddesc = db->dev;
   }
   // launch A: every resident (request, slot, kind)
-  if (nh) launch(ddesc, hdesc.data(), (uint32_t)nh, k, hbm_mask, st);
+  if (nh) {
+    const NvtxRange r("launch_a");
+    launch(ddesc, hdesc.data(), (uint32_t)nh, k, hbm_mask, st);
+  }
   tick(4);
   if (any_after_a && nh) {
     if (!after_a_ev) HR_CUDA(cudaEventCreateWithFlags(&after_a_ev, cudaEventDisableTiming));
@@ -728,6 +737,8 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
     HR_CUDA(cudaEventCreate(&c1));
   }
   ring_i = 0;
+  std::optional<NvtxRange> nvtx_stream;
+  if (!streamed.empty()) nvtx_stream.emplace("host_tier_stream");
   for (size_t i = 0; i < streamed.size(); ++i) {
     const uint32_t item = streamed[i].item;
     const bool to_arena = streamed[i].arena_off != FreeList::kNone;
@@ -759,6 +770,7 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
       if (!sl.bounce) HR_CUDA(cudaHostAlloc((void**)&sl.bounce, align_up(max_item, 4096), cudaHostAllocPortable));
       if (sl.used) HR_CUDA(cudaEventSynchronize(sl.copied));  // previous DMA out of this bounce buffer done
       constexpr size_t kPiece = 8u << 20;
+      const NvtxRange r("bounce");
       for (size_t off = 0; off < bytes[item]; off += kPiece) {
         const size_t n = std::min<size_t>(kPiece, bytes[item] - off);
         host_copy(sl.bounce + off, src + off, n);
@@ -776,10 +788,14 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
     sl.used = true;
     stats.bytes_h2d += bytes[item];
     HR_CUDA(cudaStreamWaitEvent(st, sl.copied, 0));
-    launch(ddesc ? ddesc + range[i].first : nullptr, hdesc.data() + range[i].first, (uint32_t)range[i].second, k,
-           1u << scheme[item], st);
+    {
+      const NvtxRange r("launch_b");
+      launch(ddesc ? ddesc + range[i].first : nullptr, hdesc.data() + range[i].first, (uint32_t)range[i].second, k,
+             1u << scheme[item], st);
+    }
     if (!to_arena) HR_CUDA(cudaEventRecord(sl.free_ev, st));
   }
+  nvtx_stream.reset();
   if (db) HR_CUDA(cudaEventRecord(db->done, st));
   if (call_timing) {
     HR_CUDA(cudaEventRecord(call_ev[1], st));
@@ -855,10 +871,15 @@ void Store::poll_promotions(bool wait_all) {
 // launch reads an evicted item from HBM.  Promotions are asynchronous: an item becomes resident
 // when its copy event has completed (polled at the next hr_assemble_kv), and until then it is
 // streamed from the host like any host-tier item — requests never wait for a migration.
-// Consumer: attention over the request's packed chunks (kernels/attend.cu).
-// Every requested item must be resident in the HBM arena (eager placement).
-void Store::attend(uint32_t n_req, uint32_t k, const uint32_t* ids, const void* q, uint32_t n_q, uint32_t g,
-                   void* o, float* lse, float scale, void* kv_dump, cudaStream_t st) {
+// Consumer: attention over the request's packed chunks (kernels/attend.cu), for
+// the layer window [l0, l0 + nl).  HBM-resident items are read in place; every other item is staged
+// first: the window's code and meta slabs (contiguous runs of the blob) are copied from
+// the pinned tier / host backing (pageable through the pinned bounce; disk through a read of
+// the blob) into a staging-ring slot, and the launch waits for those copies.  A call's host-tier
+// items must fit the ring at once (HR_ESTATE otherwise, before any work).
+void Store::attend(uint32_t n_req, uint32_t k, const uint32_t* ids, uint32_t l0, uint32_t nl, const void* q,
+                   uint32_t n_q, uint32_t g, void* o, float* lse, float scale, void* kv_dump, cudaStream_t st) {
+  const NvtxRange nvtx_call("hr_attend");
   require(state == State::Built, HR_ESTATE, "hr_attend before the store is built");
   require(!alg2, HR_ESTATE, "hr_attend needs eager placement (demand_mode = 0)");
   require(q && o, HR_EINVAL, "NULL query or output pointer");
@@ -867,6 +888,7 @@ void Store::attend(uint32_t n_req, uint32_t k, const uint32_t* ids, const void* 
   require(g >= 1 && n_q >= 1 && (uint64_t)g * n_q <= 128, HR_EINVAL, "g * n_q must be in [1, 128]");
   require(lay.D == 64 || lay.D == 128, HR_EINVAL, "hr_attend: head_dim must be 64 or 128");
   require(lay.T % 64 == 0, HR_EINVAL, "hr_attend: tokens per chunk must be a multiple of 64");
+  require(nl >= 1 && l0 < lay.L && nl <= lay.L - l0, HR_EINVAL, "hr_attend: layer window outside [0, L)");
   require(n_req == 0 || (k >= 1 && ids), HR_EINVAL, "bad request");
   std::vector<uint32_t> tmp(k);
   for (uint32_t r = 0; r < n_req; ++r) {
@@ -880,11 +902,63 @@ void Store::attend(uint32_t n_req, uint32_t k, const uint32_t* ids, const void* 
   }
   HR_CUDA(cudaSetDevice(cfg.device));
   if (!promos.empty()) poll_promotions(false);
-  for (uint64_t i = 0; i < (uint64_t)n_req * k; ++i)
-    for (uint32_t kind = 0; kind < 2; ++kind)
-      require(loc[2 * ids[i] + kind].hbm_off != FreeList::kNone, HR_ESTATE,
-              "hr_attend: item " + std::to_string(2 * ids[i] + kind) + " is not resident in HBM");
   if (n_req == 0) return;
+  // host-tier items of the call, each staged once
+  std::unordered_map<uint32_t, uint32_t> staged;  // item -> ring slot
+  for (uint64_t i = 0; i < (uint64_t)n_req * k; ++i)
+    for (uint32_t kind = 0; kind < 2; ++kind) {
+      const uint32_t item = 2 * ids[i] + kind;
+      if (loc[item].hbm_off == FreeList::kNone && !staged.count(item)) staged.emplace(item, (uint32_t)staged.size());
+    }
+  if (!staged.empty()) {
+    ensure_ring();
+    require(staged.size() <= slots, HR_ESTATE,
+            "hr_attend: " + std::to_string(staged.size()) + " host-tier items exceed the staging ring (" +
+                std::to_string(slots) + " slots); split the batch");
+  }
+  const uint64_t ns = (uint64_t)nl * lay.Hl;  // slabs of the window
+  std::vector<uint8_t*> slot_codes(staged.size());
+  std::vector<std::pair<uint32_t, uint32_t>> order_st(staged.begin(), staged.end());
+  std::sort(order_st.begin(), order_st.end(), [](auto& x, auto& y) { return x.second < y.second; });
+  for (const auto& [item, si] : order_st) {
+    Slot& sl = ring[si];
+    const uint32_t sc = scheme[item];
+    const uint64_t cb = lay.code_bytes_slab(sc), ms = lay.meta_stride(sc);
+    const uint64_t c0 = (uint64_t)l0 * lay.Hl * cb, cn = ns * cb;
+    const uint64_t mo = lay.meta_offset(sc), m0 = mo + (uint64_t)l0 * lay.Hl * ms, mn = ns * ms;
+    const uint64_t dst_m = align_up(cn, 256);  // window meta right after the window codes
+    HR_CUDA(cudaStreamWaitEvent(copy_stream, sl.free_ev, 0));
+    const uint8_t* src = loc[item].pin_off != FreeList::kNone    ? pin_base + loc[item].pin_off
+                         : loc[item].page_off != FreeList::kNone ? page_base + loc[item].page_off
+                         : loc[item].backing_off != FreeList::kNone ? backing_base + loc[item].backing_off
+                                                                    : nullptr;
+    const bool pinned_src = loc[item].pin_off != FreeList::kNone ||
+                            (loc[item].page_off == FreeList::kNone && loc[item].backing_off != FreeList::kNone &&
+                             backing_is_pinned);
+    if (!pinned_src) {  // pageable or disk: the window through this slot's pinned bounce buffer
+      if (!sl.bounce) HR_CUDA(cudaHostAlloc((void**)&sl.bounce, align_up(max_item, 4096), cudaHostAllocPortable));
+      if (sl.used) HR_CUDA(cudaEventSynchronize(sl.copied));
+      if (src) {
+        host_copy(sl.bounce, src + c0, cn);
+        if (mn) host_copy(sl.bounce + dst_m, src + m0, mn);
+      } else {  // DISK tier: the blob, then the window out of it
+        read_disk(item, sl.bounce);
+        if (c0) std::memmove(sl.bounce, sl.bounce + c0, cn);
+        if (mn) std::memmove(sl.bounce + dst_m, sl.bounce + m0, mn);
+      }
+      src = sl.bounce;
+      HR_CUDA(cudaMemcpyAsync(sl.dev, src, dst_m + mn, cudaMemcpyHostToDevice, copy_stream));
+    } else {
+      HR_CUDA(cudaMemcpyAsync(sl.dev, src + c0, cn, cudaMemcpyHostToDevice, copy_stream));
+      if (mn) HR_CUDA(cudaMemcpyAsync(sl.dev + dst_m, src + m0, mn, cudaMemcpyHostToDevice, copy_stream));
+    }
+    HR_CUDA(cudaEventRecord(sl.copied, copy_stream));
+    sl.used = true;
+    // the kernel addresses slab (l0 + l) * Hl + h from the descriptor: offset the pointers by the window start
+    slot_codes[si] = sl.dev;
+    stats.bytes_h2d += dst_m + mn;
+    stats.h2d_items++;
+  }
   const size_t n_desc = 2ull * n_req * k;
   DescBuf& db = desc_buffer(n_desc);
   for (uint32_t r = 0; r < n_req; ++r) {
@@ -892,25 +966,40 @@ void Store::attend(uint32_t n_req, uint32_t k, const uint32_t* ids, const void* 
     for (uint32_t j = 0; j < k; ++j)
       for (uint32_t kind = 0; kind < 2; ++kind) {
         const uint32_t item = 2 * ids[(uint64_t)r * k + j] + kind;
+        const uint32_t sc = scheme[item];
         AsmDesc d{};
-        d.codes = hbm_ptr(item);
-        d.meta = d.codes + lay.meta_offset(scheme[item]);
+        const auto it = staged.find(item);
+        if (it == staged.end()) {
+          d.codes = hbm_ptr(item);
+          d.meta = d.codes + lay.meta_offset(sc);
+          stats.hits[HR_T_HBM]++;
+        } else {
+          const uint64_t cb = lay.code_bytes_slab(sc), ms = lay.meta_stride(sc);
+          uint8_t* base = slot_codes[it->second];
+          d.codes = base - (uint64_t)l0 * lay.Hl * cb;
+          d.meta = base + align_up(ns * cb, 256) - (uint64_t)l0 * lay.Hl * ms;
+          const Loc& l = loc[item];
+          stats.hits[l.pin_off != FreeList::kNone ||
+                             (l.page_off == FreeList::kNone && l.backing_off != FreeList::kNone && backing_is_pinned)
+                         ? HR_T_PIN
+                         : HR_T_PAGE]++;
+        }
         d.count = counted ? reinterpret_cast<unsigned long long*>(delta + item) : nullptr;
         d.slot = j;
-        d.scheme = scheme[item];
+        d.scheme = sc;
         db.host[((uint64_t)r * k + j) * 2 + kind] = d;
-        stats.hits[HR_T_HBM]++;
-        stats.bytes_hbm_alg += bytes_read_alg(item);
+        stats.bytes_hbm_alg += bytes_read_alg(item) / lay.L * nl;
       }
   }
   HR_CUDA(cudaMemcpyAsync(db.dev, db.host, n_desc * sizeof(AsmDesc), cudaMemcpyHostToDevice, st));
+  for (const auto& kv : staged) HR_CUDA(cudaStreamWaitEvent(st, ring[kv.second].copied, 0));
   AttnParams p{};
   p.descs = db.dev;
   p.q = static_cast<const uint16_t*>(q);
   p.o = static_cast<uint16_t*>(o);
   p.lse = lse;
   p.kv_dump = static_cast<uint16_t*>(kv_dump);
-  p.n_req = n_req, p.k = k, p.L = lay.L, p.Hl = lay.Hl, p.T = lay.T, p.D = lay.D, p.g = g, p.n_q = n_q;
+  p.n_req = n_req, p.k = k, p.L = nl, p.l0 = l0, p.Hl = lay.Hl, p.T = lay.T, p.D = lay.D, p.g = g, p.n_q = n_q;
   p.M = g * n_q;
   p.G = lay.G, p.g_shift = (uint32_t)__builtin_ctz(lay.G), p.gse_e = lay.gse_e, p.gse_m = lay.gse_m;
   p.dtype = lay.dtype;
@@ -921,7 +1010,7 @@ void Store::attend(uint32_t n_req, uint32_t k, const uint32_t* ids, const void* 
     p.meta_stride[s] = (uint32_t)lay.meta_stride(s);
   }
   // q read + o written (algorithmic), beside the codes + meta counted above
-  stats.bytes_hbm_alg += 2ull * 2 * n_req * lay.L * lay.Hl * g * n_q * lay.D;
+  stats.bytes_hbm_alg += 2ull * 2 * n_req * nl * lay.Hl * g * n_q * lay.D;
   cudaEvent_t a = nullptr, b = nullptr;
   if (timing) {
     HR_CUDA(cudaEventCreate(&a));
@@ -934,6 +1023,7 @@ void Store::attend(uint32_t n_req, uint32_t k, const uint32_t* ids, const void* 
     timers.emplace_back(a, b);
   }
   stats.kernel_launches++;
+  for (const auto& kv : staged) HR_CUDA(cudaEventRecord(ring[kv.second].free_ev, st));
   HR_CUDA(cudaEventRecord(db.done, st));
   req_counter += n_req;
   stats.requests += n_req;
@@ -941,6 +1031,7 @@ void Store::attend(uint32_t n_req, uint32_t k, const uint32_t* ids, const void* 
 
 void Store::replace(cudaStream_t st) {
   require(state == State::Built, HR_ESTATE, "hr_replace before the store is built");
+  const NvtxRange nvtx_call("hr_replace");
   const CpuBind bind(local_cpus);  // pinned-tier fills
   HR_CUDA(cudaSetDevice(cfg.device));
   std::vector<int64_t> dh(n_items);

@@ -31,7 +31,7 @@ def torch_cuda():
 
 
 def build(torch, *, L, H, T, D, n_docs, ladder, taus, dtype, group=0, rank=0, world=1, demand=False,
-          hbm_items=None):
+          hbm_items=None, **over):
     import paper_2510_20878_b200 as hr
     prof = synth.gen_requests(n_docs, 4 * n_docs, min(4, n_docs), 1.1, seed=7)
     h = hotness.count_requests(prof, n_docs).astype(np.uint64)
@@ -41,7 +41,7 @@ def build(torch, *, L, H, T, D, n_docs, ladder, taus, dtype, group=0, rank=0, wo
     order = hotness.rank_items(h)
     hb = sum(sizes) + 4096 if hbm_items is None else sum(sizes[i] for i in order[:hbm_items])
     st = hr.Store(L=L, H=H, D=D, T=T, dtype=dtype, group=group, ladder=ladder, taus=taus, hbm_budget=hb,
-                  rank=rank, world=world, demand_mode=demand)
+                  rank=rank, world=world, demand_mode=demand, **over)
 
     def src(doc, kp, vp, stream):
         synth.gen_item_device(kp, L, H, T, D, doc, 0, dtype=dtype, stream=stream)
@@ -61,23 +61,25 @@ def check_bound(O_gpu, lse_gpu, O, lse, V_range, dtype):
     assert np.max(np.abs(lse_gpu - lse)) <= 2.0 ** -8, np.max(np.abs(lse_gpu - lse))
 
 
-def run_case(torch, st, ora, lay, reqs, n_q, g, dtype, scale=None):
+def run_case(torch, st, ora, lay, reqs, n_q, g, dtype, scale=None, layers=None):
     import paper_2510_20878_b200 as hr  # noqa: F401
     n_req, k = reqs.shape
     HQ = lay.Hl * g
-    Qb = synth.gen_query(n_req, lay.L, HQ, n_q, lay.D, dtype=dtype)
+    l0, nl = layers if layers is not None else (0, lay.L)
+    Qb = synth.gen_query(n_req, nl, HQ, n_q, lay.D, dtype=dtype)
     q = torch.from_numpy(Qb.view(np.int16)).cuda()
     o = torch.full_like(q, 0x7FFF)
-    lse = torch.full((n_req, lay.L, HQ, n_q), float("nan"), dtype=torch.float32, device="cuda")
-    dump = torch.empty(n_req * 2 * lay.L * lay.Hl * k * lay.T * lay.D, dtype=torch.int16, device="cuda")
-    st.attend(reqs, q, o, n_q, g, lse=lse, scale=scale or 0.0, kv_dump=dump)
+    lse = torch.full((n_req, nl, HQ, n_q), float("nan"), dtype=torch.float32, device="cuda")
+    dump = torch.empty(n_req * 2 * nl * lay.Hl * k * lay.T * lay.D, dtype=torch.int16, device="cuda")
+    st.attend(reqs, q, o, n_q, g, lse=lse, scale=scale or 0.0, kv_dump=dump, layers=layers)
     torch.cuda.synchronize()
     Og = o.cpu().numpy().view(np.uint16)
     Ogf = (Og.astype(np.uint32) << 16).view(np.float32) if dtype == "bf16" else Og.view(np.float16).astype(np.float32)
     lg = lse.cpu().numpy()
-    dmp = dump.cpu().numpy().view(np.uint16).reshape(n_req, 2, lay.L, lay.Hl, k * lay.T, lay.D)
+    dmp = dump.cpu().numpy().view(np.uint16).reshape(n_req, 2, nl, lay.Hl, k * lay.T, lay.D)
     for r, req in enumerate(reqs):
         K, V = ora.assemble(list(req))
+        K, V = K[l0:l0 + nl], V[l0:l0 + nl]
         bad = np.argwhere(dmp[r, 0] != K)
         assert bad.size == 0, f"decoded K differs, request {r}: {len(bad)} at {bad[:4].tolist()} " \
             f"got {[hex(int(dmp[r, 0][tuple(i)])) for i in bad[:4]]} want {[hex(int(K[tuple(i)])) for i in bad[:4]]}"
@@ -86,7 +88,7 @@ def run_case(torch, st, ora, lay, reqs, n_q, g, dtype, scale=None):
         from oracle import numerics
         v = numerics.to_f32(V, dtype).astype(np.float64)
         vr = np.empty_like(O)   # max_j |v_j - O| per (layer, query head, row, column)
-        for l in range(lay.L):
+        for l in range(nl):
             for hq in range(HQ):
                 vr[l, hq] = np.max(np.abs(v[l, hq // g][None, :, :] - O[l, hq][:, None, :]), axis=1)
         check_bound(Ogf[r].astype(np.float64), lg[r].astype(np.float64), O, L_, vr, dtype)
@@ -130,9 +132,8 @@ def test_attend_counts_hotness_and_validates(torch_cuda):
     torch.cuda.synchronize()
     delta = st.hotness_delta().cpu().numpy()
     assert np.array_equal(delta, hotness.count_requests(reqs, 8))
-    cold = next(d for d in range(8) if st.item_info(2 * d)[1] != 0)
-    with pytest.raises(hr.HaragError, match="ESTATE"):
-        st.attend(np.array([[docs[0], cold]], np.uint32), q, o, 4, 1)
+    with pytest.raises(hr.HaragError, match="EINVAL"):
+        st.attend(reqs, q, o, 4, 1, layers=(1, 2))      # window past L
     with pytest.raises(hr.HaragError, match="EINVAL"):
         st.attend(reqs, q, o, 65, 2)                     # g * n_q > 128
     with pytest.raises(hr.HaragError, match="EINVAL"):
@@ -199,3 +200,33 @@ def test_attend_full_shape_sampled(torch_cuda):
         vr = np.max(np.abs(v[None, :, :] - O[:, None, :]), axis=1)
         check_bound(Og[0, l, hq].astype(np.float64), lg[0, l, hq].astype(np.float64), O, L_, vr, "bf16")
     st.close()
+
+
+@pytest.mark.parametrize("backing_pinned", [False, True])
+def test_attend_host_tier_items_and_layer_windows(torch_cuda, backing_pinned):
+    """Items outside the HBM arena (pageable backing through the pinned bounce, or a pinned backing)
+    are staged into the ring for the call; layer windows read only their slabs.  Decoded K/V stay
+    bit-exact and O / LSE within the bound, for the whole stack and for one-layer windows."""
+    import paper_2510_20878_b200 as hr
+    torch = torch_cuda
+    st, ora, lay = build(torch, L=3, H=2, T=128, D=128, n_docs=8, ladder=PAPER, taus=(0.2, 0.2, 0.2),
+                         dtype="bf16", hbm_items=4, backing_pinned=backing_pinned, keep_backing=True)
+    reqs = synth.gen_requests(8, 3, 3, 0.3, seed=21)
+    tiers = {st.item_info(2 * int(d) + kd)[1] for d in reqs.reshape(-1) for kd in (0, 1)}
+    assert tiers - {0}, "the requests must reach host-tier items"
+    before = st.stats()["h2d_items"]
+    run_case(torch, st, ora, lay, reqs, 8, 2, "bf16")
+    assert st.stats()["h2d_items"] > before
+    for l0 in range(3):
+        run_case(torch, st, ora, lay, reqs, 8, 2, "bf16", layers=(l0, 1))
+    run_case(torch, st, ora, lay, reqs, 8, 2, "bf16", layers=(1, 2))
+    st.close()
+    # a call whose host-tier items do not fit the staging ring is refused before any work
+    st2, _, _ = build(torch, L=1, H=1, T=64, D=64, n_docs=8, ladder=NORTH, taus=(0.25, 0.25), dtype="fp16",
+                      hbm_items=2, staging_slots=2)
+    cold = [d for d in range(8) if st2.item_info(2 * d)[1] != 0 and st2.item_info(2 * d + 1)[1] != 0][:2]
+    q = torch.zeros(1 * 1 * 4 * 64, dtype=torch.int16, device="cuda")
+    o = torch.empty_like(q)
+    with pytest.raises(hr.HaragError, match="ESTATE"):
+        st2.attend(np.array([cold], np.uint32), q, o, 4, 1)
+    st2.close()

@@ -1,12 +1,16 @@
 #!/bin/bash
 # compute-sanitizer over every libharag kernel (tests/sanitize_driver.py, tiny shapes, outputs checked
-# against the oracle): memcheck, racecheck (shared-memory hazards), synccheck (barrier misuse),
-# initcheck (reads of uninitialised device memory).  Logs in gpurun_out/sanitize/.
+# against the oracle): memcheck (+ leak check), racecheck (shared-memory hazards), synccheck (barrier
+# misuse), initcheck (reads of uninitialised device memory).  Raw logs and a classified summary
+# (tools/sanitize_summary.py) in gpurun_out/sanitize/.
 mkdir -p gpurun_out/sanitize
 for tool in memcheck racecheck synccheck initcheck; do
-  extra=""
-  [ "$tool" = memcheck ] && extra="--leak-check full"
-  timeout 1200 compute-sanitizer --tool $tool $extra --print-limit 50 --error-exitcode 99 \
+  extra="--print-limit 200"
+  [ "$tool" = memcheck ] && extra="$extra --leak-check full"
+  [ "$tool" = initcheck ] && extra="--print-limit 100000"
+  timeout 1500 compute-sanitizer --tool $tool $extra --error-exitcode 99 \
     python tests/sanitize_driver.py > gpurun_out/sanitize/$tool.txt 2>&1
-  echo "$tool rc=$? $(grep -h 'ERROR SUMMARY\|RACECHECK SUMMARY\|LEAK SUMMARY' gpurun_out/sanitize/$tool.txt | tr '\n' ' ')"
+  echo "== $tool rc=$?" | tee gpurun_out/sanitize/$tool.summary.txt
+  python tools/sanitize_summary.py gpurun_out/sanitize/$tool.txt | tee -a gpurun_out/sanitize/$tool.summary.txt
+  grep -h "sanitize_driver ok" gpurun_out/sanitize/$tool.txt | tee -a gpurun_out/sanitize/$tool.summary.txt
 done
