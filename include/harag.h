@@ -119,6 +119,8 @@ typedef struct {
   uint64_t bytes_migrated;    /* host -> device bytes of hr_replace promotions (not in bytes_h2d) */
   uint64_t hits_disk;         /* item accesses served from the store file (HR_T_DISK) */
   double   host_ms;           /* host time inside hr_assemble_kv (entry -> last launch enqueued), summed */
+  double   quant_ms;          /* sum of quantize-launch durations (CUDA events) of hr_build_put* when timing is on */
+  uint64_t quant_launches;    /* quantize launches included in quant_ms */
 } hr_stats;
 
 typedef struct hr_store hr_store;

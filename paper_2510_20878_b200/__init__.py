@@ -248,7 +248,8 @@ class Store:
                 "migrations_out": s.migrations_out, "failed_promotions": s.failed_promotions,
                 "kernel_ms": s.kernel_ms, "timed_launches": s.timed_launches, "hbm_used": s.hbm_used,
                 "pin_used": s.pin_used, "h2d_ms": s.h2d_ms, "h2d_items": s.h2d_items,
-                "bytes_migrated": s.bytes_migrated, "hits_disk": s.hits_disk, "host_ms": s.host_ms}
+                "bytes_migrated": s.bytes_migrated, "hits_disk": s.hits_disk, "host_ms": s.host_ms,
+                "quant_ms": s.quant_ms, "quant_launches": s.quant_launches}
 
     def close(self) -> None:
         if self._h:

@@ -43,6 +43,7 @@ class Stats(C.Structure):
         ("kernel_ms", C.c_double), ("timed_launches", C.c_uint64), ("hbm_used", C.c_uint64),
         ("pin_used", C.c_uint64), ("h2d_ms", C.c_double), ("h2d_items", C.c_uint64),
         ("bytes_migrated", C.c_uint64), ("hits_disk", C.c_uint64), ("host_ms", C.c_double),
+        ("quant_ms", C.c_double), ("quant_launches", C.c_uint64),
     ]
 
 

@@ -1041,6 +1041,12 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     // CTA exits (compute-sanitizer synccheck: "missing wait")
     for (uint32_t b = 0; b < kOpBufs && b < n_tiles; ++b)
       MBW(&kve[b], ((n_tiles - 1 - b) / kOpBufs) & 1, 11, n_tiles);
+    // ... and of the S-ready / PV-done barriers it committed to (the softmax warps wait on them too)
+    for (uint32_t b = 0; b < kSB && b < n_tiles; ++b) {
+      const uint32_t last = (n_tiles - 1 - b) / kSB;
+      MBW(&sf[b], last & 1, 12, n_tiles);
+      MBW(&pfree[b], last & 1, 12, n_tiles);
+    }
   }
   tc_before();
   __syncthreads();

@@ -101,6 +101,7 @@ Store::~Store() {
   }
   for (auto& t : timers) cudaEventDestroy(t.first), cudaEventDestroy(t.second);
   for (auto& t : h2d_timers) cudaEventDestroy(t.first), cudaEventDestroy(t.second);
+  for (auto& t : qtimers) cudaEventDestroy(t.first), cudaEventDestroy(t.second);
   copy_pool.reset();
   if (hbm_base) cudaFree(hbm_base);
   if (pin_base) cudaFreeHost(pin_base);
@@ -333,7 +334,17 @@ void Store::build_put_batch(uint32_t n, const uint32_t* docs, const void* const*
       if (bytes[item] > mend) HR_CUDA(cudaMemsetAsync(dst + mend, 0, bytes[item] - mend, st));
     }
   }
+  cudaEvent_t qa = nullptr, qb = nullptr;
+  if (timing) {
+    HR_CUDA(cudaEventCreate(&qa));
+    HR_CUDA(cudaEventCreate(&qb));
+    HR_CUDA(cudaEventRecord(qa, st));
+  }
   launch_quantize(q, (int)(2 * n), st);
+  if (timing) {
+    HR_CUDA(cudaEventRecord(qb, st));
+    qtimers.emplace_back(qa, qb);
+  }
   for (uint32_t i = 0; i < 2 * n; ++i) {
     const uint32_t item = 2 * docs[i / 2] + i % 2;
     uint8_t* dst = dsts[i];
@@ -1394,6 +1405,16 @@ void Store::get_stats(hr_stats* out) {
     }
     timers.clear();
   }
+  for (auto& t : qtimers) {
+    HR_CUDA(cudaEventSynchronize(t.second));
+    float ms = 0;
+    HR_CUDA(cudaEventElapsedTime(&ms, t.first, t.second));
+    stats.quant_ms += ms;
+    stats.quant_launches++;
+    cudaEventDestroy(t.first);
+    cudaEventDestroy(t.second);
+  }
+  qtimers.clear();
   for (auto& t : h2d_timers) {
     HR_CUDA(cudaEventSynchronize(t.second));
     float ms = 0;

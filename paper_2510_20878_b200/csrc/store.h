@@ -171,6 +171,7 @@ struct Store {
   int grid_override = 0;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> timers;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> h2d_timers;  // copy-stream window per assemble call
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> qtimers;     // quantize launches (hr_build_put*)
   std::unique_ptr<CopyPool> copy_pool;                           // pageable -> pinned bounce workers
   // demand mode (cfg.demand_mode = 1): the paper-literal Alg. 2 step 2 state machine
   std::unique_ptr<Alg2> alg2;

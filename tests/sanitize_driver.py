@@ -26,11 +26,16 @@ import synth  # noqa: E402
 from oracle import attention, hotness  # noqa: E402
 from oracle import store as ost  # noqa: E402
 
+# HARAG_SAN_NO_PASS16=1: ladders without PASS16 (whose tiles the kernels write with the bulk-copy engine,
+# cp.async.bulk shared -> global, which initcheck does not see as initialising device memory)
+NO_PASS16 = bool(os.environ.get("HARAG_SAN_NO_PASS16"))
 NAMES = {"PASS16": ost.PASS16, "INT8": ost.INT8, "FP8E4M3": ost.FP8E4M3, "FP8E5M2": ost.FP8E5M2,
          "GSE8": ost.GSE8, "INT4": ost.INT4}
 
 
 def make(L, H, T, D, n_docs, ladder, taus, dtype="bf16", group=0, hbm_items=None, pin_items=0, pinned=False):
+    if NO_PASS16:
+        ladder = tuple("INT8" if s == "PASS16" else s for s in ladder)
     prof = synth.gen_requests(n_docs, 4 * n_docs, min(4, n_docs), 1.1, seed=7)
     h = hotness.count_requests(prof, n_docs).astype(np.uint64)
     lay = ost.Layout(L=L, H=H, T=T, D=D, dtype=dtype, group=group)
