@@ -10,6 +10,7 @@
 // the CPUs local to the store's GPU (set_affinity).
 #pragma once
 
+#include <immintrin.h>
 #include <sched.h>
 
 #include <algorithm>
@@ -25,9 +26,38 @@
 
 namespace harag {
 
+// Non-temporal (streaming-store) copy: the bounce destination is written once and read only by the
+// DMA engine, so write-allocate reads of it are wasted host DRAM traffic — and the bounce copy shares
+// host DRAM bandwidth with the very DMA it feeds.
+__attribute__((target("avx2"))) inline void copy_nt(void* dst, const void* src, size_t n) {
+  uint8_t* d = (uint8_t*)dst;
+  const uint8_t* s = (const uint8_t*)src;
+  const size_t head = (32 - ((uintptr_t)d & 31)) & 31;
+  if (n < head + 128) {
+    std::memcpy(d, s, n);
+    return;
+  }
+  std::memcpy(d, s, head);
+  d += head, s += head, n -= head;
+  const size_t body = n & ~size_t(127);
+  for (size_t i = 0; i < body; i += 128) {
+    const __m256i a = _mm256_loadu_si256((const __m256i*)(s + i));
+    const __m256i b = _mm256_loadu_si256((const __m256i*)(s + i + 32));
+    const __m256i c = _mm256_loadu_si256((const __m256i*)(s + i + 64));
+    const __m256i e = _mm256_loadu_si256((const __m256i*)(s + i + 96));
+    _mm256_stream_si256((__m256i*)(d + i), a);
+    _mm256_stream_si256((__m256i*)(d + i + 32), b);
+    _mm256_stream_si256((__m256i*)(d + i + 64), c);
+    _mm256_stream_si256((__m256i*)(d + i + 96), e);
+  }
+  _mm_sfence();
+  std::memcpy(d + body, s + body, n - body);
+}
+
 class CopyPool {
  public:
-  explicit CopyPool(unsigned n, int spin = 2000) : spin_(spin) {
+  explicit CopyPool(unsigned n, int spin = 2000, bool nt = true)
+      : spin_(spin), nt_(nt && __builtin_cpu_supports("avx2")) {
     for (unsigned i = 0; i < n; ++i) workers_.emplace_back([this, i] { run(i); });
   }
   ~CopyPool() {
@@ -59,7 +89,11 @@ class CopyPool {
     const size_t chunk = ((n + parts - 1) / parts + 4095) & ~size_t(4095);  // parts * chunk >= n
     parallel_for(parts, [&](unsigned p) {
       const size_t b = (size_t)p * chunk;
-      if (b < n) std::memcpy(d + b, s + b, std::min(chunk, n - b));
+      if (b >= n) return;
+      if (nt_)
+        copy_nt(d + b, s + b, std::min(chunk, n - b));
+      else
+        std::memcpy(d + b, s + b, std::min(chunk, n - b));
     });
   }
   // fn(0..parts-1) over the calling thread (part 0) and the workers; returns when all are done.
@@ -118,6 +152,7 @@ class CopyPool {
     }
   }
   const int spin_;
+  const bool nt_;
   std::vector<std::thread> workers_;
   std::mutex m_;
   std::condition_variable cv_;

@@ -776,11 +776,14 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
       read_disk(item, sl.bounce);
       HR_CUDA(cudaMemcpyAsync(dest[i], sl.bounce, bytes[item], cudaMemcpyHostToDevice, copy_stream));
     } else if (bounce) {
-      // pageable data is first copied to pinned memory.  The bounce runs in 8 MiB pieces so
-      // the host copy of piece p+1 overlaps the DMA of piece p (and item i+1's copy item i's DMA).
+      // pageable data is first copied to pinned memory (non-temporal stores, every host core).
+      // Whole-item pieces by default: the copy of item i+1 overlaps the DMA of item i, and splitting an
+      // item over the pool in smaller pieces measured slower (tools/bounce_bench.cpp: 2 / 4 / 8 MiB /
+      // whole 16.5 MiB pieces on 16 threads: 23 / 32 / 30 / 43 GB/s).
       if (!sl.bounce) HR_CUDA(cudaHostAlloc((void**)&sl.bounce, align_up(max_item, 4096), cudaHostAllocPortable));
       if (sl.used) HR_CUDA(cudaEventSynchronize(sl.copied));  // previous DMA out of this bounce buffer done
-      constexpr size_t kPiece = 8u << 20;
+      static const size_t kPiece = std::getenv("HARAG_BOUNCE_PIECE") ? (size_t)std::atoll(std::getenv("HARAG_BOUNCE_PIECE"))
+                                                                    : (size_t)1 << 40;
       const NvtxRange r("bounce");
       for (size_t off = 0; off < bytes[item]; off += kPiece) {
         const size_t n = std::min<size_t>(kPiece, bytes[item] - off);
@@ -849,7 +852,8 @@ void Store::host_copy(void* dst, const void* src, size_t n) {
     unsigned t = std::max(1u, std::thread::hardware_concurrency()) - 1;
     if (const char* e = std::getenv("HARAG_COPY_THREADS")) t = (unsigned)std::atoi(e);
     const int spin = std::getenv("HARAG_POOL_SPIN") ? std::atoi(std::getenv("HARAG_POOL_SPIN")) : 2000;
-    copy_pool.reset(new CopyPool(std::min(t, 31u), spin));
+    const bool nt = !(std::getenv("HARAG_COPY_NT") && std::atoi(std::getenv("HARAG_COPY_NT")) == 0);
+    copy_pool.reset(new CopyPool(std::min(t, 31u), spin, nt));
     copy_pool->set_affinity(local_cpus);
   }
   if (n) copy_pool->copy(dst, src, n);
@@ -1393,6 +1397,28 @@ uint64_t Store::placement_hash() const {
 }
 
 void Store::get_stats(hr_stats* out) {
+  // HARAG_TIMELINE=<file>: append the timed launches and host-tier copy windows (start, duration in ms,
+  // relative to the first timed launch) — a poor man's timeline where no Nsight Systems is available
+  if (const char* tl = std::getenv("HARAG_TIMELINE"); tl && !timers.empty()) {
+    if (FILE* f = std::fopen(tl, "a")) {
+      cudaEvent_t ref = timers.front().first;
+      HR_CUDA(cudaEventSynchronize(timers.back().second));
+      for (auto& t : timers) {
+        float a = 0, d = 0;
+        cudaEventElapsedTime(&a, ref, t.first);
+        cudaEventElapsedTime(&d, t.first, t.second);
+        std::fprintf(f, "kernel %.4f %.4f\n", a, d);
+      }
+      for (auto& t : h2d_timers) {
+        float a = 0, d = 0;
+        cudaEventSynchronize(t.second);
+        cudaEventElapsedTime(&a, ref, t.first);
+        cudaEventElapsedTime(&d, t.first, t.second);
+        std::fprintf(f, "h2d %.4f %.4f\n", a, d);
+      }
+      std::fclose(f);
+    }
+  }
   if (!timers.empty()) {
     for (auto& t : timers) {
       HR_CUDA(cudaEventSynchronize(t.second));

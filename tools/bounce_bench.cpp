@@ -39,9 +39,10 @@ int main(int argc, char** argv) {
   cudaStreamSynchronize(st);
   printf("pinned DMA alone: %.1f GB/s\n", n_items * item / (now() - t0) / 1e9);
   for (unsigned workers : {7u, 11u, 15u}) {
-    for (int spin : {2000}) {
-      harag::CopyPool pool(workers, spin);
-      for (size_t piece : {(size_t)2 << 20, (size_t)4 << 20, (size_t)8 << 20, item}) {
+    for (int nt : {0, 1}) {
+      harag::CopyPool pool(workers, 2000, nt != 0);
+      printf("-- %s copies\n", nt ? "non-temporal" : "memcpy");
+      for (size_t piece : {(size_t)4 << 20, (size_t)8 << 20, item}) {
         std::vector<bool> used(slots, false);
         double t1 = now();
         double host_copy = 0;
