@@ -593,6 +593,15 @@ class RandomLlama:
         lse = t.logsumexp(s, dim=-1)
         return (t.softmax(s, dim=-1) @ vv), lse
 
+    def qkv(self, l, x, pos0):
+        """Layer l's rotated q, k and the v of hidden states x [B][n][hidden]."""
+        B, n = x.shape[0], x.shape[1]
+        Hq, Hkv, D = self.Hq, self.Hkv, self.D
+        h = self.rms(x)
+        qkv = (h.reshape(B * n, -1) @ self.wqkv[l]).reshape(B, n, Hq + 2 * Hkv, D).transpose(1, 2)
+        return (self.rope(qkv[:, :Hq], pos0).contiguous(), self.rope(qkv[:, Hq:Hq + Hkv], pos0).contiguous(),
+                qkv[:, Hq + Hkv:].contiguous())
+
     def prefill(self, tokens, attend_chunks, pos0):
         """tokens [B][n] -> (first token ids [B], final hidden state of the last token [B][hidden]).
         attend_chunks(l, q, k_own, v_own) -> O [B][Hq][n][D]."""
@@ -601,12 +610,7 @@ class RandomLlama:
         x = self.emb[tokens]                                     # [B][n][hidden]
         Hq, Hkv, D = self.Hq, self.Hkv, self.D
         for l in range(self.L):
-            h = self.rms(x)
-            qkv = (h.reshape(B * n, -1) @ self.wqkv[l]).reshape(B, n, Hq + 2 * Hkv, D).transpose(1, 2)
-            q = self.rope(qkv[:, :Hq], pos0)
-            k = self.rope(qkv[:, Hq:Hq + Hkv], pos0)
-            v = qkv[:, Hq + Hkv:]
-            o = attend_chunks(l, q.contiguous(), k.contiguous(), v.contiguous())   # [B][Hq][n][D] bf16
+            o = attend_chunks(l, *self.qkv(l, x, pos0))                     # [B][Hq][n][D] bf16
             x = x + (o.transpose(1, 2).reshape(B * n, Hq * D) @ self.wo[l]).reshape(B, n, -1)
             h = self.rms(x).reshape(B * n, -1)
             gu = h @ self.wgu[l]
@@ -692,16 +696,31 @@ def run_ttft(ctx, args, n_docs=2000, B=8, n_q=32, reps=5):
     (f_ids, f_h), (u_ids, u_h) = f_tok, u_tok
     agree = float((f_ids == u_ids).float().mean().item())
     rel = float(((f_h.float() - u_h.float()).norm() / u_h.float().norm()).item())
+    # per-layer agreement: the SAME layer-0 queries through both chunk-attention paths (the two prefills
+    # differ only there; through 32 random-weight layers the bf16 rounding differences then grow)
+    q0, k0, v0 = model.qkv(0, model.emb[tokens], pos0)
+    st.assemble(reqs, ko, vo)
+    a_f, a_u = fused_attn(0, q0, k0, v0).float(), unfused_attn(0, q0, k0, v0).float()
+    rel0 = float(((a_f - a_u).norm() / a_u.norm()).item())
+    # the chunk attention alone, timed directly (the TTFT differences above subtract two ~30 ms prefills):
+    # every layer's chunk attention for the layer-0 queries, fused vs assemble + gather + SDPA
+    fc_ms, _ = timed(lambda: [fused_attn(l, q0, k0, v0) for l in range(L)])
+    uc_ms, _ = timed(lambda: (st.assemble(reqs, ko, vo), [unfused_attn(l, q0, k0, v0) for l in range(L)]))
     res = {"workload": f"Llama-3-8B-shaped decoder with random bf16 weights (32 layers, 32 query / 8 KV heads, hidden "
                        f"4096, MLP 14336, vocab 128256), batch {B} requests x {n_q} question tokens, k={k} retrieved "
                        f"512-token chunks each from the {n_docs}-doc HBM-resident C2 store (paper ladder)",
            "ttft_ms_fused": round(f_ms, 3), "ttft_ms_unfused": round(u_ms, 3), "prefill_only_ms": round(n_ms, 3),
            "speedup_fused_vs_unfused": round(u_ms / f_ms, 3),
            "chunk_attention_ms_fused": round(f_ms - n_ms, 3), "chunk_attention_ms_unfused": round(u_ms - n_ms, 3),
+           "chunk_attention_only_ms_fused": round(fc_ms, 3), "chunk_attention_only_ms_unfused": round(uc_ms, 3),
+           "chunk_attention_only_note": "32 layers of chunk attention (+ own block and LSE merge) for fixed queries, "
+                                        "timed alone: hr_attend_layers per layer vs hr_assemble_kv + gather + SDPA",
            "first_token_agreement_fused_vs_unfused": agree,
            "final_hidden_rel_l2_fused_vs_unfused": round(rel, 5),
+           "layer0_attention_rel_l2_fused_vs_unfused": round(rel0, 6),
            "agreement_note": "random weights give near-tied logits, so argmax agreement is a weak signal; the "
-                             "relative L2 difference of the last token's final hidden state compares the paths",
+                             "layer-0 attention output (same queries, both paths) is the direct comparison; "
+                             "the final hidden state shows how rounding differences grow through 32 layers",
            "fused": "hr_attend_layers per layer (packed codes, no KV materialised) + own causal block, LSE merge",
            "unfused": "hr_assemble_kv (bf16 KV of all layers) + torch SDPA per layer over [chunk ; own] KV",
            "timing": f"CUDA events over {reps} batches after 2 warm-up batches"}

@@ -172,7 +172,9 @@ def _f32_fields(x: np.ndarray):
 
 
 def gse_slab_table(x: np.ndarray, e_bits: int, m_bits: int) -> list[int]:
-    """Array for one slab: [Emin, Emax] over nonzero normal values (R8, R9)."""
+    """Array for one slab (P:172 step 1, "exponent distribution range" of the chunk): [Emin, Emax] over the
+    nonzero fp32-normal values (R8, R9), then gse_table.  Pinned by tests/test_oracle_gse_slab.py (values
+    with known exponents: P:172's example, SURVEY §8(c)'s range, zeros, bf16/fp16 subnormals)."""
     _, ef, _ = _f32_fields(x)
     nz = ef != 0
     if not np.any(nz):

@@ -32,7 +32,10 @@ constexpr int kAsmStages = HARAG_STAGES;         // shared-memory ring depth
 constexpr int kAsmCodeStage = HARAG_CODE_STAGE;  // bytes of packed codes per stage (every scheme mix)
 constexpr int kAsmMaxTileE = kAsmCodeStage;      // elements per tile (half when a launch holds PASS16 items)
 
-constexpr int kAsmInline = 64;  // launches of <= kAsmInline descriptors carry them in the kernel parameters
+#ifndef HARAG_ASM_INLINE
+#define HARAG_ASM_INLINE 64
+#endif
+constexpr int kAsmInline = HARAG_ASM_INLINE;  // launches of <= kAsmInline descriptors carry them in the kernel parameters
 
 struct AsmParams {
   const AsmDesc* descs;      // device array, or nullptr: the descriptors are inl[0..n_desc)
@@ -47,7 +50,7 @@ struct AsmParams {
   uint32_t meta_stage;       // bytes of meta window per stage (multiple of 128)
   uint64_t n_tiles;          // n_desc * L * Hl * tiles_per_slab
   uint32_t meta_stride[6];   // per scheme, bytes per slab record
-  AsmDesc inl[kAsmInline];   // small launches (a single request, a streamed item): no descriptor H2D copy
+  AsmDesc inl[kAsmInline > 0 ? kAsmInline : 1];   // small launches (a single request, a streamed item): no descriptor H2D copy
 };
 
 // Launch the fused gather -> unpack -> dequantise -> scatter (+ hotness count).
@@ -86,7 +89,17 @@ struct AttnParams {
   float scale_log2;          // softmax scale * log2(e)
   uint64_t code_slab[6];     // per scheme, code bytes per slab
   uint32_t meta_stride[6];   // per scheme, bytes per slab meta record
+  // Key splits (flash-decoding): CTA (unit, s) attends over tiles [s n / n_split, (s+1) n / n_split) of the
+  // unit's n key tiles, writes its normalised fp32 partial O and LSE to part_o / part_lse, and the last
+  // split to finish (part_cnt[unit], zero between launches) merges the n_split partials into o / lse.
+  uint32_t n_split;          // 1: no split (part_* unused)
+  float* part_o;             // [units][n_split][128][D]
+  float* part_lse;           // [units][n_split][128]
+  uint32_t* part_cnt;        // [units], zero on entry; left zero
 };
+// splits per unit for a launch of `units` units of `n_tiles` key tiles each on `sms` SMs (1 when the
+// units alone fill the machine)
+uint32_t attend_splits(uint64_t units, uint32_t n_tiles, int sms);
 void launch_attend(const AttnParams& p, cudaStream_t stream);
 
 }  // namespace harag

@@ -361,7 +361,7 @@ __device__ __forceinline__ uint4 dec_raw8(uint32_t scheme, const uint4& c, const
 // Decode one operand tile (this decoder thread's kDecChunks chunks of 8 elements) with the scheme
 // resolved ONCE per tile: a runtime switch over compile-time-specialised loops (a per-chunk switch
 // made the decode loop branch-bound).  VMAJ: V's MN-major layout, else K's K-major layout.
-template <int DT, int SCH, bool VMAJ, uint32_t D>
+template <int DT, int SCH, bool VMAJ, uint32_t D, bool DUMP>
 __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, const uint8_t* __restrict__ smeta,
                                            const uint16_t* __restrict__ vt, uint32_t gse_m, uint32_t g_shift, uint32_t g0,
                                            uint8_t* __restrict__ dst, uint32_t dt, uint16_t* __restrict__ dump,
@@ -391,7 +391,8 @@ __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, cons
           for (int k = 0; k < 8; ++k)  // byte k zero-extended by one PRMT, then the byte-address of its entry
             h[k] = *reinterpret_cast<const uint16_t*>(reinterpret_cast<const uint8_t*>(vt) +
                                                       2u * __byte_perm(k < 4 ? raw.x : raw.y, 0u, 0x4440u | (k & 3)));
-          v = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
+          v = make_uint4(__byte_perm(h[0], h[1], 0x5410), __byte_perm(h[2], h[3], 0x5410), __byte_perm(h[4], h[5], 0x5410),
+                         __byte_perm(h[6], h[7], 0x5410));
 #else
           // fields by the magic-number conversion, scale from the slab's 2^(e+1)-entry fp32 table (at most
           // 32 entries: distinct entries sit in distinct banks), fma(f, T, +0) as hr_assemble_kv
@@ -407,15 +408,15 @@ __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, cons
         }
       }
       *reinterpret_cast<uint4*>(dst + sw128_off(key, dc, kKT)) = v;
-      if (dump) *reinterpret_cast<uint4*>(dump + key * D + dc * 8) = v;
+      if constexpr (DUMP) *reinterpret_cast<uint4*>(dump + key * D + dc * 8) = v;
     }
   }
 }
-template <int DT, bool VMAJ, uint32_t D>
+template <int DT, bool VMAJ, uint32_t D, bool DUMP>
 __device__ __forceinline__ void dec_tile(uint32_t scheme, const uint8_t* stc, const uint8_t* smeta, const uint16_t* vt,
                                          uint32_t gse_m, uint32_t g_shift, uint32_t g0, uint8_t* dst, uint32_t dt,
                                          uint16_t* dump, const uint8_t* g16, uint32_t t0) {
-#define HR_DT(S) dec_tile_s<DT, S, VMAJ, D>(stc, smeta, vt, gse_m, g_shift, g0, dst, dt, dump, g16, t0)
+#define HR_DT(S) dec_tile_s<DT, S, VMAJ, D, DUMP>(stc, smeta, vt, gse_m, g_shift, g0, dst, dt, dump, g16, t0)
   switch (scheme) {
     case HR_S_PASS16: return HR_DT(HR_S_PASS16);
     case HR_S_INT8: return HR_DT(HR_S_INT8);
@@ -585,7 +586,8 @@ __device__ long long g_tr[14][96];  // per-tile event clocks of CTA 0 (pipeline 
 #define TR(ev, j) do { } while (0)
 #endif
 
-template <int DT, uint32_t D>
+// DUMP: the kv_dump test hook (a separate instantiation: the per-chunk check cost ~4% of the issue slots)
+template <int DT, uint32_t D, bool DUMP>
 __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_constant__ AttnParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // Q (A of S = Q K^T) lives in TMEM columns [kTQ, kTQ + D/2): lane = query row, column c = elements 2c, 2c+1
@@ -608,14 +610,18 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
   DocSrc* dsrc = reinterpret_cast<DocSrc*>(stage0 + kDecGroups * kStageBytes);  // [k]
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  const uint32_t unit = blockIdx.x;  // (request, layer, head)
+  const uint32_t unit = blockIdx.x / p.n_split, split = blockIdx.x - unit * p.n_split;  // (request, layer, head), split
   const uint32_t r = unit / (p.L * p.Hl), lh = unit - r * (p.L * p.Hl);
   const uint32_t l = lh / p.Hl, h = lh - l * p.Hl;
   const uint32_t slab_i = (p.l0 + l) * p.Hl + h;  // the store's slab: layer l0 + l of the call's window
   const uint32_t hq = p.Hl * p.g;  // query heads on this rank
   const uint64_t row0 = (((uint64_t)r * p.L + l) * hq + (uint64_t)h * p.g) * p.n_q;  // first query row of the unit
   const uint32_t tiles_per_doc = p.T / kKT;
-  const uint32_t n_tiles = p.k * tiles_per_doc;
+  // this CTA's key tiles: [jt0, jt0 + n_tiles) of the unit's k * T / 64 (every split: at least one tile).
+  // Pipeline indices (buffers, phases) count from 0; addressing uses the unit's tile index jt0 + j.
+  const uint32_t n_all = p.k * tiles_per_doc;
+  const uint32_t jt0 = (uint32_t)((uint64_t)split * n_all / p.n_split);
+  const uint32_t n_tiles = (uint32_t)((uint64_t)(split + 1) * n_all / p.n_split) - jt0;
 
   if (warp == 0) {  // TMEM: S, O, Q and P buffers (kTO, kTQ, kTP)
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(tmem_slot)), "n"(kTmemCols));
@@ -638,7 +644,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       mbar_init(&ste[s], kDecWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (p.descs[0].count != nullptr && l == 0 && h == 0) {  // a1: hotness of this request's items
+    if (p.descs[0].count != nullptr && l == 0 && h == 0 && split == 0) {  // a1: hotness of this request's items
       for (uint32_t j = 0; j < 2 * p.k; ++j) {
         const AsmDesc& d = p.descs[(uint64_t)r * 2 * p.k + j];
         if (d.count) atomicAdd(d.count, 1ull);
@@ -792,6 +798,56 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
 #else
     const float ltot = __uint_as_float(tmem_ld1(t_o + lane_base + D)), inv = 1.f / ltot;
 #endif
+    if (p.n_split > 1) {
+      // split s of the unit: normalised partial O_s = O / l and LSE_s -> the workspace; the last split of the
+      // unit to arrive merges all of them: LSE = ln sum_s e^(LSE_s), O = sum_s e^(LSE_s - LSE) O_s
+      const uint64_t pu = (uint64_t)unit * p.n_split;
+      float* po = p.part_o + ((pu + split) * kRows + t) * D;
+      for (uint32_t cb = 0; cb < D; cb += 32) {
+        uint32_t ov[32];
+        tmem_ld32(t_o + lane_base + cb, ov);
+        if (t < p.M) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            __stcg(reinterpret_cast<float4*>(po + cb) + q,
+                   make_float4(__uint_as_float(ov[4 * q]) * inv, __uint_as_float(ov[4 * q + 1]) * inv,
+                               __uint_as_float(ov[4 * q + 2]) * inv, __uint_as_float(ov[4 * q + 3]) * inv));
+        }
+      }
+      if (t < p.M) __stcg(p.part_lse + (pu + split) * kRows + t, 0.69314718055994531f * (m_ref + __log2f(ltot)));
+      __threadfence();
+      named_bar(9, 32 * kSoftWarps);
+      uint32_t* last = reinterpret_cast<uint32_t*>(tmem_slot) + 1;  // broadcast slot next to the TMEM address
+      if (t == 0) *last = atomicAdd(p.part_cnt + unit, 1u) == p.n_split - 1 ? 1u : 0u;
+      named_bar(9, 32 * kSoftWarps);
+      if (*last) {
+        __threadfence();  // every split's partials (ordered before its counter increment) are visible
+        if (t == 0) p.part_cnt[unit] = 0u;  // ready for the next launch (stream-ordered)
+        if (t < p.M) {
+          const uint32_t ns = p.n_split;
+          const float* pl = p.part_lse + pu * kRows + t;  // LSE of split s at pl[s * kRows]
+          float mx = -INFINITY;
+          for (uint32_t s = 0; s < ns; ++s) mx = fmaxf(mx, __ldcg(pl + s * kRows));
+          float wsum = 0.f;
+          for (uint32_t s = 0; s < ns; ++s) wsum += __expf(__ldcg(pl + s * kRows) - mx);
+          const float lse_all = mx + __logf(wsum);
+          for (uint32_t cb = 0; cb < D; cb += 8) {
+            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+            for (uint32_t s = 0; s < ns; ++s) {
+              const float w = __expf(__ldcg(pl + s * kRows) - lse_all);
+              const float4* src = reinterpret_cast<const float4*>(p.part_o + ((pu + s) * kRows + t) * D + cb);
+              const float4 a = __ldcg(src), b = __ldcg(src + 1);
+              acc[0] += w * a.x, acc[1] += w * a.y, acc[2] += w * a.z, acc[3] += w * a.w;
+              acc[4] += w * b.x, acc[5] += w * b.y, acc[6] += w * b.z, acc[7] += w * b.w;
+            }
+            *reinterpret_cast<uint4*>(p.o + (row0 + t) * D + cb) =
+                make_uint4(pack2<DT>(acc[0], acc[1]), pack2<DT>(acc[2], acc[3]), pack2<DT>(acc[4], acc[5]),
+                           pack2<DT>(acc[6], acc[7]));
+          }
+          if (p.lse) p.lse[row0 + t] = lse_all;
+        }
+      }
+    } else {
     for (uint32_t cb = 0; cb < D; cb += 32) {
       uint32_t ov[32];
       tmem_ld32(t_o + lane_base + cb, ov);
@@ -808,6 +864,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       }
     }
     if (t < p.M && p.lse) p.lse[row0 + t] = 0.69314718055994531f * (m_ref + __log2f(ltot));
+    }
   } else if (warp < kSoftWarps + kDecGroups * kDecWarps) {
     // ------------------------------------------------------------------ decoder warps
     const uint32_t grp = (uint32_t)(warp - kSoftWarps) / kDecWarps;   // tiles j with j % kDecGroups == grp
@@ -827,9 +884,12 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       named_bar(8, nd);
     }
     uint32_t cur_slot = 0xFFFFFFFFu;
+    // (doc slot, tile within the doc) of unit tile jt0 + j, advanced without a division per tile
+    uint32_t nx_slot = (jt0 + grp) / tiles_per_doc, nx_rem = jt0 + grp - nx_slot * tiles_per_doc;
     for (uint32_t j = grp; j < n_tiles; j += kDecGroups) {
       const uint32_t b = j % kOpBufs, use = j / kOpBufs;  // use-th fill of operand buffer b
-      const uint32_t slot = j / tiles_per_doc, t0 = (j - slot * tiles_per_doc) * kKT;
+      const uint32_t slot = nx_slot, t0 = nx_rem * kKT;
+      for (nx_rem += kDecGroups; nx_rem >= tiles_per_doc; nx_rem -= tiles_per_doc) ++nx_slot;
       const DocSrc ds = dsrc[slot];
       const SchemeOf dk{ds.ks}, dv{ds.vs};
       const uint8_t *kc = ds.kc, *vc = ds.vc, *km = ds.km, *vm = ds.vm;
@@ -881,11 +941,11 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       uint8_t* svd = svb + b * vbuf;
       {
         uint16_t* dump = nullptr;  // test hook: the assembled KV [r][2][l][h][k*T][D]
-        if (p.kv_dump)
+        if constexpr (DUMP)
           dump = p.kv_dump + ((((uint64_t)r * 2) * p.L + l) * p.Hl + h) * p.k * p.T * D + ((uint64_t)slot * p.T + t0) * D;
         const uint64_t kvoff = (uint64_t)p.L * p.Hl * p.k * p.T * D;
-        dec_tile<DT, false, D>(dk.scheme, stc, smk, vtk, p.gse_m, p.g_shift, gk0, skd, dt, dump, kc, t0);
-        dec_tile<DT, true, D>(dv.scheme, stc + kSlotV, smv, vtv, p.gse_m, p.g_shift, gv0, svd, dt,
+        dec_tile<DT, false, D, DUMP>(dk.scheme, stc, smk, vtk, p.gse_m, p.g_shift, gk0, skd, dt, dump, kc, t0);
+        dec_tile<DT, true, D, DUMP>(dv.scheme, stc + kSlotV, smv, vtv, p.gse_m, p.g_shift, gv0, svd, dt,
                               dump ? dump + kvoff : nullptr, vc, t0);
       }
       fence_async_smem();
@@ -901,8 +961,16 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     // tile j's K and V code tiles -> stage slot j % kStages (TMA bulk copies, completion counted in bytes on
     // stf), once the decoder group of tile j - kStages has released the slot; L2 prefetch kPF tiles ahead
     if (lane == 0) {
-      auto tile_ptrs = [&](uint32_t j, const uint8_t*& kp, const uint8_t*& vp, uint32_t& kb, uint32_t& vb) {
-        const uint32_t slot = j / tiles_per_doc, t0 = (j - slot * tiles_per_doc) * kKT;
+      // cursors (doc slot, tile within the doc) of the next tile to copy and the next to prefetch
+      struct Cur {
+        uint32_t slot, rem;
+      };
+      auto at = [&](uint32_t j) { return Cur{(jt0 + j) / tiles_per_doc, jt0 + j - (jt0 + j) / tiles_per_doc * tiles_per_doc}; };
+      auto adv = [&](Cur& c) {
+        if (++c.rem == tiles_per_doc) c.rem = 0, ++c.slot;
+      };
+      auto tile_ptrs = [&](Cur c, const uint8_t*& kp, const uint8_t*& vp, uint32_t& kb, uint32_t& vb) {
+        const uint32_t slot = c.slot, t0 = c.rem * kKT;
         const AsmDesc* d = &p.descs[((uint64_t)r * p.k + slot) * 2];
         const uint32_t ks = d[0].scheme, vs = d[1].scheme;
         kp = d[0].codes + (uint64_t)slab_i * p.code_slab[ks] + code_bytes_of(ks, t0 * D);
@@ -910,25 +978,27 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         kb = ks == HR_S_PASS16 ? 0u : code_bytes_of(ks, kKT * D);  // PASS16 tiles are read in place
         vb = vs == HR_S_PASS16 ? 0u : code_bytes_of(vs, kKT * D);
       };
-      for (uint32_t j = 0; j < kPF && j < n_tiles; ++j) {
+      Cur cp = at(0), cq = at(0);
+      for (uint32_t j = 0; j < kPF && j < n_tiles; ++j, adv(cq)) {
         const uint8_t *kp, *vp;
         uint32_t kb, vb;
-        tile_ptrs(j, kp, vp, kb, vb);
+        tile_ptrs(cq, kp, vp, kb, vb);
         if (kb) prefetch_l2(kp, kb);
         if (vb) prefetch_l2(vp, vb);
       }
-      for (uint32_t j = 0; j < n_tiles; ++j) {
+      for (uint32_t j = 0; j < n_tiles; ++j, adv(cp)) {
         const uint32_t sl = j % kStages, u = j / kStages;
         if (j + kPF < n_tiles) {
           const uint8_t *kp, *vp;
           uint32_t kb, vb;
-          tile_ptrs(j + kPF, kp, vp, kb, vb);
+          tile_ptrs(cq, kp, vp, kb, vb);
+          adv(cq);
           if (kb) prefetch_l2(kp, kb);
           if (vb) prefetch_l2(vp, vb);
         }
         const uint8_t *kp, *vp;
         uint32_t kb, vb;
-        tile_ptrs(j, kp, vp, kb, vb);
+        tile_ptrs(cp, kp, vp, kb, vb);
         if (u >= 1) MBW(&ste[sl], (u - 1) & 1, 12, j);
         ptx_arrive_expect_tx(&stf[sl], kb + vb);
         uint8_t* dst = ring + sl * kSlotBytes;
@@ -1066,6 +1136,18 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
 
 }  // namespace
 
+uint32_t attend_splits(uint64_t units, uint32_t n_tiles, int sms) {
+  // waves x tiles per split (+ a fixed cost of ~4 tiles per CTA: TMEM, Q, pipeline fill and drain, merge)
+  if (units == 0 || sms <= 0 || units >= (uint64_t)sms) return 1;
+  uint32_t best = 1;
+  uint64_t best_t = ~0ull;
+  for (uint32_t s = 1; s <= 16 && s <= n_tiles; ++s) {
+    const uint64_t waves = (units * s + sms - 1) / sms, t = waves * ((n_tiles + s - 1) / s + 4);
+    if (t < best_t) best_t = t, best = s;
+  }
+  return best;
+}
+
 void launch_attend(const AttnParams& p, cudaStream_t st) {
   require(p.D == 64 || p.D == 128, HR_EINVAL, "attend: head_dim must be 64 or 128");
   require(p.T % kKT == 0, HR_EINVAL, "attend: tokens per chunk must be a multiple of 64");
@@ -1074,19 +1156,27 @@ void launch_attend(const AttnParams& p, cudaStream_t st) {
   const size_t smem = att_smem_bytes(p.D);
   const uint64_t units = (uint64_t)p.n_req * p.L * p.Hl;
   if (!units) return;
-  require(units < (1ull << 31), HR_EINVAL, "attend: too many units");
-  static bool init[4] = {false, false, false, false};  // per (dtype, D) instantiation
+  require(p.n_split >= 1 && p.n_split <= p.k * (p.T / kKT), HR_EINVAL, "attend: bad split count");
+  require(p.n_split == 1 || (p.part_o && p.part_lse && p.part_cnt), HR_EINVAL, "attend: split workspace missing");
+  require(units * p.n_split < (1ull << 31), HR_EINVAL, "attend: too many units");
+  static bool init[8] = {};  // per (dtype, D, dump) instantiation
   auto go = [&](void (*kern)(AttnParams), int slot) {
     if (!init[slot]) {
       HR_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)att_smem_bytes(128)));
       init[slot] = true;
     }
-    kern<<<(unsigned)units, kAttThreads2, smem, st>>>(p);
+    kern<<<(unsigned)(units * p.n_split), kAttThreads2, smem, st>>>(p);
   };
-  if (p.dtype == HR_BF16)
-    p.D == 128 ? go(attend_kernel<HR_BF16, 128>, 0) : go(attend_kernel<HR_BF16, 64>, 1);
-  else
-    p.D == 128 ? go(attend_kernel<HR_FP16, 128>, 2) : go(attend_kernel<HR_FP16, 64>, 3);
+  const bool dump = p.kv_dump != nullptr;
+#define HR_GO(DT, D, DU, SLOT) go(attend_kernel<DT, D, DU>, SLOT)
+  if (p.dtype == HR_BF16) {
+    if (p.D == 128) dump ? HR_GO(HR_BF16, 128, true, 0) : HR_GO(HR_BF16, 128, false, 1);
+    else dump ? HR_GO(HR_BF16, 64, true, 2) : HR_GO(HR_BF16, 64, false, 3);
+  } else {
+    if (p.D == 128) dump ? HR_GO(HR_FP16, 128, true, 4) : HR_GO(HR_FP16, 128, false, 5);
+    else dump ? HR_GO(HR_FP16, 64, true, 6) : HR_GO(HR_FP16, 64, false, 7);
+  }
+#undef HR_GO
   HR_CUDA(cudaGetLastError());
 }
 

@@ -113,6 +113,8 @@ Store::~Store() {
       free(backing_base);
   }
   if (delta) cudaFree(delta);
+  if (att_part) cudaFree(att_part);
+  if (att_cnt) cudaFree(att_cnt);
   if (err_flag) cudaFree(err_flag);
   if (scratch) cudaFree(scratch);
   if (gse_range) cudaFree(gse_range);
@@ -1023,6 +1025,32 @@ void Store::attend(uint32_t n_req, uint32_t k, const uint32_t* ids, uint32_t l0,
   for (uint32_t s = 0; s <= HR_S_INT4; ++s) {
     p.code_slab[s] = lay.code_bytes_slab(s);
     p.meta_stride[s] = (uint32_t)lay.meta_stride(s);
+  }
+  // key splits when the call's units alone leave SMs idle (a per-layer prefill call: n_req * Hl units)
+  if (!n_sms) HR_CUDA(cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, cfg.device));
+  const uint64_t units = (uint64_t)n_req * nl * lay.Hl;
+  const char* fs = std::getenv("HARAG_ATT_SPLIT");  // tests / tuning: force the split count
+  p.n_split = fs ? (uint32_t)std::max(1, std::atoi(fs)) : attend_splits(units, k * (lay.T / 64), n_sms);
+  p.n_split = std::min<uint32_t>(p.n_split, k * (lay.T / 64));
+  if (p.n_split > 1) {
+    const uint64_t need = units * p.n_split * 128ull * (lay.D + 1);
+    // grown rarely: cudaFree waits for the launches still reading the old buffers
+    if (need > att_part_floats) {
+      if (att_part) HR_CUDA(cudaFree(att_part));
+      att_part = nullptr;
+      HR_CUDA(cudaMalloc((void**)&att_part, need * sizeof(float)));
+      att_part_floats = need;
+    }
+    if (units > att_cnt_n) {
+      if (att_cnt) HR_CUDA(cudaFree(att_cnt));
+      att_cnt = nullptr;
+      HR_CUDA(cudaMalloc((void**)&att_cnt, units * sizeof(uint32_t)));
+      HR_CUDA(cudaMemset(att_cnt, 0, units * sizeof(uint32_t)));
+      att_cnt_n = units;
+    }
+    p.part_o = att_part;
+    p.part_lse = att_part + units * p.n_split * 128ull * lay.D;
+    p.part_cnt = att_cnt;
   }
   // q read + o written (algorithmic), beside the codes + meta counted above
   stats.bytes_hbm_alg += 2ull * 2 * n_req * nl * lay.Hl * g * n_q * lay.D;

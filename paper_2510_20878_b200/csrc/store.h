@@ -157,6 +157,12 @@ struct Store {
   int dbuf_next = 0;
   std::vector<Slot> ring;
   uint64_t req_counter = 0;
+  // hr_attend key-split workspace (grown on demand): partial O / LSE and the per-unit arrival counters
+  float* att_part = nullptr;
+  uint64_t att_part_floats = 0;
+  uint32_t* att_cnt = nullptr;
+  uint64_t att_cnt_n = 0;
+  int n_sms = 0;
 
   bool timing = false;       // CUDA events around every assemble launch (stats.kernel_ms)
   bool call_timing = false;  // CUDA events around every hr_assemble_kv call (hr_last_call_ms)

@@ -109,6 +109,20 @@ def test_attend_matches_oracle(torch_cuda, ladder, dtype, D, T, g, n_q, group):
     st.close()
 
 
+@pytest.mark.parametrize("split", [1, 2, 4, 6])
+def test_attend_key_splits(torch_cuda, split, monkeypatch):
+    """Key splits (each CTA attends over a contiguous range of the unit's 64-key tiles; the last split
+    to finish merges the normalised partials by LSE): the same bound as one CTA per unit, for a forced
+    split count (1 = no split; 6 = one tile per split, ragged tile ranges across docs at 4)."""
+    monkeypatch.setenv("HARAG_ATT_SPLIT", str(split))
+    st, ora, lay = build(torch_cuda, L=2, H=2, T=128, D=128, n_docs=8, ladder=PAPER, taus=(0.3, 0.3, 0.3),
+                         dtype="bf16")
+    reqs = synth.gen_requests(8, 3, 3, 1.1, seed=13)
+    for _ in range(2):  # the arrival counters are left zero for the next launch
+        run_case(torch_cuda, st, ora, lay, reqs, 32, 4, "bf16")
+    st.close()
+
+
 def test_attend_head_sharded_and_scale(torch_cuda):
     st, ora, lay = build(torch_cuda, L=2, H=4, T=64, D=128, n_docs=6, ladder=PAPER, taus=(0.2, 0.2, 0.2),
                          dtype="bf16", rank=1, world=2)

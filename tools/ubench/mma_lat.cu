@@ -66,6 +66,12 @@ __global__ void k(int mode, int n, int count, int nchain, long long* out) {
       if (mode == 6) unrolled<256, 8, false>(tm, a0, b0);
       if (mode == 7) unrolled<144, 4, true>(tm, a0, b0);
       if (mode == 8) unrolled<64, 32, false>(tm, a0, b0);
+      if (mode == 9) unrolled<128, 8, true>(tm, a0, b0);
+      if (mode == 10) unrolled<128, 32, true>(tm, a0, b0);
+      if (mode == 11) unrolled<64, 32, true>(tm, a0, b0);
+      if (mode == 12) unrolled<256, 32, true>(tm, a0, b0);
+      if (mode == 13) unrolled<16, 32, true>(tm, a0, b0);
+      if (mode == 14) unrolled<16, 4, true>(tm, a0, b0);
       if (threadIdx.x == 0) {
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(sa(&bar)));
         asm volatile("{\n\t.reg .pred p;\nW2:\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@!p bra W2;\n}" ::"r"(sa(&bar)),
@@ -111,6 +117,8 @@ int main() {
       {2, 64, 8, 2, "SS N64 2 chains x4"}, {2, 64, 16, 2, "SS N64 2 chains x8"}, {2, 64, 16, 4, "SS N64 4 chains x4"},
       {3, 64, 16, 2, "TS N64 2 chains x8"}, {4, 64, 8, 1, "uni SS N64 x8"}, {5, 64, 8, 1, "uni TS N64 x8"},
       {6, 256, 8, 1, "uni SS N256 x8"}, {7, 144, 4, 1, "uni TS N144 x4"}, {8, 64, 32, 1, "uni SS N64 x32"}, {0, 64, 32, 1, "SS N64 x32 dep"},   {0, 256, 32, 1, "SS N256 x32 dep"},
+      {9, 128, 8, 1, "uni TS N128 x8"}, {10, 128, 32, 1, "uni TS N128 x32"}, {11, 64, 32, 1, "uni TS N64 x32"},
+      {12, 256, 32, 1, "uni TS N256 x32"}, {13, 16, 32, 1, "uni TS N16 x32"}, {14, 16, 4, 1, "uni TS N16 x4"},
   };
   for (auto& c : cs) {
     k<<<1, 128, 65536>>>(c.mode, c.n, c.count, c.nchain, out);
