@@ -241,8 +241,9 @@ static_assert(kSoftWarps == 4, "one softmax warp per TMEM lane quadrant");
 // with <= 17 warps per CTA (>= 120 registers per thread) a softmax thread holds its whole 64-column S row
 constexpr bool kWideSoftmax = kDecGroups * kDecWarps <= 16;
 // + one MMA issuer warp + one producer warp (TMA bulk copies of the code tiles into the stage ring)
-constexpr int kAttThreads2 = 32 * (kSoftWarps + kDecGroups * kDecWarps + 2);
-constexpr int kIssuerWarp = kSoftWarps + kDecGroups * kDecWarps, kProducerWarp = kIssuerWarp + 1;
+constexpr int kAttThreads2 = 32 * (kSoftWarps + kDecGroups * kDecWarps + 3);
+// S issuer, PV issuer, producer
+constexpr int kIssuerWarp = kSoftWarps + kDecGroups * kDecWarps, kProducerWarp = kIssuerWarp + 2;
 // per decoder group: the tile's meta windows [K, V] x 2 KB
 // (<= 256 groups x 8 B), the doc's GSE-8 value tables [K, V][256] x 16-bit
 constexpr uint32_t kMetaWin = 2048;
@@ -503,6 +504,32 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// Waits of warps that are typically early (softmax for S, decoders for a free operand buffer).  The
+// suspending try_wait re-polls every few tens of cycles while the CTA's other barriers are busy (~8% of
+// the kernel's instructions), but polling with a sleep between tests measured slower (tools/prof_attend.py
+// 8: plain wait 1.215-1.218 ms, 32 ns sleeps 1.237-1.240, 64 ns 1.239-1.240, 160 ns 1.241-1.245):
+// the wake-up latency lands on the critical path.  HARAG_ATT_SLEEP = ns > 0 selects the sleeping poll.
+#ifndef HARAG_ATT_SLEEP
+#define HARAG_ATT_SLEEP 0
+#endif
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+#if HARAG_ATT_SLEEP > 0
+  while (true) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(saddr(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(HARAG_ATT_SLEEP);
+  }
+#else
+  mbar_wait(bar, parity);
+#endif
+}
 #ifdef HARAG_ATT_WATCHDOG
 // debug builds: a wait that reports (block, warp, site, parity) and traps after ~2^31 cycles
 __device__ __forceinline__ void mbar_wait_wd(uint64_t* bar, uint32_t parity, int site, uint32_t j) {
@@ -736,7 +763,11 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     for (uint32_t j = 0; j < n_tiles; ++j) {
       const uint32_t b = j % kSB, ph = (j / kSB) & 1;  // buffer, phase parity of its use
       const uint32_t s_col = tmem + b * kKT + lane_base, p_col = tmem + kTP + b * (kKT / 2) + lane_base;
+#ifdef HARAG_ATT_WATCHDOG
       MBW(&sf[b], ph, 1, j);
+#else
+      mbar_wait_sleep(&sf[b], ph);
+#endif
       if (tid == 0) TR(0, j);
       tc_after();
       // one pass at the running reference m_ref (the common case: the row maximum did not grow by > tau)
@@ -931,7 +962,12 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
 #endif
       }
       if (dt == 0) TR(6, j);
-      if (use >= 1) MBW(&kve[b], (use - 1) & 1, 3, j);  // PV_{j-3} (and S_{j-3}) done: buffer b free
+      // PV_{j-kOpBufs} (and S_{j-kOpBufs}) done: buffer b free
+#ifdef HARAG_ATT_WATCHDOG
+      if (use >= 1) MBW(&kve[b], (use - 1) & 1, 3, j);
+#else
+      if (use >= 1) mbar_wait_sleep(&kve[b], (use - 1) & 1);
+#endif
       if (dt == 0) TR(2, j);
       asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's meta share has landed
       named_bar(1 + grp, 32 * kDecWarps);               // ... and every thread's meta / value-table share
@@ -1006,117 +1042,76 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         if (vb) ptx_bulk_g2s(dst + kSlotV, vp, vb, &stf[sl]);
       }
     }
-  } else {
-    // ------------------------------------------------------------------ MMA issuer
+  } else if (warp == kIssuerWarp) {
+    // ------------------------------------------------------------------ S issuer
+    // S_j = Q K_j^T into S buffer j % kSB once K_j is decoded (kvf) and PV_{j-kSB} is done: that PV read
+    // P_{j-kSB}, whose TMEM columns softmax j is about to rewrite, and it follows softmax j-kSB, the last
+    // reader of S buffer j % kSB.  (With S and PV issued by different warps the tensor pipe no longer
+    // orders S_j behind PV_{j-kSB}; this wait does.)
     const uint32_t fmt = DT == HR_BF16 ? 1u : 0u;
     const uint32_t id_s = idesc(fmt, 0, 0, kKT, kRows);  // S[128 x 64] = Q[128 x D] . K[64 x D]^T
+    MBW(qf, 0, 4, 0);
+    for (uint32_t j = 0; j < n_tiles; ++j) {
+      const uint32_t b = j % kSB, ob = j % kOpBufs;
+      if (j >= kSB) MBW(&pfree[b], ((j - kSB) / kSB) & 1, 5, j);
+      MBW(&kvf[ob], (j / kOpBufs) & 1, 9, j);
+      TR(4, j);
+      tc_after();
+      const uint32_t ka = saddr(skb + ob * (kKT * D * 2));
+      {  // A = Q from TMEM (8 columns per k-step); K-major SW128 K
+        uint32_t a[D / 16];
+        uint64_t bd[D / 16];
+#pragma unroll
+        for (uint32_t s = 0; s < D / 16; ++s) {
+          a[s] = tmem + kTQ + s * 8;
+          bd[s] = sdesc_sw128(ka + (s >> 2) * (kKT * 128) + (s & 3) * 32);
+        }
+        mma_ts_batch<D / 16>(tmem + b * kKT, a, bd, id_s, 0u);
+      }
+      mma_commit(&sf[b]);
+      TR(9, j);
+    }
+    // the last phases of the PV-done barriers (the softmax epilogue waits only the final tile's), so no
+    // tcgen05.commit arrival is left without a waiter when the CTA exits (compute-sanitizer synccheck)
+    for (uint32_t b = 0; b < kSB && b < n_tiles; ++b) MBW(&pfree[b], ((n_tiles - 1 - b) / kSB) & 1, 12, n_tiles);
+  } else {
+    // ------------------------------------------------------------------ PV issuer
+    // O += P_j V_j (A = P_j from TMEM), and the row sum of P_j into O's column D, once P_j is ready; the
+    // commits free operand buffer j % kOpBufs (kve: S_j completed before softmax j wrote P_j) and P buffer
+    // j % kSB (pfree).  A warp of its own: the S issuer's MMA batches no longer delay PV (the issue of a
+    // batch of 8 MMAs takes ~500 cycles).
+    const uint32_t fmt = DT == HR_BF16 ? 1u : 0u;
     const uint32_t id_o = idesc(fmt, 0, 1, D, kRows);    // O[128 x D] += P[128 x 64] . V[64 x D] (V MN-major SW128)
     const uint32_t id_1 = idesc(fmt, 0, 1, 16, kRows);   // O[128 x D..D+15] += P . ones
     const uint32_t oa = saddr(sones);
-    // Event-driven issue: S_j needs operands j (kvf) and its TMEM buffer free (softmax of j-2 done, i.e.
-    // PV_{j-2} already issued); PV_j needs P_j (pf).  Whichever is ready goes first, so PV_{j-1} (which
-    // frees the operand buffer decode j+1 waits for) never waits behind the decode of tile j.
-    uint32_t ns = 0, npv = 0;
-    MBW(qf, 0, 4, 0);
-#ifdef HARAG_ATT_WATCHDOG
-    long long wd0 = clock64();
-#endif
-    while (npv < n_tiles) {
-#ifdef HARAG_ATT_WATCHDOG
-      if (clock64() - wd0 > (1ll << 33)) {
-        printf("WATCHDOG MMA block %d ns %u npv %u n %u\n", (int)blockIdx.x, ns, npv, n_tiles);
-        __trap();
-      }
-#endif
-      // Blocking waits where only one event can come next (no polling: a spinning issuer took 10% of the
-      // SM's issue slots): after S_{j+1} only PV_j can follow; with every issued S matched by its PV only
-      // S can.  With both possible, PV goes first if P is ready, else whichever event comes first.
-      const bool s_ok = ns < n_tiles && ns <= npv + kSB - 1, pv_ok = npv < ns;
-      bool do_s;
-      if (!pv_ok) {
-        MBW(&kvf[ns % kOpBufs], (ns / kOpBufs) & 1, 9, ns);
-        do_s = true;
-      } else if (!s_ok) {
-        MBW(&pf[npv % kSB], (npv / kSB) & 1, 10, npv);
-        do_s = false;
-      } else {
-        while (true) {
-#ifndef HARAG_ATT_S_FIRST  // PV_j first when P_j is ready (measured 1.30 vs 1.32 ms for S-first)
-          if (mbar_test_u(&pf[npv % kSB], (npv / kSB) & 1)) { do_s = false; break; }
-          if (mbar_wait_hint_u(&kvf[ns % kOpBufs], (ns / kOpBufs) & 1, 100)) { do_s = true; break; }
-#else
-          if (mbar_test_u(&kvf[ns % kOpBufs], (ns / kOpBufs) & 1)) { do_s = true; break; }
-          if (mbar_wait_hint_u(&pf[npv % kSB], (npv / kSB) & 1, 100)) { do_s = false; break; }
-#endif
+    for (uint32_t j = 0; j < n_tiles; ++j) {
+      const uint32_t bb = j % kSB, ob = j % kOpBufs;
+      MBW(&pf[bb], (j / kSB) & 1, 10, j);
+      TR(5, j);
+      tc_after();
+      const uint32_t va = saddr(svb + ob * vbuf);
+      {  // A = P_j from TMEM: 16 keys = 8 columns per k-step
+        uint32_t a[kKT / 16];
+        uint64_t bd[kKT / 16];
+#pragma unroll
+        for (uint32_t s = 0; s < kKT / 16; ++s) {
+          a[s] = tmem + kTP + bb * (kKT / 2) + s * 8;
+          bd[s] = sdesc_sw128_mn(va + s * 2048, kKT * 128);  // 16 keys = two 8-key row groups
         }
-      }
-      if (do_s) {
-        const uint32_t b = ns % kSB, ob = ns % kOpBufs;
-        TR(4, ns);
-        tc_after();
-        const uint32_t ka = saddr(skb + ob * (kKT * D * 2));
-        {  // A = Q from TMEM (8 columns per k-step); K-major SW128 K
-          uint32_t a[D / 16];
-          uint64_t bd[D / 16];
-#pragma unroll
-          for (uint32_t s = 0; s < D / 16; ++s) {
-            a[s] = tmem + kTQ + s * 8;
-            bd[s] = sdesc_sw128(ka + (s >> 2) * (kKT * 128) + (s & 3) * 32);
-          }
-          mma_ts_batch<D / 16>(tmem + b * kKT, a, bd, id_s, 0u);
-        }
-        mma_commit(&sf[b]);
-#ifdef HARAG_ATT_WATCHDOG
-        wd0 = clock64();
-#endif
-#ifdef HARAG_ATT_MMASYNC
-        MBW(&sf[b], (ns / kSB) & 1, 5, ns);  // pipeline study: time the MMA alone
-        TR(12, ns);
-#endif
-        ++ns;
-      } else {
-        const uint32_t bb = npv % kSB, ob = npv % kOpBufs;
-        TR(5, npv);
-        tc_after();
-        const uint32_t va = saddr(svb + ob * vbuf);
-        {  // A = P_npv from TMEM: 16 keys = 8 columns per k-step
-          uint32_t a[kKT / 16];
-          uint64_t bd[kKT / 16];
-#pragma unroll
-          for (uint32_t s = 0; s < kKT / 16; ++s) {
-            a[s] = tmem + kTP + bb * (kKT / 2) + s * 8;
-            bd[s] = sdesc_sw128_mn(va + s * 2048, kKT * 128);  // 16 keys = two 8-key row groups
-          }
-          mma_ts_batch<kKT / 16>(t_o, a, bd, id_o, npv > 0 ? 1u : 0u);
-#pragma unroll
-          for (uint32_t s = 0; s < kKT / 16; ++s) bd[s] = sdesc(oa + s * 2 * 2 * 128, 2 * 128, 128);
+        mma_ts_batch<kKT / 16>(t_o, a, bd, id_o, j > 0 ? 1u : 0u);
 #ifndef HARAG_ATT_SOFTMAX_SUM
-          mma_ts_batch<kKT / 16>(t_o + D, a, bd, id_1, npv > 0 ? 1u : 0u);
+#pragma unroll
+        for (uint32_t s = 0; s < kKT / 16; ++s) bd[s] = sdesc(oa + s * 2 * 2 * 128, 2 * 128, 128);
+        mma_ts_batch<kKT / 16>(t_o + D, a, bd, id_1, j > 0 ? 1u : 0u);
 #endif
-        }
-        mma_commit(&kve[ob]);
-        mma_commit(&pfree[bb]);
-#ifdef HARAG_ATT_WATCHDOG
-        wd0 = clock64();
-#endif
-#ifdef HARAG_ATT_MMASYNC
-        MBW(&pfree[bb], (npv / kSB) & 1, 6, npv);
-        TR(13, npv);
-#endif
-        ++npv;
       }
+      mma_commit(&kve[ob]);
+      mma_commit(&pfree[bb]);
+      TR(10, j);
     }
     // consume the last phase of every operand buffer's "PV done" barrier: the decoders only wait for a
-    // buffer they reuse, so without this the final tcgen05.commit arrivals would have no waiter when the
-    // CTA exits (compute-sanitizer synccheck: "missing wait")
-    for (uint32_t b = 0; b < kOpBufs && b < n_tiles; ++b)
-      MBW(&kve[b], ((n_tiles - 1 - b) / kOpBufs) & 1, 11, n_tiles);
-    // ... and of the S-ready / PV-done barriers it committed to (the softmax warps wait on them too)
-    for (uint32_t b = 0; b < kSB && b < n_tiles; ++b) {
-      const uint32_t last = (n_tiles - 1 - b) / kSB;
-      MBW(&sf[b], last & 1, 12, n_tiles);
-      MBW(&pfree[b], last & 1, 12, n_tiles);
-    }
+    // buffer they reuse (compute-sanitizer synccheck: "missing wait" otherwise)
+    for (uint32_t b = 0; b < kOpBufs && b < n_tiles; ++b) MBW(&kve[b], ((n_tiles - 1 - b) / kOpBufs) & 1, 11, n_tiles);
   }
   tc_before();
   __syncthreads();

@@ -849,9 +849,11 @@ void Store::fill_host(uint32_t item, uint8_t* dst) {
 
 void Store::host_copy(void* dst, const void* src, size_t n) {
   if (!copy_pool) {
-    // every host core but the calling thread's (measured: one thread copies pageable -> pinned at
-    // ~8.6 GB/s on the B200 host, 16 threads at ~88 GB/s, tools/hostcopy.cpp)
-    unsigned t = std::max(1u, std::thread::hardware_concurrency()) - 1;
+    // half the host cores (+ the calling thread): the bounce copies share host DRAM with the DMA they
+    // feed, so more copy threads starve the link (tools/bounce_bench.cpp on the 16-core B200 host, whole
+    // 16.5 MiB items, non-temporal stores, 3 runs each: 7 workers 45.4-45.8 GB/s on the link, 9 workers
+    // 50.5-51.2, 11 workers 48.1-48.8, 15 workers 44.1-46.8; pinned DMA alone 54.8)
+    unsigned t = std::max(1u, std::thread::hardware_concurrency()) / 2 + 1;
     if (const char* e = std::getenv("HARAG_COPY_THREADS")) t = (unsigned)std::atoi(e);
     const int spin = std::getenv("HARAG_POOL_SPIN") ? std::atoi(std::getenv("HARAG_POOL_SPIN")) : 2000;
     const bool nt = !(std::getenv("HARAG_COPY_NT") && std::atoi(std::getenv("HARAG_COPY_NT")) == 0);

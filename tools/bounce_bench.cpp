@@ -38,11 +38,28 @@ int main(int argc, char** argv) {
   for (size_t i = 0; i < n_items; ++i) cudaMemcpyAsync(dev[i % slots], bounce[i % slots], item, cudaMemcpyHostToDevice, st);
   cudaStreamSynchronize(st);
   printf("pinned DMA alone: %.1f GB/s\n", n_items * item / (now() - t0) / 1e9);
-  for (unsigned workers : {7u, 11u, 15u}) {
+  // the driver's own staging of a pageable source (cudaMemcpyAsync straight from pageable memory)
+  t0 = now();
+  for (size_t i = 0; i < n_items / 4; ++i)
+    cudaMemcpyAsync(dev[i % slots], src + (i % 256) * item, item, cudaMemcpyHostToDevice, st);
+  cudaStreamSynchronize(st);
+  printf("pageable cudaMemcpyAsync (driver staging): %.1f GB/s\n", n_items / 4 * item / (now() - t0) / 1e9);
+  {  // host copy alone (no DMA), whole items, all workers
+    harag::CopyPool pool(15, 2000, true);
+    t0 = now();
+    for (size_t i = 0; i < n_items; ++i) pool.copy(bounce[i % slots], src + (i % 256) * item, item);
+    printf("host bounce copy alone (16 threads, NT): %.1f GB/s\n", n_items * item / (now() - t0) / 1e9);
+  }
+  const bool sweep_pieces = getenv("BB_PIECES") != nullptr;
+  const int reps = getenv("BB_REPS") ? atoi(getenv("BB_REPS")) : 1;
+  for (int rep = 0; rep < reps; ++rep)
+  for (unsigned workers : {3u, 5u, 7u, 9u, 11u, 15u}) {
     for (int nt : {0, 1}) {
       harag::CopyPool pool(workers, 2000, nt != 0);
       printf("-- %s copies\n", nt ? "non-temporal" : "memcpy");
-      for (size_t piece : {(size_t)4 << 20, (size_t)8 << 20, item}) {
+      std::vector<size_t> pieces = {item};
+      if (sweep_pieces) pieces = {(size_t)4 << 20, (size_t)8 << 20, item};
+      for (size_t piece : pieces) {
         std::vector<bool> used(slots, false);
         double t1 = now();
         double host_copy = 0;

@@ -18,3 +18,8 @@ print(f"S issue -> S seen         {(sf - si)[s].mean():8.0f}")
 print(f"P ready -> PV issue       {(pv - pf)[s].mean():8.0f}")
 print(f"operands ready -> S issue {(si - kvf)[s].mean():8.0f}")
 print(f"decode (loads in -> kvf)  {(kvf - li)[s].mean():8.0f}   stage (start -> loads in) {(li - ds)[s].mean():6.0f}")
+sid, pvd = a[:, 10], a[:, 11]
+print(f"S issue call -> returned   {(sid - si)[s].mean():8.0f}   PV issue call -> returned {(pvd - pv)[s].mean():6.0f}")
+print(f"PV_j issued -> S_j+2 issue {(si[2:] - pvd[:-2])[s].mean():8.0f}   S_j returned -> PV_j-1 issue {(pv[:-1] - sid[1:])[s].mean():6.0f}")
+kw = a[:, 3]
+print(f"decoder: start -> kve ok   {(kw - ds)[s].mean():8.0f}   kve ok -> stage landed {(li - kw)[s].mean():6.0f}")
