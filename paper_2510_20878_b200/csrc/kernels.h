@@ -50,6 +50,14 @@ struct AsmParams {
   uint32_t meta_stage;       // bytes of meta window per stage (multiple of 128)
   uint64_t n_tiles;          // n_desc * L * Hl * tiles_per_slab
   uint32_t meta_stride[6];   // per scheme, bytes per slab record
+  // Tail balancing: tiles [n_tiles - dyn_tiles, n_tiles) are claimed in chunks of dyn_chunk through an
+  // atomic counter (sched[0]; sched[1] counts producers done, the last one zeroes both), the rest are
+  // split in blocks.  sched == nullptr: blocked split only.
+  uint32_t* sched;           // [4]: u64 claim counter, u32 done count (zero between launches), or nullptr
+  uint32_t dyn_pct;          // input: percent of the tiles claimed dynamically (0: blocked split only)
+  uint32_t dyn_per_cta;      // input: dynamic chunks per CTA (sets the chunk size)
+  uint64_t dyn_tiles;        // filled in by launch_assemble
+  uint32_t dyn_chunk;
   AsmDesc inl[kAsmInline > 0 ? kAsmInline : 1];   // small launches (a single request, a streamed item): no descriptor H2D copy
 };
 

@@ -138,64 +138,91 @@ size_t smem_bytes(uint32_t meta_stage) {
   return (size_t)kAsmStages * (kAsmCodeStage + meta_stage) + kAsmStages * sizeof(TileHdr) + 2 * kAsmStages * 8;
 }
 
-// Blocked distribution: CTA b owns tiles [b*n/grid, (b+1)*n/grid) — consecutive tiles of one slab /
-// item, so the producer reloads a descriptor only when it crosses an item.
+// Blocked distribution of the first n_tiles - dyn_tiles tiles: CTA b owns [b*n/grid, (b+1)*n/grid) —
+// consecutive tiles of one slab / item, so the producer reloads a descriptor only when it crosses an item.
+// The last dyn_tiles are claimed in chunks through p.sched (the CTAs that finish their block first take
+// more of them: the static split left the slowest CTA ~5% behind on a single request).
 __device__ __forceinline__ void my_tiles(const AsmParams& p, uint64_t& t0, uint64_t& t1) {
-  t0 = p.n_tiles * blockIdx.x / gridDim.x;
-  t1 = p.n_tiles * (blockIdx.x + 1) / gridDim.x;
+  const uint64_t ns = p.sched ? p.n_tiles - p.dyn_tiles : p.n_tiles;
+  t0 = ns * blockIdx.x / gridDim.x;
+  t1 = ns * (blockIdx.x + 1) / gridDim.x;
 }
 
 // ------------------------------------------------------------------ producer
 __device__ __forceinline__ void produce(const AsmParams& p, const Smem& sm) {
-  uint64_t t0, t1;
-  my_tiles(p, t0, t1);
   const uint32_t per_desc = p.L * p.Hl * p.tiles_per_slab;
   const uint32_t n_slabs = p.L * p.Hl;
-  uint32_t di = (uint32_t)(t0 / per_desc);
-  uint32_t r = (uint32_t)(t0 - (uint64_t)di * per_desc);
-  uint32_t slab_i = r / p.tiles_per_slab;
-  uint32_t sub = r - slab_i * p.tiles_per_slab;
-  AsmDesc d = p.descs ? p.descs[di] : p.inl[di];
-  for (uint64_t i = 0; i < t1 - t0; ++i) {
-    const int stage = (int)(i % kAsmStages);
-    if (i >= kAsmStages) mbar_wait(&sm.empty()[stage], (uint32_t)(((i / kAsmStages) - 1) & 1));
-    const uint32_t e0 = sub * p.tile_e;
-    const uint32_t n_el = min(p.tile_e, p.slab - e0);
-    const uint32_t cb = code_bytes(d.scheme, n_el);
-    const uint8_t* csrc = d.codes + (uint64_t)slab_i * code_bytes(d.scheme, p.slab) + code_bytes(d.scheme, e0);
-    uint32_t mb = 0, moff = 0;
-    const uint8_t* msrc = nullptr;
-    if (d.scheme == HR_S_INT8 || d.scheme == HR_S_INT4) {
-      const uint32_t me = d.scheme == HR_S_INT8 ? 4u : 8u;
-      const uint32_t g0 = e0 >> p.g_shift, g1 = (e0 + n_el + p.G - 1) >> p.g_shift;
-      const uint32_t b0 = (g0 * me) & ~15u, b1 = (g1 * me + 15u) & ~15u;
-      msrc = d.meta + (uint64_t)slab_i * p.meta_stride[d.scheme] + b0;
-      mb = b1 - b0;
-      moff = g0 * me - b0;
-    } else if (d.scheme == HR_S_GSE8) {  // whole record: shared-exponent array + fp32 decode table
-      msrc = d.meta + (uint64_t)slab_i * p.meta_stride[d.scheme];
-      mb = p.meta_stride[d.scheme];
-    }
-    TileHdr& h = sm.hdr()[stage];
-    h.out = d.out + 2ull * (((uint64_t)slab_i * p.k + d.slot) * p.slab + e0);
-    h.n_el = n_el;
-    h.scheme = d.scheme;
-    h.meta_off = moff;
-    h.goff = e0 & (p.G - 1);
-    if (d.count != nullptr && slab_i == 0 && sub == 0) atomicAdd(d.count, 1ull);  // a1
-    uint64_t* full = &sm.full()[stage];
-    mbar_arrive_expect_tx(full, cb + mb);  // release: the header is visible with the phase flip
-    bulk_g2s(sm.codes(stage), csrc, cb, full);
-    if (mb) bulk_g2s(sm.meta(stage), msrc, mb, full);
-    if (++sub == p.tiles_per_slab) {  // advance (sub, slab, descriptor) without divisions
-      sub = 0;
-      if (++slab_i == n_slabs) {
-        slab_i = 0;
-        if (i + 1 < t1 - t0) {
-          ++di;
-          d = p.descs ? p.descs[di] : p.inl[di];
+  uint64_t i = 0;  // stage sequence number across every range this CTA produces
+  auto range = [&](uint64_t t0, uint64_t t1) {
+    if (t1 <= t0) return;
+    uint32_t di = (uint32_t)(t0 / per_desc);
+    uint32_t r = (uint32_t)(t0 - (uint64_t)di * per_desc);
+    uint32_t slab_i = r / p.tiles_per_slab;
+    uint32_t sub = r - slab_i * p.tiles_per_slab;
+    AsmDesc d = p.descs ? p.descs[di] : p.inl[di];
+    for (uint64_t t = t0; t < t1; ++t, ++i) {
+      const int stage = (int)(i % kAsmStages);
+      if (i >= kAsmStages) mbar_wait(&sm.empty()[stage], (uint32_t)(((i / kAsmStages) - 1) & 1));
+      const uint32_t e0 = sub * p.tile_e;
+      const uint32_t n_el = min(p.tile_e, p.slab - e0);
+      const uint32_t cb = code_bytes(d.scheme, n_el);
+      const uint8_t* csrc = d.codes + (uint64_t)slab_i * code_bytes(d.scheme, p.slab) + code_bytes(d.scheme, e0);
+      uint32_t mb = 0, moff = 0;
+      const uint8_t* msrc = nullptr;
+      if (d.scheme == HR_S_INT8 || d.scheme == HR_S_INT4) {
+        const uint32_t me = d.scheme == HR_S_INT8 ? 4u : 8u;
+        const uint32_t g0 = e0 >> p.g_shift, g1 = (e0 + n_el + p.G - 1) >> p.g_shift;
+        const uint32_t b0 = (g0 * me) & ~15u, b1 = (g1 * me + 15u) & ~15u;
+        msrc = d.meta + (uint64_t)slab_i * p.meta_stride[d.scheme] + b0;
+        mb = b1 - b0;
+        moff = g0 * me - b0;
+      } else if (d.scheme == HR_S_GSE8) {  // whole record: shared-exponent array + fp32 decode table
+        msrc = d.meta + (uint64_t)slab_i * p.meta_stride[d.scheme];
+        mb = p.meta_stride[d.scheme];
+      }
+      TileHdr& h = sm.hdr()[stage];
+      h.out = d.out + 2ull * (((uint64_t)slab_i * p.k + d.slot) * p.slab + e0);
+      h.n_el = n_el;
+      h.scheme = d.scheme;
+      h.meta_off = moff;
+      h.goff = e0 & (p.G - 1);
+      if (d.count != nullptr && slab_i == 0 && sub == 0) atomicAdd(d.count, 1ull);  // a1
+      uint64_t* full = &sm.full()[stage];
+      mbar_arrive_expect_tx(full, cb + mb);  // release: the header is visible with the phase flip
+      bulk_g2s(sm.codes(stage), csrc, cb, full);
+      if (mb) bulk_g2s(sm.meta(stage), msrc, mb, full);
+      if (++sub == p.tiles_per_slab) {  // advance (sub, slab, descriptor) without divisions
+        sub = 0;
+        if (++slab_i == n_slabs) {
+          slab_i = 0;
+          if (t + 1 < t1) {
+            ++di;
+            d = p.descs ? p.descs[di] : p.inl[di];
+          }
         }
       }
+    }
+  };
+  uint64_t t0, t1;
+  my_tiles(p, t0, t1);
+  range(t0, t1);
+  if (p.sched) {
+    const uint64_t base = p.n_tiles - p.dyn_tiles;
+    while (true) {
+      const uint64_t c = atomicAdd(reinterpret_cast<unsigned long long*>(p.sched), (unsigned long long)p.dyn_chunk);
+      if (c >= p.dyn_tiles) break;
+      range(base + c, base + min(c + p.dyn_chunk, p.dyn_tiles));
+    }
+    // end of this CTA's tiles: a header with n_el = 0 in the next stage
+    const int stage = (int)(i % kAsmStages);
+    if (i >= kAsmStages) mbar_wait(&sm.empty()[stage], (uint32_t)(((i / kAsmStages) - 1) & 1));
+    sm.hdr()[stage].n_el = 0;
+    mbar_arrive(&sm.full()[stage]);
+    // the last producer to finish claiming resets the counter for the next launch on the stream
+    __threadfence();
+    if (atomicAdd(reinterpret_cast<unsigned int*>(p.sched) + 2, 1u) == gridDim.x - 1) {
+      *reinterpret_cast<volatile unsigned long long*>(p.sched) = 0ull;
+      reinterpret_cast<volatile unsigned int*>(p.sched)[2] = 0u;
     }
   }
 }
@@ -297,10 +324,11 @@ __device__ __forceinline__ void consume(const AsmParams& p, const Smem& sm, int 
   const int ctid = warp * 32 + lane;
   uint64_t t0, t1;
   my_tiles(p, t0, t1);
-  for (uint64_t i = 0; i < t1 - t0; ++i) {
+  for (uint64_t i = 0; p.sched || i < t1 - t0; ++i) {
     const int stage = (int)(i % kAsmStages);
     mbar_wait(&sm.full()[stage], (uint32_t)((i / kAsmStages) & 1));
     const TileHdr h = sm.hdr()[stage];
+    if (h.n_el == 0) break;  // the producer's end marker (tail-balanced launches)
     const uint8_t* codes = sm.codes(stage);
     const uint8_t* meta = sm.meta(stage);
     switch (h.scheme) {
@@ -412,6 +440,13 @@ void launch_assemble(AsmParams p, uint32_t scheme_mask, cudaStream_t st, int gri
   const size_t smem = smem_bytes(p.meta_stage);
   uint64_t grid = grid_ctas > 0 ? (uint64_t)grid_ctas : (uint64_t)g_num_sms * ctas_per_sm(smem);
   if (grid > p.n_tiles) grid = p.n_tiles;
+  // tail balancing: the last dyn_pct % of the tiles in ~dyn_per_cta chunks per CTA
+  if (p.sched && p.dyn_pct && p.n_tiles >= 4 * grid) {
+    p.dyn_tiles = p.n_tiles * p.dyn_pct / 100;
+    p.dyn_chunk = (uint32_t)std::max<uint64_t>(1, p.dyn_tiles / (grid * std::max(1u, p.dyn_per_cta)));
+  } else {
+    p.sched = nullptr;
+  }
   if (p.dtype == HR_BF16)
     assemble_kv_kernel<HR_BF16><<<(unsigned)grid, kAsmThreads, smem, st>>>(p);
   else

@@ -763,7 +763,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     for (uint32_t j = 0; j < n_tiles; ++j) {
       const uint32_t b = j % kSB, ph = (j / kSB) & 1;  // buffer, phase parity of its use
       const uint32_t s_col = tmem + b * kKT + lane_base, p_col = tmem + kTP + b * (kKT / 2) + lane_base;
-#ifdef HARAG_ATT_WATCHDOG
+#if defined(HARAG_ATT_WATCHDOG)
       MBW(&sf[b], ph, 1, j);
 #else
       mbar_wait_sleep(&sf[b], ph);
@@ -962,16 +962,20 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
 #endif
       }
       if (dt == 0) TR(6, j);
-      // PV_{j-kOpBufs} (and S_{j-kOpBufs}) done: buffer b free
+      // One warp of the group waits for operand buffer b (PV_{j-kOpBufs} and S_{j-kOpBufs} done) and for the
+      // stage slot's TMA bytes; the named barrier releases the other three (bar.sync does not issue while
+      // blocked, the suspending mbarrier wait re-polls: four waiting warps took ~4% of the issue slots).
+      if (dt < 32) {
 #ifdef HARAG_ATT_WATCHDOG
-      if (use >= 1) MBW(&kve[b], (use - 1) & 1, 3, j);
+        if (use >= 1) MBW(&kve[b], (use - 1) & 1, 3, j);
 #else
-      if (use >= 1) mbar_wait_sleep(&kve[b], (use - 1) & 1);
+        if (use >= 1) mbar_wait_sleep(&kve[b], (use - 1) & 1);
 #endif
-      if (dt == 0) TR(2, j);
+        if (dt == 0) TR(2, j);
+        MBW(&stf[j % kStages], (j / kStages) & 1, 11, j);  // the code tiles have landed
+      }
       asm volatile("cp.async.wait_all;" ::: "memory");  // this thread's meta share has landed
       named_bar(1 + grp, 32 * kDecWarps);               // ... and every thread's meta / value-table share
-      MBW(&stf[j % kStages], (j / kStages) & 1, 11, j);  // the code tiles have landed
       if (dt == 0) TR(7, j);
       uint8_t* skd = skb + b * (kKT * D * 2);
       uint8_t* svd = svb + b * vbuf;

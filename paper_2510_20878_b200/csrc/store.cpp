@@ -74,6 +74,8 @@ Store::Store(const hr_store_config& c) : cfg(c), lay(make_layout(c)) {
   if (cfg.demand_mode) cfg.keep_backing = 1;  // the backing plays the paper's disk: every item has a copy
   slots = cfg.staging_slots;  // 0: sized in ensure_ring once the largest item is known
   if (const char* g = std::getenv("HARAG_ASM_GRID")) grid_override = std::atoi(g);  // tuning experiments
+  if (const char* g = std::getenv("HARAG_ASM_DYN")) asm_dyn_pct = (uint32_t)std::atoi(g);
+  if (const char* g = std::getenv("HARAG_ASM_CHUNKS")) asm_dyn_per_cta = (uint32_t)std::atoi(g);
   HR_CUDA(cudaSetDevice(cfg.device));
   HR_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
   if (cfg.numa_bind) local_cpus = gpu_local_cpus(cfg.device);
@@ -114,6 +116,7 @@ Store::~Store() {
   }
   if (delta) cudaFree(delta);
   if (att_part) cudaFree(att_part);
+  if (asm_sched) cudaFree(asm_sched);
   if (att_cnt) cudaFree(att_cnt);
   if (err_flag) cudaFree(err_flag);
   if (scratch) cudaFree(scratch);
@@ -473,6 +476,15 @@ void Store::launch(const AsmDesc* dev_descs, const AsmDesc* host_descs, uint32_t
   p.dtype = lay.dtype;
   p.slab = (uint32_t)lay.slab();
   for (uint32_t s = 0; s <= HR_S_INT4; ++s) p.meta_stride[s] = (uint32_t)lay.meta_stride(s);
+  if (asm_dyn_pct) {
+    if (!asm_sched) {
+      HR_CUDA(cudaMalloc((void**)&asm_sched, 64 * 16));
+      HR_CUDA(cudaMemset(asm_sched, 0, 64 * 16));
+    }
+    p.sched = asm_sched + 4 * (asm_sched_next++ % 64);
+    p.dyn_pct = asm_dyn_pct;
+    p.dyn_per_cta = asm_dyn_per_cta;
+  }
   cudaEvent_t a = nullptr, b = nullptr;
   if (timing) {
     HR_CUDA(cudaEventCreate(&a));

@@ -163,6 +163,10 @@ struct Store {
   uint32_t* att_cnt = nullptr;
   uint64_t att_cnt_n = 0;
   int n_sms = 0;
+  // assemble tail balancing: per-launch claim counters (64 slots of 16 B, zero between launches)
+  uint32_t* asm_sched = nullptr;
+  uint32_t asm_sched_next = 0;
+  uint32_t asm_dyn_pct = 25, asm_dyn_per_cta = 8;
 
   bool timing = false;       // CUDA events around every assemble launch (stats.kernel_ms)
   bool call_timing = false;  // CUDA events around every hr_assemble_kv call (hr_last_call_ms)
