@@ -82,6 +82,12 @@ struct QBatch {
   uint64_t code_slab[6], meta_off[6];
   uint32_t meta_stride[6];
   int* err;
+  // tail balancing (as assemble_kv_kernel): the last dyn_tiles tiles are claimed in chunks of dyn_chunk
+  // through sched[0..1] (u64 counter; sched[2] counts producers done, the last one zeroes both); the rest
+  // are split in blocks.  sched == nullptr: blocked split only.
+  uint32_t* sched;
+  uint64_t dyn_tiles;
+  uint32_t dyn_chunk;
 };
 
 struct QHdr {
@@ -458,44 +464,70 @@ __device__ __forceinline__ void gse_write_record(uint8_t* meta, uint32_t stride,
 // ------------------------------------------------------------------ producer
 template <int MODE>
 __device__ __forceinline__ void q_produce(const QBatch& p, const QSmem& sm, int lane) {
-  const uint64_t t0 = p.n_tiles * blockIdx.x / gridDim.x, t1 = p.n_tiles * (blockIdx.x + 1) / gridDim.x;
   const uint32_t per_job = p.L * p.Hl * p.tiles_per_slab;
-  uint32_t j = (uint32_t)(t0 / per_job);
-  uint32_t r = (uint32_t)(t0 - (uint64_t)j * per_job);
-  uint32_t slab_i = r / p.tiles_per_slab, sub = r - slab_i * p.tiles_per_slab;
-  uint32_t l = slab_i / p.Hl, hl = slab_i - l * p.Hl;
   const int m = (int)p.gse_m, nmax = 1 << (7 - m);
-  for (uint64_t i = 0; i < t1 - t0; ++i) {
-    const int stage = (int)(i % kQStages);
+  uint64_t i = 0;  // stage sequence number across this CTA's ranges
+  auto range = [&](uint64_t t0, uint64_t t1) {
+    if (t1 <= t0) return;
+    uint32_t j = (uint32_t)(t0 / per_job);
+    uint32_t r = (uint32_t)(t0 - (uint64_t)j * per_job);
+    uint32_t slab_i = r / p.tiles_per_slab, sub = r - slab_i * p.tiles_per_slab;
+    uint32_t l = slab_i / p.Hl, hl = slab_i - l * p.Hl;
+    for (uint64_t t = t0; t < t1; ++t, ++i) {
+      const int stage = (int)(i % kQStages);
+      if (i >= kQStages) mbar_wait(&sm.empty()[stage], (uint32_t)(((i / kQStages) - 1) & 1));
+      const QJob& jb = p.jobs[j];
+      const uint32_t scheme = jb.scheme;
+      const uint32_t e0 = sub * p.tile_e;
+      const uint32_t n_el = min(p.tile_e, p.slab - e0);
+      uint8_t* meta = jb.dst + p.meta_off[scheme] + (uint64_t)slab_i * p.meta_stride[scheme];
+      if (MODE == MODE_ENCODE && scheme == HR_S_GSE8) {
+        const GseArr a = gse_array(jb.range + 2 * slab_i, m, nmax);
+        gse_build_table(sm.gtab(stage), a, m, lane);
+        if (sub == 0) gse_write_record(meta, p.meta_stride[HR_S_GSE8], a, m, nmax, lane);
+        __syncwarp();
+      }
+      if (lane == 0) {
+        QHdr& h = sm.hdr()[stage];
+        h.codes = jb.dst + (uint64_t)slab_i * p.code_slab[scheme] + code_bytes(scheme, e0);
+        h.meta = scheme == HR_S_INT8 ? meta + 4 * (e0 >> p.g_shift) : scheme == HR_S_INT4 ? meta + 8 * (e0 >> p.g_shift) : meta;
+        h.range = jb.range ? jb.range + 2 * slab_i : nullptr;
+        h.n_el = n_el;
+        h.scheme = scheme;
+        uint64_t* full = &sm.full()[stage];
+        mbar_arrive_expect_tx(full, 2 * n_el);  // release: header and table visible with the phase flip
+        bulk_g2s(sm.tile(stage), jb.src + ((uint64_t)(l * p.H + p.h0 + hl) * p.slab + e0), 2 * n_el, full);
+      }
+      if (++sub == p.tiles_per_slab) {  // advance (sub, head, layer, job) without divisions
+        sub = 0;
+        ++slab_i;
+        if (++hl == p.Hl) {
+          hl = 0;
+          if (++l == p.L) l = 0, slab_i = 0, ++j;
+        }
+      }
+    }
+  };
+  const uint64_t ns = p.sched ? p.n_tiles - p.dyn_tiles : p.n_tiles;
+  range(ns * blockIdx.x / gridDim.x, ns * (blockIdx.x + 1) / gridDim.x);
+  if (p.sched) {
+    while (true) {
+      unsigned long long c = 0;
+      if (lane == 0) c = atomicAdd(reinterpret_cast<unsigned long long*>(p.sched), (unsigned long long)p.dyn_chunk);
+      c = __shfl_sync(0xFFFFFFFFu, c, 0);
+      if (c >= p.dyn_tiles) break;
+      const uint64_t ce = c + p.dyn_chunk < p.dyn_tiles ? c + p.dyn_chunk : p.dyn_tiles;
+      range(ns + c, ns + ce);
+    }
+    const int stage = (int)(i % kQStages);  // end marker: a header with n_el = 0
     if (i >= kQStages) mbar_wait(&sm.empty()[stage], (uint32_t)(((i / kQStages) - 1) & 1));
-    const QJob& jb = p.jobs[j];
-    const uint32_t scheme = jb.scheme;
-    const uint32_t e0 = sub * p.tile_e;
-    const uint32_t n_el = min(p.tile_e, p.slab - e0);
-    uint8_t* meta = jb.dst + p.meta_off[scheme] + (uint64_t)slab_i * p.meta_stride[scheme];
-    if (MODE == MODE_ENCODE && scheme == HR_S_GSE8) {
-      const GseArr a = gse_array(jb.range + 2 * slab_i, m, nmax);
-      gse_build_table(sm.gtab(stage), a, m, lane);
-      if (sub == 0) gse_write_record(meta, p.meta_stride[HR_S_GSE8], a, m, nmax, lane);
-      __syncwarp();
-    }
     if (lane == 0) {
-      QHdr& h = sm.hdr()[stage];
-      h.codes = jb.dst + (uint64_t)slab_i * p.code_slab[scheme] + code_bytes(scheme, e0);
-      h.meta = scheme == HR_S_INT8 ? meta + 4 * (e0 >> p.g_shift) : scheme == HR_S_INT4 ? meta + 8 * (e0 >> p.g_shift) : meta;
-      h.range = jb.range ? jb.range + 2 * slab_i : nullptr;
-      h.n_el = n_el;
-      h.scheme = scheme;
-      uint64_t* full = &sm.full()[stage];
-      mbar_arrive_expect_tx(full, 2 * n_el);  // release: header and table visible with the phase flip
-      bulk_g2s(sm.tile(stage), jb.src + ((uint64_t)(l * p.H + p.h0 + hl) * p.slab + e0), 2 * n_el, full);
-    }
-    if (++sub == p.tiles_per_slab) {  // advance (sub, head, layer, job) without divisions
-      sub = 0;
-      ++slab_i;
-      if (++hl == p.Hl) {
-        hl = 0;
-        if (++l == p.L) l = 0, slab_i = 0, ++j;
+      sm.hdr()[stage].n_el = 0;
+      mbar_arrive(&sm.full()[stage]);
+      __threadfence();
+      if (atomicAdd(reinterpret_cast<unsigned int*>(p.sched) + 2, 1u) == gridDim.x - 1) {
+        *reinterpret_cast<volatile unsigned long long*>(p.sched) = 0ull;
+        reinterpret_cast<volatile unsigned int*>(p.sched)[2] = 0u;
       }
     }
   }
@@ -553,12 +585,14 @@ __device__ __forceinline__ void encode_tile(const QBatch& p, const QHdr& h, cons
 
 template <int DT, int SEG>
 __device__ __forceinline__ void q_consume_encode(const QBatch& p, const QSmem& sm, int cw, int lane) {
-  const uint64_t t0 = p.n_tiles * blockIdx.x / gridDim.x, t1 = p.n_tiles * (blockIdx.x + 1) / gridDim.x;
+  const uint64_t ns = p.sched ? p.n_tiles - p.dyn_tiles : p.n_tiles;
+  const uint64_t t0 = ns * blockIdx.x / gridDim.x, t1 = ns * (blockIdx.x + 1) / gridDim.x;
   uint32_t nan_acc = 0;
-  for (uint64_t i = 0; i < t1 - t0; ++i) {
+  for (uint64_t i = 0; p.sched || i < t1 - t0; ++i) {
     const int stage = (int)(i % kQStages);
     mbar_wait(&sm.full()[stage], (uint32_t)((i / kQStages) & 1));
     const QHdr h = sm.hdr()[stage];
+    if (h.n_el == 0) break;  // the producer's end marker (tail-balanced launches)
     // GSE-8 table: 1-KB aligned, entry address = tab | 4*ef
     encode_tile<DT, SEG, kQWarps>(p, h, sm.tile(stage), smem_addr(sm.gtab(stage)), cw, lane, nan_acc);
     __syncwarp();
@@ -612,7 +646,8 @@ __global__ void __launch_bounds__(32 * kTileWarps) quant_tile_kernel(const __gri
 // normals).
 template <int DT>
 __device__ __forceinline__ void q_consume_range(const QBatch& p, const QSmem& sm, int cw, int lane) {
-  const uint64_t t0 = p.n_tiles * blockIdx.x / gridDim.x, t1 = p.n_tiles * (blockIdx.x + 1) / gridDim.x;
+  const uint64_t ns = p.sched ? p.n_tiles - p.dyn_tiles : p.n_tiles;
+  const uint64_t t0 = ns * blockIdx.x / gridDim.x, t1 = ns * (blockIdx.x + 1) / gridDim.x;
   bool bad = false;
   int emin = 255, emax = 0;  // running range of the current slab (this warp's chunks)
   int* cur = nullptr;
@@ -628,10 +663,11 @@ __device__ __forceinline__ void q_consume_range(const QBatch& p, const QSmem& sm
     }
     emin = 255, emax = 0;
   };
-  for (uint64_t i = 0; i < t1 - t0; ++i) {
+  for (uint64_t i = 0; p.sched || i < t1 - t0; ++i) {
     const int stage = (int)(i % kQStages);
     mbar_wait(&sm.full()[stage], (uint32_t)((i / kQStages) & 1));
     const QHdr h = sm.hdr()[stage];
+    if (h.n_el == 0) break;
     const uint8_t* tile = sm.tile(stage);
     const uint32_t n_ch = h.n_el / kChunk;
     if (h.range != cur) {
@@ -1001,6 +1037,11 @@ void launch_tile(const QBatch& b, cudaStream_t st) {
   quant_tile_kernel<DT, SEG><<<(unsigned)b.n_tiles, 32 * kTileWarps, smem, st>>>(b);
 }
 
+// per-device claim counters of the persistent quantize kernel (64 slots of 16 B, zero between launches)
+uint32_t* g_qsched[16] = {};
+uint32_t g_qsched_next[16] = {};
+const uint64_t g_q_dyn_pct = std::getenv("HARAG_Q_DYN") ? (uint64_t)std::atoi(std::getenv("HARAG_Q_DYN")) : 25;
+
 template <int DT, int SEG, int MODE>
 void launch_b(const QBatch& b, cudaStream_t st) {
   if (MODE == MODE_ENCODE && use_tile_kernel()) {
@@ -1015,7 +1056,21 @@ void launch_b(const QBatch& b, cudaStream_t st) {
     init = true;
   }
   const uint64_t grid = std::min<uint64_t>(b.n_tiles, (uint64_t)g_num_sms);
-  quantize_batch_kernel<DT, SEG, MODE><<<(unsigned)grid, kQThreadsB, kQSmemBytes, st>>>(b);
+  QBatch bb = b;
+  bb.sched = nullptr;
+  if (g_q_dyn_pct && b.n_tiles >= 4 * grid) {  // tail balancing (see QBatch::sched)
+    int dev = 0;
+    HR_CUDA(cudaGetDevice(&dev));
+    require(dev < 16, HR_EINVAL, "device index");
+    if (!g_qsched[dev]) {
+      HR_CUDA(cudaMalloc((void**)&g_qsched[dev], 64 * 16));
+      HR_CUDA(cudaMemset(g_qsched[dev], 0, 64 * 16));
+    }
+    bb.sched = g_qsched[dev] + 4 * (g_qsched_next[dev]++ % 64);
+    bb.dyn_tiles = b.n_tiles * g_q_dyn_pct / 100;
+    bb.dyn_chunk = (uint32_t)std::max<uint64_t>(1, bb.dyn_tiles / (grid * 8));
+  }
+  quantize_batch_kernel<DT, SEG, MODE><<<(unsigned)grid, kQThreadsB, kQSmemBytes, st>>>(bb);
 }
 
 template <int DT>
