@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define HR_ABI_VERSION 1
+#define HR_ABI_VERSION 2
 
 typedef enum {
   HR_OK = 0,
@@ -97,6 +97,10 @@ typedef struct {
   int32_t  numa_bind;      /* 1 (default): host tiers (pinned tier, backing, bounce buffers) are allocated and
                               first touched by a thread running on the CPUs NVML reports local to `device`, and
                               the bounce / disk workers run there (hr_store_local_cpus); 0: no binding */
+  int32_t  guard;          /* hr_build_store only: 1 = value-distribution guard (R29, an extension the
+                              paper does not have): before placement, every item whose Alg. 1 scheme would lose
+                              values (GSE-8 flushing nonzeros to 0, FP8 saturating) moves up the ladder
+                              (hr_guard_stats, hr_policy_guard); 0 (default) = Alg. 1 as published */
 } hr_store_config;
 
 typedef struct {
@@ -159,6 +163,10 @@ hr_status hr_build_store(hr_store* s, uint32_t n_docs, const uint64_t* hotness,
  * point), end (synchronise; every doc must have been put and no NaN/Inf
  * seen, else HR_EINVAL). */
 hr_status hr_build_begin(hr_store* s, uint32_t n_docs, const uint64_t* hotness);
+/* hr_build_begin with the caller's schemes (host uint32[2*n_docs], each one of cfg->ladder) in place of
+ * Alg. 1's — e.g. hr_policy_guard's; placement still ranks by `hotness`.  HR_EINVAL for a scheme
+ * outside the ladder. */
+hr_status hr_build_begin_schemes(hr_store* s, uint32_t n_docs, const uint64_t* hotness, const uint32_t* schemes);
 hr_status hr_build_put(hr_store* s, uint32_t doc, const void* k_src, const void* v_src, void* stream);
 /* hr_build_put for n <= 16 distinct docs in one quantize launch (all 2n items, any scheme mix):
  * docs host uint32[n], k_srcs / v_srcs host arrays of n DEVICE pointers (same rules as hr_build_put).
@@ -321,6 +329,19 @@ hr_status hr_exponent_histogram(uint32_t dtype, const void* src_dev, uint64_t n,
  * max |x_i - x^_i|; RMSE of Eq. = sqrt(out_host[0] / (L*Hl*T*D)).
  * Synchronous (returns after the stream drains).  HR_EINVAL on NaN/Inf input or
  * a bad config / scheme; temporary device memory is freed before returning. */
+/* Value-distribution guard statistics of one item (R29): src_dev =
+ * the item's source [L][H][T][D] over ALL heads (so every rank of a head-sharded store derives the same
+ * schemes), dtype / layout from cfg.  Accumulates into DEVICE stats_dev[2]: [0] += the values GSE-8
+ * (cfg's 1+e+m layout, each (layer, head) slab with its own rule-C array) would flush to zero —
+ * nonzero fp32 subnormals and exponents below G_0 - (m-1) (R9); [1] = max([1], fp32 bits of max |x|).
+ * Zero stats_dev before the first call of an item.  Stream-ordered. */
+hr_status hr_guard_stats(const hr_store_config* cfg, const void* src_dev, uint64_t* stats_dev, void* stream);
+/* The guard's policy: for item i with Alg. 1 scheme schemes_in[i] and stats[2i], stats[2i+1] (host, as
+ * hr_guard_stats leaves them), while the scheme would lose values (GSE-8: any flushed value; FP8 E4M3:
+ * max |x| > 448; E5M2: > 57344, R5) and is not ladder[0], take the previous (hotter) ladder scheme.
+ * HR_EINVAL for a scheme outside the ladder. */
+hr_status hr_policy_guard(uint32_t n_items, const uint32_t* schemes_in, const uint64_t* stats, uint32_t n_ladder,
+                          const uint32_t* ladder, uint32_t* schemes_out);
 hr_status hr_scheme_error(const hr_store_config* cfg, uint32_t scheme, const void* src_dev, double* out_host,
                           void* stream);
 

@@ -209,11 +209,12 @@ class OracleStore:
         self.schemes: list[int] = []
         self._dec: dict[int, np.ndarray] = {}
 
-    def build(self, n_docs: int, hotness, source) -> None:
-        """source(doc, kind) -> uint16 [L][Hl][T][D] (this rank's heads)."""
+    def build(self, n_docs: int, hotness, source, schemes=None) -> None:
+        """source(doc, kind) -> uint16 [L][Hl][T][D] (this rank's heads).  schemes: per-item schemes in
+        place of Alg. 1's (the value-distribution guard's, R29), else Alg. 1."""
         from .hotness import assign_schemes
         self.n_docs = n_docs
-        self.schemes = assign_schemes(hotness, self.ladder, self.taus)
+        self.schemes = list(schemes) if schemes is not None else assign_schemes(hotness, self.ladder, self.taus)
         for item in range(2 * n_docs):
             self.blobs[item] = encode_item(source(item // 2, item % 2), self.schemes[item], self.lay)
 

@@ -18,7 +18,7 @@ from ._lib import (FP8E4M3, FP8E5M2, GSE8, HR_BF16, HR_FP16, INT4, INT8, PASS16,
 __all__ = ["Store", "HaragError", "SCHEMES", "PASS16", "INT8", "FP8E4M3", "FP8E5M2", "GSE8", "INT4",
            "T_HBM", "T_PIN", "T_PAGE", "T_DISK", "R_HBM", "R_PIN", "R_PAGE", "R_BACKING", "R_FILE", "policy_rank", "policy_lists_bytes4", "policy_assign", "policy_lists_bytes",
            "policy_lists_fraction", "policy_count", "policy_epoch", "item_bytes", "Alg2",
-           "exponent_histogram", "scheme_error"]
+           "exponent_histogram", "scheme_error", "guard_stats", "policy_guard"]
 
 
 def _ptr(x) -> int:
@@ -55,7 +55,7 @@ def make_config(*, L, H, D, T, dtype="bf16", group=0, gse=(4, 3),
                 ladder=("INT8", "FP8E4M3", "FP8E5M2", "GSE8"), taus=(0.1, 0.1, 0.1),
                 hbm_budget=0, pin_budget=0, backing_pinned=False, keep_backing=True, decay_shift=1,
                 alias_R=0, device=0, rank=0, world=1, staging_slots=0, demand_mode=False,
-                disk_backing=False, page_budget=0, numa_bind=True) -> _lib.Config:
+                disk_backing=False, page_budget=0, numa_bind=True, guard=False) -> _lib.Config:
     c = _lib.default_config()
     c.L, c.H, c.D, c.T = L, H, D, T
     c.dtype = HR_FP16 if dtype == "fp16" else HR_BF16
@@ -78,6 +78,7 @@ def make_config(*, L, H, D, T, dtype="bf16", group=0, gse=(4, 3),
     c.disk_backing = int(bool(disk_backing))
     c.page_budget = int(page_budget)
     c.numa_bind = int(bool(numa_bind))
+    c.guard = int(bool(guard))
     return c
 
 
@@ -115,9 +116,14 @@ class Store:
         fn = _lib.SRC_FN(cb)
         check(lib.hr_build_store(self._h, n_docs, _p(hot, C.c_uint64), fn, None, _stream(stream)))
 
-    def build_begin(self, n_docs: int, hotness) -> None:
+    def build_begin(self, n_docs: int, hotness, schemes=None) -> None:
+        """hr_build_begin (Alg. 1), or hr_build_begin_schemes with the caller's per-item schemes."""
         hot = _u64(hotness)
-        check(lib.hr_build_begin(self._h, n_docs, _p(hot, C.c_uint64)))
+        if schemes is None:
+            check(lib.hr_build_begin(self._h, n_docs, _p(hot, C.c_uint64)))
+        else:
+            sc = _u32(schemes)
+            check(lib.hr_build_begin_schemes(self._h, n_docs, _p(hot, C.c_uint64), _p(sc, C.c_uint32)))
 
     def build_put(self, doc: int, k_src, v_src, stream=None) -> None:
         check(lib.hr_build_put(self._h, doc, _ptr(k_src), _ptr(v_src), _stream(stream)))
@@ -283,6 +289,23 @@ def policy_assign(h, ladder, taus) -> np.ndarray:
     check(lib.hr_policy_assign(h.size, _p(h, C.c_uint64), lad.size, _p(lad, C.c_uint32),
                                _p(tau, C.c_double), _p(out, C.c_uint32)))
     return out
+
+
+def policy_guard(schemes, stats, ladder) -> np.ndarray:
+    """hr_policy_guard: stats = uint64 [n][2] as hr_guard_stats leaves them (flushed, fp32 bits of max |x|)."""
+    sc, st = _u32(schemes), _u64(stats).reshape(-1)
+    lad = _u32([SCHEMES[s] if isinstance(s, str) else s for s in ladder])
+    out = np.empty(sc.size, np.uint32)
+    check(lib.hr_policy_guard(sc.size, _p(sc, C.c_uint32), _p(st, C.c_uint64), lad.size, _p(lad, C.c_uint32),
+                              _p(out, C.c_uint32)))
+    return out
+
+
+def guard_stats(src, stats, stream=None, **cfg) -> None:
+    """hr_guard_stats: accumulate the guard statistics of one item's ALL-heads source [L][H][T][D] (device)
+    into the device uint64[2] `stats` (zero it first); cfg as for Store (shape, dtype, gse)."""
+    c = make_config(**cfg)
+    check(lib.hr_guard_stats(C.byref(c), _ptr(src), _ptr(stats), _stream(stream)))
 
 
 def policy_lists_bytes(order, sizes, hbm_budget, pin_budget) -> np.ndarray:

@@ -32,6 +32,7 @@ class Config(C.Structure):
         ("decay_shift", C.c_uint32), ("bench_alias_R", C.c_uint32),
         ("device", C.c_int32), ("rank", C.c_int32), ("world", C.c_int32), ("staging_slots", C.c_uint32),
         ("disk_backing", C.c_int32), ("page_budget", C.c_uint64), ("numa_bind", C.c_int32),
+        ("guard", C.c_int32),
     ]
 
 
@@ -66,6 +67,7 @@ _SIGS = {
     "hr_store_destroy": (None, [P]),
     "hr_build_store": (I32, [P, U32, PU64, SRC_FN, P, P]),
     "hr_build_begin": (I32, [P, U32, PU64]),
+    "hr_build_begin_schemes": (I32, [P, U32, PU64, PU32]),
     "hr_build_put": (I32, [P, U32, P, P, P]),
     "hr_build_put_batch": (I32, [P, U32, PU32, PP, PP, P]),
     "hr_build_end": (I32, [P, P]),
@@ -97,6 +99,8 @@ _SIGS = {
     "hr_item_bytes": (I32, [C.POINTER(Config), U32, PU64]),
     "hr_exponent_histogram": (I32, [U32, P, U64, P, P]),
     "hr_scheme_error": (I32, [C.POINTER(Config), U32, P, C.POINTER(C.c_double), P]),
+    "hr_guard_stats": (I32, [C.POINTER(Config), P, P, P]),
+    "hr_policy_guard": (I32, [U32, PU32, PU64, U32, PU32, PU32]),
     "hr_alg2_create": (I32, [U32, PU32, PU64, U64, U64, U64, C.POINTER(P)]),
     "hr_alg2_access": (I32, [P, U32, PU32, PU32, PU32, U32, PU32]),
     "hr_alg2_set_lists": (I32, [P, PU32]),

@@ -26,4 +26,10 @@ uint32_t error_partials(uint64_t n_elems);
 void launch_error(const uint16_t* x, const uint16_t* y, uint32_t L, uint32_t H, uint32_t Hl, uint32_t h0,
                   uint64_t slab, uint32_t dtype, double* partials, uint32_t n_part, double* out, cudaStream_t stream);
 
+// Value-distribution guard statistics of one item (R29): src = [n_slabs][slab] 16-bit values
+// (an item's ALL-heads source); stats[0] += values GSE-8 (layout 1+e_bits+m_bits) flushes to zero,
+// stats[1] = max(stats[1], fp32 bits of max |x|).  Stream-ordered.
+void launch_guard(uint32_t dtype, const void* src, uint64_t n_slabs, uint64_t slab, uint32_t e_bits,
+                  uint32_t m_bits, unsigned long long* stats, cudaStream_t st);
+
 }  // namespace harag

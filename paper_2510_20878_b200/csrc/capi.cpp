@@ -92,6 +92,13 @@ hr_status hr_build_begin(hr_store* s, uint32_t n_docs, const uint64_t* hotness) 
     s->impl.build_begin(n_docs, hotness);
   });
 }
+hr_status hr_build_begin_schemes(hr_store* s, uint32_t n_docs, const uint64_t* hotness, const uint32_t* schemes) {
+  return guard([&] {
+    NONNULL(s);
+    NONNULL(schemes);
+    s->impl.build_begin(n_docs, hotness, schemes);
+  });
+}
 hr_status hr_build_put(hr_store* s, uint32_t doc, const void* k_src, const void* v_src, void* stream) {
   return guard([&] {
     NONNULL(s);
@@ -352,6 +359,29 @@ hr_status hr_exponent_histogram(uint32_t dtype, const void* src_dev, uint64_t n,
   });
 }
 
+hr_status hr_guard_stats(const hr_store_config* cfg, const void* src_dev, uint64_t* stats_dev, void* stream) {
+  return guard([&] {
+    NONNULL(cfg);
+    NONNULL(src_dev);
+    NONNULL(stats_dev);
+    harag::require(cfg->dtype == HR_BF16 || cfg->dtype == HR_FP16, HR_EINVAL, "dtype must be HR_BF16 or HR_FP16");
+    harag::require(cfg->gse_ebits >= 2 && cfg->gse_mbits >= 2 && cfg->gse_ebits + cfg->gse_mbits == 7, HR_EINVAL,
+                   "GSE-8 layout must be 1+e+m with e + m = 7, e, m >= 2");
+    harag::launch_guard(cfg->dtype, src_dev, (uint64_t)cfg->L * cfg->H, (uint64_t)cfg->T * cfg->D, cfg->gse_ebits,
+                        cfg->gse_mbits, reinterpret_cast<unsigned long long*>(stats_dev), S(stream));
+  });
+}
+hr_status hr_policy_guard(uint32_t n, const uint32_t* schemes_in, const uint64_t* stats, uint32_t n_ladder,
+                          const uint32_t* ladder, uint32_t* schemes_out) {
+  return guard([&] {
+    NONNULL(schemes_in);
+    NONNULL(stats);
+    NONNULL(ladder);
+    NONNULL(schemes_out);
+    auto sc = harag::guard_schemes(schemes_in, stats, n, ladder, n_ladder);
+    std::memcpy(schemes_out, sc.data(), sizeof(uint32_t) * n);
+  });
+}
 hr_status hr_scheme_error(const hr_store_config* cfg, uint32_t scheme, const void* src_dev, double* out_host,
                           void* stream) {
   return guard([&] {

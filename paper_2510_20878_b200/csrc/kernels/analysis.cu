@@ -166,7 +166,92 @@ int sm_count() {
   return n;
 }
 
+// Value-distribution guard (R29): one CTA per (layer, head) slab of an item's source
+// [L][H][slab] (ALL heads).  Pass 1: min / max fp32 exponent field over the nonzero normals and max |x|;
+// rule C's first shared exponent lo = max(Emin, Emax - (2^e - 1)(m - 1)) (R6); pass 2 (the slab again,
+// from L1/L2) counts the nonzero values GSE-8 flushes to field 0: fp32 subnormals and E < lo - (m - 1)
+// (R9).  stats[0] += the count, stats[1] = max(stats[1], bits of max |x|) (non-negative fp32 bits order
+// like the values).
+constexpr int kGuardThreads = 256;
+template <int DT>
+__device__ __forceinline__ uint32_t f32_bits(uint32_t bits16) {
+  return DT == HR_BF16 ? bits16 << 16 : __float_as_uint(__half2float(__ushort_as_half((unsigned short)bits16)));
+}
+template <int DT>
+__global__ void __launch_bounds__(kGuardThreads) guard_kernel(const uint16_t* __restrict__ src, uint32_t slab,
+                                                              int e_bits, int m_bits,
+                                                              unsigned long long* __restrict__ stats) {
+  __shared__ uint32_t red[3][kGuardThreads / 32];
+  __shared__ uint32_t thr_s;
+  const uint4* v = reinterpret_cast<const uint4*>(src + (uint64_t)blockIdx.x * slab);
+  const uint32_t nv = slab / 8, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  uint32_t emin = 255, emax = 0, amax = 0;
+  for (uint32_t i = threadIdx.x; i < nv; i += kGuardThreads) {
+    const uint4 w = __ldg(v + i);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t b = f32_bits<DT>((ws[k >> 1] >> (16 * (k & 1))) & 0xFFFFu) & 0x7FFFFFFFu;
+      const uint32_t ef = b >> 23;
+      amax = max(amax, b);
+      if (ef != 0) emin = min(emin, ef), emax = max(emax, ef);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) {
+    emin = min(emin, __shfl_xor_sync(0xFFFFFFFFu, emin, o));
+    emax = max(emax, __shfl_xor_sync(0xFFFFFFFFu, emax, o));
+    amax = max(amax, __shfl_xor_sync(0xFFFFFFFFu, amax, o));
+  }
+  if (lane == 0) red[0][warp] = emin, red[1][warp] = emax, red[2][warp] = amax;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kGuardThreads / 32; ++w)
+      emin = min(emin, red[0][w]), emax = max(emax, red[1][w]), amax = max(amax, red[2][w]);
+    // biased threshold: fields below it (and every nonzero subnormal) flush; no normal value at all ->
+    // every nonzero value flushes
+    int thr = 256;
+    if (emax != 0) {
+      const int step = m_bits - 1;
+      const int lo = max((int)emin - 127, (int)emax - 127 - ((1 << e_bits) - 1) * step);
+      thr = lo - step + 127;
+    }
+    thr_s = (uint32_t)max(thr, 1);
+    atomicMax(stats + 1, (unsigned long long)amax);
+  }
+  __syncthreads();
+  const uint32_t thr = thr_s;
+  uint32_t cnt = 0;
+  for (uint32_t i = threadIdx.x; i < nv; i += kGuardThreads) {
+    const uint4 w = __ldg(v + i);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t b = f32_bits<DT>((ws[k >> 1] >> (16 * (k & 1))) & 0xFFFFu) & 0x7FFFFFFFu;
+      cnt += (b != 0u && (b >> 23) < thr) ? 1u : 0u;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) cnt += __shfl_xor_sync(0xFFFFFFFFu, cnt, o);
+  if (lane == 0 && cnt) atomicAdd(stats, (unsigned long long)cnt);
+}
+
 }  // namespace
+
+void launch_guard(uint32_t dtype, const void* src, uint64_t n_slabs, uint64_t slab, uint32_t e_bits,
+                  uint32_t m_bits, unsigned long long* stats, cudaStream_t st) {
+  require(slab % 8 == 0 && slab < (1ull << 32), HR_EINVAL, "guard: slab must be a multiple of 8 elements");
+  require(reinterpret_cast<uintptr_t>(src) % 16 == 0, HR_EINVAL, "guard: source must be 16-byte aligned");
+  require(n_slabs < (1ull << 31), HR_EINVAL, "guard: too many slabs");
+  if (!n_slabs) return;
+  if (dtype == HR_BF16)
+    guard_kernel<HR_BF16><<<(unsigned)n_slabs, kGuardThreads, 0, st>>>(static_cast<const uint16_t*>(src),
+                                                                       (uint32_t)slab, (int)e_bits, (int)m_bits, stats);
+  else
+    guard_kernel<HR_FP16><<<(unsigned)n_slabs, kGuardThreads, 0, st>>>(static_cast<const uint16_t*>(src),
+                                                                       (uint32_t)slab, (int)e_bits, (int)m_bits, stats);
+  HR_CUDA(cudaGetLastError());
+}
 
 void launch_exponent_hist(uint32_t dtype, const void* src, uint64_t n, unsigned long long* hist,
                           cudaStream_t stream) {

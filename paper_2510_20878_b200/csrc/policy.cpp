@@ -158,4 +158,24 @@ std::vector<uint32_t> Alg2::resident(uint32_t tier) const {
   return std::vector<uint32_t>(q_[tier].lru.begin(), q_[tier].lru.end());
 }
 
+std::vector<uint32_t> guard_schemes(const uint32_t* schemes, const uint64_t* stats, uint32_t n, const uint32_t* ladder,
+                                    uint32_t n_ladder) {
+  require(n_ladder >= 1 && n_ladder <= 6, HR_EINVAL, "ladder must hold 1..6 schemes");
+  auto unsafe = [](uint32_t s, uint64_t flushed, uint32_t amax_bits) {
+    if (s == HR_S_GSE8) return flushed > 0;
+    if (s == HR_S_FP8E4M3) return amax_bits > 0x43E00000u;  // |x| > 448
+    if (s == HR_S_FP8E5M2) return amax_bits > 0x47600000u;  // |x| > 57344
+    return false;
+  };
+  std::vector<uint32_t> out(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    uint32_t p = 0;
+    while (p < n_ladder && ladder[p] != schemes[i]) ++p;
+    require(p < n_ladder, HR_EINVAL, "item " + std::to_string(i) + ": scheme not in the ladder");
+    while (p > 0 && unsafe(ladder[p], stats[2 * i], (uint32_t)stats[2 * i + 1])) --p;
+    out[i] = ladder[p];
+  }
+  return out;
+}
+
 }  // namespace harag

@@ -21,6 +21,13 @@ std::vector<uint64_t> partition_bounds(uint32_t n, const double* tau, uint32_t n
 std::vector<uint32_t> assign_schemes(const uint64_t* h, uint32_t n, const uint32_t* ladder, uint32_t n_ladder,
                                      const double* tau);
 
+// Value-distribution guard (R29): stats[2i] = values of item i GSE-8
+// would flush, stats[2i+1] = fp32 bits of its max |x|.  While an item's scheme would lose values (GSE-8
+// flushes some, FP8 E4M3 / E5M2 would saturate: |x| > 448 / 57344) and is not the ladder's first, it
+// takes the previous (hotter) ladder scheme.  Every scheme must be one of the ladder's.
+std::vector<uint32_t> guard_schemes(const uint32_t* schemes, const uint64_t* stats, uint32_t n, const uint32_t* ladder,
+                                    uint32_t n_ladder);
+
 // Alg. 2 step 1 by bytes (R15): longest rank-prefix fitting each budget.
 // Returns tier per item: 0 HBM (GPU_LIST), 1 PIN (PIN_LIST), 2 PAGE (PAGE_LIST), 3 DISK (the rest,
 // only when page_budget is finite).

@@ -21,6 +21,7 @@
 #include <optional>
 #include <unordered_set>
 
+#include "analysis.h"
 #include "kernels.h"
 #include "policy.h"
 #include "trace.h"
@@ -146,12 +147,19 @@ uint32_t Store::logical_tier(uint32_t item) const {
 
 uint8_t* Store::hbm_ptr(uint32_t item) const { return hbm_base + loc[item].hbm_off; }
 
-void Store::build_begin(uint32_t nd, const uint64_t* hot) {
+void Store::build_begin(uint32_t nd, const uint64_t* hot, const uint32_t* schemes) {
   require(state == State::Empty, HR_ESTATE, "store already built");
   require(nd > 0, HR_EINVAL, "n_docs must be > 0");
   require(hot != nullptr, HR_EINVAL, "hotness is NULL");
-  // Alg. 1: schemes by hotness rank
-  setup(nd, hot, assign_schemes(hot, 2 * nd, cfg.ladder, cfg.n_ladder, cfg.tau), false);
+  if (schemes) {  // the caller's schemes (e.g. the value-distribution guard's), each one of the ladder
+    for (uint32_t i = 0; i < 2 * nd; ++i)
+      require(std::find(cfg.ladder, cfg.ladder + cfg.n_ladder, schemes[i]) != cfg.ladder + cfg.n_ladder, HR_EINVAL,
+              "item " + std::to_string(i) + ": scheme not in the ladder");
+    setup(nd, hot, std::vector<uint32_t>(schemes, schemes + 2 * nd), false);
+  } else {
+    // Alg. 1: schemes by hotness rank
+    setup(nd, hot, assign_schemes(hot, 2 * nd, cfg.ladder, cfg.n_ladder, cfg.tau), false);
+  }
   state = State::Building;
 }
 
@@ -383,12 +391,38 @@ void Store::build_end(cudaStream_t st) {
 void Store::build_with_source(uint32_t nd, const uint64_t* hot, hr_src_fn src, void* user, cudaStream_t st) {
   const NvtxRange nvtx_call("hr_build");
   require(src != nullptr, HR_EINVAL, "source callback is NULL");
-  build_begin(nd, hot);
+  require(state == State::Empty, HR_ESTATE, "store already built");
+  require(nd > 0 && hot != nullptr, HR_EINVAL, "n_docs must be > 0 and hotness non-NULL");
   // kSrcBatch docs per quantize launch: the source callback fills one buffer pair per doc
   const uint64_t full = 2ull * lay.L * lay.H * lay.T * lay.D;
   const uint32_t nb = std::max<uint32_t>(1, std::min<uint32_t>(kSrcBatch, nd));
+  HR_CUDA(cudaSetDevice(cfg.device));
   HR_CUDA(cudaMalloc(&src_k, full * nb));
   HR_CUDA(cudaMalloc(&src_v, full * nb));
+  if (cfg.guard) {
+    // value-distribution guard (R29): a pass over every doc's source before placement, then Alg. 1's
+    // schemes moved up the ladder where they would lose values
+    const NvtxRange nvtx_guard("guard");
+    unsigned long long* gs = nullptr;
+    HR_CUDA(cudaMalloc((void**)&gs, sizeof(uint64_t) * 4ull * nd));
+    HR_CUDA(cudaMemsetAsync(gs, 0, sizeof(uint64_t) * 4ull * nd, st));
+    for (uint32_t doc = 0; doc < nd; ++doc) {
+      const int rc = src(user, doc, src_k, src_v, (void*)st);
+      require(rc == HR_OK, (hr_status)rc, "source callback failed for doc " + std::to_string(doc));
+      launch_guard(lay.dtype, src_k, (uint64_t)lay.L * lay.H, lay.slab(), lay.gse_e, lay.gse_m, gs + 4ull * doc, st);
+      launch_guard(lay.dtype, src_v, (uint64_t)lay.L * lay.H, lay.slab(), lay.gse_e, lay.gse_m, gs + 4ull * doc + 2,
+                   st);
+    }
+    std::vector<uint64_t> stats(4ull * nd);
+    HR_CUDA(cudaMemcpyAsync(stats.data(), gs, sizeof(uint64_t) * 4ull * nd, cudaMemcpyDeviceToHost, st));
+    HR_CUDA(cudaStreamSynchronize(st));
+    cudaFree(gs);
+    const auto a1 = assign_schemes(hot, 2 * nd, cfg.ladder, cfg.n_ladder, cfg.tau);
+    const auto sc = guard_schemes(a1.data(), stats.data(), 2 * nd, cfg.ladder, cfg.n_ladder);
+    build_begin(nd, hot, sc.data());
+  } else {
+    build_begin(nd, hot);
+  }
   uint32_t docs[kPutBatch];
   const void *ks[kPutBatch], *vs[kPutBatch];
   // bench aliasing (bench_alias_R > 0): a doc whose items all live only in a host backing blob that

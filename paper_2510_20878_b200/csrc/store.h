@@ -73,7 +73,7 @@ struct Store {
   explicit Store(const hr_store_config& c);
   ~Store();
 
-  void build_begin(uint32_t n_docs, const uint64_t* hotness);
+  void build_begin(uint32_t n_docs, const uint64_t* hotness, const uint32_t* schemes = nullptr);
   void setup(uint32_t n_docs, const uint64_t* hotness, std::vector<uint32_t> schemes, bool disk);
   std::vector<uint32_t> place_lists() const;  // Alg. 2 step 1 by bytes for this store's tiers
   void save(const char* path) const;

@@ -29,7 +29,7 @@ def test_exports_every_declared_symbol():
     missing = [n for n in names if n not in exported]
     assert not missing, missing
     assert set(hr._lib.EXPORTED) <= set(names)
-    assert hr.lib.hr_abi_version() == 1
+    assert hr.lib.hr_abi_version() == 2
 
 
 def test_config_validation():
@@ -149,3 +149,30 @@ def test_alg2_native_vs_oracle_1000_seeds():
             assert [(names[t], i) for t, i in ev] == oev
         for t in range(3):
             assert nat.resident(t) == ora.resident(names[t])
+
+
+def test_policy_guard_vs_oracle():
+    """hr_policy_guard (C++) == oracle.guard.guard_schemes on random schemes / statistics, including the
+    FP8 saturation boundaries (448, 57344) as exact fp32 bit patterns; a scheme outside the ladder is
+    HR_EINVAL."""
+    import struct
+
+    from oracle import guard
+    rng = np.random.default_rng(29)
+    ladders = [["INT8", "FP8E4M3", "FP8E5M2", "GSE8"], ["FP8E5M2", "GSE8"], ["PASS16", "INT8", "INT4"],
+               ["GSE8"], ["INT8", "GSE8", "FP8E4M3"]]
+    edges = [448.0, np.nextafter(np.float32(448.0), np.float32(1e9)), 57344.0,
+             np.nextafter(np.float32(57344.0), np.float32(1e9)), 1.0, 1e6]
+    for lad in ladders:
+        ids = [hr.SCHEMES[s] for s in lad]
+        n = 300
+        sc = rng.choice(ids, size=n).astype(np.uint32)
+        fl = rng.choice([0, 0, 1, 5], size=n).astype(np.uint64)
+        am = np.array([float(rng.choice(edges)) if rng.random() < 0.5 else float(rng.uniform(0, 1e5))
+                       for _ in range(n)], dtype=np.float32)
+        bits = np.array([struct.unpack("<I", struct.pack("<f", float(a)))[0] for a in am], dtype=np.uint64)
+        got = hr.policy_guard(sc, np.stack([fl, bits], axis=1), lad)
+        want = guard.guard_schemes([int(x) for x in sc], list(zip(fl.tolist(), am.astype(np.float64).tolist())), ids)
+        assert list(got) == want, lad
+    with pytest.raises(hr.HaragError):
+        hr.policy_guard([hr.SCHEMES["INT4"]], [[0, 0]], ["INT8", "GSE8"])
