@@ -64,3 +64,33 @@ def test_weights_are_a_convex_combination():
     q, k, v = rng.normal(size=(7, 32)), 3 * rng.normal(size=(50, 32)), rng.normal(size=(50, 32))
     O, _ = attention.attention(q, k, v, 1 / math.sqrt(32))
     assert np.all(O <= v.max(axis=0) + 1e-12) and np.all(O >= v.min(axis=0) - 1e-12)
+
+
+def test_prefill_own_block_matches_torch_sdpa_masked():
+    """Prefill form (R30): [chunk keys ; own keys] with the causal mask on the own block — against torch
+    SDPA in fp64 with the same boolean mask written out (a library routine, the special case of masked
+    attention), and row 0 against the explicit formula over the chunk keys plus own key 0 only."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(30)
+    L, H, g, n_q, N, D = 2, 2, 3, 6, 64, 32
+    Qb = numerics.f32_to_bf16(rng.normal(size=(L, H * g, n_q, D)).astype(np.float32))
+    Kb = numerics.f32_to_bf16((3 * rng.normal(size=(L, H, N, D))).astype(np.float32))
+    Vb = numerics.f32_to_bf16(rng.normal(size=(L, H, N, D)).astype(np.float32))
+    Ko = numerics.f32_to_bf16((3 * rng.normal(size=(L, H, n_q, D))).astype(np.float32))
+    Vo = numerics.f32_to_bf16(rng.normal(size=(L, H, n_q, D)).astype(np.float32))
+    O, lse = attention.attend_request(Qb, Kb, Vb, g, "bf16", K_own_bits=Ko, V_own_bits=Vo)
+    f = lambda b: torch.from_numpy(numerics.to_f32(b, "bf16").astype(np.float64))  # noqa: E731
+    q = f(Qb)
+    k = torch.cat([f(Kb), f(Ko)], dim=2).repeat_interleave(g, dim=1)
+    v = torch.cat([f(Vb), f(Vo)], dim=2).repeat_interleave(g, dim=1)
+    m = torch.ones(n_q, N + n_q, dtype=torch.bool)
+    for i in range(n_q):
+        m[i, N + i + 1:] = False
+    ref = torch.nn.functional.scaled_dot_product_attention(q, k, v, attn_mask=m).numpy()
+    assert np.allclose(O, ref, rtol=0, atol=1e-12)
+    # row 0, layer 0, query head 0: softmax over the N chunk scores and own key 0, written out
+    qq, kk, vv = q[0, 0, 0].numpy(), k[0, 0, :N + 1].numpy(), v[0, 0, :N + 1].numpy()
+    s = kk @ qq / math.sqrt(D)
+    w = np.exp(s - s.max())
+    assert np.allclose(O[0, 0, 0], (w / w.sum()) @ vv, atol=1e-12)
+    assert abs(lse[0, 0, 0] - (s.max() + math.log(w.sum()))) < 1e-12
