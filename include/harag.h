@@ -244,6 +244,17 @@ hr_status hr_attend_layers(hr_store* s, uint32_t n_req, uint32_t k, const uint32
                            uint32_t n_layers, const void* q_dev, uint32_t n_q, uint32_t g, void* o_dev, float* lse_dev,
                            float scale, void* kv_dump, void* stream);
 
+/* hr_attend_layers in the prefill form (R30; TurboRAG prefill): the question's
+ * own keys and values follow the chunk keys and are attended causally — query row (hq, i) (question
+ * token i) sees every chunk key and own keys 0..i — so O / LSE are the full prefill attention of the
+ * question tokens over [retrieved chunk KV ; question KV] in one launch.
+ *   k_own_dev, v_own_dev: device [n_req][n_layers][Hl][n_q][D] of cfg->dtype (this rank's KV heads,
+ *                         K already position-encoded), 16-byte aligned;
+ *   everything else as hr_attend_layers (no kv_dump); needs n_q <= 64 and k <= 63 (HR_EINVAL). */
+hr_status hr_attend_prefill(hr_store* s, uint32_t n_req, uint32_t k, const uint32_t* doc_ids, uint32_t layer0,
+                            uint32_t n_layers, const void* q_dev, const void* k_own_dev, const void* v_own_dev,
+                            uint32_t n_q, uint32_t g, void* o_dev, float* lse_dev, float scale, void* stream);
+
 /* ------------------------------------------------------------ persistence
  * Compress once, load many (compressed chunks are stored on disk).
  * hr_store_save writes a built store: a 4 KiB-aligned header (magic

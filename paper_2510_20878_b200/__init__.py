@@ -179,6 +179,18 @@ class Store:
                                        _ptr(q), int(n_q), int(g), _ptr(o), _ptr(lse), float(scale),
                                        _ptr(kv_dump), _stream(stream)))
 
+    def attend_prefill(self, ids, q, k_own, v_own, o, n_q: int, g: int, layers, lse=None, scale: float = 0.0,
+                       stream=None) -> None:
+        """hr_attend_prefill: chunk keys then the question's own keys (causal), layers=(l0, n);
+        k_own / v_own: device [n_req][n][Hl][n_q][D]."""
+        ids = _u32(ids)
+        if ids.ndim != 2:
+            raise ValueError("ids must be [n_req][k]")
+        n_req, k = ids.shape
+        check(lib.hr_attend_prefill(self._h, n_req, k, _p(ids, C.c_uint32), int(layers[0]), int(layers[1]), _ptr(q),
+                                    _ptr(k_own), _ptr(v_own), int(n_q), int(g), _ptr(o), _ptr(lse), float(scale),
+                                    _stream(stream)))
+
     # ------------------------------------------------------------ epochs
     def hotness_delta_ptr(self) -> tuple[int, int]:
         p = C.POINTER(C.c_int64)()

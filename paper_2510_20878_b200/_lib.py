@@ -77,6 +77,7 @@ _SIGS = {
     "hr_replace": (I32, [P, P]),
     "hr_attend": (I32, [P, U32, U32, PU32, P, U32, U32, P, P, C.c_float, P, P]),
     "hr_attend_layers": (I32, [P, U32, U32, PU32, U32, U32, P, U32, U32, P, P, C.c_float, P, P]),
+    "hr_attend_prefill": (I32, [P, U32, U32, PU32, U32, U32, P, P, P, U32, U32, P, P, C.c_float, P]),
     "hr_store_save": (I32, [P, C.c_char_p]),
     "hr_build_from_file": (I32, [P, C.c_char_p, P]),
     "hr_item_info": (I32, [P, U32, PU32, PU32, PU64]),

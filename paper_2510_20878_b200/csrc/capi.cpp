@@ -155,6 +155,17 @@ hr_status hr_attend_layers(hr_store* s, uint32_t n_req, uint32_t k, const uint32
     s->impl.attend(n_req, k, doc_ids, layer0, n_layers, q_dev, n_q, g, o_dev, lse_dev, scale, kv_dump, S(stream));
   });
 }
+hr_status hr_attend_prefill(hr_store* s, uint32_t n_req, uint32_t k, const uint32_t* doc_ids, uint32_t layer0,
+                            uint32_t n_layers, const void* q_dev, const void* k_own_dev, const void* v_own_dev,
+                            uint32_t n_q, uint32_t g, void* o_dev, float* lse_dev, float scale, void* stream) {
+  return guard([&] {
+    NONNULL(s);
+    NONNULL(k_own_dev);
+    NONNULL(v_own_dev);
+    s->impl.attend(n_req, k, doc_ids, layer0, n_layers, q_dev, n_q, g, o_dev, lse_dev, scale, nullptr, S(stream),
+                   k_own_dev, v_own_dev);
+  });
+}
 
 hr_status hr_replace(hr_store* s, void* stream) {
   return guard([&] {

@@ -100,6 +100,11 @@ struct AttnParams {
   // Key splits (flash-decoding): CTA (unit, s) attends over tiles [s n / n_split, (s+1) n / n_split) of the
   // unit's n key tiles, writes its normalised fp32 partial O and LSE to part_o / part_lse, and the last
   // split to finish (part_cnt[unit], zero between launches) merges the n_split partials into o / lse.
+  // prefill form (R30): the question's own K / V [n_req][L][Hl][n_own][D] (16-bit), attended causally after
+  // the chunk keys (row t = question token t % n_q sees own keys 0..t % n_q); n_own = 0: chunk keys only
+  const uint16_t* own_k;
+  const uint16_t* own_v;
+  uint32_t n_own;
   uint32_t n_split;          // 1: no split (part_* unused)
   float* part_o;             // [units][n_split][128][D]
   float* part_lse;           // [units][n_split][128]

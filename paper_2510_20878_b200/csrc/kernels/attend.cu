@@ -33,6 +33,8 @@
 #include <cuda_fp16.h>
 #include <cuda_fp8.h>
 
+#include <type_traits>
+
 #include "../common.h"
 #include "../kernels.h"
 
@@ -40,6 +42,9 @@ namespace harag {
 namespace {
 
 constexpr int kKT = 64;           // keys per tile
+// the question's own keys / values (prefill form, R30): 16-bit rows read in place like PASS16, keys past
+// n_own zero — an internal "scheme" of the extra doc slot k
+constexpr uint32_t kSchemeOwn = 6;
 constexpr int kRows = 128;        // MMA M
 
 __device__ __forceinline__ uint32_t saddr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -366,7 +371,7 @@ template <int DT, int SCH, bool VMAJ, uint32_t D, bool DUMP>
 __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, const uint8_t* __restrict__ smeta,
                                            const uint16_t* __restrict__ vt, uint32_t gse_m, uint32_t g_shift, uint32_t g0,
                                            uint8_t* __restrict__ dst, uint32_t dt, uint16_t* __restrict__ dump,
-                                           const uint8_t* __restrict__ g16, uint32_t t0) {
+                                           const uint8_t* __restrict__ g16, uint32_t t0, uint32_t nvalid) {
   constexpr uint32_t dcs = D / 8, nch = kKT * dcs / (32 * kDecWarps);
 #pragma unroll
   for (uint32_t i = 0; i < nch; ++i) {
@@ -378,6 +383,8 @@ __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, cons
       uint4 v;
       if constexpr (SCH == HR_S_PASS16) {  // bits unchanged: straight from global (L2-prefetched) into the operand tile
         v = __ldg(reinterpret_cast<const uint4*>(g16 + 2ull * ((t0 + key) * D + dc * 8)));
+      } else if constexpr (SCH == kSchemeOwn) {  // own rows [n_own][D]; keys past n_own are zero (masked anyway)
+        v = key < nvalid ? __ldg(reinterpret_cast<const uint4*>(g16 + 2ull * (key * D + dc * 8))) : make_uint4(0, 0, 0, 0);
       } else {
         uint2 raw;
         // the stage slot holds the tile's codes contiguously: [key][D] (1 B, or 1/2 B for INT4)
@@ -409,17 +416,20 @@ __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, cons
         }
       }
       *reinterpret_cast<uint4*>(dst + sw128_off(key, dc, kKT)) = v;
-      if constexpr (DUMP) *reinterpret_cast<uint4*>(dump + key * D + dc * 8) = v;
+      if constexpr (DUMP) {
+        if (dump) *reinterpret_cast<uint4*>(dump + key * D + dc * 8) = v;
+      }
     }
   }
 }
 template <int DT, bool VMAJ, uint32_t D, bool DUMP>
 __device__ __forceinline__ void dec_tile(uint32_t scheme, const uint8_t* stc, const uint8_t* smeta, const uint16_t* vt,
                                          uint32_t gse_m, uint32_t g_shift, uint32_t g0, uint8_t* dst, uint32_t dt,
-                                         uint16_t* dump, const uint8_t* g16, uint32_t t0) {
-#define HR_DT(S) dec_tile_s<DT, S, VMAJ, D, DUMP>(stc, smeta, vt, gse_m, g_shift, g0, dst, dt, dump, g16, t0)
+                                         uint16_t* dump, const uint8_t* g16, uint32_t t0, uint32_t nvalid) {
+#define HR_DT(S) dec_tile_s<DT, S, VMAJ, D, DUMP>(stc, smeta, vt, gse_m, g_shift, g0, dst, dt, dump, g16, t0, nvalid)
   switch (scheme) {
     case HR_S_PASS16: return HR_DT(HR_S_PASS16);
+    case kSchemeOwn: return HR_DT(kSchemeOwn);
     case HR_S_INT8: return HR_DT(HR_S_INT8);
     case HR_S_FP8E4M3: return HR_DT(HR_S_FP8E4M3);
     case HR_S_FP8E5M2: return HR_DT(HR_S_FP8E5M2);
@@ -646,7 +656,9 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
   const uint32_t tiles_per_doc = p.T / kKT;
   // this CTA's key tiles: [jt0, jt0 + n_tiles) of the unit's k * T / 64 (every split: at least one tile).
   // Pipeline indices (buffers, phases) count from 0; addressing uses the unit's tile index jt0 + j.
-  const uint32_t n_all = p.k * tiles_per_doc;
+  // + one tile of the question's own keys in the prefill form (p.n_own > 0, R30): doc slot k
+  const uint32_t n_all = p.k * tiles_per_doc + (p.n_own ? 1u : 0u);
+  const uint32_t own_tile = p.k * tiles_per_doc;  // its unit tile index (when p.n_own > 0)
   const uint32_t jt0 = (uint32_t)((uint64_t)split * n_all / p.n_split);
   const uint32_t n_tiles = (uint32_t)((uint64_t)(split + 1) * n_all / p.n_split) - jt0;
 
@@ -718,7 +730,9 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
     static_assert(kWideSoftmax, "softmax-side row sum: wide pass only");
     float psum = 0.f, lsum = 0.f;  // this tile's sum of the rounded weights; running row sum
 #endif
-    auto p_pass = [&](uint32_t s_col, uint32_t p_col) -> bool {
+    // columns >= vis of this row's tile are masked (the own tile's causal mask, R30): score -inf, weight 0
+    // MASKED: a std::integral_constant<bool>, true only for the own tile (the chunk tiles' pass carries no mask code)
+    auto p_pass = [&](auto MASKED, uint32_t s_col, uint32_t p_col, uint32_t vis) -> bool {
       const float2 c2 = make_float2(c, c), nm2 = make_float2(-m_ref, -m_ref);
       uint32_t hm = 0u;  // packed running maximum of the weights (all >= +0)
       if constexpr (kWideSoftmax) {  // the whole 64-column row in registers: both loads in flight, 32 independent pairs
@@ -726,6 +740,10 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         tmem_ld32_nw(s_col, *reinterpret_cast<uint32_t(*)[32]>(&sv[0]));
         tmem_ld32_nw(s_col + 32, *reinterpret_cast<uint32_t(*)[32]>(&sv[32]));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if constexpr (decltype(MASKED)::value) {
+#pragma unroll
+          for (uint32_t q = 0; q < (uint32_t)kKT; ++q) sv[q] = q < vis ? sv[q] : 0xFF800000u;
+        }
         uint32_t hm1 = 0u;
 #ifdef HARAG_ATT_SOFTMAX_SUM
         float2 ls2[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
@@ -749,6 +767,10 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         for (uint32_t q = 0; q < kKT / 32; ++q) {
           uint32_t sv[32], w[16];
           tmem_ld32(s_col + 32 * q, sv);
+          if constexpr (decltype(MASKED)::value) {
+#pragma unroll
+            for (uint32_t u = 0; u < 32; ++u) sv[u] = 32 * q + u < vis ? sv[u] : 0xFF800000u;
+          }
 #pragma unroll
           for (uint32_t i = 0; i < 16; ++i) {
             const float2 x = __ffma2_rn(make_float2(__uint_as_float(sv[2 * i]), __uint_as_float(sv[2 * i + 1])), c2, nm2);
@@ -771,7 +793,10 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       if (tid == 0) TR(0, j);
       tc_after();
       // one pass at the running reference m_ref (the common case: the row maximum did not grow by > tau)
-      bool grow = p_pass(s_col, p_col);
+      // the own tile (prefill form): row t is question token t % n_q, which sees own keys 0..t % n_q
+      const bool own = p.n_own && jt0 + j == own_tile;
+      const uint32_t vis = own ? min(t % p.n_q + 1, p.n_own) : (uint32_t)kKT;
+      bool grow = own ? p_pass(std::true_type{}, s_col, p_col, vis) : p_pass(std::false_type{}, s_col, p_col, vis);
       if (tid == 0) TR(8, j);
       if (__any_sync(0xFFFFFFFFu, grow)) {
         // the maximum of some row grew (always on tile 0): its row max, the O rescale, P again.  S is
@@ -783,7 +808,8 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
           uint32_t sv[32];
           tmem_ld32(s_col + 32 * q, sv);
 #pragma unroll
-          for (uint32_t u = 0; u < 32; ++u) mx4[u & 3] = fmaxf(mx4[u & 3], __uint_as_float(sv[u]));
+          for (uint32_t u = 0; u < 32; ++u)
+            if (32 * q + u < vis) mx4[u & 3] = fmaxf(mx4[u & 3], __uint_as_float(sv[u]));
         }
         const float mt = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3])) * c;  // c > 0: max(s) c = max(s c)
         if (j > 0) {
@@ -806,7 +832,8 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
 #endif
         }
         if (grow) m_ref = mt;
-        p_pass(s_col, p_col);
+        if (own) p_pass(std::true_type{}, s_col, p_col, vis);
+        else p_pass(std::false_type{}, s_col, p_col, vis);
       }
 #ifdef HARAG_ATT_SOFTMAX_SUM
       lsum += psum;
@@ -912,6 +939,15 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         d.ks = dk.scheme, d.vs = dv.scheme;
         dsrc[slot] = d;
       }
+      if (p.n_own && di == nd - 1) {  // slot k: the unit's own K / V rows [n_own][D]
+        const uint64_t orow = (((uint64_t)r * p.L + l) * p.Hl + h) * p.n_own * D;
+        DocSrc d;
+        d.kc = reinterpret_cast<const uint8_t*>(p.own_k + orow);
+        d.vc = reinterpret_cast<const uint8_t*>(p.own_v + orow);
+        d.km = d.vm = nullptr;
+        d.ks = d.vs = kSchemeOwn;
+        dsrc[p.k] = d;
+      }
       named_bar(8, nd);
     }
     uint32_t cur_slot = 0xFFFFFFFFu;
@@ -980,13 +1016,13 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       uint8_t* skd = skb + b * (kKT * D * 2);
       uint8_t* svd = svb + b * vbuf;
       {
-        uint16_t* dump = nullptr;  // test hook: the assembled KV [r][2][l][h][k*T][D]
+        uint16_t* dump = nullptr;  // test hook: the assembled KV [r][2][l][h][k*T][D] (chunk tiles only)
         if constexpr (DUMP)
-          dump = p.kv_dump + ((((uint64_t)r * 2) * p.L + l) * p.Hl + h) * p.k * p.T * D + ((uint64_t)slot * p.T + t0) * D;
+          if (slot < p.k) dump = p.kv_dump + ((((uint64_t)r * 2) * p.L + l) * p.Hl + h) * p.k * p.T * D + ((uint64_t)slot * p.T + t0) * D;
         const uint64_t kvoff = (uint64_t)p.L * p.Hl * p.k * p.T * D;
-        dec_tile<DT, false, D, DUMP>(dk.scheme, stc, smk, vtk, p.gse_m, p.g_shift, gk0, skd, dt, dump, kc, t0);
+        dec_tile<DT, false, D, DUMP>(dk.scheme, stc, smk, vtk, p.gse_m, p.g_shift, gk0, skd, dt, dump, kc, t0, p.n_own);
         dec_tile<DT, true, D, DUMP>(dv.scheme, stc + kSlotV, smv, vtv, p.gse_m, p.g_shift, gv0, svd, dt,
-                              dump ? dump + kvoff : nullptr, vc, t0);
+                              dump ? dump + kvoff : nullptr, vc, t0, p.n_own);
       }
       fence_async_smem();
       __syncwarp();
@@ -1011,6 +1047,10 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       };
       auto tile_ptrs = [&](Cur c, const uint8_t*& kp, const uint8_t*& vp, uint32_t& kb, uint32_t& vb) {
         const uint32_t slot = c.slot, t0 = c.rem * kKT;
+        if (slot >= p.k) {  // the own tile: rows read in place by the decoders, nothing to stage
+          kp = vp = nullptr, kb = vb = 0;
+          return;
+        }
         const AsmDesc* d = &p.descs[((uint64_t)r * p.k + slot) * 2];
         const uint32_t ks = d[0].scheme, vs = d[1].scheme;
         kp = d[0].codes + (uint64_t)slab_i * p.code_slab[ks] + code_bytes_of(ks, t0 * D);
@@ -1152,10 +1192,12 @@ void launch_attend(const AttnParams& p, cudaStream_t st) {
   require(p.T % kKT == 0, HR_EINVAL, "attend: tokens per chunk must be a multiple of 64");
   require(p.M >= 1 && p.M <= kRows, HR_EINVAL, "attend: g * n_q must be in [1, 128]");
   require(p.k >= 1 && p.k <= kMaxDocs, HR_EINVAL, "attend: k must be in [1, 64]");
+  require(p.n_own == 0 || (p.k < kMaxDocs && p.n_own == p.n_q && p.n_q <= (uint32_t)kKT && p.own_k && p.own_v),
+          HR_EINVAL, "attend (prefill form): own K/V needed, n_q <= 64 question tokens, k <= 63");
   const size_t smem = att_smem_bytes(p.D);
   const uint64_t units = (uint64_t)p.n_req * p.L * p.Hl;
   if (!units) return;
-  require(p.n_split >= 1 && p.n_split <= p.k * (p.T / kKT), HR_EINVAL, "attend: bad split count");
+  require(p.n_split >= 1 && p.n_split <= p.k * (p.T / kKT) + (p.n_own ? 1u : 0u), HR_EINVAL, "attend: bad split count");
   require(p.n_split == 1 || (p.part_o && p.part_lse && p.part_cnt), HR_EINVAL, "attend: split workspace missing");
   require(units * p.n_split < (1ull << 31), HR_EINVAL, "attend: too many units");
   static bool init[8] = {};  // per (dtype, D, dump) instantiation

@@ -943,13 +943,18 @@ void Store::poll_promotions(bool wait_all) {
 // the blob) into a staging-ring slot, and the launch waits for those copies.  A call's host-tier
 // items must fit the ring at once (HR_ESTATE otherwise, before any work).
 void Store::attend(uint32_t n_req, uint32_t k, const uint32_t* ids, uint32_t l0, uint32_t nl, const void* q,
-                   uint32_t n_q, uint32_t g, void* o, float* lse, float scale, void* kv_dump, cudaStream_t st) {
+                   uint32_t n_q, uint32_t g, void* o, float* lse, float scale, void* kv_dump, cudaStream_t st,
+                   const void* k_own, const void* v_own) {
   const NvtxRange nvtx_call("hr_attend");
   require(state == State::Built, HR_ESTATE, "hr_attend before the store is built");
   require(!alg2, HR_ESTATE, "hr_attend needs eager placement (demand_mode = 0)");
   require(q && o, HR_EINVAL, "NULL query or output pointer");
   require(((uintptr_t)q & 15) == 0 && ((uintptr_t)o & 15) == 0 && ((uintptr_t)kv_dump & 15) == 0, HR_EINVAL,
           "query / output pointers must be 16-byte aligned");
+  require((k_own == nullptr) == (v_own == nullptr), HR_EINVAL, "own K and V go together");
+  require(((uintptr_t)k_own & 15) == 0 && ((uintptr_t)v_own & 15) == 0, HR_EINVAL,
+          "own K / V pointers must be 16-byte aligned");
+  require(!k_own || (n_q <= 64 && k <= 63), HR_EINVAL, "prefill form: n_q <= 64 question tokens and k <= 63");
   require(g >= 1 && n_q >= 1 && (uint64_t)g * n_q <= 128, HR_EINVAL, "g * n_q must be in [1, 128]");
   require(lay.D == 64 || lay.D == 128, HR_EINVAL, "hr_attend: head_dim must be 64 or 128");
   require(lay.T % 64 == 0, HR_EINVAL, "hr_attend: tokens per chunk must be a multiple of 64");
@@ -1065,6 +1070,9 @@ void Store::attend(uint32_t n_req, uint32_t k, const uint32_t* ids, uint32_t l0,
   p.lse = lse;
   p.kv_dump = static_cast<uint16_t*>(kv_dump);
   p.n_req = n_req, p.k = k, p.L = nl, p.l0 = l0, p.Hl = lay.Hl, p.T = lay.T, p.D = lay.D, p.g = g, p.n_q = n_q;
+  p.own_k = static_cast<const uint16_t*>(k_own);
+  p.own_v = static_cast<const uint16_t*>(v_own);
+  p.n_own = k_own ? n_q : 0;
   p.M = g * n_q;
   p.G = lay.G, p.g_shift = (uint32_t)__builtin_ctz(lay.G), p.gse_e = lay.gse_e, p.gse_m = lay.gse_m;
   p.dtype = lay.dtype;
@@ -1078,8 +1086,9 @@ void Store::attend(uint32_t n_req, uint32_t k, const uint32_t* ids, uint32_t l0,
   if (!n_sms) HR_CUDA(cudaDeviceGetAttribute(&n_sms, cudaDevAttrMultiProcessorCount, cfg.device));
   const uint64_t units = (uint64_t)n_req * nl * lay.Hl;
   const char* fs = std::getenv("HARAG_ATT_SPLIT");  // tests / tuning: force the split count
-  p.n_split = fs ? (uint32_t)std::max(1, std::atoi(fs)) : attend_splits(units, k * (lay.T / 64), n_sms);
-  p.n_split = std::min<uint32_t>(p.n_split, k * (lay.T / 64));
+  const uint32_t unit_tiles = k * (lay.T / 64) + (k_own ? 1u : 0u);
+  p.n_split = fs ? (uint32_t)std::max(1, std::atoi(fs)) : attend_splits(units, unit_tiles, n_sms);
+  p.n_split = std::min<uint32_t>(p.n_split, unit_tiles);
   if (p.n_split > 1) {
     const uint64_t need = units * p.n_split * 128ull * (lay.D + 1);
     // grown rarely: cudaFree waits for the launches still reading the old buffers
@@ -1102,6 +1111,7 @@ void Store::attend(uint32_t n_req, uint32_t k, const uint32_t* ids, uint32_t l0,
   }
   // q read + o written (algorithmic), beside the codes + meta counted above
   stats.bytes_hbm_alg += 2ull * 2 * n_req * nl * lay.Hl * g * n_q * lay.D;
+  if (k_own) stats.bytes_hbm_alg += 2ull * 2 * n_req * nl * lay.Hl * n_q * lay.D;  // own K, V read
   cudaEvent_t a = nullptr, b = nullptr;
   if (timing) {
     HR_CUDA(cudaEventCreate(&a));

@@ -89,7 +89,8 @@ struct Store {
                 cudaStream_t st);
   void replace(cudaStream_t st);
   void attend(uint32_t n_req, uint32_t k, const uint32_t* ids, uint32_t l0, uint32_t nl, const void* q, uint32_t n_q,
-              uint32_t g, void* o, float* lse, float scale, void* kv_dump, cudaStream_t st);
+              uint32_t g, void* o, float* lse, float scale, void* kv_dump, cudaStream_t st,
+              const void* k_own = nullptr, const void* v_own = nullptr);
   void export_item(uint32_t item, void* dst, size_t cap, size_t* len) const;
   void get_stats(hr_stats* out);
 

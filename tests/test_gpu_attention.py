@@ -244,3 +244,42 @@ def test_attend_host_tier_items_and_layer_windows(torch_cuda, backing_pinned):
     with pytest.raises(hr.HaragError, match="ESTATE"):
         st2.attend(np.array([cold], np.uint32), q, o, 4, 1)
     st2.close()
+
+
+@pytest.mark.parametrize("split", [None, 1, 3])
+@pytest.mark.parametrize("dtype,g,n_q", [("bf16", 4, 32), ("fp16", 2, 7), ("bf16", 1, 64)])
+def test_attend_prefill_form_matches_oracle(torch_cuda, dtype, g, n_q, split, monkeypatch):
+    """hr_attend_prefill (R30): chunk keys then the question's own keys, causal on the own block — O / LSE
+    within R28's bound of the fp64 oracle (oracle.attention in prefill form), for the auto split count
+    and forced 1 / 3 splits (the own tile alone in the last split at 3: 2 docs x 1 tile + 1)."""
+    if split is not None:
+        monkeypatch.setenv("HARAG_ATT_SPLIT", str(split))
+    torch = torch_cuda
+    from oracle import numerics
+    L, H, T, D = 2, 2, 64, 128
+    st, ora, lay = build(torch, L=L, H=H, T=T, D=D, n_docs=6, ladder=PAPER, taus=(0.3, 0.3, 0.3), dtype=dtype)
+    reqs = synth.gen_requests(6, 3, 2, 1.1, seed=17)
+    n_req, k = reqs.shape
+    HQ = lay.Hl * g
+    Qb = synth.gen_query(n_req, L, HQ, n_q, D, dtype=dtype)
+    Kob = synth.gen_query(n_req, L, lay.Hl, n_q, D, seed=91, dtype=dtype)
+    Vob = synth.gen_query(n_req, L, lay.Hl, n_q, D, seed=92, dtype=dtype)
+    cu = lambda a: torch.from_numpy(a.view(np.int16)).cuda()  # noqa: E731
+    q, ko, vo = cu(Qb), cu(Kob), cu(Vob)
+    o = torch.full_like(q, 0x7FFF)
+    lse = torch.full((n_req, L, HQ, n_q), float("nan"), dtype=torch.float32, device="cuda")
+    st.attend_prefill(reqs, q, ko, vo, o, n_q, g, layers=(0, L), lse=lse)
+    torch.cuda.synchronize()
+    Og = o.cpu().numpy().view(np.uint16)
+    Ogf = (Og.astype(np.uint32) << 16).view(np.float32) if dtype == "bf16" else Og.view(np.float16).astype(np.float32)
+    lg = lse.cpu().numpy()
+    for r, req in enumerate(reqs):
+        K, V = ora.assemble(list(req))
+        O, L_ = attention.attend_request(Qb[r], K, V, g, dtype, K_own_bits=Kob[r], V_own_bits=Vob[r])
+        v = np.concatenate([numerics.to_f32(V, dtype), numerics.to_f32(Vob[r], dtype)], axis=2).astype(np.float64)
+        vr = np.empty_like(O)
+        for l in range(L):
+            for hq in range(HQ):
+                vr[l, hq] = np.max(np.abs(v[l, hq // g][None, :, :] - O[l, hq][:, None, :]), axis=1)
+        check_bound(Ogf[r].astype(np.float64), lg[r].astype(np.float64), O, L_, vr, dtype)
+    st.close()
