@@ -142,6 +142,34 @@ def fp8_decode(c: np.ndarray, variant: str) -> np.ndarray:
     return np.where(c & 0x80, -v, v)
 
 
+# ------------------------------------------------------------------- MXFP8
+# SURVEY §8(f) item 4's Blackwell-native cousin of GSE-8's shared exponents (not in the paper; DESIGN.md
+# R31): OCP-style microscaling, blocks of 32 consecutive elements share an E8M0 scale 2^(s-127), elements
+# are E4M3.  Scale exponent e = floor(log2(max |x|)) - 8 (8 = the exponent of E4M3's largest normal,
+# 448 = 1.75 * 2^8), clamped to [-127, 127]; an all-zero block takes e = -127.  Elements: the E4M3 code
+# nearest to the exact x * 2^-e (ties to even, saturating at 448: R5); decode = E4M3 value * 2^e.
+
+MX_BLOCK = 32
+
+
+def mxfp8_encode(x: np.ndarray):
+    """x: float32 [n_blocks][32] -> (codes uint8 [n_blocks][32], scales uint8 [n_blocks] = e + 127)."""
+    x = np.asarray(x, dtype=F32)
+    amax = np.max(np.abs(x.astype(np.float64)), axis=1)
+    e = np.full(amax.shape, -127, dtype=np.int64)
+    nz = amax > 0
+    e[nz] = np.array([math.frexp(float(a))[1] - 1 for a in amax[nz]], dtype=np.int64) - 8  # floor(log2) - 8
+    e = np.clip(e, -127, 127)
+    y = np.ldexp(x.astype(np.float64), -e[:, None])   # exact in fp64
+    codes = fp8_encode(y.astype(F32), "e4m3")         # |y| < 512: fp32 holds it exactly unless |y| < 2^-126
+    return codes, (e + 127).astype(np.uint8)
+
+
+def mxfp8_decode(codes: np.ndarray, scales: np.ndarray) -> np.ndarray:
+    """codes uint8 [n_blocks][32], scales uint8 [n_blocks] -> exact values (fp64)."""
+    return np.ldexp(fp8_decode(codes, "e4m3"), scales.astype(np.int64)[:, None] - 127)
+
+
 # -------------------------------------------------------------------- GSE-8
 # P:155-172.  A byte is sign | exponent index (e bits) | fraction field (m bits)
 # (R24); layouts 1+2+5, 1+3+4, 1+4+3 (P:327), default 1+4+3.

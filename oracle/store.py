@@ -25,9 +25,9 @@ import numpy as np
 
 from . import codecs, numerics
 
-PASS16, INT8, FP8E4M3, FP8E5M2, GSE8, INT4 = 0, 1, 2, 3, 4, 5
+PASS16, INT8, FP8E4M3, FP8E5M2, GSE8, INT4, MXFP8 = 0, 1, 2, 3, 4, 5, 6
 SCHEME_NAMES = {PASS16: "PASS16", INT8: "INT8", FP8E4M3: "FP8E4M3", FP8E5M2: "FP8E5M2",
-                GSE8: "GSE8", INT4: "INT4"}
+                GSE8: "GSE8", INT4: "INT4", MXFP8: "MXFP8"}
 
 
 def _a(x: int, n: int) -> int:
@@ -69,7 +69,8 @@ class Layout:
 
     def meta_record(self, scheme: int) -> int:
         ng = self.slab // self.G
-        raw = {INT8: 4 * ng, INT4: 8 * ng, GSE8: 16 + 4 * (2 << self.gse_e)}.get(scheme, 0)
+        raw = {INT8: 4 * ng, INT4: 8 * ng, GSE8: 16 + 4 * (2 << self.gse_e),
+               MXFP8: self.slab // codecs.MX_BLOCK}.get(scheme, 0)
         return _a(raw, 16)
 
     def meta_offset(self, scheme: int) -> int:
@@ -120,6 +121,10 @@ def encode_slab(bits: np.ndarray, scheme: int, lay: Layout):
         return codecs.fp8_encode(x, "e4m3"), meta
     if scheme == FP8E5M2:
         return codecs.fp8_encode(x, "e5m2"), meta
+    if scheme == MXFP8:  # R31: E8M0 scale per 32 consecutive elements, E4M3 elements
+        q, sc = codecs.mxfp8_encode(x.reshape(-1, codecs.MX_BLOCK))
+        meta[: sc.size] = sc
+        return q.reshape(-1), meta
     if scheme == GSE8:
         table = codecs.gse_slab_table(x, lay.gse_e, lay.gse_m)
         m = codecs.gse_meta(table, lay.gse_e).view(np.uint8)
@@ -147,6 +152,9 @@ def decode_slab(codes: np.ndarray, meta: np.ndarray, scheme: int, lay: Layout) -
         v = codecs.fp8_decode(codes, "e4m3")
     elif scheme == FP8E5M2:
         v = codecs.fp8_decode(codes, "e5m2")
+    elif scheme == MXFP8:
+        nb = lay.slab // codecs.MX_BLOCK
+        v = codecs.mxfp8_decode(codes.reshape(nb, codecs.MX_BLOCK), meta[:nb])
     elif scheme == GSE8:
         tab8 = meta[: 1 << lay.gse_e].view(np.int8)
         table = [int(t) for t in tab8 if t != -128]
