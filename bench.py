@@ -119,6 +119,8 @@ def alg_bytes_per_elem(scheme: str, G: int) -> float:
         return 1.0 + 16.0 / 65536 + 2.0
     if scheme == "INT4":
         return 0.5 + 8.0 / G + 2.0
+    if scheme == "MXFP8":
+        return 1.0 + 1.0 / 32 + 2.0
     return BYTES_READ[scheme] + 2.0
 
 
@@ -452,7 +454,7 @@ def run_per_scheme(ctx, wl, args):
     for i in range(NS):
         synth.gen_item_device(src[i, 0].data_ptr(), L, H, T, D, i, 0, dtype=wl["dtype"])
         synth.gen_item_device(src[i, 1].data_ptr(), L, H, T, D, i, 1, dtype=wl["dtype"])
-    for scheme in ("PASS16", "INT8", "FP8E4M3", "FP8E5M2", "GSE8", "INT4"):
+    for scheme in ("PASS16", "INT8", "FP8E4M3", "FP8E5M2", "GSE8", "INT4", "MXFP8"):
         item = hr.item_bytes(scheme, **geo)
         st = hr.Store(ladder=(scheme,), taus=(), device=ctx.device, keep_backing=False,
                       hbm_budget=2 * n_docs * item + (1 << 20), **geo)
