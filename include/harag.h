@@ -57,8 +57,11 @@ typedef enum {
   HR_S_FP8E4M3 = 2,  /* P:144; RNE, saturating at 448 (R5) */
   HR_S_FP8E5M2 = 3,  /* P:144; RNE, saturating at 57344 (R5) */
   HR_S_GSE8 = 4,     /* P:155-172; 1+e+m grouped shared exponent, per-slab array (R6-R9) */
-  HR_S_INT4 = 5      /* north_star; per-group min-max, two codes per byte (R4) */
+  HR_S_INT4 = 5,     /* north_star; per-group min-max, two codes per byte (R4) */
+  HR_S_MXFP8 = 6     /* Blackwell-style microscaling — E8M0 scale per 32 elements,
+                        E4M3 elements (R31); not in the paper's ladder, usable in any ladder */
 } hr_scheme;
+#define HR_N_SCHEMES 7
 
 typedef enum {
   HR_T_HBM = 0,      /* GPU memory (queueGPU) */

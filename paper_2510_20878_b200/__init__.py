@@ -12,10 +12,10 @@ import ctypes as C
 import numpy as np
 
 from . import _lib
-from ._lib import (FP8E4M3, FP8E5M2, GSE8, HR_BF16, HR_FP16, INT4, INT8, PASS16, R_BACKING, R_FILE, R_HBM,
+from ._lib import (FP8E4M3, FP8E5M2, GSE8, HR_BF16, HR_FP16, INT4, INT8, MXFP8, PASS16, R_BACKING, R_FILE, R_HBM,
                    R_PAGE, R_PIN, SCHEMES, T_DISK, T_HBM, T_PAGE, T_PIN, HaragError, check, lib)
 
-__all__ = ["Store", "HaragError", "SCHEMES", "PASS16", "INT8", "FP8E4M3", "FP8E5M2", "GSE8", "INT4",
+__all__ = ["Store", "HaragError", "SCHEMES", "PASS16", "INT8", "FP8E4M3", "FP8E5M2", "GSE8", "INT4", "MXFP8",
            "T_HBM", "T_PIN", "T_PAGE", "T_DISK", "R_HBM", "R_PIN", "R_PAGE", "R_BACKING", "R_FILE", "policy_rank", "policy_lists_bytes4", "policy_assign", "policy_lists_bytes",
            "policy_lists_fraction", "policy_count", "policy_epoch", "item_bytes", "Alg2",
            "exponent_histogram", "scheme_error", "guard_stats", "policy_guard"]

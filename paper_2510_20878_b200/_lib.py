@@ -16,8 +16,9 @@ HR_OK, HR_EINVAL, HR_ENOMEM, HR_ECUDA, HR_ENOTFOUND, HR_ECORRUPT, HR_ESTATE = ra
 STATUS_NAMES = {0: "HR_OK", 1: "HR_EINVAL", 2: "HR_ENOMEM", 3: "HR_ECUDA", 4: "HR_ENOTFOUND",
                 5: "HR_ECORRUPT", 6: "HR_ESTATE"}
 HR_BF16, HR_FP16 = 0, 1
-PASS16, INT8, FP8E4M3, FP8E5M2, GSE8, INT4 = range(6)
-SCHEMES = {"PASS16": PASS16, "INT8": INT8, "FP8E4M3": FP8E4M3, "FP8E5M2": FP8E5M2, "GSE8": GSE8, "INT4": INT4}
+PASS16, INT8, FP8E4M3, FP8E5M2, GSE8, INT4, MXFP8 = range(7)
+SCHEMES = {"PASS16": PASS16, "INT8": INT8, "FP8E4M3": FP8E4M3, "FP8E5M2": FP8E5M2, "GSE8": GSE8, "INT4": INT4,
+           "MXFP8": MXFP8}
 T_HBM, T_PIN, T_PAGE, T_DISK = 0, 1, 2, 3
 R_HBM, R_PIN, R_PAGE, R_BACKING, R_FILE = 1, 2, 4, 8, 16
 

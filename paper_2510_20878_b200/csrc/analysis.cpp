@@ -24,7 +24,7 @@ struct DevBuf {  // freed on every exit path
 }  // namespace
 
 void scheme_error(const hr_store_config& cfg, uint32_t scheme, const void* src, double out[2], cudaStream_t st) {
-  require(scheme <= HR_S_INT4, HR_EINVAL, "unknown scheme");
+  require(scheme < HR_N_SCHEMES, HR_EINVAL, "unknown scheme");
   require(src != nullptr && out != nullptr, HR_EINVAL, "NULL pointer");
   require(reinterpret_cast<uintptr_t>(src) % 16 == 0, HR_EINVAL, "source must be 16-byte aligned");
   const Layout lay = make_layout(cfg);
@@ -64,7 +64,7 @@ void scheme_error(const hr_store_config& cfg, uint32_t scheme, const void* src, 
   p.gse_m = lay.gse_m;
   p.dtype = lay.dtype;
   p.slab = (uint32_t)lay.slab();
-  for (uint32_t s = 0; s <= HR_S_INT4; ++s) p.meta_stride[s] = (uint32_t)lay.meta_stride(s);
+  for (uint32_t s = 0; s < HR_N_SCHEMES; ++s) p.meta_stride[s] = (uint32_t)lay.meta_stride(s);
   launch_assemble(p, 1u << scheme, st);
   double* res = part.as<double>() + 2 * n_part;
   launch_error(static_cast<const uint16_t*>(src), y.as<uint16_t>(), lay.L, lay.H, lay.Hl, lay.h0, lay.slab(),

@@ -354,7 +354,7 @@ hr_status hr_item_bytes(const hr_store_config* cfg, uint32_t scheme, uint64_t* b
   return guard([&] {
     NONNULL(cfg);
     NONNULL(bytes);
-    harag::require(scheme <= HR_S_INT4, HR_EINVAL, "unknown scheme");
+    harag::require(scheme < HR_N_SCHEMES, HR_EINVAL, "unknown scheme");
     *bytes = harag::make_layout(*cfg).item_bytes(scheme);
   });
 }

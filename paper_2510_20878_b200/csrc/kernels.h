@@ -49,7 +49,7 @@ struct AsmParams {
   uint32_t tiles_per_slab;   // ceil(slab / tile_e)
   uint32_t meta_stage;       // bytes of meta window per stage (multiple of 128)
   uint64_t n_tiles;          // n_desc * L * Hl * tiles_per_slab
-  uint32_t meta_stride[6];   // per scheme, bytes per slab record
+  uint32_t meta_stride[HR_N_SCHEMES];  // per scheme, bytes per slab record
   // Tail balancing: tiles [n_tiles - dyn_tiles, n_tiles) are claimed in chunks of dyn_chunk through an
   // atomic counter (sched[0]; sched[1] counts producers done, the last one zeroes both), the rest are
   // split in blocks.  sched == nullptr: blocked split only.
@@ -95,8 +95,8 @@ struct AttnParams {
   uint32_t l0;               // first store layer of the window (q / o / lse / kv_dump index layers 0..L-1)
   uint32_t G, g_shift, gse_e, gse_m, dtype;
   float scale_log2;          // softmax scale * log2(e)
-  uint64_t code_slab[6];     // per scheme, code bytes per slab
-  uint32_t meta_stride[6];   // per scheme, bytes per slab meta record
+  uint64_t code_slab[HR_N_SCHEMES];    // per scheme, code bytes per slab
+  uint32_t meta_stride[HR_N_SCHEMES];  // per scheme, bytes per slab meta record
   // Key splits (flash-decoding): CTA (unit, s) attends over tiles [s n / n_split, (s+1) n / n_split) of the
   // unit's n key tiles, writes its normalised fp32 partial O and LSE to part_o / part_lse, and the last
   // split to finish (part_cnt[unit], zero between launches) merges the n_split partials into o / lse.

@@ -169,9 +169,12 @@ __device__ __forceinline__ void produce(const AsmParams& p, const Smem& sm) {
       const uint8_t* csrc = d.codes + (uint64_t)slab_i * code_bytes(d.scheme, p.slab) + code_bytes(d.scheme, e0);
       uint32_t mb = 0, moff = 0;
       const uint8_t* msrc = nullptr;
-      if (d.scheme == HR_S_INT8 || d.scheme == HR_S_INT4) {
-        const uint32_t me = d.scheme == HR_S_INT8 ? 4u : 8u;
-        const uint32_t g0 = e0 >> p.g_shift, g1 = (e0 + n_el + p.G - 1) >> p.g_shift;
+      if (d.scheme == HR_S_INT8 || d.scheme == HR_S_INT4 || d.scheme == HR_S_MXFP8) {
+        // the tile's window of group records: INT8 fp32 s, INT4 (s, mn) per group of G; MXFP8 one E8M0
+        // byte per 32 elements
+        const bool mx = d.scheme == HR_S_MXFP8;
+        const uint32_t me = d.scheme == HR_S_INT8 ? 4u : mx ? 1u : 8u, gs = mx ? 5u : p.g_shift;
+        const uint32_t g0 = e0 >> gs, g1 = (e0 + n_el + (1u << gs) - 1) >> gs;
         const uint32_t b0 = (g0 * me) & ~15u, b1 = (g1 * me + 15u) & ~15u;
         msrc = d.meta + (uint64_t)slab_i * p.meta_stride[d.scheme] + b0;
         mb = b1 - b0;
@@ -288,6 +291,28 @@ __device__ __forceinline__ void decode_fp8(const TileHdr& h, const uint8_t* code
   }
 }
 
+// MXFP8 (R31): E4M3 value (exact, via fp16) times 2^(s - 127) (exact in fp32: >= 2^-136), then one RNE
+// to the output dtype; the 8 elements of a chunk share one block (chunks are 8-aligned, blocks 32)
+template <int DT>
+__device__ __forceinline__ void decode_mxfp8(const TileHdr& h, const uint8_t* codes, const uint8_t* meta, int ctid) {
+  const uint8_t* sc = meta + h.meta_off;
+#pragma unroll 2
+  for (uint32_t e = ctid * 8; e < h.n_el; e += kChunkStride) {
+    const uint2 c = *reinterpret_cast<const uint2*>(codes + e);
+    const uint32_t sb = sc[e >> 5];
+    const float m = sb ? __uint_as_float(sb << 23) : __uint_as_float(0x00400000u);  // 2^(s-127); s = 0: 2^-127
+    const uint32_t w[4] = {c.x & 0xFFFFu, c.x >> 16, c.y & 0xFFFFu, c.y >> 16};
+    uint32_t o[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      __half2_raw hr = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)w[i], __NV_E4M3);  // exact
+      const float2 f = __fmul2_rn(__half22float2(*reinterpret_cast<__half2*>(&hr)), make_float2(m, m));
+      o[i] = pack2<DT>(f.x, f.y);
+    }
+    st_v4(h.out + 2ull * e, o[0], o[1], o[2], o[3]);
+  }
+}
+
 __device__ __forceinline__ float lds_f32(uint32_t addr) {
   float v;
   asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
@@ -349,6 +374,9 @@ __device__ __forceinline__ void consume(const AsmParams& p, const Smem& sm, int 
         break;
       case HR_S_FP8E5M2:
         decode_fp8<DT, HR_S_FP8E5M2>(h, codes, ctid);
+        break;
+      case HR_S_MXFP8:
+        decode_mxfp8<DT>(h, codes, meta, ctid);
         break;
       case HR_S_GSE8:
         if (p.gse_m == 3)
@@ -435,6 +463,7 @@ void launch_assemble(AsmParams p, uint32_t scheme_mask, cudaStream_t st, int gri
   if (scheme_mask & (1u << HR_S_INT8)) meta = std::max(meta, 4 * groups + 32);
   if (scheme_mask & (1u << HR_S_INT4)) meta = std::max(meta, 8 * groups + 32);
   if (scheme_mask & (1u << HR_S_GSE8)) meta = std::max(meta, p.meta_stride[HR_S_GSE8]);
+  if (scheme_mask & (1u << HR_S_MXFP8)) meta = std::max(meta, p.tile_e / 32 + 32);
   p.meta_stage = (meta + 255) / 256 * 256;  // 256-B-aligned records (GSE-8 table addressing)
   require(p.meta_stage <= kMaxMetaStage, HR_EINVAL, "group too small for the assemble tile");
   const size_t smem = smem_bytes(p.meta_stage);

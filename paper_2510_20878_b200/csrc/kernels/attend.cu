@@ -42,7 +42,7 @@ namespace {
 constexpr int kKT = 64;           // keys per tile
 // the question's own keys / values (prefill form, R30): 16-bit rows read in place like PASS16, keys past
 // n_own zero — an internal "scheme" of the extra doc slot k
-constexpr uint32_t kSchemeOwn = 6;
+constexpr uint32_t kSchemeOwn = HR_N_SCHEMES;
 constexpr int kRows = 128;        // MMA M
 
 __device__ __forceinline__ uint32_t saddr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -335,6 +335,17 @@ __device__ __forceinline__ uint4 dec_raw8(uint32_t scheme, const uint4& c, const
         o[i] = pack2<DT>(__fadd_rn(__fmul_rn(q[i].x, m.x), m.y), __fadd_rn(__fmul_rn(q[i].y, m.x), m.y));
       return make_uint4(o[0], o[1], o[2], o[3]);
     }
+    case HR_S_MXFP8: {  // R31: exact E4M3 value (via fp16) times 2^(s-127) in fp32, one RNE to the dtype
+      const uint32_t w[4] = {c.x & 0xFFFFu, c.x >> 16, c.y & 0xFFFFu, c.y >> 16};
+      uint32_t o[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        __half2_raw hr = __nv_cvt_fp8x2_to_halfraw2((__nv_fp8x2_storage_t)w[i], __NV_E4M3);
+        const float2 f = __fmul2_rn(__half22float2(*reinterpret_cast<__half2*>(&hr)), make_float2(m.x, m.x));
+        o[i] = pack2<DT>(f.x, f.y);
+      }
+      return make_uint4(o[0], o[1], o[2], o[3]);
+    }
     case HR_S_FP8E4M3:
       return make_uint4(fp8_pair<DT, 0>(c.x, 0x4140u, 0x1404u), fp8_pair<DT, 0>(c.x, 0x4342u, 0x3424u),
                         fp8_pair<DT, 0>(c.y, 0x4140u, 0x1404u), fp8_pair<DT, 0>(c.y, 0x4342u, 0x3424u));
@@ -407,9 +418,14 @@ __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, cons
 #endif
         } else {
           float2 m = make_float2(0.f, 0.f);
-          const uint32_t g = ((((t0 + key) * D + dc * 8)) >> g_shift) - g0;  // group index in the tile window
+          const uint32_t gsh = SCH == HR_S_MXFP8 ? 5u : g_shift;
+          const uint32_t g = ((((t0 + key) * D + dc * 8)) >> gsh) - g0;  // group index in the tile window
           if (SCH == HR_S_INT8) m.x = reinterpret_cast<const float*>(smeta)[g];
           if (SCH == HR_S_INT4) m = reinterpret_cast<const float2*>(smeta)[g];
+          if (SCH == HR_S_MXFP8) {  // 2^(s - 127); s = 0: 2^-127 (an fp32 subnormal)
+            const uint32_t sb = smeta[g];
+            m.x = sb ? __uint_as_float(sb << 23) : __uint_as_float(0x00400000u);
+          }
           v = dec_raw8<DT>(SCH, make_uint4(raw.x, raw.y, 0u, 0u), m, 0u, nullptr);
         }
       }
@@ -432,6 +448,7 @@ __device__ __forceinline__ void dec_tile(uint32_t scheme, const uint8_t* stc, co
     case HR_S_FP8E4M3: return HR_DT(HR_S_FP8E4M3);
     case HR_S_FP8E5M2: return HR_DT(HR_S_FP8E5M2);
     case HR_S_INT4: return HR_DT(HR_S_INT4);
+    case HR_S_MXFP8: return HR_DT(HR_S_MXFP8);
     default: return HR_DT(HR_S_GSE8);
   }
 #undef HR_DT
@@ -446,11 +463,13 @@ __device__ __forceinline__ void cp_async(void* smem, const void* gmem) {
 
 // the tile's window of group meta (INT8: fp32 scale, INT4: (scale, min) per group) -> shared memory,
 // 4-byte copies spread over the group's threads; returns the first group index of the window
+// (MXFP8: one E8M0 byte per 32 elements, R31)
 __device__ __forceinline__ uint32_t stage_meta(uint32_t scheme, const uint8_t* meta, uint32_t t0, uint32_t D,
                                                uint32_t g_shift, uint8_t* sm, uint32_t dt) {
+  if (scheme == HR_S_MXFP8) g_shift = 5;
   const uint32_t g0 = (t0 * D) >> g_shift;
-  if (scheme != HR_S_INT8 && scheme != HR_S_INT4) return g0;
-  const uint32_t me = scheme == HR_S_INT8 ? 4u : 8u;
+  if (scheme != HR_S_INT8 && scheme != HR_S_INT4 && scheme != HR_S_MXFP8) return g0;
+  const uint32_t me = scheme == HR_S_INT8 ? 4u : scheme == HR_S_MXFP8 ? 1u : 8u;
   const uint32_t g1 = ((t0 + kKT) * D - 1) >> g_shift;  // last group of the tile
   const uint32_t words = (g1 - g0 + 1) * me / 4;
   for (uint32_t w = dt; w < words; w += 32 * kDecWarps) cp_async<4>(sm + 4 * w, meta + (uint64_t)g0 * me + 4 * w);

@@ -79,8 +79,8 @@ struct QBatch {
   uint32_t L, H, Hl, h0, T, D, G, g_shift, gse_e, gse_m, dtype;
   uint32_t slab, tile_e, tiles_per_slab;
   uint64_t n_tiles;
-  uint64_t code_slab[6], meta_off[6];
-  uint32_t meta_stride[6];
+  uint64_t code_slab[HR_N_SCHEMES], meta_off[HR_N_SCHEMES];
+  uint32_t meta_stride[HR_N_SCHEMES];
   int* err;
   // tail balancing (as assemble_kv_kernel): the last dyn_tiles tiles are claimed in chunks of dyn_chunk
   // through sched[0..1] (u64 counter; sched[2] counts producers done, the last one zeroes both); the rest
@@ -364,6 +364,32 @@ __device__ __forceinline__ void enc_fp8(const uint4& raw, uint8_t* codes, uint32
   *reinterpret_cast<uint2*>(codes + e) = make_uint2(__byte_perm(c[0], c[1], 0x5410), __byte_perm(c[2], c[3], 0x5410));
 }
 
+// ------------------------------------------------------------------ MXFP8 (R31)
+// A 32-element block = the 8 elements of each of 4 consecutive lanes.  Block max |x| from 16-bit magnitude
+// patterns (two shuffles), e = max(ef(max) - 127 - 8, -127) (ef = 0, a zero block or an fp32-subnormal
+// maximum: -127), elements = satfinite RNE E4M3 of x * 2^-e (exact: |x * 2^-e| < 512, and below 2^-126 the
+// E4M3 rounding is 0 either way), scale byte e + 127 written by the block's first lane.
+template <int DT>
+__device__ __forceinline__ void enc_mxfp8(const uint4& raw, uint8_t* codes, uint8_t* scales, uint32_t e,
+                                          uint32_t lane, uint32_t& nan_acc) {
+  const uint32_t pm = absmax_pair(raw);
+  nan_acc = __vmaxu2(nan_acc, pm);
+  uint32_t am = max(pm & 0xFFFFu, pm >> 16);
+  am = max(am, __shfl_xor_sync(0xFFFFFFFFu, am, 1));
+  am = max(am, __shfl_xor_sync(0xFFFFFFFFu, am, 2));
+  const uint32_t ef = DT == HR_BF16 ? (am >> 7) : ((__float_as_uint(__half2float(__ushort_as_half((unsigned short)am))) >> 23) & 0xFFu);
+  const int ex = ef == 0 ? -127 : max((int)ef - 135, -127);
+  const float inv = __uint_as_float((uint32_t)(127 - ex) << 23);  // 2^-e, a normal fp32 (127 - e in [8, 254])
+  float2 x[4];
+  unpack8<DT>(raw, x);
+  uint32_t c[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    c[i] = __nv_cvt_float2_to_fp8x2(__fmul2_rn(x[i], make_float2(inv, inv)), __NV_SATFINITE, __NV_E4M3);
+  *reinterpret_cast<uint2*>(codes + e) = make_uint2(__byte_perm(c[0], c[1], 0x5410), __byte_perm(c[2], c[3], 0x5410));
+  if ((lane & 3) == 0) scales[e >> 5] = (uint8_t)(ex + 127);
+}
+
 // ------------------------------------------------------------------ GSE-8
 // Table entry per fp32 biased exponent ef of the slab (built by the producer warp):
 //   bits 24..30 and 8..14   idx << m   (idx: smallest G_i >= E)
@@ -490,7 +516,8 @@ __device__ __forceinline__ void q_produce(const QBatch& p, const QSmem& sm, int 
       if (lane == 0) {
         QHdr& h = sm.hdr()[stage];
         h.codes = jb.dst + (uint64_t)slab_i * p.code_slab[scheme] + code_bytes(scheme, e0);
-        h.meta = scheme == HR_S_INT8 ? meta + 4 * (e0 >> p.g_shift) : scheme == HR_S_INT4 ? meta + 8 * (e0 >> p.g_shift) : meta;
+        h.meta = scheme == HR_S_INT8 ? meta + 4 * (e0 >> p.g_shift) : scheme == HR_S_INT4 ? meta + 8 * (e0 >> p.g_shift)
+             : scheme == HR_S_MXFP8 ? meta + (e0 >> 5) : meta;
         h.range = jb.range ? jb.range + 2 * slab_i : nullptr;
         h.n_el = n_el;
         h.scheme = scheme;
@@ -578,6 +605,13 @@ __device__ __forceinline__ void encode_tile(const QBatch& p, const QHdr& h, cons
         enc_gse<DT>(*reinterpret_cast<const uint4*>(tile + 2 * e), h.codes, gtab_addr, e, nan_acc);
       }
       break;
+    case HR_S_MXFP8:  // h.meta: the tile's first scale byte
+#pragma unroll 2
+      for (uint32_t c = cw; c < n_ch; c += NW) {
+        const uint32_t e = c * kChunk + lane * 8;
+        enc_mxfp8<DT>(*reinterpret_cast<const uint4*>(tile + 2 * e), h.codes, h.meta, e, lane, nan_acc);
+      }
+      break;
     default:
       break;
   }
@@ -627,7 +661,8 @@ __global__ void __launch_bounds__(32 * kTileWarps) quant_tile_kernel(const __gri
   QHdr h;
   uint8_t* meta = jb.dst + p.meta_off[scheme] + (uint64_t)slab_i * p.meta_stride[scheme];
   h.codes = jb.dst + (uint64_t)slab_i * p.code_slab[scheme] + code_bytes(scheme, e0);
-  h.meta = scheme == HR_S_INT8 ? meta + 4 * (e0 >> p.g_shift) : scheme == HR_S_INT4 ? meta + 8 * (e0 >> p.g_shift) : meta;
+  h.meta = scheme == HR_S_INT8 ? meta + 4 * (e0 >> p.g_shift) : scheme == HR_S_INT4 ? meta + 8 * (e0 >> p.g_shift)
+             : scheme == HR_S_MXFP8 ? meta + (e0 >> 5) : meta;
   h.range = nullptr;
   h.n_el = n_el;
   h.scheme = scheme;
@@ -1023,7 +1058,9 @@ bool use_tile_kernel() {
   }
   return v != 0;
 }
-inline bool tile_scheme(uint32_t s) { return s == HR_S_PASS16 || s == HR_S_FP8E4M3 || s == HR_S_FP8E5M2; }
+inline bool tile_scheme(uint32_t s) {
+  return s == HR_S_PASS16 || s == HR_S_FP8E4M3 || s == HR_S_FP8E5M2 || s == HR_S_MXFP8;
+}
 
 template <int DT, int SEG>
 void launch_tile(const QBatch& b, cudaStream_t st) {
@@ -1118,7 +1155,7 @@ void launch_quantize(const QuantParams* items, int n, cudaStream_t st) {
   base.err = q0.err;
   for (int i = 0; i < n; ++i) {
     const QuantParams& q = items[i];
-    require(q.scheme <= HR_S_INT4, HR_EINVAL, "unknown scheme");
+    require(q.scheme < HR_N_SCHEMES, HR_EINVAL, "unknown scheme");
     require(q.L == q0.L && q.H == q0.H && q.Hl == q0.Hl && q.h0 == q0.h0 && q.T == q0.T && q.D == q0.D &&
                 q.G == q0.G && q.dtype == q0.dtype && q.gse_m == q0.gse_m && q.err == q0.err,
             HR_EINVAL, "a quantize batch shares one layout");

@@ -19,7 +19,8 @@ struct Layout {
   uint64_t meta_raw_slab(uint32_t s) const {
     const uint64_t ng = slab() / G;
     // GSE8: int8 array [2^e] padded to 16 B + fp32 decode table [2^(e+1)]
-    return s == HR_S_INT8 ? 4 * ng : s == HR_S_INT4 ? 8 * ng : s == HR_S_GSE8 ? 16 + 4 * (2ull << gse_e) : 0;
+    return s == HR_S_INT8 ? 4 * ng : s == HR_S_INT4 ? 8 * ng : s == HR_S_GSE8 ? 16 + 4 * (2ull << gse_e)
+           : s == HR_S_MXFP8 ? slab() / 32 : 0;
   }
   uint64_t meta_stride(uint32_t s) const { return align_up(meta_raw_slab(s), 16); }
   uint64_t meta_offset(uint32_t s) const { return align_up(n_slabs() * code_bytes_slab(s), 256); }

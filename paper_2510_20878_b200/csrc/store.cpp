@@ -64,7 +64,7 @@ void FreeList::release(uint64_t off, uint64_t size) {
 // ---------------------------------------------------------------- Store
 Store::Store(const hr_store_config& c) : cfg(c), lay(make_layout(c)) {
   require(cfg.n_ladder >= 1 && cfg.n_ladder <= 6, HR_EINVAL, "n_ladder must be 1..6");
-  for (uint32_t j = 0; j < cfg.n_ladder; ++j) require(cfg.ladder[j] <= HR_S_INT4, HR_EINVAL, "unknown scheme in ladder");
+  for (uint32_t j = 0; j < cfg.n_ladder; ++j) require(cfg.ladder[j] < HR_N_SCHEMES, HR_EINVAL, "unknown scheme in ladder");
   double sum = 0;
   for (uint32_t j = 0; j + 1 < cfg.n_ladder; ++j) {
     require(cfg.tau[j] >= 0.0 && cfg.tau[j] <= 1.0, HR_EINVAL, "tau out of [0,1]");
@@ -509,7 +509,7 @@ void Store::launch(const AsmDesc* dev_descs, const AsmDesc* host_descs, uint32_t
   p.gse_m = lay.gse_m;
   p.dtype = lay.dtype;
   p.slab = (uint32_t)lay.slab();
-  for (uint32_t s = 0; s <= HR_S_INT4; ++s) p.meta_stride[s] = (uint32_t)lay.meta_stride(s);
+  for (uint32_t s = 0; s < HR_N_SCHEMES; ++s) p.meta_stride[s] = (uint32_t)lay.meta_stride(s);
   if (asm_dyn_pct) {
     if (!asm_sched) {
       HR_CUDA(cudaMalloc((void**)&asm_sched, 64 * 16));
@@ -1078,7 +1078,7 @@ void Store::attend(uint32_t n_req, uint32_t k, const uint32_t* ids, uint32_t l0,
   p.dtype = lay.dtype;
   const float sc = scale > 0.f ? scale : 1.f / std::sqrt((float)lay.D);
   p.scale_log2 = sc * 1.4426950408889634f;
-  for (uint32_t s = 0; s <= HR_S_INT4; ++s) {
+  for (uint32_t s = 0; s < HR_N_SCHEMES; ++s) {
     p.code_slab[s] = lay.code_bytes_slab(s);
     p.meta_stride[s] = (uint32_t)lay.meta_stride(s);
   }
@@ -1383,7 +1383,7 @@ void Store::build_from_file(const char* path, cudaStream_t st) {
   std::vector<uint32_t> sc(ni);
   pread_all(fd, hot.data(), ni * sizeof(uint64_t), sizeof hd, P);
   pread_all(fd, sc.data(), ni * sizeof(uint32_t), sizeof hd + ni * sizeof(uint64_t), P);
-  for (uint32_t v : sc) require(v <= HR_S_INT4, HR_ECORRUPT, "bad scheme in store file");
+  for (uint32_t v : sc) require(v < HR_N_SCHEMES, HR_ECORRUPT, "bad scheme in store file");
   const bool on_disk = cfg.disk_backing != 0;
   setup(nd, hot.data(), std::move(sc), on_disk);
   disk_off = file_offsets(hd.data_offset);

@@ -30,7 +30,7 @@ from oracle import store as ost  # noqa: E402
 # cp.async.bulk shared -> global, which initcheck does not see as initialising device memory)
 NO_PASS16 = bool(os.environ.get("HARAG_SAN_NO_PASS16"))
 NAMES = {"PASS16": ost.PASS16, "INT8": ost.INT8, "FP8E4M3": ost.FP8E4M3, "FP8E5M2": ost.FP8E5M2,
-         "GSE8": ost.GSE8, "INT4": ost.INT4}
+         "GSE8": ost.GSE8, "INT4": ost.INT4, "MXFP8": ost.MXFP8}
 
 
 def make(L, H, T, D, n_docs, ladder, taus, dtype="bf16", group=0, hbm_items=None, pin_items=0, pinned=False):

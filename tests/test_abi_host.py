@@ -52,7 +52,7 @@ def test_config_validation():
     assert list(hr.policy_assign(np.arange(8), ["INT8", "GSE8"], [0.25])) == [4] * 6 + [1] * 2
 
 
-@pytest.mark.parametrize("scheme", ["PASS16", "INT8", "FP8E4M3", "FP8E5M2", "GSE8", "INT4"])
+@pytest.mark.parametrize("scheme", ["PASS16", "INT8", "FP8E4M3", "FP8E5M2", "GSE8", "INT4", "MXFP8"])
 @pytest.mark.parametrize("shape", [(2, 2, 64, 64, 0, 1), (32, 8, 128, 512, 0, 2), (3, 4, 64, 100, 64, 1),
                                    (32, 32, 128, 512, 65536, 1)])
 def test_item_bytes_match_oracle_format(scheme, shape):

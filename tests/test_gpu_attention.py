@@ -17,7 +17,7 @@ from oracle import store as ost
 pytestmark = pytest.mark.gpu
 
 NAMES = {"PASS16": ost.PASS16, "INT8": ost.INT8, "FP8E4M3": ost.FP8E4M3, "FP8E5M2": ost.FP8E5M2,
-         "GSE8": ost.GSE8, "INT4": ost.INT4}
+         "GSE8": ost.GSE8, "INT4": ost.INT4, "MXFP8": ost.MXFP8}
 PAPER = ("INT8", "FP8E4M3", "FP8E5M2", "GSE8")
 NORTH = ("PASS16", "INT8", "INT4")
 
@@ -99,6 +99,8 @@ def run_case(torch, st, ora, lay, reqs, n_q, g, dtype, scale=None, layers=None):
     (PAPER, "bf16", 128, 128, 4, 32, 0),       # M = 128
     (PAPER, "bf16", 128, 64, 3, 5, 64),        # ragged M = 15
     (("GSE8", "INT4"), "bf16", 64, 128, 1, 1, 0),  # decode-shaped M = 1
+    (("MXFP8", "GSE8"), "bf16", 128, 64, 4, 32, 0),  # microscaled FP8 (R31)
+    (("PASS16", "MXFP8"), "fp16", 64, 128, 2, 8, 0),
 ])
 def test_attend_matches_oracle(torch_cuda, ladder, dtype, D, T, g, n_q, group):
     taus = (0.3,) * (len(ladder) - 1)

@@ -11,7 +11,7 @@ from oracle import store as ost
 pytestmark = pytest.mark.gpu
 
 NAMES = {"PASS16": ost.PASS16, "INT8": ost.INT8, "FP8E4M3": ost.FP8E4M3, "FP8E5M2": ost.FP8E5M2,
-         "GSE8": ost.GSE8, "INT4": ost.INT4}
+         "GSE8": ost.GSE8, "INT4": ost.INT4, "MXFP8": ost.MXFP8}
 PAPER = ("INT8", "FP8E4M3", "FP8E5M2", "GSE8")
 NORTH = ("PASS16", "INT8", "INT4")
 
