@@ -375,14 +375,20 @@ __device__ __forceinline__ uint4 dec_raw8(uint32_t scheme, const uint4& c, const
 
 // Decode one operand tile (this decoder thread's kDecChunks chunks of 8 elements) with the scheme
 // resolved ONCE per tile: a runtime switch over compile-time-specialised loops (a per-chunk switch
-// made the decode loop branch-bound).  VMAJ: V's MN-major layout, else K's K-major layout.
-template <int DT, int SCH, bool VMAJ, uint32_t D, bool DUMP>
+// made the decode loop branch-bound).  K and V tiles share the code: both are SW128 rows of 64 keys.
+template <int DT, int SCH, uint32_t D, bool DUMP>
 __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, const uint8_t* __restrict__ smeta,
                                            const uint16_t* __restrict__ vt, uint32_t gse_m, uint32_t g_shift, uint32_t g0,
                                            uint8_t* __restrict__ dst, uint32_t dt, uint16_t* __restrict__ dump,
                                            const uint8_t* __restrict__ g16, uint32_t t0, uint32_t nvalid) {
   constexpr uint32_t dcs = D / 8, nch = kKT * dcs / (32 * kDecWarps);
-#pragma unroll
+  // full unroll for the paper ladder's schemes; the rest (PASS16, INT4, MXFP8, own rows) by 2 (code size)
+#ifndef HARAG_ATT_UNROLL_ALL
+  constexpr int kUnroll = (SCH == HR_S_GSE8 || SCH == HR_S_INT8 || SCH == HR_S_FP8E4M3 || SCH == HR_S_FP8E5M2) ? (int)nch : 2;
+#else
+  constexpr int kUnroll = (int)nch;
+#endif
+#pragma unroll kUnroll
   for (uint32_t i = 0; i < nch; ++i) {
     const uint32_t cc = dt + i * 32 * kDecWarps;
     {
@@ -436,11 +442,11 @@ __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, cons
     }
   }
 }
-template <int DT, bool VMAJ, uint32_t D, bool DUMP>
+template <int DT, uint32_t D, bool DUMP>
 __device__ __forceinline__ void dec_tile(uint32_t scheme, const uint8_t* stc, const uint8_t* smeta, const uint16_t* vt,
                                          uint32_t gse_m, uint32_t g_shift, uint32_t g0, uint8_t* dst, uint32_t dt,
                                          uint16_t* dump, const uint8_t* g16, uint32_t t0, uint32_t nvalid) {
-#define HR_DT(S) dec_tile_s<DT, S, VMAJ, D, DUMP>(stc, smeta, vt, gse_m, g_shift, g0, dst, dt, dump, g16, t0, nvalid)
+#define HR_DT(S) dec_tile_s<DT, S, D, DUMP>(stc, smeta, vt, gse_m, g_shift, g0, dst, dt, dump, g16, t0, nvalid)
   switch (scheme) {
     case HR_S_PASS16: return HR_DT(HR_S_PASS16);
     case kSchemeOwn: return HR_DT(kSchemeOwn);
@@ -814,9 +820,14 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
       // the own tile (prefill form): row t is question token t % n_q, which sees own keys 0..t % n_q
       const bool own = p.n_own && jt0 + j == own_tile;
       const uint32_t vis = own ? min(t % p.n_q + 1, p.n_own) : (uint32_t)kKT;
-      bool grow = p_pass(s_col, p_col, vis);
-      if (tid == 0) TR(8, j);
-      if (__any_sync(0xFFFFFFFFu, grow)) {
+      // one call site of the (large, unrolled) pass: the second iteration is the rare re-pass after a row
+      // maximum grew (a second inlined copy cost instruction-cache misses)
+#pragma unroll 1
+      for (uint32_t pass = 0; pass < 2; ++pass) {
+      const bool grow = p_pass(s_col, p_col, vis);
+      if (tid == 0 && pass == 0) TR(8, j);
+      if (pass == 1 || !__any_sync(0xFFFFFFFFu, grow)) break;
+      {
         // the maximum of some row grew (always on tile 0): its row max, the O rescale, P again.  S is
         // intact (P has its own TMEM columns); the first pass's P stores complete before P is rewritten.
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -850,7 +861,7 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
 #endif
         }
         if (grow) m_ref = mt;
-        p_pass(s_col, p_col, vis);
+      }
       }
 #ifdef HARAG_ATT_SOFTMAX_SUM
       lsum += psum;
@@ -1037,9 +1048,12 @@ __global__ void __launch_bounds__(kAttThreads2, 1) attend_kernel(const __grid_co
         if constexpr (DUMP)
           if (slot < p.k) dump = p.kv_dump + ((((uint64_t)r * 2) * p.L + l) * p.Hl + h) * p.k * p.T * D + ((uint64_t)slot * p.T + t0) * D;
         const uint64_t kvoff = (uint64_t)p.L * p.Hl * p.k * p.T * D;
-        dec_tile<DT, false, D, DUMP>(dk.scheme, stc, smk, vtk, p.gse_m, p.g_shift, gk0, skd, dt, dump, kc, t0, p.n_own);
-        dec_tile<DT, true, D, DUMP>(dv.scheme, stc + kSlotV, smv, vtv, p.gse_m, p.g_shift, gv0, svd, dt,
-                              dump ? dump + kvoff : nullptr, vc, t0, p.n_own);
+        // K then V through one call site (one inlined copy of the per-scheme loops: instruction cache)
+#pragma unroll 1
+        for (uint32_t kv = 0; kv < 2; ++kv)
+          dec_tile<DT, D, DUMP>(kv ? dv.scheme : dk.scheme, kv ? stc + kSlotV : stc, kv ? smv : smk, kv ? vtv : vtk,
+                                p.gse_m, p.g_shift, kv ? gv0 : gk0, kv ? svd : skd, dt,
+                                dump ? (kv ? dump + kvoff : dump) : nullptr, kv ? vc : kc, t0, p.n_own);
       }
       fence_async_smem();
       __syncwarp();

@@ -809,13 +809,29 @@ __device__ __forceinline__ uint32_t and_or(uint32_t a, uint32_t b) {
 // negative value already carries its sign bit (bits 31 and 15), so the code of the high bf16 of a word w
 // is byte 3 of ent | ({1.fraction : 0} >> (31 - keep)), of the low bf16 byte 1 of the same with the
 // 8-bit significand.  A flushed value's entry is 0 for either sign.
-__device__ __forceinline__ void enc_gse_sx(const uint4& raw, uint8_t* codes, uint32_t tab, uint32_t e) {
+#ifdef HARAG_GSE_IMAD_ADDR
+__device__ __forceinline__ uint32_t mad_hi_u32(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t d;
+  asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+#endif
+__device__ __forceinline__ void enc_gse_sx(const uint4& raw, uint8_t* codes, uint32_t tab, uint32_t e,
+                                           uint32_t k11 = 1u << 11, uint32_t k27 = 1u << 27) {
   const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
   uint32_t c[8];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
+#ifdef HARAG_GSE_IMAD_ADDR
+    // entry addresses on the FMA pipe: tab + 4 * (sign|exponent) = mad.hi(w & mask, 2^k, tab)
+    // (the multipliers arrive as opaque register values: with literal powers of two ptxas turns the
+    // mad.hi back into an ALU shift)
+    const uint32_t eh = lds32(mad_hi_u32(w[i] & 0xFF800000u, k11, tab));
+    const uint32_t el = lds32(mad_hi_u32(w[i] & 0x0000FF80u, k27, tab));
+#else
     const uint32_t eh = lds32(tab | ((w[i] >> 21) & 0x7FCu));
     const uint32_t el = lds32(tab | ((w[i] >> 5) & 0x7FCu));
+#endif
     // bits 16..23 = 1.fraction of the high value, 0..7 of the low one, zeros elsewhere: each funnel shift
     // only moves its own value's bits into the byte it reads (3 for high, 1 for low)
     const uint32_t mm = and_or(w[i], 0x00800080u);
@@ -937,7 +953,8 @@ __global__ void __cluster_dims__(kGseQ, 1, 1) __launch_bounds__(kGseThreads, 5)
   const uint32_t taddr = smem_addr(tab);
   if constexpr (DT == HR_BF16) {
     for (uint32_t e = tid * 8; e < qe; e += kGseThreads * 8)
-      enc_gse_sx(*reinterpret_cast<const uint4*>(src_s + 2 * e), codes, taddr, e);
+      enc_gse_sx(*reinterpret_cast<const uint4*>(src_s + 2 * e), codes, taddr, e, (1u << 11) | (p.n_jobs >> 31),
+                 (1u << 27) | (p.n_jobs >> 31));
   } else {  // fp16: through fp32 with the first 256 (sign-free) entries, signs combined per element
     uint32_t nan_acc = 0;
     for (uint32_t e = tid * 8; e < qe; e += kGseThreads * 8)
