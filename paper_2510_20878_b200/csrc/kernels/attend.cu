@@ -383,11 +383,15 @@ __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, cons
                                            const uint8_t* __restrict__ g16, uint32_t t0, uint32_t nvalid) {
   constexpr uint32_t dcs = D / 8, nch = kKT * dcs / (32 * kDecWarps);
   // full unroll for the paper ladder's schemes; the rest (PASS16, INT4, MXFP8, own rows) by 2 (code size)
-#ifndef HARAG_ATT_UNROLL_ALL
-  constexpr int kUnroll = (SCH == HR_S_GSE8 || SCH == HR_S_INT8 || SCH == HR_S_FP8E4M3 || SCH == HR_S_FP8E5M2) ? (int)nch : 2;
-#else
-  constexpr int kUnroll = (int)nch;
+#ifndef HARAG_ATT_UNROLL_MAIN
+#define HARAG_ATT_UNROLL_MAIN 8
 #endif
+#ifndef HARAG_ATT_UNROLL_RARE
+#define HARAG_ATT_UNROLL_RARE 2
+#endif
+  constexpr int kUnroll = (SCH == HR_S_GSE8 || SCH == HR_S_INT8 || SCH == HR_S_FP8E4M3 || SCH == HR_S_FP8E5M2)
+                              ? (HARAG_ATT_UNROLL_MAIN < (int)nch ? HARAG_ATT_UNROLL_MAIN : (int)nch)
+                              : HARAG_ATT_UNROLL_RARE;
 #pragma unroll kUnroll
   for (uint32_t i = 0; i < nch; ++i) {
     const uint32_t cc = dt + i * 32 * kDecWarps;

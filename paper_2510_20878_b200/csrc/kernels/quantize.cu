@@ -776,7 +776,13 @@ __global__ void __launch_bounds__(kQThreadsB, 1) quantize_batch_kernel(const __g
 // the slab-wide range, builds the code-template table (one entry per thread) and encodes its quarter
 // from shared memory.  The source is read from HBM once; many small CTAs per SM overlap the copies
 // with the encode.  Used when a quarter slab fits kGseQMaxBytes (every Llama shape).
-constexpr int kGseQ = 4;                  // CTAs per cluster (= slab quarters)
+#ifndef HARAG_GSE_Q
+#define HARAG_GSE_Q 4
+#endif
+#ifndef HARAG_GSE_MINB
+#define HARAG_GSE_MINB 5
+#endif
+constexpr int kGseQ = HARAG_GSE_Q;        // CTAs per cluster (= slab parts; "quarters" at the default 4)
 constexpr int kGseThreads = 128;  // 128 elements per thread at Llama shapes: amortises the per-slab setup
 constexpr uint32_t kGseQMaxBytes = 64 * 1024;
 constexpr uint32_t kGseHdr = 8192;  // table + exchange + barrier
@@ -844,7 +850,7 @@ __device__ __forceinline__ void enc_gse_sx(const uint4& raw, uint8_t* codes, uin
 }
 
 template <int DT>
-__global__ void __cluster_dims__(kGseQ, 1, 1) __launch_bounds__(kGseThreads, 5)
+__global__ void __cluster_dims__(kGseQ, 1, 1) __launch_bounds__(kGseThreads, HARAG_GSE_MINB)
     gse_slab_kernel(const __grid_constant__ QBatch p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // [code-template table, 2 KB at a 2-KB-aligned address inside the first 4 KB][part | red | bar][source]
