@@ -39,6 +39,8 @@
 #include "ptx.h"
 
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <cstdlib>
 
 namespace harag {
@@ -770,21 +772,30 @@ __global__ void __launch_bounds__(kQThreadsB, 1) quantize_batch_kernel(const __g
 }
 
 // ---------------------------------------------------------------- GSE-8, single pass: a slab per cluster
-// A cluster of kGseQ CTAs owns one (item, layer, head) slab; CTA q bulk-copies quarter q of the slab's
+// A cluster of kGseQ CTAs owns one (item, layer, head) slab (default 2: halves); CTA q bulk-copies part q of the slab's
 // source into its shared memory (one TMA copy), computes the quarter's exponent range, writes it into
 // every peer's shared memory (DSMEM, st.shared::cluster), and after one cluster barrier each CTA has
 // the slab-wide range, builds the code-template table (one entry per thread) and encodes its quarter
 // from shared memory.  The source is read from HBM once; many small CTAs per SM overlap the copies
 // with the encode.  Used when a quarter slab fits kGseQMaxBytes (every Llama shape).
+// cluster size / threads / resident CTAs measured (tools/prof_quant.py GSE8 64, profiles/round2/tuning.md):
+// 2 x 256 threads 11.05-11.40 us/item; 4 x 128 (round 1) 12.38-12.52; 2 x 128 11.71-12.06; 2 x 512 11.73-11.81;
+// 4 x 256 12.24-12.33; 8 x 128 12.85-12.88; 1 x 256 / 512 (no cluster, one CTA per SM) 14.2-14.4
 #ifndef HARAG_GSE_Q
-#define HARAG_GSE_Q 4
+#define HARAG_GSE_Q 2
 #endif
 #ifndef HARAG_GSE_MINB
-#define HARAG_GSE_MINB 5
+#define HARAG_GSE_MINB 3
 #endif
 constexpr int kGseQ = HARAG_GSE_Q;        // CTAs per cluster (= slab parts; "quarters" at the default 4)
-constexpr int kGseThreads = 128;  // 128 elements per thread at Llama shapes: amortises the per-slab setup
-constexpr uint32_t kGseQMaxBytes = 64 * 1024;
+#ifndef HARAG_GSE_THREADS
+#define HARAG_GSE_THREADS 256
+#endif
+constexpr int kGseThreads = HARAG_GSE_THREADS;  // 128 elements per thread at Llama shapes: amortises the per-slab setup
+#ifndef HARAG_GSE_QMAX_KB
+#define HARAG_GSE_QMAX_KB 64
+#endif
+constexpr uint32_t kGseQMaxBytes = HARAG_GSE_QMAX_KB * 1024;
 constexpr uint32_t kGseHdr = 8192;  // table + exchange + barrier
 
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -1097,9 +1108,11 @@ void launch_tile(const QBatch& b, cudaStream_t st) {
   quant_tile_kernel<DT, SEG><<<(unsigned)b.n_tiles, 32 * kTileWarps, smem, st>>>(b);
 }
 
-// per-device claim counters of the persistent quantize kernel (64 slots of 16 B, zero between launches)
+// per-device claim counters of the persistent quantize kernel (64 slots of 16 B, zero between launches;
+// slots rotate, so launches on different streams of one device use different counters)
 uint32_t* g_qsched[16] = {};
-uint32_t g_qsched_next[16] = {};
+std::atomic<uint32_t> g_qsched_next[16] = {};
+std::mutex g_qsched_mu;
 const uint64_t g_q_dyn_pct = std::getenv("HARAG_Q_DYN") ? (uint64_t)std::atoi(std::getenv("HARAG_Q_DYN")) : 25;
 
 template <int DT, int SEG, int MODE>
@@ -1122,11 +1135,14 @@ void launch_b(const QBatch& b, cudaStream_t st) {
     int dev = 0;
     HR_CUDA(cudaGetDevice(&dev));
     require(dev < 16, HR_EINVAL, "device index");
-    if (!g_qsched[dev]) {
-      HR_CUDA(cudaMalloc((void**)&g_qsched[dev], 64 * 16));
-      HR_CUDA(cudaMemset(g_qsched[dev], 0, 64 * 16));
+    {
+      std::lock_guard<std::mutex> g(g_qsched_mu);
+      if (!g_qsched[dev]) {
+        HR_CUDA(cudaMalloc((void**)&g_qsched[dev], 64 * 16));
+        HR_CUDA(cudaMemset(g_qsched[dev], 0, 64 * 16));
+      }
     }
-    bb.sched = g_qsched[dev] + 4 * (g_qsched_next[dev]++ % 64);
+    bb.sched = g_qsched[dev] + 4 * (g_qsched_next[dev].fetch_add(1) % 64);
     bb.dyn_tiles = b.n_tiles * g_q_dyn_pct / 100;
     bb.dyn_chunk = (uint32_t)std::max<uint64_t>(1, bb.dyn_tiles / (grid * 8));
   }

@@ -117,6 +117,7 @@ Store::~Store() {
   }
   if (delta) cudaFree(delta);
   if (att_part) cudaFree(att_part);
+  if (att_done) cudaEventDestroy(att_done);
   if (asm_sched) cudaFree(asm_sched);
   if (att_cnt) cudaFree(att_cnt);
   if (err_flag) cudaFree(err_flag);
@@ -1108,6 +1109,9 @@ void Store::attend(uint32_t n_req, uint32_t k, const uint32_t* ids, uint32_t l0,
     p.part_o = att_part;
     p.part_lse = att_part + units * p.n_split * 128ull * lay.D;
     p.part_cnt = att_cnt;
+    // the workspace is shared by every split launch of the store: order this one after the previous one
+    // even when the caller alternates streams (a no-op wait on the same stream)
+    if (att_done) HR_CUDA(cudaStreamWaitEvent(st, att_done, 0));
   }
   // q read + o written (algorithmic), beside the codes + meta counted above
   stats.bytes_hbm_alg += 2ull * 2 * n_req * nl * lay.Hl * g * n_q * lay.D;
@@ -1119,6 +1123,10 @@ void Store::attend(uint32_t n_req, uint32_t k, const uint32_t* ids, uint32_t l0,
     HR_CUDA(cudaEventRecord(a, st));
   }
   launch_attend(p, st);
+  if (p.n_split > 1) {
+    if (!att_done) HR_CUDA(cudaEventCreateWithFlags(&att_done, cudaEventDisableTiming));
+    HR_CUDA(cudaEventRecord(att_done, st));
+  }
   if (timing) {
     HR_CUDA(cudaEventRecord(b, st));
     timers.emplace_back(a, b);

@@ -163,6 +163,7 @@ struct Store {
   uint64_t att_part_floats = 0;
   uint32_t* att_cnt = nullptr;
   uint64_t att_cnt_n = 0;
+  cudaEvent_t att_done = nullptr;  // the last key-split launch: a split launch on another stream waits for it
   int n_sms = 0;
   // assemble tail balancing: per-launch claim counters (64 slots of 16 B, zero between launches)
   uint32_t* asm_sched = nullptr;

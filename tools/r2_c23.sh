@@ -1,0 +1,5 @@
+set -x
+for r in 1 2; do for v in default gseq2t256 gseq2t512 gseq4t256; do
+  if [ $v = default ]; then unset HARAG_LIB; else export HARAG_LIB=build/variants/$v/libharag.so; fi
+  echo "$v $(timeout 120 python tools/prof_quant.py GSE8 64 2>&1 | tail -1)"
+done; done
