@@ -13,6 +13,9 @@ for n, l in (d.get('legs') or {}).items():
     if 'error' in l:
         print(n, l)
         continue
+    if 'roofline' not in l:  # the TTFT-like consumer leg
+        print(n, {k: v for k, v in l.items() if 'ms' in k or 'rel' in k or 'speed' in k})
+        continue
     print(n, {k: l.get(k) for k in ('value', 'ms_per_step', 'hits_per_tier', 'build_seconds', 'request_latency_us')})
     print('    roof', l['roofline']['frac'], l['roofline']['achieved'], 'link', (l.get('link') or {}).get('frac'),
           (l.get('link') or {}).get('achieved_GBps'), 'overlapped', (l.get('overlapped_roofline') or {}).get('frac'),
