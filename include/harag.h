@@ -232,7 +232,11 @@ hr_status hr_replace(hr_store* s, void* stream);
  * before any launch); host-tier items are staged as in hr_attend_layers;
  * duplicate / unknown ids as hr_assemble_kv.  Stream-ordered; counts hotness
  * like hr_assemble_kv (a1).  Arithmetic: bf16/fp16 tensor-core products, fp32
- * accumulation, probabilities rounded to the dtype before P.V. */
+ * accumulation, probabilities rounded to the dtype before P.V.
+ * A call whose (request, layer, KV head) units alone leave SMs idle splits each
+ * unit's keys over several CTAs and merges the partial results by LSE (a
+ * store-owned workspace; successive split launches are ordered by an event,
+ * also across streams; HARAG_ATT_SPLIT forces a split count). */
 hr_status hr_attend(hr_store* s, uint32_t n_req, uint32_t k, const uint32_t* doc_ids, const void* q_dev,
                     uint32_t n_q, uint32_t g, void* o_dev, float* lse_dev, float scale, void* kv_dump,
                     void* stream);

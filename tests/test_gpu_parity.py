@@ -744,3 +744,31 @@ def test_refused_replace_leaves_epoch_state(torch_cuda):
     assert np.array_equal(st.hotness_delta().cpu().numpy(), delta)
     reqs = synth.gen_requests(8, 6, 3, 1.1, seed=9)
     check_requests(torch, st, ora, lay, reqs)
+
+
+def test_tail_balanced_launches_reuse_their_counters(torch_cuda):
+    """Assemble's tail balancing claims the last quarter of every launch's tiles through a per-launch
+    counter (64 slots per store, zeroed by the launch's last producer): 70 consecutive launches (every slot
+    reused) on two alternating streams each produce every element of every request exactly as the oracle."""
+    torch = torch_cuda
+    # 8 requests x 4 docs x 2 items x 16 slabs x 1 tile = 1,024 tiles >= 4 x 148 CTAs: the dynamic tail is on
+    st, ora, lay, h, _ = make_pair(torch, L=4, H=4, T=128, D=64, n_docs=12, ladder=PAPER, taus=(0.2, 0.2, 0.2))
+    reqs = synth.gen_requests(12, 8, 4, 1.1, seed=21)
+    want = [ora.assemble(list(r)) for r in reqs]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    ko, vo = alloc_out(torch, st, len(reqs), 4)
+    for it in range(70):
+        s = streams[it % 2]
+        s.wait_stream(streams[(it + 1) % 2])  # the outputs are reused: order the launches
+        for t in ko + vo:
+            t.record_stream(s)
+        with torch.cuda.stream(s):
+            for t in ko + vo:
+                t.fill_(0x7FFF)
+        st.assemble(reqs, ko, vo, stream=s)
+        if it % 23 == 0 or it == 69:
+            s.synchronize()
+            for r, (K, V) in enumerate(want):
+                assert np.array_equal(ko[r].cpu().numpy().view(np.uint16).reshape(K.shape), K), (it, r)
+                assert np.array_equal(vo[r].cpu().numpy().view(np.uint16).reshape(V.shape), V), (it, r)
+    st.close()

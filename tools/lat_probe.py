@@ -44,3 +44,4 @@ for r in range(len(reqs)):
     m = a[a[:, 0] == r]
     print(f"req {r:2d} gse_items {int(m[0, 3]):2d}: call {m[:, 1].mean():6.1f} (min {m[:, 1].min():6.1f} max {m[:, 1].max():6.1f}) "
           f"kernel {m[:, 2].mean():6.1f}")
+st.close()  # prints the HARAG_HOST_PROF breakdown when set
