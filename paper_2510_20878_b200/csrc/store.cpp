@@ -81,9 +81,11 @@ Store::Store(const hr_store_config& c) : cfg(c), lay(make_layout(c)) {
   HR_CUDA(cudaStreamCreateWithFlags(&copy_stream, cudaStreamNonBlocking));
   if (cfg.numa_bind) local_cpus = gpu_local_cpus(cfg.device);
   host_prof = std::getenv("HARAG_HOST_PROF") != nullptr;
+  if (const char* m = std::getenv("HARAG_METRICS_JSONL")) metrics = std::fopen(m, "a");  // per-call metrics
 }
 
 Store::~Store() {
+  if (metrics) std::fclose(metrics);
   if (host_prof && prof_calls)
     std::fprintf(stderr, "[harag host prof] %llu calls, us/call: entry+validate %.2f desc_buffer %.2f pass1 %.2f "
                  "pass2-3 %.2f launchA %.2f tail %.2f\n", (unsigned long long)prof_calls,
@@ -572,6 +574,7 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
                      cudaStream_t st) {
   const auto host_t0 = std::chrono::steady_clock::now();
   const NvtxRange nvtx_call("hr_assemble_kv");
+  const hr_stats before = metrics ? stats : hr_stats{};
   auto tick = [&](int i) {
     if (!host_prof) return;
     const auto now = std::chrono::steady_clock::now();
@@ -866,9 +869,24 @@ void Store::assemble(uint32_t n_req, uint32_t k, const uint32_t* ids, void* cons
   }
   tick(5);
   prof_calls++;
-  stats.host_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0).count();
+  const double host_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - host_t0).count();
+  stats.host_ms += host_ms;
   req_counter += n_req;
   stats.requests += n_req;
+  if (metrics) {  // HARAG_METRICS_JSONL: one line per call (host-side counters, no device synchronisation)
+    std::fprintf(metrics,
+                 "{\"call\": %llu, \"n_req\": %u, \"k\": %u, \"hits\": [%llu, %llu, %llu], \"hits_disk\": %llu, "
+                 "\"bytes_out\": %llu, \"bytes_h2d\": %llu, \"h2d_items\": %llu, \"launches\": %llu, "
+                 "\"host_us\": %.2f}\n",
+                 (unsigned long long)metrics_calls++, n_req, k,
+                 (unsigned long long)(stats.hits[0] - before.hits[0]), (unsigned long long)(stats.hits[1] - before.hits[1]),
+                 (unsigned long long)(stats.hits[2] - before.hits[2]),
+                 (unsigned long long)(stats.hits_disk - before.hits_disk),
+                 (unsigned long long)(stats.bytes_out - before.bytes_out),
+                 (unsigned long long)(stats.bytes_h2d - before.bytes_h2d),
+                 (unsigned long long)(stats.h2d_items - before.h2d_items),
+                 (unsigned long long)(stats.kernel_launches - before.kernel_launches), 1e3 * host_ms);
+  }
 }
 
 double Store::last_call_ms() {

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <cstdio>
 #include <cstdint>
 #include <map>
 #include <unordered_set>
@@ -177,6 +178,9 @@ struct Store {
   double last_call_ms();
   // HARAG_HOST_PROF=1: host-time breakdown of hr_assemble_kv, printed when the store is destroyed
   bool host_prof = false;
+  // HARAG_METRICS_JSONL=<file>: one JSON line per hr_assemble_kv call (hits per tier, bytes, host time)
+  FILE* metrics = nullptr;
+  uint64_t metrics_calls = 0;
   double prof_ms[6] = {0, 0, 0, 0, 0, 0};
   uint64_t prof_calls = 0;
   std::chrono::steady_clock::time_point prof_t;

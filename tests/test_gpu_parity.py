@@ -772,3 +772,31 @@ def test_tail_balanced_launches_reuse_their_counters(torch_cuda):
                 assert np.array_equal(ko[r].cpu().numpy().view(np.uint16).reshape(K.shape), K), (it, r)
                 assert np.array_equal(vo[r].cpu().numpy().view(np.uint16).reshape(V.shape), V), (it, r)
     st.close()
+
+
+def test_metrics_jsonl_per_call(torch_cuda, tmp_path, monkeypatch):
+    """HARAG_METRICS_JSONL (SURVEY §5 metrics): one JSON line per hr_assemble_kv call whose counters add up
+    to the call — every item of every request counted once in a tier, KV bytes = 2 x n_req x kv_bytes(k)."""
+    import json
+    path = tmp_path / "m.jsonl"
+    monkeypatch.setenv("HARAG_METRICS_JSONL", str(path))
+    torch = torch_cuda
+    st, ora, lay, h, _ = make_pair(torch, L=2, H=2, T=64, D=64, n_docs=8, ladder=PAPER, taus=(0.2, 0.2, 0.2),
+                                   hbm_items=6)
+    reqs = [synth.gen_requests(8, n, 3, 1.1, seed=30 + n) for n in (1, 2, 4)]
+    for r in reqs:
+        ko, vo = alloc_out(torch, st, len(r), 3)
+        st.assemble(r, ko, vo)
+    torch.cuda.synchronize()
+    st.close()
+    lines = [json.loads(x) for x in path.read_text().splitlines()]
+    assert [x["call"] for x in lines] == [0, 1, 2]
+    for x, r in zip(lines, reqs):
+        assert x["n_req"] == len(r) and x["k"] == 3
+        assert sum(x["hits"]) + x["hits_disk"] == 2 * len(r) * 3
+        assert x["bytes_out"] == 2 * len(r) * st_kv_bytes(lay, 3)
+        assert x["host_us"] > 0
+
+
+def st_kv_bytes(lay, k):
+    return 2 * lay.L * lay.Hl * k * lay.T * lay.D
