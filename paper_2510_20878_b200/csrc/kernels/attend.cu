@@ -10,25 +10,23 @@
 // to the precomputed chunk KV that TurboRAG / HA-RAG prefill performs (P:41,
 // P:316); LSE lets a caller merge it with the question's own causal part.
 //
-// sm_100a design: one CTA per (request, layer, KV head) unit,
-// warp-specialised — 4 softmax warps (thread = query row = TMEM lane), 3 groups
-// of 4 decoder warps (tiles round-robin), one MMA-issuer warp and one producer
-// warp.  The unit's M = g*n_q <= 128 query rows are the A operand of
-// tcgen05.mma (M = 128, rows past M zero), loaded into TMEM once.  Per 64-key
-// tile the producer lane bulk-copies (TMA, cp.async.bulk) the tile's contiguous
-// K and V code runs into a 4-slot stage ring (mbarrier complete_tx); a decoder
-// group decodes them, bit for bit as hr_assemble_kv, into one of four K/V
-// operand buffers — K a 128-byte-swizzled K-major tile, V a 128-byte-swizzled
-// MN-major tile (the same physical layout), both written row-wise from the
-// contiguous stage slot, so stage reads and operand writes are conflict-free.
-// S = Q K^T accumulates in one of two TMEM buffers; the softmax warps run a
-// one-pass online softmax at a running reference max (rescale of O only when a
-// row max grows past a threshold) and write P (16-bit) back into the S
-// buffer's TMEM columns; O += P V takes A = P from TMEM, and the row sum of the
-// rounded P is accumulated by the tensor core (an N = 16 MMA against a ones
-// tile).  Debug builds: -DHARAG_ATT_TRACE (per-tile clock64 events of CTA 0),
-// -DHARAG_ATT_WATCHDOG (mbarrier waits that report and trap),
-// -DHARAG_ATT_MMASYNC (MMA latency in isolation).
+// sm_100a design: one CTA per (request, layer, KV head) unit — or per (unit, key split)
+// when the units alone leave SMs idle (splits merged by LSE by the last split to finish) —
+// warp-specialised: 4 softmax warps (thread = query row = TMEM lane), 3 groups of 4 decoder warps
+// (tiles round-robin), an S-issuer warp, a PV-issuer warp and a producer warp.  The unit's
+// M = g*n_q <= 128 query rows are the A operand of tcgen05.mma (M = 128, rows past M zero), loaded into
+// TMEM once.  Per 64-key tile the producer lane bulk-copies (TMA, cp.async.bulk) the tile's contiguous
+// K and V code runs into a 4-slot stage ring (mbarrier complete_tx); a decoder group decodes them, bit
+// for bit as hr_assemble_kv (every scheme incl. MXFP8), into one of four K/V operand buffers — K a
+// 128-byte-swizzled K-major tile, V a 128-byte-swizzled MN-major tile (the same physical layout), both
+// written row-wise from the contiguous stage slot, so stage reads and operand writes are conflict-free.
+// S = Q K^T accumulates in one of two TMEM buffers; the softmax warps run a one-pass online softmax at
+// a running reference max (rescale of O only when a row max grows past a threshold) and write P
+// (16-bit) into its own TMEM columns; O += P V takes A = P from TMEM, and the row sum of the rounded P
+// is accumulated by the tensor core (an N = 16 MMA against a ones tile).  Prefill form (R30): the
+// question's own K/V rows are one more tile, read in place and masked causally.  Debug builds:
+// -DHARAG_ATT_TRACE (per-tile clock64 events of CTA 0), -DHARAG_ATT_WATCHDOG (mbarrier waits that
+// report and trap).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_fp8.h>
@@ -499,16 +497,15 @@ __device__ __forceinline__ uint32_t stage_meta(uint32_t scheme, const uint8_t* m
 
 // ---------------------------------------------------------------------------------------------
 // Warp-specialised pipeline, one CTA per (request, layer, KV head) unit:
-//   warps 0-3  softmax: thread t owns query row t (TMEM lane t); loads Q; online softmax of S_j,
-//              lazy O rescale, P_j -> shared memory; epilogue O / l and LSE
-//   warps 4-11 decoders, two groups of 4: group b decodes the tiles j with j&1 == b into operand
-//              buffer b — tile j's K and V codes (L2-prefetched kPF tiles ahead; all of a thread's
-//              loads in flight before it decodes) -> bf16/fp16 operand tiles in shared memory, the
-//              assemble decode bit for bit; two groups so decode latency overlaps across tiles
-//   warp 12    MMA issuer (one lane): S_j = Q K_j^T into TMEM buffer j&1, then O += P_{j-1} V_{j-1}
-// so the tensor core computes S_{j+1} while the softmax warps work on S_j and the decoders fill
-// tile j+2.  mbarriers: sf (S ready), pf (P ready), kvf (operands ready), kve (operands and P free:
-// committed after PV), pfree (PV done per P buffer: lazy rescale, epilogue), qf (Q ready).
+//   warps 0-3    softmax: thread t owns query row t (TMEM lane t); loads Q; online softmax of S_j,
+//                lazy O rescale, P_j -> TMEM; epilogue O / l and LSE (or the split partials + merge)
+//   warps 4-15   decoders, three groups of 4: group b decodes the tiles j with j % 3 == b into operand
+//                buffer j % 4 (one warp per group waits for the buffer and the stage slot)
+//   warp 16      S issuer: S_j = Q K_j^T into TMEM S buffer j % 2 once K_j is decoded and PV_{j-2} is done
+//   warp 17      PV issuer: O += P_j V_j (+ the row sum) once P_j is ready
+//   warp 18      producer (one lane): TMA bulk copies of the code tiles, L2 prefetch ahead
+// mbarriers: sf (S ready), pf (P ready), kvf (operands ready), kve (operand buffer free: committed after
+// PV), pfree (PV done per P buffer: S issue, lazy rescale, epilogue), qf (Q ready), stf / ste (stage ring).
 #ifndef HARAG_ATT_PF
 #define HARAG_ATT_PF 4
 #endif
