@@ -118,6 +118,45 @@ def main():
             assert np.all(np.abs(got - O) <= 2.0 ** -8 * 2 * vr + 2.0 ** -8 * np.abs(O) + 1e-6), D
             assert np.all(np.abs(lse[r].cpu().numpy() - lse_w) <= 2.0 ** -8), D
         st.close()
+    # MXFP8 (R31): quantize (tile kernel) + assemble, both dtypes
+    for dtype in ("bf16", "fp16"):
+        st, ora, lay = make(2, 2, 64, 64, 8, ("MXFP8", "GSE8"), (0.5,), dtype=dtype)
+        for i in range(16):
+            assert np.array_equal(st.export_item(i), ora.blobs[i])
+        check_assemble(st, ora, synth.gen_requests(8, 4, 3, 1.1, seed=7))
+        st.close()
+        n += 1
+    # attention prefill form (R30): chunk keys + the question's own K/V, causal; forced 3 splits (the own
+    # tile alone in the last one)
+    os.environ["HARAG_ATT_SPLIT"] = "3"
+    st, ora, lay = make(2, 2, 64, 128, 6, ("INT8", "FP8E4M3", "FP8E5M2", "GSE8"), (0.2, 0.2, 0.2))
+    reqs = synth.gen_requests(6, 2, 2, 1.1, seed=8).astype(np.uint32)
+    g, n_q, D = 2, 8, 128
+    qb = synth.gen_query(2, 2, 2 * g, n_q, D)
+    kob, vob = synth.gen_query(2, 2, 2, n_q, D, seed=91), synth.gen_query(2, 2, 2, n_q, D, seed=92)
+    cu = lambda a: torch.from_numpy(a.view(np.int16)).cuda()  # noqa: E731
+    q, ko, vo = cu(qb), cu(kob), cu(vob)
+    o = torch.empty_like(q)
+    lse = torch.empty((2, 2, 2 * g, n_q), dtype=torch.float32, device="cuda")
+    st.attend_prefill(reqs, q, ko, vo, o, n_q, g, layers=(0, 2), lse=lse)
+    torch.cuda.synchronize()
+    for r in range(2):
+        K, V = ora.assemble(list(reqs[r]))
+        O, lse_w = attention.attend_request(qb[r], K, V, g, "bf16", K_own_bits=kob[r], V_own_bits=vob[r])
+        got = o[r].view(torch.bfloat16).float().cpu().numpy().astype(np.float64)
+        vr = max(np.abs(ost.numerics.to_f32(V, "bf16")).max(), np.abs(ost.numerics.to_f32(vob[r], "bf16")).max())
+        assert np.all(np.abs(got - O) <= 2.0 ** -8 * 2 * vr + 2.0 ** -8 * np.abs(O) + 1e-6)
+        assert np.all(np.abs(lse[r].cpu().numpy() - lse_w) <= 2.0 ** -8)
+    st.close()
+    del os.environ["HARAG_ATT_SPLIT"]
+    # value-distribution guard statistics (R29)
+    from oracle import guard
+    item = synth.gen_item(2, 2, 64, 64, 5, 1)
+    stats = torch.zeros(2, dtype=torch.int64, device="cuda")
+    hr.guard_stats(torch.from_numpy(item.view(np.int16)).cuda(), stats, L=2, H=2, D=64, T=64, gse=(2, 5))
+    fl, am = guard.guard_stats(item, "bf16", 2, 5)
+    got = stats.cpu().numpy().view(np.uint64)
+    assert int(got[0]) == fl and int(got[1]) == int(np.array([am], np.float32).view(np.uint32)[0])
     # analysis kernels
     x = torch.empty(2 * 2 * 64 * 64, dtype=torch.int16, device="cuda")
     synth.gen_item_device(x.data_ptr(), 2, 2, 64, 64, 3, 0)
