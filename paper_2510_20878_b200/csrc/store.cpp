@@ -1228,9 +1228,21 @@ void Store::replace(cudaStream_t st) {
         nt[i] = on_disk ? HR_T_DISK : cfg.backing_pinned ? HR_T_PIN : HR_T_PAGE;
         continue;
       }
-      if (loc[i].backing_off != FreeList::kNone) {
+      if (loc[i].backing_off != FreeList::kNone && backing_is_pinned) {
         HR_CUDA(cudaMemcpyAsync(hbm_base + off, backing_base + loc[i].backing_off, bytes[i], cudaMemcpyHostToDevice,
                                 copy_stream));
+      } else if (loc[i].backing_off != FreeList::kNone) {
+        // pageable backing: through the staging ring's pinned bounce buffers, round robin, so the
+        // host copy of one promotion overlaps the DMA of the previous ones (a cudaMemcpyAsync straight
+        // from pageable memory is staged by the driver at ~11 GB/s and blocks the host)
+        ensure_ring();
+        Slot& sl = ring[promo_slot++ % slots];
+        if (!sl.bounce) HR_CUDA(cudaHostAlloc((void**)&sl.bounce, align_up(max_item, 4096), cudaHostAllocPortable));
+        if (sl.used) HR_CUDA(cudaEventSynchronize(sl.copied));  // the bounce's previous DMA is done
+        host_copy(sl.bounce, backing_base + loc[i].backing_off, bytes[i]);
+        HR_CUDA(cudaMemcpyAsync(hbm_base + off, sl.bounce, bytes[i], cudaMemcpyHostToDevice, copy_stream));
+        HR_CUDA(cudaEventRecord(sl.copied, copy_stream));
+        sl.used = true;
       } else {  // disk-backed: through a pinned bounce, one item at a time
         ensure_ring();
         Slot& sl = ring[0];

@@ -158,6 +158,7 @@ struct Store {
   std::vector<AsmDesc> hdesc;  // host copy of an assemble call's descriptors
   int dbuf_next = 0;
   std::vector<Slot> ring;
+  uint32_t promo_slot = 0;  // round-robin bounce slot of hr_replace's pageable promotions
   uint64_t req_counter = 0;
   // hr_attend key-split workspace (grown on demand): partial O / LSE and the per-unit arrival counters
   float* att_part = nullptr;
