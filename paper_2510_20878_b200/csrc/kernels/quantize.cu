@@ -1093,6 +1093,9 @@ bool use_tile_kernel() {
   return v != 0;
 }
 inline bool tile_scheme(uint32_t s) {
+#ifdef HARAG_QTILE_GROUPED  // experiment: INT8 / INT4 on the tile kernel too
+  if (s == HR_S_INT8 || s == HR_S_INT4) return true;
+#endif
   return s == HR_S_PASS16 || s == HR_S_FP8E4M3 || s == HR_S_FP8E5M2 || s == HR_S_MXFP8;
 }
 
