@@ -21,6 +21,11 @@ struct Error : std::runtime_error {
 inline void require(bool ok, hr_status c, const std::string& m) {
   if (!ok) fail(c, m);
 }
+// literal messages bind here: no std::string is built unless the check fails (hr_assemble_kv runs a few
+// dozen checks per call)
+inline void require(bool ok, hr_status c, const char* m) {
+  if (!ok) fail(c, m);
+}
 
 inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
 

@@ -541,18 +541,20 @@ void Store::validate_request(uint32_t n_req, uint32_t k, const uint32_t* ids, vo
   require(state == State::Built, HR_ESTATE, "hr_assemble_kv before the store is built");
   require(n_req > 0 && k > 0, HR_EINVAL, "n_req and k must be > 0");
   require(ids && k_out && v_out, HR_EINVAL, "NULL argument");
-  std::vector<uint32_t> tmp(k);
+  uint32_t stack_ids[64];  // k <= 64 in practice: no heap allocation per call
+  std::vector<uint32_t> heap_ids(k > 64 ? k : 0);
+  uint32_t* tmp = k > 64 ? heap_ids.data() : stack_ids;
   for (uint32_t r = 0; r < n_req; ++r) {
     require(k_out[r] && v_out[r], HR_EINVAL, "NULL output pointer");
     require(((uintptr_t)k_out[r] & 15) == 0 && ((uintptr_t)v_out[r] & 15) == 0, HR_EINVAL,
             "output pointers must be 16-byte aligned");
     for (uint32_t j = 0; j < k; ++j) {
       tmp[j] = ids[(uint64_t)r * k + j];
-      require(tmp[j] < n_docs, HR_ENOTFOUND, "unknown doc id " + std::to_string(tmp[j]));
+      if (tmp[j] >= n_docs) fail(HR_ENOTFOUND, "unknown doc id " + std::to_string(tmp[j]));
     }
-    std::sort(tmp.begin(), tmp.end());
-    require(std::adjacent_find(tmp.begin(), tmp.end()) == tmp.end(), HR_EINVAL,
-            "duplicate doc id in request " + std::to_string(r) + " (R19)");
+    std::sort(tmp, tmp + k);
+    if (std::adjacent_find(tmp, tmp + k) != tmp + k)
+      fail(HR_EINVAL, "duplicate doc id in request " + std::to_string(r) + " (R19)");
   }
 }
 
@@ -983,11 +985,11 @@ void Store::attend(uint32_t n_req, uint32_t k, const uint32_t* ids, uint32_t l0,
   for (uint32_t r = 0; r < n_req; ++r) {
     for (uint32_t j = 0; j < k; ++j) {
       tmp[j] = ids[(uint64_t)r * k + j];
-      require(tmp[j] < n_docs, HR_ENOTFOUND, "unknown doc id " + std::to_string(tmp[j]));
+      if (tmp[j] >= n_docs) fail(HR_ENOTFOUND, "unknown doc id " + std::to_string(tmp[j]));
     }
     std::sort(tmp.begin(), tmp.end());
-    require(std::adjacent_find(tmp.begin(), tmp.end()) == tmp.end(), HR_EINVAL,
-            "duplicate doc id in request " + std::to_string(r) + " (R19)");
+    if (std::adjacent_find(tmp.begin(), tmp.end()) != tmp.end())
+      fail(HR_EINVAL, "duplicate doc id in request " + std::to_string(r) + " (R19)");
   }
   HR_CUDA(cudaSetDevice(cfg.device));
   if (!promos.empty()) poll_promotions(false);
