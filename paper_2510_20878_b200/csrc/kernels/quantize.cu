@@ -191,6 +191,18 @@ __device__ __forceinline__ float div127(float a) {
   return __fmaf_rn(r, y, q0);
 }
 
+// fl(d / 15) for the INT4 scale, the same correction with y = RN(1/15): checked against __fdiv_rn for every
+// fp32 significand at every exponent from 2^-100 to 2^127 by tests/csrc/markstein_check.cu (the quotient
+// of a power-of-two scaled d is the scaled quotient while the residual cannot underflow); smaller d take
+// the IEEE division.
+__device__ __forceinline__ float div15(float d) {
+  constexpr float y = 0.066666670143604278564f;  // RN(1/15)
+  if (d < 7.8886090522101181e-31f) return __fdiv_rn(d, 15.f);
+  const float q0 = __fmul_rn(d, y);
+  const float r = __fmaf_rn(-q0, 15.f, d);
+  return __fmaf_rn(r, y, q0);
+}
+
 // sub(a, b) of R4: fl(a - b) saturated at FLT_MAX (finite inputs whose difference overflows)
 __device__ __forceinline__ float sub_sat(float a, float b) { return fminf(__fsub_rn(a, b), 3.40282347e+38f); }
 
@@ -250,7 +262,7 @@ __device__ __forceinline__ void enc_int8_step(const uint8_t* tile, uint32_t eb, 
   const bool fast = s >= 8.0779356e-28f && s <= 4.2535296e+37f;
   uint2 w[4];
   if (__all_sync(0xFFFFFFFFu, fast)) {  // warp-uniform: the branch-free path for every normal scale
-    const float y = __fdiv_rn(1.f, s);
+    const float y = __frcp_rn(s);  // RN(1/s)
     const float2 yy = make_float2(y, y), ns = make_float2(-s, -s), mg = make_float2(kMagic, kMagic);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
@@ -297,47 +309,70 @@ __device__ __forceinline__ void enc_int8_step(const uint8_t* tile, uint32_t eb, 
 // against IEEE division on 2^33 sampled (x, mn, mx) triples per source dtype by
 // tests/csrc/markstein_check.cu.  Scales outside [2^-90, 2^125] (or a group whose range overflows) take
 // __fdiv_rn per element (warp-uniform).
+// Packed 16-bit min / NaN-propagating max of two source-dtype pairs (HMNMX2): the order of bf16 / fp16
+// values is the order of their fp32 images, so the extremes equal the fp32 ones up to the sign of a zero
+// (made +0 by the caller's fl(v + 0)).
+template <int DT>
+__device__ __forceinline__ uint32_t pmin16x2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  if constexpr (DT == HR_BF16) asm("min.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  else asm("min.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+template <int DT>
+__device__ __forceinline__ uint32_t pmaxnan16x2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  if constexpr (DT == HR_BF16) asm("max.NaN.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  else asm("max.NaN.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+
 template <int SEGL, int DT>
 __device__ __forceinline__ void enc_int4_step(const uint8_t* tile, uint32_t eb, uint32_t n_el, uint8_t* codes,
                                               float2* meta, uint32_t g_shift, uint32_t lane, uint32_t& nan_acc) {
   const uint32_t e0 = eb + lane * kLaneE, rot = (lane >> 1) & 3;
   uint4 raw[4];
   const bool valid = load_lane32<DT>(tile, e0, n_el, rot, raw);
-  nan_acc = __vmaxu2(nan_acc, __vmaxu2(__vmaxu2(absmax_pair(raw[0]), absmax_pair(raw[1])),
-                                       __vmaxu2(absmax_pair(raw[2]), absmax_pair(raw[3]))));
+  // lane statistics on the packed pairs: min, and a NaN-propagating max, so that the lane's NaN / +-Inf
+  // show up as a non-finite pattern in one of the two (a NaN in max, +Inf in max, -Inf in min)
+  uint32_t pmn = raw[0].x, pmx = raw[0].x;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const uint32_t w[4] = {raw[j].x, raw[j].y, raw[j].z, raw[j].w};
+#pragma unroll
+    for (int i = j == 0 ? 1 : 0; i < 4; ++i) pmn = pmin16x2<DT>(pmn, w[i]), pmx = pmaxnan16x2<DT>(pmx, w[i]);
+  }
+  nan_acc = __vmaxu2(nan_acc, __vmaxu2(pmn & 0x7FFF7FFFu, pmx & 0x7FFF7FFFu));
   float2 x[4][4];
 #pragma unroll
   for (int j = 0; j < 4; ++j) unpack8<DT>(raw[j], x[j]);
-  float mn = x[0][0].x, mx = x[0][0].x;
-#pragma unroll
-  for (int j = 0; j < 4; ++j)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) mn = fminf(mn, fminf(x[j][i].x, x[j][i].y)), mx = fmaxf(mx, fmaxf(x[j][i].x, x[j][i].y));
+  float mn = fminf(to_f32<DT>(pmn & 0xFFFFu), to_f32<DT>(pmn >> 16));
+  float mx = fmaxf(to_f32<DT>(pmx & 0xFFFFu), to_f32<DT>(pmx >> 16));
   mn = __fadd_rn(seg_min_f<SEGL>(mn), 0.f);
   mx = __fadd_rn(seg_max_f<SEGL>(mx), 0.f);
   const float dm = __fsub_rn(mx, mn);
-  const float s = (mx == mn) ? 1.f : __fdiv_rn(fminf(dm, 3.40282347e+38f), 15.f);
+  const float s = (mx == mn) ? 1.f : div15(fminf(dm, 3.40282347e+38f));
   if ((lane & (SEGL - 1)) == 0 && valid) meta[e0 >> g_shift] = make_float2(s, mn);
   const bool fast = s >= 8.0779356e-28f && s <= 4.2535296e+37f && dm <= 3.40282347e+38f;
   uint32_t w[4];
   if (__all_sync(0xFFFFFFFFu, fast)) {  // warp-uniform
-    const float y = __fdiv_rn(1.f, s);
+    const float y = __frcp_rn(s);  // RN(1/s)
     const float2 yy = make_float2(y, y), ns = make_float2(-s, -s), nm = make_float2(-mn, -mn);
     const float2 mg = make_float2(kMagic, kMagic);
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      uint32_t v[8];
+      uint32_t v[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const float2 u = __fadd2_rn(x[j][i], nm);
         const float2 q0 = __fmul2_rn(u, yy);
         const float2 q1 = __ffma2_rn(__ffma2_rn(q0, ns, u), yy, q0);
         const float2 q2 = __ffma2_rn(__ffma2_rn(q1, ns, u), yy, q1);  // fl(u / s)
-        const float2 rr = __fadd2_rn(q2, mg);                          // low bits: rne
-        v[2 * i] = __float_as_uint(rr.x), v[2 * i + 1] = __float_as_uint(rr.y);
+        const float2 rr = __fadd2_rn(q2, mg);                          // low bits: rne, in [0, 15]
+        // even element -> low nibble, odd -> high nibble: the low byte of lo + (hi << 4) (one LEA)
+        v[i] = __float_as_uint(rr.x) + (__float_as_uint(rr.y) << 4);
       }
-      // even elements -> low nibbles, odd -> high nibbles
-      w[j] = (gather_b0(v[0], v[2], v[4], v[6]) & 0x0F0F0F0Fu) | ((gather_b0(v[1], v[3], v[5], v[7]) & 0x0F0F0F0Fu) << 4);
+      w[j] = gather_b0(v[0], v[1], v[2], v[3]);
     }
   } else {
 #pragma unroll

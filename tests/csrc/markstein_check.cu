@@ -7,6 +7,8 @@
 // of them with x steered next to a quantisation tie, compare
 //   q  = rne(RN(u / s))               (IEEE)   vs  rne(markstein2(u, s, y)), u = RN(x - mn),
 //   s  = RN(RN(mx - mn) / 15), y = RN(1/s)     (two Markstein corrections, quantize.cu enc_int4_step)
+// Scale / reciprocal (exhaustive over fp32 significands): for every d = 1.m * 2^e, e in [-100, 127],
+//   RN(d / 15) (IEEE) vs div15(d) (one Markstein correction), and RN(1/d) (IEEE division) vs __frcp_rn(d).
 // Prints "mismatches <n> pairs <m>"; exit code 0 iff n == 0.
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tests/csrc/markstein_check tests/csrc/markstein_check.cu
 #include <cuda_bf16.h>
@@ -32,6 +34,32 @@ __device__ float markstein(float x, float s, float y) {
   const float q0 = __fmul_rn(x, y);
   const float r = __fmaf_rn(-q0, s, x);
   return __fmaf_rn(r, y, q0);
+}
+
+__device__ float div15(float d) {  // quantize.cu div15 (d >= 2^-100)
+  const float y = 0.066666670143604278564f;
+  const float q0 = __fmul_rn(d, y);
+  const float r = __fmaf_rn(-q0, 15.f, d);
+  return __fmaf_rn(r, y, q0);
+}
+__global__ void check_scale(unsigned long long* bad, unsigned long long* pairs) {
+  unsigned long long nb = 0, np = 0;
+  const unsigned long long n = 228ull << 23;  // biased exponents 27 (2^-100) .. 254 (2^127)
+  for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+       i += (unsigned long long)gridDim.x * blockDim.x) {
+    const float d = __uint_as_float((uint32_t)(((i >> 23) + 27) << 23 | (i & 0x7FFFFF)));
+    const float q = div15(d), ref = __fdiv_rn(d, 15.f);
+    const float y = __frcp_rn(d), yref = __fdiv_rn(1.f, d);
+    if (__float_as_uint(q) != __float_as_uint(ref) || __float_as_uint(y) != __float_as_uint(yref)) {
+      ++nb;
+      const unsigned k = atomicAdd(&g_nrec, 1u);
+      if (k < 16) g_rec[4 * k] = __float_as_uint(d), g_rec[4 * k + 1] = __float_as_uint(q), g_rec[4 * k + 2] = __float_as_uint(ref),
+                                 g_rec[4 * k + 3] = __float_as_uint(y) ^ __float_as_uint(yref);
+    }
+    np += 2;
+  }
+  atomicAdd(bad, nb);
+  atomicAdd(pairs, np);
 }
 
 // two corrections: q1 is faithful, q2 = RN(u / s) (Markstein's theorem)
@@ -77,7 +105,7 @@ __global__ void check_int4(int fp16, unsigned long long n, unsigned long long* b
       x = fminf(fmaxf(x, mn), mx);
     }
     const float u = __fsub_rn(x, mn);
-    const float y = __fdiv_rn(1.f, s);
+    const float y = __frcp_rn(s);
     const int ref = __float2int_rn(__fdiv_rn(u, s)), got = __float2int_rn(markstein2(u, s, y));
     if (ref != got) {
       ++nb;
@@ -138,6 +166,22 @@ int main() {
     cudaMemcpyFromSymbol(rec, g_rec, sizeof(rec));
     for (unsigned i = 0; i < n && i < 16; ++i)
       printf("  a=0x%04x x=0x%05x q=%08x ref=%08x\n", rec[4 * i], rec[4 * i + 1], rec[4 * i + 2], rec[4 * i + 3]);
+    unsigned z = 0;
+    cudaMemcpyToSymbol(g_nrec, &z, 4);
+    total_bad += *bad;
+    total_pairs += *pairs;
+  }
+  {
+    *bad = *pairs = 0;
+    check_scale<<<148 * 8, 256>>>(bad, pairs);
+    cudaDeviceSynchronize();
+    printf("scale div15 / rcp: mismatches %llu values %llu\n", *bad, *pairs);
+    unsigned n = 0;
+    uint32_t rec[64];
+    cudaMemcpyFromSymbol(&n, g_nrec, 4);
+    cudaMemcpyFromSymbol(rec, g_rec, sizeof(rec));
+    for (unsigned i = 0; i < n && i < 16; ++i)
+      printf("  d=%08x q=%08x ref=%08x rcpxor=%08x\n", rec[4 * i], rec[4 * i + 1], rec[4 * i + 2], rec[4 * i + 3]);
     unsigned z = 0;
     cudaMemcpyToSymbol(g_nrec, &z, 4);
     total_bad += *bad;
