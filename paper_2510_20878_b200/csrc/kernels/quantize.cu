@@ -838,17 +838,19 @@ __device__ __forceinline__ uint32_t cluster_rank() {
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
   return r;
 }
-__device__ __forceinline__ void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
 __device__ __forceinline__ void cluster_arrive_relaxed() {
   asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
 }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
-__device__ __forceinline__ void st_cluster_v2(uint32_t local_addr, uint32_t rank, int a, int b) {
-  uint32_t remote;
+// {a, b} into CTA `rank`'s shared memory at the image of local_addr; the store completes 8 bytes of the
+// transaction count of that CTA's mbarrier at the image of local_bar (DSMEM st.async: the receiver waits on
+// its own mbarrier instead of a release/acquire cluster barrier)
+__device__ __forceinline__ void st_async_cluster_v2(uint32_t local_addr, uint32_t local_bar, uint32_t rank, int a, int b) {
+  uint32_t remote, rbar;
   asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_addr), "r"(rank));
-  asm volatile("st.shared::cluster.v2.s32 [%0], {%1, %2};" ::"r"(remote), "r"(a), "r"(b) : "memory");
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rbar) : "r"(local_bar), "r"(rank));
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.s32 [%0], {%1, %2}, [%3];"
+               ::"r"(remote), "r"(a), "r"(b), "r"(rbar) : "memory");
 }
 
 // (a & imm) | b with b a register (one LOP3; the compiler would spend two with two immediates)
@@ -913,7 +915,9 @@ __global__ void __cluster_dims__(kGseQ, 1, 1) __launch_bounds__(kGseThreads, HAR
   const uint32_t qe = p.slab / kGseQ;  // elements per quarter (multiple of 64)
   const QJob& jb = p.jobs[j];
   if (tid == 0) {
-    mbar_init(bar, 1);
+    mbar_init(bar, 1);      // the quarter's source (TMA)
+    mbar_init(bar + 1, 1);  // the kGseQ quarter ranges (st.async from every CTA of the cluster)
+    mbar_arrive_expect_tx(bar + 1, 8 * kGseQ);
     mbar_init_fence();
   }
   __syncthreads();
@@ -969,9 +973,11 @@ __global__ void __cluster_dims__(kGseQ, 1, 1) __launch_bounds__(kGseThreads, HAR
     for (uint32_t w = 1; w < kGseThreads / 32; ++w) emin = min(emin, red[2 * w]), emax = max(emax, red[2 * w + 1]);
     // (255 - min, max) as the range pass stores it: a quarter without normals contributes (0, 0)
     const int a = emax != 0 ? 255 - emin : 0, b = emax;
-    for (uint32_t r = 0; r < kGseQ; ++r) st_cluster_v2(smem_addr(part + 2 * q), r, a, b);
+    for (uint32_t r = 0; r < kGseQ; ++r) st_async_cluster_v2(smem_addr(part + 2 * q), smem_addr(bar + 1), r, a, b);
   }
-  cluster_sync();  // every quarter's range is in every CTA's `part`
+  // every quarter's range is in this CTA's `part` (the peers' stores into this CTA have all landed, so no
+  // cluster barrier is needed before exit either)
+  mbar_wait(bar + 1, 0);
   int rng[2] = {0, 0};
 #pragma unroll
   for (int r = 0; r < kGseQ; ++r) rng[0] = max(rng[0], part[2 * r]), rng[1] = max(rng[1], part[2 * r + 1]);
