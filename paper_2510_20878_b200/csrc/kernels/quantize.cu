@@ -932,16 +932,19 @@ __global__ void __cluster_dims__(kGseQ, 1, 1) __launch_bounds__(kGseThreads, HAR
   // quarter range: min / max biased fp32 exponent over nonzero normals (as q_consume_range)
   int emin = 255, emax = 0;
   bool bad = false;
-  uint32_t mx = 0u, mn = 0xFFFFFFFFu;  // bf16: running 16-bit-pair max magnitude / min normal key
+  uint32_t mx = 0u, mn = 0x7FFF7FFFu;  // bf16: running 16-bit-pair max magnitude / min normal key
   for (uint32_t e = tid * 8; e < qe; e += kGseThreads * 8) {
     const uint4 raw = *reinterpret_cast<const uint4*>(src_s + 2 * e);
     if constexpr (DT == HR_BF16) {
       const uint32_t w[4] = {raw.x, raw.y, raw.z, raw.w};
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
+        // key = mag + 0x7F80 per half (no carry between the halves: mag <= 0x7FFF): normals (mag >= 0x80)
+        // become negative 16-bit values ordered as mag, zeros / subnormals positive, so the signed minimum
+        // is the smallest normal whenever the quarter has one
         const uint32_t mag = w[k] & 0x7FFF7FFFu;
         mx = __vmaxu2(mx, mag);
-        mn = __vminu2(mn, (mag + 0x7F807F80u) ^ 0x80008000u);
+        mn = __vmins2(mn, mag + 0x7F807F80u);
       }
     } else {
       float2 x[4];
@@ -956,10 +959,11 @@ __global__ void __cluster_dims__(kGseQ, 1, 1) __launch_bounds__(kGseThreads, HAR
     }
   }
   if constexpr (DT == HR_BF16) {
-    const uint32_t pmax = max(mx & 0xFFFFu, mx >> 16), kmin = min(mn & 0xFFFFu, mn >> 16);
+    const uint32_t pmax = max(mx & 0xFFFFu, mx >> 16);
+    const int kmin = min((int)(int16_t)(mn & 0xFFFFu), (int)(int16_t)(mn >> 16));
     bad |= pmax >= 0x7F80u;
     emax = (int)(pmax >> 7);
-    if (kmin < 0x8000u) emin = (int)((kmin + 0x80u) >> 7);
+    if (kmin < 0) emin = (int)((((uint32_t)kmin & 0xFFFFu) - 0x7F80u) >> 7);
   }
 #pragma unroll
   for (int o = 16; o; o >>= 1) {
