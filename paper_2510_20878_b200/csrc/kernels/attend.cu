@@ -293,13 +293,16 @@ __device__ __forceinline__ uint32_t hi_pair(float a, float b) {
 // subnormal codes (16-bit multiplies keep subnormals).  E4M3: bf16 sh 4, x 2^120; fp16 sh 7, x 2^8.
 // E5M2: bf16 sh 5, x 2^112; fp16: the code is the high byte of the fp16 value.  The quantizer's
 // satfinite conversions never emit the E4M3 NaN or E5M2 inf/NaN codes; those decode as finite values here.
+// One PRMT gives each half [b, sign(b) x 8] (`sel_x`: bytes k, 8|k, k', 8|k' — the 8 selects the byte's sign
+// replicated), one shift puts b & 0x7f at the field and a copy of the sign at bit 15, one AND keeps those.
 template <int DT, int E5>
-__device__ __forceinline__ uint32_t fp8_pair(uint32_t w, uint32_t sel_m, uint32_t sel_s) {
+__device__ __forceinline__ uint32_t fp8_pair(uint32_t w, uint32_t sel_x, uint32_t sel_s) {
   if constexpr (DT == HR_FP16 && E5) return __byte_perm(w, 0u, sel_s);  // [0, b0, 0, b1]
-  const uint32_t xm = __byte_perm(w & 0x7F7F7F7Fu, 0u, sel_m);         // b & 0x7f in the low byte of each half
-  const uint32_t xs = __byte_perm(w & 0x80808080u, 0u, sel_s);         // sign bits at 15 and 31
   constexpr int sh = DT == HR_BF16 ? (E5 ? 5 : 4) : 7;
-  const uint32_t r = (xm << sh) | xs;
+  constexpr uint32_t hm = 0x8000u | (0x7Fu << sh);                      // sign | the 7 code bits
+  uint32_t t;  // prmt with the sign-replicate selector bit (__byte_perm masks the selector to 3-bit fields)
+  asm("prmt.b32 %0, %1, 0, %2;" : "=r"(t) : "r"(w), "r"(sel_x));
+  const uint32_t r = (t << sh) & (hm | hm << 16);
   if constexpr (DT == HR_BF16) {
     const __nv_bfloat162 k = E5 ? __floats2bfloat162_rn(0x1p112f, 0x1p112f) : __floats2bfloat162_rn(0x1p120f, 0x1p120f);
     __nv_bfloat162 v = __hmul2(*reinterpret_cast<const __nv_bfloat162*>(&r), k);
@@ -356,11 +359,11 @@ __device__ __forceinline__ uint4 dec_raw8(uint32_t scheme, const uint4& c, const
       return make_uint4(o[0], o[1], o[2], o[3]);
     }
     case HR_S_FP8E4M3:
-      return make_uint4(fp8_pair<DT, 0>(c.x, 0x4140u, 0x1404u), fp8_pair<DT, 0>(c.x, 0x4342u, 0x3424u),
-                        fp8_pair<DT, 0>(c.y, 0x4140u, 0x1404u), fp8_pair<DT, 0>(c.y, 0x4342u, 0x3424u));
+      return make_uint4(fp8_pair<DT, 0>(c.x, 0x9180u, 0x1404u), fp8_pair<DT, 0>(c.x, 0xB3A2u, 0x3424u),
+                        fp8_pair<DT, 0>(c.y, 0x9180u, 0x1404u), fp8_pair<DT, 0>(c.y, 0xB3A2u, 0x3424u));
     case HR_S_FP8E5M2:
-      return make_uint4(fp8_pair<DT, 1>(c.x, 0x4140u, 0x1404u), fp8_pair<DT, 1>(c.x, 0x4342u, 0x3424u),
-                        fp8_pair<DT, 1>(c.y, 0x4140u, 0x1404u), fp8_pair<DT, 1>(c.y, 0x4342u, 0x3424u));
+      return make_uint4(fp8_pair<DT, 1>(c.x, 0x9180u, 0x1404u), fp8_pair<DT, 1>(c.x, 0xB3A2u, 0x3424u),
+                        fp8_pair<DT, 1>(c.y, 0x9180u, 0x1404u), fp8_pair<DT, 1>(c.y, 0xB3A2u, 0x3424u));
     default: {  // GSE-8: +-f * 2^(G_idx - (m-1)) from the slab's fp32 table (staged in shared memory)
       const uint32_t fm = ((1u << gse_m) - 1u) * 0x01010101u;
       float2 q[4];
@@ -401,13 +404,18 @@ __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, cons
   constexpr int kUnroll = (SCH == HR_S_GSE8 || SCH == HR_S_INT8 || SCH == HR_S_FP8E4M3 || SCH == HR_S_FP8E5M2)
                               ? (HARAG_ATT_UNROLL_MAIN < (int)nch ? HARAG_ATT_UNROLL_MAIN : (int)nch)
                               : HARAG_ATT_UNROLL_RARE;
+  // chunk i of this thread: element chunk cc = dt + i * 32 * kDecWarps, i.e. dc = dt % dcs (fixed) and key
+  // key0 + i * kKeyStep (kKeyStep a multiple of 8, so the row's swizzle phase key & 7 is fixed too): every
+  // stage / operand address is the first chunk's plus a compile-time offset (immediates, no per-chunk IMAD)
+  static_assert((32 * kDecWarps) % dcs == 0 && ((32 * kDecWarps) / dcs) % 8 == 0, "decoder chunk stride");
+  constexpr uint32_t kKeyStep = 32 * kDecWarps / dcs;
+  const uint32_t dc = dt % dcs, key0 = dt / dcs, so0 = sw128_off(key0, dc, kKT);
 #pragma unroll kUnroll
   for (uint32_t i = 0; i < nch; ++i) {
-    const uint32_t cc = dt + i * 32 * kDecWarps;
     {
       // a warp takes whole key rows: conflict-free reads of the contiguous stage slot, and a quarter warp
       // writes one 128-B swizzled row (K: K-major, V: MN-major — the same physical SW128 layout)
-      const uint32_t key = cc / dcs, dc = cc % dcs;
+      const uint32_t key = key0 + i * kKeyStep;
       uint4 v;
       if constexpr (SCH == HR_S_PASS16) {  // bits unchanged: straight from global (L2-prefetched) into the operand tile
         v = __ldg(reinterpret_cast<const uint4*>(g16 + 2ull * ((t0 + key) * D + dc * 8)));
@@ -448,7 +456,7 @@ __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, cons
           v = dec_raw8<DT>(SCH, make_uint4(raw.x, raw.y, 0u, 0u), m, 0u, nullptr);
         }
       }
-      *reinterpret_cast<uint4*>(dst + sw128_off(key, dc, kKT)) = v;
+      *reinterpret_cast<uint4*>(dst + so0 + i * (kKeyStep / 8) * 1024) = v;  // = sw128_off(key, dc, kKT)
       if constexpr (DUMP) {
         if (dump) *reinterpret_cast<uint4*>(dump + key * D + dc * 8) = v;
       }
