@@ -335,13 +335,18 @@ __device__ __forceinline__ void enc_int4_step(const uint8_t* tile, uint32_t eb, 
   const bool valid = load_lane32<DT>(tile, e0, n_el, rot, raw);
   // lane statistics on the packed pairs: min, and a NaN-propagating max, so that the lane's NaN / +-Inf
   // show up as a non-finite pattern in one of the two (a NaN in max, +Inf in max, -Inf in min)
-  uint32_t pmn = raw[0].x, pmx = raw[0].x;
+  // (a pairwise tree: 4 dependent levels instead of a 15-long chain)
+  uint32_t tmn[8], tmx[8];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
-    const uint32_t w[4] = {raw[j].x, raw[j].y, raw[j].z, raw[j].w};
-#pragma unroll
-    for (int i = j == 0 ? 1 : 0; i < 4; ++i) pmn = pmin16x2<DT>(pmn, w[i]), pmx = pmaxnan16x2<DT>(pmx, w[i]);
+    tmn[2 * j] = pmin16x2<DT>(raw[j].x, raw[j].y), tmx[2 * j] = pmaxnan16x2<DT>(raw[j].x, raw[j].y);
+    tmn[2 * j + 1] = pmin16x2<DT>(raw[j].z, raw[j].w), tmx[2 * j + 1] = pmaxnan16x2<DT>(raw[j].z, raw[j].w);
   }
+#pragma unroll
+  for (int w = 4; w >= 1; w >>= 1)
+#pragma unroll
+    for (int i = 0; i < w; ++i) tmn[i] = pmin16x2<DT>(tmn[i], tmn[i + w]), tmx[i] = pmaxnan16x2<DT>(tmx[i], tmx[i + w]);
+  const uint32_t pmn = tmn[0], pmx = tmx[0];
   nan_acc = __vmaxu2(nan_acc, __vmaxu2(pmn & 0x7FFF7FFFu, pmx & 0x7FFF7FFFu));
   float2 x[4][4];
 #pragma unroll
