@@ -12,7 +12,7 @@
 //
 // sm_100a design: one CTA per (request, layer, KV head) unit — or per (unit, key split)
 // when the units alone leave SMs idle (splits merged by LSE by the last split to finish) —
-// warp-specialised: 4 softmax warps (thread = query row = TMEM lane), 3 groups of 4 decoder warps
+// warp-specialised: 4 softmax warps (thread = query row = TMEM lane), 4 groups of 4 decoder warps
 // (tiles round-robin), an S-issuer warp, a PV-issuer warp and a producer warp.  The unit's
 // M = g*n_q <= 128 query rows are the A operand of tcgen05.mma (M = 128, rows past M zero), loaded into
 // TMEM once.  Per 64-key tile the producer lane bulk-copies (TMA, cp.async.bulk) the tile's contiguous
@@ -233,10 +233,11 @@ __device__ __forceinline__ float hi_f(uint32_t w) {
 #define HARAG_ATT_DEC_WARPS 4
 #endif
 #ifndef HARAG_ATT_DEC_GROUPS
-#define HARAG_ATT_DEC_GROUPS 3
+#define HARAG_ATT_DEC_GROUPS 4
 #endif
-// measured (tools/prof_attend.py 8, C2 shape, TMA stage ring): 3 x 4 decoder warps 1.447 ms (default: 18 warps,
-// so the softmax threads hold a whole S row), 4 x 4 1.455, 3 x 8 1.477, 2 x 8 1.624 ms
+// measured (tools/prof_attend.py 8, C2 shape, TMA stage ring): round 1: 3 x 4 decoder warps 1.447 ms, 4 x 4 1.455,
+// 3 x 8 1.477, 2 x 8 1.624 ms; round 2, after the decoder instruction cuts: 3 x 4 1.174-1.175, 4 x 4 (default,
+// 16 decoder warps: the softmax threads still hold a whole S row) 1.132-1.137, 5 x 4 1.220-1.223, 2 x 8 1.320-1.322
 constexpr int kSoftWarps = HARAG_ATT_SOFT_WARPS, kDecWarps = HARAG_ATT_DEC_WARPS, kDecGroups = HARAG_ATT_DEC_GROUPS;
 #ifndef HARAG_ATT_GROUP_ARRIVE
 #define HARAG_ATT_GROUP_ARRIVE 0
@@ -511,11 +512,11 @@ __device__ __forceinline__ uint32_t stage_meta(uint32_t scheme, const uint8_t* m
 // Warp-specialised pipeline, one CTA per (request, layer, KV head) unit:
 //   warps 0-3    softmax: thread t owns query row t (TMEM lane t); loads Q; online softmax of S_j,
 //                lazy O rescale, P_j -> TMEM; epilogue O / l and LSE (or the split partials + merge)
-//   warps 4-15   decoders, three groups of 4: group b decodes the tiles j with j % 3 == b into operand
-//                buffer j % 4 (one warp per group waits for the buffer and the stage slot)
-//   warp 16      S issuer: S_j = Q K_j^T into TMEM S buffer j % 2 once K_j is decoded and PV_{j-2} is done
-//   warp 17      PV issuer: O += P_j V_j (+ the row sum) once P_j is ready
-//   warp 18      producer (one lane): TMA bulk copies of the code tiles, L2 prefetch ahead
+//   warps 4-19   decoders, kDecGroups = 4 groups of 4: group b decodes the tiles j with j % 4 == b into
+//                operand buffer j % 4 (one warp per group waits for the buffer and the stage slot)
+//   warp 20      S issuer: S_j = Q K_j^T into TMEM S buffer j % 2 once K_j is decoded and PV_{j-2} is done
+//   warp 21      PV issuer: O += P_j V_j (+ the row sum) once P_j is ready
+//   warp 22      producer (one lane): TMA bulk copies of the code tiles, L2 prefetch ahead
 // mbarriers: sf (S ready), pf (P ready), kvf (operands ready), kve (operand buffer free: committed after
 // PV), pfree (PV done per P buffer: S issue, lazy rescale, epilogue), qf (Q ready), stf / ste (stage ring).
 #ifndef HARAG_ATT_PF
