@@ -399,9 +399,10 @@ __device__ __forceinline__ void dec_tile_s(const uint8_t* __restrict__ stc, cons
                                            uint8_t* __restrict__ dst, uint32_t dt, uint16_t* __restrict__ dump,
                                            const uint8_t* __restrict__ g16, uint32_t t0, uint32_t nvalid) {
   constexpr uint32_t dcs = D / 8, nch = kKT * dcs / (32 * kDecWarps);
-  // full unroll for the paper ladder's schemes; the rest (PASS16, INT4, MXFP8, own rows) by 2 (code size)
+  // the paper ladder's schemes unrolled by 4 (8 measured 1.126-1.134 vs 1.120-1.124 ms at four decoder groups), the rest
+  // (PASS16, INT4, MXFP8, own rows) by 2 (code size)
 #ifndef HARAG_ATT_UNROLL_MAIN
-#define HARAG_ATT_UNROLL_MAIN 8
+#define HARAG_ATT_UNROLL_MAIN 4
 #endif
 #ifndef HARAG_ATT_UNROLL_RARE
 #define HARAG_ATT_UNROLL_RARE 2
@@ -520,7 +521,7 @@ __device__ __forceinline__ uint32_t stage_meta(uint32_t scheme, const uint8_t* m
 // mbarriers: sf (S ready), pf (P ready), kvf (operands ready), kve (operand buffer free: committed after
 // PV), pfree (PV done per P buffer: S issue, lazy rescale, epilogue), qf (Q ready), stf / ste (stage ring).
 #ifndef HARAG_ATT_PF
-#define HARAG_ATT_PF 4
+#define HARAG_ATT_PF 2
 #endif
 constexpr uint32_t kPF = HARAG_ATT_PF;  // L2 prefetch distance in tiles
 // kSB S buffers and kSB P buffers in TMEM: S_j = Q K_j^T may be computed while softmax works on S_{j-2}
