@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <cmath>
 #include <fcntl.h>
+#include <sys/mman.h>
 #include <unistd.h>
 
 #include <atomic>
@@ -150,6 +151,18 @@ uint32_t Store::logical_tier(uint32_t item) const {
 
 uint8_t* Store::hbm_ptr(uint32_t item) const { return hbm_base + loc[item].hbm_off; }
 
+// Pageable host memory for the backing / PAGE tier: 2 MiB aligned and advised as transparent huge pages
+// (the boxes run THP in madvise mode): the bounce copies stream tens of GB through 4 KiB pages otherwise
+// (HARAG_HOST_THP=0 keeps 4 KiB pages)
+static uint8_t* alloc_pageable(uint64_t bytes) {
+  constexpr uint64_t kHuge = 2ull << 20;
+  const uint64_t n = (bytes + kHuge - 1) / kHuge * kHuge;
+  uint8_t* p = (uint8_t*)aligned_alloc(kHuge, n);
+  static const bool thp = !(std::getenv("HARAG_HOST_THP") && std::atoi(std::getenv("HARAG_HOST_THP")) == 0);
+  if (p && thp) madvise(p, n, MADV_HUGEPAGE);  // advisory: failure leaves 4 KiB pages
+  return p;
+}
+
 void Store::build_begin(uint32_t nd, const uint64_t* hot, const uint32_t* schemes) {
   require(state == State::Empty, HR_ESTATE, "store already built");
   require(nd > 0, HR_EINVAL, "n_docs must be > 0");
@@ -221,7 +234,7 @@ void Store::setup(uint32_t nd, const uint64_t* hot, std::vector<uint32_t> sc, bo
   // pageable PAGE tier cache (disk-backed stores)
   if (on_disk && cfg.page_budget) {
     page_cap = align_up(cfg.page_budget, FreeList::kAlign);
-    page_base = (uint8_t*)aligned_alloc(4096, align_up(page_cap, 4096));
+    page_base = alloc_pageable(page_cap);
     require(page_base != nullptr, HR_ENOMEM, "PAGE tier allocation failed");
     page.reset(page_cap);
   }
@@ -258,7 +271,7 @@ void Store::setup(uint32_t nd, const uint64_t* hot, std::vector<uint32_t> sc, bo
         fail(HR_ENOMEM, "cudaHostAlloc of the pinned backing failed");
       }
     } else {
-      backing_base = (uint8_t*)aligned_alloc(4096, total);
+      backing_base = alloc_pageable(total);
       require(backing_base != nullptr, HR_ENOMEM, "host backing allocation failed");
     }
   }
