@@ -100,6 +100,9 @@ struct Store {
   uint64_t bytes_read_alg(uint32_t item) const;
   DescBuf& desc_buffer(size_t n);
   void ensure_ring();
+  void ensure_bounce(Slot& sl);            // pinned bounce buffers of every slot, placement-probed
+  std::vector<uint8_t*> bounce_rejects;    // slow-probing pinned buffers, held until close
+  double bounce_best_gbps = 0;
   void launch(const AsmDesc* dev_descs, const AsmDesc* host_descs, uint32_t n, uint32_t k, uint32_t scheme_mask,
               cudaStream_t st);
   void compact_hbm();
