@@ -511,12 +511,13 @@ void Store::ensure_ring() {
   }
 }
 
-// The pinned bounce buffers of every ring slot, allocated on first need and each probed with one timed
-// H2D copy into its slot's device buffer: the physical placement of freshly pinned pages varies and a
-// slow buffer slows every item routed through its slot (tools/pin_probe.py on the 16-vCPU B200 host:
-// most 16 MiB buffers 54.3 GB/s, one or two of 16 at 29-43 GB/s, the pageable leg bimodal 0.6 / 0.9 of
-// the link per process).  A buffer below 90% of the fastest probe is replaced (up to 4 times per slot)
-// and kept pinned until the store closes, so the allocator cannot hand the same pages back.
+// The pinned bounce buffers of every ring slot, allocated on first need and each probed with timed H2D
+// copies (best of 2) into a scratch device buffer: the physical placement of freshly pinned pages varies
+// and a slow buffer slows every item routed through its slot (tools/pin_probe.py on the 16-vCPU B200
+// host: most 16 MiB buffers 54.3 GB/s, one or two of 16 at 29-43 GB/s, the pageable leg bimodal 0.6 /
+// 0.9 of the link per process).  A buffer below 90% of the fastest probe is replaced (up to 4 times per
+// slot, at most 2 x slots rejects in all) and kept pinned until the store closes, so the allocator cannot
+// hand the same pages back.
 void Store::ensure_bounce(Slot& first) {
   if (first.bounce) return;
   const size_t n = align_up(max_item, 4096);
@@ -546,7 +547,7 @@ void Store::ensure_bounce(Slot& first) {
       HR_CUDA(cudaHostAlloc((void**)&b, n, cudaHostAllocPortable));
       const double gbps = probe(b);
       bounce_best_gbps = std::max(bounce_best_gbps, gbps);
-      if (gbps >= 0.9 * bounce_best_gbps || attempt == 4) {
+      if (gbps >= 0.9 * bounce_best_gbps || attempt == 4 || bounce_rejects.size() >= 2 * ring.size()) {
         sl.bounce = b;
         break;
       }
@@ -556,7 +557,7 @@ void Store::ensure_bounce(Slot& first) {
   // a buffer accepted before a faster probe raised the bar: re-check once against the final best
   for (auto& sl : ring) {
     if (probe(sl.bounce) >= 0.9 * bounce_best_gbps) continue;
-    for (int attempt = 0; attempt < 4; ++attempt) {
+    for (int attempt = 0; attempt < 4 && bounce_rejects.size() < 2 * ring.size(); ++attempt) {
       uint8_t* b = nullptr;
       HR_CUDA(cudaHostAlloc((void**)&b, n, cudaHostAllocPortable));
       if (probe(b) >= 0.9 * bounce_best_gbps) {
