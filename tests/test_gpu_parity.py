@@ -149,6 +149,35 @@ def test_nan_rejected(torch_cuda):
         st.build_end()
 
 
+NONFINITE = {"bf16": {"nan": 0x7FC0, "+inf": 0x7F80, "-inf": 0xFF80, "max": 0x7F7F, "-max": 0xFF7F},
+             "fp16": {"nan": 0x7E00, "+inf": 0x7C00, "-inf": 0xFC00, "max": 0x7BFF, "-max": 0xFBFF}}
+
+
+@pytest.mark.parametrize("scheme", ["PASS16", "INT8", "INT4", "FP8E4M3", "FP8E5M2", "GSE8", "MXFP8"])
+@pytest.mark.parametrize("dtype", ["bf16", "fp16"])
+@pytest.mark.parametrize("value", ["nan", "+inf", "-inf", "max", "-max"])
+def test_nonfinite_rejected_every_scheme(torch_cuda, scheme, dtype, value):
+    """a NaN or +-Inf anywhere in a chunk's source is rejected at ingestion (HR_EINVAL at build end)
+    for every scheme's encoder — the INT4 path detects it through its packed NaN-propagating max / min, the
+    others through magnitude patterns; the largest finite values are accepted."""
+    import paper_2510_20878_b200 as hr
+    torch = torch_cuda
+    st = hr.Store(L=1, H=1, D=64, T=64, dtype=dtype, ladder=(scheme,), taus=(), hbm_budget=1 << 22)
+    rng = np.random.default_rng(7)
+    k = torch.zeros(64 * 64, dtype=torch.int16, device="cuda")
+    v = torch.zeros(64 * 64, dtype=torch.int16, device="cuda")
+    pos = int(rng.integers(0, 64 * 64))
+    (k if pos % 2 else v)[pos] = int(np.int16(np.uint16(NONFINITE[dtype][value])))
+    st.build_begin(1, np.zeros(2, np.uint64))
+    st.build_put(0, k, v)
+    if value in ("max", "-max"):
+        st.build_end()
+    else:
+        with pytest.raises(hr.HaragError, match="EINVAL"):
+            st.build_end()
+    st.close()
+
+
 # ------------------------------------------------------ assemble (a6-a8, a1)
 @pytest.mark.parametrize("ladder,taus,dtype", [(NORTH, (0.25, 0.25), "fp16"), (PAPER, (0.1, 0.1, 0.1), "bf16"),
                                                (PAPER, (0.25, 0.25, 0.25), "fp16")])
