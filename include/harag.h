@@ -91,7 +91,7 @@ typedef struct {
   uint32_t bench_alias_R;  /* 0 = off; >0: docs d and d' with d % R == d' % R and equal scheme share one host backing blob (bench only) */
   int32_t  device;         /* CUDA device ordinal */
   int32_t  rank, world;    /* this store owns KV heads [rank*H/world, (rank+1)*H/world) */
-  uint32_t staging_slots;  /* host-tier staging ring slots in HBM, one item each (0 -> ~2 GiB worth, 3..64) */
+  uint32_t staging_slots;  /* host-tier staging ring slots in HBM, one item each (0 -> ~2 GiB worth, 3..128) */
   int32_t  disk_backing;   /* stores built with hr_build_from_file only: 1 = items outside the HBM arena and the
                               pinned tier stay in the file and are read on every miss (the paper's DISK tier,
                               P:237; O_DIRECT when available); 0 = the file is loaded into host memory */

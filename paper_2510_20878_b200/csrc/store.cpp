@@ -497,12 +497,21 @@ Store::DescBuf& Store::desc_buffer(size_t n) {
   return d;
 }
 
+#ifndef HARAG_MAX_SLOTS
+#define HARAG_MAX_SLOTS 128
+#endif
+// At most this many staging slots: a call that streams more host-tier items than there are slots reuses a
+// slot within the call, and that copy then waits for the slot's launch B, which runs behind launch A
+// (the copy stream idles for launch A's ~4.5 ms at C2 batch 32).  128 covers C2's ~58 items per call with
+// its Zipf spread: link fraction in the copy window 0.936 -> 0.983 (pinned), 0.91 -> 0.95-0.97 (pageable).
+constexpr uint64_t kMaxSlots = HARAG_MAX_SLOTS;
+
 void Store::ensure_ring() {
   if (!ring.empty()) return;
   // Default depth: ~2 GiB of slots (3..64).  Launch B of a streamed item runs on the request stream
   // behind launch A, so a slot is recycled only after launch A; the ring must hold what the link
   // delivers meanwhile (Llama-3-8B batch 32: launch A ~5 ms = ~280 MB at 55 GB/s) or the copies stall.
-  if (!slots) slots = (uint32_t)std::min<uint64_t>(64, std::max<uint64_t>(3, ((2ull << 30) + max_item - 1) / max_item));
+  if (!slots) slots = (uint32_t)std::min<uint64_t>(kMaxSlots, std::max<uint64_t>(3, ((2ull << 30) + max_item - 1) / max_item));
   ring.resize(slots);
   for (auto& r : ring) {
     HR_CUDA(cudaMalloc(&r.dev, max_item));
